@@ -1,0 +1,170 @@
+"""PETRA fp64 CPU oracle -- primitive layers and their hand-written VJPs.
+
+TEST INFRASTRUCTURE, NOT PRODUCT CODE.  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import anything under ``oracle/``.  The CUDA path
+(``paper_2406_02052_b200``) never imports it and shares no code with it.
+
+Layout: NCHW, float64.  Every function is the plain definition written out;
+library calls (``np.tensordot``) are used only as whole contraction steps.
+
+Citations: PAPER.md line numbers (see /root/reference/PAPER.md at survey time);
+readings of silent/ambiguous passages are numbered c1..c21 as in SURVEY.md §8(c)
+and DESIGN.md "Readings".
+"""
+from __future__ import annotations
+
+import numpy as np
+
+BN_EPS = 1e-5        # reading c9 (paper silent; PyTorch default)
+BN_MOMENTUM = 0.1    # reading c9
+
+
+# --------------------------------------------------------------------------- conv
+def conv_out_size(n: int, k: int, stride: int, pad: int) -> int:
+    return (n + 2 * pad - k) // stride + 1
+
+
+def _taps(xp, k, stride, Ho, Wo):
+    """Yield (kh, kw, view) with view[b,c,i,j] = xp[b,c,i*s+kh,j*s+kw]."""
+    for kh in range(k):
+        for kw in range(k):
+            yield kh, kw, xp[:, :, kh:kh + stride * (Ho - 1) + 1:stride,
+                             kw:kw + stride * (Wo - 1) + 1:stride]
+
+
+def conv2d(x, w, stride=1, pad=0):
+    """2-D cross-correlation without bias (the convolutions of F, G, the stem and
+    the projections; "3x3 convolutions"):
+
+        out[b,o,i,j] = sum_{c,kh,kw} w[o,c,kh,kw] * xpad[b,c,i*s+kh,j*s+kw]
+
+    x: [B,C,H,W], w: [O,C,k,k]  ->  [B,O,Ho,Wo],  Ho = floor((H+2p-k)/s)+1.
+    """
+    B, C, H, W = x.shape
+    O, C2, k, k2 = w.shape
+    if C != C2 or k != k2:
+        raise ValueError(f"conv2d shape mismatch x{x.shape} w{w.shape}")
+    Ho, Wo = conv_out_size(H, k, stride, pad), conv_out_size(W, k, stride, pad)
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
+    out = np.zeros((B, O, Ho, Wo))
+    for kh, kw, view in _taps(xp, k, stride, Ho, Wo):
+        # sum over c of view[b,c,i,j] * w[o,c,kh,kw]  -> [B,Ho,Wo,O]
+        out += np.tensordot(view, w[:, :, kh, kw], axes=([1], [1])).transpose(0, 3, 1, 2)
+    return out
+
+
+def conv2d_vjp(x, w, stride, pad, dout, need_dx=True):
+    """VJP of :func:`conv2d` (Eqs. 2-3, lines 74 and 79, applied to one conv):
+
+        dW[o,c,kh,kw] = sum_{b,i,j} dout[b,o,i,j] * xpad[b,c,i*s+kh,j*s+kw]
+        dxpad[b,c,i*s+kh,j*s+kw] += sum_o dout[b,o,i,j] * w[o,c,kh,kw]
+    """
+    B, C, H, W = x.shape
+    O, _, k, _ = w.shape
+    Ho, Wo = dout.shape[2], dout.shape[3]
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
+    dxp = np.zeros_like(xp) if need_dx else None
+    dw = np.zeros_like(w)
+    for kh, kw, view in _taps(xp, k, stride, Ho, Wo):
+        dw[:, :, kh, kw] = np.tensordot(dout, view, axes=([0, 2, 3], [0, 2, 3]))
+        if need_dx:
+            contrib = np.tensordot(dout, w[:, :, kh, kw], axes=([1], [0]))  # [B,Ho,Wo,C]
+            dxp[:, :, kh:kh + stride * (Ho - 1) + 1:stride,
+                kw:kw + stride * (Wo - 1) + 1:stride] += contrib.transpose(0, 3, 1, 2)
+    dx = dxp[:, :, pad:pad + H, pad:pad + W].copy() if need_dx else None
+    return dx, dw
+
+
+# --------------------------------------------------------------------------- batch norm
+def bn_train_forward(z, gamma, beta, eps=BN_EPS):
+    """BatchNorm in training mode with batch statistics over (B,H,W) (reading c9:
+    biased variance for normalisation).  Returns (out, cache)."""
+    axes = (0, 2, 3)
+    mu = z.mean(axis=axes)
+    var = ((z - mu[None, :, None, None]) ** 2).mean(axis=axes)
+    invstd = 1.0 / np.sqrt(var + eps)
+    xhat = (z - mu[None, :, None, None]) * invstd[None, :, None, None]
+    out = gamma[None, :, None, None] * xhat + beta[None, :, None, None]
+    return out, {"xhat": xhat, "invstd": invstd, "mu": mu, "var": var, "n": z.size // z.shape[1]}
+
+
+def bn_running_update(rmean, rvar, cache, momentum=BN_MOMENTUM):
+    """EMA of the running statistics (reading c9: unbiased variance, momentum 0.1).
+    Called ONLY when activations are recomputed in the backward (PAPER.md:259:
+    "updated when recomputing the activations during the backward pass ... not
+    updated during the forward pass"), or in the last stage's single forward (c10)."""
+    n = cache["n"]
+    rmean *= (1.0 - momentum)
+    rmean += momentum * cache["mu"]
+    rvar *= (1.0 - momentum)
+    rvar += momentum * cache["var"] * n / max(n - 1, 1)
+
+
+def bn_train_vjp(cache, gamma, dout):
+    """Closed-form VJP of training-mode BN (running stats are constants):
+        dbeta = sum g,  dgamma = sum g*xhat,
+        dz = gamma*invstd*(g - mean(g) - xhat*mean(g*xhat)),   g = dout."""
+    axes = (0, 2, 3)
+    xhat, invstd = cache["xhat"], cache["invstd"]
+    dbeta = dout.sum(axis=axes)
+    dgamma = (dout * xhat).sum(axis=axes)
+    n = cache["n"]
+    dz = (gamma * invstd)[None, :, None, None] * (
+        dout - (dbeta / n)[None, :, None, None] - xhat * (dgamma / n)[None, :, None, None])
+    return dz, dgamma, dbeta
+
+
+# --------------------------------------------------------------------------- relu / pool
+def relu(a):
+    """ReLU with mask a > 0 (reading c19: derivative 0 at 0)."""
+    mask = a > 0
+    return np.where(mask, a, 0.0), mask
+
+
+def maxpool3x3s2(x):
+    """Max-pool 3x3, stride 2, pad 1 (ImageNet stem, PAPER.md:259 contrast with CIFAR).
+    Ties: first index in row-major window order.  Returns (out, argmax)."""
+    B, C, H, W = x.shape
+    Ho, Wo = conv_out_size(H, 3, 2, 1), conv_out_size(W, 3, 2, 1)
+    xp = np.pad(x, ((0, 0), (0, 0), (1, 1), (1, 1)), constant_values=-np.inf)
+    best = np.full((B, C, Ho, Wo), -np.inf)
+    arg = np.zeros((B, C, Ho, Wo), dtype=np.int64)
+    for kh in range(3):
+        for kw in range(3):
+            v = xp[:, :, kh:kh + 2 * (Ho - 1) + 1:2, kw:kw + 2 * (Wo - 1) + 1:2]
+            upd = v > best  # strict: keeps the first maximum
+            best = np.where(upd, v, best)
+            arg = np.where(upd, kh * 3 + kw, arg)
+    return best, arg
+
+
+def maxpool3x3s2_vjp(x_shape, arg, dout):
+    B, C, H, W = x_shape
+    Ho, Wo = dout.shape[2:]
+    dxp = np.zeros((B, C, H + 2, W + 2))
+    for kh in range(3):
+        for kw in range(3):
+            sel = (arg == kh * 3 + kw)
+            dxp[:, :, kh:kh + 2 * (Ho - 1) + 1:2, kw:kw + 2 * (Wo - 1) + 1:2] += np.where(sel, dout, 0.0)
+    return dxp[:, :, 1:1 + H, 1:1 + W].copy()
+
+
+# --------------------------------------------------------------------------- head / loss
+def linear(x, w, b):
+    """y = x w^T + b (the classifier, "L <- F_J(x_{J-1}, theta_J)")."""
+    return x @ w.T + b
+
+
+def softmax_cross_entropy(logits, labels):
+    """Batch-mean softmax cross-entropy (reading c18) and its gradient
+    dlogits = (softmax - onehot) / B."""
+    B = logits.shape[0]
+    m = logits.max(axis=1, keepdims=True)
+    e = np.exp(logits - m)
+    s = e.sum(axis=1, keepdims=True)
+    logp = logits - m - np.log(s)
+    loss = -logp[np.arange(B), labels].mean()
+    p = e / s
+    p[np.arange(B), labels] -= 1.0
+    return float(loss), p / B
