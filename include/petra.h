@@ -1,0 +1,277 @@
+/*
+ * petra.h -- C ABI of the B200-native PETRA stage-tick library (libpetra.so).
+ *
+ * PETRA (arXiv 2406.02052) trains a reversible network split into J stages.
+ * At every tick each stage independently (the equation system;
+ * Alg. 1):
+ *   1. runs its forward  x_j^{t+1} = F_j(x_{j-1}^t, theta_j^t)
+ *   2. runs its backward on the message received from stage j+1:
+ *        x~_{j-1}^{t+1} = F_j^{-1}(x~_j^t, theta_j^t)   approximate inversion
+ *        delta_j^{t+1}  = d_x F_j(x~_{j-1}, theta^t)^T delta_{j+1}
+ *        Delta_j^{t+1}  = d_theta F_j(x~_{j-1}, theta^t)^T delta_{j+1}
+ *   3. updates theta immediately, no weight stash: theta^{t+1} = Opt(theta^t, Delta)
+ *
+ * Conventions (all entry points):
+ *   - Every function returns petra_status; no C++ exception crosses the ABI.
+ *     On error petra_last_error() returns a thread-local detail string.
+ *   - Activations are fp32, NHWC, and travel as TWO channel halves {x^1, x^2}
+ *     ("split equally into {x_j^1, x_j^2} along the channel
+ *     dimension"): each half is a dense [B][H][W][C_half] array.  The input of a
+ *     stage whose first unit is the stem is ONE image tensor [B][H][W][3] (x2 = NULL).
+ *   - "dev" pointers are CUDA device pointers owned by the caller; "host"
+ *     pointers are host memory owned by the caller.  The library owns
+ *     everything it allocates (parameters, optimizer slots, FIFOs, workspace)
+ *     and frees it in *_destroy.
+ *   - Device work is enqueued asynchronously on the caller's stream
+ *     (a cudaStream_t passed as void*; NULL = legacy default stream).  Shape and
+ *     argument checks are synchronous and host-side.
+ *   - A handle is used by one host thread at a time.
+ *   - Parameter and gradient arrays are packed fp32 in the order reported by
+ *     petra_stage_tensor_info(); conv weights are [C_out][k_h][k_w][C_in].
+ *   - There is no CPU fallback: without a CUDA device every compute entry point
+ *     returns PETRA_E_CUDA.
+ */
+#ifndef PETRA_H
+#define PETRA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+  PETRA_OK = 0,
+  PETRA_E_ARG = 1,          /* NULL handle/pointer, bad enum, k < 1, lr < 0 or non-finite      */
+  PETRA_E_SHAPE = 2,        /* inconsistent shapes between units / stages                       */
+  PETRA_E_ODD_CHANNELS = 3, /* a two-stream activation needs an even channel count */
+  PETRA_E_EMPTY_BUFFER = 4, /* non-reversible backward with an empty FIFO: schedule bug          */
+  PETRA_E_ORDER = 5,        /* backward mb id is not the FIFO head / ids not monotone            */
+  PETRA_E_NONFINITE = 6,    /* NaN/Inf loss (latched device flag, reported by get_params)        */
+  PETRA_E_CUDA = 7,         /* CUDA runtime error or no device                                   */
+  PETRA_E_NCCL = 8,         /* reserved (transport runs in the caller, see petra_pipeline_comm)  */
+  PETRA_E_OOM = 9,          /* device allocation failed                                          */
+  PETRA_E_UNSUPPORTED = 10  /* configuration not implemented                                     */
+} petra_status;
+
+const char *petra_status_str(int status);
+const char *petra_last_error(void);
+/* Library version string and the compile target ("sm_100a"). */
+const char *petra_version(void);
+
+/* Arithmetic of the convolutions.  Streams, BN, coupling add/sub, updates are fp32 in both. */
+typedef enum {
+  PETRA_FP32 = 0,    /* SIMT fp32 convolutions: parity path (rel 1e-4 vs the fp64 oracle)   */
+  PETRA_BF16_TC = 1  /* tcgen05 bf16 x bf16 -> fp32 TMEM implicit GEMM (rel 2e-2 vs oracle) */
+} petra_precision;
+
+typedef enum {
+  PETRA_UNIT_REV = 0,  /* reversible half-coupling  x[dst] += Phi(x[src])         */
+  PETRA_UNIT_DS = 1,   /* downsampling: y[dst] = P_a(x[dst]) + Phi_s(x[src]); y[src] = P_b(x[src])  */
+  PETRA_UNIT_STEM = 2, /* conv-BN-ReLU [+ max-pool 3x3/s2] of the image, split into two halves      */
+  PETRA_UNIT_TAIL = 3  /* GAP(concat(x1,x2)) -> Linear(+bias) -> softmax cross-entropy (batch mean)  */
+} petra_unit_kind;
+
+/* One conv(no bias)-BN[-ReLU] layer; padding is (ksize-1)/2. */
+typedef struct {
+  int32_t cin, cout, ksize, stride;
+} petra_conv;
+
+typedef struct {
+  int32_t kind;            /* petra_unit_kind                                                */
+  int32_t dst_half;        /* REV/DS: 0 -> x1 is updated ("F"), 1 -> x2 is updated ("G")     */
+  int32_t n_layers;        /* REV/DS: layers of Phi (1 basic, 3 bottleneck); STEM: 1         */
+  petra_conv layer[3];     /* Phi layers (ReLU after each); STEM: the stem conv              */
+  petra_conv proj[2];      /* DS only: P_a (on x[dst]) and P_b (on x[src]), conv1x1/s + BN  */
+  int32_t maxpool;         /* STEM only: 1 = max-pool 3x3/s2/p1 after the ReLU               */
+  int32_t classes;         /* TAIL only                                                      */
+} petra_unit;
+
+typedef struct {
+  int32_t n_units;
+  const petra_unit *units;
+  int32_t batch, in_h, in_w, in_c; /* stage input: in_c = channels per half (or image channels) */
+  int32_t precision;               /* petra_precision                                          */
+  float momentum;                  /* 0.9                                       */
+  float weight_decay;              /* 5e-4 CIFAR / 1e-4 ImageNet                */
+  float bn_momentum;               /* 0.1 (reading c9)                                         */
+  float bn_eps;                    /* 1e-5 (reading c9)                                        */
+  int32_t nesterov;                /* 1                                         */
+  int32_t accumulation_k;          /* k >= 1; only k = 1 is implemented     */
+  int32_t fifo_capacity;           /* non-reversible input FIFO depth; >= 2(J-j)+1 (Table 1)   */
+} petra_stage_desc;
+
+typedef struct petra_stage petra_stage;
+
+/* Create a stage on the current CUDA device.  Parameters are initialised from
+ * `seed` (Kaiming-uniform conv/linear weights, gamma=1, beta=0, bias=0,
+ * running mean 0 / var 1, momentum 0); callers that need identical values on
+ * both sides of a parity test overwrite them with petra_stage_set_params().
+ * Errors: PETRA_E_ARG, PETRA_E_SHAPE (unit shapes do not chain),
+ * PETRA_E_ODD_CHANNELS, PETRA_E_UNSUPPORTED, PETRA_E_OOM, PETRA_E_CUDA. */
+petra_status petra_stage_create(const petra_stage_desc *desc, uint64_t seed, petra_stage **out);
+petra_status petra_stage_destroy(petra_stage *s);
+
+/* Output activation shape of the stage (per half).  For a tail stage c = classes, h = w = 1. */
+petra_status petra_stage_output_shape(const petra_stage *s, int32_t *b, int32_t *h, int32_t *w, int32_t *c);
+
+/* Parameter layout.  n_params: length of theta (== v == Delta); n_buffers:
+ * length of the BN running-statistics array. */
+petra_status petra_stage_param_count(const petra_stage *s, size_t *n_params, size_t *n_buffers);
+
+typedef enum {
+  PETRA_T_CONV_W = 0, PETRA_T_BN_GAMMA = 1, PETRA_T_BN_BETA = 2, PETRA_T_FC_W = 3, PETRA_T_FC_B = 4,
+  PETRA_T_BN_RMEAN = 5, PETRA_T_BN_RVAR = 6
+} petra_tensor_kind;
+
+typedef struct {
+  int32_t unit;        /* unit index within the stage                                      */
+  int32_t part;        /* 0..2 = Phi layer, 3 = P_a, 4 = P_b, 0 for stem / tail             */
+  int32_t kind;        /* petra_tensor_kind                                                */
+  int32_t decay;       /* 1 if weight decay applies (not on BN params, biases) */
+  int32_t ndim;
+  int32_t shape[4];    /* conv: [cout, k, k, cin]; fc: [classes, cin]; vectors: [n]        */
+  int64_t offset;      /* element offset into theta (kinds 0-4) or into the buffer array   */
+  int64_t count;
+} petra_tensor_info;
+
+/* Tensors: all learnable tensors first (theta order), then running stats. */
+petra_status petra_stage_num_tensors(const petra_stage *s, int32_t *n);
+petra_status petra_stage_tensor_info(const petra_stage *s, int32_t i, petra_tensor_info *info);
+
+/* Copy theta / momentum v / running stats to or from HOST arrays (any pointer
+ * may be NULL to skip).  Synchronises the stage's last stream.  get_params
+ * also reports a latched PETRA_E_NONFINITE. */
+petra_status petra_stage_get_params(petra_stage *s, float *theta, float *v, float *buffers);
+petra_status petra_stage_set_params(petra_stage *s, const float *theta, const float *v, const float *buffers);
+/* Gradient Delta of the last backward (before the update), host copy. */
+petra_status petra_stage_get_grads(petra_stage *s, float *delta);
+
+/* Forward tick (Alg. 1 lines 3-10).  x*_in / x*_out: dev, fp32
+ * NHWC halves.  Reversible units retain nothing; non-reversible
+ * units push their input onto their device FIFO keyed by mb_id (reading c5).
+ * BN uses batch statistics and does NOT update running stats.
+ * out must not alias in.  Errors: PETRA_E_ARG, PETRA_E_ORDER (mb_id not
+ * increasing), PETRA_E_CUDA. */
+petra_status petra_stage_forward(petra_stage *s, uint64_t mb_id,
+                                 const float *x1_in, const float *x2_in,
+                                 float *x1_out, float *x2_out, void *stream);
+
+/* Backward tick + immediate update with learning rate lr (Alg. 1 lines 11-24;
+ * PAPER.md:132-135).  Inputs: the reconstructed output x~_j (xt*_out) and
+ * delta_{j+1} (d*_out) received from stage j+1.  Reversible units reconstruct
+ * their input with the CURRENT theta (approximate inversion),
+ * keep the graph and run the VJP without a second forward;
+ * BN running stats are updated in this recomputation.
+ * Non-reversible units pop their FIFO (must match mb_id), recompute, VJP, and
+ * return the exact buffered input (reading c6).  Outputs: x~_{j-1} (xt*_in)
+ * and delta_j (d*_in), dev.  Outputs must not alias inputs.
+ * Errors: PETRA_E_ARG, PETRA_E_EMPTY_BUFFER, PETRA_E_ORDER, PETRA_E_CUDA. */
+petra_status petra_stage_backward(petra_stage *s, uint64_t mb_id,
+                                  const float *xt1_out, const float *xt2_out,
+                                  const float *d1_out, const float *d2_out,
+                                  float *xt1_in, float *xt2_in, float *d1_in, float *d2_in,
+                                  float lr, void *stream);
+
+/* Final stage (Alg. 1 lines 26-35): forward with stored activations (running
+ * stats updated here, reading c10), loss, plain backprop, update, all in one
+ * call.  Returns the RECEIVED input as x~ (copied to xt*_in, may be NULL) and
+ * delta_J w.r.t. that input (reading c7).  labels: dev int32[B].
+ * loss_dev: dev float[1] (batch-mean cross-entropy), may be NULL. */
+petra_status petra_stage_tail(petra_stage *s, uint64_t mb_id,
+                              const float *x1_in, const float *x2_in, const int32_t *labels,
+                              float lr, float *xt1_in, float *xt2_in, float *d1_in, float *d2_in,
+                              float *loss_dev, void *stream);
+
+/* ------------------------------------------------------------------ pipeline
+ * One process (rank) owns a contiguous block of stages.  petra_pipeline_tick
+ * runs tick t of every local stage (forward then backward, both at theta^t,
+ * then the update; reading c8).  Mailboxes are double-buffered: a message
+ * produced at tick t is consumed at t+1 (PAPER.md:131-134 superscripts).
+ * Same-rank neighbours hand messages over by pointer; for cross-rank
+ * neighbours the caller moves the bytes listed by petra_pipeline_comm() after
+ * each tick (NCCL send/recv on its own stream via torch.distributed).
+ */
+typedef struct {
+  int32_t n_stages;                /* J                                                */
+  const petra_stage_desc *stages;  /* all J stage descriptors (every rank passes all)  */
+  const int32_t *stage_rank;       /* rank owning stage j (contiguous, non-decreasing) */
+  int32_t rank, world;
+  uint64_t seed;                   /* stage j is created with seed + j                 */
+} petra_pipeline_desc;
+
+typedef struct petra_pipeline petra_pipeline;
+
+#define PETRA_MAX_STAGES 64
+typedef struct {              /* integer part is compared bit-exactly with the oracle      */
+  int64_t tick;
+  int32_t n_stages;           /* J (report covers all stages; non-local entries are replayed) */
+  int64_t fwd_mb[PETRA_MAX_STAGES];        /* -1 = idle this tick                        */
+  int64_t bwd_mb[PETRA_MAX_STAGES];
+  int64_t param_version[PETRA_MAX_STAGES]; /* updates applied before this tick           */
+  int64_t fifo_depth[PETRA_MAX_STAGES];    /* summed over the stage's FIFOs, after tick  */
+} petra_tick_report;
+
+petra_status petra_pipeline_create(const petra_pipeline_desc *desc, petra_pipeline **out);
+petra_status petra_pipeline_destroy(petra_pipeline *p);
+/* Borrow the handle of stage j (1-based); NULL if not local. */
+petra_status petra_pipeline_stage(petra_pipeline *p, int32_t j, petra_stage **out);
+
+/* Tick t.  inject != 0: stage 1 consumes micro-batch id mb = number of
+ * injections so far; x0 (dev, stage-1 input layout) and labels (dev int32[B])
+ * are read on the rank owning stage 1 (pass them or NULL elsewhere).  lr: the
+ * tick's learning rate.  loss_dev: dev float[1] written by the tail stage
+ * (rank owning stage J) when it ran.  report: nullable. */
+petra_status petra_pipeline_tick(petra_pipeline *p, int64_t t, int32_t inject,
+                                 const float *x0, const int32_t *labels, float lr,
+                                 float *loss_dev, void *stream, petra_tick_report *report);
+
+/* Transport plan for the messages this rank must exchange after tick t so
+ * that tick t+1 can consume them.  Each entry is one contiguous device buffer. */
+typedef struct {
+  int32_t peer;      /* rank                                  */
+  int32_t send;      /* 1 = send to peer, 0 = receive          */
+  void *ptr;         /* dev                                    */
+  int64_t bytes;
+} petra_comm_entry;
+#define PETRA_MAX_COMM 16
+typedef struct {
+  int32_t n;
+  petra_comm_entry e[PETRA_MAX_COMM];
+} petra_comm_plan;
+petra_status petra_pipeline_comm(petra_pipeline *p, int64_t t, petra_comm_plan *plan);
+
+/* ------------------------------------------------------------------ schedule (host only)
+ * The integer bookkeeping petra_pipeline_tick runs, exposed without any device
+ * work so the multi-rank routing can be tested on CPU (gloo) and compared
+ * bit-exactly with the oracle's tick engine.  stage_rank as in
+ * petra_pipeline_desc; nonrev[j-1] = number of non-reversible units of stage j
+ * (FIFO accounting).  petra_schedule_tick must be called for t = 0, 1, 2, ...;
+ * it fills report (all J stages) and the messages THIS rank exchanges after the
+ * tick: kind 0 = forward (x1, x2, labels), 1 = backward (x~1, x~2, d1, d2). */
+typedef struct petra_schedule petra_schedule;
+typedef struct {
+  int32_t peer, send, kind, stage; /* stage: 1-based index of the sending stage */
+  int64_t mb;
+} petra_sched_msg;
+typedef struct {
+  int32_t n;
+  petra_sched_msg m[8];
+} petra_sched_msgs;
+petra_status petra_schedule_create(int32_t n_stages, const int32_t *stage_rank, const int32_t *nonrev,
+                                   int32_t rank, petra_schedule **out);
+petra_status petra_schedule_tick(petra_schedule *s, int64_t t, int32_t inject, petra_tick_report *report,
+                                 petra_sched_msgs *msgs);
+petra_status petra_schedule_destroy(petra_schedule *s);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* PETRA_H */

@@ -1,0 +1,67 @@
+// kernels.h -- launchers of the PETRA B200 kernels (internal C++ interface, not the ABI).
+#pragma once
+#include <algorithm>
+#include "common.cuh"
+
+namespace petra {
+
+// ---------------------------------------------------------------- SIMT fp32 convolutions
+void conv_fwd_simt(const ConvGeom &g, const float *x, const float *w, float *z, cudaStream_t st);
+void conv_dgrad_simt(const ConvGeom &g, const float *dz, const float *w, const float *addend, float *dx,
+                     cudaStream_t st);
+size_t conv_wgrad_simt_workspace(const ConvGeom &g);
+void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *dw, float *ws, cudaStream_t st);
+
+// ---------------------------------------------------------------- tcgen05 bf16 convolutions
+bool conv_tc_supported(const ConvGeom &g, int mode);   // mode 0 fwd, 1 dgrad, 2 wgrad
+size_t conv_tc_workspace(const ConvGeom &g, int mode);
+// z[m][co] (fp32 or bf16 out) = conv(x_bf16, w_bf16)
+void conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32,
+                 __nv_bfloat16 *z_bf16, cudaStream_t st);
+// dx (fp32) = addend + conv^T(dz_bf16, wT_bf16)
+void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend,
+                   float *dx, cudaStream_t st);
+// dw (fp32) = sum_pixels dz (x) x
+void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *x, float *dw, float *ws,
+                   cudaStream_t st);
+
+// ---------------------------------------------------------------- batch norm / coupling
+size_t bn_partial_bytes(int64_t M, int C);
+template <typename TZ>
+void bn_stats(const TZ *z, int64_t M, int C, float eps, float *mean, float *invstd, float *rmean, float *rvar,
+              float mom, double *part, cudaStream_t st);
+template <typename TZ, typename TO>
+void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean, const float *invstd,
+              const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
+              __nv_bfloat16 *out_bf16, cudaStream_t st);
+template <typename TZ>
+void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float *invstd, const float *gamma,
+                   const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dst_in,
+                   float *dst_out, __nv_bfloat16 *dst_bf16, float *dgamma, float *dbeta, double *part,
+                   cudaStream_t st);
+template <typename TZ, typename TO>
+void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *invstd, const float *gamma,
+               const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
+               const float *dbeta, TO *dz, cudaStream_t st);
+
+// ---------------------------------------------------------------- optimizer / tail / misc
+struct SgdSeg {
+  int64_t offset, count;
+  int decay;
+  int co, k, ci;                 // conv weights only (for the bf16 shadows)
+  __nv_bfloat16 *w_bf16;         // nullable: bf16 shadow [Co][k][k][Ci]
+  __nv_bfloat16 *wt_bf16;        // nullable: dgrad operand [Ci][k][k][Co], taps flipped
+};
+void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *theta, float *v, const float *grad,
+                float lr, float mom, float wd, int nesterov, cudaStream_t st, bool shadow_only);
+void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int C, const float *w,
+                           const float *bias, int N, const int32_t *labels, float *feat, float *logits,
+                           float *dlogits, float *loss_row, float *dfeat, float *dw, float *db, float *d1,
+                           float *d2, float *loss, int *nonfinite, cudaStream_t st);
+void maxpool_fwd(const float *a, int B, int H, int W, int C, int Ho, int Wo, float *o1, float *o2, uint8_t *arg,
+                 cudaStream_t st);
+void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, int H, int W, int C, int Ho, int Wo,
+                 float *da, cudaStream_t st);
+void f32_to_bf16(const float *x, __nv_bfloat16 *y, int64_t n, cudaStream_t st);
+
+}  // namespace petra

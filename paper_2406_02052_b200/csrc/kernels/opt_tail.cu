@@ -1,0 +1,285 @@
+// opt_tail.cu -- immediate Nesterov-SGD update, classifier tail, max-pool, small helpers.
+//
+// update  (reading c11):  g = Delta + lambda*theta (lambda = 0 on
+//          BN parameters and biases), v <- mu*v + g, theta <- theta - lr*(g + mu*v).
+//          One launch over every tensor of the stage (segment table); it also
+//          refreshes the bf16 shadows of the conv weights used by the tensor-core
+//          path ([Co][K] and the flipped/transposed dgrad operand) -- a shadow of
+//          the single live parameter version, not a stash.
+// tail: GAP over H,W of concat(x1,x2), Linear + bias,
+//          batch-mean softmax cross-entropy, its VJP; deterministic reductions.
+// maxpool 3x3/s2/p1 with first-index ties.
+#include "../kernels.h"
+
+namespace petra {
+namespace {
+
+__global__ void sgd_kernel(const SgdSeg *__restrict__ segs, float *__restrict__ theta, float *__restrict__ v,
+                           const float *__restrict__ grad, float lr, float mom, float wd, int nesterov,
+                           int shadow_only) {
+  const SgdSeg sg = segs[blockIdx.y];
+  if (shadow_only && !sg.w_bf16) return;
+  const float lam = sg.decay ? wd : 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sg.count; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = sg.offset + i;
+    float th = theta[o];
+    if (!shadow_only) {
+      float g = fmaf(lam, th, grad[o]);
+      float vv = fmaf(mom, v[o], g);
+      v[o] = vv;
+      th -= lr * (nesterov ? fmaf(mom, vv, g) : vv);
+      theta[o] = th;
+    }
+    if (sg.w_bf16) {
+      // conv weight [Co][kh][kw][Ci]: bf16 copy in the same order, and the dgrad
+      // operand wT[ci][kh'][kw'][co] = w[co][k-1-kh'][k-1-kw'][ci]
+      __nv_bfloat16 hb = __float2bfloat16_rn(th);
+      sg.w_bf16[i] = hb;
+      if (sg.wt_bf16) {
+        int ci = (int)(i % sg.ci);
+        int64_t r = i / sg.ci;
+        int kw = (int)(r % sg.k);
+        r /= sg.k;
+        int kh = (int)(r % sg.k);
+        int co = (int)(r / sg.k);
+        int64_t j = (((int64_t)ci * sg.k + (sg.k - 1 - kh)) * sg.k + (sg.k - 1 - kw)) * sg.co + co;
+        sg.wt_bf16[j] = hb;
+      }
+    }
+  }
+}
+
+__global__ void gap_kernel(const float *__restrict__ x1, const float *__restrict__ x2, int B, int HW, int C,
+                           float *__restrict__ feat) {
+  // feat[b][c'] for c' in [0, 2C): mean over HW (fixed summation order)
+  int b = blockIdx.y;
+  int c2 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c2 >= 2 * C) return;
+  const float *src = c2 < C ? x1 : x2;
+  int c = c2 < C ? c2 : c2 - C;
+  float s = 0.f;
+  for (int p = 0; p < HW; ++p) s += src[((int64_t)b * HW + p) * C + c];
+  feat[(int64_t)b * 2 * C + c2] = s / (float)HW;
+}
+
+__global__ void fc_fwd_kernel(const float *__restrict__ feat, const float *__restrict__ w,
+                              const float *__restrict__ bias, int B, int Cin, int N, float *__restrict__ logits) {
+  // one warp per (b, n)
+  int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (gw >= B * N) return;
+  int b = gw / N, n = gw - b * N;
+  float s = 0.f;
+  for (int c = lane; c < Cin; c += 32) s = fmaf(feat[(int64_t)b * Cin + c], w[(int64_t)n * Cin + c], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) logits[(int64_t)b * N + n] = s + bias[n];
+}
+
+__global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__restrict__ labels, int B, int N,
+                          float *__restrict__ dlogits, float *__restrict__ loss_row) {
+  // one block (256 threads) per row; dlogits = (softmax - onehot)/B
+  __shared__ float red[32];
+  int b = blockIdx.x;
+  const float *l = logits + (int64_t)b * N;
+  float mx = -INFINITY;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) mx = fmaxf(mx, l[n]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  mx = red[0];
+  __syncthreads();
+  float s = 0.f;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) s += expf(l[n] - mx);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  s = red[0];
+  int y = labels[b];
+  float lse = mx + logf(s);
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    float p = expf(l[n] - lse);
+    dlogits[(int64_t)b * N + n] = (p - (n == y ? 1.f : 0.f)) / (float)B;
+  }
+  if (threadIdx.x == 0) loss_row[b] = lse - l[y];
+}
+
+__global__ void loss_mean_kernel(const float *__restrict__ loss_row, int B, float *__restrict__ loss,
+                                 int *__restrict__ nonfinite) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < B; ++b) s += loss_row[b];
+    float l = (float)(s / B);
+    if (loss) *loss = l;
+    if (!isfinite(l)) *nonfinite = 1;
+  }
+}
+
+__global__ void fc_bwd_w_kernel(const float *__restrict__ dlogits, const float *__restrict__ feat, int B, int Cin,
+                                int N, float *__restrict__ dw, float *__restrict__ db) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < (int64_t)N * Cin) {
+    int n = (int)(i / Cin), c = (int)(i - (int64_t)n * Cin);
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) s = fmaf(dlogits[(int64_t)b * N + n], feat[(int64_t)b * Cin + c], s);
+    dw[i] = s;
+  }
+  if (i < N) {
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) s += dlogits[(int64_t)b * N + i];
+    db[i] = s;
+  }
+}
+
+__global__ void fc_bwd_x_kernel(const float *__restrict__ dlogits, const float *__restrict__ w, int B, int Cin,
+                                int N, float *__restrict__ dfeat) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * Cin) return;
+  int b = (int)(i / Cin), c = (int)(i - (int64_t)b * Cin);
+  float s = 0.f;
+  for (int n = 0; n < N; ++n) s = fmaf(dlogits[(int64_t)b * N + n], w[(int64_t)n * Cin + c], s);
+  dfeat[i] = s;
+}
+
+__global__ void gap_bwd_kernel(const float *__restrict__ dfeat, int B, int HW, int C, float *__restrict__ d1,
+                               float *__restrict__ d2) {
+  int64_t n = (int64_t)B * HW * C;
+  float inv = 1.f / (float)HW;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % C);
+    int b = (int)(i / ((int64_t)HW * C));
+    d1[i] = dfeat[(int64_t)b * 2 * C + c] * inv;
+    d2[i] = dfeat[(int64_t)b * 2 * C + C + c] * inv;
+  }
+}
+
+// max-pool on a [B][H][W][C] activation, writes split halves of the output
+__global__ void maxpool_fwd_kernel(const float *__restrict__ a, int B, int H, int W, int C, int Ho, int Wo,
+                                   float *__restrict__ o1, float *__restrict__ o2, uint8_t *__restrict__ arg) {
+  int64_t n = (int64_t)B * Ho * Wo * C;
+  int Ch = C / 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % C);
+    int64_t r = i / C;
+    int wo = (int)(r % Wo);
+    r /= Wo;
+    int ho = (int)(r % Ho);
+    int b = (int)(r / Ho);
+    float best = -INFINITY;
+    int bi = 0;
+    for (int kh = 0; kh < 3; ++kh)
+      for (int kw = 0; kw < 3; ++kw) {
+        int h = ho * 2 + kh - 1, w = wo * 2 + kw - 1;
+        if (h < 0 || h >= H || w < 0 || w >= W) continue;
+        float v = a[(((int64_t)b * H + h) * W + w) * C + c];
+        if (v > best) { best = v; bi = kh * 3 + kw; }
+      }
+    arg[i] = (uint8_t)bi;
+    int64_t pix = ((int64_t)b * Ho + ho) * Wo + wo;
+    if (c < Ch) o1[pix * Ch + c] = best;
+    else o2[pix * Ch + c - Ch] = best;
+  }
+}
+
+__global__ void maxpool_bwd_kernel(const float *__restrict__ d1, const float *__restrict__ d2,
+                                   const uint8_t *__restrict__ arg, int B, int H, int W, int C, int Ho, int Wo,
+                                   float *__restrict__ da) {
+  int64_t n = (int64_t)B * H * W * C;
+  int Ch = C / 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % C);
+    int64_t r = i / C;
+    int w = (int)(r % W);
+    r /= W;
+    int h = (int)(r % H);
+    int b = (int)(r / H);
+    float s = 0.f;
+    // output windows (ho, wo) with ho*2-1 <= h <= ho*2+1
+    for (int ho = h / 2; ho <= min(Ho - 1, (h + 1) / 2); ++ho) {
+      int kh = h - (ho * 2 - 1);
+      if (kh < 0 || kh > 2) continue;
+      for (int wo = w / 2; wo <= min(Wo - 1, (w + 1) / 2); ++wo) {
+        int kw = w - (wo * 2 - 1);
+        if (kw < 0 || kw > 2) continue;
+        int64_t pix = ((int64_t)b * Ho + ho) * Wo + wo;
+        if (arg[pix * C + c] == kh * 3 + kw) s += (c < Ch) ? d1[pix * Ch + c] : d2[pix * Ch + c - Ch];
+      }
+    }
+    da[i] = s;
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float *__restrict__ x, __nv_bfloat16 *__restrict__ y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+
+inline unsigned ew_grid(int64_t n) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs));
+}
+
+}  // namespace
+
+void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *theta, float *v, const float *grad,
+                float lr, float mom, float wd, int nesterov, cudaStream_t st, bool shadow_only) {
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(max_count, 256), 2 * kNumSMs)), nseg);
+  sgd_kernel<<<grid, 256, 0, st>>>(segs_dev, theta, v, grad, lr, mom, wd, nesterov, shadow_only ? 1 : 0);
+  PETRA_LAUNCH_CHECK();
+}
+
+void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int C, const float *w,
+                           const float *bias, int N, const int32_t *labels, float *feat, float *logits,
+                           float *dlogits, float *loss_row, float *dfeat, float *dw, float *db, float *d1,
+                           float *d2, float *loss, int *nonfinite, cudaStream_t st) {
+  int Cin = 2 * C;
+  gap_kernel<<<dim3((unsigned)cdiv(Cin, 128), B), 128, 0, st>>>(x1, x2, B, HW, C, feat);
+  PETRA_LAUNCH_CHECK();
+  fc_fwd_kernel<<<(unsigned)cdiv((int64_t)B * N * 32, 256), 256, 0, st>>>(feat, w, bias, B, Cin, N, logits);
+  PETRA_LAUNCH_CHECK();
+  ce_kernel<<<B, 256, 0, st>>>(logits, labels, B, N, dlogits, loss_row);
+  PETRA_LAUNCH_CHECK();
+  loss_mean_kernel<<<1, 32, 0, st>>>(loss_row, B, loss, nonfinite);
+  PETRA_LAUNCH_CHECK();
+  fc_bwd_w_kernel<<<(unsigned)cdiv(std::max<int64_t>((int64_t)N * Cin, N), 256), 256, 0, st>>>(dlogits, feat, B,
+                                                                                               Cin, N, dw, db);
+  PETRA_LAUNCH_CHECK();
+  fc_bwd_x_kernel<<<(unsigned)cdiv((int64_t)B * Cin, 256), 256, 0, st>>>(dlogits, w, B, Cin, N, dfeat);
+  PETRA_LAUNCH_CHECK();
+  gap_bwd_kernel<<<ew_grid((int64_t)B * HW * C), 256, 0, st>>>(dfeat, B, HW, C, d1, d2);
+  PETRA_LAUNCH_CHECK();
+}
+
+void maxpool_fwd(const float *a, int B, int H, int W, int C, int Ho, int Wo, float *o1, float *o2, uint8_t *arg,
+                 cudaStream_t st) {
+  maxpool_fwd_kernel<<<ew_grid((int64_t)B * Ho * Wo * C), 256, 0, st>>>(a, B, H, W, C, Ho, Wo, o1, o2, arg);
+  PETRA_LAUNCH_CHECK();
+}
+
+void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, int H, int W, int C, int Ho, int Wo,
+                 float *da, cudaStream_t st) {
+  maxpool_bwd_kernel<<<ew_grid((int64_t)B * H * W * C), 256, 0, st>>>(d1, d2, arg, B, H, W, C, Ho, Wo, da);
+  PETRA_LAUNCH_CHECK();
+}
+
+void f32_to_bf16(const float *x, __nv_bfloat16 *y, int64_t n, cudaStream_t st) {
+  f32_to_bf16_kernel<<<ew_grid(n), 256, 0, st>>>(x, y, n);
+  PETRA_LAUNCH_CHECK();
+}
+
+}  // namespace petra

@@ -1,0 +1,144 @@
+// pipeline.cu -- the stages of one rank, their double-buffered mailboxes and the
+// per-tick driver (product code).  Cross-rank bytes are moved by the caller
+// (NCCL send/recv through torch.distributed) from the plan of petra_pipeline_comm.
+#include "pipeline.h"
+
+namespace petra {
+
+static bool has_stem(const petra_stage_desc &d) { return d.n_units > 0 && d.units[0].kind == PETRA_UNIT_STEM; }
+
+static std::vector<int> nonrev_counts(const petra_pipeline_desc &d) {
+  std::vector<int> v(d.n_stages, 0);
+  for (int j = 0; j < d.n_stages; ++j)
+    for (int u = 0; u < d.stages[j].n_units; ++u) {
+      int k = d.stages[j].units[u].kind;
+      if (k == PETRA_UNIT_DS || k == PETRA_UNIT_STEM) v[j] += 1;
+    }
+  return v;
+}
+
+Pipeline::Pipeline(const petra_pipeline_desc &d)
+    : J_(d.n_stages),
+      rank_(d.rank),
+      sched_(d.n_stages, std::vector<int>(d.stage_rank, d.stage_rank + d.n_stages), nonrev_counts(d), d.rank) {
+  if (J_ < 1 || J_ > PETRA_MAX_STAGES) throw PetraError(PETRA_E_ARG, "n_stages out of range");
+  stages_.resize(J_ + 2);
+  fwd_.resize(J_ + 2);
+  bwd_.resize(J_ + 2);
+  descs_.assign(d.stages, d.stages + J_);
+  for (int j = 1; j <= J_; ++j) {
+    if (!sched_.local(j)) continue;
+    petra_stage_desc sd = d.stages[j - 1];
+    sd.fifo_capacity = 2 * (J_ - j) + 1;  // Table 1: at most 2(J-j)+1 inputs in flight
+    stages_[j].reset(new Stage(sd, d.seed + (uint64_t)j));
+    Stage &s = *stages_[j];
+    if ((j == J_) != s.is_last()) throw PetraError(PETRA_E_SHAPE, "exactly the last stage must hold the tail");
+    for (int p = 0; p < 2; ++p) {
+      if (j < J_) {
+        fwd_[j][p].x[0] = dalloc(s.out_shape().numel() * sizeof(float));
+        fwd_[j][p].x[1] = dalloc(s.out_shape().numel() * sizeof(float));
+        fwd_[j][p].labels = dalloc((size_t)s.out_shape().B * sizeof(int32_t));
+      }
+      if (!has_stem(d.stages[j - 1])) {
+        for (int k = 0; k < 4; ++k) bwd_[j][p].x[k] = dalloc(s.in_shape().numel() * sizeof(float));
+      }
+    }
+  }
+  int j0 = sched_.first_local(), j1 = sched_.last_local();
+  if (j1 < 1) throw PetraError(PETRA_E_ARG, "rank owns no stage");
+  for (int p = 0; p < 2; ++p) {
+    if (j0 > 1) {
+      const Shape &in = stages_[j0]->in_shape();
+      ghost_fwd_[p].x[0] = dalloc(in.numel() * sizeof(float));
+      ghost_fwd_[p].x[1] = dalloc(in.numel() * sizeof(float));
+      ghost_fwd_[p].labels = dalloc((size_t)in.B * sizeof(int32_t));
+    }
+    if (j1 < J_) {
+      const Shape &out = stages_[j1]->out_shape();
+      for (int k = 0; k < 4; ++k) ghost_bwd_[p].x[k] = dalloc(out.numel() * sizeof(float));
+    }
+  }
+}
+
+static float *fp(const DevPtr &p) { return p ? p->as<float>() : nullptr; }
+
+void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labels, float lr, float *loss,
+                    cudaStream_t st, petra_tick_report *rep) {
+  std::vector<int64_t> ver, fifo;
+  std::vector<Schedule::Step> steps = sched_.tick(t, inject, &ver, &fifo);
+  const int p = (int)(t & 1), q = p ^ 1;
+  for (int j = 1; j <= J_; ++j) {
+    if (!sched_.local(j)) continue;
+    Stage &s = *stages_[j];
+    const Schedule::Step &sp = steps[j];
+    // ---- forward input message
+    const float *in1 = nullptr, *in2 = nullptr;
+    const int32_t *lab = nullptr;
+    if (sp.fwd_mb >= 0) {
+      if (j == 1) {
+        if (!x0 || !labels) throw PetraError(PETRA_E_ARG, "inject on the rank of stage 1 needs x0 and labels");
+        in1 = x0;
+        in2 = has_stem(descs_[0]) ? nullptr : x0 + s.in_shape().numel();
+        lab = labels;
+      } else {
+        Msg &m = sched_.local(j - 1) ? fwd_[j - 1][q] : ghost_fwd_[q];
+        in1 = fp(m.x[0]);
+        in2 = fp(m.x[1]);
+        lab = m.labels->as<int32_t>();
+      }
+    }
+    if (j < J_) {
+      if (sp.fwd_mb >= 0) {
+        Msg &o = fwd_[j][p];
+        s.forward((uint64_t)sp.fwd_mb, in1, in2, fp(o.x[0]), fp(o.x[1]), st);
+        PETRA_CUDA(cudaMemcpyAsync(o.labels->p, lab, (size_t)s.out_shape().B * sizeof(int32_t),
+                                   cudaMemcpyDeviceToDevice, st));
+      }
+      if (sp.bwd_mb >= 0) {
+        Msg &m = sched_.local(j + 1) ? bwd_[j + 1][q] : ghost_bwd_[q];
+        Msg &o = bwd_[j][p];
+        s.backward((uint64_t)sp.bwd_mb, fp(m.x[0]), fp(m.x[1]), fp(m.x[2]), fp(m.x[3]), fp(o.x[0]), fp(o.x[1]),
+                   fp(o.x[2]), fp(o.x[3]), lr, st);
+      }
+    } else if (sp.fwd_mb >= 0) {
+      Msg &o = bwd_[j][p];
+      s.tail((uint64_t)sp.fwd_mb, in1, in2, lab, lr, fp(o.x[0]), fp(o.x[1]), fp(o.x[2]), fp(o.x[3]), loss, st);
+    }
+  }
+  if (rep) {
+    rep->tick = t;
+    rep->n_stages = J_;
+    for (int j = 1; j <= J_; ++j) {
+      rep->fwd_mb[j - 1] = steps[j].fwd_mb;
+      rep->bwd_mb[j - 1] = steps[j].bwd_mb;
+      rep->param_version[j - 1] = ver[j];
+      rep->fifo_depth[j - 1] = fifo[j];
+    }
+  }
+}
+
+void Pipeline::comm(int64_t t, petra_comm_plan *plan) {
+  plan->n = 0;
+  const int p = (int)(t & 1);
+  auto add = [&](int peer, int send, const DevPtr &buf) {
+    if (plan->n >= PETRA_MAX_COMM) throw PetraError(PETRA_E_ARG, "comm plan overflow");
+    petra_comm_entry &e = plan->e[plan->n++];
+    e.peer = peer;
+    e.send = send;
+    e.ptr = buf->p;
+    e.bytes = (int64_t)buf->bytes;
+  };
+  for (const Schedule::Comm &c : sched_.comm(t)) {
+    if (c.kind == Schedule::MSG_FWD) {
+      Msg &m = c.send ? fwd_[c.stage][p] : ghost_fwd_[p];
+      add(c.peer, c.send, m.x[0]);
+      add(c.peer, c.send, m.x[1]);
+      add(c.peer, c.send, m.labels);
+    } else {
+      Msg &m = c.send ? bwd_[c.stage][p] : ghost_bwd_[p];
+      for (int k = 0; k < 4; ++k) add(c.peer, c.send, m.x[k]);
+    }
+  }
+}
+
+}  // namespace petra

@@ -1,0 +1,33 @@
+// pipeline.h -- stages of one rank + mailboxes (product code).
+#pragma once
+#include <memory>
+#include <vector>
+
+#include "schedule.h"
+#include "stage.h"
+
+namespace petra {
+
+struct Msg {
+  DevPtr x[4];    // forward: x1, x2 ; backward: x~1, x~2, d1, d2
+  DevPtr labels;  // forward only
+};
+
+class Pipeline {
+ public:
+  explicit Pipeline(const petra_pipeline_desc &d);
+  Stage *stage(int j) { return (j >= 1 && j <= J_) ? stages_[j].get() : nullptr; }
+  void tick(int64_t t, bool inject, const float *x0, const int32_t *labels, float lr, float *loss, cudaStream_t st,
+            petra_tick_report *rep);
+  void comm(int64_t t, petra_comm_plan *plan);
+
+ private:
+  int J_, rank_;
+  Schedule sched_;
+  std::vector<petra_stage_desc> descs_;
+  std::vector<std::unique_ptr<Stage>> stages_;
+  std::vector<std::array<Msg, 2>> fwd_, bwd_;  // [j][parity]: outputs of local stage j
+  Msg ghost_fwd_[2], ghost_bwd_[2];            // receive buffers for remote neighbours
+};
+
+}  // namespace petra

@@ -1,0 +1,779 @@
+// stage.cu -- PETRA stage engine (product code): builds the unit list of a stage,
+// owns theta / v / Delta / running stats / FIFOs / workspace, and enqueues the
+// kernel sequence of a forward tick, a backward tick (approximate inversion +
+// VJP + immediate update) and the final-stage step.
+//
+// Paper map:
+//   forward                PAPER.md:131, Alg. 1 lines 3-10
+//   backward, reversible   PAPER.md:132-135, Alg. 1 lines 12-21; "a reconstruction step
+//                          and a backward step": the recomputed conv
+//                          outputs z of the reconstruction ARE the graph of the VJP
+//   backward, non-rev      Alg. 1 lines 15-17 (buffer + recompute), reading c5/c6
+//   final stage            Alg. 1 lines 26-35, readings c7/c10
+//   BN running stats       PAPER.md:259 (updated only when recomputing)
+//   update                 PAPER.md:135, 256 (Nesterov 0.9, wd exclusions)
+#include "stage.h"
+
+#include <cmath>
+#include <cstring>
+
+#include "errors.h"
+
+namespace petra {
+
+DevBuf::DevBuf(size_t n) : bytes(n) {
+  if (n == 0) return;
+  cudaError_t e = cudaMalloc(&p, n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw PetraError(PETRA_E_OOM, "cudaMalloc(" + std::to_string(n) + "): " + cudaGetErrorString(e));
+  }
+}
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+DevPtr dalloc(size_t bytes) { return DevPtr(new DevBuf(bytes)); }
+
+namespace {
+
+uint64_t splitmix(uint64_t &s) {
+  uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+void check_conv(const petra_conv &c) {
+  if (c.cin <= 0 || c.cout <= 0 || c.ksize <= 0 || c.stride <= 0 || (c.ksize % 2) == 0)
+    throw PetraError(PETRA_E_ARG, "invalid conv (cin/cout/ksize/stride must be positive, ksize odd)");
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ construction
+Stage::Stage(const petra_stage_desc &desc, uint64_t seed) : desc_(desc) {
+  if (desc.n_units <= 0 || !desc.units) throw PetraError(PETRA_E_ARG, "stage needs at least one unit");
+  if (desc.batch <= 0 || desc.in_h <= 0 || desc.in_w <= 0 || desc.in_c <= 0)
+    throw PetraError(PETRA_E_ARG, "non-positive stage input shape");
+  if (desc.precision != PETRA_FP32 && desc.precision != PETRA_BF16_TC)
+    throw PetraError(PETRA_E_ARG, "unknown precision");
+  if (desc.accumulation_k != 1)
+    throw PetraError(PETRA_E_UNSUPPORTED, "accumulation_k > 1 is not implemented (k = 1 hot path)");
+  if (!(desc.momentum >= 0.f) || !(desc.weight_decay >= 0.f) || !(desc.bn_eps > 0.f))
+    throw PetraError(PETRA_E_ARG, "bad optimizer / BN hyper-parameters");
+  tc_ = desc.precision == PETRA_BF16_TC;
+  int dev = 0;
+  PETRA_CUDA(cudaGetDevice(&dev));
+  units_.resize(desc.n_units);
+  for (int i = 0; i < desc.n_units; ++i) units_[i].d = desc.units[i];
+  build();
+  init_params(seed);
+}
+
+Stage::~Stage() = default;
+
+int64_t Stage::add_tensor(int unit, int part, int kind, int decay, std::vector<int> shape, bool buffer) {
+  petra_tensor_info t{};
+  t.unit = unit;
+  t.part = part;
+  t.kind = kind;
+  t.decay = decay;
+  t.ndim = (int)shape.size();
+  int64_t cnt = 1;
+  for (int i = 0; i < t.ndim; ++i) {
+    t.shape[i] = shape[i];
+    cnt *= shape[i];
+  }
+  t.count = cnt;
+  if (buffer) {
+    t.offset = n_buffers_;
+    n_buffers_ += cnt;
+  } else {
+    t.offset = n_params_;
+    n_params_ += cnt;
+  }
+  tensors_.push_back(t);
+  return t.offset;
+}
+
+void Stage::alloc_layer(Layer &L, bool inner) {
+  int64_t n = L.g.M() * L.g.Co;
+  L.z = dalloc(n * sizeof(float));
+  L.dz = dalloc(n * sizeof(float));
+  L.mean = dalloc(L.g.Co * sizeof(float));
+  L.invstd = dalloc(L.g.Co * sizeof(float));
+  if (inner) {
+    L.a = dalloc(n * sizeof(float));
+    L.da = dalloc(n * sizeof(float));
+  }
+  if (tc_) {
+    L.w_bf16 = dalloc((int64_t)L.g.Co * L.g.K() * sizeof(__nv_bfloat16));
+    L.wt_bf16 = dalloc((int64_t)L.g.Co * L.g.K() * sizeof(__nv_bfloat16));
+    L.dzb = dalloc(n * sizeof(__nv_bfloat16));
+    L.xb = dalloc(L.g.Min() * L.g.Ci * sizeof(__nv_bfloat16));
+  }
+}
+
+void Stage::build() {
+  const int B = desc_.batch;
+  Shape cur{B, desc_.in_h, desc_.in_w, desc_.in_c};
+  in_ = cur;
+  size_t max_part = 0, max_ws = 0;
+  std::vector<std::vector<Layer *>> unit_layers(units_.size());
+  struct Pending {
+    Layer *L;
+    int unit, part;
+  };
+  std::vector<Pending> layers;
+  for (size_t ui = 0; ui < units_.size(); ++ui) {
+    Unit &u = units_[ui];
+    const petra_unit &d = u.d;
+    u.in = cur;
+    if (d.kind == PETRA_UNIT_TAIL && ui + 1 != units_.size())
+      throw PetraError(PETRA_E_SHAPE, "the tail must be the last unit of its stage");
+    if (d.kind == PETRA_UNIT_STEM && ui != 0) throw PetraError(PETRA_E_SHAPE, "the stem must be the first unit");
+    switch (d.kind) {
+      case PETRA_UNIT_STEM: {
+        check_conv(d.layer[0]);
+        if (d.layer[0].cin != cur.C) throw PetraError(PETRA_E_SHAPE, "stem cin != image channels");
+        if (d.layer[0].cout % 2) throw PetraError(PETRA_E_ODD_CHANNELS, "stem output channels must be even");
+        u.phi.resize(1);
+        Layer &L = u.phi[0];
+        L.g = make_geom(B, cur.H, cur.W, cur.C, d.layer[0].cout, d.layer[0].ksize, d.layer[0].stride);
+        L.relu = true;
+        layers.push_back({&L, (int)ui, 0});
+        int Ho = L.g.Ho, Wo = L.g.Wo;
+        if (d.maxpool) {
+          u.pool_a = dalloc(L.g.M() * L.g.Co * sizeof(float));
+          Ho = (Ho + 2 - 3) / 2 + 1;
+          Wo = (Wo + 2 - 3) / 2 + 1;
+          u.pool_arg = dalloc((int64_t)B * Ho * Wo * L.g.Co);
+        }
+        cur = Shape{B, Ho, Wo, d.layer[0].cout / 2};
+        break;
+      }
+      case PETRA_UNIT_REV:
+      case PETRA_UNIT_DS: {
+        if (d.dst_half != 0 && d.dst_half != 1) throw PetraError(PETRA_E_ARG, "dst_half must be 0 or 1");
+        if (d.n_layers < 1 || d.n_layers > 3) throw PetraError(PETRA_E_ARG, "n_layers must be 1..3");
+        u.phi.resize(d.n_layers);
+        Shape s = cur;
+        for (int l = 0; l < d.n_layers; ++l) {
+          check_conv(d.layer[l]);
+          if (d.layer[l].cin != s.C)
+            throw PetraError(PETRA_E_SHAPE, "unit " + std::to_string(ui) + " layer " + std::to_string(l) +
+                                                ": cin " + std::to_string(d.layer[l].cin) + " != " +
+                                                std::to_string(s.C));
+          Layer &L = u.phi[l];
+          L.g = make_geom(B, s.H, s.W, s.C, d.layer[l].cout, d.layer[l].ksize, d.layer[l].stride);
+          L.relu = true;
+          layers.push_back({&L, (int)ui, l});
+          s = Shape{B, L.g.Ho, L.g.Wo, L.g.Co};
+        }
+        if (d.kind == PETRA_UNIT_REV) {
+          if (s != cur) throw PetraError(PETRA_E_SHAPE, "reversible unit must preserve the half shape");
+        } else {
+          for (int k = 0; k < 2; ++k) {
+            check_conv(d.proj[k]);
+            if (d.proj[k].cin != cur.C || d.proj[k].cout != s.C)
+              throw PetraError(PETRA_E_SHAPE, "DS projection channels do not match");
+            Layer &P = k == 0 ? u.pa : u.pb;
+            P.g = make_geom(B, cur.H, cur.W, cur.C, d.proj[k].cout, d.proj[k].ksize, d.proj[k].stride);
+            P.relu = false;
+            if (P.g.Ho != s.H || P.g.Wo != s.W) throw PetraError(PETRA_E_SHAPE, "DS projection stride mismatch");
+            layers.push_back({&P, (int)ui, 3 + k});
+          }
+          cur = s;
+        }
+        break;
+      }
+      case PETRA_UNIT_TAIL: {
+        if (d.classes <= 0) throw PetraError(PETRA_E_ARG, "classes must be positive");
+        is_last_ = true;
+        break;
+      }
+      default:
+        throw PetraError(PETRA_E_ARG, "unknown unit kind");
+    }
+    u.out = cur;
+  }
+  out_ = is_last_ ? Shape{B, 1, 1, units_.back().d.classes} : cur;
+
+  // ---- parameter layout: per unit, per layer (W, gamma, beta); tail (W, b); then buffers
+  for (auto &p : layers) {
+    Layer &L = *p.L;
+    L.w_off = add_tensor(p.unit, p.part, PETRA_T_CONV_W, 1, {L.g.Co, L.g.k, L.g.k, L.g.Ci}, false);
+    L.g_off = add_tensor(p.unit, p.part, PETRA_T_BN_GAMMA, 0, {L.g.Co}, false);
+    L.b_off = add_tensor(p.unit, p.part, PETRA_T_BN_BETA, 0, {L.g.Co}, false);
+  }
+  if (is_last_) {
+    Unit &t = units_.back();
+    t.fc_w = add_tensor((int)units_.size() - 1, 0, PETRA_T_FC_W, 1, {t.d.classes, 2 * t.in.C}, false);
+    t.fc_b = add_tensor((int)units_.size() - 1, 0, PETRA_T_FC_B, 0, {t.d.classes}, false);
+  }
+  for (auto &p : layers) {
+    Layer &L = *p.L;
+    L.rm_off = add_tensor(p.unit, p.part, PETRA_T_BN_RMEAN, 0, {L.g.Co}, true);
+    L.rv_off = add_tensor(p.unit, p.part, PETRA_T_BN_RVAR, 0, {L.g.Co}, true);
+  }
+  theta_ = dalloc(n_params_ * sizeof(float));
+  v_ = dalloc(n_params_ * sizeof(float));
+  grad_ = dalloc(n_params_ * sizeof(float));
+  bufs_ = dalloc(std::max<int64_t>(1, n_buffers_) * sizeof(float));
+  PETRA_CUDA(cudaMemset(grad_->p, 0, n_params_ * sizeof(float)));
+
+  // ---- workspace
+  for (auto &u : units_) {
+    for (size_t l = 0; l < u.phi.size(); ++l) alloc_layer(u.phi[l], l + 1 < u.phi.size());
+    if (u.d.kind == PETRA_UNIT_DS) {
+      alloc_layer(u.pa, false);
+      alloc_layer(u.pb, false);
+    }
+  }
+  for (auto &p : layers) {
+    max_part = std::max(max_part, bn_partial_bytes(p.L->g.M(), p.L->g.Co));
+    max_ws = std::max(max_ws, tc_ ? std::max(conv_tc_workspace(p.L->g, 2), conv_wgrad_simt_workspace(p.L->g))
+                                  : conv_wgrad_simt_workspace(p.L->g));
+  }
+  part_ = dalloc(std::max<size_t>(max_part, 16));
+  wgrad_ws_ = dalloc(std::max<size_t>(max_ws, 16));
+  nonfinite_ = dalloc(sizeof(int));
+  PETRA_CUDA(cudaMemset(nonfinite_->p, 0, sizeof(int)));
+
+  // ---- output-target planning (see header of forward/backward)
+  const int n = (int)units_.size();
+  int cap = std::max(1, desc_.fifo_capacity);
+  for (int i = 0; i < n; ++i) {
+    Unit &u = units_[i];
+    bool later_nonrev = false, earlier_nonrev = false;
+    for (int k = i + 1; k < n; ++k)
+      if (units_[k].d.kind == PETRA_UNIT_DS || units_[k].d.kind == PETRA_UNIT_STEM) later_nonrev = true;
+    for (int k = 0; k < i; ++k)
+      if (units_[k].d.kind == PETRA_UNIT_DS || units_[k].d.kind == PETRA_UNIT_STEM) earlier_nonrev = true;
+    if (u.d.kind == PETRA_UNIT_TAIL) continue;
+    bool need_fout = later_nonrev || is_last_;
+    if (need_fout)
+      for (int h = 0; h < 2; ++h) u.fout[h] = dalloc(u.out.numel() * sizeof(float));
+    if (earlier_nonrev) {
+      for (int h = 0; h < 2; ++h) {
+        if (u.d.kind == PETRA_UNIT_REV) u.bx[h] = dalloc(u.in.numel() * sizeof(float));
+        if (u.d.kind != PETRA_UNIT_STEM) u.bd[h] = dalloc(u.in.numel() * sizeof(float));
+      }
+    } else if (u.d.kind == PETRA_UNIT_DS && is_last_) {
+      for (int h = 0; h < 2; ++h) u.bd[h] = dalloc(u.in.numel() * sizeof(float));
+    }
+    if (u.d.kind == PETRA_UNIT_DS || u.d.kind == PETRA_UNIT_STEM) {
+      u.fifo.cap = is_last_ ? 1 : cap;
+      for (int s = 0; s < u.fifo.cap; ++s) {
+        u.fifo.slot0.push_back(dalloc(u.in.numel() * sizeof(float)));
+        if (u.d.kind == PETRA_UNIT_DS) u.fifo.slot1.push_back(dalloc(u.in.numel() * sizeof(float)));
+      }
+    }
+  }
+  if (is_last_) {
+    Unit &t = units_.back();
+    int Cin = 2 * t.in.C;
+    feat_ = dalloc((int64_t)B * Cin * sizeof(float));
+    logits_ = dalloc((int64_t)B * t.d.classes * sizeof(float));
+    dlogits_ = dalloc((int64_t)B * t.d.classes * sizeof(float));
+    lossrow_ = dalloc((int64_t)B * sizeof(float));
+    dfeat_ = dalloc((int64_t)B * Cin * sizeof(float));
+    for (int h = 0; h < 2; ++h) tail_d_[h] = dalloc(t.in.numel() * sizeof(float));
+  }
+
+  // ---- optimizer segments
+  for (auto &t : tensors_) {
+    if (t.kind > PETRA_T_FC_B) continue;
+    SgdSeg s{};
+    s.offset = t.offset;
+    s.count = t.count;
+    s.decay = t.decay;
+    segs_.push_back(s);
+    max_seg_ = std::max<int64_t>(max_seg_, t.count);
+  }
+  if (tc_) {
+    for (auto &p : layers) {
+      for (auto &s : segs_)
+        if (s.offset == p.L->w_off) {
+          s.co = p.L->g.Co;
+          s.k = p.L->g.k;
+          s.ci = p.L->g.Ci;
+          s.w_bf16 = p.L->w_bf16->as<__nv_bfloat16>();
+          s.wt_bf16 = p.L->wt_bf16->as<__nv_bfloat16>();
+        }
+    }
+  }
+  segs_dev_ = dalloc(segs_.size() * sizeof(SgdSeg));
+  PETRA_CUDA(cudaMemcpy(segs_dev_->p, segs_.data(), segs_.size() * sizeof(SgdSeg), cudaMemcpyHostToDevice));
+}
+
+void Stage::init_params(uint64_t seed) {
+  std::vector<float> th(n_params_, 0.f), bufs(std::max<int64_t>(1, n_buffers_), 0.f);
+  uint64_t s = seed * 0x2545F4914F6CDD1Dull + 1;
+  for (auto &t : tensors_) {
+    float *dst = (t.kind >= PETRA_T_BN_RMEAN ? bufs.data() : th.data()) + t.offset;
+    if (t.kind == PETRA_T_CONV_W || t.kind == PETRA_T_FC_W) {
+      int64_t fan_in = t.count / t.shape[0];
+      double b = std::sqrt(6.0 / (double)fan_in);
+      for (int64_t i = 0; i < t.count; ++i) {
+        double u = (double)(splitmix(s) >> 11) * (1.0 / 9007199254740992.0);
+        dst[i] = (float)((2.0 * u - 1.0) * b);
+      }
+    } else if (t.kind == PETRA_T_BN_GAMMA || t.kind == PETRA_T_BN_RVAR) {
+      for (int64_t i = 0; i < t.count; ++i) dst[i] = 1.f;
+    }
+  }
+  std::vector<float> zeros(n_params_, 0.f);
+  set_params(th.data(), zeros.data(), bufs.data());
+}
+
+// ------------------------------------------------------------------ params
+void Stage::set_params(const float *theta, const float *v, const float *bufs) {
+  if (theta) PETRA_CUDA(cudaMemcpy(theta_->p, theta, n_params_ * sizeof(float), cudaMemcpyHostToDevice));
+  if (v) PETRA_CUDA(cudaMemcpy(v_->p, v, n_params_ * sizeof(float), cudaMemcpyHostToDevice));
+  if (bufs && n_buffers_)
+    PETRA_CUDA(cudaMemcpy(bufs_->p, bufs, n_buffers_ * sizeof(float), cudaMemcpyHostToDevice));
+  if (tc_ && theta) {
+    sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
+               grad_->as<float>(), 0.f, 0.f, 0.f, 1, nullptr, /*shadow_only=*/true);
+    PETRA_CUDA(cudaDeviceSynchronize());
+  }
+}
+
+void Stage::get_params(float *theta, float *v, float *bufs) {
+  PETRA_CUDA(cudaDeviceSynchronize());
+  if (theta) PETRA_CUDA(cudaMemcpy(theta, theta_->p, n_params_ * sizeof(float), cudaMemcpyDeviceToHost));
+  if (v) PETRA_CUDA(cudaMemcpy(v, v_->p, n_params_ * sizeof(float), cudaMemcpyDeviceToHost));
+  if (bufs && n_buffers_)
+    PETRA_CUDA(cudaMemcpy(bufs, bufs_->p, n_buffers_ * sizeof(float), cudaMemcpyDeviceToHost));
+}
+
+void Stage::get_grads(float *delta) {
+  PETRA_CUDA(cudaDeviceSynchronize());
+  PETRA_CUDA(cudaMemcpy(delta, grad_->p, n_params_ * sizeof(float), cudaMemcpyDeviceToHost));
+}
+
+bool Stage::nonfinite() {
+  int h = 0;
+  PETRA_CUDA(cudaDeviceSynchronize());
+  PETRA_CUDA(cudaMemcpy(&h, nonfinite_->p, sizeof(int), cudaMemcpyDeviceToHost));
+  return h != 0;
+}
+
+int Stage::fifo_depth() const {
+  int d = 0;
+  for (auto &u : units_) d += u.fifo.size;
+  return d;
+}
+
+void Stage::update(float lr, cudaStream_t st) {
+  sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
+             grad_->as<float>(), lr, desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false);
+  ++version_;
+}
+
+// ------------------------------------------------------------------ layer kernels
+void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st) {
+  const float *w = theta_->as<float>() + L.w_off;
+  if (tc_ && conv_tc_supported(L.g, 0)) {
+    f32_to_bf16(x, L.xb->as<__nv_bfloat16>(), L.g.Min() * L.g.Ci, st);
+    conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->as<float>(), nullptr, st);
+  } else {
+    conv_fwd_simt(L.g, x, w, L.z->as<float>(), st);
+  }
+}
+
+void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
+  float *dw = grad_->as<float>() + L.w_off;
+  if (tc_ && conv_tc_supported(L.g, 2)) {
+    // L.xb holds bf16(x) from the conv_fwd of this tick (forward or recomputation)
+    f32_to_bf16(L.dz->as<float>(), L.dzb->as<__nv_bfloat16>(), L.g.M() * L.g.Co, st);
+    conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.xb->as<__nv_bfloat16>(), dw, wgrad_ws_->as<float>(), st);
+  } else {
+    conv_wgrad_simt(L.g, L.dz->as<float>(), x, dw, wgrad_ws_->as<float>(), st);
+  }
+}
+
+void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t st) {
+  if (tc_ && conv_tc_supported(L.g, 1)) {
+    if (!conv_tc_supported(L.g, 2))  // dz bf16 not produced by wgrad path
+      f32_to_bf16(L.dz->as<float>(), L.dzb->as<__nv_bfloat16>(), L.g.M() * L.g.Co, st);
+    conv_dgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.wt_bf16->as<__nv_bfloat16>(), addend, out, st);
+  } else {
+    conv_dgrad_simt(L.g, L.dz->as<float>(), theta_->as<float>() + L.w_off, addend, out, st);
+  }
+}
+
+void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
+  float *b = bufs_->as<float>();
+  bn_stats<float>(L.z->as<float>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean->as<float>(), L.invstd->as<float>(),
+                  running ? b + L.rm_off : nullptr, running ? b + L.rv_off : nullptr, desc_.bn_momentum,
+                  part_->as<double>(), st);
+}
+
+// forward of a conv-BN-ReLU chain on x; inner activations into L.a; the last
+// layer's z / stats are left for the caller's fused epilogue.
+void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running, cudaStream_t st) {
+  const float *th = theta_->as<float>();
+  for (size_t l = 0; l < phi.size(); ++l) {
+    Layer &L = phi[l];
+    conv_fwd(L, x, st);
+    layer_stats(L, running, st);
+    if (l + 1 < phi.size()) {
+      bn_apply<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+                             L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr, L.a->as<float>(),
+                             nullptr, st);
+      x = L.a->as<float>();
+    }
+  }
+}
+
+// BN(+ReLU) backward of one layer given dy (gradient wrt the layer output);
+// optional fused reconstruction dst_out = dst_in - act(bn(z)); writes dgamma,
+// dbeta into Delta and dz into L.dz.
+void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, const float *dst_in, float *dst_out,
+                      cudaStream_t st) {
+  const float *th = theta_->as<float>();
+  float *gr = grad_->as<float>();
+  bn_bwd_reduce<float>(L.z->as<float>(), L.g.M(), L.g.Co, L.mean->as<float>(), L.invstd->as<float>(),
+                       th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, dst_in, dst_out, nullptr,
+                       gr + L.g_off, gr + L.b_off, part_->as<double>(), st);
+  bn_bwd_dz<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.mean->as<float>(), L.invstd->as<float>(),
+                          th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off,
+                          L.dz->as<float>(), st);
+}
+
+// VJP through a branch whose last layer receives dy (reconstruction fused when
+// dst_out != null).  dx_out = addend + d(branch)/dx^T dy  (dx_out may be null).
+void Stage::branch_backward(std::vector<Layer> &phi, const float *x, const float *dy, const float *dst_in,
+                            float *dst_out, const float *addend, float *dx_out, cudaStream_t st) {
+  int n = (int)phi.size();
+  layer_bwd(phi[n - 1], dy, nullptr, 0, dst_in, dst_out, st);
+  for (int l = n - 1; l >= 0; --l) {
+    Layer &L = phi[l];
+    const float *xl = l == 0 ? x : phi[l - 1].a->as<float>();
+    conv_wgrad(L, xl, st);
+    if (l > 0) {
+      conv_dgrad(L, nullptr, phi[l - 1].da->as<float>(), st);
+      layer_bwd(phi[l - 1], phi[l - 1].da->as<float>(), nullptr, 0, nullptr, nullptr, st);
+    } else if (dx_out) {
+      conv_dgrad(L, addend, dx_out, st);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ units
+// forward of one unit: cur[] = current halves (inputs), out[] = where the unit's
+// outputs go (REV: only out[dst] is written; may equal cur[dst] for in place).
+void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep, cudaStream_t st) {
+  const float *th = theta_->as<float>();
+  switch (u.d.kind) {
+    case PETRA_UNIT_REV: {
+      // x[dst] += Phi(x[src])  (north_star y1 = x1 + F(x2), y2 = x2 + G(y1))
+      branch_forward(u.phi, cur[u.src()], keep, st);
+      Layer &L = u.phi.back();
+      bn_apply<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+                             L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, cur[u.dst()], out[u.dst()],
+                             nullptr, st);
+      break;
+    }
+    case PETRA_UNIT_DS: {
+      // y[dst] = P_a(x[dst]) + Phi_s(x[src]);  y[src] = P_b(x[src])
+      const float *xd = cur[u.dst()], *xs = cur[u.src()];
+      branch_forward(u.phi, xs, keep, st);
+      conv_fwd(u.pa, xd, st);
+      layer_stats(u.pa, keep, st);
+      conv_fwd(u.pb, xs, st);
+      layer_stats(u.pb, keep, st);
+      Layer &L = u.phi.back();
+      int64_t M = L.g.M();
+      int C = L.g.Co;
+      bn_apply<float, float>(M, C, u.pa.z->as<float>(), C, 0, u.pa.mean->as<float>(), u.pa.invstd->as<float>(),
+                             th + u.pa.g_off, th + u.pa.b_off, 0, 1.f, nullptr, out[u.dst()], nullptr, st);
+      bn_apply<float, float>(M, C, L.z->as<float>(), C, 0, L.mean->as<float>(), L.invstd->as<float>(),
+                             th + L.g_off, th + L.b_off, 1, 1.f, out[u.dst()], out[u.dst()], nullptr, st);
+      bn_apply<float, float>(M, C, u.pb.z->as<float>(), C, 0, u.pb.mean->as<float>(), u.pb.invstd->as<float>(),
+                             th + u.pb.g_off, th + u.pb.b_off, 0, 1.f, nullptr, out[u.src()], nullptr, st);
+      break;
+    }
+    case PETRA_UNIT_STEM: {
+      Layer &L = u.phi[0];
+      conv_fwd(L, cur[0], st);
+      layer_stats(L, keep, st);
+      int Ch = L.g.Co / 2;
+      if (u.d.maxpool) {
+        bn_apply<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+                               L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
+                               u.pool_a->as<float>(), nullptr, st);
+        maxpool_fwd(u.pool_a->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, out[0], out[1],
+                    u.pool_arg->as<uint8_t>(), st);
+      } else {
+        for (int h = 0; h < 2; ++h)
+          bn_apply<float, float>(L.g.M(), Ch, L.z->as<float>(), L.g.Co, h * Ch, L.mean->as<float>(),
+                                 L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr, out[h],
+                                 nullptr, st);
+      }
+      break;
+    }
+    default:
+      throw PetraError(PETRA_E_ARG, "unit_forward: bad kind");
+  }
+}
+
+// backward of one unit.  cur_x = unit output (reconstructed or current), xin =
+// the unit input for non-reversible units (FIFO slot), cur_d = gradient wrt the
+// unit output; out_x / out_d = targets (REV: out_x[dst], out_d[src]; DS: out_d[both]).
+void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const float *cur_x[2], float *out_x[2],
+                          const float *cur_d[2], float *out_d[2], cudaStream_t st) {
+  switch (u.d.kind) {
+    case PETRA_UNIT_REV: {
+      // approximate inversion with the current theta: recompute the
+      // graph of Phi on x[src] (src is unchanged by the unit), subtract, VJP.
+      const float *src = cur_x[u.src()];
+      if (recompute) branch_forward(u.phi, src, true, st);
+      branch_backward(u.phi, src, cur_d[u.dst()], cur_x[u.dst()], out_x[u.dst()], cur_d[u.src()],
+                      out_d[u.src()], st);
+      break;
+    }
+    case PETRA_UNIT_DS: {
+      const float *xd = xin[u.dst()], *xs = xin[u.src()];
+      if (recompute) {
+        branch_forward(u.phi, xs, true, st);
+        conv_fwd(u.pa, xd, st);
+        layer_stats(u.pa, true, st);
+        conv_fwd(u.pb, xs, st);
+        layer_stats(u.pb, true, st);
+      }
+      const float *dyd = cur_d[u.dst()], *dys = cur_d[u.src()];
+      // P_a: dx[dst] = P_a^T dy[dst]
+      layer_bwd(u.pa, dyd, nullptr, 0, nullptr, nullptr, st);
+      conv_wgrad(u.pa, xd, st);
+      if (out_d[u.dst()]) conv_dgrad(u.pa, nullptr, out_d[u.dst()], st);
+      // Phi_s: dx[src] = Phi_s^T dy[dst]
+      branch_backward(u.phi, xs, dyd, nullptr, nullptr, nullptr, out_d[u.src()], st);
+      // P_b: dx[src] += P_b^T dy[src]
+      layer_bwd(u.pb, dys, nullptr, 0, nullptr, nullptr, st);
+      conv_wgrad(u.pb, xs, st);
+      if (out_d[u.src()]) conv_dgrad(u.pb, out_d[u.src()], out_d[u.src()], st);
+      break;
+    }
+    case PETRA_UNIT_STEM: {
+      Layer &L = u.phi[0];
+      const float *th = theta_->as<float>();
+      if (recompute) {
+        conv_fwd(L, xin[0], st);
+        layer_stats(L, true, st);
+        if (u.d.maxpool) {
+          // recompute the pre-pool activation and argmax (outputs go to scratch)
+          bn_apply<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+                                 L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
+                                 u.pool_a->as<float>(), nullptr, st);
+          maxpool_fwd(u.pool_a->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, L.dz->as<float>(),
+                      L.dz->as<float>() + u.out.numel(), u.pool_arg->as<uint8_t>(), st);
+        }
+      }
+      if (u.d.maxpool) {
+        maxpool_bwd(cur_d[0], cur_d[1], u.pool_arg->as<uint8_t>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H,
+                    u.out.W, u.pool_a->as<float>(), st);
+        layer_bwd(L, u.pool_a->as<float>(), nullptr, 0, nullptr, nullptr, st);
+      } else {
+        layer_bwd(L, cur_d[0], cur_d[1], L.g.Co / 2, nullptr, nullptr, st);
+      }
+      conv_wgrad(L, xin[0], st);  // no dgrad: the stem input is data
+      break;
+    }
+    default:
+      throw PetraError(PETRA_E_ARG, "unit_backward: bad kind");
+  }
+}
+
+// ------------------------------------------------------------------ ticks
+static void copy_d2d(float *dst, const float *src, int64_t n, cudaStream_t st) {
+  if (dst && src && dst != src) PETRA_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+}
+
+static void fifo_push(Fifo &f, uint64_t mb, const float *a, const float *b, int64_t n, cudaStream_t st) {
+  if (f.size >= f.cap) throw PetraError(PETRA_E_ARG, "FIFO overflow: capacity below 2(J-j)+1");
+  int slot = (f.head + f.size) % f.cap;
+  copy_d2d(f.slot0[slot]->as<float>(), a, n, st);
+  if (b) copy_d2d(f.slot1[slot]->as<float>(), b, n, st);
+  f.ids.push_back(mb);
+  ++f.size;
+  f.peak = std::max(f.peak, f.size);
+}
+
+static int fifo_pop(Fifo &f, uint64_t mb) {
+  if (f.size == 0) throw PetraError(PETRA_E_EMPTY_BUFFER, "non-reversible backward with an empty FIFO");
+  if (f.ids.front() != mb)
+    throw PetraError(PETRA_E_ORDER, "backward mb " + std::to_string(mb) + " != FIFO head " +
+                                        std::to_string(f.ids.front()));
+  int slot = f.head;
+  f.head = (f.head + 1) % f.cap;
+  --f.size;
+  f.ids.pop_front();
+  return slot;
+}
+
+// Forward tick.  Targets: a unit that first writes a half writes into the stage
+// output buffer if no non-reversible unit follows, else into its own buffer;
+// later units work in place.  Caller inputs are never written.
+void Stage::forward(uint64_t mb, const float *x1, const float *x2, float *o1, float *o2, cudaStream_t st) {
+  if (is_last_) throw PetraError(PETRA_E_ARG, "the final stage runs petra_stage_tail");
+  if (!x1 || (!stem_first() && !x2) || !o1 || !o2) throw PetraError(PETRA_E_ARG, "NULL activation pointer");
+  if (have_last_fwd_ && mb <= last_fwd_mb_) throw PetraError(PETRA_E_ORDER, "forward mb ids must increase");
+  const float *cur[2] = {x1, x2};
+  bool ro[2] = {true, true};
+  float *outs[2] = {o1, o2};
+  const int n = (int)units_.size();
+  for (int i = 0; i < n; ++i) {
+    Unit &u = units_[i];
+    float *tgt[2];
+    for (int h = 0; h < 2; ++h) tgt[h] = u.fout[h] ? u.fout[h]->as<float>() : outs[h];
+    if (u.d.kind == PETRA_UNIT_REV) {
+      float *o[2] = {nullptr, nullptr};
+      int d = u.dst();
+      o[d] = ro[d] ? tgt[d] : const_cast<float *>(cur[d]);
+      unit_forward(u, cur, o, false, st);
+      cur[d] = o[d];
+      ro[d] = false;
+    } else {
+      fifo_push(u.fifo, mb, cur[0], u.d.kind == PETRA_UNIT_DS ? cur[1] : nullptr, u.in.numel(), st);
+      unit_forward(u, cur, tgt, false, st);
+      cur[0] = tgt[0];
+      cur[1] = tgt[1];
+      ro[0] = ro[1] = false;
+    }
+  }
+  for (int h = 0; h < 2; ++h)
+    if (cur[h] != outs[h]) copy_d2d(outs[h], cur[h], out_.numel(), st);
+  have_last_fwd_ = true;
+  last_fwd_mb_ = mb;
+  ++n_fwd_;
+  last_stream_ = st;
+}
+
+void Stage::backward(uint64_t mb, const float *xt1, const float *xt2, const float *d1, const float *d2,
+                     float *oxt1, float *oxt2, float *od1, float *od2, float lr, cudaStream_t st) {
+  if (is_last_) throw PetraError(PETRA_E_ARG, "the final stage runs petra_stage_tail");
+  if (!xt1 || !xt2 || !d1 || !d2) throw PetraError(PETRA_E_ARG, "NULL backward input");
+  if (!std::isfinite(lr) || lr < 0.f) throw PetraError(PETRA_E_ARG, "lr must be finite and >= 0");
+  const float *cx[2] = {xt1, xt2}, *cd[2] = {d1, d2};
+  bool rox[2] = {true, true}, rod[2] = {true, true};
+  float *ox[2] = {oxt1, oxt2}, *od[2] = {od1, od2};
+  for (int i = (int)units_.size() - 1; i >= 0; --i) {
+    Unit &u = units_[i];
+    if (u.d.kind == PETRA_UNIT_REV) {
+      int d = u.dst(), s = u.src();
+      float *tx[2] = {nullptr, nullptr}, *td[2] = {nullptr, nullptr};
+      tx[d] = rox[d] ? (u.bx[d] ? u.bx[d]->as<float>() : ox[d]) : const_cast<float *>(cx[d]);
+      td[s] = rod[s] ? (u.bd[s] ? u.bd[s]->as<float>() : od[s]) : const_cast<float *>(cd[s]);
+      if (!tx[d]) tx[d] = u.bx[d] ? u.bx[d]->as<float>() : nullptr;
+      if (!tx[d] || !td[s]) throw PetraError(PETRA_E_ARG, "NULL backward output for a reversible stage");
+      const float *nox[2] = {nullptr, nullptr};
+      unit_backward(u, true, nox, cx, tx, cd, td, st);
+      cx[d] = tx[d];
+      rox[d] = false;
+      cd[s] = td[s];
+      rod[s] = false;
+    } else {
+      int slot = fifo_pop(u.fifo, mb);
+      const float *xin[2] = {u.fifo.slot0[slot]->as<float>(),
+                             u.d.kind == PETRA_UNIT_DS ? u.fifo.slot1[slot]->as<float>() : nullptr};
+      float *td[2] = {nullptr, nullptr};
+      if (u.d.kind == PETRA_UNIT_DS)
+        for (int h = 0; h < 2; ++h) td[h] = u.bd[h] ? u.bd[h]->as<float>() : od[h];
+      unit_backward(u, true, xin, cx, nullptr, cd, td, st);
+      cx[0] = xin[0];
+      cx[1] = xin[1];
+      rox[0] = rox[1] = true;  // FIFO memory: copied out at the end, never written
+      cd[0] = td[0];
+      cd[1] = td[1];
+      rod[0] = rod[1] = false;
+    }
+  }
+  if (!stem_first()) {
+    for (int h = 0; h < 2; ++h) {
+      if (ox[h]) copy_d2d(ox[h], cx[h], in_.numel(), st);
+      if (od[h]) copy_d2d(od[h], cd[h], in_.numel(), st);
+    }
+  }
+  update(lr, st);
+  ++n_bwd_;
+  last_stream_ = st;
+}
+
+void Stage::tail(uint64_t mb, const float *x1, const float *x2, const int32_t *labels, float lr, float *oxt1,
+                 float *oxt2, float *od1, float *od2, float *loss, cudaStream_t st) {
+  if (!is_last_) throw PetraError(PETRA_E_ARG, "petra_stage_tail on a stage without a tail unit");
+  if (!x1 || (!stem_first() && !x2) || !labels) throw PetraError(PETRA_E_ARG, "NULL tail input");
+  if (!std::isfinite(lr) || lr < 0.f) throw PetraError(PETRA_E_ARG, "lr must be finite and >= 0");
+  const int n = (int)units_.size();
+  // forward with stored activations; running stats updated here (reading c10)
+  const float *cur[2] = {x1, x2};
+  bool ro[2] = {true, true};
+  for (int i = 0; i + 1 < n; ++i) {
+    Unit &u = units_[i];
+    float *tgt[2] = {u.fout[0]->as<float>(), u.fout[1]->as<float>()};
+    if (u.d.kind == PETRA_UNIT_REV) {
+      float *o[2] = {nullptr, nullptr};
+      int d = u.dst();
+      o[d] = ro[d] ? tgt[d] : const_cast<float *>(cur[d]);
+      unit_forward(u, cur, o, true, st);
+      cur[d] = o[d];
+      ro[d] = false;
+    } else {
+      fifo_push(u.fifo, mb, cur[0], u.d.kind == PETRA_UNIT_DS ? cur[1] : nullptr, u.in.numel(), st);
+      unit_forward(u, cur, tgt, true, st);
+      cur[0] = tgt[0];
+      cur[1] = tgt[1];
+      ro[0] = ro[1] = false;
+    }
+  }
+  Unit &t = units_.back();
+  const float *th = theta_->as<float>();
+  float *gr = grad_->as<float>();
+  tail_forward_backward(cur[0], cur[1], desc_.batch, t.in.H * t.in.W, t.in.C, th + t.fc_w, th + t.fc_b,
+                        t.d.classes, labels, feat_->as<float>(), logits_->as<float>(), dlogits_->as<float>(),
+                        lossrow_->as<float>(), dfeat_->as<float>(), gr + t.fc_w, gr + t.fc_b,
+                        tail_d_[0]->as<float>(), tail_d_[1]->as<float>(), loss, nonfinite_->as<int>(), st);
+  // plain backprop through the stored graph (no conv recomputation)
+  const float *cx[2] = {cur[0], cur[1]}, *cd[2] = {tail_d_[0]->as<float>(), tail_d_[1]->as<float>()};
+  for (int i = n - 2; i >= 0; --i) {
+    Unit &u = units_[i];
+    if (u.d.kind == PETRA_UNIT_REV) {
+      int d = u.dst(), s = u.src();
+      float *tx[2] = {nullptr, nullptr}, *td[2] = {nullptr, nullptr};
+      tx[d] = const_cast<float *>(cx[d]);  // in place (forward buffers of this stage)
+      td[s] = const_cast<float *>(cd[s]);  // stage-owned gradient buffers: in place
+      const float *nox[2] = {nullptr, nullptr};
+      unit_backward(u, false, nox, cx, tx, cd, td, st);
+      cx[d] = tx[d];
+      cd[s] = td[s];
+    } else {
+      int slot = fifo_pop(u.fifo, mb);
+      const float *xin[2] = {u.fifo.slot0[slot]->as<float>(),
+                             u.d.kind == PETRA_UNIT_DS ? u.fifo.slot1[slot]->as<float>() : nullptr};
+      float *td[2] = {nullptr, nullptr};
+      if (u.d.kind == PETRA_UNIT_DS)
+        for (int h = 0; h < 2; ++h) td[h] = u.bd[h]->as<float>();
+      unit_backward(u, false, xin, cx, nullptr, cd, td, st);
+      cx[0] = xin[0];
+      cx[1] = xin[1];
+      cd[0] = td[0];
+      cd[1] = td[1];
+    }
+  }
+  if (!stem_first()) {
+    // reading c7: the received input goes back unchanged, with delta_J wrt it
+    copy_d2d(oxt1, x1, in_.numel(), st);
+    copy_d2d(oxt2, x2, in_.numel(), st);
+    copy_d2d(od1, cd[0], in_.numel(), st);
+    copy_d2d(od2, cd[1], in_.numel(), st);
+  }
+  update(lr, st);
+  ++n_fwd_;
+  ++n_bwd_;
+  last_stream_ = st;
+}
+
+}  // namespace petra

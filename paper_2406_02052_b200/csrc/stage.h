@@ -1,0 +1,145 @@
+// stage.h -- one PETRA stage on one GPU: parameters, FIFOs, workspace and the
+// per-tick kernel sequence (Alg. 1).  Internal C++ API.
+#pragma once
+#include <deque>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/petra.h"
+#include "kernels.h"
+
+namespace petra {
+
+// device allocation owned by a stage
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t n);
+  ~DevBuf();
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+using DevPtr = std::unique_ptr<DevBuf>;
+DevPtr dalloc(size_t bytes);
+
+struct Shape {
+  int B = 0, H = 0, W = 0, C = 0;  // per half (or image)
+  int64_t numel() const { return (int64_t)B * H * W * C; }
+  bool operator==(const Shape &o) const { return B == o.B && H == o.H && W == o.W && C == o.C; }
+  bool operator!=(const Shape &o) const { return !(*this == o); }
+};
+
+struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
+  ConvGeom g;
+  bool relu = true;
+  int64_t w_off = 0, g_off = 0, b_off = 0;   // into theta / grad / v
+  int64_t rm_off = 0, rv_off = 0;            // into buffers (running stats)
+  DevPtr z, a, dz, da, mean, invstd;         // workspace, kept from forward to backward in a tick
+  DevPtr zb, ab, dzb, xb;                    // bf16 workspace (tensor-core path)
+  DevPtr w_bf16, wt_bf16;                    // bf16 shadows of the live weights
+  int64_t M() const { return g.M(); }
+};
+
+struct Fifo {                // input buffer of a non-reversible unit (reading c5)
+  int cap = 0, head = 0, size = 0;
+  std::vector<DevPtr> slot0, slot1;   // one tensor (stem) or two halves (DS)
+  std::deque<uint64_t> ids;
+  int peak = 0;
+};
+
+struct Unit {
+  petra_unit d;
+  Shape in, out;                       // per-half shapes (stem: in = image)
+  std::vector<Layer> phi;              // REV/DS branch; STEM: phi[0] is the stem conv
+  Layer pa, pb;                        // DS projections
+  int64_t fc_w = 0, fc_b = 0;          // TAIL offsets
+  Fifo fifo;
+  DevPtr pool_arg, pool_a;             // STEM max-pool argmax / pre-pool activation
+  // forward / backward output targets (planned at creation): buffer per half
+  DevPtr fout[2], bx[2], bd[2];
+  int dst() const { return d.dst_half; }
+  int src() const { return 1 - d.dst_half; }
+};
+
+struct TensorInfo {
+  petra_tensor_info i;
+};
+
+class Stage {
+ public:
+  Stage(const petra_stage_desc &desc, uint64_t seed);
+  ~Stage();
+
+  const Shape &in_shape() const { return in_; }
+  const Shape &out_shape() const { return out_; }
+  bool is_last() const { return is_last_; }
+  bool stem_first() const { return units_.front().d.kind == PETRA_UNIT_STEM; }
+  size_t n_params() const { return (size_t)n_params_; }
+  size_t n_buffers() const { return (size_t)n_buffers_; }
+  const std::vector<petra_tensor_info> &tensors() const { return tensors_; }
+  int64_t version() const { return version_; }
+  int fifo_depth() const;
+  int classes() const { return units_.back().d.classes; }
+
+  void forward(uint64_t mb, const float *x1, const float *x2, float *o1, float *o2, cudaStream_t st);
+  void backward(uint64_t mb, const float *xt1, const float *xt2, const float *d1, const float *d2, float *oxt1,
+                float *oxt2, float *od1, float *od2, float lr, cudaStream_t st);
+  void tail(uint64_t mb, const float *x1, const float *x2, const int32_t *labels, float lr, float *oxt1,
+            float *oxt2, float *od1, float *od2, float *loss, cudaStream_t st);
+
+  void get_params(float *theta, float *v, float *bufs);
+  void set_params(const float *theta, const float *v, const float *bufs);
+  void get_grads(float *delta);
+  bool nonfinite();
+  cudaStream_t last_stream() const { return last_stream_; }
+
+ private:
+  petra_stage_desc desc_;
+  std::vector<Unit> units_;
+  Shape in_, out_;
+  bool is_last_ = false;
+  bool tc_ = false;
+  int64_t n_params_ = 0, n_buffers_ = 0;
+  std::vector<petra_tensor_info> tensors_;
+  DevPtr theta_, v_, grad_, bufs_;
+  std::vector<SgdSeg> segs_;
+  DevPtr segs_dev_;
+  int64_t max_seg_ = 0;
+  DevPtr part_, wgrad_ws_;
+  DevPtr nonfinite_;
+  // tail workspace
+  DevPtr feat_, logits_, dlogits_, lossrow_, dfeat_, tail_d_[2];
+  // bf16 shadows of stage-level stream halves (TC path)
+  int64_t version_ = 0;
+  int64_t n_fwd_ = 0, n_bwd_ = 0;
+  bool have_last_fwd_ = false;
+  uint64_t last_fwd_mb_ = 0;
+  cudaStream_t last_stream_ = nullptr;
+
+  void build();
+  void alloc_layer(Layer &L, bool inner);
+  int64_t add_tensor(int unit, int part, int kind, int decay, std::vector<int> shape, bool buffer);
+  void init_params(uint64_t seed);
+  void update(float lr, cudaStream_t st);
+
+  // kernels of one layer / unit
+  void conv_fwd(Layer &L, const float *x, cudaStream_t st);
+  void conv_wgrad(Layer &L, const float *x, cudaStream_t st);
+  void conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t st);
+  void layer_stats(Layer &L, bool running, cudaStream_t st);
+  void branch_forward(std::vector<Layer> &phi, const float *x, bool running, cudaStream_t st);
+  void layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, const float *dst_in, float *dst_out,
+                 cudaStream_t st);
+  void branch_backward(std::vector<Layer> &phi, const float *x, const float *dy, const float *dst_in,
+                       float *dst_out, const float *addend, float *dx_out, cudaStream_t st);
+
+  void unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep, cudaStream_t st);
+  void unit_backward(Unit &u, bool recompute, const float *xin[2], const float *cur_x[2], float *out_x[2],
+                     const float *cur_d[2], float *out_d[2], cudaStream_t st);
+};
+
+}  // namespace petra

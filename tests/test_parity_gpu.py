@@ -1,0 +1,488 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on
+identical seeded inputs and parameters.  Tolerances (north_star): rel 1e-4 for
+the fp32 path, rel 2e-2 for the bf16 tensor-core path, integer schedule
+reports bit-exact."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import engine as E
+from oracle import models as OM
+from oracle.units import Branch, ConvBN, DSUnit, RevUnit, StemUnit, TailUnit
+from tests.gpu_harness import (nchw, nhwc, oracle_to_product_units, pack_like, pack_params, per_tensor_rel,
+                               rand_params, rel)
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from paper_2406_02052_b200 import Pipeline, Stage  # noqa: E402
+from paper_2406_02052_b200 import _lib as L  # noqa: E402
+from paper_2406_02052_b200 import models as PM  # noqa: E402
+
+TOL = {L.FP32: 1e-4, L.BF16_TC: 2e-2}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    L.lib()
+
+
+def dev(a, dtype=torch.float32):
+    return torch.tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+def host(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def rev(c, dst, k=3):
+    return RevUnit(dst, Branch([ConvBN(c, c, k, 1)]))
+
+
+def bott(c, mid, dst):
+    return RevUnit(dst, Branch([ConvBN(c, mid, 1, 1), ConvBN(mid, mid, 3, 1), ConvBN(mid, c, 1, 1)]))
+
+
+def ds_basic(ci, co, s=2):
+    return DSUnit(0, Branch([ConvBN(ci, co, 3, s)]), ConvBN(ci, co, 1, s, relu=False),
+                  ConvBN(ci, co, 1, s, relu=False))
+
+
+def ds_bott(ci, mid, co, s=2):
+    return DSUnit(0, Branch([ConvBN(ci, mid, 1, 1), ConvBN(mid, mid, 3, s), ConvBN(mid, co, 1, 1)]),
+                  ConvBN(ci, co, 1, s, relu=False), ConvBN(ci, co, 1, s, relu=False))
+
+
+def make_pair(units, B, in_hwc, precision, seed=3):
+    rand_params(units, seed)
+    spec = PM.StageSpec(oracle_to_product_units(units), B, in_hwc, precision, fifo_capacity=3)
+    st = Stage(spec, seed=0)
+    th, bf = pack_params(units)
+    assert th.size == st.n_params and bf.size == st.n_buffers
+    st.set_params(th, np.zeros_like(th), bf)
+    return st
+
+
+def check(name, got, want, tol, report):
+    r = rel(got, want)
+    report.append((name, r))
+    return r <= tol
+
+
+STAGE_CASES = {
+    # name: (units factory, batch, input NCHW shapes)
+    "rev_basic_c64_32x32": (lambda: [rev(64, 0), rev(64, 1)], 2, [(2, 64, 32, 32)] * 2),
+    "rev_basic_c128_16x16": (lambda: [rev(128, 0), rev(128, 1)], 2, [(2, 128, 16, 16)] * 2),
+    "rev_bottleneck": (lambda: [bott(64, 16, 0), bott(64, 16, 1)], 4, [(4, 64, 8, 8)] * 2),
+    "ds_basic_then_rev": (lambda: [ds_basic(32, 64), rev(64, 1)], 4, [(4, 32, 16, 16)] * 2),
+    "ds_bottleneck_then_rev": (lambda: [ds_bott(32, 16, 64), bott(64, 16, 1)], 2, [(2, 32, 12, 12)] * 2),
+    "rev_then_ds": (lambda: [rev(32, 1), ds_basic(32, 64), rev(64, 1)], 2, [(2, 32, 8, 8)] * 2),
+    "stem_cifar_then_rev": (lambda: [StemUnit(3, 64, 3, 1, False), rev(32, 0)], 4, [(4, 3, 16, 16)]),
+    "stem_imagenet_maxpool": (lambda: [StemUnit(3, 32, 7, 2, True), rev(16, 0)], 2, [(2, 3, 30, 30)]),
+}
+
+
+@pytest.mark.parametrize("precision", [L.FP32])
+@pytest.mark.parametrize("case", sorted(STAGE_CASES))
+def test_stage_tick_parity(case, precision):
+    """One forward tick then one backward tick (reconstruction with the current
+    theta + VJP + immediate Nesterov update) of a non-final stage."""
+    make, B, in_shapes = STAGE_CASES[case]
+    units = make()
+    stem = isinstance(units[0], StemUnit)
+    in_hwc = tuple(np.array(in_shapes[0])[[2, 3, 1]])
+    st = make_pair(units, B, in_hwc, precision)
+    ostage = E.Stage(units, E.OptConfig(), 1, 2)
+    ostage.lr = 0.1
+    tol = TOL[precision]
+    xs = [synth.images(s, 0, i) for i, s in enumerate(in_shapes)]
+    # ---- forward
+    fo = ostage.forward(E.Fwd(0, xs, None))
+    Bq, Ho, Wo, Co = st.out_shape
+    o1 = torch.empty((Bq, Ho, Wo, Co), device="cuda")
+    o2 = torch.empty_like(o1)
+    gx = [dev(nhwc(x)) for x in xs]
+    st.forward(0, gx[0], gx[1] if not stem else None, o1, o2)
+    torch.cuda.synchronize()
+    rep = []
+    ok = check("fwd.x1", nchw(host(o1)), fo.xs[0], tol, rep) & check("fwd.x2", nchw(host(o2)), fo.xs[1], tol, rep)
+    # ---- backward on received (x~, delta): the output perturbed, random delta
+    xt = [fo.xs[h] + 0.05 * synth.normal(fo.xs[h].shape, 7, h) for h in range(2)]
+    dd = [synth.normal(fo.xs[h].shape, 8, h) for h in range(2)]
+    bo = ostage.backward(E.Bwd(0, xt, dd))
+    in_half = [torch.empty((B,) + tuple(in_hwc[:2]) + (in_hwc[2],), device="cuda") for _ in range(4)]
+    gxt, gd = [dev(nhwc(x)) for x in xt], [dev(nhwc(d)) for d in dd]
+    if stem:
+        st.backward(0, gxt[0], gxt[1], gd[0], gd[1], None, None, None, None, 0.1)
+    else:
+        st.backward(0, gxt[0], gxt[1], gd[0], gd[1], *in_half, 0.1)
+    torch.cuda.synchronize()
+    if not stem:
+        for h in range(2):
+            ok &= check(f"bwd.xt{h}", nchw(host(in_half[h])), bo.xs[h], tol, rep)
+            ok &= check(f"bwd.d{h}", nchw(host(in_half[2 + h])), bo.ds[h], tol, rep)
+    g = st.get_grads()
+    want_g = pack_like(units, ostage.last_grads)
+    for name, r in per_tensor_rel(units, g, want_g):
+        rep.append(("grad." + name, r))
+        ok &= r <= tol
+    th, v, bf = st.get_params()
+    want_th, want_bf = pack_params(units)
+    ok &= check("theta", th, want_th, tol, rep)
+    ok &= check("v", v, pack_like(units, ostage.v), tol, rep)
+    ok &= check("running", bf, want_bf, tol, rep)
+    assert ok, "\n".join(f"{n}: {r:.3e}" for n, r in rep)
+
+
+TAIL_CASES = {
+    "rev_rev_tail": (lambda: [rev(32, 0), rev(32, 1), TailUnit(64, 10)], 8, [(8, 32, 8, 8)] * 2),
+    "ds_rev_tail": (lambda: [ds_basic(16, 32), rev(32, 1), TailUnit(64, 10)], 4, [(4, 16, 8, 8)] * 2),
+    "bottleneck_tail_1000": (lambda: [bott(64, 16, 0), TailUnit(128, 1000)], 4, [(4, 64, 4, 4)] * 2),
+}
+
+
+@pytest.mark.parametrize("case", sorted(TAIL_CASES))
+def test_tail_stage_parity(case):
+    """Final stage: forward with stored graph, loss, backprop, update (reading c7/c10)."""
+    make, B, in_shapes = TAIL_CASES[case]
+    units = make()
+    in_hwc = tuple(np.array(in_shapes[0])[[2, 3, 1]])
+    st = make_pair(units, B, in_hwc, L.FP32)
+    ostage = E.Stage(units, E.OptConfig(), 2, 2)
+    ostage.lr = 0.1
+    xs = [synth.images(s, 0, i) for i, s in enumerate(in_shapes)]
+    lab = synth.labels(B, units[-1].classes, 0, 0)
+    loss_o, bo = ostage.tail_step(E.Fwd(0, xs, lab))
+    gx = [dev(nhwc(x)) for x in xs]
+    outs = [torch.empty_like(gx[0]) for _ in range(4)]
+    loss = torch.zeros(1, device="cuda")
+    st.tail(0, gx[0], gx[1], dev(lab, torch.int32), 0.1, *outs, loss)
+    torch.cuda.synchronize()
+    rep = [("loss", abs(loss.item() - loss_o) / abs(loss_o))]
+    ok = rep[0][1] <= 1e-5
+    for h in range(2):
+        ok &= check(f"xt{h}", nchw(host(outs[h])), xs[h].astype(np.float32), 0.0, rep)  # exact copy
+        ok &= check(f"d{h}", nchw(host(outs[2 + h])), bo.ds[h], 1e-4, rep)
+    for name, r in per_tensor_rel(units, st.get_grads(), pack_like(units, ostage.last_grads)):
+        rep.append(("grad." + name, r))
+        ok &= r <= 1e-4
+    th, v, bf = st.get_params()
+    want_th, want_bf = pack_params(units)
+    ok &= check("theta", th, want_th, 1e-4, rep)
+    ok &= check("running", bf, want_bf, 1e-4, rep)
+    assert ok, "\n".join(f"{n}: {r:.3e}" for n, r in rep)
+
+
+def run_pipeline_pair(o_units, counts, B, image_nchw, classes, n_mb, lr, drain, precision=L.FP32,
+                      rev_first=False):
+    rand_params(o_units, 5)
+    groups = OM.group(o_units, counts)
+    init = [pack_params(g) for g in groups]   # before the oracle trains them
+    ost = [E.Stage(g, E.OptConfig()) for g in groups]
+
+    def batch_fn(m):
+        x = synth.images(image_nchw, 0, m)
+        y = synth.labels(B, classes, 0, m)
+        if rev_first:
+            h = image_nchw[1] // 2
+            return [x[:, :h].copy(), x[:, h:].copy()], y
+        return [x], y
+
+    reps, losses, _ = E.run_petra(ost, batch_fn, n_mb, lr=lr, drain=drain)
+    p_units = oracle_to_product_units(o_units)
+    hwc = (image_nchw[2], image_nchw[3], image_nchw[1] // 2 if rev_first else image_nchw[1])
+    specs = PM.stage_specs(p_units, counts, B, hwc, precision)
+    pipe = Pipeline(specs, seed=0)
+    for j, (th, bf) in enumerate(init, 1):
+        pipe.stages[j].set_params(th, np.zeros_like(th), bf)
+    loss = torch.zeros(1, device="cuda")
+    g_reps, g_losses = [], {}
+    for t in range(len(reps)):
+        inject = t < n_mb
+        x0 = lab = None
+        if inject:
+            xs, y = batch_fn(t)
+            x0 = dev(np.concatenate([nhwc(x).ravel() for x in xs]))
+            lab = dev(y, torch.int32)
+        loss.fill_(float("nan"))
+        r = pipe.tick(t, inject, x0, lab, lr, loss)
+        torch.cuda.synchronize()
+        g_reps.append(r)
+        if r["fwd_mb"][-1] >= 0:
+            g_losses[r["fwd_mb"][-1]] = loss.item()
+    return reps, losses, ost, groups, pipe, g_reps, g_losses
+
+
+def compare_pipeline(reps, losses, ost, groups, pipe, g_reps, g_losses, tol, v_tol=None):
+    for r, g in zip(reps, g_reps):   # integer report: bit-exact
+        assert g["fwd_mb"] == r.fwd_mb and g["bwd_mb"] == r.bwd_mb, (r, g)
+        assert g["version"] == r.version and g["fifo_depth"] == r.fifo_depth, (r, g)
+    assert sorted(g_losses) == sorted(losses)
+    errs = {f"loss{m}": abs(g_losses[m] - losses[m]) / abs(losses[m]) for m in losses}
+    for j, (s, g) in enumerate(zip(ost, groups), 1):
+        th, v, _ = pipe.stages[j].get_params()
+        want, _ = pack_params(g)
+        errs[f"theta{j}"] = rel(th, want)
+        errs[f"v{j}"] = rel(v, pack_like(g, s.v))
+    print("pipeline parity:", ", ".join(f"{k} {v:.2e}" for k, v in errs.items()))
+    bad = {k: e for k, e in errs.items() if e > (v_tol if (k.startswith("v") and v_tol) else tol)}
+    assert not bad, bad
+
+
+def test_pipeline_mlp_config1():
+    """Config 1 (reading c16): 2-stage reversible MLP, d=64, batch 32, 10 ticks, fp32."""
+    units = OM.build_mlp(64, 10)
+    out = run_pipeline_pair(units, [2, 3], 32, (32, 64, 1, 1), 10, 10, 0.025, drain=False, rev_first=True)
+    compare_pipeline(*out, tol=1e-4)
+
+
+@pytest.mark.parametrize("lr", [0.0, 0.01])
+def test_pipeline_revnet18_cifar_j4(lr):
+    """Config 2 architecture (RevNet-18, 32x32, J=4) at batch 4: 4 micro-batches
+    plus drain, free-running PETRA schedule, fp32.  Integer reports bit-exact,
+    losses and theta at 1e-4.  Momentum buffers integrate every gradient and a
+    free-running run may flip a ReLU mask whose pre-activation lies within the
+    ~1e-6 fp32 drift of the messages (reading c20), so they are held to 2e-2
+    here; test_free_running_stages_vs_oracle_on_gpu_messages checks each
+    backward strictly on the GPU's own messages."""
+    units = OM.build_revnet("revnet18", 32, 10)
+    out = run_pipeline_pair(units, [5, 4, 4, 5], 4, (4, 3, 32, 32), 10, 4, lr, drain=True)
+    compare_pipeline(*out, tol=1e-4, v_tol=2e-2)
+
+
+def stage_loop(specs, init, fn, n_mb, lr, J, B, on_backward=None):
+    """Free-running PETRA schedule over standalone GPU stages with Python
+    double-buffered mailboxes (the reference for the Pipeline's bookkeeping)."""
+    gst = [Stage(s, 0) for s in specs]
+    for s, (th, bf) in zip(gst, init):
+        s.set_params(th, np.zeros_like(th), bf)
+    gf, gb, losses = [None] * (J + 2), [None] * (J + 2), {}
+    for t in range(n_mb + 2 * J - 2):
+        nf, nb = [None] * (J + 2), [None] * (J + 2)
+        for j in range(1, J + 1):
+            g = gst[j - 1]
+            if j == 1:
+                fin = None
+                if t < n_mb:
+                    xs, y = fn(t)
+                    fin = (t, [dev(nhwc(xs[0])), None], dev(y, torch.int32))
+            else:
+                fin = gf[j]
+            shp = (B,) + tuple(specs[j - 1].in_shape)
+            if j < J:
+                if fin is not None:
+                    o = [torch.empty(g.out_shape, device="cuda") for _ in range(2)]
+                    g.forward(fin[0], fin[1][0], fin[1][1], o[0], o[1])
+                    nf[j + 1] = (fin[0], o, fin[2])
+                if gb[j] is not None:
+                    mb, msg = gb[j]
+                    res = [torch.empty(shp, device="cuda") for _ in range(4)] if j > 1 else [None] * 4
+                    if on_backward:
+                        on_backward(t, j, mb, msg, "before")
+                    g.backward(mb, *msg, *res, lr)
+                    if on_backward:
+                        on_backward(t, j, mb, g, "after")
+                    if j > 1:
+                        nb[j - 1] = (mb, res)
+            elif fin is not None:
+                res = [torch.empty(shp, device="cuda") for _ in range(4)]
+                loss = torch.zeros(1, device="cuda")
+                g.tail(fin[0], fin[1][0], fin[1][1], fin[2], lr, *res, loss)
+                nb[j - 1] = (fin[0], res)
+                losses[fin[0]] = loss
+        gf, gb = nf, nb
+    torch.cuda.synchronize()
+    return gst, {m: l.item() for m, l in losses.items()}
+
+
+def test_pipeline_bitwise_equals_stage_loop():
+    """The Pipeline object (C++ mailboxes, schedule) is bitwise identical to the
+    same stages driven by a Python double-buffered loop (deterministic kernels)."""
+    units = rand_params(OM.build_revnet("revnet18", 32, 10), 5)
+    counts, B, lr, n_mb, J = [5, 4, 4, 5], 4, 0.025, 5, 4
+    groups = OM.group(units, counts)
+    init = [pack_params(g) for g in groups]
+    specs = PM.stage_specs(oracle_to_product_units(units), counts, B, (32, 32, 3))
+    fn = lambda m: ([synth.images((B, 3, 32, 32), 0, m)], synth.labels(B, 10, 0, m))
+    gst, losses = stage_loop(specs, init, fn, n_mb, lr, J, B)
+    pipe = Pipeline(specs, seed=0)
+    for j, (th, bf) in enumerate(init, 1):
+        pipe.stages[j].set_params(th, np.zeros_like(th), bf)
+    loss = torch.zeros(1, device="cuda")
+    plosses = {}
+    for t in range(n_mb + 2 * J - 2):
+        x0 = lab = None
+        if t < n_mb:
+            xs, y = fn(t)
+            x0, lab = dev(nhwc(xs[0])), dev(y, torch.int32)
+        r = pipe.tick(t, t < n_mb, x0, lab, lr, loss)
+        if r["fwd_mb"][-1] >= 0:
+            plosses[r["fwd_mb"][-1]] = loss.item()
+    assert plosses == losses
+    for j in range(1, J + 1):
+        a, b = pipe.stages[j].get_params(), gst[j - 1].get_params()
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), j
+
+
+def test_free_running_stages_vs_oracle_on_gpu_messages():
+    """Every backward of a free-running GPU pipeline (RevNet-18, J=4, lr>0)
+    against a copy of the oracle stage in the same state fed the GPU's OWN
+    message (x~, delta): rel 1e-4 per tensor.  Together with the stage-level
+    tests this pins each tick; the oracle's own free-running trajectory may
+    differ by ReLU-mask flips (reading c20)."""
+    units = rand_params(OM.build_revnet("revnet18", 32, 10), 5)
+    counts, B, lr, n_mb, J = [5, 4, 4, 5], 4, 0.025, 4, 4
+    groups = OM.group(units, counts)
+    init = [pack_params(g) for g in groups]
+    ost = [E.Stage(g, E.OptConfig()) for g in groups]
+    for j, s in enumerate(ost, 1):
+        s.j, s.J = j, J
+    specs = PM.stage_specs(oracle_to_product_units(units), counts, B, (32, 32, 3))
+    fn = lambda m: ([synth.images((B, 3, 32, 32), 0, m)], synth.labels(B, 10, 0, m))
+    worst = {}
+
+    def H(t):
+        return nchw(t.detach().cpu().numpy().astype(np.float64))
+
+    # run the GPU loop; before each GPU backward the oracle copy of that stage runs
+    # its backward on the GPU message (the oracle copy is advanced in lockstep)
+    gst = [Stage(s, 0) for s in specs]
+    for s, (th, bf) in zip(gst, init):
+        s.set_params(th, np.zeros_like(th), bf)
+    gf, gb = [None] * (J + 2), [None] * (J + 2)
+    for t in range(n_mb + 2 * J - 2):
+        nf, nb = [None] * (J + 2), [None] * (J + 2)
+        for j in range(1, J + 1):
+            g, s = gst[j - 1], ost[j - 1]
+            s.lr = lr
+            if j == 1:
+                fin = None
+                if t < n_mb:
+                    xs, y = fn(t)
+                    fin = (t, [dev(nhwc(xs[0])), None], dev(y, torch.int32), xs, y)
+            else:
+                fin = gf[j]
+            shp = (B,) + tuple(specs[j - 1].in_shape)
+            if j < J:
+                if fin is not None:
+                    o = [torch.empty(g.out_shape, device="cuda") for _ in range(2)]
+                    g.forward(fin[0], fin[1][0], fin[1][1], o[0], o[1])
+                    oxs = fin[3] if j == 1 else [H(fin[1][0]), H(fin[1][1])]
+                    s.forward(E.Fwd(fin[0], oxs, fin[4]))          # oracle FIFO gets the GPU input
+                    nf[j + 1] = (fin[0], o, fin[2], None, fin[4])
+                if gb[j] is not None:
+                    mb, msg = gb[j]
+                    om = E.Bwd(mb, [H(msg[0]), H(msg[1])], [H(msg[2]), H(msg[3])])
+                    s.backward(om)   # oracle stage holds the GPU stage's theta / v (synced)
+                    res = [torch.empty(shp, device="cuda") for _ in range(4)] if j > 1 else [None] * 4
+                    g.backward(mb, *msg, *res, lr)
+                    torch.cuda.synchronize()
+                    errs = per_tensor_rel(groups[j - 1], g.get_grads(), pack_like(groups[j - 1], s.last_grads))
+                    worst[(t, j, mb)] = max(e for _, e in errs)
+                    # re-sync the oracle stage's theta/v to the GPU's (removes drift)
+                    _sync_oracle_stage(s, groups[j - 1], g)
+                    if j > 1:
+                        nb[j - 1] = (mb, res)
+            elif fin is not None:
+                res = [torch.empty(shp, device="cuda") for _ in range(4)]
+                loss = torch.zeros(1, device="cuda")
+                g.tail(fin[0], fin[1][0], fin[1][1], fin[2], lr, *res, loss)
+                torch.cuda.synchronize()
+                s.tail_step(E.Fwd(fin[0], [H(fin[1][0]), H(fin[1][1])], fin[4]))
+                errs = per_tensor_rel(groups[j - 1], g.get_grads(), pack_like(groups[j - 1], s.last_grads))
+                worst[(t, j, fin[0])] = max(e for _, e in errs)
+                _sync_oracle_stage(s, groups[j - 1], g)
+                nb[j - 1] = (fin[0], res)
+        gf, gb = nf, nb
+    # isolated ReLU-mask flips (a pre-activation within the fp32/fp64 forward
+    # difference of 0) are the expected outliers (reading c20): at most 10% of
+    # the backward events may exceed 1e-4, none may exceed 2e-2
+    assert len(worst) == 4 * n_mb
+    print("per-backward max rel:", {k: f"{v:.1e}" for k, v in sorted(worst.items())})
+    outliers = {k: v for k, v in worst.items() if v > 1e-4}
+    assert len(outliers) <= 0.1 * len(worst) and max(worst.values()) <= 2e-2, outliers
+
+
+def _sync_oracle_stage(s, units, g):
+    """Copy the GPU stage's theta / v into the oracle stage (layout inverse of pack)."""
+    th, v, _ = g.get_params()
+    off = 0
+    for (name, p, _), vv in zip(s.params(), s.v):
+        n = p.size
+        for src, dst in ((th, p), (v, vv)):
+            a = src[off:off + n].astype(np.float64)
+            if name == "w" and p.ndim == 4:
+                co, ci, k, _ = p.shape
+                a = a.reshape(co, k, k, ci).transpose(0, 3, 1, 2)
+            dst[...] = a.reshape(p.shape)
+        off += n
+
+
+@pytest.mark.parametrize("case", ["ds_basic_then_rev", "stem_cifar_then_rev", "rev_basic_c64_32x32"])
+def test_stage_fifo_depth3(case):
+    """Three forwards in flight before the backwards (FIFO depth 3, as at stage
+    J-1 of a J=2.5 pipeline), lr=0 so the oracle's theta is fixed: every
+    backward must match the oracle on the same (x~, delta)."""
+    make, B, in_shapes = STAGE_CASES[case]
+    units = make()
+    stem = isinstance(units[0], StemUnit)
+    in_hwc = tuple(np.array(in_shapes[0])[[2, 3, 1]])
+    st = make_pair(units, B, in_hwc, L.FP32)
+    ostage = E.Stage(units, E.OptConfig(), 1, 3)
+    ostage.lr = 0.0
+    rep, ok = [], True
+    outs = []
+    for m in range(3):
+        xs = [synth.images(s, 10 + m, i) for i, s in enumerate(in_shapes)]
+        fo = ostage.forward(E.Fwd(m, xs, None))
+        o = [torch.empty(st.out_shape, device="cuda") for _ in range(2)]
+        gx = [dev(nhwc(x)) for x in xs]
+        st.forward(m, gx[0], gx[1] if not stem else None, o[0], o[1])
+        outs.append((fo, o))
+    for m in range(3):
+        fo, o = outs[m]
+        dd = [synth.normal(fo.xs[h].shape, 20 + m, h) for h in range(2)]
+        bo = ostage.backward(E.Bwd(m, fo.xs, dd))
+        res = [torch.empty((B,) + tuple(in_hwc), device="cuda") for _ in range(4)]
+        gxt = [dev(nhwc(x)) for x in fo.xs]
+        gd = [dev(nhwc(d)) for d in dd]
+        st.backward(m, gxt[0], gxt[1], gd[0], gd[1], *(res if not stem else [None] * 4), 0.0)
+        torch.cuda.synchronize()
+        if not stem:
+            for h in range(2):
+                ok &= check(f"mb{m}.xt{h}", nchw(host(res[h])), bo.xs[h], 1e-4, rep)
+                ok &= check(f"mb{m}.d{h}", nchw(host(res[2 + h])), bo.ds[h], 1e-4, rep)
+        for name, r in per_tensor_rel(units, st.get_grads(), pack_like(units, ostage.last_grads)):
+            rep.append((f"mb{m}.grad.{name}", r))
+            ok &= r <= 1e-4
+    assert ok, "\n".join(f"{n}: {r:.3e}" for n, r in rep)
+
+
+@pytest.mark.parametrize("case", sorted(TAIL_CASES))
+def test_tail_stage_consecutive(case):
+    """Three consecutive final-stage steps (state carried between calls)."""
+    make, B, in_shapes = TAIL_CASES[case]
+    units = make()
+    in_hwc = tuple(np.array(in_shapes[0])[[2, 3, 1]])
+    st = make_pair(units, B, in_hwc, L.FP32)
+    ostage = E.Stage(units, E.OptConfig(), 2, 2)
+    ostage.lr = 0.05
+    rep, ok = [], True
+    for m in range(3):
+        xs = [synth.images(s, 30 + m, i) for i, s in enumerate(in_shapes)]
+        lab = synth.labels(B, units[-1].classes, 0, m)
+        loss_o, bo = ostage.tail_step(E.Fwd(m, xs, lab))
+        gx = [dev(nhwc(x)) for x in xs]
+        outs = [torch.empty_like(gx[0]) for _ in range(4)]
+        loss = torch.zeros(1, device="cuda")
+        st.tail(m, gx[0], gx[1], dev(lab, torch.int32), 0.05, *outs, loss)
+        torch.cuda.synchronize()
+        rep.append((f"mb{m}.loss", abs(loss.item() - loss_o) / abs(loss_o)))
+        for h in range(2):
+            ok &= check(f"mb{m}.d{h}", nchw(host(outs[2 + h])), bo.ds[h], 1e-4, rep)
+        for name, r in per_tensor_rel(units, st.get_grads(), pack_like(units, ostage.last_grads)):
+            rep.append((f"mb{m}.grad." + name, r))
+            ok &= r <= 1e-4
+    assert ok, "\n".join(f"{n}: {r:.3e}" for n, r in rep)
