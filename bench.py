@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""PETRA (arXiv 2406.02052) on B200: one JSON line per run (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--model revnet18|revnet34|revnet50] [--batch B] [--stages J]
+                    [--precision bf16|fp32] [--no-cpu-baseline]
+
+A step is one steady-state PETRA tick of the whole pipeline: every stage runs
+one forward (theta^t) and one backward (approximate inversion + VJP +
+immediate Nesterov update) on different micro-batches, so
+one micro-batch of B samples completes per tick.  value = B * K / (max over
+ranks of the summed device time of the K ticks).  Default workload: BASELINE
+configs[1], RevNet-18 on CIFAR-10-shaped synthetic data, batch 64, J = 4.
+--impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the
+same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RevNet-18/50 train samples/s at 1/2/4/8 B200 stages; tensor-pipe % of peak"
+IMAGE = {"revnet18": (32, 10), "revnet34": (32, 1000), "revnet50": (224, 1000)}
+WD = {"revnet18": 5e-4, "revnet34": 1e-4, "revnet50": 1e-4}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+def workload_name(a):
+    H, classes = IMAGE[a.model]
+    ds = {"revnet18": "CIFAR-10", "revnet34": "ImageNet32", "revnet50": "ImageNet"}[a.model]
+    return (f"{a.model.replace('revnet', 'RevNet-')} PETRA, {ds} shape 3x{H}x{H} ({classes} classes), "
+            f"batch {a.batch}, J={a.stages} stages")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 9]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def oracle_tick_seconds(model, batch, J, counts, seed=0):
+    """Time the fp64 oracle on the work of one steady-state tick: every stage
+    runs one forward and one backward (the tail stage its fused step) at
+    `batch`.  Returns (seconds, threads)."""
+    import numpy as np
+    import synth
+    from oracle import engine as E, models as OM
+    H, classes = IMAGE[model]
+    units = OM.init_params(OM.build_revnet(model, H, classes), 1)
+    groups = OM.group(units, counts)
+    stages = [E.Stage(g, E.OptConfig(weight_decay=WD[model])) for g in groups]
+    x = [synth.images((batch, 3, H, H), seed, 0)]
+    y = synth.labels(batch, classes, seed, 0)
+    # stage inputs: one untimed forward pass through the stages
+    msgs = [E.Fwd(0, x, y)]
+    for s in stages[:-1]:
+        s.j, s.J = 1, J
+        msgs.append(s.forward(msgs[-1]))
+    # timed: forward + backward of every stage on the stage-local message
+    outs = []
+    t0 = time.perf_counter()
+    for j, s in enumerate(stages):
+        s.lr = 0.025
+        if j < J - 1:
+            m = s.forward(E.Fwd(1, msgs[j].xs, y))
+            s.backward(E.Bwd(0, m.xs, [np.ones_like(a) for a in m.xs]))
+        else:
+            s.tail_step(E.Fwd(1, msgs[j].xs, y))
+    dt = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count()
+    return dt, threads
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_02052_b200 import Pipeline, _lib as L, models as PM
+    from paper_2406_02052_b200.dist import Transport, contiguous_stage_ranks
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    H, classes = IMAGE[a.model]
+    units = PM.revnet(a.model, H, classes)
+    counts = PM.partition(units, a.stages, a.batch, H, H, 3)
+    prec = L.BF16_TC if a.precision == "bf16" else L.FP32
+    specs = PM.stage_specs(units, counts, a.batch, (H, H, 3), prec, WD[a.model])
+    stage_rank = contiguous_stage_ranks(a.stages, world)
+    pipe = Pipeline(specs, stage_rank, rank, world, seed=1)
+    tr = Transport(pipe) if world > 1 else None
+    J, B = a.stages, a.batch
+    dev = torch.device("cuda", local)
+    gen = torch.Generator(device=dev).manual_seed(0)
+    ring = 16
+    owns_first = stage_rank[0] == rank
+    xs = [torch.randn((B, H, H, 3), generator=gen, device=dev) for _ in range(ring)]
+    ys = [torch.randint(0, classes, (B,), generator=gen, device=dev, dtype=torch.int32) for _ in range(ring)]
+    loss = torch.zeros(1, device=dev)
+    lr = 0.1 * 64 / 256  # PAPER.md:256 with k = 1
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    st = torch.cuda.current_stream()
+    t = 0
+
+    def tick(flush_l2=False, ev=None):
+        nonlocal t
+        i = t % ring
+        if flush_l2:
+            flush.fill_(t & 0xFF)
+        if ev:
+            ev[0].record(st)
+        pipe.tick(t, True, xs[i] if owns_first else None, ys[i] if owns_first else None, lr, loss, report=False)
+        if ev:
+            ev[1].record(st)
+        if tr:
+            tr.exchange(t)
+        t += 1
+
+    # fill the pipeline (2J-2 ticks) + warm-up
+    for _ in range(2 * J - 2 + a.warmup):
+        tick()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    n0 = L.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    wall0 = time.perf_counter()
+    for k in range(a.steps):
+        tick(flush_l2=True, ev=evs[k])
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = L.launch_count() - n0
+    clk = clocks.stop()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    tms = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+    ms = float(tms.item())
+    value = B * a.steps / (ms / 1e3)
+
+    # ---- e2e through the public API: pinned host inputs copied in, loss read back, every step
+    hx = [x.cpu().pin_memory() for x in xs[:4]]
+    hy = [y.cpu().pin_memory() for y in ys[:4]]
+    hl = torch.zeros(1).pin_memory()
+    dx = torch.empty_like(xs[0])
+    dy = torch.empty_like(ys[0])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(st)
+    for k in range(a.steps):
+        i = t % 4
+        if owns_first:
+            dx.copy_(hx[i], non_blocking=True)
+            dy.copy_(hy[i], non_blocking=True)
+        pipe.tick(t, True, dx if owns_first else None, dy if owns_first else None, lr, loss, report=False)
+        hl.copy_(loss, non_blocking=True)
+        if tr:
+            tr.exchange(t)
+        t += 1
+    e1.record(st)
+    torch.cuda.synchronize()
+    ems = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    if world > 1:
+        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+    e2e = {"value": B * a.steps / (float(ems.item()) / 1e3), "unit": "samples/s",
+           "h2d_bytes_per_step": (B * H * H * 3 * 4 + B * 4) if owns_first else 0, "d2h_bytes_per_step": 4}
+
+    # ---- per-kernel device time (profiled replay of K more steps: CUDA events on the launch stream)
+    L.profile(True)
+    for _ in range(a.steps):
+        tick()
+    prof = L.profile_read()
+    L.profile(False)
+    peaks, src = load_peaks()
+    tot = sum(p["ms"] for p in prof)
+    prof.sort(key=lambda p: -p["ms"])
+    top = prof[0]
+    name = top["name"]
+    if name.startswith("conv") and name.endswith("_tc"):
+        bound, peak, unit, ach = "tensor", peaks["bf16_tflops_sustained"], "TFLOP/s", top["flops"] / top["ms"] / 1e9
+        peak_src = f"bf16_tflops_sustained ({src})"
+    elif name.startswith("conv"):
+        fp32_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        bound, peak, unit, ach = "alu", fp32_peak, "TFLOP/s", top["flops"] / top["ms"] / 1e9
+        peak_src = "148 SM x 128 FP32 lanes x 2 FLOP x sm_max_mhz (DESIGN.md)"
+    else:
+        bound, peak, unit, ach = "hbm", peaks["hbm_gbs"], "GB/s", top["bytes"] / top["ms"] / 1e6
+        peak_src = f"hbm_gbs ({src})"
+    roof = {"bound": bound, "kernel": name, "achieved": round(ach, 2), "peak": peak, "unit": unit,
+            "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_src,
+            "share_of_step": round(top["ms"] / tot, 3), "launches_per_step": top["launches"] / a.steps}
+    kernels = [{"name": p["name"], "share": round(p["ms"] / tot, 3), "launches": p["launches"],
+                "ms_per_step": round(p["ms"] / a.steps, 4),
+                "tflops": round(p["flops"] / p["ms"] / 1e9, 2) if p["flops"] else None,
+                "gbs": round(p["bytes"] / p["ms"] / 1e6, 1) if p["bytes"] else None} for p in prof]
+    conv_flops = sum(p["flops"] for p in prof) / a.steps
+
+    out = {"metric": METRIC, "value": round(value, 2), "unit": "samples/s", "n_gpus": world, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": round(ms / a.steps, 4), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None,
+           "dtype": "bf16" if prec == L.BF16_TC and any(k["name"].endswith("_tc") for k in kernels) else "f32",
+           "data": "synthetic (N(0,1) images, uniform labels; seeded device ring of 16 micro-batches)",
+           "config": {"workload": workload_name(a), "model": a.model, "global_batch": B, "micro_batch": B,
+                      "image": [3, H, H], "classes": classes, "stages": J, "partition_units": counts,
+                      "stage_rank": stage_rank, "parallelism": f"petra-stages{J}-over-{world}gpu",
+                      "precision_requested": a.precision, "lr": lr, "fill_ticks": 2 * J - 2,
+                      "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                      "wall_s_timed": round(wall, 3)},
+           "roofline": roof, "gpu_launches": launches, "clocks": clk, "e2e": e2e,
+           "kernels": kernels[:12], "algorithmic_gflop_per_step": round(conv_flops / 1e9, 2)}
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        dt, threads = oracle_tick_seconds(a.model, B if a.model != "revnet50" else 4, J, counts)
+        bb = B if a.model != "revnet50" else 4
+        out["cpu_baseline"] = {"value": round(bb / dt, 3), "unit": "samples/s", "cores": threads, "kind": "oracle",
+                               "sample": f"one steady-state tick's work (each of the {J} stages: one forward + "
+                                         f"one backward / tail step) at batch {bb}, fp64 numpy, {dt:.1f} s"}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2406_02052_b200 import models as PM
+    H, classes = IMAGE[a.model]
+    counts = PM.partition(PM.revnet(a.model, H, classes), a.stages, a.batch, H, H, 3)
+    bb = 4 if a.model == "revnet50" else 8
+    for _ in range(min(a.warmup, 1)):
+        oracle_tick_seconds(a.model, bb, a.stages, counts, seed=1)
+    tot, threads = 0.0, 1
+    for k in range(a.steps):
+        dt, threads = oracle_tick_seconds(a.model, bb, a.stages, counts, seed=k)
+        tot += dt
+    value = bb * a.steps / tot
+    sample = (f"per step: one steady-state tick's work (each of the {a.stages} stages one forward + one backward "
+              f"/ tail step) at batch {bb} (bounded sample of batch {a.batch}), fp64 numpy oracle")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "samples/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(tot / a.steps * 1e3, 2),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": workload_name(a), "model": a.model, "global_batch": a.batch,
+                                        "partition_units": counts},
+        "cpu_baseline": {"value": round(value, 4), "unit": "samples/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="revnet18", choices=list(IMAGE))
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--stages", type=int, default=4)
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -268,6 +268,25 @@ petra_status petra_schedule_tick(petra_schedule *s, int64_t t, int32_t inject, p
                                  petra_sched_msgs *msgs);
 petra_status petra_schedule_destroy(petra_schedule *s);
 
+/* ------------------------------------------------------------------ instrumentation
+ * petra_launch_count: cumulative number of CUDA kernels the library launched.
+ * petra_profile(1) starts recording CUDA events (on the launching stream)
+ * around every logical kernel, grouped by category; petra_profile(0) stops.
+ * petra_profile_read synchronises the device and returns one entry per
+ * category: launches, summed event time, and the ALGORITHMIC flops / bytes of
+ * those launches (2*M*N*K per convolution; read+write bytes of the streaming
+ * kernels) -- the numerators of the roofline fractions. */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double ms;
+  double flops;
+  double bytes;
+} petra_prof_entry;
+int64_t petra_launch_count(void);
+petra_status petra_profile(int32_t enable);
+petra_status petra_profile_read(petra_prof_entry *out, int32_t cap, int32_t *n);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -77,6 +77,11 @@ class PetraSchedMsgs(C.Structure):
     _fields_ = [("n", C.c_int32), ("m", PetraSchedMsg * 8)]
 
 
+class PetraProfEntry(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double), ("flops", C.c_double),
+                ("bytes", C.c_double)]
+
+
 P, VP, I32, I64, U64, F32 = C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_float
 SIGS = {
     "petra_status_str": (C.c_char_p, [C.c_int]),
@@ -102,7 +107,26 @@ SIGS = {
     "petra_schedule_create": (C.c_int, [I32, C.POINTER(I32), C.POINTER(I32), I32, C.POINTER(P)]),
     "petra_schedule_tick": (C.c_int, [P, I64, I32, C.POINTER(PetraTickReport), C.POINTER(PetraSchedMsgs)]),
     "petra_schedule_destroy": (C.c_int, [P]),
+    "petra_launch_count": (C.c_int64, []),
+    "petra_profile": (C.c_int, [I32]),
+    "petra_profile_read": (C.c_int, [C.POINTER(PetraProfEntry), I32, C.POINTER(I32)]),
 }
+
+
+def launch_count() -> int:
+    return int(lib().petra_launch_count())
+
+
+def profile(enable: bool):
+    call("petra_profile", int(bool(enable)))
+
+
+def profile_read():
+    arr = (PetraProfEntry * 64)()
+    n = C.c_int32()
+    call("petra_profile_read", arr, 64, C.byref(n))
+    return [dict(name=arr[i].name.decode(), launches=arr[i].launches, ms=arr[i].ms, flops=arr[i].flops,
+                 bytes=arr[i].bytes) for i in range(n.value)]
 
 
 class PetraError(RuntimeError):

@@ -6,6 +6,8 @@
 #include <stdexcept>
 #include <string>
 
+#include "prof.h"
+
 namespace petra {
 
 struct CudaError : std::runtime_error {
@@ -20,7 +22,11 @@ struct CudaError : std::runtime_error {
                                __FILE__ + ":" + std::to_string(__LINE__));                 \
   } while (0)
 
-#define PETRA_LAUNCH_CHECK() PETRA_CUDA(cudaGetLastError())
+#define PETRA_LAUNCH_CHECK()       \
+  do {                             \
+    ::petra::count_launch();       \
+    PETRA_CUDA(cudaGetLastError()); \
+  } while (0)
 
 constexpr int kNumSMs = 148;  // B200
 

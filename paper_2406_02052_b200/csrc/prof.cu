@@ -1,0 +1,72 @@
+// prof.cu -- launch counter and event-based per-category timing (product code).
+#include <cstring>
+
+#include "../../include/petra.h"
+#include "errors.h"
+#include "prof.h"
+
+namespace petra {
+std::atomic<int64_t> Prof::launches{0};
+bool Prof::enabled = false;
+std::vector<Prof::Rec> Prof::recs;
+std::vector<std::string> Prof::names;
+std::vector<cudaEvent_t> Prof::pool;
+static size_t g_pool_next = 0;
+
+int Prof::category(const char *name) {
+  for (size_t i = 0; i < names.size(); ++i)
+    if (names[i] == name) return (int)i;
+  names.push_back(name);
+  return (int)names.size() - 1;
+}
+
+cudaEvent_t Prof::ev() {
+  if (g_pool_next == pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    pool.push_back(e);
+  }
+  return pool[g_pool_next++];
+}
+}  // namespace petra
+
+using petra::Prof;
+
+extern "C" {
+
+int64_t petra_launch_count(void) { return Prof::launches.load(); }
+
+petra_status petra_profile(int32_t enable) {
+  if (enable) {
+    cudaDeviceSynchronize();
+    Prof::recs.clear();
+    petra::g_pool_next = 0;
+  }
+  Prof::enabled = enable != 0;
+  return PETRA_OK;
+}
+
+petra_status petra_profile_read(petra_prof_entry *out, int32_t cap, int32_t *n) {
+  if (!out || !n) return PETRA_E_ARG;
+  if (cudaDeviceSynchronize() != cudaSuccess) return PETRA_E_CUDA;
+  int nc = (int)Prof::names.size();
+  std::vector<petra_prof_entry> agg(nc);
+  for (int i = 0; i < nc; ++i) {
+    std::memset(&agg[i], 0, sizeof(petra_prof_entry));
+    std::strncpy(agg[i].name, Prof::names[i].c_str(), sizeof(agg[i].name) - 1);
+  }
+  for (auto &r : Prof::recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    agg[r.cat].launches += 1;
+    agg[r.cat].ms += ms;
+    agg[r.cat].flops += r.flops;
+    agg[r.cat].bytes += r.bytes;
+  }
+  int k = 0;
+  for (int i = 0; i < nc && k < cap; ++i)
+    if (agg[i].launches) out[k++] = agg[i];
+  *n = k;
+  return PETRA_OK;
+}
+}

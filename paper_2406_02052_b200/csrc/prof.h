@@ -1,0 +1,51 @@
+// prof.h -- launch counting and optional per-category CUDA-event timing (product code).
+// The bench reads these through petra_profile_* to report the dominant
+// kernel's achieved FLOP/s or GB/s, measured with events on the launch stream.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace petra {
+
+struct Prof {
+  static std::atomic<int64_t> launches;  // every kernel launch of the library
+  static bool enabled;
+  struct Rec {
+    int cat;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  static std::vector<Rec> recs;
+  static std::vector<std::string> names;
+  static std::vector<cudaEvent_t> pool;
+  static int category(const char *name);
+  static cudaEvent_t ev();
+};
+
+// RAII scope around one logical kernel (may contain several launches)
+struct ProfScope {
+  int cat = -1;
+  cudaStream_t st;
+  cudaEvent_t a{}, b{};
+  double flops, bytes;
+  ProfScope(const char *name, cudaStream_t s, double fl, double by) : st(s), flops(fl), bytes(by) {
+    if (!Prof::enabled) return;
+    cat = Prof::category(name);
+    a = Prof::ev();
+    b = Prof::ev();
+    cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (cat < 0) return;
+    cudaEventRecord(b, st);
+    Prof::recs.push_back({cat, a, b, flops, bytes});
+  }
+};
+
+inline void count_launch(int n = 1) { Prof::launches.fetch_add(n, std::memory_order_relaxed); }
+
+}  // namespace petra

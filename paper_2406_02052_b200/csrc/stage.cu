@@ -367,15 +367,30 @@ int Stage::fifo_depth() const {
 }
 
 void Stage::update(float lr, cudaStream_t st) {
+  ProfScope ps("sgd_update", st, 0.0, 20.0 * (double)n_params_);
   sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
              grad_->as<float>(), lr, desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false);
   ++version_;
 }
 
 // ------------------------------------------------------------------ layer kernels
+static void apply_bn(int64_t M, int C, const float *z, int ldz, int zc0, const float *mean, const float *invstd,
+                     const float *gamma, const float *beta, int relu, float sign, const float *acc, float *out,
+                     __nv_bfloat16 *out_bf16, cudaStream_t st) {
+  ProfScope ps("bn_apply", st, 0.0, 4.0 * (double)M * C * (acc ? 3 : 2));
+  bn_apply<float, float>(M, C, z, ldz, zc0, mean, invstd, gamma, beta, relu, sign, acc, out, out_bf16, st);
+}
+
+static double conv_flops(const ConvGeom &g) { return 2.0 * (double)g.M() * g.Co * g.K(); }
+static double conv_bytes(const ConvGeom &g, int esz) {
+  return (double)esz * ((double)g.Min() * g.Ci + (double)g.Co * g.K()) + 4.0 * (double)g.M() * g.Co;
+}
+
 void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st) {
   const float *w = theta_->as<float>() + L.w_off;
-  if (tc_ && conv_tc_supported(L.g, 0)) {
+  bool tc = tc_ && conv_tc_supported(L.g, 0);
+  ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
+  if (tc) {
     f32_to_bf16(x, L.xb->as<__nv_bfloat16>(), L.g.Min() * L.g.Ci, st);
     conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->as<float>(), nullptr, st);
   } else {
@@ -385,7 +400,9 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st) {
 
 void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   float *dw = grad_->as<float>() + L.w_off;
-  if (tc_ && conv_tc_supported(L.g, 2)) {
+  bool tc = tc_ && conv_tc_supported(L.g, 2);
+  ProfScope ps(tc ? "conv_wgrad_tc" : "conv_wgrad_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
+  if (tc) {
     // L.xb holds bf16(x) from the conv_fwd of this tick (forward or recomputation)
     f32_to_bf16(L.dz->as<float>(), L.dzb->as<__nv_bfloat16>(), L.g.M() * L.g.Co, st);
     conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.xb->as<__nv_bfloat16>(), dw, wgrad_ws_->as<float>(), st);
@@ -395,7 +412,9 @@ void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
 }
 
 void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t st) {
-  if (tc_ && conv_tc_supported(L.g, 1)) {
+  bool tc = tc_ && conv_tc_supported(L.g, 1);
+  ProfScope ps(tc ? "conv_dgrad_tc" : "conv_dgrad_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
+  if (tc) {
     if (!conv_tc_supported(L.g, 2))  // dz bf16 not produced by wgrad path
       f32_to_bf16(L.dz->as<float>(), L.dzb->as<__nv_bfloat16>(), L.g.M() * L.g.Co, st);
     conv_dgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.wt_bf16->as<__nv_bfloat16>(), addend, out, st);
@@ -405,6 +424,7 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
 }
 
 void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
+  ProfScope ps("bn_stats", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co);
   float *b = bufs_->as<float>();
   bn_stats<float>(L.z->as<float>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean->as<float>(), L.invstd->as<float>(),
                   running ? b + L.rm_off : nullptr, running ? b + L.rv_off : nullptr, desc_.bn_momentum,
@@ -420,7 +440,7 @@ void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running
     conv_fwd(L, x, st);
     layer_stats(L, running, st);
     if (l + 1 < phi.size()) {
-      bn_apply<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+      apply_bn(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
                              L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr, L.a->as<float>(),
                              nullptr, st);
       x = L.a->as<float>();
@@ -435,9 +455,14 @@ void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, cons
                       cudaStream_t st) {
   const float *th = theta_->as<float>();
   float *gr = grad_->as<float>();
+  double n = (double)L.g.M() * L.g.Co;
+  {
+  ProfScope ps("bn_bwd_reduce", st, 0.0, 4.0 * n * (dst_out ? 4 : 2));
   bn_bwd_reduce<float>(L.z->as<float>(), L.g.M(), L.g.Co, L.mean->as<float>(), L.invstd->as<float>(),
                        th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, dst_in, dst_out, nullptr,
                        gr + L.g_off, gr + L.b_off, part_->as<double>(), st);
+  }
+  ProfScope ps("bn_bwd_dz", st, 0.0, 12.0 * n);
   bn_bwd_dz<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.mean->as<float>(), L.invstd->as<float>(),
                           th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off,
                           L.dz->as<float>(), st);
@@ -472,7 +497,7 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       // x[dst] += Phi(x[src])  (north_star y1 = x1 + F(x2), y2 = x2 + G(y1))
       branch_forward(u.phi, cur[u.src()], keep, st);
       Layer &L = u.phi.back();
-      bn_apply<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+      apply_bn(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
                              L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, cur[u.dst()], out[u.dst()],
                              nullptr, st);
       break;
@@ -488,11 +513,11 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       Layer &L = u.phi.back();
       int64_t M = L.g.M();
       int C = L.g.Co;
-      bn_apply<float, float>(M, C, u.pa.z->as<float>(), C, 0, u.pa.mean->as<float>(), u.pa.invstd->as<float>(),
+      apply_bn(M, C, u.pa.z->as<float>(), C, 0, u.pa.mean->as<float>(), u.pa.invstd->as<float>(),
                              th + u.pa.g_off, th + u.pa.b_off, 0, 1.f, nullptr, out[u.dst()], nullptr, st);
-      bn_apply<float, float>(M, C, L.z->as<float>(), C, 0, L.mean->as<float>(), L.invstd->as<float>(),
+      apply_bn(M, C, L.z->as<float>(), C, 0, L.mean->as<float>(), L.invstd->as<float>(),
                              th + L.g_off, th + L.b_off, 1, 1.f, out[u.dst()], out[u.dst()], nullptr, st);
-      bn_apply<float, float>(M, C, u.pb.z->as<float>(), C, 0, u.pb.mean->as<float>(), u.pb.invstd->as<float>(),
+      apply_bn(M, C, u.pb.z->as<float>(), C, 0, u.pb.mean->as<float>(), u.pb.invstd->as<float>(),
                              th + u.pb.g_off, th + u.pb.b_off, 0, 1.f, nullptr, out[u.src()], nullptr, st);
       break;
     }
@@ -502,14 +527,15 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       layer_stats(L, keep, st);
       int Ch = L.g.Co / 2;
       if (u.d.maxpool) {
-        bn_apply<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+        apply_bn(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
                                L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
                                u.pool_a->as<float>(), nullptr, st);
+        ProfScope ps("maxpool", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co * 1.25);
         maxpool_fwd(u.pool_a->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, out[0], out[1],
                     u.pool_arg->as<uint8_t>(), st);
       } else {
         for (int h = 0; h < 2; ++h)
-          bn_apply<float, float>(L.g.M(), Ch, L.z->as<float>(), L.g.Co, h * Ch, L.mean->as<float>(),
+          apply_bn(L.g.M(), Ch, L.z->as<float>(), L.g.Co, h * Ch, L.mean->as<float>(),
                                  L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr, out[h],
                                  nullptr, st);
       }
@@ -565,7 +591,7 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
         layer_stats(L, true, st);
         if (u.d.maxpool) {
           // recompute the pre-pool activation and argmax (outputs go to scratch)
-          bn_apply<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+          apply_bn(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
                                  L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
                                  u.pool_a->as<float>(), nullptr, st);
           maxpool_fwd(u.pool_a->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, L.dz->as<float>(),
@@ -589,7 +615,10 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
 
 // ------------------------------------------------------------------ ticks
 static void copy_d2d(float *dst, const float *src, int64_t n, cudaStream_t st) {
-  if (dst && src && dst != src) PETRA_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  if (dst && src && dst != src) {
+    ProfScope ps("copy", st, 0.0, 8.0 * (double)n);
+    PETRA_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
 }
 
 static void fifo_push(Fifo &f, uint64_t mb, const float *a, const float *b, int64_t n, cudaStream_t st) {
@@ -732,10 +761,13 @@ void Stage::tail(uint64_t mb, const float *x1, const float *x2, const int32_t *l
   Unit &t = units_.back();
   const float *th = theta_->as<float>();
   float *gr = grad_->as<float>();
-  tail_forward_backward(cur[0], cur[1], desc_.batch, t.in.H * t.in.W, t.in.C, th + t.fc_w, th + t.fc_b,
-                        t.d.classes, labels, feat_->as<float>(), logits_->as<float>(), dlogits_->as<float>(),
-                        lossrow_->as<float>(), dfeat_->as<float>(), gr + t.fc_w, gr + t.fc_b,
-                        tail_d_[0]->as<float>(), tail_d_[1]->as<float>(), loss, nonfinite_->as<int>(), st);
+  {
+    ProfScope pst("tail_loss", st, 6.0 * desc_.batch * 2.0 * t.in.C * t.d.classes, 12.0 * (double)t.in.numel());
+    tail_forward_backward(cur[0], cur[1], desc_.batch, t.in.H * t.in.W, t.in.C, th + t.fc_w, th + t.fc_b,
+                          t.d.classes, labels, feat_->as<float>(), logits_->as<float>(), dlogits_->as<float>(),
+                          lossrow_->as<float>(), dfeat_->as<float>(), gr + t.fc_w, gr + t.fc_b,
+                          tail_d_[0]->as<float>(), tail_d_[1]->as<float>(), loss, nonfinite_->as<int>(), st);
+  }
   // plain backprop through the stored graph (no conv recomputation)
   const float *cx[2] = {cur[0], cur[1]}, *cd[2] = {tail_d_[0]->as<float>(), tail_d_[1]->as<float>()};
   for (int i = n - 2; i >= 0; --i) {
