@@ -283,6 +283,21 @@ typedef struct {
   double flops;
   double bytes;
 } petra_prof_entry;
+/* Kernel-level test hook: run ONE convolution pass on host buffers (device
+ * buffers are allocated, used and freed inside; synchronous).
+ *   mode 0 forward : out[B*Ho*Wo][Co]  = conv(a = x[B][H][W][Ci], b = w[Co][k][k][Ci])
+ *   mode 1 dgrad   : out[B*H*W][Ci]    = addend + conv^T(a = dz[B][Ho][Wo][Co], b = w)
+ *   mode 2 wgrad   : out[Co][k][k][Ci] = sum over pixels of dz (a) (x) x (b = x)
+ * engine 0 = SIMT fp32 kernels, 1 = tcgen05 bf16 kernels (inputs rounded to bf16;
+ * PETRA_E_UNSUPPORTED if the geometry has no tensor-core path).  addend may be NULL. */
+typedef struct {
+  int32_t batch, h, w, cin, cout, ksize, stride;
+} petra_conv_geom;
+petra_status petra_conv_run(int32_t mode, int32_t engine, const petra_conv_geom *g, const float *a,
+                            const float *b, const float *addend, float *out);
+/* Which engine the library uses for a convolution pass at a given precision:
+ * 0 = SIMT fp32, 1 = tcgen05 bf16 (operands rounded to bf16, fp32 accumulation). */
+int32_t petra_conv_engine(const petra_conv_geom *g, int32_t mode, int32_t precision);
 int64_t petra_launch_count(void);
 petra_status petra_profile(int32_t enable);
 petra_status petra_profile_read(petra_prof_entry *out, int32_t cap, int32_t *n);

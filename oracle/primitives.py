@@ -19,6 +19,20 @@ import numpy as np
 BN_EPS = 1e-5        # reading c9 (paper silent; PyTorch default)
 BN_MOMENTUM = 0.1    # reading c9
 
+# Operand-precision emulation (reading c22).  The paper fixes no
+# precision; the oracle is exact fp64 by default.  A test that compares a kernel
+# computing a convolution on rounded operands (bf16 tensor cores) may install
+# rounding functions here so that the ReLU masks -- integer decisions taken from
+# floating point -- are decided on the same rounded operands on both sides.
+# Each entry: None (exact) or f(array, pass_name, geometry) -> rounded array,
+# geometry = (B, H, W, Ci, Co, k, stride).  Products/sums stay fp64.
+OPERAND_ROUND = {"fwd": None, "dgrad": None, "wgrad": None}
+
+
+def _rnd(kind, a, geom):
+    f = OPERAND_ROUND[kind]
+    return a if f is None else f(a, kind, geom)
+
 
 # --------------------------------------------------------------------------- conv
 def conv_out_size(n: int, k: int, stride: int, pad: int) -> int:
@@ -46,6 +60,8 @@ def conv2d(x, w, stride=1, pad=0):
     if C != C2 or k != k2:
         raise ValueError(f"conv2d shape mismatch x{x.shape} w{w.shape}")
     Ho, Wo = conv_out_size(H, k, stride, pad), conv_out_size(W, k, stride, pad)
+    geom = (B, H, W, C, O, k, stride)
+    x, w = _rnd("fwd", x, geom), _rnd("fwd", w, geom)
     xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
     out = np.zeros((B, O, Ho, Wo))
     for kh, kw, view in _taps(xp, k, stride, Ho, Wo):
@@ -63,13 +79,16 @@ def conv2d_vjp(x, w, stride, pad, dout, need_dx=True):
     B, C, H, W = x.shape
     O, _, k, _ = w.shape
     Ho, Wo = dout.shape[2], dout.shape[3]
-    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
+    geom = (B, H, W, C, O, k, stride)
+    xw, dw_out = _rnd("wgrad", x, geom), _rnd("wgrad", dout, geom)
+    dd_out, wd = _rnd("dgrad", dout, geom), _rnd("dgrad", w, geom)
+    xp = np.pad(xw, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
     dxp = np.zeros_like(xp) if need_dx else None
     dw = np.zeros_like(w)
     for kh, kw, view in _taps(xp, k, stride, Ho, Wo):
-        dw[:, :, kh, kw] = np.tensordot(dout, view, axes=([0, 2, 3], [0, 2, 3]))
+        dw[:, :, kh, kw] = np.tensordot(dw_out, view, axes=([0, 2, 3], [0, 2, 3]))
         if need_dx:
-            contrib = np.tensordot(dout, w[:, :, kh, kw], axes=([1], [0]))  # [B,Ho,Wo,C]
+            contrib = np.tensordot(dd_out, wd[:, :, kh, kw], axes=([1], [0]))  # [B,Ho,Wo,C]
             dxp[:, :, kh:kh + stride * (Ho - 1) + 1:stride,
                 kw:kw + stride * (Wo - 1) + 1:stride] += contrib.transpose(0, 3, 1, 2)
     dx = dxp[:, :, pad:pad + H, pad:pad + W].copy() if need_dx else None

@@ -77,6 +77,11 @@ class PetraSchedMsgs(C.Structure):
     _fields_ = [("n", C.c_int32), ("m", PetraSchedMsg * 8)]
 
 
+class PetraConvGeom(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("h", C.c_int32), ("w", C.c_int32), ("cin", C.c_int32),
+                ("cout", C.c_int32), ("ksize", C.c_int32), ("stride", C.c_int32)]
+
+
 class PetraProfEntry(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double), ("flops", C.c_double),
                 ("bytes", C.c_double)]
@@ -107,6 +112,8 @@ SIGS = {
     "petra_schedule_create": (C.c_int, [I32, C.POINTER(I32), C.POINTER(I32), I32, C.POINTER(P)]),
     "petra_schedule_tick": (C.c_int, [P, I64, I32, C.POINTER(PetraTickReport), C.POINTER(PetraSchedMsgs)]),
     "petra_schedule_destroy": (C.c_int, [P]),
+    "petra_conv_run": (C.c_int, [I32, I32, C.POINTER(PetraConvGeom), VP, VP, VP, VP]),
+    "petra_conv_engine": (C.c_int32, [C.POINTER(PetraConvGeom), I32, I32]),
     "petra_launch_count": (C.c_int64, []),
     "petra_profile": (C.c_int, [I32]),
     "petra_profile_read": (C.c_int, [C.POINTER(PetraProfEntry), I32, C.POINTER(I32)]),

@@ -1,15 +1,539 @@
-// conv_tc.cu -- tcgen05 (5th-gen tensor core) bf16 implicit-GEMM convolutions.
-// Placeholder until the sm_100a kernels land: reports "unsupported" so the
-// engine routes to the SIMT kernels.
+// conv_tc.cu -- tcgen05 (5th-gen tensor core) bf16 implicit-GEMM convolutions for sm_100a.
+//
+// forward  z[m][co] = sum_{tap,ci} x[b][h+kh-p][w+kw-p][ci] * w[co][tap][ci]      (M = B*H*W pixels)
+// dgrad    dx[m][ci] = addend + sum_{tap,co} dz[b][h+kh-p][w+kw-p][co] * wT[ci][tap][co]
+//          (wT = flipped, transposed weights maintained by the update kernel; stride 1)
+// wgrad    dw[co][tap][ci] = sum_{pixels} dz[p][co] * x[p shifted by tap][ci]   (deterministic split-K)
+//
+// Design (B200-first):
+//  * persistent warp-specialised CTAs (one per SM): warp 0 = TMA producer, warp 1 =
+//    MMA issuer (one thread issues tcgen05.mma) + TMEM owner, warps 2-5 = epilogue;
+//  * A (activations) is an implicit im2col: one 4-D TMA box per (tap, 64-channel block)
+//    whose coordinates are shifted by the tap offset; the halo / padding comes from
+//    TMA's zero fill of out-of-bounds coordinates.  A 128-row M tile is a rectangle of
+//    whole image rows (or whole images), so the box lands in smem exactly in the
+//    128B-swizzled K-major layout UMMA reads;
+//  * B (weights) via 2-D TMA; fp32 accumulators live in TMEM, double buffered so the
+//    epilogue of tile i overlaps the MMAs of tile i+1; epilogue = tcgen05.ld -> fp32 store.
+#include <cudaTypedefs.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../errors.h"
 #include "../kernels.h"
+#include "tc_common.cuh"
 
 namespace petra {
-bool conv_tc_supported(const ConvGeom &, int) { return false; }
-size_t conv_tc_workspace(const ConvGeom &, int) { return 0; }
-void conv_fwd_tc(const ConvGeom &, const __nv_bfloat16 *, const __nv_bfloat16 *, float *, __nv_bfloat16 *,
-                 cudaStream_t) {}
-void conv_dgrad_tc(const ConvGeom &, const __nv_bfloat16 *, const __nv_bfloat16 *, const float *, float *,
-                   cudaStream_t) {}
-void conv_wgrad_tc(const ConvGeom &, const __nv_bfloat16 *, const __nv_bfloat16 *, float *, float *,
-                   cudaStream_t) {}
+namespace {
+
+constexpr int BM = 128, BK = 64;
+constexpr int kThreads = 192;  // 6 warps
+constexpr uint32_t A_BYTES = BM * BK * 2;
+
+struct ConvTCParams {
+  int M, N;         // GEMM sizes (pixels, output channels)
+  int k, p;         // filter size, pad
+  int CB;           // 64-channel blocks of the reduction operand
+  int H, W, R, NB;  // image dims, rows per tile, images per tile
+  const float *addend;
+  float *out;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, ConvTCParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t B_BYTES = BN * BK * 2;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles_n = P.N / BN;
+  const int n_tiles = (P.M / BM) * n_tiles_n;
+  const int KB = P.k * P.k * P.CB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);
+    }
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      const int HW = P.H * P.W;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int mt = tile / n_tiles_n, nt = tile % n_tiles_n;
+        const int m0 = mt * BM;
+        const int b0 = m0 / HW, h0 = (m0 % HW) / P.W;
+        for (int kb = 0; kb < KB; ++kb) {
+          const int tap = kb / P.CB, cb = kb % P.CB;
+          const int kh = tap / P.k, kw = tap % P.k;
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *sa = smem + stage * STAGE_BYTES;
+          tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tc::tma_load_4d(sa, &tmA, &full[stage], cb * BK, kw - P.p, h0 + kh - P.p, b0);
+          tc::tma_load_2d(sa + A_BYTES, &tmB, &full[stage], kb * BK, nt * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t dtm = tmem_base + acc * BN;
+        for (int kb = 0; kb < KB; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
+          const uint64_t ad = tc::sw128_desc(sa, 16, 1024);
+          const uint64_t bd = tc::sw128_desc(sa + A_BYTES, 16, 1024);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)  // advance 32 B (16 bf16) along K inside the swizzle row
+            tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          tc::umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc::umma_commit(&tfull[acc]);
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..5
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const int mt = tile / n_tiles_n, nt = tile % n_tiles_n;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      const int64_t m = (int64_t)mt * BM + row;
+      float *orow = P.out + m * P.N + nt * BN;
+      const float *arow = P.addend ? P.addend + m * P.N + nt * BN : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+        if (arow) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            float4 a4 = *reinterpret_cast<const float4 *>(arow + c + j);
+            v[j] += a4.x; v[j + 1] += a4.y; v[j + 2] += a4.z; v[j + 3] += a4.w;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4 *>(orow + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+// ------------------------------------------------------------------ wgrad
+// D[r][n] = sum_p x[p + off(tap(r))][ci(r)] * dz[p][n],  r = tap*Ci + ci  (M side),
+// n = output channel (N side), p = pixel (K, 64 per block).  Both operands are
+// MN-major in smem: A = two 64-channel boxes (rows r0..r0+63, r0+64..r0+127, each
+// possibly a different tap) of 64 shifted pixels, B = BN/64 boxes of dz.  Split-K
+// over pixel blocks; the epilogue stores D transposed: ws[split][n][r], i.e. the
+// weight layout [Co][k][k][Ci], so the fixed-order reduction over splits is dW.
+struct WgradParams {
+  int Mr;            // taps * Ci (rows of D)
+  int N;             // Co
+  int Ci, k, p;
+  int H, W;
+  int KBtot;         // pixel blocks of 64
+  int kb_per_split;
+  int n_mt, n_nt, splits;
+  float *out;        // [splits][N][Mr]
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDZ, WgradParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t HALF_A = 64 * 64 * 2;      // one 64x64 bf16 box
+  constexpr uint32_t B_BYTES = BN * 64 * 2;
+  constexpr uint32_t STAGE_BYTES = 2 * HALF_A + B_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_work = P.n_mt * P.n_nt * P.splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);
+    }
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&tmX);
+    tc::tma_prefetch(&tmDZ);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // work item -> (m tile, n tile, split)
+  auto decode = [&](int w, int &mt, int &nt, int &sp) {
+    sp = w % P.splits;
+    int r = w / P.splits;
+    nt = r % P.n_nt;
+    mt = r / P.n_nt;
+  };
+  const int HW = P.H * P.W;
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        int mt, nt, sp;
+        decode(w, mt, nt, sp);
+        const int kb0 = sp * P.kb_per_split, kb1 = min(P.KBtot, kb0 + P.kb_per_split);
+        int tapj[2], ci0j[2];
+        bool valid[2];
+        for (int j = 0; j < 2; ++j) {
+          int r = mt * 128 + j * 64;
+          valid[j] = r < P.Mr;
+          tapj[j] = r / P.Ci;
+          ci0j[j] = r % P.Ci;
+        }
+        const uint32_t bytes = (valid[1] ? 2 : 1) * HALF_A + B_BYTES;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int p0 = kb * 64;
+          const int b0 = p0 / HW, h0 = (p0 % HW) / P.W;
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *sa = smem + stage * STAGE_BYTES;
+          tc::mbar_arrive_expect_tx(&full[stage], bytes);
+          for (int j = 0; j < 2; ++j) {
+            if (!valid[j]) continue;
+            const int kh = tapj[j] / P.k, kw = tapj[j] % P.k;
+            tc::tma_load_4d(sa + j * HALF_A, &tmX, &full[stage], ci0j[j], kw - P.p, h0 + kh - P.p, b0);
+          }
+          for (int nb = 0; nb < BN / 64; ++nb)
+            tc::tma_load_2d(sa + 2 * HALF_A + nb * HALF_A, &tmDZ, &full[stage], nt * BN + nb * 64, p0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(128, BN, 1, 1);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+        int mt, nt, sp;
+        decode(w, mt, nt, sp);
+        const int kb0 = sp * P.kb_per_split, kb1 = min(P.KBtot, kb0 + P.kb_per_split);
+        const int acc = it & 1;
+        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t dtm = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
+          // MN-major: LBO = next 64-element MN block (8 KB), SBO = next 8 K-rows (1 KB)
+          const uint64_t ad = tc::sw128_desc(sa, HALF_A, 1024);
+          const uint64_t bd = tc::sw128_desc(sa + 2 * HALF_A, HALF_A, 1024);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // 16 pixels = 16 rows x 128 B = 2048 B per step
+            tc::umma_bf16(dtm, ad + (uint64_t)(k * 2048 >> 4), bd + (uint64_t)(k * 2048 >> 4), idesc,
+                          (kb > kb0 || k) ? 1u : 0u);
+          tc::umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc::umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      int mt, nt, sp;
+      decode(w, mt, nt, sp);
+      const int acc = it & 1;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      const int r = mt * 128 + row;
+      float *o = P.out + (int64_t)sp * P.N * P.Mr;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+        if (r < P.Mr) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[(int64_t)(nt * BN + c + j) * P.Mr + r] = v[j];
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+__global__ void wgrad_reduce_kernel(const float *__restrict__ part, int splits, int64_t n, float *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];
+    out[i] = s;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw PetraError(PETRA_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_map(const void *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides_bytes,
+                     const cuuint32_t *box) {
+  CUtensorMap m;
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(base), dims,
+                           strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw PetraError(PETRA_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+// activation map [B][H][W][C] bf16, box (64 ch, W, R rows, NB images)
+CUtensorMap act_map(const __nv_bfloat16 *x, int B, int H, int W, int C, int R, int NB) {
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t st[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)W, (cuuint32_t)R, (cuuint32_t)NB};
+  return make_map(x, 4, dims, st, box);
+}
+
+// K-major matrix [rows][K] bf16, box (64 K, box_rows)
+CUtensorMap mat_map(const __nv_bfloat16 *w, int rows, int K, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t st[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  return make_map(w, 2, dims, st, box);
+}
+
+struct Tiling {
+  int R, NB;
+  bool ok;
+};
+Tiling tiling(int B, int H, int W) {
+  Tiling t{0, 0, false};
+  if (W > BM || BM % W) return t;
+  int rows = BM / W;
+  if (rows <= H) {
+    if (H % rows) return t;
+    t.R = rows;
+    t.NB = 1;
+  } else {
+    if (rows % H) return t;
+    t.R = H;
+    t.NB = rows / H;
+    if (B % t.NB) return t;
+  }
+  t.ok = true;
+  return t;
+}
+
+int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64); }
+
+template <int BN, int STAGES>
+void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P, cudaStream_t st) {
+  size_t smem = (size_t)STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    PETRA_CUDA(cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    attr = true;
+  }
+  int tiles = (P.M / BM) * (P.N / BN);
+  int grid = std::min(tiles, kNumSMs);
+  conv_tc_kernel<BN, STAGES><<<grid, kThreads, smem, st>>>(ta, tb, P);
+  PETRA_LAUNCH_CHECK();
+}
+
+void run_conv(const ConvGeom &g, bool dgrad, const __nv_bfloat16 *a, const __nv_bfloat16 *w, const float *addend,
+              float *out, cudaStream_t st) {
+  // forward: A = x [B][H][W][Ci], weights [Co][k*k*Ci], N = Co
+  // dgrad  : A = dz [B][H][W][Co], weights^T [Ci][k*k*Co], N = Ci   (stride 1: H = Ho)
+  const int Cin = dgrad ? g.Co : g.Ci, N = dgrad ? g.Ci : g.Co;
+  Tiling t = tiling(g.B, g.H, g.W);
+  ConvTCParams P;
+  P.M = g.B * g.H * g.W;
+  P.N = N;
+  P.k = g.k;
+  P.p = g.p;
+  P.CB = Cin / 64;
+  P.H = g.H;
+  P.W = g.W;
+  P.R = t.R;
+  P.NB = t.NB;
+  P.addend = addend;
+  P.out = out;
+  const int BN = pick_bn(N);
+  CUtensorMap ta = act_map(a, g.B, g.H, g.W, Cin, t.R, t.NB);
+  CUtensorMap tb = mat_map(w, N, g.k * g.k * Cin, BN);
+  if (BN == 256) launch_conv<256, 4>(ta, tb, P, st);
+  else if (BN == 128) launch_conv<128, 5>(ta, tb, P, st);
+  else launch_conv<64, 6>(ta, tb, P, st);
+}
+
+struct WgradPlan {
+  int BN, splits, kb_per_split, n_mt, n_nt, KBtot;
+};
+WgradPlan wgrad_plan(const ConvGeom &g) {
+  WgradPlan w;
+  w.BN = g.Co % 256 == 0 ? 256 : (g.Co % 128 == 0 ? 128 : 64);
+  w.n_nt = g.Co / w.BN;
+  w.n_mt = (int)cdiv((int64_t)g.k * g.k * g.Ci, 128);
+  w.KBtot = (int)(g.M() / 64);
+  int tiles = w.n_mt * w.n_nt;
+  int want = std::max(1, std::min(w.KBtot, (int)cdiv(kNumSMs, tiles)));
+  w.kb_per_split = (int)cdiv(w.KBtot, want);
+  w.splits = (int)cdiv(w.KBtot, w.kb_per_split);
+  return w;
+}
+
+template <int BN, int STAGES>
+void launch_wgrad(const CUtensorMap &tx, const CUtensorMap &tdz, const WgradParams &P, cudaStream_t st) {
+  size_t smem = (size_t)STAGES * (2 * 64 * 64 * 2 + BN * 64 * 2) + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    PETRA_CUDA(cudaFuncSetAttribute(wgrad_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    attr = true;
+  }
+  int work = P.n_mt * P.n_nt * P.splits;
+  wgrad_tc_kernel<BN, STAGES><<<std::min(work, kNumSMs), kThreads, smem, st>>>(tx, tdz, P);
+  PETRA_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+bool conv_tc_supported(const ConvGeom &g, int mode) {
+  if (g.s != 1 || g.Ci % 64 || g.Co % 64) return false;
+  if (mode == 2) {
+    if (g.M() % 64 || g.Ho != g.H || g.Wo != g.W) return false;
+    Tiling t{0, 0, false};
+    if (g.W <= 64 && 64 % g.W == 0) {
+      int rows = 64 / g.W;
+      if (rows <= g.H) return g.H % rows == 0;
+      return rows % g.H == 0 && g.B % (rows / g.H) == 0;
+    }
+    (void)t;
+    return false;
+  }
+  if (g.Ho != g.H || g.Wo != g.W) return false;
+  if ((int64_t)g.B * g.H * g.W % BM) return false;
+  return tiling(g.B, g.H, g.W).ok;
+}
+
+size_t conv_tc_workspace(const ConvGeom &g, int mode) {
+  if (mode != 2 || !conv_tc_supported(g, 2)) return 0;
+  WgradPlan w = wgrad_plan(g);
+  return w.splits > 1 ? (size_t)w.splits * g.Co * g.K() * sizeof(float) : 0;
+}
+
+void conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32,
+                 __nv_bfloat16 *, cudaStream_t st) {
+  run_conv(g, false, x, w, nullptr, z_f32, st);
+}
+
+void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend,
+                   float *dx, cudaStream_t st) {
+  run_conv(g, true, dz, wt, addend, dx, st);
+}
+
+void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *x, float *dw, float *ws,
+                   cudaStream_t st) {
+  WgradPlan w = wgrad_plan(g);
+  int rows = 64 / g.W, R, NB;
+  if (rows <= g.H) { R = rows; NB = 1; } else { R = g.H; NB = rows / g.H; }
+  CUtensorMap tx = act_map(x, g.B, g.H, g.W, g.Ci, R, NB);
+  // dz as a [pixels][Co] matrix, box (64 channels, 64 pixels)
+  CUtensorMap tdz = mat_map(dz, (int)g.M(), g.Co, 64);
+  WgradParams P;
+  P.Mr = g.K();
+  P.N = g.Co;
+  P.Ci = g.Ci;
+  P.k = g.k;
+  P.p = g.p;
+  P.H = g.H;
+  P.W = g.W;
+  P.KBtot = w.KBtot;
+  P.kb_per_split = w.kb_per_split;
+  P.n_mt = w.n_mt;
+  P.n_nt = w.n_nt;
+  P.splits = w.splits;
+  P.out = w.splits > 1 ? ws : dw;
+  if (w.BN == 256) launch_wgrad<256, 3>(tx, tdz, P, st);
+  else if (w.BN == 128) launch_wgrad<128, 4>(tx, tdz, P, st);
+  else launch_wgrad<64, 6>(tx, tdz, P, st);
+  if (w.splits > 1) {
+    int64_t n = (int64_t)g.Co * g.K();
+    wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st>>>(ws, w.splits, n, dw);
+    PETRA_LAUNCH_CHECK();
+  }
+}
+
 }  // namespace petra

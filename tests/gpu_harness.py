@@ -92,3 +92,37 @@ def rand_params(units, seed):
                 p[...] = 0.1 * synth.normal(p.shape, seed, 101, i)
             i += 1
     return units
+
+
+def bf16_round(a):
+    """Round to bfloat16 (round-to-nearest-even) through fp32, as the kernels do."""
+    f = np.ascontiguousarray(np.asarray(a, np.float32))
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+class bf16_emulation:
+    """Context manager: make the oracle round conv operands to bf16 exactly where
+    libpetra runs that convolution pass on the tcgen05 engine (reading c22)."""
+
+    def __enter__(self):
+        import ctypes as C
+        from oracle import primitives as OP
+        self.OP = OP
+        self.saved = dict(OP.OPERAND_ROUND)
+        cache = {}
+
+        def hook(a, kind, geom):
+            mode = {"fwd": 0, "dgrad": 1, "wgrad": 2}[kind]
+            key = (mode, geom)
+            if key not in cache:
+                g = L.PetraConvGeom(*geom)
+                cache[key] = L.lib().petra_conv_engine(C.byref(g), mode, L.BF16_TC) == 1
+            return bf16_round(a) if cache[key] else a
+        for k in OP.OPERAND_ROUND:
+            OP.OPERAND_ROUND[k] = hook
+        return self
+
+    def __exit__(self, *exc):
+        self.OP.OPERAND_ROUND.update(self.saved)

@@ -1,0 +1,87 @@
+"""Kernel-level GPU tests (T1): one convolution pass through petra_conv_run.
+  * SIMT fp32 kernels vs the oracle's fp64 conv / VJP (rel 1e-6);
+  * tcgen05 bf16 kernels vs the SIMT kernels on bf16-exact inputs: every product
+    is exact in fp32 on both, so only the summation order differs (rel 1e-5)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import primitives as P
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+from paper_2406_02052_b200 import _lib as L  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def bf16_exact(a):
+    return torch.tensor(a, dtype=torch.float32).to(torch.bfloat16).to(torch.float32).numpy()
+
+
+def conv_run(mode, engine, geom, a, b, addend=None):
+    B, H, W, Ci, Co, k, s = geom
+    g = L.PetraConvGeom(B, H, W, Ci, Co, k, s)
+    p = (k - 1) // 2
+    Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+    n_out = {0: B * Ho * Wo * Co, 1: B * H * W * Ci, 2: Co * k * k * Ci}[mode]
+    out = np.zeros(n_out, np.float32)
+    a, b = np.ascontiguousarray(a, np.float32), np.ascontiguousarray(b, np.float32)
+    ad = None if addend is None else np.ascontiguousarray(addend, np.float32)
+    st = L.lib().petra_conv_run(mode, engine, C.byref(g), a.ctypes.data, b.ctypes.data,
+                                None if ad is None else ad.ctypes.data, out.ctypes.data)
+    if st != 0:
+        raise L.PetraError(st, "petra_conv_run", "")
+    return out
+
+
+GEOMS = [  # (B, H, W, Ci, Co, k, stride)
+    (2, 32, 32, 64, 64, 3, 1), (2, 16, 16, 128, 128, 3, 1), (8, 8, 8, 256, 256, 3, 1),
+    (8, 4, 4, 512, 512, 3, 1), (2, 16, 16, 256, 64, 1, 1), (2, 16, 16, 64, 256, 1, 1),
+    (4, 8, 8, 64, 192, 3, 1),
+]
+SIMT_GEOMS = GEOMS[:2] + [(2, 9, 7, 3, 16, 3, 1), (2, 10, 10, 16, 32, 3, 2), (2, 9, 9, 8, 12, 1, 2),
+                          (2, 15, 15, 3, 8, 7, 2)]
+
+
+def inputs(geom, seed):
+    B, H, W, Ci, Co, k, s = geom
+    p = (k - 1) // 2
+    Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+    x = bf16_exact(synth.normal((B, H, W, Ci), seed, 1))
+    w = bf16_exact(synth.normal((Co, k, k, Ci), seed, 2) / np.sqrt(k * k * Ci))
+    dz = bf16_exact(synth.normal((B, Ho, Wo, Co), seed, 3))
+    add = synth.normal((B, H, W, Ci), seed, 4).astype(np.float32)
+    return x, w, dz, add
+
+
+@pytest.mark.parametrize("geom", SIMT_GEOMS)
+def test_simt_conv_vs_oracle(geom):
+    B, H, W, Ci, Co, k, s = geom
+    x, w, dz, add = inputs(geom, 1)
+    xo, wo, dzo = x.transpose(0, 3, 1, 2), w.transpose(0, 3, 1, 2), dz.transpose(0, 3, 1, 2)
+    want_z = P.conv2d(xo.astype(np.float64), wo.astype(np.float64), s, (k - 1) // 2)
+    dx_w, dw_w = P.conv2d_vjp(xo.astype(np.float64), wo.astype(np.float64), s, (k - 1) // 2, dzo.astype(np.float64))
+    z = conv_run(0, 0, geom, x, w).reshape(want_z.transpose(0, 2, 3, 1).shape)
+    assert rel(z, want_z.transpose(0, 2, 3, 1)) < 1e-6
+    dx = conv_run(1, 0, geom, dz, w, add).reshape(add.shape)
+    assert rel(dx, dx_w.transpose(0, 2, 3, 1) + add) < 1e-6
+    dw = conv_run(2, 0, geom, dz, x).reshape(w.shape)
+    assert rel(dw, dw_w.transpose(0, 2, 3, 1)) < 1e-6
+
+
+@pytest.mark.parametrize("geom", GEOMS)
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_tc_conv_vs_simt(geom, mode):
+    x, w, dz, add = inputs(geom, 2)
+    a = x if mode == 0 else dz
+    b = x if mode == 2 else w
+    addend = add if mode == 1 else None
+    assert L.lib().petra_conv_engine(C.byref(L.PetraConvGeom(*geom)), mode, L.BF16_TC) == 1
+    ref = conv_run(mode, 0, geom, a, b, addend)
+    got = conv_run(mode, 1, geom, a, b, addend)
+    assert rel(got, ref) < 1e-5, rel(got, ref)

@@ -9,8 +9,8 @@ import synth
 from oracle import engine as E
 from oracle import models as OM
 from oracle.units import Branch, ConvBN, DSUnit, RevUnit, StemUnit, TailUnit
-from tests.gpu_harness import (nchw, nhwc, oracle_to_product_units, pack_like, pack_params, per_tensor_rel,
-                               rand_params, rel)
+from tests.gpu_harness import (bf16_emulation, nchw, nhwc, oracle_to_product_units, pack_like, pack_params,
+                               per_tensor_rel, rand_params, rel)
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -19,7 +19,10 @@ from paper_2406_02052_b200 import Pipeline, Stage  # noqa: E402
 from paper_2406_02052_b200 import _lib as L  # noqa: E402
 from paper_2406_02052_b200 import models as PM  # noqa: E402
 
-TOL = {L.FP32: 1e-4, L.BF16_TC: 2e-2}
+# fp32 path vs the exact oracle: 1e-4.  bf16 tensor-core path vs the oracle that
+# rounds conv operands to bf16 where the kernel does (reading c22): 1e-3; the
+# forward outputs of the bf16 path are also held to 2e-2 against the EXACT oracle.
+TOL = {L.FP32: 1e-4, L.BF16_TC: 1e-3}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -83,11 +86,39 @@ STAGE_CASES = {
 }
 
 
-@pytest.mark.parametrize("precision", [L.FP32])
+@pytest.mark.parametrize("precision", [L.FP32, L.BF16_TC])
 @pytest.mark.parametrize("case", sorted(STAGE_CASES))
 def test_stage_tick_parity(case, precision):
     """One forward tick then one backward tick (reconstruction with the current
     theta + VJP + immediate Nesterov update) of a non-final stage."""
+    if precision == L.BF16_TC:
+        exact_fwd = _stage_forward_only(case)
+        with bf16_emulation():
+            _stage_tick(case, precision, exact_fwd)
+    else:
+        _stage_tick(case, precision, None)
+
+
+def _stage_forward_only(case):
+    """Forward of the bf16 path vs the EXACT fp64 oracle (north_star rel 2e-2)."""
+    make, B, in_shapes = STAGE_CASES[case]
+    units = make()
+    stem = isinstance(units[0], StemUnit)
+    in_hwc = tuple(np.array(in_shapes[0])[[2, 3, 1]])
+    st = make_pair(units, B, in_hwc, L.BF16_TC)
+    ostage = E.Stage(units, E.OptConfig(), 1, 2)
+    xs = [synth.images(s, 0, i) for i, s in enumerate(in_shapes)]
+    fo = ostage.forward(E.Fwd(0, xs, None))
+    o = [torch.empty(st.out_shape, device="cuda") for _ in range(2)]
+    gx = [dev(nhwc(x)) for x in xs]
+    st.forward(0, gx[0], gx[1] if not stem else None, o[0], o[1])
+    torch.cuda.synchronize()
+    errs = [rel(nchw(host(o[h])), fo.xs[h]) for h in range(2)]
+    assert max(errs) <= 2e-2, errs
+    return errs
+
+
+def _stage_tick(case, precision, exact_fwd):
     make, B, in_shapes = STAGE_CASES[case]
     units = make()
     stem = isinstance(units[0], StemUnit)
