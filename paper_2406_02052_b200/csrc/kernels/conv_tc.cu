@@ -1,25 +1,25 @@
 // conv_tc.cu -- tcgen05 (5th-gen tensor core) bf16 implicit-GEMM convolutions for sm_100a.
 //
-// forward  z[m][co] = sum_{tap,ci} x[b][h+kh-p][w+kw-p][ci] * w[co][tap][ci]      (M = B*H*W pixels)
-// dgrad    dx[m][ci] = addend + sum_{tap,co} dz[b][h+kh-p][w+kw-p][co] * wT[ci][tap][co]
-//          (wT = flipped, transposed weights maintained by the update kernel; stride 1)
-// wgrad    dw[co][tap][ci] = sum_{pixels} dz[p][co] * x[p shifted by tap][ci]   (deterministic split-K)
+// forward  z[m][co] = sum_{tap,ci} x[b][s*ho+kh-p][s*wo+kw-p][ci] * w[co][tap][ci]   (M = B*Ho*Wo)
+// dgrad    dx[m][ci] = addend + sum_{tap,co} dz[.][.][co] * wT[ci][tap'][co]
+//          stride 1: a plain conv of dz with the flipped/transposed weights wT;
+//          stride 2: stride-phase decomposition -- output pixels (2i+ph, 2j+pw) form 4
+//          sub-grids, each a stride-1 conv of dz with the taps kh = ph+p (mod 2) only.
+// wgrad    dw[co][tap][ci] = sum_{pixels} dz[p][co] * x[s*p + tap offset][ci]   (split-K)
 //
 // Design (B200-first):
 //  * persistent warp-specialised CTAs (one per SM): warp 0 = TMA producer, warp 1 =
-//    MMA issuer (one thread issues tcgen05.mma) + TMEM owner, warps 2-5 = epilogue;
-//  * A (activations) is an implicit im2col: one 4-D TMA box per (tap, 64-channel block)
-//    whose coordinates are shifted by the tap offset; the halo / padding comes from
-//    TMA's zero fill of out-of-bounds coordinates.  A 128-row M tile is a rectangle of
-//    whole image rows (or whole images), so the box lands in smem exactly in the
-//    128B-swizzled K-major layout UMMA reads;
-//  * B (weights) via 2-D TMA; fp32 accumulators live in TMEM, double buffered so the
-//    epilogue of tile i overlaps the MMAs of tile i+1; epilogue = tcgen05.ld -> fp32 store.
+//    tcgen05.mma issuer (one thread) + TMEM owner, warps 2-5 = epilogue;
+//  * A (activations) is an implicit im2col: one 4-D TMA box per (tap, 64-channel
+//    block), coordinates shifted by the tap offset, stride s via TMA traversal
+//    strides, halo / padding from TMA's zero fill of out-of-bounds coordinates.  A
+//    128-row M tile is a rectangle of whole output rows (or whole images), so the
+//    box lands in smem exactly in the 128B-swizzled K-major layout UMMA reads;
+//  * B (weights) via 2-D TMA; fp32 accumulators in TMEM, double buffered so the
+//    epilogue (tcgen05.ld -> fp32 store) of tile i overlaps the MMAs of tile i+1.
 #include <cudaTypedefs.h>
 
-#include <map>
 #include <mutex>
-#include <tuple>
 
 #include "../errors.h"
 #include "../kernels.h"
@@ -31,19 +31,25 @@ namespace {
 constexpr int BM = 128, BK = 64;
 constexpr int kThreads = 192;  // 6 warps
 constexpr uint32_t A_BYTES = BM * BK * 2;
+constexpr int kMaxTaps = 9;
 
 struct ConvTCParams {
-  int M, N;         // GEMM sizes (pixels, output channels)
-  int k, p;         // filter size, pad
-  int CB;           // 64-channel blocks of the reduction operand
-  int H, W, R, NB;  // image dims, rows per tile, images per tile
+  int M, N;                  // GEMM: M = pixels of the output grid, N = output channels
+  int CB;                    // 64-channel blocks of the reduction operand
+  int Cred;                  // channels of the reduction operand (B's K = wk * Cred + c)
+  int ntaps;
+  int dh[kMaxTaps], dw[kMaxTaps], wk[kMaxTaps];  // A coordinate offsets, weight tap index
+  int Gh, Gw;                // output grid of the GEMM (rows x cols per image)
+  int s_in;                  // A row coordinate = s_in * grid_row + dh
+  int OH, OW, oss, ph, pw;   // grid (i, j) -> output pixel (i*oss+ph, j*oss+pw) of an OH x OW image
   const float *addend;
-  float *out;
+  float *out;                // [B*OH*OW][N]
 };
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, ConvTCParams P) {
+conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ ConvTCParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t B_BYTES = BN * BK * 2;
@@ -57,7 +63,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_n = P.N / BN;
   const int n_tiles = (P.M / BM) * n_tiles_n;
-  const int KB = P.k * P.k * P.CB;
+  const int KB = P.ntaps * P.CB;
+  const int GHW = P.Gh * P.Gw;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -82,19 +89,17 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      const int HW = P.H * P.W;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int mt = tile / n_tiles_n, nt = tile % n_tiles_n;
         const int m0 = mt * BM;
-        const int b0 = m0 / HW, h0 = (m0 % HW) / P.W;
+        const int b0 = m0 / GHW, i0 = (m0 % GHW) / P.Gw;
         for (int kb = 0; kb < KB; ++kb) {
-          const int tap = kb / P.CB, cb = kb % P.CB;
-          const int kh = tap / P.k, kw = tap % P.k;
+          const int t = kb / P.CB, cb = kb % P.CB;
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * STAGE_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tc::tma_load_4d(sa, &tmA, &full[stage], cb * BK, kw - P.p, h0 + kh - P.p, b0);
-          tc::tma_load_2d(sa + A_BYTES, &tmB, &full[stage], kb * BK, nt * BN);
+          tc::tma_load_4d(sa, &tmA, &full[stage], cb * BK, P.dw[t], P.s_in * i0 + P.dh[t], b0);
+          tc::tma_load_2d(sa + A_BYTES, &tmB, &full[stage], P.wk[t] * P.Cred + cb * BK, nt * BN);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -134,23 +139,25 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int mt = tile / n_tiles_n, nt = tile % n_tiles_n;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
-      const int64_t m = (int64_t)mt * BM + row;
-      float *orow = P.out + m * P.N + nt * BN;
-      const float *arow = P.addend ? P.addend + m * P.N + nt * BN : nullptr;
+      const int m = mt * BM + row;
+      const int b = m / GHW, r = m % GHW, i = r / P.Gw, j = r % P.Gw;
+      const int64_t opix = ((int64_t)b * P.OH + i * P.oss + P.ph) * P.OW + j * P.oss + P.pw;
+      float *orow = P.out + opix * P.N + nt * BN;
+      const float *arow = P.addend ? P.addend + opix * P.N + nt * BN : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         float v[16];
         tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
         if (arow) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            float4 a4 = *reinterpret_cast<const float4 *>(arow + c + j);
-            v[j] += a4.x; v[j + 1] += a4.y; v[j + 2] += a4.z; v[j + 3] += a4.w;
+          for (int jj = 0; jj < 16; jj += 4) {
+            float4 a4 = *reinterpret_cast<const float4 *>(arow + c + jj);
+            v[jj] += a4.x; v[jj + 1] += a4.y; v[jj + 2] += a4.z; v[jj + 3] += a4.w;
           }
         }
 #pragma unroll
-        for (int j = 0; j < 16; j += 4)
-          *reinterpret_cast<float4 *>(orow + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        for (int jj = 0; jj < 16; jj += 4)
+          *reinterpret_cast<float4 *>(orow + c + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
       }
       tc::tc_fence_before();
       __syncwarp();
@@ -165,29 +172,30 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------ wgrad
-// D[r][n] = sum_p x[p + off(tap(r))][ci(r)] * dz[p][n],  r = tap*Ci + ci  (M side),
-// n = output channel (N side), p = pixel (K, 64 per block).  Both operands are
-// MN-major in smem: A = two 64-channel boxes (rows r0..r0+63, r0+64..r0+127, each
-// possibly a different tap) of 64 shifted pixels, B = BN/64 boxes of dz.  Split-K
-// over pixel blocks; the epilogue stores D transposed: ws[split][n][r], i.e. the
-// weight layout [Co][k][k][Ci], so the fixed-order reduction over splits is dW.
+// D[r][n] = sum_p x[s*p + off(tap(r))][ci(r)] * dz[p][n],  r = tap*Ci + ci (M side),
+// n = output channel (N side), p = output pixel (K, 64 per block).  Both operands
+// are MN-major in smem: A = two 64-channel boxes (rows r0..r0+63 and r0+64..r0+127,
+// each possibly another tap) of 64 shifted pixels, B = BN/64 boxes of dz.  Split-K
+// over pixel blocks; the epilogue stores D transposed, ws[split][n][r] -- the weight
+// layout [Co][k][k][Ci] -- so the fixed-order reduction over splits yields dW.
 struct WgradParams {
-  int Mr;            // taps * Ci (rows of D)
-  int N;             // Co
-  int Ci, k, p;
-  int H, W;
-  int KBtot;         // pixel blocks of 64
+  int Mr;                 // taps * Ci (rows of D)
+  int N;                  // Co
+  int Ci, k, p, s;
+  int Gh, Gw;             // output pixel grid (Ho x Wo)
+  int KBtot;              // pixel blocks of 64
   int kb_per_split;
   int n_mt, n_nt, splits;
-  float *out;        // [splits][N][Mr]
+  float *out;             // [splits][N][Mr]
 };
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDZ, WgradParams P) {
+wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDZ,
+                const __grid_constant__ WgradParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr uint32_t HALF_A = 64 * 64 * 2;      // one 64x64 bf16 box
+  constexpr uint32_t HALF_A = 64 * 64 * 2;  // one 64x64 bf16 box
   constexpr uint32_t B_BYTES = BN * 64 * 2;
   constexpr uint32_t STAGE_BYTES = 2 * HALF_A + B_BYTES;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
@@ -217,14 +225,13 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // work item -> (m tile, n tile, split)
   auto decode = [&](int w, int &mt, int &nt, int &sp) {
     sp = w % P.splits;
     int r = w / P.splits;
     nt = r % P.n_nt;
     mt = r / P.n_nt;
   };
-  const int HW = P.H * P.W;
+  const int GHW = P.Gh * P.Gw;
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
@@ -244,14 +251,14 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
         const uint32_t bytes = (valid[1] ? 2 : 1) * HALF_A + B_BYTES;
         for (int kb = kb0; kb < kb1; ++kb) {
           const int p0 = kb * 64;
-          const int b0 = p0 / HW, h0 = (p0 % HW) / P.W;
+          const int b0 = p0 / GHW, i0 = (p0 % GHW) / P.Gw;
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * STAGE_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], bytes);
           for (int j = 0; j < 2; ++j) {
             if (!valid[j]) continue;
             const int kh = tapj[j] / P.k, kw = tapj[j] % P.k;
-            tc::tma_load_4d(sa + j * HALF_A, &tmX, &full[stage], ci0j[j], kw - P.p, h0 + kh - P.p, b0);
+            tc::tma_load_4d(sa + j * HALF_A, &tmX, &full[stage], ci0j[j], kw - P.p, P.s * i0 + kh - P.p, b0);
           }
           for (int nb = 0; nb < BN / 64; ++nb)
             tc::tma_load_2d(sa + 2 * HALF_A + nb * HALF_A, &tmDZ, &full[stage], nt * BN + nb * 64, p0);
@@ -308,7 +315,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
         tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
         if (r < P.Mr) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) o[(int64_t)(nt * BN + c + j) * P.Mr + r] = v[j];
+          for (int jj = 0; jj < 16; ++jj) o[(int64_t)(nt * BN + c + jj) * P.Mr + r] = v[jj];
         }
       }
       tc::tc_fence_before();
@@ -323,11 +330,28 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
   }
 }
 
-__global__ void wgrad_reduce_kernel(const float *__restrict__ part, int splits, int64_t n, float *__restrict__ out) {
+__global__ void splitk_sum_kernel(const float *__restrict__ part, int splits, int64_t n, float *__restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];
+    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];  // fixed order: deterministic
     out[i] = s;
+  }
+}
+
+// out[pixels of phase (ph, pw)] = addend (or 0): the stride-2 dgrad phases without taps
+__global__ void phase_fill_kernel(int B, int OH, int OW, int C, int ph, int pw, const float *__restrict__ addend,
+                                  float *__restrict__ out) {
+  const int Gh = (OH - ph + 1) / 2, Gw = (OW - pw + 1) / 2;
+  const int64_t n = (int64_t)B * Gh * Gw * C;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % C);
+    int64_t g = i / C;
+    int j = (int)(g % Gw);
+    int64_t r = g / Gw;
+    int ii = (int)(r % Gh);
+    int b = (int)(r / Gh);
+    int64_t o = (((int64_t)b * OH + 2 * ii + ph) * OW + 2 * j + pw) * C + c;
+    out[o] = addend ? addend[o] : 0.f;
   }
 }
 
@@ -347,9 +371,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 CUtensorMap make_map(const void *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides_bytes,
-                     const cuuint32_t *box) {
+                     const cuuint32_t *box, const cuuint32_t *es) {
   CUtensorMap m;
-  cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(base), dims,
                            strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -357,12 +380,14 @@ CUtensorMap make_map(const void *base, int rank, const cuuint64_t *dims, const c
   return m;
 }
 
-// activation map [B][H][W][C] bf16, box (64 ch, W, R rows, NB images)
-CUtensorMap act_map(const __nv_bfloat16 *x, int B, int H, int W, int C, int R, int NB) {
+// activation map [B][H][W][C] bf16; box = (64 ch, Gw output cols, R output rows, NB
+// images) read with traversal stride s along W and H (the box spans s*Gw x s*R inputs)
+CUtensorMap act_map(const __nv_bfloat16 *x, int B, int H, int W, int C, int Gw, int R, int NB, int s) {
   cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
   cuuint64_t st[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-  cuuint32_t box[4] = {64, (cuuint32_t)W, (cuuint32_t)R, (cuuint32_t)NB};
-  return make_map(x, 4, dims, st, box);
+  cuuint32_t box[4] = {64, (cuuint32_t)(Gw * s), (cuuint32_t)(R * s), (cuuint32_t)NB};
+  cuuint32_t es[4] = {1, (cuuint32_t)s, (cuuint32_t)s, 1};
+  return make_map(x, 4, dims, st, box, es);
 }
 
 // K-major matrix [rows][K] bf16, box (64 K, box_rows)
@@ -370,25 +395,27 @@ CUtensorMap mat_map(const __nv_bfloat16 *w, int rows, int K, int box_rows) {
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
   cuuint64_t st[1] = {(cuuint64_t)K * 2};
   cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
-  return make_map(w, 2, dims, st, box);
+  cuuint32_t es[2] = {1, 1};
+  return make_map(w, 2, dims, st, box, es);
 }
 
+// A tile of `rows` GEMM rows must be a rectangle of whole grid rows (or whole images)
 struct Tiling {
   int R, NB;
   bool ok;
 };
-Tiling tiling(int B, int H, int W) {
+Tiling tiling(int B, int Gh, int Gw, int rows_per_tile) {
   Tiling t{0, 0, false};
-  if (W > BM || BM % W) return t;
-  int rows = BM / W;
-  if (rows <= H) {
-    if (H % rows) return t;
+  if (Gw > rows_per_tile || rows_per_tile % Gw) return t;
+  int rows = rows_per_tile / Gw;
+  if (rows <= Gh) {
+    if (Gh % rows) return t;
     t.R = rows;
     t.NB = 1;
   } else {
-    if (rows % H) return t;
-    t.R = H;
-    t.NB = rows / H;
+    if (rows % Gh) return t;
+    t.R = Gh;
+    t.NB = rows / Gh;
     if (B % t.NB) return t;
   }
   t.ok = true;
@@ -407,42 +434,113 @@ void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParam
     attr = true;
   }
   int tiles = (P.M / BM) * (P.N / BN);
-  int grid = std::min(tiles, kNumSMs);
-  conv_tc_kernel<BN, STAGES><<<grid, kThreads, smem, st>>>(ta, tb, P);
+  conv_tc_kernel<BN, STAGES><<<std::min(tiles, kNumSMs), kThreads, smem, st>>>(ta, tb, P);
   PETRA_LAUNCH_CHECK();
 }
 
-void run_conv(const ConvGeom &g, bool dgrad, const __nv_bfloat16 *a, const __nv_bfloat16 *w, const float *addend,
-              float *out, cudaStream_t st) {
-  // forward: A = x [B][H][W][Ci], weights [Co][k*k*Ci], N = Co
-  // dgrad  : A = dz [B][H][W][Co], weights^T [Ci][k*k*Co], N = Ci   (stride 1: H = Ho)
-  const int Cin = dgrad ? g.Co : g.Ci, N = dgrad ? g.Ci : g.Co;
-  Tiling t = tiling(g.B, g.H, g.W);
-  ConvTCParams P;
-  P.M = g.B * g.H * g.W;
-  P.N = N;
-  P.k = g.k;
-  P.p = g.p;
-  P.CB = Cin / 64;
-  P.H = g.H;
-  P.W = g.W;
-  P.R = t.R;
-  P.NB = t.NB;
-  P.addend = addend;
-  P.out = out;
-  const int BN = pick_bn(N);
-  CUtensorMap ta = act_map(a, g.B, g.H, g.W, Cin, t.R, t.NB);
-  CUtensorMap tb = mat_map(w, N, g.k * g.k * Cin, BN);
+void launch_any(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P, cudaStream_t st) {
+  const int BN = pick_bn(P.N);
   if (BN == 256) launch_conv<256, 4>(ta, tb, P, st);
   else if (BN == 128) launch_conv<128, 5>(ta, tb, P, st);
   else launch_conv<64, 6>(ta, tb, P, st);
 }
 
+bool geom_ok(const ConvGeom &g) {
+  if (g.Ci % 64 || g.Co % 64 || g.k > 3) return false;
+  if (g.s != 1 && g.s != 2) return false;
+  if (g.s == 2 && ((g.H & 1) || (g.W & 1) || g.Ho * 2 != g.H || g.Wo * 2 != g.W)) return false;
+  if (g.s == 1 && (g.Ho != g.H || g.Wo != g.W)) return false;
+  return true;
+}
+
+void run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *out, cudaStream_t st) {
+  Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
+  ConvTCParams P{};
+  P.M = (int)g.M();
+  P.N = g.Co;
+  P.Cred = g.Ci;
+  P.CB = g.Ci / 64;
+  P.ntaps = g.k * g.k;
+  for (int tap = 0; tap < P.ntaps; ++tap) {
+    P.dh[tap] = tap / g.k - g.p;
+    P.dw[tap] = tap % g.k - g.p;
+    P.wk[tap] = tap;
+  }
+  P.Gh = g.Ho;
+  P.Gw = g.Wo;
+  P.s_in = g.s;
+  P.OH = g.Ho;
+  P.OW = g.Wo;
+  P.oss = 1;
+  P.out = out;
+  CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, g.Wo, t.R, t.NB, g.s);
+  CUtensorMap tb = mat_map(w, g.Co, g.K(), pick_bn(g.Co));
+  launch_any(ta, tb, P, st);
+}
+
+void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend, float *dx,
+               cudaStream_t st) {
+  // A = dz [B][Ho][Wo][Co] (stride-1 boxes), B = wT [Ci][k*k*Co], N = Ci
+  CUtensorMap tb = mat_map(wt, g.Ci, g.k * g.k * g.Co, pick_bn(g.Ci));
+  Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
+  CUtensorMap ta = act_map(dz, g.B, g.Ho, g.Wo, g.Co, g.Wo, t.R, t.NB, 1);
+  ConvTCParams P{};
+  P.M = (int)g.M();
+  P.N = g.Ci;
+  P.Cred = g.Co;
+  P.CB = g.Co / 64;
+  P.Gh = g.Ho;
+  P.Gw = g.Wo;
+  P.s_in = 1;
+  P.OH = g.H;
+  P.OW = g.W;
+  P.addend = addend;
+  P.out = dx;
+  const int k = g.k;
+  if (g.s == 1) {
+    P.ntaps = k * k;
+    for (int tap = 0; tap < k * k; ++tap) {  // dx = conv(dz, wT): wT tap index = tap
+      P.dh[tap] = tap / k - g.p;
+      P.dw[tap] = tap % k - g.p;
+      P.wk[tap] = tap;
+    }
+    P.oss = 1;
+    launch_any(ta, tb, P, st);
+    return;
+  }
+  // stride 2: phase (ph, pw) of dx gets the taps with kh = ph + p (mod 2), kw = pw + p (mod 2);
+  // dx[2i+ph][2j+pw] += dz[i + (ph+p-kh)/2][j + (pw+p-kw)/2] * w[kh][kw]
+  P.oss = 2;
+  for (int ph = 0; ph < 2; ++ph)
+    for (int pw = 0; pw < 2; ++pw) {
+      int n = 0;
+      for (int kh = 0; kh < k; ++kh)
+        for (int kw = 0; kw < k; ++kw) {
+          if (((ph + g.p - kh) & 1) || ((pw + g.p - kw) & 1)) continue;
+          P.dh[n] = (ph + g.p - kh) / 2;
+          P.dw[n] = (pw + g.p - kw) / 2;
+          P.wk[n] = (k - 1 - kh) * k + (k - 1 - kw);  // wT stores taps flipped
+          ++n;
+        }
+      if (n == 0) {
+        int64_t cnt = (int64_t)g.B * g.Ho * g.Wo * g.Ci;
+        phase_fill_kernel<<<(unsigned)std::min<int64_t>(cdiv(cnt, 256), 4 * kNumSMs), 256, 0, st>>>(
+            g.B, g.H, g.W, g.Ci, ph, pw, addend, dx);
+        PETRA_LAUNCH_CHECK();
+        continue;
+      }
+      P.ntaps = n;
+      P.ph = ph;
+      P.pw = pw;
+      launch_any(ta, tb, P, st);
+    }
+}
+
 struct WgradPlan {
-  int BN, splits, kb_per_split, n_mt, n_nt, KBtot;
+  int BN, splits, kb_per_split, n_mt, n_nt, KBtot, R, NB;
 };
 WgradPlan wgrad_plan(const ConvGeom &g) {
-  WgradPlan w;
+  WgradPlan w{};
   w.BN = g.Co % 256 == 0 ? 256 : (g.Co % 128 == 0 ? 128 : 64);
   w.n_nt = g.Co / w.BN;
   w.n_mt = (int)cdiv((int64_t)g.k * g.k * g.Ci, 128);
@@ -451,6 +549,9 @@ WgradPlan wgrad_plan(const ConvGeom &g) {
   int want = std::max(1, std::min(w.KBtot, (int)cdiv(kNumSMs, tiles)));
   w.kb_per_split = (int)cdiv(w.KBtot, want);
   w.splits = (int)cdiv(w.KBtot, w.kb_per_split);
+  Tiling t = tiling(g.B, g.Ho, g.Wo, 64);
+  w.R = t.R;
+  w.NB = t.NB;
   return w;
 }
 
@@ -471,21 +572,10 @@ void launch_wgrad(const CUtensorMap &tx, const CUtensorMap &tdz, const WgradPara
 }  // namespace
 
 bool conv_tc_supported(const ConvGeom &g, int mode) {
-  if (g.s != 1 || g.Ci % 64 || g.Co % 64) return false;
-  if (mode == 2) {
-    if (g.M() % 64 || g.Ho != g.H || g.Wo != g.W) return false;
-    Tiling t{0, 0, false};
-    if (g.W <= 64 && 64 % g.W == 0) {
-      int rows = 64 / g.W;
-      if (rows <= g.H) return g.H % rows == 0;
-      return rows % g.H == 0 && g.B % (rows / g.H) == 0;
-    }
-    (void)t;
-    return false;
-  }
-  if (g.Ho != g.H || g.Wo != g.W) return false;
-  if ((int64_t)g.B * g.H * g.W % BM) return false;
-  return tiling(g.B, g.H, g.W).ok;
+  if (!geom_ok(g)) return false;
+  if (mode == 2) return g.M() % 64 == 0 && tiling(g.B, g.Ho, g.Wo, 64).ok;
+  if (g.M() % BM) return false;
+  return tiling(g.B, g.Ho, g.Wo, BM).ok;
 }
 
 size_t conv_tc_workspace(const ConvGeom &g, int mode) {
@@ -496,30 +586,28 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode) {
 
 void conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32,
                  __nv_bfloat16 *, cudaStream_t st) {
-  run_conv(g, false, x, w, nullptr, z_f32, st);
+  run_fwd(g, x, w, z_f32, st);
 }
 
 void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend,
                    float *dx, cudaStream_t st) {
-  run_conv(g, true, dz, wt, addend, dx, st);
+  run_dgrad(g, dz, wt, addend, dx, st);
 }
 
 void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *x, float *dw, float *ws,
                    cudaStream_t st) {
   WgradPlan w = wgrad_plan(g);
-  int rows = 64 / g.W, R, NB;
-  if (rows <= g.H) { R = rows; NB = 1; } else { R = g.H; NB = rows / g.H; }
-  CUtensorMap tx = act_map(x, g.B, g.H, g.W, g.Ci, R, NB);
-  // dz as a [pixels][Co] matrix, box (64 channels, 64 pixels)
-  CUtensorMap tdz = mat_map(dz, (int)g.M(), g.Co, 64);
-  WgradParams P;
+  CUtensorMap tx = act_map(x, g.B, g.H, g.W, g.Ci, g.Wo, w.R, w.NB, g.s);
+  CUtensorMap tdz = mat_map(dz, (int)g.M(), g.Co, 64);  // dz as [pixels][Co], box (64 ch, 64 pixels)
+  WgradParams P{};
   P.Mr = g.K();
   P.N = g.Co;
   P.Ci = g.Ci;
   P.k = g.k;
   P.p = g.p;
-  P.H = g.H;
-  P.W = g.W;
+  P.s = g.s;
+  P.Gh = g.Ho;
+  P.Gw = g.Wo;
   P.KBtot = w.KBtot;
   P.kb_per_split = w.kb_per_split;
   P.n_mt = w.n_mt;
@@ -531,7 +619,7 @@ void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat
   else launch_wgrad<64, 6>(tx, tdz, P, st);
   if (w.splits > 1) {
     int64_t n = (int64_t)g.Co * g.K();
-    wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st>>>(ws, w.splits, n, dw);
+    splitk_sum_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st>>>(ws, w.splits, n, dw);
     PETRA_LAUNCH_CHECK();
   }
 }

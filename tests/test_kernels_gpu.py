@@ -43,6 +43,9 @@ GEOMS = [  # (B, H, W, Ci, Co, k, stride)
     (2, 32, 32, 64, 64, 3, 1), (2, 16, 16, 128, 128, 3, 1), (8, 8, 8, 256, 256, 3, 1),
     (8, 4, 4, 512, 512, 3, 1), (2, 16, 16, 256, 64, 1, 1), (2, 16, 16, 64, 256, 1, 1),
     (4, 8, 8, 64, 192, 3, 1),
+    # stride-2 downsampling convs (R18 DS units: 3x3/s2 Phi_s, 1x1/s2 projections)
+    (2, 32, 32, 64, 128, 3, 2), (2, 32, 32, 64, 128, 1, 2), (8, 16, 16, 128, 256, 3, 2),
+    (8, 8, 8, 256, 512, 3, 2), (8, 8, 8, 256, 512, 1, 2),
 ]
 SIMT_GEOMS = GEOMS[:2] + [(2, 9, 7, 3, 16, 3, 1), (2, 10, 10, 16, 32, 3, 2), (2, 9, 9, 8, 12, 1, 2),
                           (2, 15, 15, 3, 8, 7, 2)]
