@@ -27,9 +27,10 @@ void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat
 
 // ---------------------------------------------------------------- batch norm / coupling
 size_t bn_partial_bytes(int64_t M, int C);
+size_t bn_counter_count(int C);  // zero-initialised unsigned counters a reduction needs
 template <typename TZ>
 void bn_stats(const TZ *z, int64_t M, int C, float eps, float *mean, float *invstd, float *rmean, float *rvar,
-              float mom, double *part, cudaStream_t st);
+              float mom, double *part, unsigned *counter, cudaStream_t st);
 template <typename TZ, typename TO>
 void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean, const float *invstd,
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
@@ -38,11 +39,12 @@ template <typename TZ>
 void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float *invstd, const float *gamma,
                    const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dst_in,
                    float *dst_out, __nv_bfloat16 *dst_bf16, float *dgamma, float *dbeta, double *part,
-                   cudaStream_t st);
-template <typename TZ, typename TO>
+                   unsigned *counter, cudaStream_t st);
+// dz (fp32, nullable) and/or its bf16 copy (nullable: the tensor-core operand)
+template <typename TZ>
 void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *invstd, const float *gamma,
                const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
-               const float *dbeta, TO *dz, cudaStream_t st);
+               const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, cudaStream_t st);
 
 // ---------------------------------------------------------------- optimizer / tail / misc
 struct SgdSeg {

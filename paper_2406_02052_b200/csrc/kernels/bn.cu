@@ -1,17 +1,19 @@
 // bn.cu -- BatchNorm (training mode) + ReLU + additive coupling, HBM-streaming kernels.
 //
-//   stats    : mu_c, sigma2_c = biased batch mean / variance of z over all rows
-//              (B*H*W), invstd = 1/sqrt(sigma2+eps); optional running-stat EMA
-//              (only in the backward recomputation; reading c9).
-//   apply    : out = acc + sign * act(gamma*(z-mu)*invstd + beta)
-//              forward coupling (sign +1) / DS / stem / bottleneck
-//              inner activations.
+//   stats     : mu_c, sigma2_c = biased batch mean / variance of z over all rows
+//               (B*H*W), invstd = 1/sqrt(sigma2+eps); optional running-stat EMA
+//               (only in the backward recomputation; reading c9).
+//   apply     : out = acc + sign * act(gamma*(z-mu)*invstd + beta)
+//               forward coupling (sign +1) / DS / stem / bottleneck
+//               inner activations; optionally also writes a bf16 copy of out (the
+//               next convolution's tensor-core operand).
 //   bwd_reduce: per channel  sum g,  sum g*xhat  with g = dy * 1[out > 0]
-//              (= dbeta, dgamma), optionally fused with the reconstruction
-//              dst_out = dst_in - act(bn(z))  (approximate inversion).
-//   bwd_dz   : dz = gamma*invstd*(g - sum(g)/n - xhat*sum(g*xhat)/n).
-// All reductions are deterministic: per-block fp64 partials merged in a fixed
-// order by a finalize kernel (no float atomics).
+//               (= dbeta, dgamma), optionally fused with the reconstruction
+//               dst_out = dst_in - act(bn(z))  (approximate inversion).
+//   bwd_dz    : dz = gamma*invstd*(g - sum(g)/n - xhat*sum(g*xhat)/n).
+// Deterministic: per-block fp64 partials, merged in a fixed order by the last
+// block to finish (atomic ticket after a fence) -- one launch per reduction, no
+// float atomics.  Streaming passes move 4 channels per thread (16-byte accesses).
 #include "../kernels.h"
 
 namespace petra {
@@ -22,69 +24,243 @@ __device__ __forceinline__ float ldv(const __nv_bfloat16 *p, int64_t i) { return
 __device__ __forceinline__ void stv(float *p, int64_t i, float v) { p[i] = v; }
 __device__ __forceinline__ void stv(__nv_bfloat16 *p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
 
-constexpr int RT = 256;  // threads per reduce block: 32 channels x 8 row-warps
+__device__ __forceinline__ float4 ld4(const float *p, int64_t i) { return *reinterpret_cast<const float4 *>(p + i); }
+__device__ __forceinline__ float4 ld4(const __nv_bfloat16 *p, int64_t i) {
+  uint2 u = *reinterpret_cast<const uint2 *>(p + i);
+  __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162 *>(&u.x), b = *reinterpret_cast<__nv_bfloat162 *>(&u.y);
+  float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+  return make_float4(fa.x, fa.y, fb.x, fb.y);
+}
+__device__ __forceinline__ void st4(float *p, int64_t i, float4 v) { *reinterpret_cast<float4 *>(p + i) = v; }
+__device__ __forceinline__ void st4(__nv_bfloat16 *p, int64_t i, float4 v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t *>(&a);
+  u.y = *reinterpret_cast<uint32_t *>(&b);
+  *reinterpret_cast<uint2 *>(p + i) = u;
+}
+__device__ __forceinline__ float f4(const float4 &v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
 
-inline int reduce_row_blocks(int64_t M, int C) {
-  int ctiles = (int)cdiv(C, 32);
-  int64_t want = std::max<int64_t>(1, (4 * kNumSMs) / ctiles);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(want, cdiv(M, 32)));
+// reduction blocks: one wave of NT-thread blocks (stats 1024, backward reduce 512:
+// >= 64 KB of loads in flight per SM)
+constexpr int RT_STATS = 1024, RT_BWD = 512;
+
+// Reduction geometry: a block covers a tile of CT channels (TPR threads per row,
+// 4 channels each; RG = 256/TPR row groups) and a contiguous chunk of rpb rows.
+struct RedGeom {
+  int CT, TPR, RG, ctiles, nrb;
+  int64_t rpb;
+};
+inline RedGeom red_geom(int64_t M, int C, int RT) {
+  RedGeom g;
+  if (C % 4 == 0) {
+    g.CT = std::min(C, 128);
+    while (C % g.CT) g.CT -= 4;  // a multiple of 4 dividing C
+    g.TPR = g.CT / 4;
+  } else {
+    g.CT = 32;
+    g.TPR = 32;
+  }
+  g.RG = RT / g.TPR;
+  g.ctiles = (int)cdiv(C, g.CT);
+  int64_t want = std::max<int64_t>(1, kNumSMs / g.ctiles);  // one wave: few partials to merge
+  g.nrb = (int)std::max<int64_t>(1, std::min<int64_t>(want, cdiv(M, 4 * g.RG)));
+  g.rpb = cdiv(M, g.nrb);
+  g.nrb = (int)cdiv(M, g.rpb);
+  return g;
 }
 
-template <typename TZ>
-__global__ void __launch_bounds__(RT) bn_stats_partial_kernel(const TZ *__restrict__ z, int64_t M, int C,
-                                                              int64_t rows_per_blk, double *__restrict__ part) {
-  __shared__ double sh[2][8][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c = blockIdx.y * 32 + lane;
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_blk;
-  const int64_t r1 = min(M, r0 + rows_per_blk);
-  double s = 0.0, ss = 0.0;
-  if (c < C) {
-    for (int64_t r = r0 + w; r < r1; r += 8) {
-      double v = (double)ldv(z, r * C + c);
-      s += v;
-      ss += v * v;
+// dy(m, c): single [M][C] tensor, or split halves dy0 = channels [0, cs), dy1 = [cs, C)
+__device__ __forceinline__ float load_dy(const float *dy0, const float *dy1, int cs, int C, int64_t m, int c) {
+  if (dy1 == nullptr) return dy0[m * C + c];
+  return c < cs ? dy0[m * cs + c] : dy1[m * (C - cs) + (c - cs)];
+}
+__device__ __forceinline__ float4 load_dy4(const float *dy0, const float *dy1, int cs, int C, int64_t m, int c) {
+  if (dy1 == nullptr) return ld4(dy0, m * C + c);
+  return c < cs ? ld4(dy0, m * cs + c) : ld4(dy1, m * (C - cs) + (c - cs));
+}
+
+// Block-level fixed-order combine of per-thread sums (row groups) into this
+// block's partial part[blk][c][0..1]; sh is a [RT][4] double scratch, used for one
+// quantity at a time.
+template <int RT>
+__device__ __forceinline__ void write_partial(double (*sh)[4], const double *a, const double *b, bool vec, int TPR,
+                                              int RG, int c0, int C, double *part) {
+  const int t = threadIdx.x;
+  const int nslots = vec ? TPR * 4 : TPR;
+  for (int q = 0; q < 2; ++q) {
+    const double *src = q == 0 ? a : b;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sh[t][k] = src[k];
+    __syncthreads();
+    for (int slot = t; slot < nslots; slot += RT) {
+      int cjs = vec ? slot / 4 : slot, k = vec ? slot % 4 : 0;
+      int cc = vec ? c0 + 4 * cjs + k : c0 + cjs;
+      if (cc >= C) continue;
+      double x = 0;
+      for (int g = 0; g < RG; ++g) x += sh[g * TPR + cjs][k];
+      part[((int64_t)blockIdx.x * C + cc) * 2 + q] = x;
     }
   }
-  sh[0][w][lane] = s;
-  sh[1][w][lane] = ss;
+}
+
+// true in exactly one block per channel tile: the last to finish its partial
+__device__ __forceinline__ bool last_block(unsigned *counter, int nrb) {
+  __shared__ unsigned ticket;
+  __threadfence();
   __syncthreads();
-  if (w == 0 && c < C) {
-    double a = 0.0, b = 0.0;
+  if (threadIdx.x == 0) ticket = atomicAdd(&counter[blockIdx.y], 1u);
+  __syncthreads();
+  if (ticket != (unsigned)(nrb - 1)) return false;
+  __threadfence();
+  return true;
+}
+
+// merge the nrb partials of channels [c0, c0+CT) in a fixed order: RT/CT threads
+// per channel over fixed strided subsets (4 L2-coherent 16-byte loads in flight),
+// then a fixed-order shared-memory combine.  Result valid in threads t < CT.
+template <int RT>
+__device__ __forceinline__ void merge_tile(const double *part, int nrb, int C, int c0, int CT, double (*sh)[4],
+                                           double &a, double &b) {
+  const int t = threadIdx.x;
+  const int per = RT / CT;
+  const int cl = t % CT, sub = t / CT;
+  const int c = c0 + cl;
+  double2 acc[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  if (sub < per && c < C) {
+    const double2 *p2 = reinterpret_cast<const double2 *>(part);
+    int i = sub;
+    for (; i + 3 * per < nrb; i += 4 * per) {
+      double2 v[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { a += sh[0][i][lane]; b += sh[1][i][lane]; }
-    part[((int64_t)blockIdx.x * C + c) * 2 + 0] = a;
-    part[((int64_t)blockIdx.x * C + c) * 2 + 1] = b;
+      for (int u = 0; u < 4; ++u) v[u] = __ldcg(p2 + (int64_t)(i + u * per) * C + c);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc[u].x += v[u].x;
+        acc[u].y += v[u].y;
+      }
+    }
+    for (; i < nrb; i += per) {
+      double2 v = __ldcg(p2 + (int64_t)i * C + c);
+      acc[0].x += v.x;
+      acc[0].y += v.y;
+    }
   }
+  __syncthreads();
+  sh[t][0] = (acc[0].x + acc[1].x) + (acc[2].x + acc[3].x);
+  sh[t][1] = (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y);
+  __syncthreads();
+  a = 0;
+  b = 0;
+  if (t < CT)
+    for (int k = 0; k < per; ++k) {
+      a += sh[k * CT + t][0];
+      b += sh[k * CT + t][1];
+    }
 }
 
-__global__ void bn_stats_finalize_kernel(const double *__restrict__ part, int nrb, int C, int64_t M,
-                                         float eps, float *__restrict__ mean, float *__restrict__ invstd,
-                                         float *__restrict__ rmean, float *__restrict__ rvar, float mom) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double s = 0.0, ss = 0.0;
-  for (int i = 0; i < nrb; ++i) {
-    s += part[((int64_t)i * C + c) * 2 + 0];
-    ss += part[((int64_t)i * C + c) * 2 + 1];
+// ---------------------------------------------------------------- stats
+template <typename TZ>
+__global__ void __launch_bounds__(RT_STATS) bn_stats_kernel(const TZ *__restrict__ z, int64_t M, int C, int CT, int TPR,
+                                                      int RG, int64_t rpb, int nrb, double *__restrict__ part,
+                                                      unsigned *__restrict__ counter, float eps,
+                                                      float *__restrict__ mean, float *__restrict__ invstd,
+                                                      float *__restrict__ rmean, float *__restrict__ rvar,
+                                                      float mom) {
+  constexpr int RT = RT_STATS;
+  __shared__ double sh[RT][4];
+  const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
+  const int c0 = blockIdx.y * CT;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(M, r0 + rpb);
+  double s[4] = {0, 0, 0, 0}, ss[4] = {0, 0, 0, 0};
+  const bool vec = (C % 4 == 0);
+  const int c = vec ? c0 + 4 * cj : c0 + cj;
+  if (c < C && rgi < RG && vec) {
+    int64_t r = r0 + rgi;
+    for (; r + 3 * RG < r1; r += 4 * RG) {  // 4 independent 16-byte loads in flight
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = ld4(z, (r + u * RG) * C + c);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          double d = f4(v[u], k);
+          s[k] += d;
+          ss[k] += d * d;
+        }
+    }
+    for (; r < r1; r += RG) {
+      float4 v = ld4(z, r * C + c);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double d = f4(v, k);
+        s[k] += d;
+        ss[k] += d * d;
+      }
+    }
+  } else if (c < C && rgi < RG) {
+    for (int64_t r = r0 + rgi; r < r1; r += RG) {
+      {
+        double d = ldv(z, r * C + c);
+        s[0] += d;
+        ss[0] += d * d;
+      }
+    }
   }
-  double mu = s / (double)M;
-  double var = ss / (double)M - mu * mu;
-  if (var < 0.0) var = 0.0;
-  mean[c] = (float)mu;
-  invstd[c] = (float)(1.0 / sqrt(var + (double)eps));
-  if (rmean) {
-    double unb = M > 1 ? var * (double)M / (double)(M - 1) : var;
-    rmean[c] = (float)((1.0 - mom) * rmean[c] + mom * mu);
-    rvar[c] = (float)((1.0 - mom) * rvar[c] + mom * unb);
+  write_partial<RT>(sh, s, ss, vec, TPR, RG, c0, C, part);
+  if (!last_block(counter, nrb)) return;
+  double su, sq;
+  merge_tile<RT>(part, nrb, C, c0, CT, sh, su, sq);
+  const int ch = c0 + t;
+  if (t < CT && ch < C) {
+    double mu = su / (double)M;
+    double var = sq / (double)M - mu * mu;
+    if (var < 0.0) var = 0.0;
+    mean[ch] = (float)mu;
+    invstd[ch] = (float)(1.0 / sqrt(var + (double)eps));
+    if (rmean) {
+      double unb = M > 1 ? var * (double)M / (double)(M - 1) : var;
+      rmean[ch] = (float)((1.0 - mom) * rmean[ch] + mom * mu);
+      rvar[ch] = (float)((1.0 - mom) * rvar[ch] + mom * unb);
+    }
   }
+  if (t == 0) counter[blockIdx.y] = 0u;  // ready for the next launch
 }
 
+// ---------------------------------------------------------------- apply
 template <typename TZ, typename TO>
 __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int ldz, int zc0,
                                 const float *__restrict__ mean, const float *__restrict__ invstd,
                                 const float *__restrict__ gamma, const float *__restrict__ beta, int relu,
                                 float sign, const float *acc, TO *out, __nv_bfloat16 *out_bf16) {
+  const bool vec = (C % 4 == 0) && (ldz % 4 == 0) && (zc0 % 4 == 0);
+  if (vec) {
+    const int C4 = C / 4;
+    const int64_t n = M * C4;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      int64_t m = i / C4;
+      int c = (int)(i - m * C4) * 4;
+      int cz = zc0 + c;
+      float4 zv = ld4(z, m * ldz + cz);
+      float4 o;
+      float *op = &o.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float y = fmaf(gamma[cz + k] * invstd[cz + k], f4(zv, k) - mean[cz + k], beta[cz + k]);
+        if (relu) y = y > 0.f ? y : 0.f;
+        op[k] = sign * y;
+      }
+      if (acc) {
+        float4 a = ld4(acc, m * C + c);
+        o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
+      }
+      st4(out, m * C + c, o);
+      if (out_bf16) st4(out_bf16, m * C + c, o);
+    }
+    return;
+  }
   const int64_t n = M * C;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t m = i / C;
@@ -99,76 +275,136 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
   }
 }
 
-// dy(m, c): single [M][C] tensor, or split halves dy0 = channels [0, cs), dy1 = [cs, C)
-__device__ __forceinline__ float load_dy(const float *dy0, const float *dy1, int cs, int C, int64_t m, int c) {
-  if (dy1 == nullptr) return dy0[m * C + c];
-  return c < cs ? dy0[m * cs + c] : dy1[m * (C - cs) + (c - cs)];
-}
-
+// ---------------------------------------------------------------- backward reduce (+ reconstruction)
 template <typename TZ>
-__global__ void __launch_bounds__(RT) bn_bwd_reduce_kernel(
-    const TZ *__restrict__ z, int64_t M, int C, const float *__restrict__ mean, const float *__restrict__ invstd,
-    const float *__restrict__ gamma, const float *__restrict__ beta, int relu, const float *dy0, const float *dy1,
-    int cs, const float *dst_in, float *dst_out, __nv_bfloat16 *dst_bf16, int64_t rows_per_blk,
-    double *__restrict__ part) {
-  __shared__ double sh[2][8][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c = blockIdx.y * 32 + lane;
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_blk;
-  const int64_t r1 = min(M, r0 + rows_per_blk);
-  double sg = 0.0, sgx = 0.0;
-  if (c < C) {
-    const float mu = mean[c], is = invstd[c], ga = gamma[c], be = beta[c];
-    for (int64_t r = r0 + w; r < r1; r += 8) {
-      float xh = (ldv(z, r * C + c) - mu) * is;
-      float y = fmaf(ga, xh, be);
-      float g = load_dy(dy0, dy1, cs, C, r, c);
-      if (relu) {
-        if (!(y > 0.f)) g = 0.f;
-        y = y > 0.f ? y : 0.f;
+__global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
+    const TZ *__restrict__ z, int64_t M, int C, int CT, int TPR, int RG, int64_t rpb, int nrb,
+    const float *__restrict__ mean, const float *__restrict__ invstd, const float *__restrict__ gamma,
+    const float *__restrict__ beta, int relu, const float *dy0, const float *dy1, int cs, const float *dst_in,
+    float *dst_out, __nv_bfloat16 *dst_bf16, double *__restrict__ part, unsigned *__restrict__ counter,
+    float *__restrict__ dgamma, float *__restrict__ dbeta) {
+  constexpr int RT = RT_BWD;
+  __shared__ double sh[RT][4];
+  const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
+  const int c0 = blockIdx.y * CT;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(M, r0 + rpb);
+  double sg[4] = {0, 0, 0, 0}, sgx[4] = {0, 0, 0, 0};
+  const bool vec = (C % 4 == 0) && (dy1 == nullptr || cs % 4 == 0);
+  const int c = vec ? c0 + 4 * cj : c0 + cj;
+  if (c < C && rgi < RG) {
+    if (vec) {
+      float mu[4], is[4], ga[4], be[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        mu[k] = mean[c + k];
+        is[k] = invstd[c + k];
+        ga[k] = gamma[c + k];
+        be[k] = beta[c + k];
       }
-      if (dst_out) {
-        float o = dst_in[r * C + c] - y;   // reconstruct: dst - Phi(src)
-        dst_out[r * C + c] = o;
-        if (dst_bf16) dst_bf16[r * C + c] = __float2bfloat16_rn(o);
+      auto row = [&](int64_t r, const float4 &zv, float4 g4, float4 d4) {
+        float *gp = &g4.x, *dp = &d4.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float xh = (f4(zv, k) - mu[k]) * is[k];
+          float y = fmaf(ga[k], xh, be[k]);
+          float g = gp[k];
+          if (relu) {
+            if (!(y > 0.f)) g = 0.f;
+            y = y > 0.f ? y : 0.f;
+          }
+          dp[k] -= y;
+          sg[k] += (double)g;
+          sgx[k] += (double)g * (double)xh;
+        }
+        if (dst_out) {
+          st4(dst_out, r * C + c, d4);
+          if (dst_bf16) st4(dst_bf16, r * C + c, d4);
+        }
+      };
+      int64_t r = r0 + rgi;
+      for (; r + 3 * RG < r1; r += 4 * RG) {  // all loads of 4 rows first
+        float4 zv[4], g4[4], d4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t ru = r + u * RG;
+          zv[u] = ld4(z, ru * C + c);
+          g4[u] = load_dy4(dy0, dy1, cs, C, ru, c);
+          d4[u] = dst_out ? ld4(dst_in, ru * C + c) : make_float4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) row(r + u * RG, zv[u], g4[u], d4[u]);
       }
-      sg += (double)g;
-      sgx += (double)g * (double)xh;
+      for (; r < r1; r += RG) {
+        float4 zv = ld4(z, r * C + c);
+        float4 g4 = load_dy4(dy0, dy1, cs, C, r, c);
+        float4 d4 = dst_out ? ld4(dst_in, r * C + c) : make_float4(0, 0, 0, 0);
+        row(r, zv, g4, d4);
+      }
+    } else {
+      const float mu = mean[c], is = invstd[c], ga = gamma[c], be = beta[c];
+      for (int64_t r = r0 + rgi; r < r1; r += RG) {
+        float xh = (ldv(z, r * C + c) - mu) * is;
+        float y = fmaf(ga, xh, be);
+        float g = load_dy(dy0, dy1, cs, C, r, c);
+        if (relu) {
+          if (!(y > 0.f)) g = 0.f;
+          y = y > 0.f ? y : 0.f;
+        }
+        if (dst_out) {
+          float o = dst_in[r * C + c] - y;
+          dst_out[r * C + c] = o;
+          if (dst_bf16) dst_bf16[r * C + c] = __float2bfloat16_rn(o);
+        }
+        sg[0] += (double)g;
+        sgx[0] += (double)g * (double)xh;
+      }
     }
   }
-  sh[0][w][lane] = sg;
-  sh[1][w][lane] = sgx;
-  __syncthreads();
-  if (w == 0 && c < C) {
-    double a = 0.0, b = 0.0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) { a += sh[0][i][lane]; b += sh[1][i][lane]; }
-    part[((int64_t)blockIdx.x * C + c) * 2 + 0] = a;
-    part[((int64_t)blockIdx.x * C + c) * 2 + 1] = b;
+  write_partial<RT>(sh, sg, sgx, vec, TPR, RG, c0, C, part);
+  if (!last_block(counter, nrb)) return;
+  double a, b;
+  merge_tile<RT>(part, nrb, C, c0, CT, sh, a, b);
+  const int ch = c0 + t;
+  if (t < CT && ch < C) {
+    dbeta[ch] = (float)a;
+    dgamma[ch] = (float)b;
   }
+  if (t == 0) counter[blockIdx.y] = 0u;
 }
 
-__global__ void bn_bwd_finalize_kernel(const double *__restrict__ part, int nrb, int C,
-                                       float *__restrict__ dgamma, float *__restrict__ dbeta) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double a = 0.0, b = 0.0;
-  for (int i = 0; i < nrb; ++i) {
-    a += part[((int64_t)i * C + c) * 2 + 0];
-    b += part[((int64_t)i * C + c) * 2 + 1];
-  }
-  dbeta[c] = (float)a;
-  dgamma[c] = (float)b;
-}
-
-template <typename TZ, typename TO>
+// ---------------------------------------------------------------- dz
+template <typename TZ>
 __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, const float *__restrict__ mean,
                                  const float *__restrict__ invstd, const float *__restrict__ gamma,
                                  const float *__restrict__ beta, int relu, const float *dy0, const float *dy1,
                                  int cs, const float *__restrict__ dgamma, const float *__restrict__ dbeta,
-                                 TO *__restrict__ dz) {
-  const int64_t n = M * C;
+                                 float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16) {
   const float invM = 1.0f / (float)M;
+  const bool vec = (C % 4 == 0) && (dy1 == nullptr || cs % 4 == 0);
+  if (vec) {
+    const int C4 = C / 4;
+    const int64_t n = M * C4;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      int64_t m = i / C4;
+      int c = (int)(i - m * C4) * 4;
+      float4 zv = ld4(z, m * C + c);
+      float4 g4 = load_dy4(dy0, dy1, cs, C, m, c);
+      float4 o;
+      float *op = &o.x, *gp = &g4.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float is = invstd[c + k];
+        float xh = (f4(zv, k) - mean[c + k]) * is;
+        float g = gp[k];
+        if (relu && !(fmaf(gamma[c + k], xh, beta[c + k]) > 0.f)) g = 0.f;
+        op[k] = gamma[c + k] * is * (g - dbeta[c + k] * invM - xh * dgamma[c + k] * invM);
+      }
+      if (dz) st4(dz, m * C + c, o);
+      if (dz_bf16) st4(dz_bf16, m * C + c, o);
+    }
+    return;
+  }
+  const int64_t n = M * C;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t m = i / C;
     int c = (int)(i - m * C);
@@ -177,7 +413,8 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
     float g = load_dy(dy0, dy1, cs, C, m, c);
     if (relu && !(fmaf(gamma[c], xh, beta[c]) > 0.f)) g = 0.f;
     float v = gamma[c] * is * (g - dbeta[c] * invM - xh * dgamma[c] * invM);
-    stv(dz, i, v);
+    if (dz) stv(dz, i, v);
+    if (dz_bf16) dz_bf16[i] = __float2bfloat16_rn(v);
   }
 }
 
@@ -187,32 +424,30 @@ inline unsigned ew_grid(int64_t n) {
 
 }  // namespace
 
-size_t bn_partial_bytes(int64_t M, int C) { return (size_t)reduce_row_blocks(M, C) * C * 2 * sizeof(double); }
+size_t bn_partial_bytes(int64_t M, int C) {
+  return (size_t)std::max(red_geom(M, C, RT_STATS).nrb, red_geom(M, C, RT_BWD).nrb) * C * 2 * sizeof(double);
+}
+size_t bn_counter_count(int C) { return (size_t)red_geom(1 << 20, C, RT_BWD).ctiles; }
 
 template <typename TZ>
 void bn_stats(const TZ *z, int64_t M, int C, float eps, float *mean, float *invstd, float *rmean, float *rvar,
-              float mom, double *part, cudaStream_t st) {
-  int nrb = reduce_row_blocks(M, C);
-  int64_t rpb = cdiv(M, nrb);
-  nrb = (int)cdiv(M, rpb);
-  dim3 grid(nrb, (unsigned)cdiv(C, 32));
-  bn_stats_partial_kernel<TZ><<<grid, RT, 0, st>>>(z, M, C, rpb, part);
-  PETRA_LAUNCH_CHECK();
-  bn_stats_finalize_kernel<<<(unsigned)cdiv(C, 128), 128, 0, st>>>(part, nrb, C, M, eps, mean, invstd, rmean,
-                                                                   rvar, mom);
+              float mom, double *part, unsigned *counter, cudaStream_t st) {
+  RedGeom g = red_geom(M, C, RT_STATS);
+  bn_stats_kernel<TZ><<<dim3(g.nrb, g.ctiles), RT_STATS, 0, st>>>(z, M, C, g.CT, g.TPR, g.RG, g.rpb, g.nrb, part, counter,
+                                                            eps, mean, invstd, rmean, rvar, mom);
   PETRA_LAUNCH_CHECK();
 }
 template void bn_stats<float>(const float *, int64_t, int, float, float *, float *, float *, float *, float,
-                              double *, cudaStream_t);
+                              double *, unsigned *, cudaStream_t);
 template void bn_stats<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int, float, float *, float *, float *,
-                                      float *, float, double *, cudaStream_t);
+                                      float *, float, double *, unsigned *, cudaStream_t);
 
 template <typename TZ, typename TO>
 void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean, const float *invstd,
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
               __nv_bfloat16 *out_bf16, cudaStream_t st) {
-  bn_apply_kernel<TZ, TO><<<ew_grid(M * C), 256, 0, st>>>(M, C, z, ldz, zc0, mean, invstd, gamma, beta, relu,
-                                                          sign, acc, out, out_bf16);
+  bn_apply_kernel<TZ, TO><<<ew_grid(M * C / 4), 256, 0, st>>>(M, C, z, ldz, zc0, mean, invstd, gamma, beta, relu,
+                                                              sign, acc, out, out_bf16);
   PETRA_LAUNCH_CHECK();
 }
 template void bn_apply<float, float>(int64_t, int, const float *, int, int, const float *, const float *,
@@ -221,54 +456,39 @@ template void bn_apply<float, float>(int64_t, int, const float *, int, int, cons
 template void bn_apply<__nv_bfloat16, float>(int64_t, int, const __nv_bfloat16 *, int, int, const float *,
                                              const float *, const float *, const float *, int, float,
                                              const float *, float *, __nv_bfloat16 *, cudaStream_t);
-template void bn_apply<float, __nv_bfloat16>(int64_t, int, const float *, int, int, const float *,
-                                             const float *, const float *, const float *, int, float,
-                                             const float *, __nv_bfloat16 *, __nv_bfloat16 *, cudaStream_t);
-template void bn_apply<__nv_bfloat16, __nv_bfloat16>(int64_t, int, const __nv_bfloat16 *, int, int,
-                                                     const float *, const float *, const float *,
-                                                     const float *, int, float, const float *,
-                                                     __nv_bfloat16 *, __nv_bfloat16 *, cudaStream_t);
 
 template <typename TZ>
 void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float *invstd, const float *gamma,
                    const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dst_in,
                    float *dst_out, __nv_bfloat16 *dst_bf16, float *dgamma, float *dbeta, double *part,
-                   cudaStream_t st) {
-  int nrb = reduce_row_blocks(M, C);
-  int64_t rpb = cdiv(M, nrb);
-  nrb = (int)cdiv(M, rpb);
-  dim3 grid(nrb, (unsigned)cdiv(C, 32));
-  bn_bwd_reduce_kernel<TZ><<<grid, RT, 0, st>>>(z, M, C, mean, invstd, gamma, beta, relu, dy0, dy1, cs, dst_in,
-                                                dst_out, dst_bf16, rpb, part);
-  PETRA_LAUNCH_CHECK();
-  bn_bwd_finalize_kernel<<<(unsigned)cdiv(C, 128), 128, 0, st>>>(part, nrb, C, dgamma, dbeta);
+                   unsigned *counter, cudaStream_t st) {
+  RedGeom g = red_geom(M, C, RT_BWD);
+  bn_bwd_reduce_kernel<TZ><<<dim3(g.nrb, g.ctiles), RT_BWD, 0, st>>>(z, M, C, g.CT, g.TPR, g.RG, g.rpb, g.nrb, mean,
+                                                                 invstd, gamma, beta, relu, dy0, dy1, cs, dst_in,
+                                                                 dst_out, dst_bf16, part, counter, dgamma, dbeta);
   PETRA_LAUNCH_CHECK();
 }
 template void bn_bwd_reduce<float>(const float *, int64_t, int, const float *, const float *, const float *,
                                    const float *, int, const float *, const float *, int, const float *, float *,
-                                   __nv_bfloat16 *, float *, float *, double *, cudaStream_t);
+                                   __nv_bfloat16 *, float *, float *, double *, unsigned *, cudaStream_t);
 template void bn_bwd_reduce<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int, const float *, const float *,
                                            const float *, const float *, int, const float *, const float *, int,
                                            const float *, float *, __nv_bfloat16 *, float *, float *, double *,
-                                           cudaStream_t);
+                                           unsigned *, cudaStream_t);
 
-template <typename TZ, typename TO>
+template <typename TZ>
 void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *invstd, const float *gamma,
                const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
-               const float *dbeta, TO *dz, cudaStream_t st) {
-  bn_bwd_dz_kernel<TZ, TO><<<ew_grid(M * C), 256, 0, st>>>(M, C, z, mean, invstd, gamma, beta, relu, dy0, dy1,
-                                                           cs, dgamma, dbeta, dz);
+               const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, cudaStream_t st) {
+  bn_bwd_dz_kernel<TZ><<<ew_grid(M * C / 4), 256, 0, st>>>(M, C, z, mean, invstd, gamma, beta, relu, dy0, dy1, cs,
+                                                           dgamma, dbeta, dz, dz_bf16);
   PETRA_LAUNCH_CHECK();
 }
-template void bn_bwd_dz<float, float>(int64_t, int, const float *, const float *, const float *, const float *,
-                                      const float *, int, const float *, const float *, int, const float *,
-                                      const float *, float *, cudaStream_t);
-template void bn_bwd_dz<__nv_bfloat16, __nv_bfloat16>(int64_t, int, const __nv_bfloat16 *, const float *,
-                                                      const float *, const float *, const float *, int,
-                                                      const float *, const float *, int, const float *,
-                                                      const float *, __nv_bfloat16 *, cudaStream_t);
-template void bn_bwd_dz<float, __nv_bfloat16>(int64_t, int, const float *, const float *, const float *,
-                                              const float *, const float *, int, const float *, const float *,
-                                              int, const float *, const float *, __nv_bfloat16 *, cudaStream_t);
+template void bn_bwd_dz<float>(int64_t, int, const float *, const float *, const float *, const float *,
+                               const float *, int, const float *, const float *, int, const float *, const float *,
+                               float *, __nv_bfloat16 *, cudaStream_t);
+template void bn_bwd_dz<__nv_bfloat16>(int64_t, int, const __nv_bfloat16 *, const float *, const float *,
+                                       const float *, const float *, int, const float *, const float *, int,
+                                       const float *, const float *, float *, __nv_bfloat16 *, cudaStream_t);
 
 }  // namespace petra

@@ -331,27 +331,33 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
 }
 
 __global__ void splitk_sum_kernel(const float *__restrict__ part, int splits, int64_t n, float *__restrict__ out) {
+  // 4 independent accumulators (4 loads in flight), combined in a fixed order: deterministic
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];  // fixed order: deterministic
-    out[i] = s;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int z = 0;
+    for (; z + 3 < splits; z += 4) {
+      s0 += part[(int64_t)z * n + i];
+      s1 += part[(int64_t)(z + 1) * n + i];
+      s2 += part[(int64_t)(z + 2) * n + i];
+      s3 += part[(int64_t)(z + 3) * n + i];
+    }
+    for (; z < splits; ++z) s0 += part[(int64_t)z * n + i];
+    out[i] = (s0 + s1) + (s2 + s3);
   }
 }
 
-// out[pixels of phase (ph, pw)] = addend (or 0): the stride-2 dgrad phases without taps
-__global__ void phase_fill_kernel(int B, int OH, int OW, int C, int ph, int pw, const float *__restrict__ addend,
+// out = addend (or 0) on every pixel (h, w) whose phase bit (h&1)*2 + (w&1) is set
+// in `mask`: the stride-2 dgrad phases without taps, all in one launch (float4)
+__global__ void phase_fill_kernel(int B, int OH, int OW, int C, int mask, const float *__restrict__ addend,
                                   float *__restrict__ out) {
-  const int Gh = (OH - ph + 1) / 2, Gw = (OW - pw + 1) / 2;
-  const int64_t n = (int64_t)B * Gh * Gw * C;
+  const int C4 = C / 4;
+  const int64_t n = (int64_t)B * OH * OW * C4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)(i % C);
-    int64_t g = i / C;
-    int j = (int)(g % Gw);
-    int64_t r = g / Gw;
-    int ii = (int)(r % Gh);
-    int b = (int)(r / Gh);
-    int64_t o = (((int64_t)b * OH + 2 * ii + ph) * OW + 2 * j + pw) * C + c;
-    out[o] = addend ? addend[o] : 0.f;
+    int64_t pix = i / C4;
+    int w = (int)(pix % OW), h = (int)((pix / OW) % OH);
+    if (!((mask >> ((h & 1) * 2 + (w & 1))) & 1)) continue;
+    float4 v = addend ? reinterpret_cast<const float4 *>(addend)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    reinterpret_cast<float4 *>(out)[i] = v;
   }
 }
 
@@ -511,6 +517,7 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *
   // stride 2: phase (ph, pw) of dx gets the taps with kh = ph + p (mod 2), kw = pw + p (mod 2);
   // dx[2i+ph][2j+pw] += dz[i + (ph+p-kh)/2][j + (pw+p-kw)/2] * w[kh][kw]
   P.oss = 2;
+  int empty_mask = 0;
   for (int ph = 0; ph < 2; ++ph)
     for (int pw = 0; pw < 2; ++pw) {
       int n = 0;
@@ -522,11 +529,8 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *
           P.wk[n] = (k - 1 - kh) * k + (k - 1 - kw);  // wT stores taps flipped
           ++n;
         }
-      if (n == 0) {
-        int64_t cnt = (int64_t)g.B * g.Ho * g.Wo * g.Ci;
-        phase_fill_kernel<<<(unsigned)std::min<int64_t>(cdiv(cnt, 256), 4 * kNumSMs), 256, 0, st>>>(
-            g.B, g.H, g.W, g.Ci, ph, pw, addend, dx);
-        PETRA_LAUNCH_CHECK();
+      if (n == 0) {  // no tap reaches this phase (1x1 / stride 2): dx = addend or 0 there
+        empty_mask |= 1 << (ph * 2 + pw);
         continue;
       }
       P.ntaps = n;
@@ -534,6 +538,12 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *
       P.pw = pw;
       launch_any(ta, tb, P, st);
     }
+  if (empty_mask) {
+    int64_t cnt = (int64_t)g.B * g.H * g.W * (g.Ci / 4);
+    phase_fill_kernel<<<(unsigned)std::min<int64_t>(cdiv(cnt, 256), 8 * kNumSMs), 256, 0, st>>>(
+        g.B, g.H, g.W, g.Ci, empty_mask, addend, dx);
+    PETRA_LAUNCH_CHECK();
+  }
 }
 
 struct WgradPlan {

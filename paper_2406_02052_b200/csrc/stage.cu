@@ -236,6 +236,10 @@ void Stage::build() {
                                   : conv_wgrad_simt_workspace(p.L->g));
   }
   part_ = dalloc(std::max<size_t>(max_part, 16));
+  size_t max_ctr = 1;
+  for (auto &p : layers) max_ctr = std::max(max_ctr, bn_counter_count(p.L->g.Co));
+  counters_ = dalloc(max_ctr * sizeof(unsigned));
+  PETRA_CUDA(cudaMemset(counters_->p, 0, max_ctr * sizeof(unsigned)));
   wgrad_ws_ = dalloc(std::max<size_t>(max_ws, 16));
   nonfinite_ = dalloc(sizeof(int));
   PETRA_CUDA(cudaMemset(nonfinite_->p, 0, sizeof(int)));
@@ -386,12 +390,15 @@ static double conv_bytes(const ConvGeom &g, int esz) {
   return (double)esz * ((double)g.Min() * g.Ci + (double)g.Co * g.K()) + 4.0 * (double)g.M() * g.Co;
 }
 
-void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st) {
+void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready) {
   const float *w = theta_->as<float>() + L.w_off;
   bool tc = tc_ && conv_tc_supported(L.g, 0);
+  if (tc && !x_bf16_ready) {  // bf16 operand of a stream input (also read by the TC wgrad)
+    ProfScope pc("cvt_bf16", st, 0.0, 6.0 * (double)L.g.Min() * L.g.Ci);
+    f32_to_bf16(x, L.xb->as<__nv_bfloat16>(), L.g.Min() * L.g.Ci, st);
+  }
   ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    f32_to_bf16(x, L.xb->as<__nv_bfloat16>(), L.g.Min() * L.g.Ci, st);
     conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->as<float>(), nullptr, st);
   } else {
     conv_fwd_simt(L.g, x, w, L.z->as<float>(), st);
@@ -403,8 +410,8 @@ void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   bool tc = tc_ && conv_tc_supported(L.g, 2);
   ProfScope ps(tc ? "conv_wgrad_tc" : "conv_wgrad_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    // L.xb holds bf16(x) from the conv_fwd of this tick (forward or recomputation)
-    f32_to_bf16(L.dz->as<float>(), L.dzb->as<__nv_bfloat16>(), L.g.M() * L.g.Co, st);
+    // L.xb holds bf16(x) from the conv_fwd of this tick (forward or recomputation);
+    // L.dzb was written in bf16 by bn_bwd_dz
     conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.xb->as<__nv_bfloat16>(), dw, wgrad_ws_->as<float>(), st);
   } else {
     conv_wgrad_simt(L.g, L.dz->as<float>(), x, dw, wgrad_ws_->as<float>(), st);
@@ -415,8 +422,6 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
   bool tc = tc_ && conv_tc_supported(L.g, 1);
   ProfScope ps(tc ? "conv_dgrad_tc" : "conv_dgrad_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    if (!conv_tc_supported(L.g, 2))  // dz bf16 not produced by wgrad path
-      f32_to_bf16(L.dz->as<float>(), L.dzb->as<__nv_bfloat16>(), L.g.M() * L.g.Co, st);
     conv_dgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.wt_bf16->as<__nv_bfloat16>(), addend, out, st);
   } else {
     conv_dgrad_simt(L.g, L.dz->as<float>(), theta_->as<float>() + L.w_off, addend, out, st);
@@ -428,21 +433,25 @@ void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
   float *b = bufs_->as<float>();
   bn_stats<float>(L.z->as<float>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean->as<float>(), L.invstd->as<float>(),
                   running ? b + L.rm_off : nullptr, running ? b + L.rv_off : nullptr, desc_.bn_momentum,
-                  part_->as<double>(), st);
+                  part_->as<double>(), counters_->as<unsigned>(), st);
 }
 
 // forward of a conv-BN-ReLU chain on x; inner activations into L.a; the last
 // layer's z / stats are left for the caller's fused epilogue.
 void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running, cudaStream_t st) {
   const float *th = theta_->as<float>();
+  bool ready = false;
   for (size_t l = 0; l < phi.size(); ++l) {
     Layer &L = phi[l];
-    conv_fwd(L, x, st);
+    conv_fwd(L, x, st, ready);
     layer_stats(L, running, st);
     if (l + 1 < phi.size()) {
-      apply_bn(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
-                             L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr, L.a->as<float>(),
-                             nullptr, st);
+      // inner activation; its bf16 copy is written straight into the next layer's operand
+      Layer &N = phi[l + 1];
+      ready = tc_ && conv_tc_supported(N.g, 0);
+      apply_bn(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(), L.invstd->as<float>(),
+               th + L.g_off, th + L.b_off, 1, 1.f, nullptr, L.a->as<float>(),
+               ready ? N.xb->as<__nv_bfloat16>() : nullptr, st);
       x = L.a->as<float>();
     }
   }
@@ -460,12 +469,15 @@ void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, cons
   ProfScope ps("bn_bwd_reduce", st, 0.0, 4.0 * n * (dst_out ? 4 : 2));
   bn_bwd_reduce<float>(L.z->as<float>(), L.g.M(), L.g.Co, L.mean->as<float>(), L.invstd->as<float>(),
                        th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, dst_in, dst_out, nullptr,
-                       gr + L.g_off, gr + L.b_off, part_->as<double>(), st);
+                       gr + L.g_off, gr + L.b_off, part_->as<double>(), counters_->as<unsigned>(), st);
   }
-  ProfScope ps("bn_bwd_dz", st, 0.0, 12.0 * n);
-  bn_bwd_dz<float, float>(L.g.M(), L.g.Co, L.z->as<float>(), L.mean->as<float>(), L.invstd->as<float>(),
-                          th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off,
-                          L.dz->as<float>(), st);
+  // dz in bf16 for tensor-core dgrad / wgrad, in fp32 only if a SIMT pass consumes it
+  const bool tc_d = tc_ && conv_tc_supported(L.g, 1), tc_w = tc_ && conv_tc_supported(L.g, 2);
+  float *dz32 = (!tc_d || !tc_w) ? L.dz->as<float>() : nullptr;
+  __nv_bfloat16 *dz16 = (tc_d || tc_w) ? L.dzb->as<__nv_bfloat16>() : nullptr;
+  ProfScope ps("bn_bwd_dz", st, 0.0, 8.0 * n + (dz32 ? 4.0 : 0.0) * n + (dz16 ? 2.0 : 0.0) * n);
+  bn_bwd_dz<float>(L.g.M(), L.g.Co, L.z->as<float>(), L.mean->as<float>(), L.invstd->as<float>(), th + L.g_off,
+                   th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off, dz32, dz16, st);
 }
 
 // VJP through a branch whose last layer receives dy (reconstruction fused when

@@ -109,7 +109,7 @@ class Stage {
   std::vector<SgdSeg> segs_;
   DevPtr segs_dev_;
   int64_t max_seg_ = 0;
-  DevPtr part_, wgrad_ws_;
+  DevPtr part_, wgrad_ws_, counters_;
   DevPtr nonfinite_;
   // tail workspace
   DevPtr feat_, logits_, dlogits_, lossrow_, dfeat_, tail_d_[2];
@@ -127,7 +127,7 @@ class Stage {
   void update(float lr, cudaStream_t st);
 
   // kernels of one layer / unit
-  void conv_fwd(Layer &L, const float *x, cudaStream_t st);
+  void conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready = false);
   void conv_wgrad(Layer &L, const float *x, cudaStream_t st);
   void conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t st);
   void layer_stats(Layer &L, bool running, cudaStream_t st);
