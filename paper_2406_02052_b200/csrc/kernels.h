@@ -14,13 +14,13 @@ void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *
 
 // ---------------------------------------------------------------- tcgen05 bf16 convolutions
 bool conv_tc_supported(const ConvGeom &g, int mode);   // mode 0 fwd, 1 dgrad, 2 wgrad
-size_t conv_tc_workspace(const ConvGeom &g, int mode);
+size_t conv_tc_workspace(const ConvGeom &g, int mode);  // split-K workspace bytes
 // z[m][co] (fp32 or bf16 out) = conv(x_bf16, w_bf16)
 void conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32,
-                 __nv_bfloat16 *z_bf16, cudaStream_t st);
+                 __nv_bfloat16 *z_bf16, float *ws, cudaStream_t st);
 // dx (fp32) = addend + conv^T(dz_bf16, wT_bf16)
 void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend,
-                   float *dx, cudaStream_t st);
+                   float *dx, float *ws, cudaStream_t st);
 // dw (fp32) = sum_pixels dz (x) x
 void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *x, float *dw, float *ws,
                    cudaStream_t st);

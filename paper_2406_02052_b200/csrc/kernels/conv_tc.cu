@@ -42,6 +42,8 @@ struct ConvTCParams {
   int Gh, Gw;                // output grid of the GEMM (rows x cols per image)
   int s_in;                  // A row coordinate = s_in * grid_row + dh
   int OH, OW, oss, ph, pw;   // grid (i, j) -> output pixel (i*oss+ph, j*oss+pw) of an OH x OW image
+  int splits, kb_per_split;  // split-K (small-M layers): splits > 1 -> partials into ws[split][M][N]
+  float *ws;
   const float *addend;
   float *out;                // [B*OH*OW][N]
 };
@@ -62,9 +64,18 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_n = P.N / BN;
-  const int n_tiles = (P.M / BM) * n_tiles_n;
+  const int n_work = (P.M / BM) * n_tiles_n * P.splits;  // (m tile, n tile, K split)
   const int KB = P.ntaps * P.CB;
   const int GHW = P.Gh * P.Gw;
+  // work item -> tile coordinates and K-block range
+  auto decode = [&](int w, int &mt, int &nt, int &sp, int &kb0, int &kb1) {
+    sp = w % P.splits;
+    const int tile = w / P.splits;
+    mt = tile / n_tiles_n;
+    nt = tile % n_tiles_n;
+    kb0 = sp * P.kb_per_split;
+    kb1 = min(KB, kb0 + P.kb_per_split);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -89,11 +100,12 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int mt = tile / n_tiles_n, nt = tile % n_tiles_n;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        int mt, nt, sp, kb0, kb1;
+        decode(w, mt, nt, sp, kb0, kb1);
         const int m0 = mt * BM;
         const int b0 = m0 / GHW, i0 = (m0 % GHW) / P.Gw;
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           const int t = kb / P.CB, cb = kb % P.CB;
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * STAGE_BYTES;
@@ -110,12 +122,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+        int mt, nt, sp, kb0, kb1;
+        decode(w, mt, nt, sp, kb0, kb1);
         const int acc = it & 1;
         tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc::tc_fence_after();
         const uint32_t dtm = tmem_base + acc * BN;
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&full[stage], phase);
           tc::tc_fence_after();
           const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
@@ -123,7 +137,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const uint64_t bd = tc::sw128_desc(sa + A_BYTES, 16, 1024);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // advance 32 B (16 bf16) along K inside the swizzle row
-            tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           tc::umma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -134,16 +148,23 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
     int it = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      int mt, nt, sp, kb0, kb1;
+      decode(w, mt, nt, sp, kb0, kb1);
       const int acc = it & 1;
-      const int mt = tile / n_tiles_n, nt = tile % n_tiles_n;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
       const int m = mt * BM + row;
-      const int b = m / GHW, r = m % GHW, i = r / P.Gw, j = r % P.Gw;
-      const int64_t opix = ((int64_t)b * P.OH + i * P.oss + P.ph) * P.OW + j * P.oss + P.pw;
-      float *orow = P.out + opix * P.N + nt * BN;
-      const float *arow = P.addend ? P.addend + opix * P.N + nt * BN : nullptr;
+      float *orow;
+      const float *arow = nullptr;
+      if (P.splits > 1) {  // partial of this K split, GEMM-row order; reduced by splitk_out_kernel
+        orow = P.ws + ((int64_t)sp * P.M + m) * P.N + nt * BN;
+      } else {
+        const int b = m / GHW, r = m % GHW, i = r / P.Gw, j = r % P.Gw;
+        const int64_t opix = ((int64_t)b * P.OH + i * P.oss + P.ph) * P.OW + j * P.oss + P.pw;
+        orow = P.out + opix * P.N + nt * BN;
+        arow = P.addend ? P.addend + opix * P.N + nt * BN : nullptr;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         float v[16];
@@ -168,6 +189,28 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+// out[opix(m)][n] = addend + sum over splits of ws[s][m][n]  (fixed order: deterministic)
+__global__ void splitk_out_kernel(const ConvTCParams P) {
+  const int N4 = P.N / 4;
+  const int64_t n = (int64_t)P.M * N4;
+  const int GHW = P.Gh * P.Gw;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / N4), c = (int)(i % N4) * 4;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int z = 0; z < P.splits; ++z) {
+      float4 v = *reinterpret_cast<const float4 *>(P.ws + ((int64_t)z * P.M + m) * P.N + c);
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    const int b = m / GHW, r = m % GHW, ii = r / P.Gw, jj = r % P.Gw;
+    const int64_t o = (((int64_t)b * P.OH + ii * P.oss + P.ph) * P.OW + jj * P.oss + P.pw) * P.N + c;
+    if (P.addend) {
+      float4 a = *reinterpret_cast<const float4 *>(P.addend + o);
+      s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
+    }
+    *reinterpret_cast<float4 *>(P.out + o) = s;
   }
 }
 
@@ -430,6 +473,29 @@ Tiling tiling(int B, int Gh, int Gw, int rows_per_tile) {
 
 int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64); }
 
+// N tile and K split for a conv GEMM: the largest N tile that still fills a wave
+// of SMs; below that, BN = 64 and a split of K (deterministic workspace reduction).
+struct ConvPlan {
+  int BN, splits, kb_per_split;
+};
+ConvPlan conv_plan(int M, int N, int KB) {
+  ConvPlan p{64, 1, KB};
+  const int mt = M / BM;
+  for (int bn : {256, 128, 64}) {
+    if (N % bn) continue;
+    p.BN = bn;
+    if (mt * (N / bn) >= kNumSMs) break;
+  }
+  const int tiles = mt * (N / p.BN);
+  if (tiles * 4 < kNumSMs * 3) {  // under 75% of one wave: split K
+    int want = std::max(1, (kNumSMs + tiles / 2) / tiles);
+    want = std::min(want, std::max(1, KB / 4));  // at least 4 K-blocks per split
+    p.kb_per_split = (int)cdiv(KB, want);
+    p.splits = (int)cdiv(KB, p.kb_per_split);
+  }
+  return p;
+}
+
 template <int BN, int STAGES>
 void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P, cudaStream_t st) {
   size_t smem = (size_t)STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256;
@@ -439,15 +505,30 @@ void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParam
                                     (int)smem));
     attr = true;
   }
-  int tiles = (P.M / BM) * (P.N / BN);
-  conv_tc_kernel<BN, STAGES><<<std::min(tiles, kNumSMs), kThreads, smem, st>>>(ta, tb, P);
+  int work = (P.M / BM) * (P.N / BN) * P.splits;
+  conv_tc_kernel<BN, STAGES><<<std::min(work, kNumSMs), kThreads, smem, st>>>(ta, tb, P);
   PETRA_LAUNCH_CHECK();
+  if (P.splits > 1) {
+    int64_t n = (int64_t)P.M * P.N / 4;
+    splitk_out_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs), 256, 0, st>>>(P);
+    PETRA_LAUNCH_CHECK();
+  }
 }
 
-void launch_any(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P, cudaStream_t st) {
-  const int BN = pick_bn(P.N);
-  if (BN == 256) launch_conv<256, 4>(ta, tb, P, st);
-  else if (BN == 128) launch_conv<128, 5>(ta, tb, P, st);
+// tensor maps are built per launch (host-side, ~1 us); B's box height = BN
+void launch_any(const CUtensorMap &ta, const __nv_bfloat16 *w, int wrows, int wK, ConvTCParams &P, float *ws,
+                cudaStream_t st) {
+  ConvPlan pl = conv_plan(P.M, P.N, P.ntaps * P.CB);
+  P.splits = pl.splits;
+  P.kb_per_split = pl.kb_per_split;
+  P.ws = ws;
+  if (pl.splits > 1 && !ws) {
+    P.splits = 1;
+    P.kb_per_split = P.ntaps * P.CB;
+  }
+  CUtensorMap tb = mat_map(w, wrows, wK, pl.BN);
+  if (pl.BN == 256) launch_conv<256, 4>(ta, tb, P, st);
+  else if (pl.BN == 128) launch_conv<128, 5>(ta, tb, P, st);
   else launch_conv<64, 6>(ta, tb, P, st);
 }
 
@@ -459,7 +540,8 @@ bool geom_ok(const ConvGeom &g) {
   return true;
 }
 
-void run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *out, cudaStream_t st) {
+void run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *out, float *ws,
+             cudaStream_t st) {
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
   ConvTCParams P{};
   P.M = (int)g.M();
@@ -480,14 +562,13 @@ void run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, 
   P.oss = 1;
   P.out = out;
   CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, g.Wo, t.R, t.NB, g.s);
-  CUtensorMap tb = mat_map(w, g.Co, g.K(), pick_bn(g.Co));
-  launch_any(ta, tb, P, st);
+  launch_any(ta, w, g.Co, g.K(), P, ws, st);
 }
 
 void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend, float *dx,
-               cudaStream_t st) {
+               float *ws, cudaStream_t st) {
   // A = dz [B][Ho][Wo][Co] (stride-1 boxes), B = wT [Ci][k*k*Co], N = Ci
-  CUtensorMap tb = mat_map(wt, g.Ci, g.k * g.k * g.Co, pick_bn(g.Ci));
+  const int wK = g.k * g.k * g.Co;
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
   CUtensorMap ta = act_map(dz, g.B, g.Ho, g.Wo, g.Co, g.Wo, t.R, t.NB, 1);
   ConvTCParams P{};
@@ -511,7 +592,7 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *
       P.wk[tap] = tap;
     }
     P.oss = 1;
-    launch_any(ta, tb, P, st);
+    launch_any(ta, wt, g.Ci, wK, P, ws, st);
     return;
   }
   // stride 2: phase (ph, pw) of dx gets the taps with kh = ph + p (mod 2), kw = pw + p (mod 2);
@@ -536,7 +617,7 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *
       P.ntaps = n;
       P.ph = ph;
       P.pw = pw;
-      launch_any(ta, tb, P, st);
+      launch_any(ta, wt, g.Ci, wK, P, ws, st);
     }
   if (empty_mask) {
     int64_t cnt = (int64_t)g.B * g.H * g.W * (g.Ci / 4);
@@ -589,19 +670,25 @@ bool conv_tc_supported(const ConvGeom &g, int mode) {
 }
 
 size_t conv_tc_workspace(const ConvGeom &g, int mode) {
-  if (mode != 2 || !conv_tc_supported(g, 2)) return 0;
-  WgradPlan w = wgrad_plan(g);
-  return w.splits > 1 ? (size_t)w.splits * g.Co * g.K() * sizeof(float) : 0;
+  if (!conv_tc_supported(g, mode)) return 0;
+  if (mode == 2) {
+    WgradPlan w = wgrad_plan(g);
+    return w.splits > 1 ? (size_t)w.splits * g.Co * g.K() * sizeof(float) : 0;
+  }
+  const int N = mode == 0 ? g.Co : g.Ci;
+  const int KB = (mode == 0 ? g.k * g.k * g.Ci : g.k * g.k * g.Co) / 64;  // upper bound (all taps)
+  ConvPlan p = conv_plan((int)g.M(), N, KB);
+  return p.splits > 1 ? (size_t)p.splits * g.M() * N * sizeof(float) : 0;
 }
 
 void conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32,
-                 __nv_bfloat16 *, cudaStream_t st) {
-  run_fwd(g, x, w, z_f32, st);
+                 __nv_bfloat16 *, float *ws, cudaStream_t st) {
+  run_fwd(g, x, w, z_f32, ws, st);
 }
 
 void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend,
-                   float *dx, cudaStream_t st) {
-  run_dgrad(g, dz, wt, addend, dx, st);
+                   float *dx, float *ws, cudaStream_t st) {
+  run_dgrad(g, dz, wt, addend, dx, ws, st);
 }
 
 void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *x, float *dw, float *ws,

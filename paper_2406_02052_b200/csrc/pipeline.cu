@@ -46,6 +46,13 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
   }
   int j0 = sched_.first_local(), j1 = sched_.last_local();
   if (j1 < 1) throw PetraError(PETRA_E_ARG, "rank owns no stage");
+  streams_.assign(J_ + 2, nullptr);
+  done_.assign(J_ + 2, nullptr);
+  for (int j = j0; j <= j1; ++j) {
+    PETRA_CUDA(cudaStreamCreateWithFlags(&streams_[j], cudaStreamNonBlocking));
+    PETRA_CUDA(cudaEventCreateWithFlags(&done_[j], cudaEventDisableTiming));
+  }
+  PETRA_CUDA(cudaEventCreateWithFlags(&start_, cudaEventDisableTiming));
   for (int p = 0; p < 2; ++p) {
     if (j0 > 1) {
       const Shape &in = stages_[j0]->in_shape();
@@ -60,6 +67,14 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
   }
 }
 
+Pipeline::~Pipeline() {
+  for (auto s : streams_)
+    if (s) cudaStreamDestroy(s);
+  for (auto e : done_)
+    if (e) cudaEventDestroy(e);
+  if (start_) cudaEventDestroy(start_);
+}
+
 static float *fp(const DevPtr &p) { return p ? p->as<float>() : nullptr; }
 
 void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labels, float lr, float *loss,
@@ -67,9 +82,13 @@ void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labe
   std::vector<int64_t> ver, fifo;
   std::vector<Schedule::Step> steps = sched_.tick(t, inject, &ver, &fifo);
   const int p = (int)(t & 1), q = p ^ 1;
+  const cudaStream_t caller = st;
+  PETRA_CUDA(cudaEventRecord(start_, caller));  // fork: everything before this tick is visible
   for (int j = 1; j <= J_; ++j) {
     if (!sched_.local(j)) continue;
     Stage &s = *stages_[j];
+    st = streams_[j];
+    PETRA_CUDA(cudaStreamWaitEvent(st, start_, 0));
     const Schedule::Step &sp = steps[j];
     // ---- forward input message
     const float *in1 = nullptr, *in2 = nullptr;
@@ -104,7 +123,10 @@ void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labe
       Msg &o = bwd_[j][p];
       s.tail((uint64_t)sp.fwd_mb, in1, in2, lab, lr, fp(o.x[0]), fp(o.x[1]), fp(o.x[2]), fp(o.x[3]), loss, st);
     }
+    PETRA_CUDA(cudaEventRecord(done_[j], st));
   }
+  for (int j = 1; j <= J_; ++j)  // join: the caller's stream sees the whole tick
+    if (sched_.local(j)) PETRA_CUDA(cudaStreamWaitEvent(caller, done_[j], 0));
   if (rep) {
     rep->tick = t;
     rep->n_stages = J_;

@@ -28,6 +28,14 @@ class Pipeline {
   std::vector<std::unique_ptr<Stage>> stages_;
   std::vector<std::array<Msg, 2>> fwd_, bwd_;  // [j][parity]: outputs of local stage j
   Msg ghost_fwd_[2], ghost_bwd_[2];            // receive buffers for remote neighbours
+  // one stream per local stage: the stages of a tick are independent (they only
+  // read mailboxes of the previous tick), so their kernels overlap on the GPU
+  std::vector<cudaStream_t> streams_;
+  std::vector<cudaEvent_t> done_;
+  cudaEvent_t start_ = nullptr;
+
+ public:
+  ~Pipeline();
 };
 
 }  // namespace petra

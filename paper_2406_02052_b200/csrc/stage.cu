@@ -232,8 +232,9 @@ void Stage::build() {
   }
   for (auto &p : layers) {
     max_part = std::max(max_part, bn_partial_bytes(p.L->g.M(), p.L->g.Co));
-    max_ws = std::max(max_ws, tc_ ? std::max(conv_tc_workspace(p.L->g, 2), conv_wgrad_simt_workspace(p.L->g))
-                                  : conv_wgrad_simt_workspace(p.L->g));
+    max_ws = std::max(max_ws, conv_wgrad_simt_workspace(p.L->g));
+    if (tc_)
+      for (int mode = 0; mode < 3; ++mode) max_ws = std::max(max_ws, conv_tc_workspace(p.L->g, mode));
   }
   part_ = dalloc(std::max<size_t>(max_part, 16));
   size_t max_ctr = 1;
@@ -399,7 +400,8 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
   }
   ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->as<float>(), nullptr, st);
+    conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->as<float>(), nullptr,
+                wgrad_ws_->as<float>(), st);
   } else {
     conv_fwd_simt(L.g, x, w, L.z->as<float>(), st);
   }
@@ -422,7 +424,8 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
   bool tc = tc_ && conv_tc_supported(L.g, 1);
   ProfScope ps(tc ? "conv_dgrad_tc" : "conv_dgrad_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    conv_dgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.wt_bf16->as<__nv_bfloat16>(), addend, out, st);
+    conv_dgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.wt_bf16->as<__nv_bfloat16>(), addend, out,
+                  wgrad_ws_->as<float>(), st);
   } else {
     conv_dgrad_simt(L.g, L.dz->as<float>(), theta_->as<float>() + L.w_off, addend, out, st);
   }
