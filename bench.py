@@ -167,6 +167,8 @@ def run_ours(a):
     st = torch.cuda.current_stream()
     t = 0
 
+    host_ms = []
+
     def tick(flush_l2=False, ev=None):
         nonlocal t
         i = t % ring
@@ -174,8 +176,10 @@ def run_ours(a):
             flush.fill_(t & 0xFF)
         if ev:
             ev[0].record(st)
+        h0 = time.perf_counter()
         pipe.tick(t, True, xs[i] if owns_first else None, ys[i] if owns_first else None, lr, loss, report=False)
         if ev:
+            host_ms.append((time.perf_counter() - h0) * 1e3)
             ev[1].record(st)
         if tr:
             tr.exchange(t)
@@ -238,6 +242,13 @@ def run_ours(a):
     e2e = {"value": B * a.steps / (float(ems.item()) / 1e3), "unit": "samples/s",
            "h2d_bytes_per_step": (B * H * H * 3 * 4 + B * 4) if owns_first else 0, "d2h_bytes_per_step": 4}
 
+    # ---- per-stage device time per tick (events around each stage's work on its stream)
+    pipe.timing(True)
+    for _ in range(a.steps):
+        tick()
+    stage_ms = [round(x, 4) for x in pipe.stage_ms()]
+    pipe.timing(False)
+
     # ---- per-kernel device time (profiled replay of K more steps: CUDA events on the launch stream)
     L.profile(True)
     for _ in range(a.steps):
@@ -278,9 +289,11 @@ def run_ours(a):
                       "stage_rank": stage_rank, "parallelism": f"petra-stages{J}-over-{world}gpu",
                       "precision_requested": a.precision, "lr": lr, "fill_ticks": 2 * J - 2,
                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                      "wall_s_timed": round(wall, 3)},
+                      "wall_s_timed": round(wall, 3),
+                      "host_enqueue_ms_per_step": round(statistics.median(host_ms), 4) if host_ms else None},
            "roofline": roof, "gpu_launches": launches, "clocks": clk, "e2e": e2e,
-           "kernels": kernels[:12], "algorithmic_gflop_per_step": round(conv_flops / 1e9, 2)}
+           "kernels": kernels[:12], "algorithmic_gflop_per_step": round(conv_flops / 1e9, 2),
+           "stage_ms_per_tick": stage_ms}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         dt, threads = oracle_tick_seconds(a.model, B if a.model != "revnet50" else 4, J, counts)
         bb = B if a.model != "revnet50" else 4

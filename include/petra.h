@@ -245,6 +245,13 @@ typedef struct {
 } petra_comm_plan;
 petra_status petra_pipeline_comm(petra_pipeline *p, int64_t t, petra_comm_plan *plan);
 
+/* Per-stage device time: enable != 0 starts recording CUDA events around each
+ * local stage's work of every tick (on the stage's stream); petra_pipeline_stage_ms
+ * synchronises and returns, per stage j = 1..J (0 for non-local stages), the
+ * summed milliseconds and the number of ticks recorded since enabling. */
+petra_status petra_pipeline_timing(petra_pipeline *p, int32_t enable);
+petra_status petra_pipeline_stage_ms(petra_pipeline *p, float *ms, int32_t n, int32_t *ticks);
+
 /* ------------------------------------------------------------------ schedule (host only)
  * The integer bookkeeping petra_pipeline_tick runs, exposed without any device
  * work so the multi-rank routing can be tested on CPU (gloo) and compared

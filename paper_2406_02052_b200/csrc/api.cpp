@@ -206,6 +206,19 @@ petra_status petra_pipeline_comm(petra_pipeline *p, int64_t t, petra_comm_plan *
   return guard([&] { p->p->comm(t, plan); });
 }
 
+petra_status petra_pipeline_timing(petra_pipeline *p, int32_t enable) {
+  if (!p) return fail(PETRA_E_ARG, "NULL pipeline");
+  return guard([&] { p->p->timing(enable != 0); });
+}
+
+petra_status petra_pipeline_stage_ms(petra_pipeline *p, float *ms, int32_t n, int32_t *ticks) {
+  if (!p || !ms) return fail(PETRA_E_ARG, "NULL argument");
+  return guard([&] {
+    int t = p->p->stage_ms(ms, n);
+    if (ticks) *ticks = t;
+  });
+}
+
 petra_status petra_schedule_create(int32_t n, const int32_t *stage_rank, const int32_t *nonrev, int32_t rank,
                                    petra_schedule **out) {
   if (!stage_rank || !nonrev || !out || n < 1) return fail(PETRA_E_ARG, "bad schedule arguments");

@@ -16,6 +16,7 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
   int64_t nx = g.Min() * g.Ci, nz = g.M() * g.Co, nw = (int64_t)g.Co * g.K();
   int64_t na = mode == 0 ? nx : nz, nb = mode == 2 ? nx : nw, no = mode == 0 ? nz : (mode == 1 ? nx : nw);
   if (engine == 1 && !conv_tc_supported(g, mode)) return PETRA_E_UNSUPPORTED;
+  if (engine == 1) conv_tc_prepare();
   DevPtr da = dalloc(na * 4), db = dalloc(nb * 4), dout = dalloc(no * 4), dadd;
   PETRA_CUDA(cudaMemcpy(da->p, a, na * 4, cudaMemcpyHostToDevice));
   PETRA_CUDA(cudaMemcpy(db->p, b, nb * 4, cudaMemcpyHostToDevice));
@@ -48,8 +49,8 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     }
     f32_to_bf16(db->as<float>(), bb->as<__nv_bfloat16>(), nb, st);
     DevPtr ws = dalloc(std::max<size_t>(16, conv_tc_workspace(g, mode)));
-    if (mode == 0) conv_fwd_tc(g, ab->as<__nv_bfloat16>(), bb->as<__nv_bfloat16>(), dout->as<float>(), nullptr, ws->as<float>(),
-                            st);
+    if (mode == 0) conv_fwd_tc(g, ab->as<__nv_bfloat16>(), bb->as<__nv_bfloat16>(), dout->as<float>(), ws->as<float>(),
+                            nullptr, st);
     else if (mode == 1)
       conv_dgrad_tc(g, ab->as<__nv_bfloat16>(), bb->as<__nv_bfloat16>(), addend ? dadd->as<float>() : nullptr,
                     dout->as<float>(), ws->as<float>(), st);

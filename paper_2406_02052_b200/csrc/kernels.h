@@ -14,10 +14,15 @@ void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *
 
 // ---------------------------------------------------------------- tcgen05 bf16 convolutions
 bool conv_tc_supported(const ConvGeom &g, int mode);   // mode 0 fwd, 1 dgrad, 2 wgrad
+void conv_tc_prepare();  // one-time kernel attributes (before any graph capture)
 size_t conv_tc_workspace(const ConvGeom &g, int mode);  // split-K workspace bytes
-// z[m][co] (fp32 or bf16 out) = conv(x_bf16, w_bf16)
-void conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32,
-                 __nv_bfloat16 *z_bf16, float *ws, cudaStream_t st);
+// z[m][co] (fp32) = conv(x_bf16, w_bf16).  stats_part (nullable, >= 148*4*Co*2 floats):
+// the epilogue also writes BN partial sums of z; returns the number of partial rows
+// to merge with bn_stats_from_partials (0 = not fused, run bn_stats on z).
+int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32, float *ws,
+                float *stats_part, cudaStream_t st);
+void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float eps, float *mean, float *invstd,
+                            float *rmean, float *rvar, float mom, cudaStream_t st);
 // dx (fp32) = addend + conv^T(dz_bf16, wT_bf16)
 void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend,
                    float *dx, float *ws, cudaStream_t st);
@@ -54,8 +59,10 @@ struct SgdSeg {
   __nv_bfloat16 *w_bf16;         // nullable: bf16 shadow [Co][k][k][Ci]
   __nv_bfloat16 *wt_bf16;        // nullable: dgrad operand [Ci][k][k][Co], taps flipped
 };
+// lr_dev: device scalar (written per tick from pinned host memory, so a captured
+// CUDA graph replays with the current learning rate)
 void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *theta, float *v, const float *grad,
-                float lr, float mom, float wd, int nesterov, cudaStream_t st, bool shadow_only);
+                const float *lr_dev, float mom, float wd, int nesterov, cudaStream_t st, bool shadow_only);
 void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int C, const float *w,
                            const float *bias, int N, const int32_t *labels, float *feat, float *logits,
                            float *dlogits, float *loss_row, float *dfeat, float *dw, float *db, float *d1,

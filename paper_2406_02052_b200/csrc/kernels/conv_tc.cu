@@ -32,6 +32,7 @@ constexpr int BM = 128, BK = 64;
 constexpr int kThreads = 192;  // 6 warps
 constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr int kMaxTaps = 9;
+constexpr int kMaxStatN = 512;  // widest conv output with fused BN statistics
 
 struct ConvTCParams {
   int M, N;                  // GEMM: M = pixels of the output grid, N = output channels
@@ -46,7 +47,25 @@ struct ConvTCParams {
   float *ws;
   const float *addend;
   float *out;                // [B*OH*OW][N]
+  float *stats;              // nullable: per-(CTA, epilogue warp) BN partials [grid][4][N][2] (sum, sum sq)
 };
+
+// Column sums of a 32-row x 16-column fragment held one row per lane: butterfly
+// transpose-reduce (8+4+2+1+1 shuffles).  Afterwards lane L holds the sum over the
+// 32 rows of column (L >> 1) in x[0] (lanes 2k, 2k+1 both).
+__device__ __forceinline__ void colsum16(float (&x)[16], int lane) {
+#pragma unroll
+  for (int half = 8, off = 16; half >= 1; half >>= 1, off >>= 1) {
+    const bool upper = lane & off;
+#pragma unroll
+    for (int k = 0; k < half; ++k) {
+      float send = upper ? x[k] : x[k + half];
+      float keep = upper ? x[k + half] : x[k];
+      x[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  x[0] += __shfl_xor_sync(0xffffffffu, x[0], 1);
+}
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -61,6 +80,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  float *sstat = reinterpret_cast<float *>(tmem_slot + 4);  // [4 warps][N][2] BN partial sums (fused stats)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_n = P.N / BN;
@@ -147,6 +167,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   } else {  // ---------------- epilogue warps 2..5
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
+    float *my_stat = sstat + (size_t)q * P.N * 2;
+    if (P.stats)
+      for (int i = lane; i < 2 * P.N; i += 32) my_stat[i] = 0.f;
+    __syncwarp();
     int it = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
       int mt, nt, sp, kb0, kb1;
@@ -179,16 +203,79 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
         for (int jj = 0; jj < 16; jj += 4)
           *reinterpret_cast<float4 *>(orow + c + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+        if (P.stats) {  // BN batch statistics of z, fused (sum and sum of squares per column)
+          float sq[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) sq[jj] = v[jj] * v[jj];
+          colsum16(v, lane);
+          colsum16(sq, lane);
+          if (!(lane & 1)) {
+            const int col = nt * BN + c + (lane >> 1);
+            my_stat[2 * col] += v[0];
+            my_stat[2 * col + 1] += sq[0];
+          }
+        }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+    if (P.stats) {
+      __syncwarp();
+      float *g = P.stats + ((size_t)blockIdx.x * 4 + q) * P.N * 2;
+      for (int i = lane; i < 2 * P.N; i += 32) g[i] = my_stat[i];
     }
   }
   __syncthreads();
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+// BN statistics from the fused partials: per channel, fp64 sum over the P = grid*4
+// partial rows in a fixed order (32 threads per channel x strided subsets, then a
+// fixed-order shared-memory combine); optional running-stat EMA (reading c9).
+__global__ void __launch_bounds__(256) stats_finalize_kernel(const float *__restrict__ part, int P, int N, int64_t M,
+                                                             float eps, float *__restrict__ mean,
+                                                             float *__restrict__ invstd, float *__restrict__ rmean,
+                                                             float *__restrict__ rvar, float mom) {
+  __shared__ double sh[2][32][9];
+  const int cl = threadIdx.x & 7, sub = threadIdx.x >> 3;  // 8 channels x 32 subsets per block
+  const int c = blockIdx.x * 8 + cl;
+  double a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+  if (c < N) {
+    int i = sub;
+    for (; i + 32 < P; i += 64) {
+      float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)i * N + c) * 2);
+      float2 v = *reinterpret_cast<const float2 *>(part + ((size_t)(i + 32) * N + c) * 2);
+      a0 += u.x; b0 += u.y;
+      a1 += v.x; b1 += v.y;
+    }
+    if (i < P) {
+      float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)i * N + c) * 2);
+      a0 += u.x; b0 += u.y;
+    }
+  }
+  sh[0][sub][cl] = a0 + a1;
+  sh[1][sub][cl] = b0 + b1;
+  __syncthreads();
+  if (sub == 0 && c < N) {
+    double s = 0, ss = 0;
+    for (int k = 0; k < 32; ++k) {
+      s += sh[0][k][cl];
+      ss += sh[1][k][cl];
+    }
+    double mu = s / (double)M;
+    double var = ss / (double)M - mu * mu;
+    if (var < 0.0) var = 0.0;
+    mean[c] = (float)mu;
+    invstd[c] = (float)(1.0 / sqrt(var + (double)eps));
+    if (rmean) {
+      double unb = M > 1 ? var * (double)M / (double)(M - 1) : var;
+      rmean[c] = (float)((1.0 - mom) * rmean[c] + mom * mu);
+      rvar[c] = (float)((1.0 - mom) * rvar[c] + mom * unb);
+    }
   }
 }
 
@@ -498,13 +585,8 @@ ConvPlan conv_plan(int M, int N, int KB) {
 
 template <int BN, int STAGES>
 void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P, cudaStream_t st) {
-  size_t smem = (size_t)STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    PETRA_CUDA(cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-    attr = true;
-  }
+  // attribute set by conv_tc_prepare; + fused-stats area [4][N][2] floats
+  size_t smem = (size_t)STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256 + (P.stats ? (size_t)P.N * 32 : 0);
   int work = (P.M / BM) * (P.N / BN) * P.splits;
   conv_tc_kernel<BN, STAGES><<<std::min(work, kNumSMs), kThreads, smem, st>>>(ta, tb, P);
   PETRA_LAUNCH_CHECK();
@@ -526,6 +608,7 @@ void launch_any(const CUtensorMap &ta, const __nv_bfloat16 *w, int wrows, int wK
     P.splits = 1;
     P.kb_per_split = P.ntaps * P.CB;
   }
+  if (P.splits > 1 || P.N > kMaxStatN) P.stats = nullptr;  // stats need final z (split-K: standalone pass)
   CUtensorMap tb = mat_map(w, wrows, wK, pl.BN);
   if (pl.BN == 256) launch_conv<256, 4>(ta, tb, P, st);
   else if (pl.BN == 128) launch_conv<128, 5>(ta, tb, P, st);
@@ -540,8 +623,8 @@ bool geom_ok(const ConvGeom &g) {
   return true;
 }
 
-void run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *out, float *ws,
-             cudaStream_t st) {
+int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *out, float *ws, float *stats,
+            cudaStream_t st) {
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
   ConvTCParams P{};
   P.M = (int)g.M();
@@ -561,8 +644,12 @@ void run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, 
   P.OW = g.Wo;
   P.oss = 1;
   P.out = out;
+  P.stats = stats;
   CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, g.Wo, t.R, t.NB, g.s);
   launch_any(ta, w, g.Co, g.K(), P, ws, st);
+  if (!P.stats) return 0;
+  const int BN = conv_plan(P.M, P.N, P.ntaps * P.CB).BN;
+  return std::min((P.M / BM) * (P.N / BN) * P.splits, kNumSMs) * 4;  // partial rows written
 }
 
 void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend, float *dx,
@@ -648,19 +735,33 @@ WgradPlan wgrad_plan(const ConvGeom &g) {
 
 template <int BN, int STAGES>
 void launch_wgrad(const CUtensorMap &tx, const CUtensorMap &tdz, const WgradParams &P, cudaStream_t st) {
-  size_t smem = (size_t)STAGES * (2 * 64 * 64 * 2 + BN * 64 * 2) + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    PETRA_CUDA(cudaFuncSetAttribute(wgrad_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-    attr = true;
-  }
+  size_t smem = (size_t)STAGES * (2 * 64 * 64 * 2 + BN * 64 * 2) + 1024 + 256;  // attribute: conv_tc_prepare
   int work = P.n_mt * P.n_nt * P.splits;
   wgrad_tc_kernel<BN, STAGES><<<std::min(work, kNumSMs), kThreads, smem, st>>>(tx, tdz, P);
   PETRA_LAUNCH_CHECK();
 }
 
 }  // namespace
+
+void conv_tc_prepare() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto set = [](const void *f, int STAGES, int BN) {
+      size_t smem = (size_t)STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256 + kMaxStatN * 32;
+      PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    };
+    set((const void *)conv_tc_kernel<256, 4>, 4, 256);
+    set((const void *)conv_tc_kernel<128, 5>, 5, 128);
+    set((const void *)conv_tc_kernel<64, 6>, 6, 64);
+    auto setw = [](const void *f, int STAGES, int BN) {
+      size_t smem = (size_t)STAGES * (2 * 64 * 64 * 2 + BN * 64 * 2) + 1024 + 256;
+      PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    };
+    setw((const void *)wgrad_tc_kernel<256, 3>, 3, 256);
+    setw((const void *)wgrad_tc_kernel<128, 4>, 4, 128);
+    setw((const void *)wgrad_tc_kernel<64, 6>, 6, 64);
+  });
+}
 
 bool conv_tc_supported(const ConvGeom &g, int mode) {
   if (!geom_ok(g)) return false;
@@ -681,9 +782,15 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode) {
   return p.splits > 1 ? (size_t)p.splits * g.M() * N * sizeof(float) : 0;
 }
 
-void conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32,
-                 __nv_bfloat16 *, float *ws, cudaStream_t st) {
-  run_fwd(g, x, w, z_f32, ws, st);
+int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32, float *ws,
+                float *stats_part, cudaStream_t st) {
+  return run_fwd(g, x, w, z_f32, ws, stats_part, st);
+}
+
+void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float eps, float *mean, float *invstd,
+                            float *rmean, float *rvar, float mom, cudaStream_t st) {
+  stats_finalize_kernel<<<(unsigned)cdiv(N, 8), 256, 0, st>>>(part, P, N, M, eps, mean, invstd, rmean, rvar, mom);
+  PETRA_LAUNCH_CHECK();
 }
 
 void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend,

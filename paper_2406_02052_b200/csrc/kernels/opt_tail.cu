@@ -15,11 +15,12 @@ namespace petra {
 namespace {
 
 __global__ void sgd_kernel(const SgdSeg *__restrict__ segs, float *__restrict__ theta, float *__restrict__ v,
-                           const float *__restrict__ grad, float lr, float mom, float wd, int nesterov,
-                           int shadow_only) {
+                           const float *__restrict__ grad, const float *__restrict__ lr_dev, float mom, float wd,
+                           int nesterov, int shadow_only) {
   const SgdSeg sg = segs[blockIdx.y];
   if (shadow_only && !sg.w_bf16) return;
   const float lam = sg.decay ? wd : 0.f;
+  const float lr = shadow_only ? 0.f : *lr_dev;  // device-resident: graph replays read the tick's lr
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sg.count; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t o = sg.offset + i;
     float th = theta[o];
@@ -237,9 +238,9 @@ inline unsigned ew_grid(int64_t n) {
 }  // namespace
 
 void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *theta, float *v, const float *grad,
-                float lr, float mom, float wd, int nesterov, cudaStream_t st, bool shadow_only) {
+                const float *lr_dev, float mom, float wd, int nesterov, cudaStream_t st, bool shadow_only) {
   dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(max_count, 256), 2 * kNumSMs)), nseg);
-  sgd_kernel<<<grid, 256, 0, st>>>(segs_dev, theta, v, grad, lr, mom, wd, nesterov, shadow_only ? 1 : 0);
+  sgd_kernel<<<grid, 256, 0, st>>>(segs_dev, theta, v, grad, lr_dev, mom, wd, nesterov, shadow_only ? 1 : 0);
   PETRA_LAUNCH_CHECK();
 }
 

@@ -3,6 +3,8 @@
 // (NCCL send/recv through torch.distributed) from the plan of petra_pipeline_comm.
 #include "pipeline.h"
 
+#include <cstdlib>
+
 namespace petra {
 
 static bool has_stem(const petra_stage_desc &d) { return d.n_units > 0 && d.units[0].kind == PETRA_UNIT_STEM; }
@@ -53,6 +55,16 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
     PETRA_CUDA(cudaEventCreateWithFlags(&done_[j], cudaEventDisableTiming));
   }
   PETRA_CUDA(cudaEventCreateWithFlags(&start_, cudaEventDisableTiming));
+  if (sched_.local(1)) {
+    const Shape &in = stages_[1]->in_shape();
+    int64_t n = in.numel() * (has_stem(d.stages[0]) ? 1 : 2);
+    for (int p = 0; p < 2; ++p) {
+      x0_stage_[p] = dalloc(n * sizeof(float));
+      lab_stage_[p] = dalloc((size_t)in.B * sizeof(int32_t));
+    }
+  }
+  const char *g = getenv("PETRA_GRAPHS");
+  graphs_ = !(g && g[0] == '0');
   for (int p = 0; p < 2; ++p) {
     if (j0 > 1) {
       const Shape &in = stages_[j0]->in_shape();
@@ -67,7 +79,39 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
   }
 }
 
+cudaEvent_t Pipeline::ev() {
+  if (ev_next_ == ev_pool_.size()) {
+    cudaEvent_t e;
+    PETRA_CUDA(cudaEventCreate(&e));
+    ev_pool_.push_back(e);
+  }
+  return ev_pool_[ev_next_++];
+}
+
+void Pipeline::timing(bool on) {
+  PETRA_CUDA(cudaDeviceSynchronize());
+  for (auto &v : tev_) v.clear();
+  ev_next_ = 0;
+  timed_ticks_ = 0;
+  timing_ = on;
+}
+
+int Pipeline::stage_ms(float *ms, int n) {
+  PETRA_CUDA(cudaDeviceSynchronize());
+  for (int j = 1; j <= J_ && j <= n; ++j) {
+    double acc = 0;
+    for (auto &pr : tev_[j]) {
+      float x = 0.f;
+      PETRA_CUDA(cudaEventElapsedTime(&x, pr.first, pr.second));
+      acc += x;
+    }
+    ms[j - 1] = (float)acc;
+  }
+  return timed_ticks_;
+}
+
 Pipeline::~Pipeline() {
+  for (auto e : ev_pool_) cudaEventDestroy(e);
   for (auto s : streams_)
     if (s) cudaStreamDestroy(s);
   for (auto e : done_)
@@ -90,41 +134,66 @@ void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labe
     st = streams_[j];
     PETRA_CUDA(cudaStreamWaitEvent(st, start_, 0));
     const Schedule::Step &sp = steps[j];
+    TickArgs a;
+    a.fwd = sp.fwd_mb >= 0;
+    a.bwd = sp.bwd_mb >= 0;
+    a.fmb = (uint64_t)std::max<int64_t>(sp.fwd_mb, 0);
+    a.bmb = (uint64_t)std::max<int64_t>(sp.bwd_mb, 0);
     // ---- forward input message
-    const float *in1 = nullptr, *in2 = nullptr;
-    const int32_t *lab = nullptr;
-    if (sp.fwd_mb >= 0) {
+    if (a.fwd) {
       if (j == 1) {
         if (!x0 || !labels) throw PetraError(PETRA_E_ARG, "inject on the rank of stage 1 needs x0 and labels");
-        in1 = x0;
-        in2 = has_stem(descs_[0]) ? nullptr : x0 + s.in_shape().numel();
-        lab = labels;
+        // copy into fixed staging buffers: the captured graph reads fixed addresses
+        PETRA_CUDA(cudaMemcpyAsync(x0_stage_[p]->p, x0, x0_stage_[p]->bytes, cudaMemcpyDeviceToDevice, st));
+        PETRA_CUDA(cudaMemcpyAsync(lab_stage_[p]->p, labels, lab_stage_[p]->bytes, cudaMemcpyDeviceToDevice, st));
+        a.x1 = x0_stage_[p]->as<float>();
+        a.x2 = has_stem(descs_[0]) ? nullptr : a.x1 + s.in_shape().numel();
+        a.labels = lab_stage_[p]->as<int32_t>();
       } else {
         Msg &m = sched_.local(j - 1) ? fwd_[j - 1][q] : ghost_fwd_[q];
-        in1 = fp(m.x[0]);
-        in2 = fp(m.x[1]);
-        lab = m.labels->as<int32_t>();
+        a.x1 = fp(m.x[0]);
+        a.x2 = fp(m.x[1]);
+        a.labels = m.labels->as<int32_t>();
       }
     }
     if (j < J_) {
-      if (sp.fwd_mb >= 0) {
+      if (a.fwd) {
         Msg &o = fwd_[j][p];
-        s.forward((uint64_t)sp.fwd_mb, in1, in2, fp(o.x[0]), fp(o.x[1]), st);
-        PETRA_CUDA(cudaMemcpyAsync(o.labels->p, lab, (size_t)s.out_shape().B * sizeof(int32_t),
+        a.o[0] = fp(o.x[0]);
+        a.o[1] = fp(o.x[1]);
+        PETRA_CUDA(cudaMemcpyAsync(o.labels->p, a.labels, (size_t)s.out_shape().B * sizeof(int32_t),
                                    cudaMemcpyDeviceToDevice, st));
       }
-      if (sp.bwd_mb >= 0) {
+      if (a.bwd) {
         Msg &m = sched_.local(j + 1) ? bwd_[j + 1][q] : ghost_bwd_[q];
-        Msg &o = bwd_[j][p];
-        s.backward((uint64_t)sp.bwd_mb, fp(m.x[0]), fp(m.x[1]), fp(m.x[2]), fp(m.x[3]), fp(o.x[0]), fp(o.x[1]),
-                   fp(o.x[2]), fp(o.x[3]), lr, st);
+        for (int k = 0; k < 2; ++k) {
+          a.xt[k] = fp(m.x[k]);
+          a.d[k] = fp(m.x[2 + k]);
+        }
       }
-    } else if (sp.fwd_mb >= 0) {
+    }
+    if (a.bwd || (j == J_ && a.fwd)) {
       Msg &o = bwd_[j][p];
-      s.tail((uint64_t)sp.fwd_mb, in1, in2, lab, lr, fp(o.x[0]), fp(o.x[1]), fp(o.x[2]), fp(o.x[3]), loss, st);
+      for (int k = 0; k < 2; ++k) {
+        a.oxt[k] = fp(o.x[k]);
+        a.od[k] = fp(o.x[2 + k]);
+      }
+    }
+    if (j == J_) a.loss = loss;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing_) {
+      e0 = ev();
+      e1 = ev();
+      PETRA_CUDA(cudaEventRecord(e0, st));
+    }
+    s.tick(a, lr, st, graphs_);
+    if (timing_) {
+      PETRA_CUDA(cudaEventRecord(e1, st));
+      tev_[j].push_back({e0, e1});
     }
     PETRA_CUDA(cudaEventRecord(done_[j], st));
   }
+  if (timing_) ++timed_ticks_;
   for (int j = 1; j <= J_; ++j)  // join: the caller's stream sees the whole tick
     if (sched_.local(j)) PETRA_CUDA(cudaStreamWaitEvent(caller, done_[j], 0));
   if (rep) {

@@ -20,6 +20,8 @@ class Pipeline {
   void tick(int64_t t, bool inject, const float *x0, const int32_t *labels, float lr, float *loss, cudaStream_t st,
             petra_tick_report *rep);
   void comm(int64_t t, petra_comm_plan *plan);
+  void timing(bool on);
+  int stage_ms(float *ms, int n);
 
  private:
   int J_, rank_;
@@ -33,6 +35,14 @@ class Pipeline {
   std::vector<cudaStream_t> streams_;
   std::vector<cudaEvent_t> done_;
   cudaEvent_t start_ = nullptr;
+  DevPtr x0_stage_[2], lab_stage_[2];  // caller inputs copied to fixed buffers (graph keys stay fixed)
+  bool graphs_ = true;
+  bool timing_ = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev_[PETRA_MAX_STAGES + 2];
+  std::vector<cudaEvent_t> ev_pool_;
+  size_t ev_next_ = 0;
+  int timed_ticks_ = 0;
+  cudaEvent_t ev();
 
  public:
   ~Pipeline();

@@ -70,7 +70,10 @@ Stage::Stage(const petra_stage_desc &desc, uint64_t seed) : desc_(desc) {
   init_params(seed);
 }
 
-Stage::~Stage() = default;
+Stage::~Stage() {
+  for (auto &kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
+  if (lr_host_) cudaFreeHost(lr_host_);
+}
 
 int64_t Stage::add_tensor(int unit, int part, int kind, int decay, std::vector<int> shape, bool buffer) {
   petra_tensor_info t{};
@@ -232,6 +235,7 @@ void Stage::build() {
   }
   for (auto &p : layers) {
     max_part = std::max(max_part, bn_partial_bytes(p.L->g.M(), p.L->g.Co));
+    max_part = std::max(max_part, (size_t)kNumSMs * 4 * p.L->g.Co * 2 * sizeof(float));  // fused conv stats
     max_ws = std::max(max_ws, conv_wgrad_simt_workspace(p.L->g));
     if (tc_)
       for (int mode = 0; mode < 3; ++mode) max_ws = std::max(max_ws, conv_tc_workspace(p.L->g, mode));
@@ -242,6 +246,9 @@ void Stage::build() {
   counters_ = dalloc(max_ctr * sizeof(unsigned));
   PETRA_CUDA(cudaMemset(counters_->p, 0, max_ctr * sizeof(unsigned)));
   wgrad_ws_ = dalloc(std::max<size_t>(max_ws, 16));
+  lr_dev_ = dalloc(sizeof(float));
+  PETRA_CUDA(cudaMallocHost(&lr_host_, kLrRing * sizeof(float)));
+  if (tc_) conv_tc_prepare();
   nonfinite_ = dalloc(sizeof(int));
   PETRA_CUDA(cudaMemset(nonfinite_->p, 0, sizeof(int)));
 
@@ -340,7 +347,7 @@ void Stage::set_params(const float *theta, const float *v, const float *bufs) {
     PETRA_CUDA(cudaMemcpy(bufs_->p, bufs, n_buffers_ * sizeof(float), cudaMemcpyHostToDevice));
   if (tc_ && theta) {
     sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
-               grad_->as<float>(), 0.f, 0.f, 0.f, 1, nullptr, /*shadow_only=*/true);
+               grad_->as<float>(), nullptr, 0.f, 0.f, 1, nullptr, /*shadow_only=*/true);
     PETRA_CUDA(cudaDeviceSynchronize());
   }
 }
@@ -371,11 +378,18 @@ int Stage::fifo_depth() const {
   return d;
 }
 
-void Stage::update(float lr, cudaStream_t st) {
+// the tick's learning rate -> device scalar (pinned ring: the async copy's source
+// stays valid while up to kLrRing ticks are in flight)
+void Stage::upload_lr(float lr, cudaStream_t st) {
+  float *h = lr_host_ + (lr_next_++ % kLrRing);
+  *h = lr;
+  PETRA_CUDA(cudaMemcpyAsync(lr_dev_->p, h, sizeof(float), cudaMemcpyHostToDevice, st));
+}
+
+void Stage::enqueue_update(cudaStream_t st) {
   ProfScope ps("sgd_update", st, 0.0, 20.0 * (double)n_params_);
   sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
-             grad_->as<float>(), lr, desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false);
-  ++version_;
+             grad_->as<float>(), lr_dev_->as<float>(), desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false);
 }
 
 // ------------------------------------------------------------------ layer kernels
@@ -400,8 +414,8 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
   }
   ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->as<float>(), nullptr,
-                wgrad_ws_->as<float>(), st);
+    L.stats_rows = conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->as<float>(),
+                               wgrad_ws_->as<float>(), reinterpret_cast<float *>(part_->p), st);
   } else {
     conv_fwd_simt(L.g, x, w, L.z->as<float>(), st);
   }
@@ -432,8 +446,16 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
 }
 
 void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
-  ProfScope ps("bn_stats", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co);
   float *b = bufs_->as<float>();
+  if (L.stats_rows > 0) {  // sums already produced by the tensor-core conv epilogue
+    ProfScope ps("bn_stats_merge", st, 0.0, 8.0 * L.stats_rows * L.g.Co);
+    bn_stats_from_partials(reinterpret_cast<const float *>(part_->p), L.stats_rows, L.g.Co, L.g.M(), desc_.bn_eps,
+                           L.mean->as<float>(), L.invstd->as<float>(), running ? b + L.rm_off : nullptr,
+                           running ? b + L.rv_off : nullptr, desc_.bn_momentum, st);
+    L.stats_rows = 0;
+    return;
+  }
+  ProfScope ps("bn_stats", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co);
   bn_stats<float>(L.z->as<float>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean->as<float>(), L.invstd->as<float>(),
                   running ? b + L.rm_off : nullptr, running ? b + L.rv_off : nullptr, desc_.bn_momentum,
                   part_->as<double>(), counters_->as<unsigned>(), st);
@@ -629,6 +651,10 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
 }
 
 // ------------------------------------------------------------------ ticks
+// Host bookkeeping (FIFO slots, id order, counters) is kept apart from the device
+// enqueue functions, so that the device work of a tick can be captured once into a
+// CUDA graph and replayed: its pointers depend only on the mailbox parity and the
+// FIFO slots, both fixed per graph key.
 static void copy_d2d(float *dst, const float *src, int64_t n, cudaStream_t st) {
   if (dst && src && dst != src) {
     ProfScope ps("copy", st, 0.0, 8.0 * (double)n);
@@ -636,17 +662,18 @@ static void copy_d2d(float *dst, const float *src, int64_t n, cudaStream_t st) {
   }
 }
 
-static void fifo_push(Fifo &f, uint64_t mb, const float *a, const float *b, int64_t n, cudaStream_t st) {
+// reserve the FIFO slot a forward pushes its input into (reading c5)
+static int fifo_reserve(Fifo &f, uint64_t mb) {
   if (f.size >= f.cap) throw PetraError(PETRA_E_ARG, "FIFO overflow: capacity below 2(J-j)+1");
   int slot = (f.head + f.size) % f.cap;
-  copy_d2d(f.slot0[slot]->as<float>(), a, n, st);
-  if (b) copy_d2d(f.slot1[slot]->as<float>(), b, n, st);
   f.ids.push_back(mb);
   ++f.size;
   f.peak = std::max(f.peak, f.size);
+  return slot;
 }
 
-static int fifo_pop(Fifo &f, uint64_t mb) {
+// the slot a backward pops (must be the FIFO head, Alg. 1 line 16)
+static int fifo_take(Fifo &f, uint64_t mb) {
   if (f.size == 0) throw PetraError(PETRA_E_EMPTY_BUFFER, "non-reversible backward with an empty FIFO");
   if (f.ids.front() != mb)
     throw PetraError(PETRA_E_ORDER, "backward mb " + std::to_string(mb) + " != FIFO head " +
@@ -658,17 +685,31 @@ static int fifo_pop(Fifo &f, uint64_t mb) {
   return slot;
 }
 
-// Forward tick.  Targets: a unit that first writes a half writes into the stage
-// output buffer if no non-reversible unit follows, else into its own buffer;
-// later units work in place.  Caller inputs are never written.
-void Stage::forward(uint64_t mb, const float *x1, const float *x2, float *o1, float *o2, cudaStream_t st) {
-  if (is_last_) throw PetraError(PETRA_E_ARG, "the final stage runs petra_stage_tail");
-  if (!x1 || (!stem_first() && !x2) || !o1 || !o2) throw PetraError(PETRA_E_ARG, "NULL activation pointer");
-  if (have_last_fwd_ && mb <= last_fwd_mb_) throw PetraError(PETRA_E_ORDER, "forward mb ids must increase");
+std::vector<int> Stage::reserve_push(uint64_t mb) {
+  std::vector<int> slots(units_.size(), -1);
+  for (size_t i = 0; i < units_.size(); ++i)
+    if (units_[i].d.kind == PETRA_UNIT_DS || units_[i].d.kind == PETRA_UNIT_STEM) slots[i] = fifo_reserve(units_[i].fifo, mb);
+  return slots;
+}
+
+std::vector<int> Stage::take_pop(uint64_t mb) {
+  std::vector<int> slots(units_.size(), -1);
+  for (int i = (int)units_.size() - 1; i >= 0; --i)
+    if (units_[i].d.kind == PETRA_UNIT_DS || units_[i].d.kind == PETRA_UNIT_STEM) slots[i] = fifo_take(units_[i].fifo, mb);
+  return slots;
+}
+
+// Forward.  Targets: a unit that first writes a half writes into the
+// stage output buffer if no non-reversible unit follows, else into its own buffer;
+// later units work in place.  Caller inputs are never written.  keep = final stage
+// (running stats updated in this single forward, reading c10; outputs stay in the
+// stage's buffers for its own backward).
+void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *o2, const std::vector<int> &push,
+                            bool keep, const float **fin, cudaStream_t st) {
   const float *cur[2] = {x1, x2};
   bool ro[2] = {true, true};
   float *outs[2] = {o1, o2};
-  const int n = (int)units_.size();
+  const int n = (int)units_.size() - (is_last_ ? 1 : 0);
   for (int i = 0; i < n; ++i) {
     Unit &u = units_[i];
     float *tgt[2];
@@ -677,56 +718,57 @@ void Stage::forward(uint64_t mb, const float *x1, const float *x2, float *o1, fl
       float *o[2] = {nullptr, nullptr};
       int d = u.dst();
       o[d] = ro[d] ? tgt[d] : const_cast<float *>(cur[d]);
-      unit_forward(u, cur, o, false, st);
+      unit_forward(u, cur, o, keep, st);
       cur[d] = o[d];
       ro[d] = false;
     } else {
-      fifo_push(u.fifo, mb, cur[0], u.d.kind == PETRA_UNIT_DS ? cur[1] : nullptr, u.in.numel(), st);
-      unit_forward(u, cur, tgt, false, st);
+      int slot = push[i];
+      copy_d2d(u.fifo.slot0[slot]->as<float>(), cur[0], u.in.numel(), st);
+      if (u.d.kind == PETRA_UNIT_DS) copy_d2d(u.fifo.slot1[slot]->as<float>(), cur[1], u.in.numel(), st);
+      unit_forward(u, cur, tgt, keep, st);
       cur[0] = tgt[0];
       cur[1] = tgt[1];
       ro[0] = ro[1] = false;
     }
   }
+  if (fin) {
+    fin[0] = cur[0];
+    fin[1] = cur[1];
+    return;
+  }
   for (int h = 0; h < 2; ++h)
     if (cur[h] != outs[h]) copy_d2d(outs[h], cur[h], out_.numel(), st);
-  have_last_fwd_ = true;
-  last_fwd_mb_ = mb;
-  ++n_fwd_;
-  last_stream_ = st;
 }
 
-void Stage::backward(uint64_t mb, const float *xt1, const float *xt2, const float *d1, const float *d2,
-                     float *oxt1, float *oxt2, float *od1, float *od2, float lr, cudaStream_t st) {
-  if (is_last_) throw PetraError(PETRA_E_ARG, "the final stage runs petra_stage_tail");
-  if (!xt1 || !xt2 || !d1 || !d2) throw PetraError(PETRA_E_ARG, "NULL backward input");
-  if (!std::isfinite(lr) || lr < 0.f) throw PetraError(PETRA_E_ARG, "lr must be finite and >= 0");
-  const float *cx[2] = {xt1, xt2}, *cd[2] = {d1, d2};
-  bool rox[2] = {true, true}, rod[2] = {true, true};
-  float *ox[2] = {oxt1, oxt2}, *od[2] = {od1, od2};
-  for (int i = (int)units_.size() - 1; i >= 0; --i) {
+// Backward walk over units (reverse order): reversible units reconstruct their
+// input with the current theta and run the VJP; non-reversible
+// units recompute from their FIFO slot (Alg. 1 lines 16-17).  recompute = false
+// in the final stage (plain backprop through the graph kept by its forward).
+void Stage::enqueue_backward_walk(int last_unit, bool recompute, const float *cx[2], const float *cd[2],
+                                  bool rox[2], bool rod[2], float *ox[2], float *od[2], const std::vector<int> &pop,
+                                  cudaStream_t st) {
+  for (int i = last_unit; i >= 0; --i) {
     Unit &u = units_[i];
     if (u.d.kind == PETRA_UNIT_REV) {
       int d = u.dst(), s = u.src();
       float *tx[2] = {nullptr, nullptr}, *td[2] = {nullptr, nullptr};
       tx[d] = rox[d] ? (u.bx[d] ? u.bx[d]->as<float>() : ox[d]) : const_cast<float *>(cx[d]);
       td[s] = rod[s] ? (u.bd[s] ? u.bd[s]->as<float>() : od[s]) : const_cast<float *>(cd[s]);
-      if (!tx[d]) tx[d] = u.bx[d] ? u.bx[d]->as<float>() : nullptr;
       if (!tx[d] || !td[s]) throw PetraError(PETRA_E_ARG, "NULL backward output for a reversible stage");
       const float *nox[2] = {nullptr, nullptr};
-      unit_backward(u, true, nox, cx, tx, cd, td, st);
+      unit_backward(u, recompute, nox, cx, tx, cd, td, st);
       cx[d] = tx[d];
       rox[d] = false;
       cd[s] = td[s];
       rod[s] = false;
     } else {
-      int slot = fifo_pop(u.fifo, mb);
+      int slot = pop[i];
       const float *xin[2] = {u.fifo.slot0[slot]->as<float>(),
                              u.d.kind == PETRA_UNIT_DS ? u.fifo.slot1[slot]->as<float>() : nullptr};
       float *td[2] = {nullptr, nullptr};
       if (u.d.kind == PETRA_UNIT_DS)
         for (int h = 0; h < 2; ++h) td[h] = u.bd[h] ? u.bd[h]->as<float>() : od[h];
-      unit_backward(u, true, xin, cx, nullptr, cd, td, st);
+      unit_backward(u, recompute, xin, cx, nullptr, cd, td, st);
       cx[0] = xin[0];
       cx[1] = xin[1];
       rox[0] = rox[1] = true;  // FIFO memory: copied out at the end, never written
@@ -735,44 +777,28 @@ void Stage::backward(uint64_t mb, const float *xt1, const float *xt2, const floa
       rod[0] = rod[1] = false;
     }
   }
-  if (!stem_first()) {
+}
+
+void Stage::enqueue_backward(const float *xt1, const float *xt2, const float *d1, const float *d2, float *oxt1,
+                             float *oxt2, float *od1, float *od2, const std::vector<int> &pop, cudaStream_t st) {
+  const float *cx[2] = {xt1, xt2}, *cd[2] = {d1, d2};
+  bool rox[2] = {true, true}, rod[2] = {true, true};
+  float *ox[2] = {oxt1, oxt2}, *od[2] = {od1, od2};
+  enqueue_backward_walk((int)units_.size() - 1, true, cx, cd, rox, rod, ox, od, pop, st);
+  if (!stem_first())
     for (int h = 0; h < 2; ++h) {
       if (ox[h]) copy_d2d(ox[h], cx[h], in_.numel(), st);
       if (od[h]) copy_d2d(od[h], cd[h], in_.numel(), st);
     }
-  }
-  update(lr, st);
-  ++n_bwd_;
-  last_stream_ = st;
 }
 
-void Stage::tail(uint64_t mb, const float *x1, const float *x2, const int32_t *labels, float lr, float *oxt1,
-                 float *oxt2, float *od1, float *od2, float *loss, cudaStream_t st) {
-  if (!is_last_) throw PetraError(PETRA_E_ARG, "petra_stage_tail on a stage without a tail unit");
-  if (!x1 || (!stem_first() && !x2) || !labels) throw PetraError(PETRA_E_ARG, "NULL tail input");
-  if (!std::isfinite(lr) || lr < 0.f) throw PetraError(PETRA_E_ARG, "lr must be finite and >= 0");
-  const int n = (int)units_.size();
-  // forward with stored activations; running stats updated here (reading c10)
-  const float *cur[2] = {x1, x2};
-  bool ro[2] = {true, true};
-  for (int i = 0; i + 1 < n; ++i) {
-    Unit &u = units_[i];
-    float *tgt[2] = {u.fout[0]->as<float>(), u.fout[1]->as<float>()};
-    if (u.d.kind == PETRA_UNIT_REV) {
-      float *o[2] = {nullptr, nullptr};
-      int d = u.dst();
-      o[d] = ro[d] ? tgt[d] : const_cast<float *>(cur[d]);
-      unit_forward(u, cur, o, true, st);
-      cur[d] = o[d];
-      ro[d] = false;
-    } else {
-      fifo_push(u.fifo, mb, cur[0], u.d.kind == PETRA_UNIT_DS ? cur[1] : nullptr, u.in.numel(), st);
-      unit_forward(u, cur, tgt, true, st);
-      cur[0] = tgt[0];
-      cur[1] = tgt[1];
-      ro[0] = ro[1] = false;
-    }
-  }
+// Final stage (Alg. 1 lines 26-35): forward keeping the graph, loss, backprop, and
+// the received input returned unchanged with delta_J wrt it (reading c7).
+void Stage::enqueue_tail(const float *x1, const float *x2, const int32_t *labels, float *oxt1, float *oxt2,
+                         float *od1, float *od2, float *loss, const std::vector<int> &push,
+                         const std::vector<int> &pop, cudaStream_t st) {
+  const float *cur[2];
+  enqueue_forward(x1, x2, nullptr, nullptr, push, true, cur, st);
   Unit &t = units_.back();
   const float *th = theta_->as<float>();
   float *gr = grad_->as<float>();
@@ -783,43 +809,143 @@ void Stage::tail(uint64_t mb, const float *x1, const float *x2, const int32_t *l
                           lossrow_->as<float>(), dfeat_->as<float>(), gr + t.fc_w, gr + t.fc_b,
                           tail_d_[0]->as<float>(), tail_d_[1]->as<float>(), loss, nonfinite_->as<int>(), st);
   }
-  // plain backprop through the stored graph (no conv recomputation)
+  // the stage's own forward buffers and gradient buffers are written in place
   const float *cx[2] = {cur[0], cur[1]}, *cd[2] = {tail_d_[0]->as<float>(), tail_d_[1]->as<float>()};
-  for (int i = n - 2; i >= 0; --i) {
-    Unit &u = units_[i];
-    if (u.d.kind == PETRA_UNIT_REV) {
-      int d = u.dst(), s = u.src();
-      float *tx[2] = {nullptr, nullptr}, *td[2] = {nullptr, nullptr};
-      tx[d] = const_cast<float *>(cx[d]);  // in place (forward buffers of this stage)
-      td[s] = const_cast<float *>(cd[s]);  // stage-owned gradient buffers: in place
-      const float *nox[2] = {nullptr, nullptr};
-      unit_backward(u, false, nox, cx, tx, cd, td, st);
-      cx[d] = tx[d];
-      cd[s] = td[s];
-    } else {
-      int slot = fifo_pop(u.fifo, mb);
-      const float *xin[2] = {u.fifo.slot0[slot]->as<float>(),
-                             u.d.kind == PETRA_UNIT_DS ? u.fifo.slot1[slot]->as<float>() : nullptr};
-      float *td[2] = {nullptr, nullptr};
-      if (u.d.kind == PETRA_UNIT_DS)
-        for (int h = 0; h < 2; ++h) td[h] = u.bd[h]->as<float>();
-      unit_backward(u, false, xin, cx, nullptr, cd, td, st);
-      cx[0] = xin[0];
-      cx[1] = xin[1];
-      cd[0] = td[0];
-      cd[1] = td[1];
-    }
-  }
+  bool rox[2] = {false, false}, rod[2] = {false, false};
+  float *ox[2] = {nullptr, nullptr}, *od[2] = {nullptr, nullptr};
+  enqueue_backward_walk((int)units_.size() - 2, false, cx, cd, rox, rod, ox, od, pop, st);
   if (!stem_first()) {
-    // reading c7: the received input goes back unchanged, with delta_J wrt it
     copy_d2d(oxt1, x1, in_.numel(), st);
     copy_d2d(oxt2, x2, in_.numel(), st);
     copy_d2d(od1, cd[0], in_.numel(), st);
     copy_d2d(od2, cd[1], in_.numel(), st);
   }
-  update(lr, st);
+}
+
+// ---- public entry points (standalone stages: direct enqueue)
+void Stage::check_fwd(uint64_t mb, const float *x1, const float *x2) {
+  if (!x1 || (!stem_first() && !x2)) throw PetraError(PETRA_E_ARG, "NULL activation pointer");
+  if (have_last_fwd_ && mb <= last_fwd_mb_) throw PetraError(PETRA_E_ORDER, "forward mb ids must increase");
+}
+
+static void check_lr(float lr) {
+  if (!std::isfinite(lr) || lr < 0.f) throw PetraError(PETRA_E_ARG, "lr must be finite and >= 0");
+}
+
+void Stage::forward(uint64_t mb, const float *x1, const float *x2, float *o1, float *o2, cudaStream_t st) {
+  if (is_last_) throw PetraError(PETRA_E_ARG, "the final stage runs petra_stage_tail");
+  check_fwd(mb, x1, x2);
+  if (!o1 || !o2) throw PetraError(PETRA_E_ARG, "NULL output pointer");
+  std::vector<int> push = reserve_push(mb);
+  enqueue_forward(x1, x2, o1, o2, push, false, nullptr, st);
+  have_last_fwd_ = true;
+  last_fwd_mb_ = mb;
+  ++n_fwd_;
+  last_stream_ = st;
+}
+
+void Stage::backward(uint64_t mb, const float *xt1, const float *xt2, const float *d1, const float *d2,
+                     float *oxt1, float *oxt2, float *od1, float *od2, float lr, cudaStream_t st) {
+  if (is_last_) throw PetraError(PETRA_E_ARG, "the final stage runs petra_stage_tail");
+  if (!xt1 || !xt2 || !d1 || !d2) throw PetraError(PETRA_E_ARG, "NULL backward input");
+  check_lr(lr);
+  std::vector<int> pop = take_pop(mb);
+  upload_lr(lr, st);
+  enqueue_backward(xt1, xt2, d1, d2, oxt1, oxt2, od1, od2, pop, st);
+  enqueue_update(st);
+  ++version_;
+  ++n_bwd_;
+  last_stream_ = st;
+}
+
+void Stage::tail(uint64_t mb, const float *x1, const float *x2, const int32_t *labels, float lr, float *oxt1,
+                 float *oxt2, float *od1, float *od2, float *loss, cudaStream_t st) {
+  if (!is_last_) throw PetraError(PETRA_E_ARG, "petra_stage_tail on a stage without a tail unit");
+  if (!labels) throw PetraError(PETRA_E_ARG, "NULL labels");
+  check_fwd(mb, x1, x2);
+  check_lr(lr);
+  std::vector<int> push = reserve_push(mb), pop = take_pop(mb);
+  upload_lr(lr, st);
+  enqueue_tail(x1, x2, labels, oxt1, oxt2, od1, od2, loss, push, pop, st);
+  enqueue_update(st);
+  have_last_fwd_ = true;
+  last_fwd_mb_ = mb;
+  ++version_;
   ++n_fwd_;
   ++n_bwd_;
+  last_stream_ = st;
+}
+
+// ---- pipeline entry point: forward and/or backward (or the tail step) of one
+// tick, replayed from a cached CUDA graph when graphs are enabled.
+void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
+  const bool fwd = a.fwd, bwd = a.bwd;
+  if (is_last_ && fwd != bwd) throw PetraError(PETRA_E_ARG, "the final stage runs forward and backward together");
+  std::vector<int> push, pop;
+  if (fwd) {
+    check_fwd(a.fmb, a.x1, a.x2);
+    if (is_last_ && !a.labels) throw PetraError(PETRA_E_ARG, "NULL labels");
+    push = reserve_push(a.fmb);
+  }
+  if (bwd) {
+    check_lr(lr);
+    pop = take_pop(is_last_ ? a.fmb : a.bmb);
+  }
+  if (!fwd && !bwd) return;
+  if (bwd) upload_lr(lr, st);
+  auto enqueue = [&](cudaStream_t s) {
+    if (is_last_) {
+      enqueue_tail(a.x1, a.x2, a.labels, a.oxt[0], a.oxt[1], a.od[0], a.od[1], a.loss, push, pop, s);
+    } else {
+      if (fwd) enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
+      if (bwd) enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, s);
+    }
+    if (bwd) enqueue_update(s);
+  };
+  if (!use_graph || Prof::enabled) {
+    enqueue(st);
+  } else {
+    std::vector<uintptr_t> key = {(uintptr_t)fwd, (uintptr_t)bwd};
+    for (const void *p : {(const void *)a.x1, (const void *)a.x2, (const void *)a.labels, (const void *)a.o[0],
+                          (const void *)a.o[1], (const void *)a.xt[0], (const void *)a.xt[1], (const void *)a.d[0],
+                          (const void *)a.d[1], (const void *)a.oxt[0], (const void *)a.oxt[1],
+                          (const void *)a.od[0], (const void *)a.od[1], (const void *)a.loss})
+      key.push_back((uintptr_t)p);
+    for (int v : push) key.push_back((uintptr_t)(v + 1));
+    for (int v : pop) key.push_back((uintptr_t)(v + 1));
+    auto it = graphs_.find(key);
+    if (it == graphs_.end()) {
+      const int64_t n0 = Prof::launches.load();
+      cudaGraph_t g = nullptr;
+      PETRA_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+      try {
+        enqueue(st);
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      PETRA_CUDA(cudaStreamEndCapture(st, &g));
+      CachedGraph cg;
+      cudaError_t e = cudaGraphInstantiate(&cg.exec, g, 0);
+      cudaGraphDestroy(g);
+      PETRA_CUDA(e);
+      cg.kernels = Prof::launches.load() - n0;
+      Prof::launches.fetch_sub(cg.kernels);  // counted when the graph is launched
+      it = graphs_.emplace(std::move(key), cg).first;
+    }
+    PETRA_CUDA(cudaGraphLaunch(it->second.exec, st));
+    count_launch((int)it->second.kernels);
+  }
+  if (fwd) {
+    have_last_fwd_ = true;
+    last_fwd_mb_ = a.fmb;
+    ++n_fwd_;
+  }
+  if (bwd) {
+    ++version_;
+    ++n_bwd_;
+  }
   last_stream_ = st;
 }
 

@@ -41,6 +41,7 @@ struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
   DevPtr z, a, dz, da, mean, invstd;         // workspace, kept from forward to backward in a tick
   DevPtr zb, ab, dzb, xb;                    // bf16 workspace (tensor-core path)
   DevPtr w_bf16, wt_bf16;                    // bf16 shadows of the live weights
+  int stats_rows = 0;                        // > 0: BN partials written by the conv epilogue
   int64_t M() const { return g.M(); }
 };
 
@@ -65,8 +66,23 @@ struct Unit {
   int src() const { return 1 - d.dst_half; }
 };
 
-struct TensorInfo {
-  petra_tensor_info i;
+// one tick of a stage for the pipeline: forward (fmb) and/or backward (bmb)
+struct TickArgs {
+  bool fwd = false, bwd = false;
+  uint64_t fmb = 0, bmb = 0;
+  const float *x1 = nullptr, *x2 = nullptr;  // forward input (tail: its input)
+  const int32_t *labels = nullptr;           // tail only
+  float *o[2] = {nullptr, nullptr};          // forward output
+  const float *xt[2] = {nullptr, nullptr};   // backward input x~_j
+  const float *d[2] = {nullptr, nullptr};    // backward input delta_{j+1}
+  float *oxt[2] = {nullptr, nullptr};        // backward output x~_{j-1}
+  float *od[2] = {nullptr, nullptr};         // backward output delta_j
+  float *loss = nullptr;                     // tail only
+};
+
+struct CachedGraph {
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;
 };
 
 class Stage {
@@ -90,6 +106,7 @@ class Stage {
                 float *oxt2, float *od1, float *od2, float lr, cudaStream_t st);
   void tail(uint64_t mb, const float *x1, const float *x2, const int32_t *labels, float lr, float *oxt1,
             float *oxt2, float *od1, float *od2, float *loss, cudaStream_t st);
+  void tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph);
 
   void get_params(float *theta, float *v, float *bufs);
   void set_params(const float *theta, const float *v, const float *bufs);
@@ -124,7 +141,25 @@ class Stage {
   void alloc_layer(Layer &L, bool inner);
   int64_t add_tensor(int unit, int part, int kind, int decay, std::vector<int> shape, bool buffer);
   void init_params(uint64_t seed);
-  void update(float lr, cudaStream_t st);
+  static constexpr int kLrRing = 256;
+  DevPtr lr_dev_;
+  float *lr_host_ = nullptr;
+  uint64_t lr_next_ = 0;
+  std::map<std::vector<uintptr_t>, CachedGraph> graphs_;
+  void upload_lr(float lr, cudaStream_t st);
+  void enqueue_update(cudaStream_t st);
+  std::vector<int> reserve_push(uint64_t mb);
+  std::vector<int> take_pop(uint64_t mb);
+  void check_fwd(uint64_t mb, const float *x1, const float *x2);
+  void enqueue_forward(const float *x1, const float *x2, float *o1, float *o2, const std::vector<int> &push,
+                       bool keep, const float **fin, cudaStream_t st);
+  void enqueue_backward_walk(int last_unit, bool recompute, const float *cx[2], const float *cd[2], bool rox[2],
+                             bool rod[2], float *ox[2], float *od[2], const std::vector<int> &pop, cudaStream_t st);
+  void enqueue_backward(const float *xt1, const float *xt2, const float *d1, const float *d2, float *oxt1,
+                        float *oxt2, float *od1, float *od2, const std::vector<int> &pop, cudaStream_t st);
+  void enqueue_tail(const float *x1, const float *x2, const int32_t *labels, float *oxt1, float *oxt2, float *od1,
+                    float *od2, float *loss, const std::vector<int> &push, const std::vector<int> &pop,
+                    cudaStream_t st);
 
   // kernels of one layer / unit
   void conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready = false);

@@ -144,6 +144,15 @@ class Pipeline:
                _stream(stream), C.byref(rep) if report else None)
         return report_dict(rep) if report else None
 
+    def timing(self, on=True):
+        L.call("petra_pipeline_timing", self.h, int(bool(on)))
+
+    def stage_ms(self):
+        arr = (C.c_float * self.J)()
+        n = C.c_int32()
+        L.call("petra_pipeline_stage_ms", self.h, arr, self.J, C.byref(n))
+        return [arr[i] / max(n.value, 1) for i in range(self.J)]
+
     def comm(self, t):
         plan = L.PetraCommPlan()
         L.call("petra_pipeline_comm", self.h, t, C.byref(plan))
