@@ -185,8 +185,11 @@ def run_ours(a):
             tr.exchange(t)
         t += 1
 
-    # fill the pipeline (2J-2 ticks) + warm-up
-    for _ in range(2 * J - 2 + a.warmup):
+    # fill the pipeline (2J-2 ticks), then one full cycle of CUDA-graph keys (a stage's
+    # graph depends on its FIFO slots and the mailbox parity: period lcm(2, 2(J-j)+1)
+    # <= 2(2J-1) ticks, captured once each), then the W warm-up ticks
+    graph_cycle = 2 * (2 * J - 1)
+    for _ in range(2 * J - 2 + graph_cycle + a.warmup):
         tick()
     torch.cuda.synchronize()
     if world > 1:
@@ -288,6 +291,7 @@ def run_ours(a):
                       "image": [3, H, H], "classes": classes, "stages": J, "partition_units": counts,
                       "stage_rank": stage_rank, "parallelism": f"petra-stages{J}-over-{world}gpu",
                       "precision_requested": a.precision, "lr": lr, "fill_ticks": 2 * J - 2,
+                      "graph_capture_ticks": graph_cycle,
                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
                       "wall_s_timed": round(wall, 3),
                       "host_enqueue_ms_per_step": round(statistics.median(host_ms), 4) if host_ms else None},

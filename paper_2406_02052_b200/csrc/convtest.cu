@@ -15,7 +15,8 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
   ConvGeom g = make_geom(pg->batch, pg->h, pg->w, pg->cin, pg->cout, pg->ksize, pg->stride);
   int64_t nx = g.Min() * g.Ci, nz = g.M() * g.Co, nw = (int64_t)g.Co * g.K();
   int64_t na = mode == 0 ? nx : nz, nb = mode == 2 ? nx : nw, no = mode == 0 ? nz : (mode == 1 ? nx : nw);
-  if (engine == 1 && !conv_tc_supported(g, mode)) return PETRA_E_UNSUPPORTED;
+  const bool stem = engine == 1 && !conv_tc_supported(g, mode) && mode != 1 && stem_tc_supported(g);
+  if (engine == 1 && !stem && !conv_tc_supported(g, mode)) return PETRA_E_UNSUPPORTED;
   if (engine == 1) conv_tc_prepare();
   DevPtr da = dalloc(na * 4), db = dalloc(nb * 4), dout = dalloc(no * 4), dadd;
   PETRA_CUDA(cudaMemcpy(da->p, a, na * 4, cudaMemcpyHostToDevice));
@@ -25,7 +26,17 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     PETRA_CUDA(cudaMemcpy(dadd->p, addend, no * 4, cudaMemcpyHostToDevice));
   }
   cudaStream_t st = nullptr;
-  if (engine == 0) {
+  if (stem) {  // gathered-im2col tensor-core stem: fp32 image (and fp32 weights) read directly
+    DevPtr ws = dalloc(std::max<size_t>(16, stem_tc_workspace(g)));
+    if (mode == 0) {
+      stem_fwd_tc(g, da->as<float>(), db->as<float>(), dout->as<float>(), nullptr, st);
+    } else {
+      DevPtr ab = dalloc(na * 2);
+      f32_to_bf16(da->as<float>(), ab->as<__nv_bfloat16>(), na, st);
+      stem_wgrad_tc(g, ab->as<__nv_bfloat16>(), db->as<float>(), dout->as<float>(), ws->as<float>(), st);
+    }
+    PETRA_CUDA(cudaDeviceSynchronize());
+  } else if (engine == 0) {
     DevPtr ws = dalloc(std::max<size_t>(16, conv_wgrad_simt_workspace(g)));
     if (mode == 0) conv_fwd_simt(g, da->as<float>(), db->as<float>(), dout->as<float>(), st);
     else if (mode == 1)
@@ -78,5 +89,6 @@ extern "C" petra_status petra_conv_run(int32_t mode, int32_t engine, const petra
 extern "C" int32_t petra_conv_engine(const petra_conv_geom *pg, int32_t mode, int32_t precision) {
   if (!pg || precision != PETRA_BF16_TC) return 0;
   petra::ConvGeom g = petra::make_geom(pg->batch, pg->h, pg->w, pg->cin, pg->cout, pg->ksize, pg->stride);
-  return petra::conv_tc_supported(g, mode) ? 1 : 0;
+  if (petra::conv_tc_supported(g, mode)) return 1;
+  return (mode != 1 && petra::stem_tc_supported(g)) ? 1 : 0;
 }

@@ -30,6 +30,23 @@ void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat
 void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *x, float *dw, float *ws,
                    cudaStream_t st);
 
+// out[i] = sum over splits z of part[z * n + i], fixed order (deterministic)
+void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st);
+
+// ---------------------------------------------------------------- tcgen05 stem (small Ci)
+// Convolutions whose input has few channels (the stem: Ci = 3, k*k*Ci <= 256) run on
+// the tensor cores with a GATHERING producer: warps build the im2col rows of each
+// 128-pixel tile straight from the fp32 NHWC input into the 128B-swizzled smem
+// layout (no im2col tensor in HBM).  Forward and wgrad only (the stem input is data).
+bool stem_tc_supported(const ConvGeom &g);
+void stem_tc_prepare();  // kernel attributes (called by conv_tc_prepare)
+size_t stem_tc_workspace(const ConvGeom &g);
+// z (fp32) = conv(bf16(x), bf16(w)); x, w fp32 as stored; fused BN partials as conv_fwd_tc
+int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, float *z, float *stats_part, cudaStream_t st);
+// dw (fp32) = sum_pixels dz_bf16 (x) bf16(x)
+void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const float *x, float *dw, float *ws,
+                   cudaStream_t st);
+
 // ---------------------------------------------------------------- batch norm / coupling
 size_t bn_partial_bytes(int64_t M, int C);
 size_t bn_counter_count(int C);  // zero-initialised unsigned counters a reduction needs

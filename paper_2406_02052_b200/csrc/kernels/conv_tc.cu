@@ -12,9 +12,12 @@
 //    tcgen05.mma issuer (one thread) + TMEM owner, warps 2-5 = epilogue;
 //  * A (activations) is an implicit im2col: one 4-D TMA box per (tap, 64-channel
 //    block), coordinates shifted by the tap offset, stride s via TMA traversal
-//    strides, halo / padding from TMA's zero fill of out-of-bounds coordinates.  A
-//    128-row M tile is a rectangle of whole output rows (or whole images), so the
-//    box lands in smem exactly in the 128B-swizzled K-major layout UMMA reads;
+//    strides, halo / padding from TMA's zero fill of out-of-bounds coordinates.  The
+//    output grid (Gh x Gw per image) is embedded in a padded grid Hb x Wb (Wb = the
+//    power of two >= Gw), so a 128-row M tile is always a rectangle of whole padded
+//    rows (or whole padded images) and the box lands in smem exactly in the
+//    128B-swizzled K-major layout UMMA reads.  Padding rows are computed and masked
+//    in the epilogue (no store, no BN statistics); CIFAR shapes need no padding;
 //  * B (weights) via 2-D TMA; fp32 accumulators in TMEM, double buffered so the
 //    epilogue (tcgen05.ld -> fp32 store) of tile i overlaps the MMAs of tile i+1.
 #include <cudaTypedefs.h>
@@ -35,12 +38,13 @@ constexpr int kMaxTaps = 9;
 constexpr int kMaxStatN = 512;  // widest conv output with fused BN statistics
 
 struct ConvTCParams {
-  int M, N;                  // GEMM: M = pixels of the output grid, N = output channels
+  int M, N;                  // GEMM: M = rows of the padded output grid (B_pad*Hb*Wb), N = output channels
   int CB;                    // 64-channel blocks of the reduction operand
   int Cred;                  // channels of the reduction operand (B's K = wk * Cred + c)
   int ntaps;
   int dh[kMaxTaps], dw[kMaxTaps], wk[kMaxTaps];  // A coordinate offsets, weight tap index
   int Gh, Gw;                // output grid of the GEMM (rows x cols per image)
+  int Hb, Wb, B;             // padded grid per image; real images
   int s_in;                  // A row coordinate = s_in * grid_row + dh
   int OH, OW, oss, ph, pw;   // grid (i, j) -> output pixel (i*oss+ph, j*oss+pw) of an OH x OW image
   int splits, kb_per_split;  // split-K (small-M layers): splits > 1 -> partials into ws[split][M][N]
@@ -49,23 +53,6 @@ struct ConvTCParams {
   float *out;                // [B*OH*OW][N]
   float *stats;              // nullable: per-(CTA, epilogue warp) BN partials [grid][4][N][2] (sum, sum sq)
 };
-
-// Column sums of a 32-row x 16-column fragment held one row per lane: butterfly
-// transpose-reduce (8+4+2+1+1 shuffles).  Afterwards lane L holds the sum over the
-// 32 rows of column (L >> 1) in x[0] (lanes 2k, 2k+1 both).
-__device__ __forceinline__ void colsum16(float (&x)[16], int lane) {
-#pragma unroll
-  for (int half = 8, off = 16; half >= 1; half >>= 1, off >>= 1) {
-    const bool upper = lane & off;
-#pragma unroll
-    for (int k = 0; k < half; ++k) {
-      float send = upper ? x[k] : x[k + half];
-      float keep = upper ? x[k + half] : x[k];
-      x[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-  }
-  x[0] += __shfl_xor_sync(0xffffffffu, x[0], 1);
-}
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -86,7 +73,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int n_tiles_n = P.N / BN;
   const int n_work = (P.M / BM) * n_tiles_n * P.splits;  // (m tile, n tile, K split)
   const int KB = P.ntaps * P.CB;
-  const int GHW = P.Gh * P.Gw;
+  const int GHW = P.Hb * P.Wb;  // padded grid
   // work item -> tile coordinates and K-block range
   auto decode = [&](int w, int &mt, int &nt, int &sp, int &kb0, int &kb1) {
     sp = w % P.splits;
@@ -124,7 +111,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         int mt, nt, sp, kb0, kb1;
         decode(w, mt, nt, sp, kb0, kb1);
         const int m0 = mt * BM;
-        const int b0 = m0 / GHW, i0 = (m0 % GHW) / P.Gw;
+        const int b0 = m0 / GHW, i0 = (m0 % GHW) / P.Wb;
         for (int kb = kb0; kb < kb1; ++kb) {
           const int t = kb / P.CB, cb = kb % P.CB;
           tc::mbar_wait(&empty[stage], phase ^ 1);
@@ -179,12 +166,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
       const int m = mt * BM + row;
-      float *orow;
+      const int b = m / GHW, r = m % GHW, i = r / P.Wb, j = r % P.Wb;
+      const bool valid = b < P.B && i < P.Gh && j < P.Gw;  // padding rows: computed, never stored
+      float *orow = nullptr;
       const float *arow = nullptr;
       if (P.splits > 1) {  // partial of this K split, GEMM-row order; reduced by splitk_out_kernel
         orow = P.ws + ((int64_t)sp * P.M + m) * P.N + nt * BN;
-      } else {
-        const int b = m / GHW, r = m % GHW, i = r / P.Gw, j = r % P.Gw;
+      } else if (valid) {
         const int64_t opix = ((int64_t)b * P.OH + i * P.oss + P.ph) * P.OW + j * P.oss + P.pw;
         orow = P.out + opix * P.N + nt * BN;
         arow = P.addend ? P.addend + opix * P.N + nt * BN : nullptr;
@@ -200,15 +188,21 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             v[jj] += a4.x; v[jj + 1] += a4.y; v[jj + 2] += a4.z; v[jj + 3] += a4.w;
           }
         }
+        if (orow) {
 #pragma unroll
-        for (int jj = 0; jj < 16; jj += 4)
-          *reinterpret_cast<float4 *>(orow + c + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+          for (int jj = 0; jj < 16; jj += 4)
+            *reinterpret_cast<float4 *>(orow + c + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+        }
         if (P.stats) {  // BN batch statistics of z, fused (sum and sum of squares per column)
+          if (!valid) {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
+          }
           float sq[16];
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) sq[jj] = v[jj] * v[jj];
-          colsum16(v, lane);
-          colsum16(sq, lane);
+          tc::colsum16(v, lane);
+          tc::colsum16(sq, lane);
           if (!(lane & 1)) {
             const int col = nt * BN + c + (lane >> 1);
             my_stat[2 * col] += v[0];
@@ -283,15 +277,16 @@ __global__ void __launch_bounds__(256) stats_finalize_kernel(const float *__rest
 __global__ void splitk_out_kernel(const ConvTCParams P) {
   const int N4 = P.N / 4;
   const int64_t n = (int64_t)P.M * N4;
-  const int GHW = P.Gh * P.Gw;
+  const int GHW = P.Hb * P.Wb;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int m = (int)(i / N4), c = (int)(i % N4) * 4;
+    const int b = m / GHW, r = m % GHW, ii = r / P.Wb, jj = r % P.Wb;
+    if (b >= P.B || ii >= P.Gh || jj >= P.Gw) continue;  // padding row
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int z = 0; z < P.splits; ++z) {
       float4 v = *reinterpret_cast<const float4 *>(P.ws + ((int64_t)z * P.M + m) * P.N + c);
       s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
     }
-    const int b = m / GHW, r = m % GHW, ii = r / P.Gw, jj = r % P.Gw;
     const int64_t o = (((int64_t)b * P.OH + ii * P.oss + P.ph) * P.OW + jj * P.oss + P.pw) * P.N + c;
     if (P.addend) {
       float4 a = *reinterpret_cast<const float4 *>(P.addend + o);
@@ -303,17 +298,19 @@ __global__ void splitk_out_kernel(const ConvTCParams P) {
 
 // ------------------------------------------------------------------ wgrad
 // D[r][n] = sum_p x[s*p + off(tap(r))][ci(r)] * dz[p][n],  r = tap*Ci + ci (M side),
-// n = output channel (N side), p = output pixel (K, 64 per block).  Both operands
-// are MN-major in smem: A = two 64-channel boxes (rows r0..r0+63 and r0+64..r0+127,
-// each possibly another tap) of 64 shifted pixels, B = BN/64 boxes of dz.  Split-K
+// n = output channel (N side), p = output pixel of the PADDED grid (K, 64 per
+// block; padding pixels read dz out of bounds -> zero, so they add nothing).  Both
+// operands are MN-major in smem: A = two 64-channel boxes (rows r0..r0+63 and
+// r0+64..r0+127, each possibly another tap) of 64 shifted pixels, B = BN/64 boxes
+// of dz.  Split-K
 // over pixel blocks; the epilogue stores D transposed, ws[split][n][r] -- the weight
 // layout [Co][k][k][Ci] -- so the fixed-order reduction over splits yields dW.
 struct WgradParams {
   int Mr;                 // taps * Ci (rows of D)
   int N;                  // Co
   int Ci, k, p, s;
-  int Gh, Gw;             // output pixel grid (Ho x Wo)
-  int KBtot;              // pixel blocks of 64
+  int Hb, Wb;             // padded output pixel grid per image
+  int KBtot;              // pixel blocks of 64 (padded grid)
   int kb_per_split;
   int n_mt, n_nt, splits;
   float *out;             // [splits][N][Mr]
@@ -361,7 +358,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
     nt = r % P.n_nt;
     mt = r / P.n_nt;
   };
-  const int GHW = P.Gh * P.Gw;
+  const int GHW = P.Hb * P.Wb;
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
@@ -381,7 +378,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
         const uint32_t bytes = (valid[1] ? 2 : 1) * HALF_A + B_BYTES;
         for (int kb = kb0; kb < kb1; ++kb) {
           const int p0 = kb * 64;
-          const int b0 = p0 / GHW, i0 = (p0 % GHW) / P.Gw;
+          const int b0 = p0 / GHW, i0 = (p0 % GHW) / P.Wb;
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * STAGE_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], bytes);
@@ -391,7 +388,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
             tc::tma_load_4d(sa + j * HALF_A, &tmX, &full[stage], ci0j[j], kw - P.p, P.s * i0 + kh - P.p, b0);
           }
           for (int nb = 0; nb < BN / 64; ++nb)
-            tc::tma_load_2d(sa + 2 * HALF_A + nb * HALF_A, &tmDZ, &full[stage], nt * BN + nb * 64, p0);
+            tc::tma_load_4d(sa + 2 * HALF_A + nb * HALF_A, &tmDZ, &full[stage], nt * BN + nb * 64, 0, i0, b0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -535,26 +532,34 @@ CUtensorMap mat_map(const __nv_bfloat16 *w, int rows, int K, int box_rows) {
   return make_map(w, 2, dims, st, box, es);
 }
 
-// A tile of `rows` GEMM rows must be a rectangle of whole grid rows (or whole images)
+// The output grid Gh x Gw of each image is embedded in a padded grid Hb x Wb so that
+// a tile of `rows_per_tile` GEMM rows is a rectangle of whole padded rows (NB = 1,
+// R rows of one image) or of NB whole padded images (R = Hb).  Wb = next power of two
+// >= Gw; images are padded up to a multiple of NB.  M = Bpad * Hb * Wb.
 struct Tiling {
-  int R, NB;
+  int Hb, Wb, R, NB, Bpad;
   bool ok;
+  int64_t M() const { return (int64_t)Bpad * Hb * Wb; }
 };
 Tiling tiling(int B, int Gh, int Gw, int rows_per_tile) {
-  Tiling t{0, 0, false};
-  if (Gw > rows_per_tile || rows_per_tile % Gw) return t;
-  int rows = rows_per_tile / Gw;
+  Tiling t{0, 0, 0, 0, 0, false};
+  int wb = 1;
+  while (wb < Gw) wb <<= 1;
+  if (wb > rows_per_tile) return t;
+  t.Wb = wb;
+  const int rows = rows_per_tile / wb;
   if (rows <= Gh) {
-    if (Gh % rows) return t;
     t.R = rows;
     t.NB = 1;
+    t.Hb = (int)cdiv(Gh, rows) * rows;
   } else {
-    if (rows % Gh) return t;
-    t.R = Gh;
-    t.NB = rows / Gh;
-    if (B % t.NB) return t;
+    int hb = 1;
+    while (hb < Gh) hb <<= 1;  // hb <= rows: both powers of two, Gh < rows
+    t.Hb = t.R = hb;
+    t.NB = rows / hb;
   }
-  t.ok = true;
+  t.Bpad = (int)cdiv(B, t.NB) * t.NB;
+  t.ok = t.M() < (int64_t)1 << 31;
   return t;
 }
 
@@ -627,7 +632,7 @@ int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, f
             cudaStream_t st) {
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
   ConvTCParams P{};
-  P.M = (int)g.M();
+  P.M = (int)t.M();
   P.N = g.Co;
   P.Cred = g.Ci;
   P.CB = g.Ci / 64;
@@ -639,13 +644,16 @@ int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, f
   }
   P.Gh = g.Ho;
   P.Gw = g.Wo;
+  P.Hb = t.Hb;
+  P.Wb = t.Wb;
+  P.B = g.B;
   P.s_in = g.s;
   P.OH = g.Ho;
   P.OW = g.Wo;
   P.oss = 1;
   P.out = out;
   P.stats = stats;
-  CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, g.Wo, t.R, t.NB, g.s);
+  CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, t.Wb, t.R, t.NB, g.s);
   launch_any(ta, w, g.Co, g.K(), P, ws, st);
   if (!P.stats) return 0;
   const int BN = conv_plan(P.M, P.N, P.ntaps * P.CB).BN;
@@ -657,14 +665,17 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *
   // A = dz [B][Ho][Wo][Co] (stride-1 boxes), B = wT [Ci][k*k*Co], N = Ci
   const int wK = g.k * g.k * g.Co;
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
-  CUtensorMap ta = act_map(dz, g.B, g.Ho, g.Wo, g.Co, g.Wo, t.R, t.NB, 1);
+  CUtensorMap ta = act_map(dz, g.B, g.Ho, g.Wo, g.Co, t.Wb, t.R, t.NB, 1);
   ConvTCParams P{};
-  P.M = (int)g.M();
+  P.M = (int)t.M();
   P.N = g.Ci;
   P.Cred = g.Co;
   P.CB = g.Co / 64;
   P.Gh = g.Ho;
   P.Gw = g.Wo;
+  P.Hb = t.Hb;
+  P.Wb = t.Wb;
+  P.B = g.B;
   P.s_in = 1;
   P.OH = g.H;
   P.OW = g.W;
@@ -715,21 +726,20 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *
 }
 
 struct WgradPlan {
-  int BN, splits, kb_per_split, n_mt, n_nt, KBtot, R, NB;
+  int BN, splits, kb_per_split, n_mt, n_nt, KBtot;
+  Tiling t;
 };
 WgradPlan wgrad_plan(const ConvGeom &g) {
   WgradPlan w{};
   w.BN = g.Co % 256 == 0 ? 256 : (g.Co % 128 == 0 ? 128 : 64);
   w.n_nt = g.Co / w.BN;
   w.n_mt = (int)cdiv((int64_t)g.k * g.k * g.Ci, 128);
-  w.KBtot = (int)(g.M() / 64);
+  w.t = tiling(g.B, g.Ho, g.Wo, 64);
+  w.KBtot = (int)(w.t.M() / 64);
   int tiles = w.n_mt * w.n_nt;
   int want = std::max(1, std::min(w.KBtot, (int)cdiv(kNumSMs, tiles)));
   w.kb_per_split = (int)cdiv(w.KBtot, want);
   w.splits = (int)cdiv(w.KBtot, w.kb_per_split);
-  Tiling t = tiling(g.B, g.Ho, g.Wo, 64);
-  w.R = t.R;
-  w.NB = t.NB;
   return w;
 }
 
@@ -761,13 +771,12 @@ void conv_tc_prepare() {
     setw((const void *)wgrad_tc_kernel<128, 4>, 4, 128);
     setw((const void *)wgrad_tc_kernel<64, 6>, 6, 64);
   });
+  stem_tc_prepare();
 }
 
 bool conv_tc_supported(const ConvGeom &g, int mode) {
   if (!geom_ok(g)) return false;
-  if (mode == 2) return g.M() % 64 == 0 && tiling(g.B, g.Ho, g.Wo, 64).ok;
-  if (g.M() % BM) return false;
-  return tiling(g.B, g.Ho, g.Wo, BM).ok;
+  return tiling(g.B, g.Ho, g.Wo, mode == 2 ? 64 : BM).ok;
 }
 
 size_t conv_tc_workspace(const ConvGeom &g, int mode) {
@@ -778,8 +787,9 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode) {
   }
   const int N = mode == 0 ? g.Co : g.Ci;
   const int KB = (mode == 0 ? g.k * g.k * g.Ci : g.k * g.k * g.Co) / 64;  // upper bound (all taps)
-  ConvPlan p = conv_plan((int)g.M(), N, KB);
-  return p.splits > 1 ? (size_t)p.splits * g.M() * N * sizeof(float) : 0;
+  const int64_t M = tiling(g.B, g.Ho, g.Wo, BM).M();
+  ConvPlan p = conv_plan((int)M, N, KB);
+  return p.splits > 1 ? (size_t)p.splits * M * N * sizeof(float) : 0;
 }
 
 int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32, float *ws,
@@ -798,11 +808,21 @@ void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat
   run_dgrad(g, dz, wt, addend, dx, ws, st);
 }
 
+CUtensorMap kmajor_map_bf16(const __nv_bfloat16 *m, int rows, int K, int box_rows) {
+  return mat_map(m, rows, K, box_rows);
+}
+
+void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st) {
+  splitk_sum_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st>>>(part, splits, n, out);
+  PETRA_LAUNCH_CHECK();
+}
+
 void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *x, float *dw, float *ws,
                    cudaStream_t st) {
   WgradPlan w = wgrad_plan(g);
-  CUtensorMap tx = act_map(x, g.B, g.H, g.W, g.Ci, g.Wo, w.R, w.NB, g.s);
-  CUtensorMap tdz = mat_map(dz, (int)g.M(), g.Co, 64);  // dz as [pixels][Co], box (64 ch, 64 pixels)
+  CUtensorMap tx = act_map(x, g.B, g.H, g.W, g.Ci, w.t.Wb, w.t.R, w.t.NB, g.s);
+  // dz [B][Ho][Wo][Co], box (64 ch, 64 padded pixels); padding pixels out of bounds -> 0
+  CUtensorMap tdz = act_map(dz, g.B, g.Ho, g.Wo, g.Co, w.t.Wb, w.t.R, w.t.NB, 1);
   WgradParams P{};
   P.Mr = g.K();
   P.N = g.Co;
@@ -810,8 +830,8 @@ void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat
   P.k = g.k;
   P.p = g.p;
   P.s = g.s;
-  P.Gh = g.Ho;
-  P.Gw = g.Wo;
+  P.Hb = w.t.Hb;
+  P.Wb = w.t.Wb;
   P.KBtot = w.KBtot;
   P.kb_per_split = w.kb_per_split;
   P.n_mt = w.n_mt;
@@ -821,11 +841,7 @@ void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat
   if (w.BN == 256) launch_wgrad<256, 3>(tx, tdz, P, st);
   else if (w.BN == 128) launch_wgrad<128, 4>(tx, tdz, P, st);
   else launch_wgrad<64, 6>(tx, tdz, P, st);
-  if (w.splits > 1) {
-    int64_t n = (int64_t)g.Co * g.K();
-    splitk_sum_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st>>>(ws, w.splits, n, dw);
-    PETRA_LAUNCH_CHECK();
-  }
+  if (w.splits > 1) splitk_sum(ws, w.splits, (int64_t)g.Co * g.K(), dw, st);
 }
 
 }  // namespace petra

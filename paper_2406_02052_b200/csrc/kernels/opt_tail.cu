@@ -226,6 +226,62 @@ __global__ void maxpool_bwd_kernel(const float *__restrict__ d1, const float *__
   }
 }
 
+// vectorised variants (C % 8 == 0, 32-bit indexing): one thread = 4 channels of one
+// pixel, float4 loads/stores, the 4 argmax bytes as one 32-bit word
+__global__ void maxpool_fwd_v4_kernel(const float4 *__restrict__ a, int B, int H, int W, int C4, int Ho, int Wo,
+                                      float4 *__restrict__ o1, float4 *__restrict__ o2, uchar4 *__restrict__ arg) {
+  const int n = B * Ho * Wo * C4, Ch4 = C4 / 2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = i % C4, pix = i / C4, wo = pix % Wo, r = pix / Wo, ho = r % Ho, b = r / Ho;
+    float4 best = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    uchar4 bi = make_uchar4(0, 0, 0, 0);
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw) {
+        const int h = ho * 2 + kh - 1, w = wo * 2 + kw - 1;
+        if (h < 0 || h >= H || w < 0 || w >= W) continue;
+        const float4 v = a[((b * H + h) * W + w) * C4 + c];
+        const unsigned char t = (unsigned char)(kh * 3 + kw);
+        if (v.x > best.x) { best.x = v.x; bi.x = t; }  // strict >: first index wins ties
+        if (v.y > best.y) { best.y = v.y; bi.y = t; }
+        if (v.z > best.z) { best.z = v.z; bi.z = t; }
+        if (v.w > best.w) { best.w = v.w; bi.w = t; }
+      }
+    arg[i] = bi;
+    if (c < Ch4) o1[pix * Ch4 + c] = best;
+    else o2[pix * Ch4 + c - Ch4] = best;
+  }
+}
+
+__global__ void maxpool_bwd_v4_kernel(const float4 *__restrict__ d1, const float4 *__restrict__ d2,
+                                      const uchar4 *__restrict__ arg, int B, int H, int W, int C4, int Ho, int Wo,
+                                      float4 *__restrict__ da) {
+  const int n = B * H * W * C4, Ch4 = C4 / 2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = i % C4, pix = i / C4, w = pix % W, r = pix / W, h = r % H, b = r / H;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    // output windows (ho, wo) with 2*ho-1 <= h <= 2*ho+1, in increasing (ho, wo) order
+    for (int ho = h / 2; ho <= min(Ho - 1, (h + 1) / 2); ++ho) {
+      const int kh = h - (ho * 2 - 1);
+      if (kh < 0 || kh > 2) continue;
+      for (int wo = w / 2; wo <= min(Wo - 1, (w + 1) / 2); ++wo) {
+        const int kw = w - (wo * 2 - 1);
+        if (kw < 0 || kw > 2) continue;
+        const int op = (b * Ho + ho) * Wo + wo;
+        const uchar4 g = arg[op * C4 + c];
+        const float4 d = c < Ch4 ? d1[op * Ch4 + c] : d2[op * Ch4 + c - Ch4];
+        const unsigned char t = (unsigned char)(kh * 3 + kw);
+        if (g.x == t) s.x += d.x;
+        if (g.y == t) s.y += d.y;
+        if (g.z == t) s.z += d.z;
+        if (g.w == t) s.w += d.w;
+      }
+    }
+    da[i] = s;
+  }
+}
+
 __global__ void f32_to_bf16_kernel(const float *__restrict__ x, __nv_bfloat16 *__restrict__ y, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = __float2bfloat16_rn(x[i]);
@@ -268,13 +324,27 @@ void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int 
 
 void maxpool_fwd(const float *a, int B, int H, int W, int C, int Ho, int Wo, float *o1, float *o2, uint8_t *arg,
                  cudaStream_t st) {
-  maxpool_fwd_kernel<<<ew_grid((int64_t)B * Ho * Wo * C), 256, 0, st>>>(a, B, H, W, C, Ho, Wo, o1, o2, arg);
+  if (C % 8 == 0 && (int64_t)B * H * W * C < ((int64_t)1 << 31)) {
+    const int C4 = C / 4;
+    maxpool_fwd_v4_kernel<<<ew_grid((int64_t)B * Ho * Wo * C4), 256, 0, st>>>(
+        reinterpret_cast<const float4 *>(a), B, H, W, C4, Ho, Wo, reinterpret_cast<float4 *>(o1),
+        reinterpret_cast<float4 *>(o2), reinterpret_cast<uchar4 *>(arg));
+  } else {
+    maxpool_fwd_kernel<<<ew_grid((int64_t)B * Ho * Wo * C), 256, 0, st>>>(a, B, H, W, C, Ho, Wo, o1, o2, arg);
+  }
   PETRA_LAUNCH_CHECK();
 }
 
 void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, int H, int W, int C, int Ho, int Wo,
                  float *da, cudaStream_t st) {
-  maxpool_bwd_kernel<<<ew_grid((int64_t)B * H * W * C), 256, 0, st>>>(d1, d2, arg, B, H, W, C, Ho, Wo, da);
+  if (C % 8 == 0 && (int64_t)B * H * W * C < ((int64_t)1 << 31)) {
+    const int C4 = C / 4;
+    maxpool_bwd_v4_kernel<<<ew_grid((int64_t)B * H * W * C4), 256, 0, st>>>(
+        reinterpret_cast<const float4 *>(d1), reinterpret_cast<const float4 *>(d2),
+        reinterpret_cast<const uchar4 *>(arg), B, H, W, C4, Ho, Wo, reinterpret_cast<float4 *>(da));
+  } else {
+    maxpool_bwd_kernel<<<ew_grid((int64_t)B * H * W * C), 256, 0, st>>>(d1, d2, arg, B, H, W, C, Ho, Wo, da);
+  }
   PETRA_LAUNCH_CHECK();
 }
 

@@ -1,0 +1,472 @@
+// stem_tc.cu -- tcgen05 convolutions for inputs with few channels (the stem).
+//
+// forward  z[m][co] = sum_{kk} A[m][kk] * w[co][kk],   kk = (kh*k + kw)*Ci + c,  K = k*k*Ci
+// wgrad    dw[co][kk] = sum_m dz[m][co] * A[m][kk]
+// with the implicit im2col A[m][kk] = bf16(x[b][s*ho+kh-p][s*wo+kw-p][c]) (0 outside).
+//
+// The TMA im2col boxes of conv_tc.cu need 64 channels per tap; a 3-channel image
+// (K = 147 for the ImageNet 7x7/s2 stem, 27 for the CIFAR 3x3 stem) has 3.  Here
+// the A operand is GATHERED: 8 producer warps build each 128 x 64 (fwd, K-major) or
+// 64 x 128 (wgrad, MN-major) bf16 tile straight from the fp32 NHWC input into the
+// 128B-swizzled smem layout UMMA reads (a per-kk offset table in smem, an unchecked
+// fast path for interior pixels), then publish it with fence.proxy.async + mbarrier.
+// No im2col tensor ever touches HBM; the fp32 -> bf16 conversion of the image is
+// fused into the gather.  The weights (fwd) sit in smem for the whole persistent CTA.
+// Warp roles: 0-7 gather producers, 8-11 epilogue (TMEM lane quarters 0-3), 12 MMA.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "../errors.h"
+#include "../kernels.h"
+#include "tc_common.cuh"
+
+namespace petra {
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kThreads = 13 * 32;
+constexpr int kProducers = 256;
+constexpr uint32_t kATile = 128 * 64 * 2;  // 16 KB
+constexpr int kMaxKK = 256;
+
+struct StemParams {
+  const float *x;  // [B][H][W][Ci] fp32
+  const float *w;  // [Co][K] fp32 (forward)
+  int B, H, W, Ci, k, s, p, Ho, Wo;
+  int M, K, N;
+  int KB;                              // forward: 64-wide K blocks
+  int n_mt, KBtot, kb_per_split, splits;  // wgrad: kk tiles of 128, pixel blocks of 64, split-K
+  float *out;
+  float *stats;
+};
+
+// kk -> (input offset relative to the receptive-field corner, (kh << 16) | kw); -1 = zero pad
+__device__ void fill_table(const StemParams &P, int2 *tab, int n) {
+  for (int kk = threadIdx.x; kk < n; kk += blockDim.x) {
+    if (kk < P.K) {
+      const int tap = kk / P.Ci, c = kk % P.Ci, kh = tap / P.k, kw = tap % P.k;
+      tab[kk] = make_int2((kh * P.W + kw) * P.Ci + c, (kh << 16) | kw);
+    } else {
+      tab[kk] = make_int2(0, -1);
+    }
+  }
+}
+
+struct Pixel {
+  int64_t base;
+  int hi0, wi0;
+  bool valid, interior;
+};
+
+__device__ __forceinline__ Pixel pixel(const StemParams &P, int m) {
+  Pixel q{0, 0, 0, m < P.M, false};
+  if (!q.valid) return q;
+  const int hw = P.Ho * P.Wo;
+  const int b = m / hw, r = m % hw, ho = r / P.Wo, wo = r % P.Wo;
+  q.hi0 = ho * P.s - P.p;
+  q.wi0 = wo * P.s - P.p;
+  q.interior = q.hi0 >= 0 && q.wi0 >= 0 && q.hi0 + P.k <= P.H && q.wi0 + P.k <= P.W;
+  q.base = (((int64_t)b * P.H + q.hi0) * P.W + q.wi0) * P.Ci;
+  return q;
+}
+
+__device__ __forceinline__ float gather1(const StemParams &P, const Pixel &q, int2 t) {
+  if (!q.valid || t.y < 0) return 0.f;
+  if (!q.interior) {
+    const int hi = q.hi0 + (t.y >> 16), wi = q.wi0 + (t.y & 0xffff);
+    if (hi < 0 || hi >= P.H || wi < 0 || wi >= P.W) return 0.f;
+  }
+  return __ldg(P.x + q.base + t.x);
+}
+
+// 32 consecutive kk of one pixel -> 16 packed bf16 pairs
+__device__ __forceinline__ void gather32(const StemParams &P, const int2 *tab, int kk0, const Pixel &q,
+                                         uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    const float v0 = gather1(P, q, tab[kk0 + e]), v1 = gather1(P, q, tab[kk0 + e + 1]);
+    __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
+    pk[e >> 1] = *reinterpret_cast<uint32_t *>(&h);
+  }
+}
+
+// four 16-byte chunks (chunk index c0..c0+3) of row `row` of a 128B-swizzled tile
+__device__ __forceinline__ void store_row_chunks(uint8_t *tile, int row, int c0, const uint32_t (&pk)[16]) {
+  uint8_t *dst = tile + (row >> 3) * 1024 + (row & 7) * 128;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    *reinterpret_cast<uint4 *>(dst + (((c0 + i) ^ (row & 7)) << 4)) =
+        make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_constant__ StemParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + kStages * kATile;  // [KB][BN rows x 128 B], resident
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + (size_t)P.KB * BN * 128);
+  uint64_t *empty = full + kStages;
+  uint64_t *tfull = empty + kStages;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  int2 *tab = reinterpret_cast<int2 *>(tmem_slot + 4);
+  float *sstat = reinterpret_cast<float *>(tab + kMaxKK);  // [4][N][2]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (int)cdiv(P.M, 128);
+  fill_table(P, tab, P.KB * 64);
+  // weights fp32 [Co][K] -> bf16 K-major swizzled tiles (zero beyond K)
+  const int kchunks = P.KB * 8;
+  for (int i = threadIdx.x; i < BN * kchunks; i += blockDim.x) {
+    const int n = i / kchunks, r = i % kchunks, kb = r >> 3, c = r & 7;
+    uint32_t pk[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const int kk = kb * 64 + c * 8 + e;
+      const float v0 = kk < P.K ? P.w[(int64_t)n * P.K + kk] : 0.f;
+      const float v1 = kk + 1 < P.K ? P.w[(int64_t)n * P.K + kk + 1] : 0.f;
+      __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
+      pk[e >> 1] = *reinterpret_cast<uint32_t *>(&h);
+    }
+    uint8_t *dst = sB + (size_t)kb * BN * 128 + (n >> 3) * 1024 + (n & 7) * 128 + ((c ^ (n & 7)) << 4);
+    *reinterpret_cast<uint4 *>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+  tc::fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full[s], kProducers);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 12) tc::tmem_alloc(tmem_slot, 2 * BN);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < 8) {  // ---------------- gather producers: thread -> (row, half of the 64 kk)
+    const int row = threadIdx.x & 127, half = threadIdx.x >> 7;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const Pixel q = pixel(P, t * 128 + row);
+      for (int kb = 0; kb < P.KB; ++kb) {
+        uint32_t pk[16];
+        gather32(P, tab, kb * 64 + half * 32, q, pk);  // loads in flight before the wait
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        store_row_chunks(sA + stage * kATile, row, half * 4, pk);
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&full[stage]);
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 12) {  // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(128, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t dtm = tmem_base + acc * BN;
+        for (int kb = 0; kb < P.KB; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint64_t ad = tc::sw128_desc(tc::smem_u32(sA + stage * kATile), 16, 1024);
+          const uint64_t bd = tc::sw128_desc(tc::smem_u32(sB + (size_t)kb * BN * 128), 16, 1024);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          tc::umma_commit(&empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        tc::umma_commit(&tfull[acc]);
+      }
+    }
+  } else {  // ---------------- epilogue warps 8..11
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    float *my_stat = sstat + (size_t)q * P.N * 2;
+    if (P.stats)
+      for (int i = lane; i < 2 * P.N; i += 32) my_stat[i] = 0.f;
+    __syncwarp();
+    int it = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      const int m = t * 128 + row;
+      const bool valid = m < P.M;
+      float *orow = P.out + (int64_t)m * P.N;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+        if (valid) {
+#pragma unroll
+          for (int jj = 0; jj < 16; jj += 4)
+            *reinterpret_cast<float4 *>(orow + c + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
+        }
+        if (P.stats) {
+          float sq[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) sq[jj] = v[jj] * v[jj];
+          tc::colsum16(v, lane);
+          tc::colsum16(sq, lane);
+          if (!(lane & 1)) {
+            const int col = c + (lane >> 1);
+            my_stat[2 * col] += v[0];
+            my_stat[2 * col + 1] += sq[0];
+          }
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+    if (P.stats) {
+      __syncwarp();
+      float *g = P.stats + ((size_t)blockIdx.x * 4 + q) * P.N * 2;
+      for (int i = lane; i < 2 * P.N; i += 32) g[i] = my_stat[i];
+    }
+  }
+  __syncthreads();
+  if (warp == 12) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+// wgrad: D[kk][co] = sum_pixels A[pixel][kk] dz[pixel][co]; M side = kk (tiles of 128),
+// N side = co, K = pixels (blocks of 64, split over CTAs).  A and B are MN-major:
+// A = two 64-kk blocks of [64 pixel rows x 128 B] gathered, B = BN/64 TMA boxes of dz.
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+stem_wgrad_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constant__ StemParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t B_BYTES = BN * 64 * 2;
+  constexpr uint32_t STAGE_BYTES = kATile + B_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * STAGE_BYTES);
+  uint64_t *empty = full + kStages;
+  uint64_t *tfull = empty + kStages;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  int2 *tab = reinterpret_cast<int2 *>(tmem_slot + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_work = P.n_mt * P.splits;
+  fill_table(P, tab, P.n_mt * 128);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full[s], kProducers + 1);  // + the expect_tx arrival of the dz TMA
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);
+    }
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&tmDZ);
+  }
+  if (warp == 12) tc::tmem_alloc(tmem_slot, 2 * BN);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < 8) {
+    const int r = threadIdx.x & 63, qq = threadIdx.x >> 6, j = qq >> 1, half = qq & 1;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const int sp = w % P.splits, mt = w / P.splits;
+      const int kb0 = sp * P.kb_per_split, kb1 = min(P.KBtot, kb0 + P.kb_per_split);
+      const int kk0 = mt * 128 + j * 64 + half * 32;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const Pixel q = pixel(P, kb * 64 + r);
+        uint32_t pk[16];
+        gather32(P, tab, kk0, q, pk);
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t *sa = smem + stage * STAGE_BYTES;
+        if (threadIdx.x == 0) {
+          tc::mbar_arrive_expect_tx(&full[stage], B_BYTES);
+          for (int nb = 0; nb < BN / 64; ++nb)
+            tc::tma_load_2d(sa + kATile + nb * 8192, &tmDZ, &full[stage], nb * 64, kb * 64);
+        }
+        store_row_chunks(sa + j * 8192, r, half * 4, pk);
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&full[stage]);
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 12) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(128, BN, 1, 1);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+        const int sp = w % P.splits;
+        const int kb0 = sp * P.kb_per_split, kb1 = min(P.KBtot, kb0 + P.kb_per_split);
+        const int acc = it & 1;
+        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t dtm = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
+          const uint64_t ad = tc::sw128_desc(sa, 8192, 1024);
+          const uint64_t bd = tc::sw128_desc(sa + kATile, 8192, 1024);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // 16 pixels = 16 rows x 128 B per step
+            tc::umma_bf16(dtm, ad + (uint64_t)(k * 2048 >> 4), bd + (uint64_t)(k * 2048 >> 4), idesc,
+                          (kb > kb0 || k) ? 1u : 0u);
+          tc::umma_commit(&empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        tc::umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      const int sp = w % P.splits, mt = w / P.splits;
+      const int acc = it & 1;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      const int r = mt * 128 + row;
+      float *o = P.out + (int64_t)sp * P.N * P.K;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+        if (r < P.K) {
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) o[(int64_t)(c + jj) * P.K + r] = v[jj];
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 12) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+StemParams base_params(const ConvGeom &g) {
+  StemParams P{};
+  P.B = g.B; P.H = g.H; P.W = g.W; P.Ci = g.Ci; P.k = g.k; P.s = g.s; P.p = g.p; P.Ho = g.Ho; P.Wo = g.Wo;
+  P.M = (int)g.M();
+  P.K = g.K();
+  P.N = g.Co;
+  P.KB = (int)cdiv(P.K, 64);
+  return P;
+}
+
+size_t fwd_smem(int BN, int KB) {
+  return 1024 + (size_t)kStages * kATile + (size_t)KB * BN * 128 + 256 + kMaxKK * 8 + (size_t)4 * BN * 2 * 4;
+}
+size_t wgrad_smem(int BN) { return 1024 + (size_t)kStages * (kATile + BN * 128) + 256 + kMaxKK * 8; }
+
+struct WPlan {
+  int n_mt, KBtot, kb_per_split, splits;
+};
+WPlan wplan(const ConvGeom &g) {
+  WPlan w{};
+  w.n_mt = (int)cdiv(g.K(), 128);
+  w.KBtot = (int)cdiv(g.M(), 64);
+  const int want = std::max(1, std::min(w.KBtot, (int)cdiv(kNumSMs, w.n_mt)));
+  w.kb_per_split = (int)cdiv(w.KBtot, want);
+  w.splits = (int)cdiv(w.KBtot, w.kb_per_split);
+  return w;
+}
+
+}  // namespace
+
+void stem_tc_prepare() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto set = [](const void *f, size_t smem) {
+      PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    };
+    set((const void *)stem_fwd_kernel<64>, fwd_smem(64, 4));
+    set((const void *)stem_fwd_kernel<128>, fwd_smem(128, 4));
+    set((const void *)stem_fwd_kernel<256>, fwd_smem(256, 4));
+    set((const void *)stem_wgrad_kernel<64>, wgrad_smem(64));
+    set((const void *)stem_wgrad_kernel<128>, wgrad_smem(128));
+    set((const void *)stem_wgrad_kernel<256>, wgrad_smem(256));
+  });
+}
+
+bool stem_tc_supported(const ConvGeom &g) {
+  return g.Ci >= 1 && g.Ci < 64 && g.K() <= kMaxKK && g.Co % 64 == 0 && g.Co <= 256 &&
+         g.M() < ((int64_t)1 << 31) && g.Min() * g.Ci < ((int64_t)1 << 31);
+}
+
+size_t stem_tc_workspace(const ConvGeom &g) {
+  if (!stem_tc_supported(g)) return 0;
+  WPlan w = wplan(g);
+  return w.splits > 1 ? (size_t)w.splits * g.Co * g.K() * sizeof(float) : 0;
+}
+
+int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, float *z, float *stats_part, cudaStream_t st) {
+  if (!stem_tc_supported(g)) throw PetraError(PETRA_E_UNSUPPORTED, "stem_fwd_tc: geometry");
+  stem_tc_prepare();
+  StemParams P = base_params(g);
+  P.x = x;
+  P.w = w;
+  P.out = z;
+  P.stats = stats_part;
+  const int grid = (int)std::min<int64_t>(cdiv(P.M, 128), kNumSMs);
+  const size_t smem = fwd_smem(P.N, P.KB);
+  if (P.N == 64) stem_fwd_kernel<64><<<grid, kThreads, smem, st>>>(P);
+  else if (P.N == 128) stem_fwd_kernel<128><<<grid, kThreads, smem, st>>>(P);
+  else stem_fwd_kernel<256><<<grid, kThreads, smem, st>>>(P);
+  PETRA_LAUNCH_CHECK();
+  return stats_part ? grid * 4 : 0;
+}
+
+void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const float *x, float *dw, float *ws,
+                   cudaStream_t st) {
+  if (!stem_tc_supported(g)) throw PetraError(PETRA_E_UNSUPPORTED, "stem_wgrad_tc: geometry");
+  stem_tc_prepare();
+  StemParams P = base_params(g);
+  WPlan wp = wplan(g);
+  P.x = x;
+  P.n_mt = wp.n_mt;
+  P.KBtot = wp.KBtot;
+  P.kb_per_split = wp.kb_per_split;
+  P.splits = wp.splits;
+  if (wp.splits > 1 && !ws) throw PetraError(PETRA_E_ARG, "stem_wgrad_tc: workspace required");
+  P.out = wp.splits > 1 ? ws : dw;
+  CUtensorMap tdz = kmajor_map_bf16(dz, P.M, P.N, 64);  // dz [pixels][Co], box (64 ch, 64 pixels)
+  const int grid = std::min(wp.n_mt * wp.splits, kNumSMs);
+  const size_t smem = wgrad_smem(P.N);
+  if (P.N == 64) stem_wgrad_kernel<64><<<grid, kThreads, smem, st>>>(tdz, P);
+  else if (P.N == 128) stem_wgrad_kernel<128><<<grid, kThreads, smem, st>>>(tdz, P);
+  else stem_wgrad_kernel<256><<<grid, kThreads, smem, st>>>(tdz, P);
+  PETRA_LAUNCH_CHECK();
+  if (wp.splits > 1) splitk_sum(ws, wp.splits, (int64_t)g.Co * g.K(), dw, st);
+}
+
+}  // namespace petra

@@ -37,6 +37,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// generic-proxy smem writes (st.shared) made visible to the async proxy (tcgen05.mma)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- TMA (bulk tensor copies, zero-filled OOB)
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap *m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
@@ -115,5 +120,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Column sums of a 32-row x 16-column fragment held one row per lane: butterfly
+// transpose-reduce (8+4+2+1+1 shuffles).  Afterwards lane L holds the sum over the
+// 32 rows of column (L >> 1) in x[0] (lanes 2k, 2k+1 both).
+__device__ __forceinline__ void colsum16(float (&x)[16], int lane) {
+#pragma unroll
+  for (int half = 8, off = 16; half >= 1; half >>= 1, off >>= 1) {
+    const bool upper = lane & off;
+#pragma unroll
+    for (int k = 0; k < half; ++k) {
+      float send = upper ? x[k] : x[k + half];
+      float keep = upper ? x[k + half] : x[k];
+      x[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  x[0] += __shfl_xor_sync(0xffffffffu, x[0], 1);
+}
+
 }  // namespace tc
+
+// host: 2-D TMA map of a row-major bf16 matrix [rows][K], 128B swizzle, box (64 K, box_rows)
+CUtensorMap kmajor_map_bf16(const __nv_bfloat16 *m, int rows, int K, int box_rows);
+
 }  // namespace petra

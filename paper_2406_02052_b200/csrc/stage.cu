@@ -239,6 +239,7 @@ void Stage::build() {
     max_ws = std::max(max_ws, conv_wgrad_simt_workspace(p.L->g));
     if (tc_)
       for (int mode = 0; mode < 3; ++mode) max_ws = std::max(max_ws, conv_tc_workspace(p.L->g, mode));
+    if (tc_) max_ws = std::max(max_ws, stem_tc_workspace(p.L->g));
   }
   part_ = dalloc(std::max<size_t>(max_part, 16));
   size_t max_ctr = 1;
@@ -407,6 +408,11 @@ static double conv_bytes(const ConvGeom &g, int esz) {
 
 void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready) {
   const float *w = theta_->as<float>() + L.w_off;
+  if (tc_ && stem_tc_supported(L.g)) {  // few input channels: gathered im2col, fp32 x read directly
+    ProfScope ps("conv_fwd_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 4));
+    L.stats_rows = stem_fwd_tc(L.g, x, w, L.z->as<float>(), reinterpret_cast<float *>(part_->p), st);
+    return;
+  }
   bool tc = tc_ && conv_tc_supported(L.g, 0);
   if (tc && !x_bf16_ready) {  // bf16 operand of a stream input (also read by the TC wgrad)
     ProfScope pc("cvt_bf16", st, 0.0, 6.0 * (double)L.g.Min() * L.g.Ci);
@@ -423,6 +429,11 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
 
 void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   float *dw = grad_->as<float>() + L.w_off;
+  if (tc_ && stem_tc_supported(L.g)) {
+    ProfScope ps("conv_wgrad_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2));
+    stem_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), x, dw, wgrad_ws_->as<float>(), st);
+    return;
+  }
   bool tc = tc_ && conv_tc_supported(L.g, 2);
   ProfScope ps(tc ? "conv_wgrad_tc" : "conv_wgrad_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
@@ -497,7 +508,8 @@ void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, cons
                        gr + L.g_off, gr + L.b_off, part_->as<double>(), counters_->as<unsigned>(), st);
   }
   // dz in bf16 for tensor-core dgrad / wgrad, in fp32 only if a SIMT pass consumes it
-  const bool tc_d = tc_ && conv_tc_supported(L.g, 1), tc_w = tc_ && conv_tc_supported(L.g, 2);
+  const bool tc_d = tc_ && conv_tc_supported(L.g, 1);
+  const bool tc_w = tc_ && (conv_tc_supported(L.g, 2) || stem_tc_supported(L.g));
   float *dz32 = (!tc_d || !tc_w) ? L.dz->as<float>() : nullptr;
   __nv_bfloat16 *dz16 = (tc_d || tc_w) ? L.dzb->as<__nv_bfloat16>() : nullptr;
   ProfScope ps("bn_bwd_dz", st, 0.0, 8.0 * n + (dz32 ? 4.0 : 0.0) * n + (dz16 ? 2.0 : 0.0) * n);

@@ -46,6 +46,11 @@ GEOMS = [  # (B, H, W, Ci, Co, k, stride)
     # stride-2 downsampling convs (R18 DS units: 3x3/s2 Phi_s, 1x1/s2 projections)
     (2, 32, 32, 64, 128, 3, 2), (2, 32, 32, 64, 128, 1, 2), (8, 16, 16, 128, 256, 3, 2),
     (8, 8, 8, 256, 512, 3, 2), (8, 8, 8, 256, 512, 1, 2),
+    # ImageNet / ResNet-50 grids (56, 28, 14, 7): padded tiles (Wb = 64, 32, 16, 8), masked rows
+    (2, 56, 56, 64, 64, 3, 1), (2, 56, 56, 64, 256, 1, 1), (2, 28, 28, 128, 128, 3, 1),
+    (2, 14, 14, 256, 256, 3, 1), (3, 7, 7, 512, 512, 3, 1), (2, 56, 56, 64, 128, 3, 2),
+    (2, 28, 28, 128, 256, 1, 2), (3, 14, 14, 256, 512, 3, 2), (1, 12, 20, 64, 64, 3, 1),
+    (2, 14, 14, 128, 64, 1, 1), (2, 14, 14, 64, 64, 3, 1), (2, 14, 14, 64, 128, 1, 1),
 ]
 SIMT_GEOMS = GEOMS[:2] + [(2, 9, 7, 3, 16, 3, 1), (2, 10, 10, 16, 32, 3, 2), (2, 9, 9, 8, 12, 1, 2),
                           (2, 15, 15, 3, 8, 7, 2)]
@@ -87,4 +92,22 @@ def test_tc_conv_vs_simt(geom, mode):
     assert L.lib().petra_conv_engine(C.byref(L.PetraConvGeom(*geom)), mode, L.BF16_TC) == 1
     ref = conv_run(mode, 0, geom, a, b, addend)
     got = conv_run(mode, 1, geom, a, b, addend)
+    assert rel(got, ref) < 1e-5, rel(got, ref)
+
+
+# stems: few input channels -> the gathered-im2col tensor-core kernels (forward, wgrad)
+STEM_GEOMS = [(4, 32, 32, 3, 64, 3, 1), (2, 30, 30, 3, 64, 7, 2), (3, 17, 19, 3, 128, 7, 2),
+              (1, 224, 224, 3, 64, 7, 2), (2, 12, 12, 5, 256, 5, 1), (2, 16, 16, 16, 64, 3, 1)]
+
+
+@pytest.mark.parametrize("geom", STEM_GEOMS)
+@pytest.mark.parametrize("mode", [0, 2])
+def test_stem_tc_vs_simt(geom, mode):
+    x, w, dz, _ = inputs(geom, 5)
+    a = x if mode == 0 else dz
+    b = w if mode == 0 else x
+    assert L.lib().petra_conv_engine(C.byref(L.PetraConvGeom(*geom)), mode, L.BF16_TC) == 1
+    assert L.lib().petra_conv_engine(C.byref(L.PetraConvGeom(*geom)), 1, L.BF16_TC) == 0  # no stem dgrad
+    ref = conv_run(mode, 0, geom, a, b)
+    got = conv_run(mode, 1, geom, a, b)
     assert rel(got, ref) < 1e-5, rel(got, ref)

@@ -83,6 +83,27 @@ STAGE_CASES = {
     "rev_then_ds": (lambda: [rev(32, 1), ds_basic(32, 64), rev(64, 1)], 2, [(2, 32, 8, 8)] * 2),
     "stem_cifar_then_rev": (lambda: [StemUnit(3, 64, 3, 1, False), rev(32, 0)], 4, [(4, 3, 16, 16)]),
     "stem_imagenet_maxpool": (lambda: [StemUnit(3, 32, 7, 2, True), rev(16, 0)], 2, [(2, 3, 30, 30)]),
+    # ResNet-50 grids with padded tensor-core tiles (14 -> Wb 16, 7 -> Wb 8, odd batch)
+    "r50_bottleneck_single_14x14": (lambda: [bott(128, 64, 1)], 2, [(2, 128, 14, 14)] * 2),
+    "r50_ds_bottleneck_single_14_to_7": (lambda: [ds_bott(128, 64, 256)], 3, [(3, 128, 14, 14)] * 2),
+    "r50_bottleneck_14x14": (lambda: [bott(128, 64, 0), bott(128, 64, 1)], 2, [(2, 128, 14, 14)] * 2),
+    "r50_ds_bottleneck_14_to_7": (lambda: [ds_bott(128, 64, 256), bott(256, 64, 1)], 3, [(3, 128, 14, 14)] * 2),
+}
+# Reading c23: in bf16, conv inputs that differ from the emulating
+# oracle's by fp32-vs-fp64 accumulation (~1e-6) occasionally round to the other bf16
+# neighbour; through a chain of >= 2 tensor-core conv-BN-ReLU layers such single-ulp
+# moves flip ReLU masks at z ~ 0, and each flipped mask passes (or blocks) an O(1)
+# dy.  Measured (tools/diag_bott.py): single-layer branches agree to < 1e-3, two- or
+# three-layer chains to ~1.5e-3, and a chain fed by a RECONSTRUCTED activation (the
+# second unit of a stage) to ~1e-2, largest on the cancelling BN-gradient sums; the
+# fp32 path agrees to 1e-4 on every case and padding plays no part (16x16 behaves
+# like 14x14).  Tiers for the bf16 path vs the emulating oracle: (messages and
+# parameters, per gradient tensor); the forward stays at 2e-2 vs the EXACT oracle.
+BF16_TIER = {
+    "r50_bottleneck_single_14x14": (5e-3, 5e-3),
+    "r50_ds_bottleneck_single_14_to_7": (5e-3, 5e-3),
+    "r50_bottleneck_14x14": (2e-2, 5e-2),
+    "r50_ds_bottleneck_14_to_7": (2e-2, 5e-2),
 }
 
 
@@ -127,6 +148,9 @@ def _stage_tick(case, precision, exact_fwd):
     ostage = E.Stage(units, E.OptConfig(), 1, 2)
     ostage.lr = 0.1
     tol = TOL[precision]
+    tol_g = tol
+    if precision == L.BF16_TC and case in BF16_TIER:
+        tol, tol_g = BF16_TIER[case]
     xs = [synth.images(s, 0, i) for i, s in enumerate(in_shapes)]
     # ---- forward
     fo = ostage.forward(E.Fwd(0, xs, None))
@@ -157,7 +181,7 @@ def _stage_tick(case, precision, exact_fwd):
     want_g = pack_like(units, ostage.last_grads)
     for name, r in per_tensor_rel(units, g, want_g):
         rep.append(("grad." + name, r))
-        ok &= r <= tol
+        ok &= r <= tol_g
     th, v, bf = st.get_params()
     want_th, want_bf = pack_params(units)
     ok &= check("theta", th, want_th, tol, rep)
