@@ -60,7 +60,7 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     }
     f32_to_bf16(db->as<float>(), bb->as<__nv_bfloat16>(), nb, st);
     DevPtr ws = dalloc(std::max<size_t>(16, conv_tc_workspace(g, mode)));
-    if (mode == 0) conv_fwd_tc(g, ab->as<__nv_bfloat16>(), bb->as<__nv_bfloat16>(), dout->as<float>(), ws->as<float>(),
+    if (mode == 0) conv_fwd_tc(g, ab->as<__nv_bfloat16>(), bb->as<__nv_bfloat16>(), dout->p, false, ws->as<float>(),
                             nullptr, st);
     else if (mode == 1)
       conv_dgrad_tc(g, ab->as<__nv_bfloat16>(), bb->as<__nv_bfloat16>(), addend ? dadd->as<float>() : nullptr,

@@ -16,10 +16,11 @@ void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *
 bool conv_tc_supported(const ConvGeom &g, int mode);   // mode 0 fwd, 1 dgrad, 2 wgrad
 void conv_tc_prepare();  // one-time kernel attributes (before any graph capture)
 size_t conv_tc_workspace(const ConvGeom &g, int mode);  // split-K workspace bytes
-// z[m][co] (fp32) = conv(x_bf16, w_bf16).  stats_part (nullable, >= 148*4*Co*2 floats):
-// the epilogue also writes BN partial sums of z; returns the number of partial rows
-// to merge with bn_stats_from_partials (0 = not fused, run bn_stats on z).
-int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32, float *ws,
+// z[m][co] = conv(x_bf16, w_bf16), stored fp32 or (z_bf16) bf16.  stats_part (nullable,
+// >= 148*4*Co*2 floats): the epilogue also writes BN partial sums of z as stored;
+// returns the number of partial rows to merge with bn_stats_from_partials (0 = not
+// fused, run bn_stats on z).
+int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, void *z, bool z_bf16, float *ws,
                 float *stats_part, cudaStream_t st);
 void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float eps, float *mean, float *invstd,
                             float *rmean, float *rvar, float mom, cudaStream_t st);

@@ -49,14 +49,45 @@ struct ConvTCParams {
   int OH, OW, oss, ph, pw;   // grid (i, j) -> output pixel (i*oss+ph, j*oss+pw) of an OH x OW image
   int splits, kb_per_split;  // split-K (small-M layers): splits > 1 -> partials into ws[split][M][N]
   float *ws;
-  const float *addend;
-  float *out;                // [B*OH*OW][N]
+  const float *addend;       // nullable (fp32 output only): out = addend + conv
+  void *out;                 // [B*OH*OW][N], fp32 or bf16 (OUT16); written by TMA stores through tmO
   float *stats;              // nullable: per-(CTA, epilogue warp) BN partials [grid][4][N][2] (sum, sum sq)
 };
 
-template <int BN, int STAGES>
+// Epilogue staging: each epilogue warp owns two 4 KB buffers (32 rows x 128 B, the
+// 128B-swizzled layout of a TMA box); it writes one column chunk of its 32 rows,
+// fences, and lane 0 issues the TMA store while the warp fills the other buffer.
+// Out-of-bounds box elements (padding rows of the padded grid) are not written.
+constexpr uint32_t kEpiBuf = 32 * 128;
+constexpr uint32_t kEpiBytes = 4 * 2 * kEpiBuf;
+
+// row `lane` of a 32 x 128 B swizzled box: 32 fp32 or 64 bf16 values
+template <bool BF16>
+__device__ __forceinline__ void stage_row(uint8_t *buf, int lane, const float *v) {
+  uint8_t *rowp = buf + lane * 128;
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch) {
+    uint4 u;
+    if constexpr (BF16) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * ch + 2 * e], v[8 * ch + 2 * e + 1]);
+        w[e] = *reinterpret_cast<uint32_t *>(&h);
+      }
+      u = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+      u = make_uint4(__float_as_uint(v[4 * ch]), __float_as_uint(v[4 * ch + 1]), __float_as_uint(v[4 * ch + 2]),
+                     __float_as_uint(v[4 * ch + 3]));
+    }
+    *reinterpret_cast<uint4 *>(rowp + ((ch ^ (lane & 7)) << 4)) = u;
+  }
+}
+
+template <int BN, int STAGES, bool OUT16>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmW,
                const __grid_constant__ ConvTCParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -67,7 +98,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  float *sstat = reinterpret_cast<float *>(tmem_slot + 4);  // [4 warps][N][2] BN partial sums (fused stats)
+  uint8_t *sepi = smem + STAGES * STAGE_BYTES + 1024;      // [4 warps][2][32 x 128 B] epilogue staging
+  float *sstat = reinterpret_cast<float *>(sepi + kEpiBytes);  // [4 warps][N][2] BN partial sums (fused stats)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_n = P.N / BN;
@@ -155,9 +187,31 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
     float *my_stat = sstat + (size_t)q * P.N * 2;
+    uint8_t *ebuf = sepi + q * 2 * kEpiBuf;
+    int eb = 0;  // staging buffer to fill next
     if (P.stats)
       for (int i = lane; i < 2 * P.N; i += 32) my_stat[i] = 0.f;
     __syncwarp();
+    if (lane == 0) {
+      tc::tma_prefetch(&tmO);
+      tc::tma_prefetch(&tmW);
+    }
+    // hand one staged chunk to the TMA engine (lane 0), after all lanes' smem writes
+    auto flush = [&](const CUtensorMap *map, int c0, int c1, int c2, int c3, bool four_d) {
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (four_d) tc::tma_store_4d(map, ebuf + eb * kEpiBuf, c0, c1, c2, c3);
+        else tc::tma_store_2d(map, ebuf + eb * kEpiBuf, c0, c1);
+        tc::bulk_commit();
+      }
+      eb ^= 1;
+    };
+    // before overwriting buffer eb: its previous store (two chunks ago) has read smem
+    auto acquire = [&]() {
+      if (lane == 0) tc::bulk_wait_read<1>();
+      __syncwarp();
+    };
     int it = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
       int mt, nt, sp, kb0, kb1;
@@ -165,48 +219,66 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int acc = it & 1;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       const int m = mt * BM + row;
-      const int b = m / GHW, r = m % GHW, i = r / P.Wb, j = r % P.Wb;
-      const bool valid = b < P.B && i < P.Gh && j < P.Gw;  // padding rows: computed, never stored
-      float *orow = nullptr;
-      const float *arow = nullptr;
-      if (P.splits > 1) {  // partial of this K split, GEMM-row order; reduced by splitk_out_kernel
-        orow = P.ws + ((int64_t)sp * P.M + m) * P.N + nt * BN;
-      } else if (valid) {
-        const int64_t opix = ((int64_t)b * P.OH + i * P.oss + P.ph) * P.OW + j * P.oss + P.pw;
-        orow = P.out + opix * P.N + nt * BN;
-        arow = P.addend ? P.addend + opix * P.N + nt * BN : nullptr;
-      }
+      if (P.splits > 1) {  // fp32 partial of this K split, GEMM-row order -> ws[split][M][N]
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        float v[16];
-        tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
-        if (arow) {
-#pragma unroll
-          for (int jj = 0; jj < 16; jj += 4) {
-            float4 a4 = *reinterpret_cast<const float4 *>(arow + c + jj);
-            v[jj] += a4.x; v[jj + 1] += a4.y; v[jj + 2] += a4.z; v[jj + 3] += a4.w;
-          }
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tc::tmem_ld16(trow + c, *reinterpret_cast<float(*)[16]>(v));
+          tc::tmem_ld16(trow + c + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+          acquire();
+          stage_row<false>(ebuf + eb * kEpiBuf, lane, v);
+          flush(&tmW, nt * BN + c, sp * P.M + mt * BM + q * 32, 0, 0, false);
         }
-        if (orow) {
-#pragma unroll
-          for (int jj = 0; jj < 16; jj += 4)
-            *reinterpret_cast<float4 *>(orow + c + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+      } else {
+        const int b = m / GHW, r = m % GHW, i = r / P.Wb, j = r % P.Wb;
+        const bool valid = b < P.B && i < P.Gh && j < P.Gw;  // padding rows: computed, never stored
+        const float *arow = nullptr;
+        if (valid && P.addend) {
+          const int64_t opix = ((int64_t)b * P.OH + i * P.oss + P.ph) * P.OW + j * P.oss + P.pw;
+          arow = P.addend + opix * P.N + nt * BN;
         }
-        if (P.stats) {  // BN batch statistics of z, fused (sum and sum of squares per column)
-          if (!valid) {
+        // TMA box origin of this warp's 32 rows in the (N, Gw, Gh, B) output view
+        const int m0w = mt * BM + q * 32;
+        const int wb = m0w / GHW, wr = m0w % GHW, wi = wr / P.Wb, wj = wr % P.Wb;
+        constexpr int CW = OUT16 ? 64 : 32;  // columns per 128-byte staged row
+#pragma unroll 1
+        for (int c = 0; c < BN; c += CW) {
+          float v[CW];
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
+          for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
+          if (arow) {
+#pragma unroll
+            for (int jj = 0; jj < CW; jj += 4) {
+              float4 a4 = *reinterpret_cast<const float4 *>(arow + c + jj);
+              v[jj] += a4.x; v[jj + 1] += a4.y; v[jj + 2] += a4.z; v[jj + 3] += a4.w;
+            }
           }
-          float sq[16];
+          if constexpr (OUT16) {  // statistics of the values as stored (reading c24)
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) sq[jj] = v[jj] * v[jj];
-          tc::colsum16(v, lane);
-          tc::colsum16(sq, lane);
-          if (!(lane & 1)) {
-            const int col = nt * BN + c + (lane >> 1);
-            my_stat[2 * col] += v[0];
-            my_stat[2 * col + 1] += sq[0];
+            for (int jj = 0; jj < CW; ++jj) v[jj] = __bfloat162float(__float2bfloat16_rn(v[jj]));
+          }
+          acquire();
+          stage_row<OUT16>(ebuf + eb * kEpiBuf, lane, v);
+          flush(&tmO, nt * BN + c, wj, wi, wb, true);
+          if (P.stats) {  // BN batch statistics of z, fused (sum and sum of squares per column)
+#pragma unroll
+            for (int h = 0; h < CW; h += 16) {
+              float x[16], sq[16];
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) {
+                x[jj] = valid ? v[h + jj] : 0.f;
+                sq[jj] = x[jj] * x[jj];
+              }
+              tc::colsum16(x, lane);
+              tc::colsum16(sq, lane);
+              if (!(lane & 1)) {
+                const int col = nt * BN + c + h + (lane >> 1);
+                my_stat[2 * col] += x[0];
+                my_stat[2 * col + 1] += sq[0];
+              }
+            }
           }
         }
       }
@@ -214,6 +286,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) tc::bulk_wait_all();
     if (P.stats) {
       __syncwarp();
       float *g = P.stats + ((size_t)blockIdx.x * 4 + q) * P.N * 2;
@@ -274,6 +347,7 @@ __global__ void __launch_bounds__(256) stats_finalize_kernel(const float *__rest
 }
 
 // out[opix(m)][n] = addend + sum over splits of ws[s][m][n]  (fixed order: deterministic)
+template <bool OUT16>
 __global__ void splitk_out_kernel(const ConvTCParams P) {
   const int N4 = P.N / 4;
   const int64_t n = (int64_t)P.M * N4;
@@ -292,7 +366,13 @@ __global__ void splitk_out_kernel(const ConvTCParams P) {
       float4 a = *reinterpret_cast<const float4 *>(P.addend + o);
       s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
     }
-    *reinterpret_cast<float4 *>(P.out + o) = s;
+    if constexpr (OUT16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(s.x, s.y), hi = __floats2bfloat162_rn(s.z, s.w);
+      *reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(P.out) + o) =
+          make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+    } else {
+      *reinterpret_cast<float4 *>(static_cast<float *>(P.out) + o) = s;
+    }
   }
 }
 
@@ -504,9 +584,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 CUtensorMap make_map(const void *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides_bytes,
-                     const cuuint32_t *box, const cuuint32_t *es) {
+                     const cuuint32_t *box, const cuuint32_t *es,
+                     CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   CUtensorMap m;
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(base), dims,
+  CUresult r = encode_fn()(&m, dt, rank, const_cast<void *>(base), dims,
                            strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw PetraError(PETRA_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
@@ -588,23 +669,61 @@ ConvPlan conv_plan(int M, int N, int KB) {
   return p;
 }
 
-template <int BN, int STAGES>
+// Output view of a conv GEMM for the TMA-store epilogue: grid pixel (b, i, j) ->
+// out[b][i*oss+ph][j*oss+pw][:] as a 4-D (N, Gw, Gh, B) tensor; the box is one epilogue
+// warp's 32 GEMM rows (a run of whole padded rows / images, or a 32-wide piece of
+// one padded row) x 128 bytes of columns.  Padding rows fall outside Gw / Gh / B.
+CUtensorMap out_map(void *out, bool bf16, const ConvTCParams &P) {
+  const int es = bf16 ? 2 : 4;
+  char *base = static_cast<char *>(out) + ((int64_t)P.ph * P.OW + P.pw) * P.N * es;
+  cuuint64_t dims[4] = {(cuuint64_t)P.N, (cuuint64_t)P.Gw, (cuuint64_t)P.Gh, (cuuint64_t)P.B};
+  cuuint64_t st[3] = {(cuuint64_t)P.oss * P.N * es, (cuuint64_t)P.oss * P.OW * P.N * es,
+                      (cuuint64_t)P.OH * P.OW * P.N * es};
+  int bw = std::min(P.Wb, 32), bh = 1, bb = 1;
+  if (P.Wb < 32) {
+    const int rows = 32 / P.Wb;
+    if (rows <= P.Hb) bh = rows;
+    else { bh = P.Hb; bb = rows / P.Hb; }
+  }
+  cuuint32_t box[4] = {(cuuint32_t)(128 / es), (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bb};
+  cuuint32_t el[4] = {1, 1, 1, 1};
+  return make_map(base, 4, dims, st, box, el,
+                  bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+}
+
+// split-K partials ws[split][M][N] fp32 as a 2-D (N, splits*M) tensor, box 32 x 32
+CUtensorMap ws_map(float *ws, int N, int64_t rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)rows};
+  cuuint64_t st[1] = {(cuuint64_t)N * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t el[2] = {1, 1};
+  return make_map(ws, 2, dims, st, box, el, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+}
+
+constexpr int conv_stages(int BN) { return BN == 256 ? 3 : (BN == 128 ? 5 : 6); }
+constexpr size_t conv_smem(int BN, size_t stat_bytes) {
+  return 1024 + (size_t)conv_stages(BN) * (A_BYTES + BN * BK * 2) + 1024 + kEpiBytes + stat_bytes;
+}
+
+template <int BN, bool OUT16>
 void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P, cudaStream_t st) {
-  // attribute set by conv_tc_prepare; + fused-stats area [4][N][2] floats
-  size_t smem = (size_t)STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256 + (P.stats ? (size_t)P.N * 32 : 0);
-  int work = (P.M / BM) * (P.N / BN) * P.splits;
-  conv_tc_kernel<BN, STAGES><<<std::min(work, kNumSMs), kThreads, smem, st>>>(ta, tb, P);
+  constexpr int STAGES = conv_stages(BN);
+  const size_t smem = conv_smem(BN, P.stats ? (size_t)P.N * 32 : 0);  // attribute: conv_tc_prepare
+  const int work = (P.M / BM) * (P.N / BN) * P.splits;
+  const CUtensorMap to = out_map(P.out, OUT16, P);
+  const CUtensorMap tw = P.splits > 1 ? ws_map(P.ws, P.N, (int64_t)P.splits * P.M) : to;
+  conv_tc_kernel<BN, STAGES, OUT16><<<std::min(work, kNumSMs), kThreads, smem, st>>>(ta, tb, to, tw, P);
   PETRA_LAUNCH_CHECK();
   if (P.splits > 1) {
     int64_t n = (int64_t)P.M * P.N / 4;
-    splitk_out_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs), 256, 0, st>>>(P);
+    splitk_out_kernel<OUT16><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs), 256, 0, st>>>(P);
     PETRA_LAUNCH_CHECK();
   }
 }
 
 // tensor maps are built per launch (host-side, ~1 us); B's box height = BN
 void launch_any(const CUtensorMap &ta, const __nv_bfloat16 *w, int wrows, int wK, ConvTCParams &P, float *ws,
-                cudaStream_t st) {
+                bool out16, cudaStream_t st) {
   ConvPlan pl = conv_plan(P.M, P.N, P.ntaps * P.CB);
   P.splits = pl.splits;
   P.kb_per_split = pl.kb_per_split;
@@ -614,10 +733,17 @@ void launch_any(const CUtensorMap &ta, const __nv_bfloat16 *w, int wrows, int wK
     P.kb_per_split = P.ntaps * P.CB;
   }
   if (P.splits > 1 || P.N > kMaxStatN) P.stats = nullptr;  // stats need final z (split-K: standalone pass)
+  if (out16 && P.addend) throw PetraError(PETRA_E_ARG, "conv_tc: addend needs an fp32 output");
   CUtensorMap tb = mat_map(w, wrows, wK, pl.BN);
-  if (pl.BN == 256) launch_conv<256, 4>(ta, tb, P, st);
-  else if (pl.BN == 128) launch_conv<128, 5>(ta, tb, P, st);
-  else launch_conv<64, 6>(ta, tb, P, st);
+  if (out16) {
+    if (pl.BN == 256) launch_conv<256, true>(ta, tb, P, st);
+    else if (pl.BN == 128) launch_conv<128, true>(ta, tb, P, st);
+    else launch_conv<64, true>(ta, tb, P, st);
+  } else {
+    if (pl.BN == 256) launch_conv<256, false>(ta, tb, P, st);
+    else if (pl.BN == 128) launch_conv<128, false>(ta, tb, P, st);
+    else launch_conv<64, false>(ta, tb, P, st);
+  }
 }
 
 bool geom_ok(const ConvGeom &g) {
@@ -628,8 +754,8 @@ bool geom_ok(const ConvGeom &g) {
   return true;
 }
 
-int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *out, float *ws, float *stats,
-            cudaStream_t st) {
+int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, void *out, bool out16, float *ws,
+            float *stats, cudaStream_t st) {
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
   ConvTCParams P{};
   P.M = (int)t.M();
@@ -654,7 +780,7 @@ int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, f
   P.out = out;
   P.stats = stats;
   CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, t.Wb, t.R, t.NB, g.s);
-  launch_any(ta, w, g.Co, g.K(), P, ws, st);
+  launch_any(ta, w, g.Co, g.K(), P, ws, out16, st);
   if (!P.stats) return 0;
   const int BN = conv_plan(P.M, P.N, P.ntaps * P.CB).BN;
   return std::min((P.M / BM) * (P.N / BN) * P.splits, kNumSMs) * 4;  // partial rows written
@@ -690,7 +816,7 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *
       P.wk[tap] = tap;
     }
     P.oss = 1;
-    launch_any(ta, wt, g.Ci, wK, P, ws, st);
+    launch_any(ta, wt, g.Ci, wK, P, ws, false, st);
     return;
   }
   // stride 2: phase (ph, pw) of dx gets the taps with kh = ph + p (mod 2), kw = pw + p (mod 2);
@@ -715,7 +841,7 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *
       P.ntaps = n;
       P.ph = ph;
       P.pw = pw;
-      launch_any(ta, wt, g.Ci, wK, P, ws, st);
+      launch_any(ta, wt, g.Ci, wK, P, ws, false, st);
     }
   if (empty_mask) {
     int64_t cnt = (int64_t)g.B * g.H * g.W * (g.Ci / 4);
@@ -756,13 +882,16 @@ void launch_wgrad(const CUtensorMap &tx, const CUtensorMap &tdz, const WgradPara
 void conv_tc_prepare() {
   static std::once_flag once;
   std::call_once(once, [] {
-    auto set = [](const void *f, int STAGES, int BN) {
-      size_t smem = (size_t)STAGES * (A_BYTES + BN * BK * 2) + 1024 + 256 + kMaxStatN * 32;
-      PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto set = [](const void *f, int BN) {
+      PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)conv_smem(BN, kMaxStatN * 32)));
     };
-    set((const void *)conv_tc_kernel<256, 4>, 4, 256);
-    set((const void *)conv_tc_kernel<128, 5>, 5, 128);
-    set((const void *)conv_tc_kernel<64, 6>, 6, 64);
+    set((const void *)conv_tc_kernel<256, conv_stages(256), false>, 256);
+    set((const void *)conv_tc_kernel<128, conv_stages(128), false>, 128);
+    set((const void *)conv_tc_kernel<64, conv_stages(64), false>, 64);
+    set((const void *)conv_tc_kernel<256, conv_stages(256), true>, 256);
+    set((const void *)conv_tc_kernel<128, conv_stages(128), true>, 128);
+    set((const void *)conv_tc_kernel<64, conv_stages(64), true>, 64);
     auto setw = [](const void *f, int STAGES, int BN) {
       size_t smem = (size_t)STAGES * (2 * 64 * 64 * 2 + BN * 64 * 2) + 1024 + 256;
       PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -792,9 +921,9 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode) {
   return p.splits > 1 ? (size_t)p.splits * M * N * sizeof(float) : 0;
 }
 
-int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, float *z_f32, float *ws,
+int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, void *z, bool z_bf16, float *ws,
                 float *stats_part, cudaStream_t st) {
-  return run_fwd(g, x, w, z_f32, ws, stats_part, st);
+  return run_fwd(g, x, w, z, z_bf16, ws, stats_part, st);
 }
 
 void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float eps, float *mean, float *invstd,

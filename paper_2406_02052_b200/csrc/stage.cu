@@ -420,7 +420,7 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
   }
   ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    L.stats_rows = conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->as<float>(),
+    L.stats_rows = conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->p, false,
                                wgrad_ws_->as<float>(), reinterpret_cast<float *>(part_->p), st);
   } else {
     conv_fwd_simt(L.g, x, w, L.z->as<float>(), st);
