@@ -25,8 +25,9 @@ BN_MOMENTUM = 0.1    # reading c9
 # rounding functions here so that the ReLU masks -- integer decisions taken from
 # floating point -- are decided on the same rounded operands on both sides.
 # Each entry: None (exact) or f(array, pass_name, geometry) -> rounded array,
-# geometry = (B, H, W, Ci, Co, k, stride).  Products/sums stay fp64.
-OPERAND_ROUND = {"fwd": None, "dgrad": None, "wgrad": None}
+# geometry = (B, H, W, Ci, Co, k, stride).  Products/sums stay fp64.  "fwd_out" is
+# applied to the convolution's result (a kernel that stores z in bf16, reading c24).
+OPERAND_ROUND = {"fwd": None, "dgrad": None, "wgrad": None, "fwd_out": None}
 
 
 def _rnd(kind, a, geom):
@@ -67,7 +68,7 @@ def conv2d(x, w, stride=1, pad=0):
     for kh, kw, view in _taps(xp, k, stride, Ho, Wo):
         # sum over c of view[b,c,i,j] * w[o,c,kh,kw]  -> [B,Ho,Wo,O]
         out += np.tensordot(view, w[:, :, kh, kw], axes=([1], [1])).transpose(0, 3, 1, 2)
-    return out
+    return _rnd("fwd_out", out, geom)
 
 
 def conv2d_vjp(x, w, stride, pad, dout, need_dx=True):

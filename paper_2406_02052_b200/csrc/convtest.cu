@@ -29,7 +29,7 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
   if (stem) {  // gathered-im2col tensor-core stem: fp32 image (and fp32 weights) read directly
     DevPtr ws = dalloc(std::max<size_t>(16, stem_tc_workspace(g)));
     if (mode == 0) {
-      stem_fwd_tc(g, da->as<float>(), db->as<float>(), dout->as<float>(), nullptr, st);
+      stem_fwd_tc(g, da->as<float>(), db->as<float>(), dout->p, false, nullptr, st);
     } else {
       DevPtr ab = dalloc(na * 2);
       f32_to_bf16(da->as<float>(), ab->as<__nv_bfloat16>(), na, st);

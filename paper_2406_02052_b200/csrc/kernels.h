@@ -42,8 +42,10 @@ void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream
 bool stem_tc_supported(const ConvGeom &g);
 void stem_tc_prepare();  // kernel attributes (called by conv_tc_prepare)
 size_t stem_tc_workspace(const ConvGeom &g);
-// z (fp32) = conv(bf16(x), bf16(w)); x, w fp32 as stored; fused BN partials as conv_fwd_tc
-int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, float *z, float *stats_part, cudaStream_t st);
+// z = conv(bf16(x), bf16(w)) stored fp32 or (z_bf16) bf16; x, w fp32 as stored; fused BN
+// partials as conv_fwd_tc
+int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, void *z, bool z_bf16, float *stats_part,
+                cudaStream_t st);
 // dw (fp32) = sum_pixels dz_bf16 (x) bf16(x)
 void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const float *x, float *dw, float *ws,
                    cudaStream_t st);

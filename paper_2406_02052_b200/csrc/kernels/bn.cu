@@ -256,7 +256,7 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
         float4 a = ld4(acc, m * C + c);
         o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
       }
-      st4(out, m * C + c, o);
+      if (out) st4(out, m * C + c, o);
       if (out_bf16) st4(out_bf16, m * C + c, o);
     }
     return;
@@ -270,7 +270,7 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
     if (relu) y = y > 0.f ? y : 0.f;
     float o = sign * y;
     if (acc) o += acc[i];
-    stv(out, i, o);
+    if (out) stv(out, i, o);
     if (out_bf16) out_bf16[i] = __float2bfloat16_rn(o);
   }
 }

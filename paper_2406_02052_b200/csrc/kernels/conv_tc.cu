@@ -287,10 +287,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
     if (lane == 0) tc::bulk_wait_all();
-    if (P.stats) {
-      __syncwarp();
-      float *g = P.stats + ((size_t)blockIdx.x * 4 + q) * P.N * 2;
-      for (int i = lane; i < 2 * P.N; i += 32) g[i] = my_stat[i];
+    if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      float *g = P.stats + (size_t)blockIdx.x * P.N * 2;
+      for (int i = q * 32 + lane; i < 2 * P.N; i += 128)
+        g[i] = (sstat[i] + sstat[2 * P.N + i]) + (sstat[4 * P.N + i] + sstat[6 * P.N + i]);
     }
   }
   __syncthreads();
@@ -300,38 +301,39 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
 }
 
-// BN statistics from the fused partials: per channel, fp64 sum over the P = grid*4
-// partial rows in a fixed order (32 threads per channel x strided subsets, then a
-// fixed-order shared-memory combine); optional running-stat EMA (reading c9).
-__global__ void __launch_bounds__(256) stats_finalize_kernel(const float *__restrict__ part, int P, int N, int64_t M,
-                                                             float eps, float *__restrict__ mean,
-                                                             float *__restrict__ invstd, float *__restrict__ rmean,
-                                                             float *__restrict__ rvar, float mom) {
-  __shared__ double sh[2][32][9];
-  const int cl = threadIdx.x & 7, sub = threadIdx.x >> 3;  // 8 channels x 32 subsets per block
-  const int c = blockIdx.x * 8 + cl;
+// BN statistics from the fused partials part[P][N][2] (one row per conv CTA): a
+// block of 32 warps per 32 channels, warp w sums rows w, w+32, ... in fp64 (lane =
+// channel, coalesced), then warp 0 combines the 32 warp sums in a fixed order;
+// optional running-stat EMA (reading c9).
+__global__ void __launch_bounds__(1024) stats_finalize_kernel(const float *__restrict__ part, int P, int N, int64_t M,
+                                                              float eps, float *__restrict__ mean,
+                                                              float *__restrict__ invstd, float *__restrict__ rmean,
+                                                              float *__restrict__ rvar, float mom) {
+  __shared__ double sh[2][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   double a0 = 0, a1 = 0, b0 = 0, b1 = 0;
   if (c < N) {
-    int i = sub;
+    int i = w;
     for (; i + 32 < P; i += 64) {
-      float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)i * N + c) * 2);
-      float2 v = *reinterpret_cast<const float2 *>(part + ((size_t)(i + 32) * N + c) * 2);
+      const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)i * N + c) * 2);
+      const float2 v = *reinterpret_cast<const float2 *>(part + ((size_t)(i + 32) * N + c) * 2);
       a0 += u.x; b0 += u.y;
       a1 += v.x; b1 += v.y;
     }
     if (i < P) {
-      float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)i * N + c) * 2);
+      const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)i * N + c) * 2);
       a0 += u.x; b0 += u.y;
     }
   }
-  sh[0][sub][cl] = a0 + a1;
-  sh[1][sub][cl] = b0 + b1;
+  sh[0][w][lane] = a0 + a1;
+  sh[1][w][lane] = b0 + b1;
   __syncthreads();
-  if (sub == 0 && c < N) {
+  if (w == 0 && c < N) {
     double s = 0, ss = 0;
     for (int k = 0; k < 32; ++k) {
-      s += sh[0][k][cl];
-      ss += sh[1][k][cl];
+      s += sh[0][k][lane];
+      ss += sh[1][k][lane];
     }
     double mu = s / (double)M;
     double var = ss / (double)M - mu * mu;
@@ -783,7 +785,7 @@ int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, v
   launch_any(ta, w, g.Co, g.K(), P, ws, out16, st);
   if (!P.stats) return 0;
   const int BN = conv_plan(P.M, P.N, P.ntaps * P.CB).BN;
-  return std::min((P.M / BM) * (P.N / BN) * P.splits, kNumSMs) * 4;  // partial rows written
+  return std::min((P.M / BM) * (P.N / BN) * P.splits, kNumSMs);  // partial rows written (one per CTA)
 }
 
 void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend, float *dx,
@@ -928,7 +930,7 @@ int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *
 
 void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float eps, float *mean, float *invstd,
                             float *rmean, float *rvar, float mom, cudaStream_t st) {
-  stats_finalize_kernel<<<(unsigned)cdiv(N, 8), 256, 0, st>>>(part, P, N, M, eps, mean, invstd, rmean, rvar, mom);
+  stats_finalize_kernel<<<(unsigned)cdiv(N, 32), 1024, 0, st>>>(part, P, N, M, eps, mean, invstd, rmean, rvar, mom);
   PETRA_LAUNCH_CHECK();
 }
 

@@ -37,7 +37,7 @@ struct StemParams {
   int M, K, N;
   int KB;                              // forward: 64-wide K blocks
   int n_mt, KBtot, kb_per_split, splits;  // wgrad: kk tiles of 128, pixel blocks of 64, split-K
-  float *out;
+  void *out;                           // fwd: z fp32 or bf16 (OUT16); wgrad: fp32
   float *stats;
 };
 
@@ -100,7 +100,7 @@ __device__ __forceinline__ void store_row_chunks(uint8_t *tile, int row, int c0,
         make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
 }
 
-template <int BN>
+template <int BN, bool OUT16>
 __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_constant__ StemParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -205,15 +205,30 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
       tc::tc_fence_after();
       const int m = t * 128 + row;
       const bool valid = m < P.M;
-      float *orow = P.out + (int64_t)m * P.N;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         float v[16];
         tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
         if (valid) {
+          if constexpr (OUT16) {  // z stored in bf16; statistics of the stored values (reading c24)
+            uint32_t w[8];
 #pragma unroll
-          for (int jj = 0; jj < 16; jj += 4)
-            *reinterpret_cast<float4 *>(orow + c + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+            for (int jj = 0; jj < 16; jj += 2) {
+              __nv_bfloat162 h = __floats2bfloat162_rn(v[jj], v[jj + 1]);
+              w[jj >> 1] = *reinterpret_cast<uint32_t *>(&h);
+              const float2 f = __bfloat1622float2(h);
+              v[jj] = f.x;
+              v[jj + 1] = f.y;
+            }
+            uint4 *o = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(P.out) + (int64_t)m * P.N + c);
+            o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          } else {
+            float *orow = static_cast<float *>(P.out) + (int64_t)m * P.N + c;
+#pragma unroll
+            for (int jj = 0; jj < 16; jj += 4)
+              *reinterpret_cast<float4 *>(orow + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+          }
         } else {
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
@@ -235,10 +250,11 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
-    if (P.stats) {
-      __syncwarp();
-      float *g = P.stats + ((size_t)blockIdx.x * 4 + q) * P.N * 2;
-      for (int i = lane; i < 2 * P.N; i += 32) g[i] = my_stat[i];
+    if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      float *g = P.stats + (size_t)blockIdx.x * P.N * 2;
+      for (int i = q * 32 + lane; i < 2 * P.N; i += 128)
+        g[i] = (sstat[i] + sstat[2 * P.N + i]) + (sstat[4 * P.N + i] + sstat[6 * P.N + i]);
     }
   }
   __syncthreads();
@@ -350,7 +366,7 @@ stem_wgrad_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constan
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
       const int r = mt * 128 + row;
-      float *o = P.out + (int64_t)sp * P.N * P.K;
+      float *o = static_cast<float *>(P.out) + (int64_t)sp * P.N * P.K;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         float v[16];
@@ -409,9 +425,12 @@ void stem_tc_prepare() {
     auto set = [](const void *f, size_t smem) {
       PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     };
-    set((const void *)stem_fwd_kernel<64>, fwd_smem(64, 4));
-    set((const void *)stem_fwd_kernel<128>, fwd_smem(128, 4));
-    set((const void *)stem_fwd_kernel<256>, fwd_smem(256, 4));
+    set((const void *)stem_fwd_kernel<64, false>, fwd_smem(64, 4));
+    set((const void *)stem_fwd_kernel<128, false>, fwd_smem(128, 4));
+    set((const void *)stem_fwd_kernel<256, false>, fwd_smem(256, 4));
+    set((const void *)stem_fwd_kernel<64, true>, fwd_smem(64, 4));
+    set((const void *)stem_fwd_kernel<128, true>, fwd_smem(128, 4));
+    set((const void *)stem_fwd_kernel<256, true>, fwd_smem(256, 4));
     set((const void *)stem_wgrad_kernel<64>, wgrad_smem(64));
     set((const void *)stem_wgrad_kernel<128>, wgrad_smem(128));
     set((const void *)stem_wgrad_kernel<256>, wgrad_smem(256));
@@ -429,7 +448,8 @@ size_t stem_tc_workspace(const ConvGeom &g) {
   return w.splits > 1 ? (size_t)w.splits * g.Co * g.K() * sizeof(float) : 0;
 }
 
-int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, float *z, float *stats_part, cudaStream_t st) {
+int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, void *z, bool z_bf16, float *stats_part,
+                cudaStream_t st) {
   if (!stem_tc_supported(g)) throw PetraError(PETRA_E_UNSUPPORTED, "stem_fwd_tc: geometry");
   stem_tc_prepare();
   StemParams P = base_params(g);
@@ -439,11 +459,17 @@ int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, float *z, flo
   P.stats = stats_part;
   const int grid = (int)std::min<int64_t>(cdiv(P.M, 128), kNumSMs);
   const size_t smem = fwd_smem(P.N, P.KB);
-  if (P.N == 64) stem_fwd_kernel<64><<<grid, kThreads, smem, st>>>(P);
-  else if (P.N == 128) stem_fwd_kernel<128><<<grid, kThreads, smem, st>>>(P);
-  else stem_fwd_kernel<256><<<grid, kThreads, smem, st>>>(P);
+  if (z_bf16) {
+    if (P.N == 64) stem_fwd_kernel<64, true><<<grid, kThreads, smem, st>>>(P);
+    else if (P.N == 128) stem_fwd_kernel<128, true><<<grid, kThreads, smem, st>>>(P);
+    else stem_fwd_kernel<256, true><<<grid, kThreads, smem, st>>>(P);
+  } else {
+    if (P.N == 64) stem_fwd_kernel<64, false><<<grid, kThreads, smem, st>>>(P);
+    else if (P.N == 128) stem_fwd_kernel<128, false><<<grid, kThreads, smem, st>>>(P);
+    else stem_fwd_kernel<256, false><<<grid, kThreads, smem, st>>>(P);
+  }
   PETRA_LAUNCH_CHECK();
-  return stats_part ? grid * 4 : 0;
+  return stats_part ? grid : 0;
 }
 
 void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const float *x, float *dw, float *ws,

@@ -101,7 +101,8 @@ int64_t Stage::add_tensor(int unit, int part, int kind, int decay, std::vector<i
 
 void Stage::alloc_layer(Layer &L, bool inner) {
   int64_t n = L.g.M() * L.g.Co;
-  L.z = dalloc(n * sizeof(float));
+  L.z16 = tc_ && (conv_tc_supported(L.g, 0) || stem_tc_supported(L.g));
+  L.z = dalloc(n * (L.z16 ? sizeof(__nv_bfloat16) : sizeof(float)));
   L.dz = dalloc(n * sizeof(float));
   L.mean = dalloc(L.g.Co * sizeof(float));
   L.invstd = dalloc(L.g.Co * sizeof(float));
@@ -144,6 +145,7 @@ void Stage::build() {
         Layer &L = u.phi[0];
         L.g = make_geom(B, cur.H, cur.W, cur.C, d.layer[0].cout, d.layer[0].ksize, d.layer[0].stride);
         L.relu = true;
+        L.is_stem = true;
         layers.push_back({&L, (int)ui, 0});
         int Ho = L.g.Ho, Wo = L.g.Wo;
         if (d.maxpool) {
@@ -394,11 +396,17 @@ void Stage::enqueue_update(cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ layer kernels
-static void apply_bn(int64_t M, int C, const float *z, int ldz, int zc0, const float *mean, const float *invstd,
-                     const float *gamma, const float *beta, int relu, float sign, const float *acc, float *out,
-                     __nv_bfloat16 *out_bf16, cudaStream_t st) {
-  ProfScope ps("bn_apply", st, 0.0, 4.0 * (double)M * C * (acc ? 3 : 2));
-  bn_apply<float, float>(M, C, z, ldz, zc0, mean, invstd, gamma, beta, relu, sign, acc, out, out_bf16, st);
+static void apply_bn(int64_t M, int C, const void *z, bool z16, int ldz, int zc0, const float *mean,
+                     const float *invstd, const float *gamma, const float *beta, int relu, float sign,
+                     const float *acc, float *out, __nv_bfloat16 *out_bf16, cudaStream_t st) {
+  ProfScope ps("bn_apply", st, 0.0,
+               (double)M * C * ((z16 ? 2.0 : 4.0) + (acc ? 4.0 : 0.0) + (out ? 4.0 : 0.0) + (out_bf16 ? 2.0 : 0.0)));
+  if (z16)
+    bn_apply<__nv_bfloat16, float>(M, C, static_cast<const __nv_bfloat16 *>(z), ldz, zc0, mean, invstd, gamma, beta,
+                                   relu, sign, acc, out, out_bf16, st);
+  else
+    bn_apply<float, float>(M, C, static_cast<const float *>(z), ldz, zc0, mean, invstd, gamma, beta, relu, sign, acc,
+                           out, out_bf16, st);
 }
 
 static double conv_flops(const ConvGeom &g) { return 2.0 * (double)g.M() * g.Co * g.K(); }
@@ -410,7 +418,7 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
   const float *w = theta_->as<float>() + L.w_off;
   if (tc_ && stem_tc_supported(L.g)) {  // few input channels: gathered im2col, fp32 x read directly
     ProfScope ps("conv_fwd_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 4));
-    L.stats_rows = stem_fwd_tc(L.g, x, w, L.z->as<float>(), reinterpret_cast<float *>(part_->p), st);
+    L.stats_rows = stem_fwd_tc(L.g, x, w, L.z->p, L.z16, reinterpret_cast<float *>(part_->p), st);
     return;
   }
   bool tc = tc_ && conv_tc_supported(L.g, 0);
@@ -420,7 +428,7 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
   }
   ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    L.stats_rows = conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->p, false,
+    L.stats_rows = conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->p, L.z16,
                                wgrad_ws_->as<float>(), reinterpret_cast<float *>(part_->p), st);
   } else {
     conv_fwd_simt(L.g, x, w, L.z->as<float>(), st);
@@ -467,9 +475,15 @@ void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
     return;
   }
   ProfScope ps("bn_stats", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co);
-  bn_stats<float>(L.z->as<float>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean->as<float>(), L.invstd->as<float>(),
-                  running ? b + L.rm_off : nullptr, running ? b + L.rv_off : nullptr, desc_.bn_momentum,
-                  part_->as<double>(), counters_->as<unsigned>(), st);
+  if (L.z16)
+    bn_stats<__nv_bfloat16>(L.z->as<__nv_bfloat16>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean->as<float>(),
+                            L.invstd->as<float>(), running ? b + L.rm_off : nullptr,
+                            running ? b + L.rv_off : nullptr, desc_.bn_momentum, part_->as<double>(),
+                            counters_->as<unsigned>(), st);
+  else
+    bn_stats<float>(L.z->as<float>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean->as<float>(), L.invstd->as<float>(),
+                    running ? b + L.rm_off : nullptr, running ? b + L.rv_off : nullptr, desc_.bn_momentum,
+                    part_->as<double>(), counters_->as<unsigned>(), st);
 }
 
 // forward of a conv-BN-ReLU chain on x; inner activations into L.a; the last
@@ -485,8 +499,10 @@ void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running
       // inner activation; its bf16 copy is written straight into the next layer's operand
       Layer &N = phi[l + 1];
       ready = tc_ && conv_tc_supported(N.g, 0);
-      apply_bn(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(), L.invstd->as<float>(),
-               th + L.g_off, th + L.b_off, 1, 1.f, nullptr, L.a->as<float>(),
+      // the fp32 copy only feeds SIMT passes of the next layer (forward or wgrad)
+      const bool need32 = !ready || !conv_tc_supported(N.g, 2);
+      apply_bn(L.g.M(), L.g.Co, L.z->p, L.z16, L.g.Co, 0, L.mean->as<float>(), L.invstd->as<float>(),
+               th + L.g_off, th + L.b_off, 1, 1.f, nullptr, need32 ? L.a->as<float>() : nullptr,
                ready ? N.xb->as<__nv_bfloat16>() : nullptr, st);
       x = L.a->as<float>();
     }
@@ -502,19 +518,31 @@ void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, cons
   float *gr = grad_->as<float>();
   double n = (double)L.g.M() * L.g.Co;
   {
-  ProfScope ps("bn_bwd_reduce", st, 0.0, 4.0 * n * (dst_out ? 4 : 2));
-  bn_bwd_reduce<float>(L.z->as<float>(), L.g.M(), L.g.Co, L.mean->as<float>(), L.invstd->as<float>(),
-                       th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, dst_in, dst_out, nullptr,
-                       gr + L.g_off, gr + L.b_off, part_->as<double>(), counters_->as<unsigned>(), st);
+  ProfScope ps("bn_bwd_reduce", st, 0.0, n * ((L.z16 ? 2.0 : 4.0) + 4.0 + (dst_out ? 8.0 : 0.0)));
+  if (L.z16)
+    bn_bwd_reduce<__nv_bfloat16>(L.z->as<__nv_bfloat16>(), L.g.M(), L.g.Co, L.mean->as<float>(),
+                                 L.invstd->as<float>(), th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs,
+                                 dst_in, dst_out, nullptr, gr + L.g_off, gr + L.b_off, part_->as<double>(),
+                                 counters_->as<unsigned>(), st);
+  else
+    bn_bwd_reduce<float>(L.z->as<float>(), L.g.M(), L.g.Co, L.mean->as<float>(), L.invstd->as<float>(),
+                         th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, dst_in, dst_out, nullptr,
+                         gr + L.g_off, gr + L.b_off, part_->as<double>(), counters_->as<unsigned>(), st);
   }
   // dz in bf16 for tensor-core dgrad / wgrad, in fp32 only if a SIMT pass consumes it
-  const bool tc_d = tc_ && conv_tc_supported(L.g, 1);
+  // (the stem has no dgrad: its input is data)
+  const bool tc_d = tc_ && (L.is_stem || conv_tc_supported(L.g, 1));
   const bool tc_w = tc_ && (conv_tc_supported(L.g, 2) || stem_tc_supported(L.g));
   float *dz32 = (!tc_d || !tc_w) ? L.dz->as<float>() : nullptr;
   __nv_bfloat16 *dz16 = (tc_d || tc_w) ? L.dzb->as<__nv_bfloat16>() : nullptr;
-  ProfScope ps("bn_bwd_dz", st, 0.0, 8.0 * n + (dz32 ? 4.0 : 0.0) * n + (dz16 ? 2.0 : 0.0) * n);
-  bn_bwd_dz<float>(L.g.M(), L.g.Co, L.z->as<float>(), L.mean->as<float>(), L.invstd->as<float>(), th + L.g_off,
-                   th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off, dz32, dz16, st);
+  ProfScope ps("bn_bwd_dz", st, 0.0, n * ((L.z16 ? 2.0 : 4.0) + 4.0 + (dz32 ? 4.0 : 0.0) + (dz16 ? 2.0 : 0.0)));
+  if (L.z16)
+    bn_bwd_dz<__nv_bfloat16>(L.g.M(), L.g.Co, L.z->as<__nv_bfloat16>(), L.mean->as<float>(), L.invstd->as<float>(),
+                             th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off,
+                             dz32, dz16, st);
+  else
+    bn_bwd_dz<float>(L.g.M(), L.g.Co, L.z->as<float>(), L.mean->as<float>(), L.invstd->as<float>(), th + L.g_off,
+                     th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off, dz32, dz16, st);
 }
 
 // VJP through a branch whose last layer receives dy (reconstruction fused when
@@ -546,7 +574,7 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       // x[dst] += Phi(x[src])  (north_star y1 = x1 + F(x2), y2 = x2 + G(y1))
       branch_forward(u.phi, cur[u.src()], keep, st);
       Layer &L = u.phi.back();
-      apply_bn(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+      apply_bn(L.g.M(), L.g.Co, L.z->p, L.z16, L.g.Co, 0, L.mean->as<float>(),
                              L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, cur[u.dst()], out[u.dst()],
                              nullptr, st);
       break;
@@ -562,11 +590,11 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       Layer &L = u.phi.back();
       int64_t M = L.g.M();
       int C = L.g.Co;
-      apply_bn(M, C, u.pa.z->as<float>(), C, 0, u.pa.mean->as<float>(), u.pa.invstd->as<float>(),
+      apply_bn(M, C, u.pa.z->p, u.pa.z16, C, 0, u.pa.mean->as<float>(), u.pa.invstd->as<float>(),
                              th + u.pa.g_off, th + u.pa.b_off, 0, 1.f, nullptr, out[u.dst()], nullptr, st);
-      apply_bn(M, C, L.z->as<float>(), C, 0, L.mean->as<float>(), L.invstd->as<float>(),
+      apply_bn(M, C, L.z->p, L.z16, C, 0, L.mean->as<float>(), L.invstd->as<float>(),
                              th + L.g_off, th + L.b_off, 1, 1.f, out[u.dst()], out[u.dst()], nullptr, st);
-      apply_bn(M, C, u.pb.z->as<float>(), C, 0, u.pb.mean->as<float>(), u.pb.invstd->as<float>(),
+      apply_bn(M, C, u.pb.z->p, u.pb.z16, C, 0, u.pb.mean->as<float>(), u.pb.invstd->as<float>(),
                              th + u.pb.g_off, th + u.pb.b_off, 0, 1.f, nullptr, out[u.src()], nullptr, st);
       break;
     }
@@ -576,7 +604,7 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       layer_stats(L, keep, st);
       int Ch = L.g.Co / 2;
       if (u.d.maxpool) {
-        apply_bn(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+        apply_bn(L.g.M(), L.g.Co, L.z->p, L.z16, L.g.Co, 0, L.mean->as<float>(),
                                L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
                                u.pool_a->as<float>(), nullptr, st);
         ProfScope ps("maxpool", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co * 1.25);
@@ -584,7 +612,7 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
                     u.pool_arg->as<uint8_t>(), st);
       } else {
         for (int h = 0; h < 2; ++h)
-          apply_bn(L.g.M(), Ch, L.z->as<float>(), L.g.Co, h * Ch, L.mean->as<float>(),
+          apply_bn(L.g.M(), Ch, L.z->p, L.z16, L.g.Co, h * Ch, L.mean->as<float>(),
                                  L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr, out[h],
                                  nullptr, st);
       }
@@ -640,7 +668,7 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
         layer_stats(L, true, st);
         if (u.d.maxpool) {
           // recompute the pre-pool activation and argmax (outputs go to scratch)
-          apply_bn(L.g.M(), L.g.Co, L.z->as<float>(), L.g.Co, 0, L.mean->as<float>(),
+          apply_bn(L.g.M(), L.g.Co, L.z->p, L.z16, L.g.Co, 0, L.mean->as<float>(),
                                  L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
                                  u.pool_a->as<float>(), nullptr, st);
           maxpool_fwd(u.pool_a->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, L.dz->as<float>(),

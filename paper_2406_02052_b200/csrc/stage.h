@@ -42,6 +42,8 @@ struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
   DevPtr zb, ab, dzb, xb;                    // bf16 workspace (tensor-core path)
   DevPtr w_bf16, wt_bf16;                    // bf16 shadows of the live weights
   int stats_rows = 0;                        // > 0: BN partials written by the conv epilogue
+  bool z16 = false;                          // z stored in bf16 (tensor-core conv output, reading c24)
+  bool is_stem = false;                      // no dgrad: the input is data
   int64_t M() const { return g.M(); }
 };
 

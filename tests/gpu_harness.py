@@ -104,7 +104,8 @@ def bf16_round(a):
 
 class bf16_emulation:
     """Context manager: make the oracle round conv operands to bf16 exactly where
-    libpetra runs that convolution pass on the tcgen05 engine (reading c22)."""
+    libpetra runs that convolution pass on the tcgen05 engine (reading c22), and the
+    forward result z too, which that engine stores in bf16 (reading c24)."""
 
     def __enter__(self):
         import ctypes as C
@@ -114,7 +115,7 @@ class bf16_emulation:
         cache = {}
 
         def hook(a, kind, geom):
-            mode = {"fwd": 0, "dgrad": 1, "wgrad": 2}[kind]
+            mode = {"fwd": 0, "dgrad": 1, "wgrad": 2, "fwd_out": 0}[kind]
             key = (mode, geom)
             if key not in cache:
                 g = L.PetraConvGeom(*geom)

@@ -97,11 +97,12 @@ STAGE_CASES = {
 # three-layer chains to ~1.5e-3, and a chain fed by a RECONSTRUCTED activation (the
 # second unit of a stage) to ~1e-2, largest on the cancelling BN-gradient sums; the
 # fp32 path agrees to 1e-4 on every case and padding plays no part (16x16 behaves
-# like 14x14).  Tiers for the bf16 path vs the emulating oracle: (messages and
-# parameters, per gradient tensor); the forward stays at 2e-2 vs the EXACT oracle.
+# like 14x14).  With z stored in bf16 (reading c24) the chains measure ~6e-3.
+# Tiers for the bf16 path vs the emulating oracle: (messages and parameters, per
+# gradient tensor); the forward stays at 2e-2 vs the EXACT oracle.
 BF16_TIER = {
-    "r50_bottleneck_single_14x14": (5e-3, 5e-3),
-    "r50_ds_bottleneck_single_14_to_7": (5e-3, 5e-3),
+    "r50_bottleneck_single_14x14": (1e-2, 1e-2),
+    "r50_ds_bottleneck_single_14_to_7": (1e-2, 1e-2),
     "r50_bottleneck_14x14": (2e-2, 5e-2),
     "r50_ds_bottleneck_14_to_7": (2e-2, 5e-2),
 }
