@@ -296,12 +296,19 @@ typedef struct {
  *   mode 1 dgrad   : out[B*H*W][Ci]    = addend + conv^T(a = dz[B][Ho][Wo][Co], b = w)
  *   mode 2 wgrad   : out[Co][k][k][Ci] = sum over pixels of dz (a) (x) x (b = x)
  * engine 0 = SIMT fp32 kernels, 1 = tcgen05 bf16 kernels (inputs rounded to bf16;
- * PETRA_E_UNSUPPORTED if the geometry has no tensor-core path).  addend may be NULL. */
+ * PETRA_E_UNSUPPORTED if the geometry has no tensor-core path), 2 = tcgen05 with the
+ * activation operands held zero-bordered ([B][H+2][W+2][C], as the library keeps them
+ * for 3x3 stride-1 layers; large grids then run the halo kernel).  addend may be NULL. */
 typedef struct {
   int32_t batch, h, w, cin, cout, ksize, stride;
 } petra_conv_geom;
 petra_status petra_conv_run(int32_t mode, int32_t engine, const petra_conv_geom *g, const float *a,
                             const float *b, const float *addend, float *out);
+/* Kernel benchmark: one convolution pass (as petra_conv_run, on seeded random device
+ * inputs) repeated `iters` times after one warm-up; *avg_ms = mean device time per pass
+ * (CUDA events).  flags bit 0: forward output z in bf16 (the tensor-core stage layout). */
+petra_status petra_conv_bench(int32_t mode, int32_t engine, const petra_conv_geom *g, int32_t flags,
+                              int32_t iters, float *avg_ms);
 /* Which engine the library uses for a convolution pass at a given precision:
  * 0 = SIMT fp32, 1 = tcgen05 bf16 (operands rounded to bf16, fp32 accumulation) --
  * the TMA implicit GEMM for Ci, Co multiples of 64, or, for few input channels (the

@@ -1,6 +1,7 @@
 // convtest.cu -- petra_conv_run: one convolution pass on host buffers (kernel-level tests).
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <vector>
 
 #include "../../include/petra.h"
@@ -9,13 +10,17 @@
 #include "stage.h"
 
 namespace {
+// one convolution pass on host buffers; iters > 0: also the mean device time of
+// `iters` further passes (CUDA events; operands prepared once, outside the timing)
 petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a, const float *b,
-                 const float *addend, float *out) {
+                 const float *addend, float *out, int iters = 0, float *ms = nullptr, bool out16 = false) {
   using namespace petra;
   ConvGeom g = make_geom(pg->batch, pg->h, pg->w, pg->cin, pg->cout, pg->ksize, pg->stride);
   int64_t nx = g.Min() * g.Ci, nz = g.M() * g.Co, nw = (int64_t)g.Co * g.K();
   int64_t na = mode == 0 ? nx : nz, nb = mode == 2 ? nx : nw, no = mode == 0 ? nz : (mode == 1 ? nx : nw);
-  const bool stem = engine == 1 && !conv_tc_supported(g, mode) && mode != 1 && stem_tc_supported(g);
+  const bool padded = engine == 2;  // tcgen05 on zero-bordered operands (halo kernel where eligible)
+  if (padded) engine = 1;
+  const bool stem = engine == 1 && !padded && !conv_tc_supported(g, mode) && mode != 1 && stem_tc_supported(g);
   if (engine == 1 && !stem && !conv_tc_supported(g, mode)) return PETRA_E_UNSUPPORTED;
   if (engine == 1) conv_tc_prepare();
   DevPtr da = dalloc(na * 4), db = dalloc(nb * 4), dout = dalloc(no * 4), dadd;
@@ -26,27 +31,40 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     PETRA_CUDA(cudaMemcpy(dadd->p, addend, no * 4, cudaMemcpyHostToDevice));
   }
   cudaStream_t st = nullptr;
+  DevPtr ab, bb, ws;
+  const bool a_pad = padded, b_pad = padded && mode == 2;
+  std::function<void()> launch;
   if (stem) {  // gathered-im2col tensor-core stem: fp32 image (and fp32 weights) read directly
-    DevPtr ws = dalloc(std::max<size_t>(16, stem_tc_workspace(g)));
+    ws = dalloc(std::max<size_t>(16, stem_tc_workspace(g)));
     if (mode == 0) {
-      stem_fwd_tc(g, da->as<float>(), db->as<float>(), dout->p, false, nullptr, st);
+      launch = [&] { stem_fwd_tc(g, da->as<float>(), db->as<float>(), dout->p, out16, nullptr, st); };
     } else {
-      DevPtr ab = dalloc(na * 2);
+      ab = dalloc(na * 2);
       f32_to_bf16(da->as<float>(), ab->as<__nv_bfloat16>(), na, st);
-      stem_wgrad_tc(g, ab->as<__nv_bfloat16>(), db->as<float>(), dout->as<float>(), ws->as<float>(), st);
+      launch = [&] {
+        stem_wgrad_tc(g, ab->as<__nv_bfloat16>(), db->as<float>(), dout->as<float>(), ws->as<float>(), st);
+      };
     }
-    PETRA_CUDA(cudaDeviceSynchronize());
   } else if (engine == 0) {
-    DevPtr ws = dalloc(std::max<size_t>(16, conv_wgrad_simt_workspace(g)));
-    if (mode == 0) conv_fwd_simt(g, da->as<float>(), db->as<float>(), dout->as<float>(), st);
-    else if (mode == 1)
-      conv_dgrad_simt(g, da->as<float>(), db->as<float>(), addend ? dadd->as<float>() : nullptr,
-                      dout->as<float>(), st);
-    else conv_wgrad_simt(g, da->as<float>(), db->as<float>(), dout->as<float>(), ws->as<float>(), st);
-    PETRA_CUDA(cudaDeviceSynchronize());
+    ws = dalloc(std::max<size_t>(16, conv_wgrad_simt_workspace(g)));
+    launch = [&] {
+      if (mode == 0) conv_fwd_simt(g, da->as<float>(), db->as<float>(), dout->as<float>(), st);
+      else if (mode == 1)
+        conv_dgrad_simt(g, da->as<float>(), db->as<float>(), addend ? dadd->as<float>() : nullptr,
+                        dout->as<float>(), st);
+      else conv_wgrad_simt(g, da->as<float>(), db->as<float>(), dout->as<float>(), ws->as<float>(), st);
+    };
   } else {
-    DevPtr ab = dalloc(na * 2), bb = dalloc(nb * 2);
-    f32_to_bf16(da->as<float>(), ab->as<__nv_bfloat16>(), na, st);
+    // operand a (x or dz) and, for wgrad, b (= x) zero-bordered when padded
+    const int aH = mode == 0 ? g.H : g.Ho, aW = mode == 0 ? g.W : g.Wo, aC = mode == 0 ? g.Ci : g.Co;
+    const int64_t na_buf = a_pad ? (int64_t)g.B * (aH + 2) * (aW + 2) * aC : na;
+    const int64_t nb_buf = b_pad ? (int64_t)g.B * (g.H + 2) * (g.W + 2) * g.Ci : nb;
+    ab = dalloc(na_buf * 2);
+    bb = dalloc(nb_buf * 2);
+    PETRA_CUDA(cudaMemset(ab->p, 0, na_buf * 2));
+    PETRA_CUDA(cudaMemset(bb->p, 0, nb_buf * 2));
+    if (a_pad) f32_to_bf16_padded(da->as<float>(), ab->as<__nv_bfloat16>(), g.B, aH, aW, aC, st);
+    else f32_to_bf16(da->as<float>(), ab->as<__nv_bfloat16>(), na, st);
     if (mode == 1) {  // flipped / transposed weights wT[ci][kh'][kw'][co] = w[co][k-1-kh'][k-1-kw'][ci]
       std::vector<float> wt(nw);
       int k = g.k;
@@ -58,26 +76,71 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
                   b[(((int64_t)co * k + kh) * k + kw) * g.Ci + ci];
       PETRA_CUDA(cudaMemcpy(db->p, wt.data(), nb * 4, cudaMemcpyHostToDevice));
     }
-    f32_to_bf16(db->as<float>(), bb->as<__nv_bfloat16>(), nb, st);
-    DevPtr ws = dalloc(std::max<size_t>(16, conv_tc_workspace(g, mode)));
-    if (mode == 0) conv_fwd_tc(g, ab->as<__nv_bfloat16>(), bb->as<__nv_bfloat16>(), dout->p, false, ws->as<float>(),
-                            nullptr, st);
-    else if (mode == 1)
-      conv_dgrad_tc(g, ab->as<__nv_bfloat16>(), bb->as<__nv_bfloat16>(), addend ? dadd->as<float>() : nullptr,
-                    dout->as<float>(), ws->as<float>(), st);
-    else conv_wgrad_tc(g, ab->as<__nv_bfloat16>(), bb->as<__nv_bfloat16>(), dout->as<float>(), ws->as<float>(), st);
-    PETRA_CUDA(cudaDeviceSynchronize());
+    if (b_pad) f32_to_bf16_padded(db->as<float>(), bb->as<__nv_bfloat16>(), g.B, g.H, g.W, g.Ci, st);
+    else f32_to_bf16(db->as<float>(), bb->as<__nv_bfloat16>(), nb, st);
+    ws = dalloc(std::max<size_t>(16, conv_tc_workspace(g, mode)));
+    launch = [&] {
+      if (mode == 0)
+        conv_fwd_tc(g, ab->as<__nv_bfloat16>(), a_pad, bb->as<__nv_bfloat16>(), dout->p, out16, ws->as<float>(),
+                    nullptr, st);
+      else if (mode == 1)
+        conv_dgrad_tc(g, ab->as<__nv_bfloat16>(), a_pad, bb->as<__nv_bfloat16>(),
+                      addend ? dadd->as<float>() : nullptr, dout->as<float>(), ws->as<float>(), st);
+      else
+        conv_wgrad_tc(g, ab->as<__nv_bfloat16>(), a_pad, bb->as<__nv_bfloat16>(), b_pad, dout->as<float>(),
+                      ws->as<float>(), st);
+    };
   }
-  PETRA_CUDA(cudaMemcpy(out, dout->p, no * 4, cudaMemcpyDeviceToHost));
+  launch();
+  PETRA_CUDA(cudaDeviceSynchronize());
+  if (iters > 0) {
+    cudaEvent_t e0, e1;
+    PETRA_CUDA(cudaEventCreate(&e0));
+    PETRA_CUDA(cudaEventCreate(&e1));
+    PETRA_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) launch();
+    PETRA_CUDA(cudaEventRecord(e1, st));
+    PETRA_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    PETRA_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (out) PETRA_CUDA(cudaMemcpy(out, dout->p, no * 4, cudaMemcpyDeviceToHost));
   return PETRA_OK;
 }
 }  // namespace
 
 extern "C" petra_status petra_conv_run(int32_t mode, int32_t engine, const petra_conv_geom *g, const float *a,
                                        const float *b, const float *addend, float *out) {
-  if (!g || !a || !b || !out || mode < 0 || mode > 2 || engine < 0 || engine > 1) return PETRA_E_ARG;
+  if (!g || !a || !b || !out || mode < 0 || mode > 2 || engine < 0 || engine > 2) return PETRA_E_ARG;
   try {
     return run(mode, engine, g, a, b, addend, out);
+  } catch (const petra::PetraError &e) {
+    return e.status;
+  } catch (...) {
+    cudaGetLastError();
+    return PETRA_E_CUDA;
+  }
+}
+
+extern "C" petra_status petra_conv_bench(int32_t mode, int32_t engine, const petra_conv_geom *g, int32_t flags,
+                                         int32_t iters, float *avg_ms) {
+  if (!g || !avg_ms || iters < 1 || mode < 0 || mode > 2 || engine < 0 || engine > 2) return PETRA_E_ARG;
+  try {
+    petra::ConvGeom cg = petra::make_geom(g->batch, g->h, g->w, g->cin, g->cout, g->ksize, g->stride);
+    const int64_t nx = cg.Min() * cg.Ci, nz = cg.M() * cg.Co, nw = (int64_t)cg.Co * cg.K();
+    const int64_t na = mode == 0 ? nx : nz, nb = mode == 2 ? nx : nw;
+    std::vector<float> a(na), b(nb);
+    uint32_t r = 12345u;
+    auto rnd = [&r]() {
+      r = r * 1664525u + 1013904223u;
+      return (float)((r >> 9) & 0xFFFF) / 32768.f - 1.f;
+    };
+    for (auto &v : a) v = rnd();
+    for (auto &v : b) v = rnd() * 0.05f;
+    return run(mode, engine, g, a.data(), b.data(), nullptr, nullptr, iters, avg_ms, (flags & 1) != 0);
   } catch (const petra::PetraError &e) {
     return e.status;
   } catch (...) {

@@ -13,23 +13,31 @@ size_t conv_wgrad_simt_workspace(const ConvGeom &g);
 void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *dw, float *ws, cudaStream_t st);
 
 // ---------------------------------------------------------------- tcgen05 bf16 convolutions
+// bf16 activation operands are [B][H][W][C], or -- "padded" -- [B][H+2][W+2][C] with
+// zero borders (the 3x3 / stride-1 layers: read by the halo kernel, conv_halo.cu;
+// the other kernels read the interior of a padded buffer through strided TMA views).
 bool conv_tc_supported(const ConvGeom &g, int mode);   // mode 0 fwd, 1 dgrad, 2 wgrad
 void conv_tc_prepare();  // one-time kernel attributes (before any graph capture)
 size_t conv_tc_workspace(const ConvGeom &g, int mode);  // split-K workspace bytes
 // z[m][co] = conv(x_bf16, w_bf16), stored fp32 or (z_bf16) bf16.  stats_part (nullable,
-// >= 148*4*Co*2 floats): the epilogue also writes BN partial sums of z as stored;
+// >= 148*Co*2 floats): the epilogue also writes BN partial sums of z as stored;
 // returns the number of partial rows to merge with bn_stats_from_partials (0 = not
 // fused, run bn_stats on z).
-int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, void *z, bool z_bf16, float *ws,
-                float *stats_part, cudaStream_t st);
+int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,
+                bool z_bf16, float *ws, float *stats_part, cudaStream_t st);
 void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float eps, float *mean, float *invstd,
                             float *rmean, float *rvar, float mom, cudaStream_t st);
 // dx (fp32) = addend + conv^T(dz_bf16, wT_bf16)
-void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend,
-                   float *dx, float *ws, cudaStream_t st);
+void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_padded, const __nv_bfloat16 *wt,
+                   const float *addend, float *dx, float *ws, cudaStream_t st);
 // dw (fp32) = sum_pixels dz (x) x
-void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *x, float *dw, float *ws,
-                   cudaStream_t st);
+void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_padded, const __nv_bfloat16 *x,
+                   bool x_padded, float *dw, float *ws, cudaStream_t st);
+// halo kernel (conv_halo.cu): 3x3 stride-1 pass on a padded operand
+void conv_halo_prepare();
+bool conv_halo_eligible(int B, int H, int W, int Cred, int N);
+int conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad, const __nv_bfloat16 *wmat,
+                  const float *addend, void *out, bool out16, float *stats, cudaStream_t st);
 
 // out[i] = sum over splits z of part[z * n + i], fixed order (deterministic)
 void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st);
@@ -56,20 +64,23 @@ size_t bn_counter_count(int C);  // zero-initialised unsigned counters a reducti
 template <typename TZ>
 void bn_stats(const TZ *z, int64_t M, int C, float eps, float *mean, float *invstd, float *rmean, float *rvar,
               float mom, double *part, unsigned *counter, cudaStream_t st);
+// out_bf16 (nullable) is written padded when pH > 0: rows m = (b*pH + h)*pW + w go to the
+// interior of a zero-bordered [B][pH+2][pW+2][C] buffer
 template <typename TZ, typename TO>
 void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean, const float *invstd,
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
-              __nv_bfloat16 *out_bf16, cudaStream_t st);
+              __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st);
 template <typename TZ>
 void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float *invstd, const float *gamma,
                    const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dst_in,
                    float *dst_out, __nv_bfloat16 *dst_bf16, float *dgamma, float *dbeta, double *part,
                    unsigned *counter, cudaStream_t st);
-// dz (fp32, nullable) and/or its bf16 copy (nullable: the tensor-core operand)
+// dz (fp32, nullable) and/or its bf16 copy (nullable: the tensor-core operand; padded
+// as in bn_apply when pH > 0)
 template <typename TZ>
 void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *invstd, const float *gamma,
                const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
-               const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, cudaStream_t st);
+               const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, int pH, int pW, cudaStream_t st);
 
 // ---------------------------------------------------------------- optimizer / tail / misc
 struct SgdSeg {
@@ -92,5 +103,7 @@ void maxpool_fwd(const float *a, int B, int H, int W, int C, int Ho, int Wo, flo
 void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, int H, int W, int C, int Ho, int Wo,
                  float *da, cudaStream_t st);
 void f32_to_bf16(const float *x, __nv_bfloat16 *y, int64_t n, cudaStream_t st);
+// y = bf16(x) into the interior of a zero-bordered [B][H+2][W+2][C] buffer
+void f32_to_bf16_padded(const float *x, __nv_bfloat16 *y, int B, int H, int W, int C, cudaStream_t st);
 
 }  // namespace petra

@@ -41,6 +41,23 @@ __device__ __forceinline__ void st4(__nv_bfloat16 *p, int64_t i, float4 v) {
 }
 __device__ __forceinline__ float f4(const float4 &v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
 
+// row of flat index i over rows of C4 float4 groups (shift when C4 is a power of two)
+__device__ __forceinline__ int64_t row_of(int64_t i, int C4, int sh) { return sh >= 0 ? (i >> sh) : i / C4; }
+inline int log2_or_neg(int v) {
+  if (v <= 0 || (v & (v - 1))) return -1;
+  int s = 0;
+  while ((1 << s) < v) ++s;
+  return s;
+}
+// row m of an H x W grid -> row of the zero-bordered (H+2) x (W+2) layout (pH <= 0: m)
+__device__ __forceinline__ int64_t pad_row(int64_t m, int pH, int pW) {
+  if (pH <= 0) return m;
+  const int64_t hw = (int64_t)pH * pW;
+  const int64_t b = m / hw;
+  const int r = (int)(m - b * hw), h = r / pW, w = r - h * pW;
+  return (b * (pH + 2) + h + 1) * (pW + 2) + w + 1;
+}
+
 // reduction blocks: one wave of NT-thread blocks (stats 1024, backward reduce 512:
 // >= 64 KB of loads in flight per SM)
 constexpr int RT_STATS = 1024, RT_BWD = 512;
@@ -234,13 +251,14 @@ template <typename TZ, typename TO>
 __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int ldz, int zc0,
                                 const float *__restrict__ mean, const float *__restrict__ invstd,
                                 const float *__restrict__ gamma, const float *__restrict__ beta, int relu,
-                                float sign, const float *acc, TO *out, __nv_bfloat16 *out_bf16) {
+                                float sign, const float *acc, TO *out, __nv_bfloat16 *out_bf16, int pH, int pW,
+                                int sh) {
   const bool vec = (C % 4 == 0) && (ldz % 4 == 0) && (zc0 % 4 == 0);
   if (vec) {
     const int C4 = C / 4;
     const int64_t n = M * C4;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-      int64_t m = i / C4;
+      int64_t m = row_of(i, C4, sh);
       int c = (int)(i - m * C4) * 4;
       int cz = zc0 + c;
       float4 zv = ld4(z, m * ldz + cz);
@@ -257,7 +275,7 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
         o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
       }
       if (out) st4(out, m * C + c, o);
-      if (out_bf16) st4(out_bf16, m * C + c, o);
+      if (out_bf16) st4(out_bf16, pad_row(m, pH, pW) * C + c, o);
     }
     return;
   }
@@ -271,7 +289,7 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
     float o = sign * y;
     if (acc) o += acc[i];
     if (out) stv(out, i, o);
-    if (out_bf16) out_bf16[i] = __float2bfloat16_rn(o);
+    if (out_bf16) out_bf16[pad_row(m, pH, pW) * C + c] = __float2bfloat16_rn(o);
   }
 }
 
@@ -378,14 +396,15 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
                                  const float *__restrict__ invstd, const float *__restrict__ gamma,
                                  const float *__restrict__ beta, int relu, const float *dy0, const float *dy1,
                                  int cs, const float *__restrict__ dgamma, const float *__restrict__ dbeta,
-                                 float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16) {
+                                 float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW,
+                                 int sh) {
   const float invM = 1.0f / (float)M;
   const bool vec = (C % 4 == 0) && (dy1 == nullptr || cs % 4 == 0);
   if (vec) {
     const int C4 = C / 4;
     const int64_t n = M * C4;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-      int64_t m = i / C4;
+      int64_t m = row_of(i, C4, sh);
       int c = (int)(i - m * C4) * 4;
       float4 zv = ld4(z, m * C + c);
       float4 g4 = load_dy4(dy0, dy1, cs, C, m, c);
@@ -400,7 +419,7 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
         op[k] = gamma[c + k] * is * (g - dbeta[c + k] * invM - xh * dgamma[c + k] * invM);
       }
       if (dz) st4(dz, m * C + c, o);
-      if (dz_bf16) st4(dz_bf16, m * C + c, o);
+      if (dz_bf16) st4(dz_bf16, pad_row(m, pH, pW) * C + c, o);
     }
     return;
   }
@@ -414,7 +433,7 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
     if (relu && !(fmaf(gamma[c], xh, beta[c]) > 0.f)) g = 0.f;
     float v = gamma[c] * is * (g - dbeta[c] * invM - xh * dgamma[c] * invM);
     if (dz) stv(dz, i, v);
-    if (dz_bf16) dz_bf16[i] = __float2bfloat16_rn(v);
+    if (dz_bf16) dz_bf16[pad_row(m, pH, pW) * C + c] = __float2bfloat16_rn(v);
   }
 }
 
@@ -445,17 +464,18 @@ template void bn_stats<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int, float
 template <typename TZ, typename TO>
 void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean, const float *invstd,
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
-              __nv_bfloat16 *out_bf16, cudaStream_t st) {
+              __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st) {
   bn_apply_kernel<TZ, TO><<<ew_grid(M * C / 4), 256, 0, st>>>(M, C, z, ldz, zc0, mean, invstd, gamma, beta, relu,
-                                                              sign, acc, out, out_bf16);
+                                                              sign, acc, out, out_bf16, pH, pW,
+                                                              log2_or_neg(C / 4));
   PETRA_LAUNCH_CHECK();
 }
 template void bn_apply<float, float>(int64_t, int, const float *, int, int, const float *, const float *,
                                      const float *, const float *, int, float, const float *, float *,
-                                     __nv_bfloat16 *, cudaStream_t);
+                                     __nv_bfloat16 *, int, int, cudaStream_t);
 template void bn_apply<__nv_bfloat16, float>(int64_t, int, const __nv_bfloat16 *, int, int, const float *,
                                              const float *, const float *, const float *, int, float,
-                                             const float *, float *, __nv_bfloat16 *, cudaStream_t);
+                                             const float *, float *, __nv_bfloat16 *, int, int, cudaStream_t);
 
 template <typename TZ>
 void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float *invstd, const float *gamma,
@@ -479,16 +499,17 @@ template void bn_bwd_reduce<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int, 
 template <typename TZ>
 void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *invstd, const float *gamma,
                const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
-               const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, cudaStream_t st) {
+               const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, int pH, int pW, cudaStream_t st) {
   bn_bwd_dz_kernel<TZ><<<ew_grid(M * C / 4), 256, 0, st>>>(M, C, z, mean, invstd, gamma, beta, relu, dy0, dy1, cs,
-                                                           dgamma, dbeta, dz, dz_bf16);
+                                                           dgamma, dbeta, dz, dz_bf16, pH, pW, log2_or_neg(C / 4));
   PETRA_LAUNCH_CHECK();
 }
 template void bn_bwd_dz<float>(int64_t, int, const float *, const float *, const float *, const float *,
                                const float *, int, const float *, const float *, int, const float *, const float *,
-                               float *, __nv_bfloat16 *, cudaStream_t);
+                               float *, __nv_bfloat16 *, int, int, cudaStream_t);
 template void bn_bwd_dz<__nv_bfloat16>(int64_t, int, const __nv_bfloat16 *, const float *, const float *,
                                        const float *, const float *, int, const float *, const float *, int,
-                                       const float *, const float *, float *, __nv_bfloat16 *, cudaStream_t);
+                                       const float *, const float *, float *, __nv_bfloat16 *, int, int,
+                                       cudaStream_t);
 
 }  // namespace petra

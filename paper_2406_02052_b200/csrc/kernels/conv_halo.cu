@@ -1,0 +1,356 @@
+// conv_halo.cu -- 3x3 / stride-1 tcgen05 convolutions on a zero-bordered activation
+// buffer, with ONE A load per 64-channel block instead of one per tap.
+//
+// The bf16 operand x (forward) or dz (stride-1 dgrad) is stored padded, [B][H+2][W+2][C]
+// with zero borders (written so by its producer kernels).  GEMM rows are the padded
+// positions p of that grid; tap (kh, kw) reads row p + (kh-1)*(W+2) + (kw-1).  A tile of
+// 128 consecutive positions therefore needs the contiguous "halo" run of rows
+// [m0 - (W+3), m0 + 127 + (W+3)] -- one 2-D TMA box per channel block -- and each tap's
+// A operand is the same smem run viewed from a start shifted by whole 128-byte rows.
+// (Measured, tools/umma_shift_probe.cu: the 128B swizzle of a tcgen05 K-major operand
+// follows the absolute smem address, so row-shifted descriptor starts with base
+// offset 0 read exactly the rows a TMA box wrote.)  Compared with the per-tap im2col
+// boxes of conv_tc.cu this cuts the A bytes moved into shared memory 9x.
+// Border positions are computed and dropped by the epilogue, which stages each warp's
+// 32 rows in smem and writes them out coalesced (8 lanes per 128-byte pixel chunk).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "../errors.h"
+#include "../kernels.h"
+#include "tc_common.cuh"
+
+namespace petra {
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kHaloMax = 256;                   // TMA box height limit
+constexpr uint32_t kHaloBytes = kHaloMax * 128;  // one A stage (32 KB)
+constexpr uint32_t kRowPitch = 144;              // epilogue staging row pitch (bank spread)
+constexpr uint32_t kEpiWarp = 32 * kRowPitch;
+constexpr int kMaxStatN = 512;
+
+struct HaloParams {
+  int Mp;                  // GEMM rows = B * Hp * Wp padded positions
+  int N;                   // output channels
+  int CB, Cred;            // 64-channel blocks / channels of the reduction operand
+  int ntaps;
+  int off[9], wk[9];       // A row offset and weight tap index of each tap
+  int Hp, Wp, H, W, B;
+  int lead, HR;            // halo rows before the tile (Wp + 1); rows per halo box
+  const float *addend;     // nullable, fp32 output only
+  void *out;               // [B][H][W][N] fp32 or bf16
+  float *stats;            // nullable: one BN partial row per CTA [grid][N][2]
+};
+
+template <int BN, int ASTAGES, int BSTAGES, bool OUT16>
+__global__ void __launch_bounds__(kThreads, 1)
+conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ HaloParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t B_BYTES = BN * 128;
+  uint8_t *sA = smem;
+  uint8_t *sB = sA + ASTAGES * kHaloBytes;
+  uint64_t *afull = reinterpret_cast<uint64_t *>(sB + BSTAGES * B_BYTES);
+  uint64_t *aempty = afull + ASTAGES;
+  uint64_t *bfull = aempty + ASTAGES;
+  uint64_t *bempty = bfull + BSTAGES;
+  uint64_t *tfull = bempty + BSTAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint8_t *sepi = reinterpret_cast<uint8_t *>(afull) + 512;   // [4 warps][32 rows x 144 B]
+  float *sstat = reinterpret_cast<float *>(sepi + 4 * kEpiWarp);  // [4][N][2]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_nt = P.N / BN;
+  const int n_work = (int)cdiv(P.Mp, 128) * n_nt;
+  const int GHW = P.Hp * P.Wp;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ASTAGES; ++s) {
+      tc::mbar_init(&afull[s], 1);
+      tc::mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < BSTAGES; ++s) {
+      tc::mbar_init(&bfull[s], 1);
+      tc::mbar_init(&bempty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);
+    }
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer: halo per channel block, B per (channel block, tap)
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int mt = w / n_nt, nt = w % n_nt;
+        const int r0 = mt * 128 - P.lead;  // may be negative: TMA zero-fills
+        for (int cb = 0; cb < P.CB; ++cb) {
+          tc::mbar_wait(&aempty[as], aph ^ 1);
+          tc::mbar_arrive_expect_tx(&afull[as], P.HR * 128);
+          tc::tma_load_2d(sA + as * kHaloBytes, &tmA, &afull[as], cb * 64, r0);
+          if (++as == ASTAGES) { as = 0; aph ^= 1; }
+          for (int t = 0; t < P.ntaps; ++t) {
+            tc::mbar_wait(&bempty[bs], bph ^ 1);
+            tc::mbar_arrive_expect_tx(&bfull[bs], B_BYTES);
+            tc::tma_load_2d(sB + bs * B_BYTES, &tmB, &bfull[bs], P.wk[t] * P.Cred + cb * 64, nt * BN);
+            if (++bs == BSTAGES) { bs = 0; bph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = tc::idesc_bf16(128, BN, 0, 0);
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
+      int it = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+        const int acc = it & 1;
+        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t dtm = tmem_base + acc * BN;
+        for (int cb = 0; cb < P.CB; ++cb) {
+          tc::mbar_wait(&afull[as], aph);
+          tc::tc_fence_after();
+          const uint32_t abase = tc::smem_u32(sA + as * kHaloBytes) + P.lead * 128;
+          for (int t = 0; t < P.ntaps; ++t) {
+            tc::mbar_wait(&bfull[bs], bph);
+            tc::tc_fence_after();
+            const uint64_t ad = tc::sw128_desc(abase + P.off[t] * 128, 16, 1024);
+            const uint64_t bd = tc::sw128_desc(tc::smem_u32(sB + bs * B_BYTES), 16, 1024);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (cb > 0 || t > 0 || k > 0) ? 1u : 0u);
+            tc::umma_commit(&bempty[bs]);
+            if (++bs == BSTAGES) { bs = 0; bph ^= 1; }
+          }
+          tc::umma_commit(&aempty[as]);
+          if (++as == ASTAGES) { as = 0; aph ^= 1; }
+        }
+        tc::umma_commit(&tfull[acc]);
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..5
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    float *my_stat = sstat + (size_t)q * P.N * 2;
+    uint8_t *ebuf = sepi + q * kEpiWarp;
+    if (P.stats)
+      for (int i = lane; i < 2 * P.N; i += 32) my_stat[i] = 0.f;
+    __syncwarp();
+    constexpr int ES = OUT16 ? 2 : 4;
+    constexpr int CW = 128 / ES;  // columns per 128-byte chunk
+    int it = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      const int mt = w / n_nt, nt = w % n_nt;
+      const int acc = it & 1;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const int m = mt * 128 + row;
+      const int b = m / GHW, r = m % GHW, hp = r / P.Wp, wp = r % P.Wp;
+      const bool valid = b < P.B && hp >= 1 && hp <= P.H && wp >= 1 && wp <= P.W;
+      const int64_t opix = valid ? ((int64_t)b * P.H + hp - 1) * P.W + wp - 1 : -1;
+      const float *arow = (valid && P.addend) ? P.addend + opix * P.N + nt * BN : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += CW) {
+        float v[CW];
+#pragma unroll
+        for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
+        if (arow) {
+#pragma unroll
+          for (int jj = 0; jj < CW; jj += 4) {
+            const float4 a4 = *reinterpret_cast<const float4 *>(arow + c + jj);
+            v[jj] += a4.x; v[jj + 1] += a4.y; v[jj + 2] += a4.z; v[jj + 3] += a4.w;
+          }
+        }
+        // stage this lane's row (128 B) ...
+        uint8_t *rp = ebuf + lane * kRowPitch;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint4 u;
+          if constexpr (OUT16) {
+            uint32_t wv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 hb = __floats2bfloat162_rn(v[8 * ch + 2 * e], v[8 * ch + 2 * e + 1]);
+              wv[e] = *reinterpret_cast<uint32_t *>(&hb);
+              const float2 f = __bfloat1622float2(hb);  // statistics of the stored values (reading c24)
+              v[8 * ch + 2 * e] = f.x;
+              v[8 * ch + 2 * e + 1] = f.y;
+            }
+            u = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          } else {
+            u = make_uint4(__float_as_uint(v[4 * ch]), __float_as_uint(v[4 * ch + 1]), __float_as_uint(v[4 * ch + 2]),
+                           __float_as_uint(v[4 * ch + 3]));
+          }
+          *reinterpret_cast<uint4 *>(rp + ch * 16) = u;
+        }
+        __syncwarp();
+        // ... and write the warp's 32 rows out: 8 lanes per 128-byte pixel chunk
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int idx = k * 32 + lane, rr = idx >> 3, piece = idx & 7;
+          const int64_t op = __shfl_sync(0xffffffffu, opix, rr);
+          if (op >= 0) {
+            const uint4 u = *reinterpret_cast<const uint4 *>(ebuf + rr * kRowPitch + piece * 16);
+            char *dst = static_cast<char *>(P.out) + (op * P.N + nt * BN + c) * ES + piece * 16;
+            *reinterpret_cast<uint4 *>(dst) = u;
+          }
+        }
+        __syncwarp();
+        if (P.stats) {
+#pragma unroll
+          for (int h = 0; h < CW; h += 16) {
+            float x[16], sq[16];
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              x[jj] = valid ? v[h + jj] : 0.f;
+              sq[jj] = x[jj] * x[jj];
+            }
+            tc::colsum16(x, lane);
+            tc::colsum16(sq, lane);
+            if (!(lane & 1)) {
+              const int col = nt * BN + c + h + (lane >> 1);
+              my_stat[2 * col] += x[0];
+              my_stat[2 * col + 1] += sq[0];
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+    if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      float *g = P.stats + (size_t)blockIdx.x * P.N * 2;
+      for (int i = q * 32 + lane; i < 2 * P.N; i += 128)
+        g[i] = (sstat[i] + sstat[2 * P.N + i]) + (sstat[4 * P.N + i] + sstat[6 * P.N + i]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+constexpr int a_stages(int) { return 2; }
+constexpr int b_stages(int BN) { return BN == 256 ? 3 : (BN == 128 ? 6 : 10); }
+constexpr size_t halo_smem(int BN) {
+  return 1024 + (size_t)a_stages(BN) * kHaloBytes + (size_t)b_stages(BN) * BN * 128 + 512 + 4 * kEpiWarp +
+         (size_t)kMaxStatN * 32;
+}
+
+template <int BN, bool OUT16>
+void launch(const CUtensorMap &ta, const CUtensorMap &tb, const HaloParams &P, cudaStream_t st) {
+  const int work = (int)cdiv(P.Mp, 128) * (P.N / BN);
+  conv_halo_kernel<BN, a_stages(BN), b_stages(BN), OUT16>
+      <<<std::min(work, kNumSMs), kThreads, halo_smem(BN), st>>>(ta, tb, P);
+  PETRA_LAUNCH_CHECK();
+}
+
+int pick_bn(int N, int mtiles) {
+  int bn = 64;
+  for (int c : {256, 128, 64})
+    if (N % c == 0) {
+      bn = c;
+      if (mtiles * (N / c) >= kNumSMs) break;
+    }
+  return bn;
+}
+
+}  // namespace
+
+void conv_halo_prepare() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto set = [](const void *f, int BN) {
+      PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)halo_smem(BN)));
+    };
+    set((const void *)conv_halo_kernel<64, a_stages(64), b_stages(64), false>, 64);
+    set((const void *)conv_halo_kernel<128, a_stages(128), b_stages(128), false>, 128);
+    set((const void *)conv_halo_kernel<256, a_stages(256), b_stages(256), false>, 256);
+    set((const void *)conv_halo_kernel<64, a_stages(64), b_stages(64), true>, 64);
+    set((const void *)conv_halo_kernel<128, a_stages(128), b_stages(128), true>, 128);
+    set((const void *)conv_halo_kernel<256, a_stages(256), b_stages(256), true>, 256);
+  });
+}
+
+// a 3x3 stride-1 pass whose padded grid tiles fill at least ~3/4 of a wave of SMs
+// (smaller grids keep the split-K path of conv_tc.cu)
+bool conv_halo_eligible(int B, int H, int W, int Cred, int N) {
+  if (Cred % 64 || N % 64) return false;
+  const int Wp = W + 2, Hp = H + 2;
+  if (128 + 2 * (Wp + 1) > kHaloMax) return false;
+  const int64_t Mp = (int64_t)B * Hp * Wp;
+  if (Mp >= ((int64_t)1 << 31)) return false;
+  const int mtiles = (int)cdiv(Mp, 128);
+  const int bn = pick_bn(N, mtiles);
+  return (int64_t)mtiles * (N / bn) * 4 >= (int64_t)kNumSMs * 3;
+}
+
+// out[b][h][w][n] (= addend +) sum_{tap, c} a_pad[b][h+kh][w+kw][c] * wmat[n][wk(tap)*Cred + c]
+// a_pad: [B][H+2][W+2][Cred] bf16 with zero borders; wmat: [N][9*Cred] bf16
+// (forward: x and w; stride-1 dgrad: dz and the flipped/transposed wT, same tap order).
+int conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad, const __nv_bfloat16 *wmat,
+                  const float *addend, void *out, bool out16, float *stats, cudaStream_t st) {
+  if (!conv_halo_eligible(B, H, W, Cred, N)) throw PetraError(PETRA_E_UNSUPPORTED, "conv_halo_run: geometry");
+  if (out16 && addend) throw PetraError(PETRA_E_ARG, "conv_halo_run: addend needs an fp32 output");
+  conv_halo_prepare();
+  HaloParams P{};
+  P.Hp = H + 2;
+  P.Wp = W + 2;
+  P.H = H;
+  P.W = W;
+  P.B = B;
+  P.Mp = B * P.Hp * P.Wp;
+  P.N = N;
+  P.Cred = Cred;
+  P.CB = Cred / 64;
+  P.ntaps = 9;
+  for (int t = 0; t < 9; ++t) {
+    P.off[t] = (t / 3 - 1) * P.Wp + (t % 3 - 1);
+    P.wk[t] = t;
+  }
+  P.lead = P.Wp + 1;
+  P.HR = 128 + 2 * P.lead;
+  P.addend = addend;
+  P.out = out;
+  P.stats = N <= kMaxStatN ? stats : nullptr;
+  const int mtiles = (int)cdiv(P.Mp, 128);
+  const int BN = pick_bn(N, mtiles);
+  cuuint64_t adims[2] = {(cuuint64_t)Cred, (cuuint64_t)P.Mp};
+  cuuint64_t ast[1] = {(cuuint64_t)Cred * 2};
+  cuuint32_t abox[2] = {64, (cuuint32_t)P.HR};
+  cuuint32_t es[2] = {1, 1};
+  CUtensorMap ta = tma_map(a_pad, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, adims, ast, abox, es);
+  CUtensorMap tb = kmajor_map_bf16(wmat, N, 9 * Cred, BN);
+  if (out16) {
+    if (BN == 256) launch<256, true>(ta, tb, P, st);
+    else if (BN == 128) launch<128, true>(ta, tb, P, st);
+    else launch<64, true>(ta, tb, P, st);
+  } else {
+    if (BN == 256) launch<256, false>(ta, tb, P, st);
+    else if (BN == 128) launch<128, false>(ta, tb, P, st);
+    else launch<64, false>(ta, tb, P, st);
+  }
+  return P.stats ? std::min(mtiles * (N / BN), kNumSMs) : 0;
+}
+
+}  // namespace petra

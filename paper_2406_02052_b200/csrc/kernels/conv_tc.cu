@@ -596,14 +596,18 @@ CUtensorMap make_map(const void *base, int rank, const cuuint64_t *dims, const c
   return m;
 }
 
-// activation map [B][H][W][C] bf16; box = (64 ch, Gw output cols, R output rows, NB
-// images) read with traversal stride s along W and H (the box spans s*Gw x s*R inputs)
-CUtensorMap act_map(const __nv_bfloat16 *x, int B, int H, int W, int C, int Gw, int R, int NB, int s) {
+// activation map [B][H][W][C] bf16 (or the interior of a zero-bordered [B][H+2][W+2][C]
+// buffer: padded); box = (64 ch, Gw output cols, R output rows, NB images) read with
+// traversal stride s along W and H (the box spans s*Gw x s*R inputs)
+CUtensorMap act_map(const __nv_bfloat16 *x, int B, int H, int W, int C, int Gw, int R, int NB, int s,
+                    bool padded = false) {
+  const int P = padded ? 1 : 0;
+  const __nv_bfloat16 *base = x + (padded ? ((int64_t)(W + 2) + 1) * C : 0);
   cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
-  cuuint64_t st[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  cuuint64_t st[3] = {(cuuint64_t)C * 2, (cuuint64_t)(W + 2 * P) * C * 2, (cuuint64_t)(H + 2 * P) * (W + 2 * P) * C * 2};
   cuuint32_t box[4] = {64, (cuuint32_t)(Gw * s), (cuuint32_t)(R * s), (cuuint32_t)NB};
   cuuint32_t es[4] = {1, (cuuint32_t)s, (cuuint32_t)s, 1};
-  return make_map(x, 4, dims, st, box, es);
+  return make_map(base, 4, dims, st, box, es);
 }
 
 // K-major matrix [rows][K] bf16, box (64 K, box_rows)
@@ -756,8 +760,10 @@ bool geom_ok(const ConvGeom &g) {
   return true;
 }
 
-int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, void *out, bool out16, float *ws,
-            float *stats, cudaStream_t st) {
+int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const __nv_bfloat16 *w, void *out, bool out16,
+            float *ws, float *stats, cudaStream_t st) {
+  if (x_pad && g.k == 3 && g.s == 1 && conv_halo_eligible(g.B, g.H, g.W, g.Ci, g.Co))
+    return conv_halo_run(g.B, g.H, g.W, g.Ci, g.Co, x, w, nullptr, out, out16, stats, st);
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
   ConvTCParams P{};
   P.M = (int)t.M();
@@ -781,19 +787,23 @@ int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, v
   P.oss = 1;
   P.out = out;
   P.stats = stats;
-  CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, t.Wb, t.R, t.NB, g.s);
+  CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, t.Wb, t.R, t.NB, g.s, x_pad);
   launch_any(ta, w, g.Co, g.K(), P, ws, out16, st);
   if (!P.stats) return 0;
   const int BN = conv_plan(P.M, P.N, P.ntaps * P.CB).BN;
   return std::min((P.M / BM) * (P.N / BN) * P.splits, kNumSMs);  // partial rows written (one per CTA)
 }
 
-void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend, float *dx,
-               float *ws, cudaStream_t st) {
+void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_pad, const __nv_bfloat16 *wt, const float *addend,
+               float *dx, float *ws, cudaStream_t st) {
   // A = dz [B][Ho][Wo][Co] (stride-1 boxes), B = wT [Ci][k*k*Co], N = Ci
   const int wK = g.k * g.k * g.Co;
+  if (dz_pad && g.k == 3 && g.s == 1 && conv_halo_eligible(g.B, g.Ho, g.Wo, g.Co, g.Ci)) {
+    conv_halo_run(g.B, g.Ho, g.Wo, g.Co, g.Ci, dz, wt, addend, dx, false, nullptr, st);
+    return;
+  }
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
-  CUtensorMap ta = act_map(dz, g.B, g.Ho, g.Wo, g.Co, t.Wb, t.R, t.NB, 1);
+  CUtensorMap ta = act_map(dz, g.B, g.Ho, g.Wo, g.Co, t.Wb, t.R, t.NB, 1, dz_pad);
   ConvTCParams P{};
   P.M = (int)t.M();
   P.N = g.Ci;
@@ -903,6 +913,7 @@ void conv_tc_prepare() {
     setw((const void *)wgrad_tc_kernel<64, 6>, 6, 64);
   });
   stem_tc_prepare();
+  conv_halo_prepare();
 }
 
 bool conv_tc_supported(const ConvGeom &g, int mode) {
@@ -923,9 +934,9 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode) {
   return p.splits > 1 ? (size_t)p.splits * M * N * sizeof(float) : 0;
 }
 
-int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, void *z, bool z_bf16, float *ws,
-                float *stats_part, cudaStream_t st) {
-  return run_fwd(g, x, w, z, z_bf16, ws, stats_part, st);
+int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,
+                bool z_bf16, float *ws, float *stats_part, cudaStream_t st) {
+  return run_fwd(g, x, x_padded, w, z, z_bf16, ws, stats_part, st);
 }
 
 void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float eps, float *mean, float *invstd,
@@ -934,13 +945,18 @@ void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float ep
   PETRA_LAUNCH_CHECK();
 }
 
-void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *wt, const float *addend,
-                   float *dx, float *ws, cudaStream_t st) {
-  run_dgrad(g, dz, wt, addend, dx, ws, st);
+void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_padded, const __nv_bfloat16 *wt,
+                   const float *addend, float *dx, float *ws, cudaStream_t st) {
+  run_dgrad(g, dz, dz_padded, wt, addend, dx, ws, st);
 }
 
 CUtensorMap kmajor_map_bf16(const __nv_bfloat16 *m, int rows, int K, int box_rows) {
   return mat_map(m, rows, K, box_rows);
+}
+
+CUtensorMap tma_map(const void *base, CUtensorMapDataType dt, int rank, const cuuint64_t *dims,
+                    const cuuint64_t *strides_bytes, const cuuint32_t *box, const cuuint32_t *es) {
+  return make_map(base, rank, dims, strides_bytes, box, es, dt);
 }
 
 void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st) {
@@ -948,12 +964,12 @@ void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream
   PETRA_LAUNCH_CHECK();
 }
 
-void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *x, float *dw, float *ws,
-                   cudaStream_t st) {
+void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_padded, const __nv_bfloat16 *x,
+                   bool x_padded, float *dw, float *ws, cudaStream_t st) {
   WgradPlan w = wgrad_plan(g);
-  CUtensorMap tx = act_map(x, g.B, g.H, g.W, g.Ci, w.t.Wb, w.t.R, w.t.NB, g.s);
+  CUtensorMap tx = act_map(x, g.B, g.H, g.W, g.Ci, w.t.Wb, w.t.R, w.t.NB, g.s, x_padded);
   // dz [B][Ho][Wo][Co], box (64 ch, 64 padded pixels); padding pixels out of bounds -> 0
-  CUtensorMap tdz = act_map(dz, g.B, g.Ho, g.Wo, g.Co, w.t.Wb, w.t.R, w.t.NB, 1);
+  CUtensorMap tdz = act_map(dz, g.B, g.Ho, g.Wo, g.Co, w.t.Wb, w.t.R, w.t.NB, 1, dz_padded);
   WgradParams P{};
   P.Mr = g.K();
   P.N = g.Co;

@@ -287,6 +287,24 @@ __global__ void f32_to_bf16_kernel(const float *__restrict__ x, __nv_bfloat16 *_
     y[i] = __float2bfloat16_rn(x[i]);
 }
 
+// interior of a zero-bordered [B][H+2][W+2][C] bf16 buffer (C % 4 == 0)
+__global__ void f32_to_bf16_padded_kernel(const float4 *__restrict__ x, uint2 *__restrict__ y, int B, int H, int W,
+                                          int C4) {
+  const int64_t n = (int64_t)B * H * W * C4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C4);
+    const int64_t m = i / C4;
+    const int w = (int)(m % W);
+    const int64_t r = m / W;
+    const int h = (int)(r % H);
+    const int64_t b = r / H;
+    const float4 v = x[i];
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    y[((b * (H + 2) + h + 1) * (W + 2) + w + 1) * C4 + c] =
+        make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+  }
+}
+
 inline unsigned ew_grid(int64_t n) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs));
 }
@@ -345,6 +363,13 @@ void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, in
   } else {
     maxpool_bwd_kernel<<<ew_grid((int64_t)B * H * W * C), 256, 0, st>>>(d1, d2, arg, B, H, W, C, Ho, Wo, da);
   }
+  PETRA_LAUNCH_CHECK();
+}
+
+void f32_to_bf16_padded(const float *x, __nv_bfloat16 *y, int B, int H, int W, int C, cudaStream_t st) {
+  const int C4 = C / 4;
+  f32_to_bf16_padded_kernel<<<ew_grid((int64_t)B * H * W * C4), 256, 0, st>>>(
+      reinterpret_cast<const float4 *>(x), reinterpret_cast<uint2 *>(y), B, H, W, C4);
   PETRA_LAUNCH_CHECK();
 }
 

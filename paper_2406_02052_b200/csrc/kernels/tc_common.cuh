@@ -161,5 +161,8 @@ __device__ __forceinline__ void colsum16(float (&x)[16], int lane) {
 
 // host: 2-D TMA map of a row-major bf16 matrix [rows][K], 128B swizzle, box (64 K, box_rows)
 CUtensorMap kmajor_map_bf16(const __nv_bfloat16 *m, int rows, int K, int box_rows);
+// host: any tiled TMA map with 128B swizzle (throws PetraError on failure)
+CUtensorMap tma_map(const void *base, CUtensorMapDataType dt, int rank, const cuuint64_t *dims,
+                    const cuuint64_t *strides_bytes, const cuuint32_t *box, const cuuint32_t *es);
 
 }  // namespace petra

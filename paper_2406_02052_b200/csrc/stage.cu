@@ -14,6 +14,8 @@
 //   update                 PAPER.md:135, 256 (Nesterov 0.9, wd exclusions)
 #include "stage.h"
 
+#include <cstdlib>
+
 #include <cmath>
 #include <cstring>
 
@@ -113,8 +115,21 @@ void Stage::alloc_layer(Layer &L, bool inner) {
   if (tc_) {
     L.w_bf16 = dalloc((int64_t)L.g.Co * L.g.K() * sizeof(__nv_bfloat16));
     L.wt_bf16 = dalloc((int64_t)L.g.Co * L.g.K() * sizeof(__nv_bfloat16));
-    L.dzb = dalloc(n * sizeof(__nv_bfloat16));
-    L.xb = dalloc(L.g.Min() * L.g.Ci * sizeof(__nv_bfloat16));
+    // 3x3 stride-1 layers keep their bf16 operands zero-bordered for the halo kernel
+    // (opt-in, PETRA_HALO=1: measured no faster than the per-tap im2col kernel yet)
+    static const bool halo = [] {
+      const char *e = getenv("PETRA_HALO");
+      return e && e[0] == '1';
+    }();
+    const bool s1k3 = halo && !L.is_stem && L.g.k == 3 && L.g.s == 1;
+    L.xpad = s1k3 && conv_tc_supported(L.g, 0);
+    L.dzpad = s1k3 && conv_tc_supported(L.g, 1);
+    const int64_t nxb = L.xpad ? (int64_t)L.g.B * (L.g.H + 2) * (L.g.W + 2) * L.g.Ci : L.g.Min() * L.g.Ci;
+    const int64_t ndz = L.dzpad ? (int64_t)L.g.B * (L.g.Ho + 2) * (L.g.Wo + 2) * L.g.Co : n;
+    L.dzb = dalloc(ndz * sizeof(__nv_bfloat16));
+    L.xb = dalloc(nxb * sizeof(__nv_bfloat16));
+    if (L.dzpad) PETRA_CUDA(cudaMemset(L.dzb->p, 0, ndz * sizeof(__nv_bfloat16)));  // borders stay zero
+    if (L.xpad) PETRA_CUDA(cudaMemset(L.xb->p, 0, nxb * sizeof(__nv_bfloat16)));
   }
 }
 
@@ -398,15 +413,16 @@ void Stage::enqueue_update(cudaStream_t st) {
 // ------------------------------------------------------------------ layer kernels
 static void apply_bn(int64_t M, int C, const void *z, bool z16, int ldz, int zc0, const float *mean,
                      const float *invstd, const float *gamma, const float *beta, int relu, float sign,
-                     const float *acc, float *out, __nv_bfloat16 *out_bf16, cudaStream_t st) {
+                     const float *acc, float *out, __nv_bfloat16 *out_bf16, cudaStream_t st, int pH = 0,
+                     int pW = 0) {
   ProfScope ps("bn_apply", st, 0.0,
                (double)M * C * ((z16 ? 2.0 : 4.0) + (acc ? 4.0 : 0.0) + (out ? 4.0 : 0.0) + (out_bf16 ? 2.0 : 0.0)));
   if (z16)
     bn_apply<__nv_bfloat16, float>(M, C, static_cast<const __nv_bfloat16 *>(z), ldz, zc0, mean, invstd, gamma, beta,
-                                   relu, sign, acc, out, out_bf16, st);
+                                   relu, sign, acc, out, out_bf16, pH, pW, st);
   else
     bn_apply<float, float>(M, C, static_cast<const float *>(z), ldz, zc0, mean, invstd, gamma, beta, relu, sign, acc,
-                           out, out_bf16, st);
+                           out, out_bf16, pH, pW, st);
 }
 
 static double conv_flops(const ConvGeom &g) { return 2.0 * (double)g.M() * g.Co * g.K(); }
@@ -424,11 +440,12 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
   bool tc = tc_ && conv_tc_supported(L.g, 0);
   if (tc && !x_bf16_ready) {  // bf16 operand of a stream input (also read by the TC wgrad)
     ProfScope pc("cvt_bf16", st, 0.0, 6.0 * (double)L.g.Min() * L.g.Ci);
-    f32_to_bf16(x, L.xb->as<__nv_bfloat16>(), L.g.Min() * L.g.Ci, st);
+    if (L.xpad) f32_to_bf16_padded(x, L.xb->as<__nv_bfloat16>(), L.g.B, L.g.H, L.g.W, L.g.Ci, st);
+    else f32_to_bf16(x, L.xb->as<__nv_bfloat16>(), L.g.Min() * L.g.Ci, st);
   }
   ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    L.stats_rows = conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.w_bf16->as<__nv_bfloat16>(), L.z->p, L.z16,
+    L.stats_rows = conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.xpad, L.w_bf16->as<__nv_bfloat16>(), L.z->p, L.z16,
                                wgrad_ws_->as<float>(), reinterpret_cast<float *>(part_->p), st);
   } else {
     conv_fwd_simt(L.g, x, w, L.z->as<float>(), st);
@@ -447,7 +464,8 @@ void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   if (tc) {
     // L.xb holds bf16(x) from the conv_fwd of this tick (forward or recomputation);
     // L.dzb was written in bf16 by bn_bwd_dz
-    conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.xb->as<__nv_bfloat16>(), dw, wgrad_ws_->as<float>(), st);
+    conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.xb->as<__nv_bfloat16>(), L.xpad, dw,
+                  wgrad_ws_->as<float>(), st);
   } else {
     conv_wgrad_simt(L.g, L.dz->as<float>(), x, dw, wgrad_ws_->as<float>(), st);
   }
@@ -457,7 +475,7 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
   bool tc = tc_ && conv_tc_supported(L.g, 1);
   ProfScope ps(tc ? "conv_dgrad_tc" : "conv_dgrad_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    conv_dgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.wt_bf16->as<__nv_bfloat16>(), addend, out,
+    conv_dgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.wt_bf16->as<__nv_bfloat16>(), addend, out,
                   wgrad_ws_->as<float>(), st);
   } else {
     conv_dgrad_simt(L.g, L.dz->as<float>(), theta_->as<float>() + L.w_off, addend, out, st);
@@ -503,7 +521,7 @@ void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running
       const bool need32 = !ready || !conv_tc_supported(N.g, 2);
       apply_bn(L.g.M(), L.g.Co, L.z->p, L.z16, L.g.Co, 0, L.mean->as<float>(), L.invstd->as<float>(),
                th + L.g_off, th + L.b_off, 1, 1.f, nullptr, need32 ? L.a->as<float>() : nullptr,
-               ready ? N.xb->as<__nv_bfloat16>() : nullptr, st);
+               ready ? N.xb->as<__nv_bfloat16>() : nullptr, st, N.xpad ? N.g.H : 0, N.g.W);
       x = L.a->as<float>();
     }
   }
@@ -539,10 +557,11 @@ void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, cons
   if (L.z16)
     bn_bwd_dz<__nv_bfloat16>(L.g.M(), L.g.Co, L.z->as<__nv_bfloat16>(), L.mean->as<float>(), L.invstd->as<float>(),
                              th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off,
-                             dz32, dz16, st);
+                             dz32, dz16, L.dzpad ? L.g.Ho : 0, L.g.Wo, st);
   else
     bn_bwd_dz<float>(L.g.M(), L.g.Co, L.z->as<float>(), L.mean->as<float>(), L.invstd->as<float>(), th + L.g_off,
-                     th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off, dz32, dz16, st);
+                     th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off, dz32, dz16,
+                     L.dzpad ? L.g.Ho : 0, L.g.Wo, st);
 }
 
 // VJP through a branch whose last layer receives dy (reconstruction fused when

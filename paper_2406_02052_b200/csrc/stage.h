@@ -44,6 +44,7 @@ struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
   int stats_rows = 0;                        // > 0: BN partials written by the conv epilogue
   bool z16 = false;                          // z stored in bf16 (tensor-core conv output, reading c24)
   bool is_stem = false;                      // no dgrad: the input is data
+  bool xpad = false, dzpad = false;          // xb / dzb zero-bordered [B][H+2][W+2][C] (3x3 stride-1 layers)
   int64_t M() const { return g.M(); }
 };
 

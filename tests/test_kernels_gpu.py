@@ -111,3 +111,23 @@ def test_stem_tc_vs_simt(geom, mode):
     ref = conv_run(mode, 0, geom, a, b)
     got = conv_run(mode, 1, geom, a, b)
     assert rel(got, ref) < 1e-5, rel(got, ref)
+
+
+# zero-bordered operands (engine 2): 3x3 stride-1 grids large enough for the halo
+# kernel (>= 3/4 of a wave of 128-row tiles), plus small / strided ones that read the
+# padded buffers through interior TMA views
+PAD_GEOMS = [(16, 32, 32, 64, 64, 3, 1), (8, 56, 56, 64, 64, 3, 1), (16, 16, 16, 128, 128, 3, 1),
+             (64, 8, 8, 256, 256, 3, 1), (4, 28, 28, 128, 256, 3, 1), (2, 16, 16, 64, 64, 3, 1),
+             (3, 14, 14, 256, 128, 3, 1)]
+
+
+@pytest.mark.parametrize("geom", PAD_GEOMS)
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_tc_padded_operands_vs_simt(geom, mode):
+    x, w, dz, add = inputs(geom, 7)
+    a = x if mode == 0 else dz
+    b = x if mode == 2 else w
+    addend = add if mode == 1 else None
+    ref = conv_run(mode, 0, geom, a, b, addend)
+    got = conv_run(mode, 2, geom, a, b, addend)
+    assert rel(got, ref) < 1e-5, rel(got, ref)
