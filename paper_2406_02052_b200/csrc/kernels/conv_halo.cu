@@ -25,11 +25,12 @@ namespace petra {
 namespace {
 
 constexpr int kThreads = 192;
-constexpr int kHaloMax = 256;                   // TMA box height limit
-constexpr uint32_t kHaloBytes = kHaloMax * 128;  // one A stage (32 KB)
+constexpr int kBoxMax = 256;                     // TMA box height limit (rows per halo load)
 constexpr uint32_t kRowPitch = 144;              // epilogue staging row pitch (bank spread)
 constexpr uint32_t kEpiWarp = 32 * kRowPitch;
 constexpr int kMaxStatN = 512;
+constexpr int kMaxBStages = 8;
+constexpr size_t kSmemLimit = 232448;            // 227 KB opt-in per CTA
 
 struct HaloParams {
   int Mp;                  // GEMM rows = B * Hp * Wp padded positions
@@ -38,42 +39,51 @@ struct HaloParams {
   int ntaps;
   int off[9], wk[9];       // A row offset and weight tap index of each tap
   int Hp, Wp, H, W, B;
-  int lead, HR;            // halo rows before the tile (Wp + 1); rows per halo box
+  int lead, HR;            // halo rows before the tile group (Wp + 1); rows loaded per halo
+  int box_rows;            // rows per TMA box (HR = boxes * box_rows, box_rows % 8 == 0)
+  uint32_t a_stage;        // bytes per A stage (HR * 128)
+  int bstages;             // B ring depth
   const float *addend;     // nullable, fp32 output only
   void *out;               // [B][H][W][N] fp32 or bf16
   float *stats;            // nullable: one BN partial row per CTA [grid][N][2]
 };
 
-template <int BN, int ASTAGES, int BSTAGES, bool OUT16>
+// T consecutive 128-row M tiles share every B (weight) stage: the MMA warp applies one
+// (tap, channel block) weight tile to all T tiles before releasing it, so the weight
+// bytes per output row drop T-fold; their accumulators sit side by side in TMEM.
+template <int BN, int T, bool OUT16>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ HaloParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t B_BYTES = BN * 128;
+  constexpr int ASTAGES = 2;
+  constexpr int ACC = T * BN;  // TMEM columns per accumulator set
   uint8_t *sA = smem;
-  uint8_t *sB = sA + ASTAGES * kHaloBytes;
-  uint64_t *afull = reinterpret_cast<uint64_t *>(sB + BSTAGES * B_BYTES);
+  uint8_t *sB = sA + ASTAGES * P.a_stage;
+  uint64_t *afull = reinterpret_cast<uint64_t *>(sB + P.bstages * B_BYTES);
   uint64_t *aempty = afull + ASTAGES;
   uint64_t *bfull = aempty + ASTAGES;
-  uint64_t *bempty = bfull + BSTAGES;
-  uint64_t *tfull = bempty + BSTAGES;
+  uint64_t *bempty = bfull + kMaxBStages;
+  uint64_t *tfull = bempty + kMaxBStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  uint8_t *sepi = reinterpret_cast<uint8_t *>(afull) + 512;   // [4 warps][32 rows x 144 B]
+  uint8_t *sepi = reinterpret_cast<uint8_t *>(afull) + 512;       // [4 warps][32 rows x 144 B]
   float *sstat = reinterpret_cast<float *>(sepi + 4 * kEpiWarp);  // [4][N][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_nt = P.N / BN;
-  const int n_work = (int)cdiv(P.Mp, 128) * n_nt;
+  const int n_work = (int)cdiv(P.Mp, 128 * T) * n_nt;
   const int GHW = P.Hp * P.Wp;
+  const int BS = P.bstages;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ASTAGES; ++s) {
       tc::mbar_init(&afull[s], 1);
       tc::mbar_init(&aempty[s], 1);
     }
-    for (int s = 0; s < BSTAGES; ++s) {
+    for (int s = 0; s < BS; ++s) {
       tc::mbar_init(&bfull[s], 1);
       tc::mbar_init(&bempty[s], 1);
     }
@@ -85,7 +95,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
   }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * ACC);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -96,18 +106,19 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const int mt = w / n_nt, nt = w % n_nt;
-        const int r0 = mt * 128 - P.lead;  // may be negative: TMA zero-fills
+        const int mg = w / n_nt, nt = w % n_nt;
+        const int r0 = mg * 128 * T - P.lead;  // may be negative: TMA zero-fills
         for (int cb = 0; cb < P.CB; ++cb) {
           tc::mbar_wait(&aempty[as], aph ^ 1);
           tc::mbar_arrive_expect_tx(&afull[as], P.HR * 128);
-          tc::tma_load_2d(sA + as * kHaloBytes, &tmA, &afull[as], cb * 64, r0);
+          for (int r = 0; r < P.HR; r += P.box_rows)  // equal boxes, 1 KB-aligned (swizzle-consistent)
+            tc::tma_load_2d(sA + as * P.a_stage + r * 128, &tmA, &afull[as], cb * 64, r0 + r);
           if (++as == ASTAGES) { as = 0; aph ^= 1; }
           for (int t = 0; t < P.ntaps; ++t) {
             tc::mbar_wait(&bempty[bs], bph ^ 1);
             tc::mbar_arrive_expect_tx(&bfull[bs], B_BYTES);
             tc::tma_load_2d(sB + bs * B_BYTES, &tmB, &bfull[bs], P.wk[t] * P.Cred + cb * 64, nt * BN);
-            if (++bs == BSTAGES) { bs = 0; bph ^= 1; }
+            if (++bs == BS) { bs = 0; bph ^= 1; }
           }
         }
       }
@@ -122,21 +133,24 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int acc = it & 1;
         tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc::tc_fence_after();
-        const uint32_t dtm = tmem_base + acc * BN;
+        const uint32_t dtm = tmem_base + acc * ACC;
         for (int cb = 0; cb < P.CB; ++cb) {
           tc::mbar_wait(&afull[as], aph);
           tc::tc_fence_after();
-          const uint32_t abase = tc::smem_u32(sA + as * kHaloBytes) + P.lead * 128;
+          const uint32_t abase = tc::smem_u32(sA + as * P.a_stage) + P.lead * 128;
           for (int t = 0; t < P.ntaps; ++t) {
             tc::mbar_wait(&bfull[bs], bph);
             tc::tc_fence_after();
-            const uint64_t ad = tc::sw128_desc(abase + P.off[t] * 128, 16, 1024);
             const uint64_t bd = tc::sw128_desc(tc::smem_u32(sB + bs * B_BYTES), 16, 1024);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (cb > 0 || t > 0 || k > 0) ? 1u : 0u);
+            for (int tt = 0; tt < T; ++tt) {
+              const uint64_t ad = tc::sw128_desc(abase + (tt * 128 + P.off[t]) * 128, 16, 1024);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                tc::umma_bf16(dtm + tt * BN, ad + 2 * k, bd + 2 * k, idesc, (cb > 0 || t > 0 || k > 0) ? 1u : 0u);
+            }
             tc::umma_commit(&bempty[bs]);
-            if (++bs == BSTAGES) { bs = 0; bph ^= 1; }
+            if (++bs == BS) { bs = 0; bph ^= 1; }
           }
           tc::umma_commit(&aempty[as]);
           if (++as == ASTAGES) { as = 0; aph ^= 1; }
@@ -156,78 +170,81 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     constexpr int CW = 128 / ES;  // columns per 128-byte chunk
     int it = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
-      const int mt = w / n_nt, nt = w % n_nt;
+      const int mg = w / n_nt, nt = w % n_nt;
       const int acc = it & 1;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
-      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      const int m = mt * 128 + row;
-      const int b = m / GHW, r = m % GHW, hp = r / P.Wp, wp = r % P.Wp;
-      const bool valid = b < P.B && hp >= 1 && hp <= P.H && wp >= 1 && wp <= P.W;
-      const int64_t opix = valid ? ((int64_t)b * P.H + hp - 1) * P.W + wp - 1 : -1;
-      const float *arow = (valid && P.addend) ? P.addend + opix * P.N + nt * BN : nullptr;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += CW) {
-        float v[CW];
+      for (int tt = 0; tt < T; ++tt) {
+        const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC + tt * BN;
+        const int m = (mg * T + tt) * 128 + row;
+        const int b = m / GHW, r = m % GHW, hp = r / P.Wp, wp = r % P.Wp;
+        const bool valid = b < P.B && hp >= 1 && hp <= P.H && wp >= 1 && wp <= P.W;
+        const int64_t opix = valid ? ((int64_t)b * P.H + hp - 1) * P.W + wp - 1 : -1;
+        const float *arow = (valid && P.addend) ? P.addend + opix * P.N + nt * BN : nullptr;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += CW) {
+          float v[CW];
 #pragma unroll
-        for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
-        if (arow) {
+          for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
+          if (arow) {
 #pragma unroll
-          for (int jj = 0; jj < CW; jj += 4) {
-            const float4 a4 = *reinterpret_cast<const float4 *>(arow + c + jj);
-            v[jj] += a4.x; v[jj + 1] += a4.y; v[jj + 2] += a4.z; v[jj + 3] += a4.w;
-          }
-        }
-        // stage this lane's row (128 B) ...
-        uint8_t *rp = ebuf + lane * kRowPitch;
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          uint4 u;
-          if constexpr (OUT16) {
-            uint32_t wv[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 hb = __floats2bfloat162_rn(v[8 * ch + 2 * e], v[8 * ch + 2 * e + 1]);
-              wv[e] = *reinterpret_cast<uint32_t *>(&hb);
-              const float2 f = __bfloat1622float2(hb);  // statistics of the stored values (reading c24)
-              v[8 * ch + 2 * e] = f.x;
-              v[8 * ch + 2 * e + 1] = f.y;
+            for (int jj = 0; jj < CW; jj += 4) {
+              const float4 a4 = *reinterpret_cast<const float4 *>(arow + c + jj);
+              v[jj] += a4.x; v[jj + 1] += a4.y; v[jj + 2] += a4.z; v[jj + 3] += a4.w;
             }
-            u = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-          } else {
-            u = make_uint4(__float_as_uint(v[4 * ch]), __float_as_uint(v[4 * ch + 1]), __float_as_uint(v[4 * ch + 2]),
-                           __float_as_uint(v[4 * ch + 3]));
           }
-          *reinterpret_cast<uint4 *>(rp + ch * 16) = u;
-        }
-        __syncwarp();
-        // ... and write the warp's 32 rows out: 8 lanes per 128-byte pixel chunk
+          // stage this lane's row (128 B) ...
+          uint8_t *rp = ebuf + lane * kRowPitch;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int idx = k * 32 + lane, rr = idx >> 3, piece = idx & 7;
-          const int64_t op = __shfl_sync(0xffffffffu, opix, rr);
-          if (op >= 0) {
-            const uint4 u = *reinterpret_cast<const uint4 *>(ebuf + rr * kRowPitch + piece * 16);
-            char *dst = static_cast<char *>(P.out) + (op * P.N + nt * BN + c) * ES + piece * 16;
-            *reinterpret_cast<uint4 *>(dst) = u;
-          }
-        }
-        __syncwarp();
-        if (P.stats) {
+          for (int ch = 0; ch < 8; ++ch) {
+            uint4 u;
+            if constexpr (OUT16) {
+              uint32_t wv[4];
 #pragma unroll
-          for (int h = 0; h < CW; h += 16) {
-            float x[16], sq[16];
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-              x[jj] = valid ? v[h + jj] : 0.f;
-              sq[jj] = x[jj] * x[jj];
+              for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 hb = __floats2bfloat162_rn(v[8 * ch + 2 * e], v[8 * ch + 2 * e + 1]);
+                wv[e] = *reinterpret_cast<uint32_t *>(&hb);
+                const float2 f = __bfloat1622float2(hb);  // statistics of the stored values (reading c24)
+                v[8 * ch + 2 * e] = f.x;
+                v[8 * ch + 2 * e + 1] = f.y;
+              }
+              u = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            } else {
+              u = make_uint4(__float_as_uint(v[4 * ch]), __float_as_uint(v[4 * ch + 1]),
+                             __float_as_uint(v[4 * ch + 2]), __float_as_uint(v[4 * ch + 3]));
             }
-            tc::colsum16(x, lane);
-            tc::colsum16(sq, lane);
-            if (!(lane & 1)) {
-              const int col = nt * BN + c + h + (lane >> 1);
-              my_stat[2 * col] += x[0];
-              my_stat[2 * col + 1] += sq[0];
+            *reinterpret_cast<uint4 *>(rp + ch * 16) = u;
+          }
+          __syncwarp();
+          // ... and write the warp's 32 rows out: 8 lanes per 128-byte pixel chunk
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int idx = k * 32 + lane, rr = idx >> 3, piece = idx & 7;
+            const int64_t op = __shfl_sync(0xffffffffu, opix, rr);
+            if (op >= 0) {
+              const uint4 u = *reinterpret_cast<const uint4 *>(ebuf + rr * kRowPitch + piece * 16);
+              char *dst = static_cast<char *>(P.out) + (op * P.N + nt * BN + c) * ES + piece * 16;
+              *reinterpret_cast<uint4 *>(dst) = u;
+            }
+          }
+          __syncwarp();
+          if (P.stats) {
+#pragma unroll
+            for (int h = 0; h < CW; h += 16) {
+              float x[16], sq[16];
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) {
+                x[jj] = valid ? v[h + jj] : 0.f;
+                sq[jj] = x[jj] * x[jj];
+              }
+              tc::colsum16(x, lane);
+              tc::colsum16(sq, lane);
+              if (!(lane & 1)) {
+                const int col = nt * BN + c + h + (lane >> 1);
+                my_stat[2 * col] += x[0];
+                my_stat[2 * col + 1] += sq[0];
+              }
             }
           }
         }
@@ -246,33 +263,76 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   __syncthreads();
   if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem_base, 2 * BN);
+    tc::tmem_dealloc(tmem_base, 2 * ACC);
   }
 }
 
-constexpr int a_stages(int) { return 2; }
-constexpr int b_stages(int BN) { return BN == 256 ? 3 : (BN == 128 ? 6 : 10); }
-constexpr size_t halo_smem(int BN) {
-  return 1024 + (size_t)a_stages(BN) * kHaloBytes + (size_t)b_stages(BN) * BN * 128 + 512 + 4 * kEpiWarp +
-         (size_t)kMaxStatN * 32;
+size_t fixed_smem() { return 1024 + 512 + 4 * kEpiWarp + (size_t)kMaxStatN * 32; }
+// the halo of T tiles (128*T + 2*(W+3) rows) as equal TMA boxes of <= 256 rows, each a
+// multiple of 8 rows so every box starts 1 KB-aligned
+void halo_rows(int T, int W, int &box_rows, int &HR) {
+  const int need = 128 * T + 2 * (W + 3);
+  const int nbox = (int)cdiv(need, kBoxMax);
+  box_rows = (int)cdiv(cdiv(need, nbox), 8) * 8;
+  HR = nbox * box_rows;
+}
+uint32_t a_stage_bytes(int T, int W) {
+  int br, HR;
+  halo_rows(T, W, br, HR);
+  return (uint32_t)HR * 128;
 }
 
-template <int BN, bool OUT16>
+struct HaloPlan {
+  int BN, T, bstages;
+  bool ok;
+};
+// Tile group T (weight reuse) and N tile: the largest T whose A halos fit next to >= 3
+// weight stages while the work items still fill 3/4 of a wave (measured: the weight
+// bytes per output row, not load/epilogue overlap, bound these kernels); grids whose
+// zero border adds > 35% rows, or that fill under 3/4 of a wave, stay on the split-K
+// path of conv_tc.cu.
+HaloPlan halo_plan(int B, int H, int W, int Cred, int N) {
+  HaloPlan p{0, 0, 0, false};
+  if (Cred % 64 || N % 64) return p;
+  const int64_t Mp = (int64_t)B * (H + 2) * (W + 2);
+  if (Mp >= ((int64_t)1 << 31) || Mp * 100 > (int64_t)B * H * W * 135) return p;
+  for (int pass = 0; pass < 1; ++pass) {
+    const int64_t min_work = (kNumSMs * 3 + 3) / 4;
+    for (int bn : {256, 128, 64}) {
+      if (N % bn) continue;
+      for (int T : {4, 2, 1}) {
+        if (T * bn * 2 > 512) continue;  // two accumulator sets in TMEM
+        const size_t base = fixed_smem() + 2 * (size_t)a_stage_bytes(T, W);
+        if (base + 3 * (size_t)bn * 128 > kSmemLimit) continue;
+        const int64_t work = cdiv(Mp, 128 * T) * (N / bn);
+        if (work < min_work) continue;
+        p.BN = bn;
+        p.T = T;
+        p.bstages = (int)std::min<size_t>(kMaxBStages, (kSmemLimit - base) / ((size_t)bn * 128));
+        p.ok = true;
+        return p;
+      }
+    }
+  }
+  return p;
+}
+
+template <int BN, int T, bool OUT16>
 void launch(const CUtensorMap &ta, const CUtensorMap &tb, const HaloParams &P, cudaStream_t st) {
-  const int work = (int)cdiv(P.Mp, 128) * (P.N / BN);
-  conv_halo_kernel<BN, a_stages(BN), b_stages(BN), OUT16>
-      <<<std::min(work, kNumSMs), kThreads, halo_smem(BN), st>>>(ta, tb, P);
+  const int work = (int)cdiv(P.Mp, 128 * T) * (P.N / BN);
+  const size_t smem = fixed_smem() + 2 * (size_t)P.a_stage + (size_t)P.bstages * BN * 128;
+  conv_halo_kernel<BN, T, OUT16><<<std::min(work, kNumSMs), kThreads, smem, st>>>(ta, tb, P);
   PETRA_LAUNCH_CHECK();
 }
 
-int pick_bn(int N, int mtiles) {
-  int bn = 64;
-  for (int c : {256, 128, 64})
-    if (N % c == 0) {
-      bn = c;
-      if (mtiles * (N / c) >= kNumSMs) break;
-    }
-  return bn;
+template <bool OUT16>
+void dispatch(int BN, int T, const CUtensorMap &ta, const CUtensorMap &tb, const HaloParams &P, cudaStream_t st) {
+  if (BN == 64 && T == 4) launch<64, 4, OUT16>(ta, tb, P, st);
+  else if (BN == 64 && T == 2) launch<64, 2, OUT16>(ta, tb, P, st);
+  else if (BN == 64) launch<64, 1, OUT16>(ta, tb, P, st);
+  else if (BN == 128 && T == 2) launch<128, 2, OUT16>(ta, tb, P, st);
+  else if (BN == 128) launch<128, 1, OUT16>(ta, tb, P, st);
+  else launch<256, 1, OUT16>(ta, tb, P, st);
 }
 
 }  // namespace
@@ -280,37 +340,35 @@ int pick_bn(int N, int mtiles) {
 void conv_halo_prepare() {
   static std::once_flag once;
   std::call_once(once, [] {
-    auto set = [](const void *f, int BN) {
-      PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)halo_smem(BN)));
+    auto set = [](const void *f) {
+      PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
     };
-    set((const void *)conv_halo_kernel<64, a_stages(64), b_stages(64), false>, 64);
-    set((const void *)conv_halo_kernel<128, a_stages(128), b_stages(128), false>, 128);
-    set((const void *)conv_halo_kernel<256, a_stages(256), b_stages(256), false>, 256);
-    set((const void *)conv_halo_kernel<64, a_stages(64), b_stages(64), true>, 64);
-    set((const void *)conv_halo_kernel<128, a_stages(128), b_stages(128), true>, 128);
-    set((const void *)conv_halo_kernel<256, a_stages(256), b_stages(256), true>, 256);
+    set((const void *)conv_halo_kernel<64, 4, false>);
+    set((const void *)conv_halo_kernel<64, 2, false>);
+    set((const void *)conv_halo_kernel<64, 1, false>);
+    set((const void *)conv_halo_kernel<128, 2, false>);
+    set((const void *)conv_halo_kernel<128, 1, false>);
+    set((const void *)conv_halo_kernel<256, 1, false>);
+    set((const void *)conv_halo_kernel<64, 4, true>);
+    set((const void *)conv_halo_kernel<64, 2, true>);
+    set((const void *)conv_halo_kernel<64, 1, true>);
+    set((const void *)conv_halo_kernel<128, 2, true>);
+    set((const void *)conv_halo_kernel<128, 1, true>);
+    set((const void *)conv_halo_kernel<256, 1, true>);
   });
 }
 
-// a 3x3 stride-1 pass whose padded grid tiles fill at least ~3/4 of a wave of SMs
+// a 3x3 stride-1 pass whose padded grid fills at least ~3/4 of a wave of work items
 // (smaller grids keep the split-K path of conv_tc.cu)
-bool conv_halo_eligible(int B, int H, int W, int Cred, int N) {
-  if (Cred % 64 || N % 64) return false;
-  const int Wp = W + 2, Hp = H + 2;
-  if (128 + 2 * (Wp + 1) > kHaloMax) return false;
-  const int64_t Mp = (int64_t)B * Hp * Wp;
-  if (Mp >= ((int64_t)1 << 31)) return false;
-  const int mtiles = (int)cdiv(Mp, 128);
-  const int bn = pick_bn(N, mtiles);
-  return (int64_t)mtiles * (N / bn) * 4 >= (int64_t)kNumSMs * 3;
-}
+bool conv_halo_eligible(int B, int H, int W, int Cred, int N) { return halo_plan(B, H, W, Cred, N).ok; }
 
 // out[b][h][w][n] (= addend +) sum_{tap, c} a_pad[b][h+kh][w+kw][c] * wmat[n][wk(tap)*Cred + c]
 // a_pad: [B][H+2][W+2][Cred] bf16 with zero borders; wmat: [N][9*Cred] bf16
 // (forward: x and w; stride-1 dgrad: dz and the flipped/transposed wT, same tap order).
 int conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad, const __nv_bfloat16 *wmat,
                   const float *addend, void *out, bool out16, float *stats, cudaStream_t st) {
-  if (!conv_halo_eligible(B, H, W, Cred, N)) throw PetraError(PETRA_E_UNSUPPORTED, "conv_halo_run: geometry");
+  const HaloPlan pl = halo_plan(B, H, W, Cred, N);
+  if (!pl.ok) throw PetraError(PETRA_E_UNSUPPORTED, "conv_halo_run: geometry");
   if (out16 && addend) throw PetraError(PETRA_E_ARG, "conv_halo_run: addend needs an fp32 output");
   conv_halo_prepare();
   HaloParams P{};
@@ -329,28 +387,22 @@ int conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_p
     P.wk[t] = t;
   }
   P.lead = P.Wp + 1;
-  P.HR = 128 + 2 * P.lead;
+  halo_rows(pl.T, W, P.box_rows, P.HR);
+  P.a_stage = (uint32_t)P.HR * 128;
+  P.bstages = pl.bstages;
   P.addend = addend;
   P.out = out;
   P.stats = N <= kMaxStatN ? stats : nullptr;
-  const int mtiles = (int)cdiv(P.Mp, 128);
-  const int BN = pick_bn(N, mtiles);
   cuuint64_t adims[2] = {(cuuint64_t)Cred, (cuuint64_t)P.Mp};
   cuuint64_t ast[1] = {(cuuint64_t)Cred * 2};
-  cuuint32_t abox[2] = {64, (cuuint32_t)P.HR};
+  cuuint32_t abox[2] = {64, (cuuint32_t)P.box_rows};
   cuuint32_t es[2] = {1, 1};
   CUtensorMap ta = tma_map(a_pad, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, adims, ast, abox, es);
-  CUtensorMap tb = kmajor_map_bf16(wmat, N, 9 * Cred, BN);
-  if (out16) {
-    if (BN == 256) launch<256, true>(ta, tb, P, st);
-    else if (BN == 128) launch<128, true>(ta, tb, P, st);
-    else launch<64, true>(ta, tb, P, st);
-  } else {
-    if (BN == 256) launch<256, false>(ta, tb, P, st);
-    else if (BN == 128) launch<128, false>(ta, tb, P, st);
-    else launch<64, false>(ta, tb, P, st);
-  }
-  return P.stats ? std::min(mtiles * (N / BN), kNumSMs) : 0;
+  CUtensorMap tb = kmajor_map_bf16(wmat, N, 9 * Cred, pl.BN);
+  if (out16) dispatch<true>(pl.BN, pl.T, ta, tb, P, st);
+  else dispatch<false>(pl.BN, pl.T, ta, tb, P, st);
+  const int work = (int)cdiv(P.Mp, 128 * pl.T) * (N / pl.BN);
+  return P.stats ? std::min(work, kNumSMs) : 0;
 }
 
 }  // namespace petra

@@ -74,6 +74,9 @@ Stage::Stage(const petra_stage_desc &desc, uint64_t seed) : desc_(desc) {
 
 Stage::~Stage() {
   for (auto &kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
+  if (side_) cudaStreamDestroy(side_);
+  if (fork_) cudaEventDestroy(fork_);
+  if (join_) cudaEventDestroy(join_);
   if (lr_host_) cudaFreeHost(lr_host_);
 }
 
@@ -103,33 +106,36 @@ int64_t Stage::add_tensor(int unit, int part, int kind, int decay, std::vector<i
 
 void Stage::alloc_layer(Layer &L, bool inner) {
   int64_t n = L.g.M() * L.g.Co;
+  L.ctx = &ctx_;
   L.z16 = tc_ && (conv_tc_supported(L.g, 0) || stem_tc_supported(L.g));
-  L.z = dalloc(n * (L.z16 ? sizeof(__nv_bfloat16) : sizeof(float)));
-  L.dz = dalloc(n * sizeof(float));
-  L.mean = dalloc(L.g.Co * sizeof(float));
-  L.invstd = dalloc(L.g.Co * sizeof(float));
-  if (inner) {
-    L.a = dalloc(n * sizeof(float));
-    L.da = dalloc(n * sizeof(float));
+  for (int c = 0; c < 2; ++c) {
+    L.z_[c] = dalloc(n * (L.z16 ? sizeof(__nv_bfloat16) : sizeof(float)));
+    L.mean_[c] = dalloc(L.g.Co * sizeof(float));
+    L.invstd_[c] = dalloc(L.g.Co * sizeof(float));
+    if (inner) L.a_[c] = dalloc(n * sizeof(float));
   }
+  L.dz = dalloc(n * sizeof(float));
+  if (inner) L.da = dalloc(n * sizeof(float));
   if (tc_) {
     L.w_bf16 = dalloc((int64_t)L.g.Co * L.g.K() * sizeof(__nv_bfloat16));
     L.wt_bf16 = dalloc((int64_t)L.g.Co * L.g.K() * sizeof(__nv_bfloat16));
     // 3x3 stride-1 layers keep their bf16 operands zero-bordered for the halo kernel
-    // (opt-in, PETRA_HALO=1: measured no faster than the per-tap im2col kernel yet)
+    // (on by default; PETRA_HALO=0 keeps every layer on the per-tap im2col kernel)
     static const bool halo = [] {
       const char *e = getenv("PETRA_HALO");
-      return e && e[0] == '1';
+      return !(e && e[0] == '0');
     }();
     const bool s1k3 = halo && !L.is_stem && L.g.k == 3 && L.g.s == 1;
-    L.xpad = s1k3 && conv_tc_supported(L.g, 0);
-    L.dzpad = s1k3 && conv_tc_supported(L.g, 1);
+    L.xpad = s1k3 && conv_tc_supported(L.g, 0) && conv_halo_eligible(L.g.B, L.g.H, L.g.W, L.g.Ci, L.g.Co);
+    L.dzpad = s1k3 && conv_tc_supported(L.g, 1) && conv_halo_eligible(L.g.B, L.g.Ho, L.g.Wo, L.g.Co, L.g.Ci);
     const int64_t nxb = L.xpad ? (int64_t)L.g.B * (L.g.H + 2) * (L.g.W + 2) * L.g.Ci : L.g.Min() * L.g.Ci;
     const int64_t ndz = L.dzpad ? (int64_t)L.g.B * (L.g.Ho + 2) * (L.g.Wo + 2) * L.g.Co : n;
     L.dzb = dalloc(ndz * sizeof(__nv_bfloat16));
-    L.xb = dalloc(nxb * sizeof(__nv_bfloat16));
     if (L.dzpad) PETRA_CUDA(cudaMemset(L.dzb->p, 0, ndz * sizeof(__nv_bfloat16)));  // borders stay zero
-    if (L.xpad) PETRA_CUDA(cudaMemset(L.xb->p, 0, nxb * sizeof(__nv_bfloat16)));
+    for (int c = 0; c < 2; ++c) {
+      L.xb_[c] = dalloc(nxb * sizeof(__nv_bfloat16));
+      if (L.xpad) PETRA_CUDA(cudaMemset(L.xb_[c]->p, 0, nxb * sizeof(__nv_bfloat16)));
+    }
   }
 }
 
@@ -164,10 +170,11 @@ void Stage::build() {
         layers.push_back({&L, (int)ui, 0});
         int Ho = L.g.Ho, Wo = L.g.Wo;
         if (d.maxpool) {
-          u.pool_a = dalloc(L.g.M() * L.g.Co * sizeof(float));
+          u.ctx = &ctx_;
+          for (int c = 0; c < 2; ++c) u.pool_a_[c] = dalloc(L.g.M() * L.g.Co * sizeof(float));
           Ho = (Ho + 2 - 3) / 2 + 1;
           Wo = (Wo + 2 - 3) / 2 + 1;
-          u.pool_arg = dalloc((int64_t)B * Ho * Wo * L.g.Co);
+          for (int c = 0; c < 2; ++c) u.pool_arg_[c] = dalloc((int64_t)B * Ho * Wo * L.g.Co);
         }
         cur = Shape{B, Ho, Wo, d.layer[0].cout / 2};
         break;
@@ -258,12 +265,17 @@ void Stage::build() {
       for (int mode = 0; mode < 3; ++mode) max_ws = std::max(max_ws, conv_tc_workspace(p.L->g, mode));
     if (tc_) max_ws = std::max(max_ws, stem_tc_workspace(p.L->g));
   }
-  part_ = dalloc(std::max<size_t>(max_part, 16));
   size_t max_ctr = 1;
   for (auto &p : layers) max_ctr = std::max(max_ctr, bn_counter_count(p.L->g.Co));
-  counters_ = dalloc(max_ctr * sizeof(unsigned));
-  PETRA_CUDA(cudaMemset(counters_->p, 0, max_ctr * sizeof(unsigned)));
-  wgrad_ws_ = dalloc(std::max<size_t>(max_ws, 16));
+  for (int c = 0; c < 2; ++c) {
+    part_[c] = dalloc(std::max<size_t>(max_part, 16));
+    counters_[c] = dalloc(max_ctr * sizeof(unsigned));
+    PETRA_CUDA(cudaMemset(counters_[c]->p, 0, max_ctr * sizeof(unsigned)));
+    wgrad_ws_[c] = dalloc(std::max<size_t>(max_ws, 16));
+  }
+  PETRA_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  PETRA_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+  PETRA_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
   lr_dev_ = dalloc(sizeof(float));
   PETRA_CUDA(cudaMallocHost(&lr_host_, kLrRing * sizeof(float)));
   if (tc_) conv_tc_prepare();
@@ -434,21 +446,21 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
   const float *w = theta_->as<float>() + L.w_off;
   if (tc_ && stem_tc_supported(L.g)) {  // few input channels: gathered im2col, fp32 x read directly
     ProfScope ps("conv_fwd_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 4));
-    L.stats_rows = stem_fwd_tc(L.g, x, w, L.z->p, L.z16, reinterpret_cast<float *>(part_->p), st);
+    L.stats_rows() = stem_fwd_tc(L.g, x, w, L.z()->p, L.z16, reinterpret_cast<float *>(part()->p), st);
     return;
   }
   bool tc = tc_ && conv_tc_supported(L.g, 0);
   if (tc && !x_bf16_ready) {  // bf16 operand of a stream input (also read by the TC wgrad)
     ProfScope pc("cvt_bf16", st, 0.0, 6.0 * (double)L.g.Min() * L.g.Ci);
-    if (L.xpad) f32_to_bf16_padded(x, L.xb->as<__nv_bfloat16>(), L.g.B, L.g.H, L.g.W, L.g.Ci, st);
-    else f32_to_bf16(x, L.xb->as<__nv_bfloat16>(), L.g.Min() * L.g.Ci, st);
+    if (L.xpad) f32_to_bf16_padded(x, L.xb()->as<__nv_bfloat16>(), L.g.B, L.g.H, L.g.W, L.g.Ci, st);
+    else f32_to_bf16(x, L.xb()->as<__nv_bfloat16>(), L.g.Min() * L.g.Ci, st);
   }
   ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
-    L.stats_rows = conv_fwd_tc(L.g, L.xb->as<__nv_bfloat16>(), L.xpad, L.w_bf16->as<__nv_bfloat16>(), L.z->p, L.z16,
-                               wgrad_ws_->as<float>(), reinterpret_cast<float *>(part_->p), st);
+    L.stats_rows() = conv_fwd_tc(L.g, L.xb()->as<__nv_bfloat16>(), L.xpad, L.w_bf16->as<__nv_bfloat16>(), L.z()->p, L.z16,
+                               wgrad_ws()->as<float>(), reinterpret_cast<float *>(part()->p), st);
   } else {
-    conv_fwd_simt(L.g, x, w, L.z->as<float>(), st);
+    conv_fwd_simt(L.g, x, w, L.z()->as<float>(), st);
   }
 }
 
@@ -456,7 +468,7 @@ void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   float *dw = grad_->as<float>() + L.w_off;
   if (tc_ && stem_tc_supported(L.g)) {
     ProfScope ps("conv_wgrad_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2));
-    stem_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), x, dw, wgrad_ws_->as<float>(), st);
+    stem_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), x, dw, wgrad_ws()->as<float>(), st);
     return;
   }
   bool tc = tc_ && conv_tc_supported(L.g, 2);
@@ -464,10 +476,10 @@ void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   if (tc) {
     // L.xb holds bf16(x) from the conv_fwd of this tick (forward or recomputation);
     // L.dzb was written in bf16 by bn_bwd_dz
-    conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.xb->as<__nv_bfloat16>(), L.xpad, dw,
-                  wgrad_ws_->as<float>(), st);
+    conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.xb()->as<__nv_bfloat16>(), L.xpad, dw,
+                  wgrad_ws()->as<float>(), st);
   } else {
-    conv_wgrad_simt(L.g, L.dz->as<float>(), x, dw, wgrad_ws_->as<float>(), st);
+    conv_wgrad_simt(L.g, L.dz->as<float>(), x, dw, wgrad_ws()->as<float>(), st);
   }
 }
 
@@ -476,7 +488,7 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
   ProfScope ps(tc ? "conv_dgrad_tc" : "conv_dgrad_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
   if (tc) {
     conv_dgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.wt_bf16->as<__nv_bfloat16>(), addend, out,
-                  wgrad_ws_->as<float>(), st);
+                  wgrad_ws()->as<float>(), st);
   } else {
     conv_dgrad_simt(L.g, L.dz->as<float>(), theta_->as<float>() + L.w_off, addend, out, st);
   }
@@ -484,24 +496,24 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
 
 void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
   float *b = bufs_->as<float>();
-  if (L.stats_rows > 0) {  // sums already produced by the tensor-core conv epilogue
-    ProfScope ps("bn_stats_merge", st, 0.0, 8.0 * L.stats_rows * L.g.Co);
-    bn_stats_from_partials(reinterpret_cast<const float *>(part_->p), L.stats_rows, L.g.Co, L.g.M(), desc_.bn_eps,
-                           L.mean->as<float>(), L.invstd->as<float>(), running ? b + L.rm_off : nullptr,
+  if (L.stats_rows() > 0) {  // sums already produced by the tensor-core conv epilogue
+    ProfScope ps("bn_stats_merge", st, 0.0, 8.0 * L.stats_rows() * L.g.Co);
+    bn_stats_from_partials(reinterpret_cast<const float *>(part()->p), L.stats_rows(), L.g.Co, L.g.M(), desc_.bn_eps,
+                           L.mean()->as<float>(), L.invstd()->as<float>(), running ? b + L.rm_off : nullptr,
                            running ? b + L.rv_off : nullptr, desc_.bn_momentum, st);
-    L.stats_rows = 0;
+    L.stats_rows() = 0;
     return;
   }
   ProfScope ps("bn_stats", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co);
   if (L.z16)
-    bn_stats<__nv_bfloat16>(L.z->as<__nv_bfloat16>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean->as<float>(),
-                            L.invstd->as<float>(), running ? b + L.rm_off : nullptr,
-                            running ? b + L.rv_off : nullptr, desc_.bn_momentum, part_->as<double>(),
-                            counters_->as<unsigned>(), st);
+    bn_stats<__nv_bfloat16>(L.z()->as<__nv_bfloat16>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean()->as<float>(),
+                            L.invstd()->as<float>(), running ? b + L.rm_off : nullptr,
+                            running ? b + L.rv_off : nullptr, desc_.bn_momentum, part()->as<double>(),
+                            counters()->as<unsigned>(), st);
   else
-    bn_stats<float>(L.z->as<float>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean->as<float>(), L.invstd->as<float>(),
+    bn_stats<float>(L.z()->as<float>(), L.g.M(), L.g.Co, desc_.bn_eps, L.mean()->as<float>(), L.invstd()->as<float>(),
                     running ? b + L.rm_off : nullptr, running ? b + L.rv_off : nullptr, desc_.bn_momentum,
-                    part_->as<double>(), counters_->as<unsigned>(), st);
+                    part()->as<double>(), counters()->as<unsigned>(), st);
 }
 
 // forward of a conv-BN-ReLU chain on x; inner activations into L.a; the last
@@ -519,10 +531,10 @@ void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running
       ready = tc_ && conv_tc_supported(N.g, 0);
       // the fp32 copy only feeds SIMT passes of the next layer (forward or wgrad)
       const bool need32 = !ready || !conv_tc_supported(N.g, 2);
-      apply_bn(L.g.M(), L.g.Co, L.z->p, L.z16, L.g.Co, 0, L.mean->as<float>(), L.invstd->as<float>(),
-               th + L.g_off, th + L.b_off, 1, 1.f, nullptr, need32 ? L.a->as<float>() : nullptr,
-               ready ? N.xb->as<__nv_bfloat16>() : nullptr, st, N.xpad ? N.g.H : 0, N.g.W);
-      x = L.a->as<float>();
+      apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(), L.invstd()->as<float>(),
+               th + L.g_off, th + L.b_off, 1, 1.f, nullptr, need32 ? L.a()->as<float>() : nullptr,
+               ready ? N.xb()->as<__nv_bfloat16>() : nullptr, st, N.xpad ? N.g.H : 0, N.g.W);
+      x = L.a()->as<float>();
     }
   }
 }
@@ -538,14 +550,14 @@ void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, cons
   {
   ProfScope ps("bn_bwd_reduce", st, 0.0, n * ((L.z16 ? 2.0 : 4.0) + 4.0 + (dst_out ? 8.0 : 0.0)));
   if (L.z16)
-    bn_bwd_reduce<__nv_bfloat16>(L.z->as<__nv_bfloat16>(), L.g.M(), L.g.Co, L.mean->as<float>(),
-                                 L.invstd->as<float>(), th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs,
-                                 dst_in, dst_out, nullptr, gr + L.g_off, gr + L.b_off, part_->as<double>(),
-                                 counters_->as<unsigned>(), st);
+    bn_bwd_reduce<__nv_bfloat16>(L.z()->as<__nv_bfloat16>(), L.g.M(), L.g.Co, L.mean()->as<float>(),
+                                 L.invstd()->as<float>(), th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs,
+                                 dst_in, dst_out, nullptr, gr + L.g_off, gr + L.b_off, part()->as<double>(),
+                                 counters()->as<unsigned>(), st);
   else
-    bn_bwd_reduce<float>(L.z->as<float>(), L.g.M(), L.g.Co, L.mean->as<float>(), L.invstd->as<float>(),
+    bn_bwd_reduce<float>(L.z()->as<float>(), L.g.M(), L.g.Co, L.mean()->as<float>(), L.invstd()->as<float>(),
                          th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, dst_in, dst_out, nullptr,
-                         gr + L.g_off, gr + L.b_off, part_->as<double>(), counters_->as<unsigned>(), st);
+                         gr + L.g_off, gr + L.b_off, part()->as<double>(), counters()->as<unsigned>(), st);
   }
   // dz in bf16 for tensor-core dgrad / wgrad, in fp32 only if a SIMT pass consumes it
   // (the stem has no dgrad: its input is data)
@@ -555,11 +567,11 @@ void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, cons
   __nv_bfloat16 *dz16 = (tc_d || tc_w) ? L.dzb->as<__nv_bfloat16>() : nullptr;
   ProfScope ps("bn_bwd_dz", st, 0.0, n * ((L.z16 ? 2.0 : 4.0) + 4.0 + (dz32 ? 4.0 : 0.0) + (dz16 ? 2.0 : 0.0)));
   if (L.z16)
-    bn_bwd_dz<__nv_bfloat16>(L.g.M(), L.g.Co, L.z->as<__nv_bfloat16>(), L.mean->as<float>(), L.invstd->as<float>(),
+    bn_bwd_dz<__nv_bfloat16>(L.g.M(), L.g.Co, L.z()->as<__nv_bfloat16>(), L.mean()->as<float>(), L.invstd()->as<float>(),
                              th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off,
                              dz32, dz16, L.dzpad ? L.g.Ho : 0, L.g.Wo, st);
   else
-    bn_bwd_dz<float>(L.g.M(), L.g.Co, L.z->as<float>(), L.mean->as<float>(), L.invstd->as<float>(), th + L.g_off,
+    bn_bwd_dz<float>(L.g.M(), L.g.Co, L.z()->as<float>(), L.mean()->as<float>(), L.invstd()->as<float>(), th + L.g_off,
                      th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, gr + L.g_off, gr + L.b_off, dz32, dz16,
                      L.dzpad ? L.g.Ho : 0, L.g.Wo, st);
 }
@@ -572,7 +584,7 @@ void Stage::branch_backward(std::vector<Layer> &phi, const float *x, const float
   layer_bwd(phi[n - 1], dy, nullptr, 0, dst_in, dst_out, st);
   for (int l = n - 1; l >= 0; --l) {
     Layer &L = phi[l];
-    const float *xl = l == 0 ? x : phi[l - 1].a->as<float>();
+    const float *xl = l == 0 ? x : phi[l - 1].a()->as<float>();
     conv_wgrad(L, xl, st);
     if (l > 0) {
       conv_dgrad(L, nullptr, phi[l - 1].da->as<float>(), st);
@@ -593,8 +605,8 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       // x[dst] += Phi(x[src])  (north_star y1 = x1 + F(x2), y2 = x2 + G(y1))
       branch_forward(u.phi, cur[u.src()], keep, st);
       Layer &L = u.phi.back();
-      apply_bn(L.g.M(), L.g.Co, L.z->p, L.z16, L.g.Co, 0, L.mean->as<float>(),
-                             L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, cur[u.dst()], out[u.dst()],
+      apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(),
+                             L.invstd()->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, cur[u.dst()], out[u.dst()],
                              nullptr, st);
       break;
     }
@@ -609,11 +621,11 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       Layer &L = u.phi.back();
       int64_t M = L.g.M();
       int C = L.g.Co;
-      apply_bn(M, C, u.pa.z->p, u.pa.z16, C, 0, u.pa.mean->as<float>(), u.pa.invstd->as<float>(),
+      apply_bn(M, C, u.pa.z()->p, u.pa.z16, C, 0, u.pa.mean()->as<float>(), u.pa.invstd()->as<float>(),
                              th + u.pa.g_off, th + u.pa.b_off, 0, 1.f, nullptr, out[u.dst()], nullptr, st);
-      apply_bn(M, C, L.z->p, L.z16, C, 0, L.mean->as<float>(), L.invstd->as<float>(),
+      apply_bn(M, C, L.z()->p, L.z16, C, 0, L.mean()->as<float>(), L.invstd()->as<float>(),
                              th + L.g_off, th + L.b_off, 1, 1.f, out[u.dst()], out[u.dst()], nullptr, st);
-      apply_bn(M, C, u.pb.z->p, u.pb.z16, C, 0, u.pb.mean->as<float>(), u.pb.invstd->as<float>(),
+      apply_bn(M, C, u.pb.z()->p, u.pb.z16, C, 0, u.pb.mean()->as<float>(), u.pb.invstd()->as<float>(),
                              th + u.pb.g_off, th + u.pb.b_off, 0, 1.f, nullptr, out[u.src()], nullptr, st);
       break;
     }
@@ -623,16 +635,16 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       layer_stats(L, keep, st);
       int Ch = L.g.Co / 2;
       if (u.d.maxpool) {
-        apply_bn(L.g.M(), L.g.Co, L.z->p, L.z16, L.g.Co, 0, L.mean->as<float>(),
-                               L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
-                               u.pool_a->as<float>(), nullptr, st);
+        apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(),
+                               L.invstd()->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
+                               u.pool_a()->as<float>(), nullptr, st);
         ProfScope ps("maxpool", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co * 1.25);
-        maxpool_fwd(u.pool_a->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, out[0], out[1],
-                    u.pool_arg->as<uint8_t>(), st);
+        maxpool_fwd(u.pool_a()->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, out[0], out[1],
+                    u.pool_arg()->as<uint8_t>(), st);
       } else {
         for (int h = 0; h < 2; ++h)
-          apply_bn(L.g.M(), Ch, L.z->p, L.z16, L.g.Co, h * Ch, L.mean->as<float>(),
-                                 L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr, out[h],
+          apply_bn(L.g.M(), Ch, L.z()->p, L.z16, L.g.Co, h * Ch, L.mean()->as<float>(),
+                                 L.invstd()->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr, out[h],
                                  nullptr, st);
       }
       break;
@@ -687,17 +699,17 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
         layer_stats(L, true, st);
         if (u.d.maxpool) {
           // recompute the pre-pool activation and argmax (outputs go to scratch)
-          apply_bn(L.g.M(), L.g.Co, L.z->p, L.z16, L.g.Co, 0, L.mean->as<float>(),
-                                 L.invstd->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
-                                 u.pool_a->as<float>(), nullptr, st);
-          maxpool_fwd(u.pool_a->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, L.dz->as<float>(),
-                      L.dz->as<float>() + u.out.numel(), u.pool_arg->as<uint8_t>(), st);
+          apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(),
+                                 L.invstd()->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
+                                 u.pool_a()->as<float>(), nullptr, st);
+          maxpool_fwd(u.pool_a()->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, L.dz->as<float>(),
+                      L.dz->as<float>() + u.out.numel(), u.pool_arg()->as<uint8_t>(), st);
         }
       }
       if (u.d.maxpool) {
-        maxpool_bwd(cur_d[0], cur_d[1], u.pool_arg->as<uint8_t>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H,
-                    u.out.W, u.pool_a->as<float>(), st);
-        layer_bwd(L, u.pool_a->as<float>(), nullptr, 0, nullptr, nullptr, st);
+        maxpool_bwd(cur_d[0], cur_d[1], u.pool_arg()->as<uint8_t>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H,
+                    u.out.W, u.pool_a()->as<float>(), st);
+        layer_bwd(L, u.pool_a()->as<float>(), nullptr, 0, nullptr, nullptr, st);
       } else {
         layer_bwd(L, cur_d[0], cur_d[1], L.g.Co / 2, nullptr, nullptr, st);
       }
@@ -896,6 +908,7 @@ void Stage::forward(uint64_t mb, const float *x1, const float *x2, float *o1, fl
   check_fwd(mb, x1, x2);
   if (!o1 || !o2) throw PetraError(PETRA_E_ARG, "NULL output pointer");
   std::vector<int> push = reserve_push(mb);
+  ctx_ = 0;
   enqueue_forward(x1, x2, o1, o2, push, false, nullptr, st);
   have_last_fwd_ = true;
   last_fwd_mb_ = mb;
@@ -910,7 +923,9 @@ void Stage::backward(uint64_t mb, const float *xt1, const float *xt2, const floa
   check_lr(lr);
   std::vector<int> pop = take_pop(mb);
   upload_lr(lr, st);
+  ctx_ = 1;
   enqueue_backward(xt1, xt2, d1, d2, oxt1, oxt2, od1, od2, pop, st);
+  ctx_ = 0;
   enqueue_update(st);
   ++version_;
   ++n_bwd_;
@@ -925,6 +940,7 @@ void Stage::tail(uint64_t mb, const float *x1, const float *x2, const int32_t *l
   check_lr(lr);
   std::vector<int> push = reserve_push(mb), pop = take_pop(mb);
   upload_lr(lr, st);
+  ctx_ = 0;
   enqueue_tail(x1, x2, labels, oxt1, oxt2, od1, od2, loss, push, pop, st);
   enqueue_update(st);
   have_last_fwd_ = true;
@@ -954,10 +970,27 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
   if (bwd) upload_lr(lr, st);
   auto enqueue = [&](cudaStream_t s) {
     if (is_last_) {
+      ctx_ = 0;
       enqueue_tail(a.x1, a.x2, a.labels, a.oxt[0], a.oxt[1], a.od[0], a.od[1], a.loss, push, pop, s);
+    } else if (fwd && bwd) {
+      // forward (theta^t, context 0) and backward (context 1) of different micro-batches
+      // are independent until the update: run them on two streams, join, then update
+      PETRA_CUDA(cudaEventRecord(fork_, s));
+      PETRA_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+      ctx_ = 0;
+      enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
+      ctx_ = 1;
+      enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, side_);
+      PETRA_CUDA(cudaEventRecord(join_, side_));
+      PETRA_CUDA(cudaStreamWaitEvent(s, join_, 0));
+      ctx_ = 0;
+    } else if (fwd) {
+      ctx_ = 0;
+      enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
     } else {
-      if (fwd) enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
-      if (bwd) enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, s);
+      ctx_ = 1;
+      enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, s);
+      ctx_ = 0;
     }
     if (bwd) enqueue_update(s);
   };

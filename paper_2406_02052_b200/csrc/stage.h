@@ -38,10 +38,20 @@ struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
   bool relu = true;
   int64_t w_off = 0, g_off = 0, b_off = 0;   // into theta / grad / v
   int64_t rm_off = 0, rv_off = 0;            // into buffers (running stats)
-  DevPtr z, a, dz, da, mean, invstd;         // workspace, kept from forward to backward in a tick
-  DevPtr zb, ab, dzb, xb;                    // bf16 workspace (tensor-core path)
+  // Per-context workspace: context 0 = forward, 1 = backward (recompute + VJP).  The
+  // forward and the backward of a pipeline tick run concurrently on two streams, so
+  // everything either writes has one copy per context; *ctx selects the live one.
+  DevPtr z_[2], a_[2], mean_[2], invstd_[2], xb_[2];
+  int stats_rows_[2] = {0, 0};               // > 0: BN partials written by the conv epilogue
+  const int *ctx = nullptr;
+  DevPtr &z() { return z_[*ctx]; }
+  DevPtr &a() { return a_[*ctx]; }
+  DevPtr &mean() { return mean_[*ctx]; }
+  DevPtr &invstd() { return invstd_[*ctx]; }
+  DevPtr &xb() { return xb_[*ctx]; }
+  int &stats_rows() { return stats_rows_[*ctx]; }
+  DevPtr dz, da, dzb;                        // backward-only workspace
   DevPtr w_bf16, wt_bf16;                    // bf16 shadows of the live weights
-  int stats_rows = 0;                        // > 0: BN partials written by the conv epilogue
   bool z16 = false;                          // z stored in bf16 (tensor-core conv output, reading c24)
   bool is_stem = false;                      // no dgrad: the input is data
   bool xpad = false, dzpad = false;          // xb / dzb zero-bordered [B][H+2][W+2][C] (3x3 stride-1 layers)
@@ -62,7 +72,10 @@ struct Unit {
   Layer pa, pb;                        // DS projections
   int64_t fc_w = 0, fc_b = 0;          // TAIL offsets
   Fifo fifo;
-  DevPtr pool_arg, pool_a;             // STEM max-pool argmax / pre-pool activation
+  DevPtr pool_arg_[2], pool_a_[2];     // STEM max-pool argmax / pre-pool activation (per context)
+  const int *ctx = nullptr;
+  DevPtr &pool_arg() { return pool_arg_[*ctx]; }
+  DevPtr &pool_a() { return pool_a_[*ctx]; }
   // forward / backward output targets (planned at creation): buffer per half
   DevPtr fout[2], bx[2], bd[2];
   int dst() const { return d.dst_half; }
@@ -129,7 +142,13 @@ class Stage {
   std::vector<SgdSeg> segs_;
   DevPtr segs_dev_;
   int64_t max_seg_ = 0;
-  DevPtr part_, wgrad_ws_, counters_;
+  DevPtr part_[2], wgrad_ws_[2], counters_[2];  // per context (see Layer)
+  int ctx_ = 0;                                 // workspace context being enqueued
+  DevPtr &part() { return part_[ctx_]; }
+  DevPtr &wgrad_ws() { return wgrad_ws_[ctx_]; }
+  DevPtr &counters() { return counters_[ctx_]; }
+  cudaStream_t side_ = nullptr;                 // the backward's stream (fork / join per tick)
+  cudaEvent_t fork_ = nullptr, join_ = nullptr;
   DevPtr nonfinite_;
   // tail workspace
   DevPtr feat_, logits_, dlogits_, lossrow_, dfeat_, tail_d_[2];
