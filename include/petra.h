@@ -101,7 +101,9 @@ typedef struct {
   float bn_momentum;               /* 0.1 (reading c9)                                         */
   float bn_eps;                    /* 1e-5 (reading c9)                                        */
   int32_t nesterov;                /* 1                                         */
-  int32_t accumulation_k;          /* k >= 1; only k = 1 is implemented     */
+  int32_t accumulation_k;          /* k >= 1 (Alg. 1 lines 19-23): Delta_j +=
+                                      Delta_mb / k every backward; Nesterov update with Delta_j and
+                                      reset when t mod k == 0 (t counts backwards from 1)           */
   int32_t fifo_capacity;           /* non-reversible input FIFO depth; >= 2(J-j)+1 (Table 1)   */
 } petra_stage_desc;
 
@@ -257,7 +259,8 @@ petra_status petra_pipeline_stage_ms(petra_pipeline *p, float *ms, int32_t n, in
  * work so the multi-rank routing can be tested on CPU (gloo) and compared
  * bit-exactly with the oracle's tick engine.  stage_rank as in
  * petra_pipeline_desc; nonrev[j-1] = number of non-reversible units of stage j
- * (FIFO accounting).  petra_schedule_tick must be called for t = 0, 1, 2, ...;
+ * (FIFO accounting); accum_k[j-1] = stage j's accumulation factor k (its
+ * param_version advances on every k-th backward, Alg. 1 lines 19-23).  petra_schedule_tick must be called for t = 0, 1, 2, ...;
  * it fills report (all J stages) and the messages THIS rank exchanges after the
  * tick: kind 0 = forward (x1, x2, labels), 1 = backward (x~1, x~2, d1, d2). */
 typedef struct petra_schedule petra_schedule;
@@ -270,7 +273,8 @@ typedef struct {
   petra_sched_msg m[8];
 } petra_sched_msgs;
 petra_status petra_schedule_create(int32_t n_stages, const int32_t *stage_rank, const int32_t *nonrev,
-                                   int32_t rank, petra_schedule **out);
+                                   const int32_t *accum_k /* nullable: all 1 */, int32_t rank,
+                                   petra_schedule **out);
 petra_status petra_schedule_tick(petra_schedule *s, int64_t t, int32_t inject, petra_tick_report *report,
                                  petra_sched_msgs *msgs);
 petra_status petra_schedule_destroy(petra_schedule *s);

@@ -111,7 +111,7 @@ SIGS = {
     "petra_pipeline_comm": (C.c_int, [P, I64, C.POINTER(PetraCommPlan)]),
     "petra_pipeline_timing": (C.c_int, [P, I32]),
     "petra_pipeline_stage_ms": (C.c_int, [P, C.POINTER(C.c_float), I32, C.POINTER(I32)]),
-    "petra_schedule_create": (C.c_int, [I32, C.POINTER(I32), C.POINTER(I32), I32, C.POINTER(P)]),
+    "petra_schedule_create": (C.c_int, [I32, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32), I32, C.POINTER(P)]),
     "petra_schedule_tick": (C.c_int, [P, I64, I32, C.POINTER(PetraTickReport), C.POINTER(PetraSchedMsgs)]),
     "petra_schedule_destroy": (C.c_int, [P]),
     "petra_conv_run": (C.c_int, [I32, I32, C.POINTER(PetraConvGeom), VP, VP, VP, VP]),

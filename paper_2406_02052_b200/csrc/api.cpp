@@ -219,13 +219,14 @@ petra_status petra_pipeline_stage_ms(petra_pipeline *p, float *ms, int32_t n, in
   });
 }
 
-petra_status petra_schedule_create(int32_t n, const int32_t *stage_rank, const int32_t *nonrev, int32_t rank,
-                                   petra_schedule **out) {
+petra_status petra_schedule_create(int32_t n, const int32_t *stage_rank, const int32_t *nonrev,
+                                   const int32_t *accum_k, int32_t rank, petra_schedule **out) {
   if (!stage_rank || !nonrev || !out || n < 1) return fail(PETRA_E_ARG, "bad schedule arguments");
   return guard([&] {
     auto *h = new petra_schedule;
     h->s.reset(new petra::Schedule(n, std::vector<int>(stage_rank, stage_rank + n),
-                                   std::vector<int>(nonrev, nonrev + n), rank));
+                                   std::vector<int>(nonrev, nonrev + n), rank,
+                                   accum_k ? std::vector<int>(accum_k, accum_k + n) : std::vector<int>()));
     *out = h;
   });
 }

@@ -15,8 +15,10 @@ namespace petra {
 namespace {
 
 __global__ void sgd_kernel(const SgdSeg *__restrict__ segs, float *__restrict__ theta, float *__restrict__ v,
-                           const float *__restrict__ grad, const float *__restrict__ lr_dev, float mom, float wd,
-                           int nesterov, int shadow_only) {
+                           const float *__restrict__ grad, float *__restrict__ acc, float inv_k, int mode,
+                           const float *__restrict__ lr_dev, float mom, float wd, int nesterov, int shadow_only) {
+  // mode (Alg. 1 lines 19-22):  SGD_PLAIN   k = 1, update with Delta;
+  // SGD_ACCUMULATE  acc += Delta/k, no update;  SGD_ACC_UPDATE  update with acc + Delta/k, acc = 0
   const SgdSeg sg = segs[blockIdx.y];
   if (shadow_only && !sg.w_bf16) return;
   const float lam = sg.decay ? wd : 0.f;
@@ -24,8 +26,17 @@ __global__ void sgd_kernel(const SgdSeg *__restrict__ segs, float *__restrict__ 
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sg.count; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t o = sg.offset + i;
     float th = theta[o];
+    if (mode == SGD_ACCUMULATE) {
+      acc[o] += grad[o] * inv_k;
+      continue;
+    }
     if (!shadow_only) {
-      float g = fmaf(lam, th, grad[o]);
+      float d = grad[o];
+      if (mode == SGD_ACC_UPDATE) {
+        d = fmaf(d, inv_k, acc[o]);
+        acc[o] = 0.f;
+      }
+      float g = fmaf(lam, th, d);
       float vv = fmaf(mom, v[o], g);
       v[o] = vv;
       th -= lr * (nesterov ? fmaf(mom, vv, g) : vv);
@@ -312,9 +323,11 @@ inline unsigned ew_grid(int64_t n) {
 }  // namespace
 
 void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *theta, float *v, const float *grad,
-                const float *lr_dev, float mom, float wd, int nesterov, cudaStream_t st, bool shadow_only) {
+                float *acc, int k, int mode, const float *lr_dev, float mom, float wd, int nesterov, cudaStream_t st,
+                bool shadow_only) {
   dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(max_count, 256), 2 * kNumSMs)), nseg);
-  sgd_kernel<<<grid, 256, 0, st>>>(segs_dev, theta, v, grad, lr_dev, mom, wd, nesterov, shadow_only ? 1 : 0);
+  sgd_kernel<<<grid, 256, 0, st>>>(segs_dev, theta, v, grad, acc, 1.f / (float)k, mode, lr_dev, mom, wd, nesterov,
+                                           shadow_only ? 1 : 0);
   PETRA_LAUNCH_CHECK();
 }
 

@@ -19,10 +19,17 @@ static std::vector<int> nonrev_counts(const petra_pipeline_desc &d) {
   return v;
 }
 
+static std::vector<int> accum_ks(const petra_pipeline_desc &d) {
+  std::vector<int> k(d.n_stages, 1);
+  for (int j = 0; j < d.n_stages; ++j) k[j] = d.stages[j].accumulation_k;
+  return k;
+}
+
 Pipeline::Pipeline(const petra_pipeline_desc &d)
     : J_(d.n_stages),
       rank_(d.rank),
-      sched_(d.n_stages, std::vector<int>(d.stage_rank, d.stage_rank + d.n_stages), nonrev_counts(d), d.rank) {
+      sched_(d.n_stages, std::vector<int>(d.stage_rank, d.stage_rank + d.n_stages), nonrev_counts(d), d.rank,
+             accum_ks(d)) {
   if (J_ < 1 || J_ > PETRA_MAX_STAGES) throw PetraError(PETRA_E_ARG, "n_stages out of range");
   stages_.resize(J_ + 2);
   fwd_.resize(J_ + 2);

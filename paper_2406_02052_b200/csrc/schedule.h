@@ -31,10 +31,15 @@ class Schedule {
     int64_t mb;
   };
 
-  Schedule(int J, std::vector<int> rank_of, std::vector<int> nonrev, int rank)
-      : J_(J), rank_of_(std::move(rank_of)), nonrev_(std::move(nonrev)), rank_(rank) {
-    if (J < 1 || (int)rank_of_.size() != J || (int)nonrev_.size() != J)
+  // accum_k[j-1] = accumulation factor k of stage j (Alg. 1 lines 19-23): the
+  // parameter version advances on every k-th backward (t mod k == 0, t from 1)
+  Schedule(int J, std::vector<int> rank_of, std::vector<int> nonrev, int rank, std::vector<int> accum_k = {})
+      : J_(J), rank_of_(std::move(rank_of)), nonrev_(std::move(nonrev)), k_(std::move(accum_k)), rank_(rank) {
+    if (k_.empty()) k_.assign(J > 0 ? J : 0, 1);
+    if (J < 1 || (int)rank_of_.size() != J || (int)nonrev_.size() != J || (int)k_.size() != J)
       throw PetraError(PETRA_E_ARG, "schedule: bad stage count");
+    for (int k : k_)
+      if (k < 1) throw PetraError(PETRA_E_ARG, "schedule: accumulation k must be >= 1");
     for (int j = 1; j < J; ++j)
       if (rank_of_[j] < rank_of_[j - 1]) throw PetraError(PETRA_E_ARG, "stage_rank must be non-decreasing");
     j0_ = J + 1;
@@ -47,6 +52,7 @@ class Schedule {
     fwd_.assign(J + 2, {});
     bwd_.assign(J + 2, {});
     version_.assign(J + 2, 0);
+    nbwd_.assign(J + 2, 0);
     fifo_.assign(J + 2, 0);
   }
 
@@ -83,7 +89,7 @@ class Schedule {
       if (fin >= 0) fifo_[j] += nonrev_[j - 1];
       if (bin >= 0) {
         fifo_[j] -= nonrev_[j - 1];
-        version_[j] += 1;
+        if (++nbwd_[j] % k_[j - 1] == 0) version_[j] += 1;
       }
     }
     if (fifo_after) fifo_after->assign(fifo_.begin(), fifo_.end());
@@ -108,11 +114,11 @@ class Schedule {
 
  private:
   int J_;
-  std::vector<int> rank_of_, nonrev_;
+  std::vector<int> rank_of_, nonrev_, k_;
   int rank_;
   int j0_, j1_;
   std::vector<std::array<Box, 2>> fwd_, bwd_;
-  std::vector<int64_t> version_, fifo_;
+  std::vector<int64_t> version_, fifo_, nbwd_;
   int64_t n_inject_ = 0, last_t_ = -1;
 };
 

@@ -59,8 +59,7 @@ Stage::Stage(const petra_stage_desc &desc, uint64_t seed) : desc_(desc) {
     throw PetraError(PETRA_E_ARG, "non-positive stage input shape");
   if (desc.precision != PETRA_FP32 && desc.precision != PETRA_BF16_TC)
     throw PetraError(PETRA_E_ARG, "unknown precision");
-  if (desc.accumulation_k != 1)
-    throw PetraError(PETRA_E_UNSUPPORTED, "accumulation_k > 1 is not implemented (k = 1 hot path)");
+  if (desc.accumulation_k < 1) throw PetraError(PETRA_E_ARG, "accumulation_k must be >= 1");
   if (!(desc.momentum >= 0.f) || !(desc.weight_decay >= 0.f) || !(desc.bn_eps > 0.f))
     throw PetraError(PETRA_E_ARG, "bad optimizer / BN hyper-parameters");
   tc_ = desc.precision == PETRA_BF16_TC;
@@ -246,6 +245,10 @@ void Stage::build() {
   theta_ = dalloc(n_params_ * sizeof(float));
   v_ = dalloc(n_params_ * sizeof(float));
   grad_ = dalloc(n_params_ * sizeof(float));
+  if (desc_.accumulation_k > 1) {  // Delta_j of Alg. 1: the running average of k backwards
+    acc_ = dalloc(n_params_ * sizeof(float));
+    PETRA_CUDA(cudaMemset(acc_->p, 0, n_params_ * sizeof(float)));
+  }
   bufs_ = dalloc(std::max<int64_t>(1, n_buffers_) * sizeof(float));
   PETRA_CUDA(cudaMemset(grad_->p, 0, n_params_ * sizeof(float)));
 
@@ -377,7 +380,7 @@ void Stage::set_params(const float *theta, const float *v, const float *bufs) {
     PETRA_CUDA(cudaMemcpy(bufs_->p, bufs, n_buffers_ * sizeof(float), cudaMemcpyHostToDevice));
   if (tc_ && theta) {
     sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
-               grad_->as<float>(), nullptr, 0.f, 0.f, 1, nullptr, /*shadow_only=*/true);
+               grad_->as<float>(), nullptr, 1, SGD_PLAIN, nullptr, 0.f, 0.f, 1, nullptr, /*shadow_only=*/true);
     PETRA_CUDA(cudaDeviceSynchronize());
   }
 }
@@ -416,10 +419,25 @@ void Stage::upload_lr(float lr, cudaStream_t st) {
   PETRA_CUDA(cudaMemcpyAsync(lr_dev_->p, h, sizeof(float), cudaMemcpyHostToDevice, st));
 }
 
-void Stage::enqueue_update(cudaStream_t st) {
-  ProfScope ps("sgd_update", st, 0.0, 20.0 * (double)n_params_);
+// the optimizer mode of the backward about to be enqueued (Alg. 1 lines 19-23:
+// Delta += Delta_mb / k every backward, update and reset when t mod k == 0, t from 1)
+int Stage::next_update_mode() const {
+  const int k = desc_.accumulation_k;
+  if (k == 1) return SGD_PLAIN;
+  return (t_ % k == 0) ? SGD_ACC_UPDATE : SGD_ACCUMULATE;
+}
+
+void Stage::advance_step(int mode) {
+  ++t_;
+  if (mode != SGD_ACCUMULATE) ++version_;
+}
+
+void Stage::enqueue_update(int mode, cudaStream_t st) {
+  ProfScope ps("sgd_update", st, 0.0,
+               (mode == SGD_PLAIN ? 20.0 : mode == SGD_ACCUMULATE ? 12.0 : 28.0) * (double)n_params_);
   sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
-             grad_->as<float>(), lr_dev_->as<float>(), desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false);
+             grad_->as<float>(), acc_ ? acc_->as<float>() : nullptr, desc_.accumulation_k, mode, lr_dev_->as<float>(),
+             desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false);
 }
 
 // ------------------------------------------------------------------ layer kernels
@@ -926,8 +944,9 @@ void Stage::backward(uint64_t mb, const float *xt1, const float *xt2, const floa
   ctx_ = 1;
   enqueue_backward(xt1, xt2, d1, d2, oxt1, oxt2, od1, od2, pop, st);
   ctx_ = 0;
-  enqueue_update(st);
-  ++version_;
+  const int mode = next_update_mode();
+  enqueue_update(mode, st);
+  advance_step(mode);
   ++n_bwd_;
   last_stream_ = st;
 }
@@ -942,10 +961,11 @@ void Stage::tail(uint64_t mb, const float *x1, const float *x2, const int32_t *l
   upload_lr(lr, st);
   ctx_ = 0;
   enqueue_tail(x1, x2, labels, oxt1, oxt2, od1, od2, loss, push, pop, st);
-  enqueue_update(st);
+  const int mode = next_update_mode();
+  enqueue_update(mode, st);
+  advance_step(mode);
   have_last_fwd_ = true;
   last_fwd_mb_ = mb;
-  ++version_;
   ++n_fwd_;
   ++n_bwd_;
   last_stream_ = st;
@@ -968,6 +988,7 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
   }
   if (!fwd && !bwd) return;
   if (bwd) upload_lr(lr, st);
+  const int mode = bwd ? next_update_mode() : SGD_PLAIN;
   auto enqueue = [&](cudaStream_t s) {
     if (is_last_) {
       ctx_ = 0;
@@ -992,12 +1013,12 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
       enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, s);
       ctx_ = 0;
     }
-    if (bwd) enqueue_update(s);
+    if (bwd) enqueue_update(mode, s);
   };
   if (!use_graph || Prof::enabled) {
     enqueue(st);
   } else {
-    std::vector<uintptr_t> key = {(uintptr_t)fwd, (uintptr_t)bwd};
+    std::vector<uintptr_t> key = {(uintptr_t)fwd, (uintptr_t)bwd, (uintptr_t)mode};
     for (const void *p : {(const void *)a.x1, (const void *)a.x2, (const void *)a.labels, (const void *)a.o[0],
                           (const void *)a.o[1], (const void *)a.xt[0], (const void *)a.xt[1], (const void *)a.d[0],
                           (const void *)a.d[1], (const void *)a.oxt[0], (const void *)a.oxt[1],
@@ -1035,7 +1056,7 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
     ++n_fwd_;
   }
   if (bwd) {
-    ++version_;
+    advance_step(mode);
     ++n_bwd_;
   }
   last_stream_ = st;

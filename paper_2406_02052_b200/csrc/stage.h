@@ -138,7 +138,7 @@ class Stage {
   bool tc_ = false;
   int64_t n_params_ = 0, n_buffers_ = 0;
   std::vector<petra_tensor_info> tensors_;
-  DevPtr theta_, v_, grad_, bufs_;
+  DevPtr theta_, v_, grad_, bufs_, acc_;     // acc_: Delta_j of Alg. 1 (k > 1 only)
   std::vector<SgdSeg> segs_;
   DevPtr segs_dev_;
   int64_t max_seg_ = 0;
@@ -153,7 +153,8 @@ class Stage {
   // tail workspace
   DevPtr feat_, logits_, dlogits_, lossrow_, dfeat_, tail_d_[2];
   // bf16 shadows of stage-level stream halves (TC path)
-  int64_t version_ = 0;
+  int64_t version_ = 0;                          // optimizer updates applied
+  int64_t t_ = 1;                                // Alg. 1 step counter t (reading c12: starts at 1)
   int64_t n_fwd_ = 0, n_bwd_ = 0;
   bool have_last_fwd_ = false;
   uint64_t last_fwd_mb_ = 0;
@@ -169,7 +170,9 @@ class Stage {
   uint64_t lr_next_ = 0;
   std::map<std::vector<uintptr_t>, CachedGraph> graphs_;
   void upload_lr(float lr, cudaStream_t st);
-  void enqueue_update(cudaStream_t st);
+  int next_update_mode() const;
+  void advance_step(int mode);
+  void enqueue_update(int mode, cudaStream_t st);
   std::vector<int> reserve_push(uint64_t mb);
   std::vector<int> take_pop(uint64_t mb);
   void check_fwd(uint64_t mb, const float *x1, const float *x2);

@@ -168,6 +168,7 @@ class StageSpec:
     bn_momentum: float = 0.1
     bn_eps: float = 1e-5
     fifo_capacity: int = 1
+    accumulation_k: int = 1   # Alg. 1 lines 19-23
 
     def to_c(self):
         arr = (L.PetraUnit * len(self.units))(*[u.to_c() for u in self.units])
@@ -176,18 +177,18 @@ class StageSpec:
         d.batch = self.batch
         d.in_h, d.in_w, d.in_c = self.in_shape
         d.precision, d.momentum, d.weight_decay = self.precision, self.momentum, self.weight_decay
-        d.bn_momentum, d.bn_eps, d.nesterov, d.accumulation_k = self.bn_momentum, self.bn_eps, 1, 1
+        d.bn_momentum, d.bn_eps, d.nesterov, d.accumulation_k = self.bn_momentum, self.bn_eps, 1, self.accumulation_k
         d.fifo_capacity = self.fifo_capacity
         return d, arr   # keep arr alive with d
 
 
-def stage_specs(units, counts, batch, image_hwc, precision=L.FP32, weight_decay=5e-4):
+def stage_specs(units, counts, batch, image_hwc, precision=L.FP32, weight_decay=5e-4, accumulation_k=1):
     ins, _ = shapes(units, batch, *image_hwc)
     out, i = [], 0
     J = len(counts)
     for j, n in enumerate(counts, 1):
         B, H, W, Cc = ins[i]
         out.append(StageSpec(units[i:i + n], batch, (H, W, Cc), precision, weight_decay=weight_decay,
-                             fifo_capacity=2 * (J - j) + 1))
+                             fifo_capacity=2 * (J - j) + 1, accumulation_k=accumulation_k))
         i += n
     return out

@@ -162,12 +162,13 @@ class Pipeline:
 class Schedule:
     """petra_schedule_* : the host-only integer bookkeeping of the pipeline."""
 
-    def __init__(self, stage_rank, nonrev, rank=0):
+    def __init__(self, stage_rank, nonrev, rank=0, accum_k=None):
         J = len(stage_rank)
         sr = (C.c_int32 * J)(*stage_rank)
         nr = (C.c_int32 * J)(*nonrev)
+        ks = (C.c_int32 * J)(*accum_k) if accum_k is not None else None
         h = C.c_void_p()
-        L.call("petra_schedule_create", J, sr, nr, rank, C.byref(h))
+        L.call("petra_schedule_create", J, sr, nr, ks, rank, C.byref(h))
         self.h = h
 
     def tick(self, t, inject):

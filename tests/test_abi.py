@@ -45,7 +45,7 @@ def test_null_arguments_are_rejected():
     assert lib.petra_stage_create(None, 0, None) == 1
     assert lib.petra_stage_forward(None, 0, None, None, None, None, None) == 1
     assert lib.petra_pipeline_tick(None, 0, 0, None, None, 0.0, None, None, None) == 1
-    assert lib.petra_schedule_create(0, None, None, 0, None) == 1
+    assert lib.petra_schedule_create(0, None, None, None, 0, None) == 1
 
 
 @pytest.mark.parametrize("J", [1, 2, 4, 10])
@@ -67,6 +67,23 @@ def test_schedule_matches_oracle_engine(J):
         assert got["fwd_mb"] == r.fwd_mb and got["bwd_mb"] == r.bwd_mb, (r, got)
         assert got["version"] == r.version and got["fifo_depth"] == r.fifo_depth, (r, got)
         assert msgs == []  # single rank: no transport
+
+
+@pytest.mark.parametrize("ks", [[2, 2, 2, 2], [1, 3, 2, 4]])
+def test_schedule_accumulation_matches_oracle_engine(ks):
+    """Accumulation k > 1 (Alg. 1 lines 19-23): the schedule's param_version is
+    the oracle stages' update count, bit-exact, with a different k per stage."""
+    from tests.test_oracle_engine import batch_fn, chain
+    groups, _ = chain(4, "rdr")
+    stages = [E.Stage(g, E.OptConfig(k=k)) for g, k in zip(groups, ks)]
+    T = 9
+    reps, _, _ = E.run_petra(stages, batch_fn, T, lr=0.01)
+    nonrev = [sum(1 for u in g if not u.reversible and not getattr(u, "is_tail", False)) for g in groups]
+    s = Schedule([0] * 4, nonrev, accum_k=ks)
+    for r in reps:
+        got, _ = s.tick(r.tick, r.tick < T)
+        assert got["version"] == r.version and got["fwd_mb"] == r.fwd_mb, (r, got)
+    assert [st.version for st in stages] == [(T // k) for k in ks]
 
 
 def test_schedule_comm_plan_two_ranks():

@@ -231,11 +231,11 @@ def test_tail_stage_parity(case):
 
 
 def run_pipeline_pair(o_units, counts, B, image_nchw, classes, n_mb, lr, drain, precision=L.FP32,
-                      rev_first=False):
+                      rev_first=False, k=1):
     rand_params(o_units, 5)
     groups = OM.group(o_units, counts)
     init = [pack_params(g) for g in groups]   # before the oracle trains them
-    ost = [E.Stage(g, E.OptConfig()) for g in groups]
+    ost = [E.Stage(g, E.OptConfig(k=k)) for g in groups]
 
     def batch_fn(m):
         x = synth.images(image_nchw, 0, m)
@@ -248,7 +248,7 @@ def run_pipeline_pair(o_units, counts, B, image_nchw, classes, n_mb, lr, drain, 
     reps, losses, _ = E.run_petra(ost, batch_fn, n_mb, lr=lr, drain=drain)
     p_units = oracle_to_product_units(o_units)
     hwc = (image_nchw[2], image_nchw[3], image_nchw[1] // 2 if rev_first else image_nchw[1])
-    specs = PM.stage_specs(p_units, counts, B, hwc, precision)
+    specs = PM.stage_specs(p_units, counts, B, hwc, precision, accumulation_k=k)
     pipe = Pipeline(specs, seed=0)
     for j, (th, bf) in enumerate(init, 1):
         pipe.stages[j].set_params(th, np.zeros_like(th), bf)
@@ -286,11 +286,25 @@ def compare_pipeline(reps, losses, ost, groups, pipe, g_reps, g_losses, tol, v_t
     assert not bad, bad
 
 
-def test_pipeline_mlp_config1():
-    """Config 1 (reading c16): 2-stage reversible MLP, d=64, batch 32, 10 ticks, fp32."""
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_pipeline_mlp_config1(k):
+    """Config 1 (reading c16): 2-stage reversible MLP, d=64, batch 32, 10 ticks, fp32;
+    k > 1 = gradient accumulation (Alg. 1 lines 19-23): updates on
+    every k-th backward with the average Delta, version = floor(n_bwd / k) bit-exact."""
     units = OM.build_mlp(64, 10)
-    out = run_pipeline_pair(units, [2, 3], 32, (32, 64, 1, 1), 10, 10, 0.025, drain=False, rev_first=True)
+    out = run_pipeline_pair(units, [2, 3], 32, (32, 64, 1, 1), 10, 10, 0.025 * k, drain=False, rev_first=True,
+                            k=k)
     compare_pipeline(*out, tol=1e-4)
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_pipeline_revnet18_accumulation(k):
+    """RevNet-18 J=4 with accumulation k (lr scaled with k,
+    PAPER.md:256): 6 micro-batches plus drain, fp32; integers bit-exact, losses and
+    theta 1e-4 (momentum buffers 2e-2 as in the k = 1 free-running test)."""
+    units = OM.build_revnet("revnet18", 32, 10)
+    out = run_pipeline_pair(units, [5, 4, 4, 5], 4, (4, 3, 32, 32), 10, 6, 0.01 * k, drain=True, k=k)
+    compare_pipeline(*out, tol=1e-4, v_tol=2e-2)
 
 
 @pytest.mark.parametrize("lr", [0.0, 0.01])
