@@ -125,6 +125,24 @@ petra_status petra_stage_output_shape(const petra_stage *s, int32_t *b, int32_t 
  * length of the BN running-statistics array. */
 petra_status petra_stage_param_count(const petra_stage *s, size_t *n_params, size_t *n_buffers);
 
+/* Device memory of a stage by category (Table 3 accounting, PAPER.md:310-330:
+ * PETRA keeps one parameter version and buffers only the inputs of its
+ * non-reversible units).  Bytes the library allocated for this stage:
+ *   params     theta + BN running statistics (fp32)
+ *   optimizer  v, Delta (last backward) and the Delta_j accumulator (k > 1)
+ *   shadows    bf16 copies of the live conv weights (tensor-core operands; a copy of
+ *              the single live version, rewritten by every update, not a stash)
+ *   fifo       input FIFO slots of the non-reversible units (capacity 2(J-j)+1)
+ *   fifo_live  bytes of those slots holding an input right now
+ *   workspace  everything else: per-layer conv outputs / BN statistics / operand
+ *              copies of the tick, tail buffers
+ *   total      sum of the above categories (fifo_live excluded)
+ * Host-only, no synchronisation.  Errors: PETRA_E_ARG (NULL). */
+typedef struct {
+  uint64_t total, params, optimizer, shadows, fifo, fifo_live, workspace;
+} petra_memory_report;
+petra_status petra_stage_memory(const petra_stage *s, petra_memory_report *out);
+
 typedef enum {
   PETRA_T_CONV_W = 0, PETRA_T_BN_GAMMA = 1, PETRA_T_BN_BETA = 2, PETRA_T_FC_W = 3, PETRA_T_FC_B = 4,
   PETRA_T_BN_RMEAN = 5, PETRA_T_BN_RVAR = 6
@@ -310,7 +328,8 @@ petra_status petra_conv_run(int32_t mode, int32_t engine, const petra_conv_geom 
                             const float *b, const float *addend, float *out);
 /* Kernel benchmark: one convolution pass (as petra_conv_run, on seeded random device
  * inputs) repeated `iters` times after one warm-up; *avg_ms = mean device time per pass
- * (CUDA events).  flags bit 0: forward output z in bf16 (the tensor-core stage layout). */
+ * (CUDA events).  flags bit 0: forward output z in bf16 (the tensor-core stage layout);
+ * bit 1: forward with the BN statistics fused into the epilogue (as a stage runs it). */
 petra_status petra_conv_bench(int32_t mode, int32_t engine, const petra_conv_geom *g, int32_t flags,
                               int32_t iters, float *avg_ms);
 /* Which engine the library uses for a convolution pass at a given precision:

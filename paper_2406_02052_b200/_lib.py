@@ -48,6 +48,11 @@ class PetraTensorInfo(C.Structure):
                 ("ndim", C.c_int32), ("shape", C.c_int32 * 4), ("offset", C.c_int64), ("count", C.c_int64)]
 
 
+class PetraMemoryReport(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("total", "params", "optimizer", "shadows", "fifo", "fifo_live",
+                                          "workspace")]
+
+
 class PetraTickReport(C.Structure):
     _fields_ = [("tick", C.c_int64), ("n_stages", C.c_int32),
                 ("fwd_mb", C.c_int64 * MAX_STAGES), ("bwd_mb", C.c_int64 * MAX_STAGES),
@@ -96,6 +101,7 @@ SIGS = {
     "petra_stage_destroy": (C.c_int, [P]),
     "petra_stage_output_shape": (C.c_int, [P, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32), C.POINTER(I32)]),
     "petra_stage_param_count": (C.c_int, [P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "petra_stage_memory": (C.c_int, [P, C.POINTER(PetraMemoryReport)]),
     "petra_stage_num_tensors": (C.c_int, [P, C.POINTER(I32)]),
     "petra_stage_tensor_info": (C.c_int, [P, I32, C.POINTER(PetraTensorInfo)]),
     "petra_stage_get_params": (C.c_int, [P, VP, VP, VP]),

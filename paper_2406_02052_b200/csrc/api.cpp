@@ -114,6 +114,12 @@ petra_status petra_stage_param_count(const petra_stage *s, size_t *np, size_t *n
   return PETRA_OK;
 }
 
+petra_status petra_stage_memory(const petra_stage *s, petra_memory_report *out) {
+  if (!s || !out) return fail(PETRA_E_ARG, "NULL argument");
+  s->s->memory(out);
+  return PETRA_OK;
+}
+
 petra_status petra_stage_num_tensors(const petra_stage *s, int32_t *n) {
   if (!s || !n) return fail(PETRA_E_ARG, "NULL argument");
   *n = (int32_t)s->s->tensors().size();

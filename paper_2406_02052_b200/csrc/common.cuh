@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "prof.h"
 
@@ -29,6 +30,36 @@ struct CudaError : std::runtime_error {
   } while (0)
 
 constexpr int kNumSMs = 148;  // B200
+
+// Programmatic dependent launch (PDL).  Every library kernel is launched with
+// programmatic stream serialisation and begins with griddepcontrol.wait (all of
+// its stream predecessor's memory operations are visible after it) followed by
+// griddepcontrol.launch_dependents, so the NEXT kernel of the stream is launched
+// and made resident while this one runs, and starts the moment it completes: the
+// kernel-boundary gap of a chain of small dependent kernels shrinks to the wait.
+// A kernel never touches global memory before its wait, so the ordering is that of
+// plain stream serialisation (PETRA_PDL=0 launches without the attribute).
+__device__ __forceinline__ void pdl_wait_trigger() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PETRA_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

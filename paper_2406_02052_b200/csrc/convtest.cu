@@ -13,7 +13,8 @@ namespace {
 // one convolution pass on host buffers; iters > 0: also the mean device time of
 // `iters` further passes (CUDA events; operands prepared once, outside the timing)
 petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a, const float *b,
-                 const float *addend, float *out, int iters = 0, float *ms = nullptr, bool out16 = false) {
+                 const float *addend, float *out, int iters = 0, float *ms = nullptr, bool out16 = false,
+                 bool stats = false) {
   using namespace petra;
   ConvGeom g = make_geom(pg->batch, pg->h, pg->w, pg->cin, pg->cout, pg->ksize, pg->stride);
   int64_t nx = g.Min() * g.Ci, nz = g.M() * g.Co, nw = (int64_t)g.Co * g.K();
@@ -31,13 +32,14 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     PETRA_CUDA(cudaMemcpy(dadd->p, addend, no * 4, cudaMemcpyHostToDevice));
   }
   cudaStream_t st = nullptr;
-  DevPtr ab, bb, ws;
+  DevPtr ab, bb, ws, part = dalloc((size_t)kNumSMs * 4 * g.Co * 2 * sizeof(float));
+  float *stats_part = stats ? part->as<float>() : nullptr;
   const bool a_pad = padded, b_pad = padded && mode == 2;
   std::function<void()> launch;
   if (stem) {  // gathered-im2col tensor-core stem: fp32 image (and fp32 weights) read directly
     ws = dalloc(std::max<size_t>(16, stem_tc_workspace(g)));
     if (mode == 0) {
-      launch = [&] { stem_fwd_tc(g, da->as<float>(), db->as<float>(), dout->p, out16, nullptr, st); };
+      launch = [&] { stem_fwd_tc(g, da->as<float>(), db->as<float>(), dout->p, out16, stats_part, st); };
     } else {
       ab = dalloc(na * 2);
       f32_to_bf16(da->as<float>(), ab->as<__nv_bfloat16>(), na, st);
@@ -82,7 +84,7 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     launch = [&] {
       if (mode == 0)
         conv_fwd_tc(g, ab->as<__nv_bfloat16>(), a_pad, bb->as<__nv_bfloat16>(), dout->p, out16, ws->as<float>(),
-                    nullptr, st);
+                    stats_part, st);
       else if (mode == 1)
         conv_dgrad_tc(g, ab->as<__nv_bfloat16>(), a_pad, bb->as<__nv_bfloat16>(),
                       addend ? dadd->as<float>() : nullptr, dout->as<float>(), ws->as<float>(), st);
@@ -140,7 +142,8 @@ extern "C" petra_status petra_conv_bench(int32_t mode, int32_t engine, const pet
     };
     for (auto &v : a) v = rnd();
     for (auto &v : b) v = rnd() * 0.05f;
-    return run(mode, engine, g, a.data(), b.data(), nullptr, nullptr, iters, avg_ms, (flags & 1) != 0);
+    return run(mode, engine, g, a.data(), b.data(), nullptr, nullptr, iters, avg_ms, (flags & 1) != 0,
+               (flags & 2) != 0);
   } catch (const petra::PetraError &e) {
     return e.status;
   } catch (...) {

@@ -73,8 +73,8 @@ void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean
 template <typename TZ>
 void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float *invstd, const float *gamma,
                    const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dst_in,
-                   float *dst_out, __nv_bfloat16 *dst_bf16, float *dgamma, float *dbeta, double *part,
-                   unsigned *counter, cudaStream_t st);
+                   float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW, float *dgamma, float *dbeta,
+                   double *part, unsigned *counter, cudaStream_t st);
 // dz (fp32, nullable) and/or its bf16 copy (nullable: the tensor-core operand; padded
 // as in bn_apply when pH > 0)
 template <typename TZ>

@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(RT_STATS) bn_stats_kernel(const TZ *__restrict
                                                       float *__restrict__ mean, float *__restrict__ invstd,
                                                       float *__restrict__ rmean, float *__restrict__ rvar,
                                                       float mom) {
+  pdl_wait_trigger();
   constexpr int RT = RT_STATS;
   __shared__ double sh[RT][4];
   const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
@@ -252,8 +253,44 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
                                 const float *__restrict__ mean, const float *__restrict__ invstd,
                                 const float *__restrict__ gamma, const float *__restrict__ beta, int relu,
                                 float sign, const float *acc, TO *out, __nv_bfloat16 *out_bf16, int pH, int pW,
-                                int sh) {
+                                int sh, int fixed) {
+  pdl_wait_trigger();
   const bool vec = (C % 4 == 0) && (ldz % 4 == 0) && (zc0 % 4 == 0);
+  if (vec && fixed) {
+    // the grid stride is a multiple of C/4: each thread keeps one 4-channel group,
+    // whose BN constants live in registers; rows advance by stride / (C/4)
+    const int C4 = C / 4;
+    const int64_t n = M * C4, stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i0 >= n) return;
+    const int c = (int)(i0 % C4) * 4, cz = zc0 + c;
+    const int64_t dm = stride / C4;
+    float a[4], mu[4], be[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a[k] = gamma[cz + k] * invstd[cz + k];
+      mu[k] = mean[cz + k];
+      be[k] = beta[cz + k];
+    }
+    for (int64_t i = i0, m = i0 / C4; i < n; i += stride, m += dm) {
+      const float4 zv = ld4(z, m * ldz + cz);
+      float4 o;
+      float *op = &o.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float y = fmaf(a[k], f4(zv, k) - mu[k], be[k]);
+        if (relu) y = y > 0.f ? y : 0.f;
+        op[k] = sign * y;
+      }
+      if (acc) {
+        const float4 av = ld4(acc, m * C + c);
+        o.x += av.x; o.y += av.y; o.z += av.z; o.w += av.w;
+      }
+      if (out) st4(out, m * C + c, o);
+      if (out_bf16) st4(out_bf16, pad_row(m, pH, pW) * C + c, o);
+    }
+    return;
+  }
   if (vec) {
     const int C4 = C / 4;
     const int64_t n = M * C4;
@@ -299,8 +336,9 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
     const TZ *__restrict__ z, int64_t M, int C, int CT, int TPR, int RG, int64_t rpb, int nrb,
     const float *__restrict__ mean, const float *__restrict__ invstd, const float *__restrict__ gamma,
     const float *__restrict__ beta, int relu, const float *dy0, const float *dy1, int cs, const float *dst_in,
-    float *dst_out, __nv_bfloat16 *dst_bf16, double *__restrict__ part, unsigned *__restrict__ counter,
-    float *__restrict__ dgamma, float *__restrict__ dbeta) {
+    float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW, double *__restrict__ part,
+    unsigned *__restrict__ counter, float *__restrict__ dgamma, float *__restrict__ dbeta) {
+  pdl_wait_trigger();
   constexpr int RT = RT_BWD;
   __shared__ double sh[RT][4];
   const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
@@ -336,7 +374,7 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
         }
         if (dst_out) {
           st4(dst_out, r * C + c, d4);
-          if (dst_bf16) st4(dst_bf16, r * C + c, d4);
+          if (dst_bf16) st4(dst_bf16, pad_row(r, pH, pW) * C + c, d4);
         }
       };
       int64_t r = r0 + rgi;
@@ -371,7 +409,7 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
         if (dst_out) {
           float o = dst_in[r * C + c] - y;
           dst_out[r * C + c] = o;
-          if (dst_bf16) dst_bf16[r * C + c] = __float2bfloat16_rn(o);
+          if (dst_bf16) dst_bf16[pad_row(r, pH, pW) * C + c] = __float2bfloat16_rn(o);
         }
         sg[0] += (double)g;
         sgx[0] += (double)g * (double)xh;
@@ -397,9 +435,44 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
                                  const float *__restrict__ beta, int relu, const float *dy0, const float *dy1,
                                  int cs, const float *__restrict__ dgamma, const float *__restrict__ dbeta,
                                  float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW,
-                                 int sh) {
+                                 int sh, int fixed) {
+  pdl_wait_trigger();
   const float invM = 1.0f / (float)M;
   const bool vec = (C % 4 == 0) && (dy1 == nullptr || cs % 4 == 0);
+  if (vec && fixed) {  // one 4-channel group per thread (see bn_apply_kernel)
+    const int C4 = C / 4;
+    const int64_t n = M * C4, stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i0 >= n) return;
+    const int c = (int)(i0 % C4) * 4;
+    const int64_t dm = stride / C4;
+    float is[4], mu[4], ga[4], be[4], db[4], dg[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      is[k] = invstd[c + k];
+      mu[k] = mean[c + k];
+      ga[k] = gamma[c + k];
+      be[k] = beta[c + k];
+      db[k] = dbeta[c + k] * invM;
+      dg[k] = dgamma[c + k];
+    }
+    for (int64_t i = i0, m = i0 / C4; i < n; i += stride, m += dm) {
+      const float4 zv = ld4(z, m * C + c);
+      float4 g4 = load_dy4(dy0, dy1, cs, C, m, c);
+      float4 o;
+      float *op = &o.x, *gp = &g4.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float xh = (f4(zv, k) - mu[k]) * is[k];
+        float g = gp[k];
+        if (relu && !(fmaf(ga[k], xh, be[k]) > 0.f)) g = 0.f;
+        op[k] = ga[k] * is[k] * (g - db[k] - xh * dg[k] * invM);
+      }
+      if (dz) st4(dz, m * C + c, o);
+      if (dz_bf16) st4(dz_bf16, pad_row(m, pH, pW) * C + c, o);
+    }
+    return;
+  }
   if (vec) {
     const int C4 = C / 4;
     const int64_t n = M * C4;
@@ -441,6 +514,20 @@ inline unsigned ew_grid(int64_t n) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs));
 }
 
+// grid of a per-channel elementwise pass over M x C (256 threads, 4 channels each):
+// a multiple of q = (C/4) / gcd(C/4, 256) blocks, so the grid stride is a multiple of
+// C/4 and every thread keeps one channel group; 0 if C % 4 or q is unreasonable
+inline unsigned chan_grid(int64_t M, int C) {
+  if (C % 4) return 0;
+  const int C4 = C / 4;
+  int a = C4, b = 256;
+  while (b) { const int t = a % b; a = b; b = t; }
+  const int64_t q = C4 / a;
+  if (q > 8 * kNumSMs) return 0;
+  const int64_t g = ew_grid(M * C4);
+  return (unsigned)std::max<int64_t>(q, g / q * q);
+}
+
 }  // namespace
 
 size_t bn_partial_bytes(int64_t M, int C) {
@@ -452,7 +539,7 @@ template <typename TZ>
 void bn_stats(const TZ *z, int64_t M, int C, float eps, float *mean, float *invstd, float *rmean, float *rvar,
               float mom, double *part, unsigned *counter, cudaStream_t st) {
   RedGeom g = red_geom(M, C, RT_STATS);
-  bn_stats_kernel<TZ><<<dim3(g.nrb, g.ctiles), RT_STATS, 0, st>>>(z, M, C, g.CT, g.TPR, g.RG, g.rpb, g.nrb, part, counter,
+  launch_k(bn_stats_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_STATS, 0, st, z, M, C, g.CT, g.TPR, g.RG, g.rpb, g.nrb, part, counter,
                                                             eps, mean, invstd, rmean, rvar, mom);
   PETRA_LAUNCH_CHECK();
 }
@@ -465,9 +552,9 @@ template <typename TZ, typename TO>
 void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean, const float *invstd,
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
               __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st) {
-  bn_apply_kernel<TZ, TO><<<ew_grid(M * C / 4), 256, 0, st>>>(M, C, z, ldz, zc0, mean, invstd, gamma, beta, relu,
-                                                              sign, acc, out, out_bf16, pH, pW,
-                                                              log2_or_neg(C / 4));
+  const unsigned cg = (ldz % 4 == 0 && zc0 % 4 == 0) ? chan_grid(M, C) : 0;
+  launch_k(bn_apply_kernel<TZ, TO>, cg ? cg : ew_grid(M * C / 4), 256, 0, st, M, C, z, ldz, zc0, mean, invstd, gamma,
+           beta, relu, sign, acc, out, out_bf16, pH, pW, log2_or_neg(C / 4), cg ? 1 : 0);
   PETRA_LAUNCH_CHECK();
 }
 template void bn_apply<float, float>(int64_t, int, const float *, int, int, const float *, const float *,
@@ -480,28 +567,30 @@ template void bn_apply<__nv_bfloat16, float>(int64_t, int, const __nv_bfloat16 *
 template <typename TZ>
 void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float *invstd, const float *gamma,
                    const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dst_in,
-                   float *dst_out, __nv_bfloat16 *dst_bf16, float *dgamma, float *dbeta, double *part,
-                   unsigned *counter, cudaStream_t st) {
+                   float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW, float *dgamma, float *dbeta,
+                   double *part, unsigned *counter, cudaStream_t st) {
   RedGeom g = red_geom(M, C, RT_BWD);
-  bn_bwd_reduce_kernel<TZ><<<dim3(g.nrb, g.ctiles), RT_BWD, 0, st>>>(z, M, C, g.CT, g.TPR, g.RG, g.rpb, g.nrb, mean,
+  launch_k(bn_bwd_reduce_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 0, st, z, M, C, g.CT, g.TPR, g.RG, g.rpb, g.nrb, mean,
                                                                  invstd, gamma, beta, relu, dy0, dy1, cs, dst_in,
-                                                                 dst_out, dst_bf16, part, counter, dgamma, dbeta);
+                                                                 dst_out, dst_bf16, pH, pW, part, counter, dgamma,
+                                                                 dbeta);
   PETRA_LAUNCH_CHECK();
 }
 template void bn_bwd_reduce<float>(const float *, int64_t, int, const float *, const float *, const float *,
                                    const float *, int, const float *, const float *, int, const float *, float *,
-                                   __nv_bfloat16 *, float *, float *, double *, unsigned *, cudaStream_t);
+                                   __nv_bfloat16 *, int, int, float *, float *, double *, unsigned *, cudaStream_t);
 template void bn_bwd_reduce<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int, const float *, const float *,
                                            const float *, const float *, int, const float *, const float *, int,
-                                           const float *, float *, __nv_bfloat16 *, float *, float *, double *,
-                                           unsigned *, cudaStream_t);
+                                           const float *, float *, __nv_bfloat16 *, int, int, float *, float *,
+                                           double *, unsigned *, cudaStream_t);
 
 template <typename TZ>
 void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *invstd, const float *gamma,
                const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
                const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, int pH, int pW, cudaStream_t st) {
-  bn_bwd_dz_kernel<TZ><<<ew_grid(M * C / 4), 256, 0, st>>>(M, C, z, mean, invstd, gamma, beta, relu, dy0, dy1, cs,
-                                                           dgamma, dbeta, dz, dz_bf16, pH, pW, log2_or_neg(C / 4));
+  const unsigned cg = (dy1 == nullptr || cs % 4 == 0) ? chan_grid(M, C) : 0;
+  launch_k(bn_bwd_dz_kernel<TZ>, cg ? cg : ew_grid(M * C / 4), 256, 0, st, M, C, z, mean, invstd, gamma, beta, relu,
+           dy0, dy1, cs, dgamma, dbeta, dz, dz_bf16, pH, pW, log2_or_neg(C / 4), cg ? 1 : 0);
   PETRA_LAUNCH_CHECK();
 }
 template void bn_bwd_dz<float>(int64_t, int, const float *, const float *, const float *, const float *,

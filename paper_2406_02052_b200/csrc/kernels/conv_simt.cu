@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(NT)
 conv_simt_kernel(ConvGeom g, const float *__restrict__ asrc, const float *__restrict__ bsrc,
                  float *__restrict__ out, const float *__restrict__ addend,
                  int64_t M, int N, int64_t K, int64_t kchunk) {
+  pdl_wait_trigger();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int t = threadIdx.x;
@@ -173,6 +174,7 @@ conv_simt_kernel(ConvGeom g, const float *__restrict__ asrc, const float *__rest
 
 __global__ void splitk_reduce_kernel(const float *__restrict__ part, int splits, int64_t n,
                                      float *__restrict__ out) {
+  pdl_wait_trigger();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
@@ -186,7 +188,7 @@ __global__ void splitk_reduce_kernel(const float *__restrict__ part, int splits,
 void conv_fwd_simt(const ConvGeom &g, const float *x, const float *w, float *z, cudaStream_t st) {
   int64_t M = g.M();
   dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(g.Co, BN), 1);
-  conv_simt_kernel<FWD><<<grid, NT, 0, st>>>(g, x, w, z, nullptr, M, g.Co, g.K(), g.K());
+  launch_k(conv_simt_kernel<FWD>, grid, NT, 0, st, g, x, w, z, nullptr, M, g.Co, g.K(), g.K());
   PETRA_LAUNCH_CHECK();
 }
 
@@ -195,7 +197,7 @@ void conv_dgrad_simt(const ConvGeom &g, const float *dz, const float *w, const f
   int64_t M = g.Min();
   int64_t K = (int64_t)g.k * g.k * g.Co;
   dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(g.Ci, BN), 1);
-  conv_simt_kernel<DGRAD><<<grid, NT, 0, st>>>(g, dz, w, dx, addend, M, g.Ci, K, K);
+  launch_k(conv_simt_kernel<DGRAD>, grid, NT, 0, st, g, dz, w, dx, addend, M, g.Ci, K, K);
   PETRA_LAUNCH_CHECK();
 }
 
@@ -215,14 +217,14 @@ void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *
   splits = (int)cdiv(K, kchunk);
   dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN), splits);
   if (splits == 1) {
-    conv_simt_kernel<WGRAD><<<grid, NT, 0, st>>>(g, dz, x, dw, nullptr, M, (int)N, K, kchunk);
+    launch_k(conv_simt_kernel<WGRAD>, grid, NT, 0, st, g, dz, x, dw, nullptr, M, (int)N, K, kchunk);
     PETRA_LAUNCH_CHECK();
     return;
   }
-  conv_simt_kernel<WGRAD><<<grid, NT, 0, st>>>(g, dz, x, ws, nullptr, M, (int)N, K, kchunk);
+  launch_k(conv_simt_kernel<WGRAD>, grid, NT, 0, st, g, dz, x, ws, nullptr, M, (int)N, K, kchunk);
   PETRA_LAUNCH_CHECK();
   int64_t n = M * N;
-  splitk_reduce_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st>>>(
+  launch_k(splitk_reduce_kernel, (unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st, 
       ws, splits, n, dw);
   PETRA_LAUNCH_CHECK();
 }

@@ -14,55 +14,82 @@
 namespace petra {
 namespace {
 
-__global__ void sgd_kernel(const SgdSeg *__restrict__ segs, float *__restrict__ theta, float *__restrict__ v,
-                           const float *__restrict__ grad, float *__restrict__ acc, float inv_k, int mode,
-                           const float *__restrict__ lr_dev, float mom, float wd, int nesterov, int shadow_only) {
+__global__ void __launch_bounds__(256) sgd_kernel(const SgdSeg *__restrict__ segs, float *__restrict__ theta,
+                                                  float *__restrict__ v, const float *__restrict__ grad,
+                                                  float *__restrict__ acc, float inv_k, int mode,
+                                                  const float *__restrict__ lr_dev, float mom, float wd, int nesterov,
+                                                  int shadow_only) {
+  pdl_wait_trigger();
   // mode (Alg. 1 lines 19-22):  SGD_PLAIN   k = 1, update with Delta;
   // SGD_ACCUMULATE  acc += Delta/k, no update;  SGD_ACC_UPDATE  update with acc + Delta/k, acc = 0
   const SgdSeg sg = segs[blockIdx.y];
   if (shadow_only && !sg.w_bf16) return;
   const float lam = sg.decay ? wd : 0.f;
   const float lr = shadow_only ? 0.f : *lr_dev;  // device-resident: graph replays read the tick's lr
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sg.count; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t o = sg.offset + i;
+  // theta[o] after this tick's update (or unchanged for shadow_only)
+  auto update = [&](int64_t o) -> float {
     float th = theta[o];
-    if (mode == SGD_ACCUMULATE) {
-      acc[o] += grad[o] * inv_k;
-      continue;
+    if (shadow_only) return th;
+    float d = grad[o];
+    if (mode == SGD_ACC_UPDATE) {
+      d = fmaf(d, inv_k, acc[o]);
+      acc[o] = 0.f;
     }
-    if (!shadow_only) {
-      float d = grad[o];
-      if (mode == SGD_ACC_UPDATE) {
-        d = fmaf(d, inv_k, acc[o]);
-        acc[o] = 0.f;
+    const float g = fmaf(lam, th, d);
+    const float vv = fmaf(mom, v[o], g);
+    v[o] = vv;
+    th -= lr * (nesterov ? fmaf(mom, vv, g) : vv);
+    theta[o] = th;
+    return th;
+  };
+  if (mode == SGD_ACCUMULATE) {  // Delta_j += Delta / k; theta (and its shadows) unchanged
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sg.count;
+         i += (int64_t)gridDim.x * blockDim.x)
+      acc[sg.offset + i] += grad[sg.offset + i] * inv_k;
+    return;
+  }
+  if (sg.wt_bf16) {
+    // conv weight [Co][kh][kw][Ci] in 32(co) x 32(ci) tiles of one tap: theta, v and
+    // the bf16 copy w_bf16 (same order) are read / written along ci, the dgrad operand
+    // wT[ci][tap'][co] = w[co][tap][ci] (tap' = k*k-1-tap, flipped) along co through
+    // a shared-memory transpose -- every global access coalesced
+    __shared__ __nv_bfloat16 tile[32][33];
+    const int taps = sg.k * sg.k;
+    const int nco = (sg.co + 31) / 32, nci = (sg.ci + 31) / 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int t = blockIdx.x; t < taps * nco * nci; t += gridDim.x) {
+      const int cib = t % nci, r = t / nci, cob = r % nco, tap = r / nco;
+      const int ci = cib * 32 + tx;
+#pragma unroll
+      for (int rr = ty; rr < 32; rr += 8) {
+        const int co = cob * 32 + rr;
+        if (co < sg.co && ci < sg.ci) {
+          const int64_t i = ((int64_t)co * taps + tap) * sg.ci + ci;
+          const __nv_bfloat16 hb = __float2bfloat16_rn(update(sg.offset + i));
+          sg.w_bf16[i] = hb;
+          tile[rr][tx] = hb;
+        }
       }
-      float g = fmaf(lam, th, d);
-      float vv = fmaf(mom, v[o], g);
-      v[o] = vv;
-      th -= lr * (nesterov ? fmaf(mom, vv, g) : vv);
-      theta[o] = th;
-    }
-    if (sg.w_bf16) {
-      // conv weight [Co][kh][kw][Ci]: bf16 copy in the same order, and the dgrad
-      // operand wT[ci][kh'][kw'][co] = w[co][k-1-kh'][k-1-kw'][ci]
-      __nv_bfloat16 hb = __float2bfloat16_rn(th);
-      sg.w_bf16[i] = hb;
-      if (sg.wt_bf16) {
-        int ci = (int)(i % sg.ci);
-        int64_t r = i / sg.ci;
-        int kw = (int)(r % sg.k);
-        r /= sg.k;
-        int kh = (int)(r % sg.k);
-        int co = (int)(r / sg.k);
-        int64_t j = (((int64_t)ci * sg.k + (sg.k - 1 - kh)) * sg.k + (sg.k - 1 - kw)) * sg.co + co;
-        sg.wt_bf16[j] = hb;
+      __syncthreads();
+      const int co = cob * 32 + tx;
+#pragma unroll
+      for (int rr = ty; rr < 32; rr += 8) {
+        const int cj = cib * 32 + rr;
+        if (co < sg.co && cj < sg.ci) sg.wt_bf16[((int64_t)cj * taps + (taps - 1 - tap)) * sg.co + co] = tile[tx][rr];
       }
+      __syncthreads();
     }
+    return;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sg.count; i += (int64_t)gridDim.x * blockDim.x) {
+    const float th = update(sg.offset + i);
+    if (sg.w_bf16) sg.w_bf16[i] = __float2bfloat16_rn(th);
   }
 }
 
 __global__ void gap_kernel(const float *__restrict__ x1, const float *__restrict__ x2, int B, int HW, int C,
                            float *__restrict__ feat) {
+  pdl_wait_trigger();
   // feat[b][c'] for c' in [0, 2C): mean over HW (fixed summation order)
   int b = blockIdx.y;
   int c2 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -76,6 +103,7 @@ __global__ void gap_kernel(const float *__restrict__ x1, const float *__restrict
 
 __global__ void fc_fwd_kernel(const float *__restrict__ feat, const float *__restrict__ w,
                               const float *__restrict__ bias, int B, int Cin, int N, float *__restrict__ logits) {
+  pdl_wait_trigger();
   // one warp per (b, n)
   int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
@@ -90,6 +118,7 @@ __global__ void fc_fwd_kernel(const float *__restrict__ feat, const float *__res
 
 __global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__restrict__ labels, int B, int N,
                           float *__restrict__ dlogits, float *__restrict__ loss_row) {
+  pdl_wait_trigger();
   // one block (256 threads) per row; dlogits = (softmax - onehot)/B
   __shared__ float red[32];
   int b = blockIdx.x;
@@ -134,6 +163,7 @@ __global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__res
 
 __global__ void loss_mean_kernel(const float *__restrict__ loss_row, int B, float *__restrict__ loss,
                                  int *__restrict__ nonfinite) {
+  pdl_wait_trigger();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double s = 0.0;
     for (int b = 0; b < B; ++b) s += loss_row[b];
@@ -145,6 +175,7 @@ __global__ void loss_mean_kernel(const float *__restrict__ loss_row, int B, floa
 
 __global__ void fc_bwd_w_kernel(const float *__restrict__ dlogits, const float *__restrict__ feat, int B, int Cin,
                                 int N, float *__restrict__ dw, float *__restrict__ db) {
+  pdl_wait_trigger();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < (int64_t)N * Cin) {
     int n = (int)(i / Cin), c = (int)(i - (int64_t)n * Cin);
@@ -161,6 +192,7 @@ __global__ void fc_bwd_w_kernel(const float *__restrict__ dlogits, const float *
 
 __global__ void fc_bwd_x_kernel(const float *__restrict__ dlogits, const float *__restrict__ w, int B, int Cin,
                                 int N, float *__restrict__ dfeat) {
+  pdl_wait_trigger();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)B * Cin) return;
   int b = (int)(i / Cin), c = (int)(i - (int64_t)b * Cin);
@@ -171,6 +203,7 @@ __global__ void fc_bwd_x_kernel(const float *__restrict__ dlogits, const float *
 
 __global__ void gap_bwd_kernel(const float *__restrict__ dfeat, int B, int HW, int C, float *__restrict__ d1,
                                float *__restrict__ d2) {
+  pdl_wait_trigger();
   int64_t n = (int64_t)B * HW * C;
   float inv = 1.f / (float)HW;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -184,6 +217,7 @@ __global__ void gap_bwd_kernel(const float *__restrict__ dfeat, int B, int HW, i
 // max-pool on a [B][H][W][C] activation, writes split halves of the output
 __global__ void maxpool_fwd_kernel(const float *__restrict__ a, int B, int H, int W, int C, int Ho, int Wo,
                                    float *__restrict__ o1, float *__restrict__ o2, uint8_t *__restrict__ arg) {
+  pdl_wait_trigger();
   int64_t n = (int64_t)B * Ho * Wo * C;
   int Ch = C / 2;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -212,6 +246,7 @@ __global__ void maxpool_fwd_kernel(const float *__restrict__ a, int B, int H, in
 __global__ void maxpool_bwd_kernel(const float *__restrict__ d1, const float *__restrict__ d2,
                                    const uint8_t *__restrict__ arg, int B, int H, int W, int C, int Ho, int Wo,
                                    float *__restrict__ da) {
+  pdl_wait_trigger();
   int64_t n = (int64_t)B * H * W * C;
   int Ch = C / 2;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -241,6 +276,7 @@ __global__ void maxpool_bwd_kernel(const float *__restrict__ d1, const float *__
 // pixel, float4 loads/stores, the 4 argmax bytes as one 32-bit word
 __global__ void maxpool_fwd_v4_kernel(const float4 *__restrict__ a, int B, int H, int W, int C4, int Ho, int Wo,
                                       float4 *__restrict__ o1, float4 *__restrict__ o2, uchar4 *__restrict__ arg) {
+  pdl_wait_trigger();
   const int n = B * Ho * Wo * C4, Ch4 = C4 / 2;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int c = i % C4, pix = i / C4, wo = pix % Wo, r = pix / Wo, ho = r % Ho, b = r / Ho;
@@ -268,6 +304,7 @@ __global__ void maxpool_fwd_v4_kernel(const float4 *__restrict__ a, int B, int H
 __global__ void maxpool_bwd_v4_kernel(const float4 *__restrict__ d1, const float4 *__restrict__ d2,
                                       const uchar4 *__restrict__ arg, int B, int H, int W, int C4, int Ho, int Wo,
                                       float4 *__restrict__ da) {
+  pdl_wait_trigger();
   const int n = B * H * W * C4, Ch4 = C4 / 2;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int c = i % C4, pix = i / C4, w = pix % W, r = pix / W, h = r % H, b = r / H;
@@ -294,6 +331,7 @@ __global__ void maxpool_bwd_v4_kernel(const float4 *__restrict__ d1, const float
 }
 
 __global__ void f32_to_bf16_kernel(const float *__restrict__ x, __nv_bfloat16 *__restrict__ y, int64_t n) {
+  pdl_wait_trigger();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = __float2bfloat16_rn(x[i]);
 }
@@ -301,6 +339,7 @@ __global__ void f32_to_bf16_kernel(const float *__restrict__ x, __nv_bfloat16 *_
 // interior of a zero-bordered [B][H+2][W+2][C] bf16 buffer (C % 4 == 0)
 __global__ void f32_to_bf16_padded_kernel(const float4 *__restrict__ x, uint2 *__restrict__ y, int B, int H, int W,
                                           int C4) {
+  pdl_wait_trigger();
   const int64_t n = (int64_t)B * H * W * C4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % C4);
@@ -326,7 +365,7 @@ void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *thet
                 float *acc, int k, int mode, const float *lr_dev, float mom, float wd, int nesterov, cudaStream_t st,
                 bool shadow_only) {
   dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(max_count, 256), 2 * kNumSMs)), nseg);
-  sgd_kernel<<<grid, 256, 0, st>>>(segs_dev, theta, v, grad, acc, 1.f / (float)k, mode, lr_dev, mom, wd, nesterov,
+  launch_k(sgd_kernel, grid, 256, 0, st, segs_dev, theta, v, grad, acc, 1.f / (float)k, mode, lr_dev, mom, wd, nesterov,
                                            shadow_only ? 1 : 0);
   PETRA_LAUNCH_CHECK();
 }
@@ -336,20 +375,20 @@ void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int 
                            float *dlogits, float *loss_row, float *dfeat, float *dw, float *db, float *d1,
                            float *d2, float *loss, int *nonfinite, cudaStream_t st) {
   int Cin = 2 * C;
-  gap_kernel<<<dim3((unsigned)cdiv(Cin, 128), B), 128, 0, st>>>(x1, x2, B, HW, C, feat);
+  launch_k(gap_kernel, dim3((unsigned)cdiv(Cin, 128), B), 128, 0, st, x1, x2, B, HW, C, feat);
   PETRA_LAUNCH_CHECK();
-  fc_fwd_kernel<<<(unsigned)cdiv((int64_t)B * N * 32, 256), 256, 0, st>>>(feat, w, bias, B, Cin, N, logits);
+  launch_k(fc_fwd_kernel, (unsigned)cdiv((int64_t)B * N * 32, 256), 256, 0, st, feat, w, bias, B, Cin, N, logits);
   PETRA_LAUNCH_CHECK();
-  ce_kernel<<<B, 256, 0, st>>>(logits, labels, B, N, dlogits, loss_row);
+  launch_k(ce_kernel, B, 256, 0, st, logits, labels, B, N, dlogits, loss_row);
   PETRA_LAUNCH_CHECK();
-  loss_mean_kernel<<<1, 32, 0, st>>>(loss_row, B, loss, nonfinite);
+  launch_k(loss_mean_kernel, 1, 32, 0, st, loss_row, B, loss, nonfinite);
   PETRA_LAUNCH_CHECK();
-  fc_bwd_w_kernel<<<(unsigned)cdiv(std::max<int64_t>((int64_t)N * Cin, N), 256), 256, 0, st>>>(dlogits, feat, B,
+  launch_k(fc_bwd_w_kernel, (unsigned)cdiv(std::max<int64_t>((int64_t)N * Cin, N), 256), 256, 0, st, dlogits, feat, B,
                                                                                                Cin, N, dw, db);
   PETRA_LAUNCH_CHECK();
-  fc_bwd_x_kernel<<<(unsigned)cdiv((int64_t)B * Cin, 256), 256, 0, st>>>(dlogits, w, B, Cin, N, dfeat);
+  launch_k(fc_bwd_x_kernel, (unsigned)cdiv((int64_t)B * Cin, 256), 256, 0, st, dlogits, w, B, Cin, N, dfeat);
   PETRA_LAUNCH_CHECK();
-  gap_bwd_kernel<<<ew_grid((int64_t)B * HW * C), 256, 0, st>>>(dfeat, B, HW, C, d1, d2);
+  launch_k(gap_bwd_kernel, ew_grid((int64_t)B * HW * C), 256, 0, st, dfeat, B, HW, C, d1, d2);
   PETRA_LAUNCH_CHECK();
 }
 
@@ -357,11 +396,11 @@ void maxpool_fwd(const float *a, int B, int H, int W, int C, int Ho, int Wo, flo
                  cudaStream_t st) {
   if (C % 8 == 0 && (int64_t)B * H * W * C < ((int64_t)1 << 31)) {
     const int C4 = C / 4;
-    maxpool_fwd_v4_kernel<<<ew_grid((int64_t)B * Ho * Wo * C4), 256, 0, st>>>(
+    launch_k(maxpool_fwd_v4_kernel, ew_grid((int64_t)B * Ho * Wo * C4), 256, 0, st, 
         reinterpret_cast<const float4 *>(a), B, H, W, C4, Ho, Wo, reinterpret_cast<float4 *>(o1),
         reinterpret_cast<float4 *>(o2), reinterpret_cast<uchar4 *>(arg));
   } else {
-    maxpool_fwd_kernel<<<ew_grid((int64_t)B * Ho * Wo * C), 256, 0, st>>>(a, B, H, W, C, Ho, Wo, o1, o2, arg);
+    launch_k(maxpool_fwd_kernel, ew_grid((int64_t)B * Ho * Wo * C), 256, 0, st, a, B, H, W, C, Ho, Wo, o1, o2, arg);
   }
   PETRA_LAUNCH_CHECK();
 }
@@ -370,24 +409,24 @@ void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, in
                  float *da, cudaStream_t st) {
   if (C % 8 == 0 && (int64_t)B * H * W * C < ((int64_t)1 << 31)) {
     const int C4 = C / 4;
-    maxpool_bwd_v4_kernel<<<ew_grid((int64_t)B * H * W * C4), 256, 0, st>>>(
+    launch_k(maxpool_bwd_v4_kernel, ew_grid((int64_t)B * H * W * C4), 256, 0, st, 
         reinterpret_cast<const float4 *>(d1), reinterpret_cast<const float4 *>(d2),
         reinterpret_cast<const uchar4 *>(arg), B, H, W, C4, Ho, Wo, reinterpret_cast<float4 *>(da));
   } else {
-    maxpool_bwd_kernel<<<ew_grid((int64_t)B * H * W * C), 256, 0, st>>>(d1, d2, arg, B, H, W, C, Ho, Wo, da);
+    launch_k(maxpool_bwd_kernel, ew_grid((int64_t)B * H * W * C), 256, 0, st, d1, d2, arg, B, H, W, C, Ho, Wo, da);
   }
   PETRA_LAUNCH_CHECK();
 }
 
 void f32_to_bf16_padded(const float *x, __nv_bfloat16 *y, int B, int H, int W, int C, cudaStream_t st) {
   const int C4 = C / 4;
-  f32_to_bf16_padded_kernel<<<ew_grid((int64_t)B * H * W * C4), 256, 0, st>>>(
+  launch_k(f32_to_bf16_padded_kernel, ew_grid((int64_t)B * H * W * C4), 256, 0, st, 
       reinterpret_cast<const float4 *>(x), reinterpret_cast<uint2 *>(y), B, H, W, C4);
   PETRA_LAUNCH_CHECK();
 }
 
 void f32_to_bf16(const float *x, __nv_bfloat16 *y, int64_t n, cudaStream_t st) {
-  f32_to_bf16_kernel<<<ew_grid(n), 256, 0, st>>>(x, y, n);
+  launch_k(f32_to_bf16_kernel, ew_grid(n), 256, 0, st, x, y, n);
   PETRA_LAUNCH_CHECK();
 }
 

@@ -102,6 +102,7 @@ __device__ __forceinline__ void store_row_chunks(uint8_t *tile, int row, int c0,
 
 template <int BN, bool OUT16>
 __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_constant__ StemParams P) {
+  pdl_wait_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
@@ -270,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 stem_wgrad_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constant__ StemParams P) {
+  pdl_wait_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t B_BYTES = BN * 64 * 2;
@@ -460,13 +462,13 @@ int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, void *z, bool
   const int grid = (int)std::min<int64_t>(cdiv(P.M, 128), kNumSMs);
   const size_t smem = fwd_smem(P.N, P.KB);
   if (z_bf16) {
-    if (P.N == 64) stem_fwd_kernel<64, true><<<grid, kThreads, smem, st>>>(P);
-    else if (P.N == 128) stem_fwd_kernel<128, true><<<grid, kThreads, smem, st>>>(P);
-    else stem_fwd_kernel<256, true><<<grid, kThreads, smem, st>>>(P);
+    if (P.N == 64) launch_k(stem_fwd_kernel<64, true>, grid, kThreads, smem, st, P);
+    else if (P.N == 128) launch_k(stem_fwd_kernel<128, true>, grid, kThreads, smem, st, P);
+    else launch_k(stem_fwd_kernel<256, true>, grid, kThreads, smem, st, P);
   } else {
-    if (P.N == 64) stem_fwd_kernel<64, false><<<grid, kThreads, smem, st>>>(P);
-    else if (P.N == 128) stem_fwd_kernel<128, false><<<grid, kThreads, smem, st>>>(P);
-    else stem_fwd_kernel<256, false><<<grid, kThreads, smem, st>>>(P);
+    if (P.N == 64) launch_k(stem_fwd_kernel<64, false>, grid, kThreads, smem, st, P);
+    else if (P.N == 128) launch_k(stem_fwd_kernel<128, false>, grid, kThreads, smem, st, P);
+    else launch_k(stem_fwd_kernel<256, false>, grid, kThreads, smem, st, P);
   }
   PETRA_LAUNCH_CHECK();
   return stats_part ? grid : 0;
@@ -488,9 +490,9 @@ void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const float *x, f
   CUtensorMap tdz = kmajor_map_bf16(dz, P.M, P.N, 64);  // dz [pixels][Co], box (64 ch, 64 pixels)
   const int grid = std::min(wp.n_mt * wp.splits, kNumSMs);
   const size_t smem = wgrad_smem(P.N);
-  if (P.N == 64) stem_wgrad_kernel<64><<<grid, kThreads, smem, st>>>(tdz, P);
-  else if (P.N == 128) stem_wgrad_kernel<128><<<grid, kThreads, smem, st>>>(tdz, P);
-  else stem_wgrad_kernel<256><<<grid, kThreads, smem, st>>>(tdz, P);
+  if (P.N == 64) launch_k(stem_wgrad_kernel<64>, grid, kThreads, smem, st, tdz, P);
+  else if (P.N == 128) launch_k(stem_wgrad_kernel<128>, grid, kThreads, smem, st, tdz, P);
+  else launch_k(stem_wgrad_kernel<256>, grid, kThreads, smem, st, tdz, P);
   PETRA_LAUNCH_CHECK();
   if (wp.splits > 1) splitk_sum(ws, wp.splits, (int64_t)g.Co * g.K(), dw, st);
 }

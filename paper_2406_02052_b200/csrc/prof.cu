@@ -1,8 +1,10 @@
 // prof.cu -- launch counter and event-based per-category timing (product code).
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/petra.h"
 #include "errors.h"
+#include "common.cuh"
 #include "prof.h"
 
 namespace petra {
@@ -12,6 +14,14 @@ std::vector<Prof::Rec> Prof::recs;
 std::vector<std::string> Prof::names;
 std::vector<cudaEvent_t> Prof::pool;
 static size_t g_pool_next = 0;
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("PETRA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int Prof::category(const char *name) {
   for (size_t i = 0; i < names.size(); ++i)

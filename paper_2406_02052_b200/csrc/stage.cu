@@ -23,8 +23,12 @@
 
 namespace petra {
 
+// bytes allocated by the stage under construction (Stage::memory)
+static thread_local size_t *g_alloc_acc = nullptr;
+
 DevBuf::DevBuf(size_t n) : bytes(n) {
   if (n == 0) return;
+  if (g_alloc_acc) *g_alloc_acc += n;
   cudaError_t e = cudaMalloc(&p, n);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -67,6 +71,10 @@ Stage::Stage(const petra_stage_desc &desc, uint64_t seed) : desc_(desc) {
   PETRA_CUDA(cudaGetDevice(&dev));
   units_.resize(desc.n_units);
   for (int i = 0; i < desc.n_units; ++i) units_[i].d = desc.units[i];
+  struct AccGuard {
+    explicit AccGuard(size_t *p) { g_alloc_acc = p; }
+    ~AccGuard() { g_alloc_acc = nullptr; }
+  } guard(&alloc_bytes_);
   build();
   init_params(seed);
 }
@@ -405,6 +413,31 @@ bool Stage::nonfinite() {
   return h != 0;
 }
 
+void Stage::memory(petra_memory_report *r) const {
+  auto b = [](const DevPtr &p) -> uint64_t { return p ? p->bytes : 0; };
+  *r = petra_memory_report{};
+  r->params = b(theta_) + (n_buffers_ ? b(bufs_) : 0);
+  r->optimizer = b(v_) + b(grad_) + b(acc_);
+  auto layer = [&](const Layer &L) { r->shadows += b(L.w_bf16) + b(L.wt_bf16); };
+  for (auto &u : units_) {
+    for (auto &L : u.phi) layer(L);
+    if (u.d.kind == PETRA_UNIT_DS) {
+      layer(u.pa);
+      layer(u.pb);
+    }
+    uint64_t slot = 0, all = 0;
+    for (size_t s = 0; s < u.fifo.slot0.size(); ++s) {
+      uint64_t one = b(u.fifo.slot0[s]) + (s < u.fifo.slot1.size() ? b(u.fifo.slot1[s]) : 0);
+      all += one;
+      slot = one;
+    }
+    r->fifo += all;
+    r->fifo_live += slot * (uint64_t)u.fifo.size;
+  }
+  r->total = alloc_bytes_;
+  r->workspace = r->total - r->params - r->optimizer - r->shadows - r->fifo;
+}
+
 int Stage::fifo_depth() const {
   int d = 0;
   for (auto &u : units_) d += u.fifo.size;
@@ -536,9 +569,9 @@ void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
 
 // forward of a conv-BN-ReLU chain on x; inner activations into L.a; the last
 // layer's z / stats are left for the caller's fused epilogue.
-void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running, cudaStream_t st) {
+void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running, cudaStream_t st, bool ready0) {
   const float *th = theta_->as<float>();
-  bool ready = false;
+  bool ready = ready0;
   for (size_t l = 0; l < phi.size(); ++l) {
     Layer &L = phi[l];
     conv_fwd(L, x, st, ready);
@@ -561,21 +594,21 @@ void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running
 // optional fused reconstruction dst_out = dst_in - act(bn(z)); writes dgamma,
 // dbeta into Delta and dz into L.dz.
 void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, const float *dst_in, float *dst_out,
-                      cudaStream_t st) {
+                      cudaStream_t st, Bf16Out ob) {
   const float *th = theta_->as<float>();
   float *gr = grad_->as<float>();
   double n = (double)L.g.M() * L.g.Co;
   {
-  ProfScope ps("bn_bwd_reduce", st, 0.0, n * ((L.z16 ? 2.0 : 4.0) + 4.0 + (dst_out ? 8.0 : 0.0)));
+  ProfScope ps("bn_bwd_reduce", st, 0.0, n * ((L.z16 ? 2.0 : 4.0) + 4.0 + (dst_out ? 8.0 : 0.0) + (ob.p ? 2.0 : 0.0)));
   if (L.z16)
     bn_bwd_reduce<__nv_bfloat16>(L.z()->as<__nv_bfloat16>(), L.g.M(), L.g.Co, L.mean()->as<float>(),
                                  L.invstd()->as<float>(), th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs,
-                                 dst_in, dst_out, nullptr, gr + L.g_off, gr + L.b_off, part()->as<double>(),
-                                 counters()->as<unsigned>(), st);
+                                 dst_in, dst_out, ob.p, ob.pH, ob.pW, gr + L.g_off, gr + L.b_off,
+                                 part()->as<double>(), counters()->as<unsigned>(), st);
   else
     bn_bwd_reduce<float>(L.z()->as<float>(), L.g.M(), L.g.Co, L.mean()->as<float>(), L.invstd()->as<float>(),
-                         th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, dst_in, dst_out, nullptr,
-                         gr + L.g_off, gr + L.b_off, part()->as<double>(), counters()->as<unsigned>(), st);
+                         th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, dst_in, dst_out, ob.p, ob.pH,
+                         ob.pW, gr + L.g_off, gr + L.b_off, part()->as<double>(), counters()->as<unsigned>(), st);
   }
   // dz in bf16 for tensor-core dgrad / wgrad, in fp32 only if a SIMT pass consumes it
   // (the stem has no dgrad: its input is data)
@@ -597,9 +630,9 @@ void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, cons
 // VJP through a branch whose last layer receives dy (reconstruction fused when
 // dst_out != null).  dx_out = addend + d(branch)/dx^T dy  (dx_out may be null).
 void Stage::branch_backward(std::vector<Layer> &phi, const float *x, const float *dy, const float *dst_in,
-                            float *dst_out, const float *addend, float *dx_out, cudaStream_t st) {
+                            float *dst_out, const float *addend, float *dx_out, cudaStream_t st, Bf16Out ob) {
   int n = (int)phi.size();
-  layer_bwd(phi[n - 1], dy, nullptr, 0, dst_in, dst_out, st);
+  layer_bwd(phi[n - 1], dy, nullptr, 0, dst_in, dst_out, st, dst_out ? ob : Bf16Out{});
   for (int l = n - 1; l >= 0; --l) {
     Layer &L = phi[l];
     const float *xl = l == 0 ? x : phi[l - 1].a()->as<float>();
@@ -616,16 +649,26 @@ void Stage::branch_backward(std::vector<Layer> &phi, const float *x, const float
 // ------------------------------------------------------------------ units
 // forward of one unit: cur[] = current halves (inputs), out[] = where the unit's
 // outputs go (REV: only out[dst] is written; may equal cur[dst] for in place).
-void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep, cudaStream_t st) {
+// The bf16 operand of the next unit's first convolution (when that unit reads the
+// half this one writes): written by the producing kernel instead of a separate
+// conversion pass.
+Bf16Out Stage::src_operand(Unit &n) {
+  if (!tc_ || n.d.kind != PETRA_UNIT_REV) return {};
+  Layer &L = n.phi[0];
+  if (!conv_tc_supported(L.g, 0)) return {};
+  return Bf16Out{L.xb()->as<__nv_bfloat16>(), L.xpad ? L.g.H : 0, L.g.W};
+}
+
+void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep, cudaStream_t st, Bf16Out ob,
+                         bool src_ready) {
   const float *th = theta_->as<float>();
   switch (u.d.kind) {
     case PETRA_UNIT_REV: {
       // x[dst] += Phi(x[src])  (north_star y1 = x1 + F(x2), y2 = x2 + G(y1))
-      branch_forward(u.phi, cur[u.src()], keep, st);
+      branch_forward(u.phi, cur[u.src()], keep, st, src_ready);
       Layer &L = u.phi.back();
-      apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(),
-                             L.invstd()->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, cur[u.dst()], out[u.dst()],
-                             nullptr, st);
+      apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(), L.invstd()->as<float>(),
+               th + L.g_off, th + L.b_off, 1, 1.f, cur[u.dst()], out[u.dst()], ob.p, st, ob.pH, ob.pW);
       break;
     }
     case PETRA_UNIT_DS: {
@@ -676,15 +719,15 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
 // the unit input for non-reversible units (FIFO slot), cur_d = gradient wrt the
 // unit output; out_x / out_d = targets (REV: out_x[dst], out_d[src]; DS: out_d[both]).
 void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const float *cur_x[2], float *out_x[2],
-                          const float *cur_d[2], float *out_d[2], cudaStream_t st) {
+                          const float *cur_d[2], float *out_d[2], cudaStream_t st, Bf16Out ob, bool src_ready) {
   switch (u.d.kind) {
     case PETRA_UNIT_REV: {
       // approximate inversion with the current theta: recompute the
       // graph of Phi on x[src] (src is unchanged by the unit), subtract, VJP.
       const float *src = cur_x[u.src()];
-      if (recompute) branch_forward(u.phi, src, true, st);
+      if (recompute) branch_forward(u.phi, src, true, st, src_ready);
       branch_backward(u.phi, src, cur_d[u.dst()], cur_x[u.dst()], out_x[u.dst()], cur_d[u.src()],
-                      out_d[u.src()], st);
+                      out_d[u.src()], st, ob);
       break;
     }
     case PETRA_UNIT_DS: {
@@ -799,6 +842,7 @@ void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *
   bool ro[2] = {true, true};
   float *outs[2] = {o1, o2};
   const int n = (int)units_.size() - (is_last_ ? 1 : 0);
+  bool ready = false;  // bf16 operand of this unit's src already written by its producer
   for (int i = 0; i < n; ++i) {
     Unit &u = units_[i];
     float *tgt[2];
@@ -807,10 +851,14 @@ void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *
       float *o[2] = {nullptr, nullptr};
       int d = u.dst();
       o[d] = ro[d] ? tgt[d] : const_cast<float *>(cur[d]);
-      unit_forward(u, cur, o, keep, st);
+      Bf16Out ob = (i + 1 < n && units_[i + 1].d.kind == PETRA_UNIT_REV && units_[i + 1].src() == d)
+                       ? src_operand(units_[i + 1]) : Bf16Out{};
+      unit_forward(u, cur, o, keep, st, ob, ready);
+      ready = ob.p != nullptr;
       cur[d] = o[d];
       ro[d] = false;
     } else {
+      ready = false;
       int slot = push[i];
       copy_d2d(u.fifo.slot0[slot]->as<float>(), cur[0], u.in.numel(), st);
       if (u.d.kind == PETRA_UNIT_DS) copy_d2d(u.fifo.slot1[slot]->as<float>(), cur[1], u.in.numel(), st);
@@ -836,6 +884,7 @@ void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *
 void Stage::enqueue_backward_walk(int last_unit, bool recompute, const float *cx[2], const float *cd[2],
                                   bool rox[2], bool rod[2], float *ox[2], float *od[2], const std::vector<int> &pop,
                                   cudaStream_t st) {
+  bool ready = false;  // bf16 operand of this unit's src written by the previous reconstruction
   for (int i = last_unit; i >= 0; --i) {
     Unit &u = units_[i];
     if (u.d.kind == PETRA_UNIT_REV) {
@@ -845,12 +894,18 @@ void Stage::enqueue_backward_walk(int last_unit, bool recompute, const float *cx
       td[s] = rod[s] ? (u.bd[s] ? u.bd[s]->as<float>() : od[s]) : const_cast<float *>(cd[s]);
       if (!tx[d] || !td[s]) throw PetraError(PETRA_E_ARG, "NULL backward output for a reversible stage");
       const float *nox[2] = {nullptr, nullptr};
-      unit_backward(u, recompute, nox, cx, tx, cd, td, st);
+      // the reconstructed dst half is the src of the unit processed next (recomputed
+      // from it): its bf16 operand comes out of the reconstruction kernel
+      Bf16Out ob = (recompute && i > 0 && units_[i - 1].d.kind == PETRA_UNIT_REV && units_[i - 1].src() == d)
+                       ? src_operand(units_[i - 1]) : Bf16Out{};
+      unit_backward(u, recompute, nox, cx, tx, cd, td, st, ob, ready && recompute);
+      ready = ob.p != nullptr;
       cx[d] = tx[d];
       rox[d] = false;
       cd[s] = td[s];
       rod[s] = false;
     } else {
+      ready = false;
       int slot = pop[i];
       const float *xin[2] = {u.fifo.slot0[slot]->as<float>(),
                              u.d.kind == PETRA_UNIT_DS ? u.fifo.slot1[slot]->as<float>() : nullptr};

@@ -82,6 +82,14 @@ struct Unit {
   int src() const { return 1 - d.dst_half; }
 };
 
+// bf16 copy of a stream half written by the kernel that produces it: the
+// tensor-core operand of the next unit's first convolution (pH > 0: zero-bordered
+// H x W layout of the halo kernel)
+struct Bf16Out {
+  __nv_bfloat16 *p = nullptr;
+  int pH = 0, pW = 0;
+};
+
 // one tick of a stage for the pipeline: forward (fmb) and/or backward (bmb)
 struct TickArgs {
   bool fwd = false, bwd = false;
@@ -115,6 +123,7 @@ class Stage {
   const std::vector<petra_tensor_info> &tensors() const { return tensors_; }
   int64_t version() const { return version_; }
   int fifo_depth() const;
+  void memory(petra_memory_report *r) const;
   int classes() const { return units_.back().d.classes; }
 
   void forward(uint64_t mb, const float *x1, const float *x2, float *o1, float *o2, cudaStream_t st);
@@ -136,6 +145,7 @@ class Stage {
   Shape in_, out_;
   bool is_last_ = false;
   bool tc_ = false;
+  size_t alloc_bytes_ = 0;   // every DevBuf created while this stage was being built
   int64_t n_params_ = 0, n_buffers_ = 0;
   std::vector<petra_tensor_info> tensors_;
   DevPtr theta_, v_, grad_, bufs_, acc_;     // acc_: Delta_j of Alg. 1 (k > 1 only)
@@ -191,15 +201,18 @@ class Stage {
   void conv_wgrad(Layer &L, const float *x, cudaStream_t st);
   void conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t st);
   void layer_stats(Layer &L, bool running, cudaStream_t st);
-  void branch_forward(std::vector<Layer> &phi, const float *x, bool running, cudaStream_t st);
+  void branch_forward(std::vector<Layer> &phi, const float *x, bool running, cudaStream_t st, bool ready0 = false);
   void layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, const float *dst_in, float *dst_out,
-                 cudaStream_t st);
+                 cudaStream_t st, Bf16Out ob = {});
   void branch_backward(std::vector<Layer> &phi, const float *x, const float *dy, const float *dst_in,
-                       float *dst_out, const float *addend, float *dx_out, cudaStream_t st);
+                       float *dst_out, const float *addend, float *dx_out, cudaStream_t st, Bf16Out ob = {});
+  Bf16Out src_operand(Unit &next);
 
-  void unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep, cudaStream_t st);
+  void unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep, cudaStream_t st, Bf16Out ob = {},
+                    bool src_ready = false);
   void unit_backward(Unit &u, bool recompute, const float *xin[2], const float *cur_x[2], float *out_x[2],
-                     const float *cur_d[2], float *out_d[2], cudaStream_t st);
+                     const float *cur_d[2], float *out_d[2], cudaStream_t st, Bf16Out ob = {},
+                     bool src_ready = false);
 };
 
 }  // namespace petra

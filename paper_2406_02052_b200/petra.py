@@ -79,6 +79,12 @@ class Stage:
         L.call("petra_stage_set_params", self.h, None if th is None else th.ctypes.data,
                None if vv is None else vv.ctypes.data, None if bf is None else bf.ctypes.data)
 
+    def memory(self):
+        """petra_stage_memory: device bytes by category (Table 3 accounting)."""
+        r = L.PetraMemoryReport()
+        L.call("petra_stage_memory", self.h, C.byref(r))
+        return {n: getattr(r, n) for n, _ in L.PetraMemoryReport._fields_}
+
     def get_grads(self):
         g = np.zeros(self.n_params, np.float32)
         L.call("petra_stage_get_grads", self.h, g.ctypes.data)

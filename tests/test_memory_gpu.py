@@ -1,0 +1,75 @@
+"""Table 3 accounting: petra_stage_memory
+reports every device byte a stage allocated, by category; each category is
+checked against its closed form from the stage's shapes."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from paper_2406_02052_b200 import Stage  # noqa: E402
+from paper_2406_02052_b200 import _lib as L  # noqa: E402
+from paper_2406_02052_b200 import models as PM  # noqa: E402
+
+
+def conv_weights(units):
+    n = 0
+    for u in units:
+        for ci, co, k, s in list(u.layers) + list(u.proj):
+            n += ci * co * k * k
+    return n
+
+
+@pytest.mark.parametrize("precision", [L.FP32, L.BF16_TC])
+@pytest.mark.parametrize("k", [1, 2])
+def test_stage_memory_categories(precision, k):
+    torch.cuda.set_device(0)
+    units = PM.revnet("revnet18")
+    counts = [5, 4, 4, 5]
+    specs = PM.stage_specs(units, counts, 8, (32, 32, 3), precision, accumulation_k=k)
+    ins, _ = PM.shapes(units, 8, 32, 32, 3)
+    i0 = 0
+    for j, spec in enumerate(specs, 1):
+        st = Stage(spec, 0)
+        m = st.memory()
+        us = units[i0:i0 + counts[j - 1]]
+        assert m["params"] == 4 * (st.n_params + st.n_buffers)
+        assert m["optimizer"] == 4 * st.n_params * (3 if k > 1 else 2)
+        want_sh = 2 * 2 * conv_weights(us) if precision == L.BF16_TC else 0
+        assert m["shadows"] == want_sh
+        # FIFO: capacity 2(J-j)+1 (1 in the final stage) copies of each non-reversible unit's input
+        cap = spec.fifo_capacity if j < len(specs) else 1
+        fifo = 0
+        for u, (B, H, W, C) in zip(us, ins[i0:i0 + counts[j - 1]]):
+            if u.kind == L.UNIT_STEM:
+                fifo += cap * B * H * W * C * 4
+            elif u.kind == L.UNIT_DS:
+                fifo += cap * 2 * B * H * W * C * 4
+        assert m["fifo"] == fifo
+        assert m["fifo_live"] == 0
+        assert m["total"] == m["params"] + m["optimizer"] + m["shadows"] + m["fifo"] + m["workspace"]
+        assert m["workspace"] > 0
+        st.close()
+        i0 += counts[j - 1]
+
+
+def test_fifo_live_bytes_follow_pushes():
+    """A forward pushes the input of every non-reversible unit; the backward pops it."""
+    torch.cuda.set_device(0)
+    units = PM.revnet("revnet18")
+    spec = PM.stage_specs(units, [5, 4, 4, 5], 4, (32, 32, 3), L.FP32)[1]   # DS + REV units
+    st = Stage(spec, 0)
+    B, H, W, C = (4,) + tuple(spec.in_shape)
+    x = [torch.randn(B, H, W, C, device="cuda") for _ in range(2)]
+    o = [torch.empty(st.out_shape, device="cuda") for _ in range(2)]
+    per = sum(2 * B * H * W * C * 4 for u in spec.units if u.kind == L.UNIT_DS)
+    st.forward(0, x[0], x[1], o[0], o[1])
+    st.forward(1, x[0], x[1], o[0], o[1])
+    torch.cuda.synchronize()
+    assert st.memory()["fifo_live"] == 2 * per
+    d = [torch.randn_like(o[0]) for _ in range(2)]
+    res = [torch.empty(B, H, W, C, device="cuda") for _ in range(4)]
+    st.backward(0, o[0], o[1], d[0], d[1], *res, 0.0)
+    torch.cuda.synchronize()
+    assert st.memory()["fifo_live"] == per
+    st.close()
