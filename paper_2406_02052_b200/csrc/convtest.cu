@@ -36,15 +36,21 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
   float *stats_part = stats ? part->as<float>() : nullptr;
   const bool a_pad = padded, b_pad = padded && mode == 2;
   std::function<void()> launch;
-  if (stem) {  // gathered-im2col tensor-core stem: fp32 image (and fp32 weights) read directly
+  if (stem) {  // gathered-im2col tensor-core stem: 4-channel bf16 copy of the image
     ws = dalloc(std::max<size_t>(16, stem_tc_workspace(g)));
     if (mode == 0) {
-      launch = [&] { stem_fwd_tc(g, da->as<float>(), db->as<float>(), dout->p, out16, stats_part, st); };
+      ab = dalloc(stem_operand_elems(g) * 2);
+      launch = [&] {
+        image_to_bf16x4(da->as<float>(), ab->as<__nv_bfloat16>(), g, st);
+        stem_fwd_tc(g, ab->as<__nv_bfloat16>(), db->as<float>(), dout->p, out16, stats_part, st);
+      };
     } else {
       ab = dalloc(na * 2);
+      bb = dalloc(stem_operand_elems(g) * 2);
       f32_to_bf16(da->as<float>(), ab->as<__nv_bfloat16>(), na, st);
+      image_to_bf16x4(db->as<float>(), bb->as<__nv_bfloat16>(), g, st);
       launch = [&] {
-        stem_wgrad_tc(g, ab->as<__nv_bfloat16>(), db->as<float>(), dout->as<float>(), ws->as<float>(), st);
+        stem_wgrad_tc(g, ab->as<__nv_bfloat16>(), bb->as<__nv_bfloat16>(), dout->as<float>(), ws->as<float>(), st);
       };
     }
   } else if (engine == 0) {

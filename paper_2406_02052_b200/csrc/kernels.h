@@ -43,19 +43,23 @@ int conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_p
 void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st);
 
 // ---------------------------------------------------------------- tcgen05 stem (small Ci)
-// Convolutions whose input has few channels (the stem: Ci = 3, k*k*Ci <= 256) run on
-// the tensor cores with a GATHERING producer: warps build the im2col rows of each
-// 128-pixel tile straight from the fp32 NHWC input into the 128B-swizzled smem
-// layout (no im2col tensor in HBM).  Forward and wgrad only (the stem input is data).
+// Convolutions whose input has few channels (the stem: Ci <= 4, k <= 8) run on the
+// tensor cores with a GATHERING producer: warps build the im2col rows of each
+// 128-pixel tile from a bf16 copy of the image padded to 4 channels (one 8-byte load
+// per pixel and kernel tap) into the 128B-swizzled smem layout (no im2col tensor in
+// HBM).  Forward and wgrad only (the stem input is data).
 bool stem_tc_supported(const ConvGeom &g);
 void stem_tc_prepare();  // kernel attributes (called by conv_tc_prepare)
 size_t stem_tc_workspace(const ConvGeom &g);
-// z = conv(bf16(x), bf16(w)) stored fp32 or (z_bf16) bf16; x, w fp32 as stored; fused BN
+size_t stem_operand_elems(const ConvGeom &g);  // bf16 elements of the 4-channel image copy
+// xq[pixel][0..3] = bf16(x[pixel][c]) (0 for c >= Ci): the stem's tensor-core operand
+void image_to_bf16x4(const float *x, __nv_bfloat16 *xq, const ConvGeom &g, cudaStream_t st);
+// z = conv(xq, bf16(w)) stored fp32 or (z_bf16) bf16; w fp32 as stored; fused BN
 // partials as conv_fwd_tc
-int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, void *z, bool z_bf16, float *stats_part,
-                cudaStream_t st);
-// dw (fp32) = sum_pixels dz_bf16 (x) bf16(x)
-void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const float *x, float *dw, float *ws,
+int stem_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *xq, const float *w, void *z, bool z_bf16,
+                float *stats_part, cudaStream_t st);
+// dw (fp32) = sum_pixels dz_bf16 (x) xq
+void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *xq, float *dw, float *ws,
                    cudaStream_t st);
 
 // ---------------------------------------------------------------- batch norm / coupling

@@ -55,6 +55,7 @@ template <int BN, int T, bool OUT16>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ HaloParams P) {
+  pdl_wait_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t B_BYTES = BN * 128;
@@ -194,6 +195,10 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               v[jj] += a4.x; v[jj + 1] += a4.y; v[jj + 2] += a4.z; v[jj + 3] += a4.w;
             }
           }
+          if (!valid) {  // padding row: never stored, zero for the statistics
+#pragma unroll
+            for (int jj = 0; jj < CW; ++jj) v[jj] = 0.f;
+          }
           // stage this lane's row (128 B) ...
           uint8_t *rp = ebuf + lane * kRowPitch;
 #pragma unroll
@@ -228,25 +233,18 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               *reinterpret_cast<uint4 *>(dst) = u;
             }
           }
-          __syncwarp();
-          if (P.stats) {
-#pragma unroll
-            for (int h = 0; h < CW; h += 16) {
-              float x[16], sq[16];
-#pragma unroll
-              for (int jj = 0; jj < 16; ++jj) {
-                x[jj] = valid ? v[h + jj] : 0.f;
-                sq[jj] = x[jj] * x[jj];
-              }
-              tc::colsum16(x, lane);
-              tc::colsum16(sq, lane);
-              if (!(lane & 1)) {
-                const int col = nt * BN + c + h + (lane >> 1);
-                my_stat[2 * col] += x[0];
-                my_stat[2 * col + 1] += sq[0];
-              }
+          if (P.stats) {  // statistics of z as stored (reading c24), from the staged rows
+            float s[2], sq[2];
+            tc::staged_colsums<OUT16, false>(ebuf, kRowPitch, lane, s, sq);
+            const int col = nt * BN + c + (OUT16 ? 2 * lane : lane);
+            my_stat[2 * col] += s[0];
+            my_stat[2 * col + 1] += sq[0];
+            if (OUT16) {
+              my_stat[2 * col + 2] += s[1];
+              my_stat[2 * col + 3] += sq[1];
             }
           }
+          __syncwarp();
         }
       }
       tc::tc_fence_before();
@@ -321,7 +319,7 @@ template <int BN, int T, bool OUT16>
 void launch(const CUtensorMap &ta, const CUtensorMap &tb, const HaloParams &P, cudaStream_t st) {
   const int work = (int)cdiv(P.Mp, 128 * T) * (P.N / BN);
   const size_t smem = fixed_smem() + 2 * (size_t)P.a_stage + (size_t)P.bstages * BN * 128;
-  conv_halo_kernel<BN, T, OUT16><<<std::min(work, kNumSMs), kThreads, smem, st>>>(ta, tb, P);
+  launch_k(conv_halo_kernel<BN, T, OUT16>, std::min(work, kNumSMs), kThreads, smem, st, ta, tb, P);
   PETRA_LAUNCH_CHECK();
 }
 

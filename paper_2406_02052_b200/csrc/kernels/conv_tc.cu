@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmW,
                const __grid_constant__ ConvTCParams P) {
+  pdl_wait_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t B_BYTES = BN * BK * 2;
@@ -255,29 +256,23 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               v[jj] += a4.x; v[jj + 1] += a4.y; v[jj + 2] += a4.z; v[jj + 3] += a4.w;
             }
           }
-          if constexpr (OUT16) {  // statistics of the values as stored (reading c24)
+          if (!valid) {  // padding row: never stored (outside the TMA box), zero for the statistics
 #pragma unroll
-            for (int jj = 0; jj < CW; ++jj) v[jj] = __bfloat162float(__float2bfloat16_rn(v[jj]));
+            for (int jj = 0; jj < CW; ++jj) v[jj] = 0.f;
           }
           acquire();
-          stage_row<OUT16>(ebuf + eb * kEpiBuf, lane, v);
+          uint8_t *staged = ebuf + eb * kEpiBuf;
+          stage_row<OUT16>(staged, lane, v);
           flush(&tmO, nt * BN + c, wj, wi, wb, true);
-          if (P.stats) {  // BN batch statistics of z, fused (sum and sum of squares per column)
-#pragma unroll
-            for (int h = 0; h < CW; h += 16) {
-              float x[16], sq[16];
-#pragma unroll
-              for (int jj = 0; jj < 16; ++jj) {
-                x[jj] = valid ? v[h + jj] : 0.f;
-                sq[jj] = x[jj] * x[jj];
-              }
-              tc::colsum16(x, lane);
-              tc::colsum16(sq, lane);
-              if (!(lane & 1)) {
-                const int col = nt * BN + c + h + (lane >> 1);
-                my_stat[2 * col] += x[0];
-                my_stat[2 * col + 1] += sq[0];
-              }
+          if (P.stats) {  // BN batch statistics of z as stored (reading c24), from the staged rows
+            float s[2], sq[2];
+            tc::staged_colsums<OUT16, true>(staged, 128, lane, s, sq);
+            const int col = nt * BN + c + (OUT16 ? 2 * lane : lane);
+            my_stat[2 * col] += s[0];
+            my_stat[2 * col + 1] += sq[0];
+            if (OUT16) {
+              my_stat[2 * col + 2] += s[1];
+              my_stat[2 * col + 3] += sq[1];
             }
           }
         }
@@ -309,6 +304,7 @@ __global__ void __launch_bounds__(1024) stats_finalize_kernel(const float *__res
                                                               float eps, float *__restrict__ mean,
                                                               float *__restrict__ invstd, float *__restrict__ rmean,
                                                               float *__restrict__ rvar, float mom) {
+  pdl_wait_trigger();
   __shared__ double sh[2][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
@@ -351,6 +347,7 @@ __global__ void __launch_bounds__(1024) stats_finalize_kernel(const float *__res
 // out[opix(m)][n] = addend + sum over splits of ws[s][m][n]  (fixed order: deterministic)
 template <bool OUT16>
 __global__ void splitk_out_kernel(const ConvTCParams P) {
+  pdl_wait_trigger();
   const int N4 = P.N / 4;
   const int64_t n = (int64_t)P.M * N4;
   const int GHW = P.Hb * P.Wb;
@@ -402,6 +399,7 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
 wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDZ,
                 const __grid_constant__ WgradParams P) {
+  pdl_wait_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t HALF_A = 64 * 64 * 2;  // one 64x64 bf16 box
@@ -540,6 +538,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
 }
 
 __global__ void splitk_sum_kernel(const float *__restrict__ part, int splits, int64_t n, float *__restrict__ out) {
+  pdl_wait_trigger();
   // 4 independent accumulators (4 loads in flight), combined in a fixed order: deterministic
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
@@ -559,6 +558,7 @@ __global__ void splitk_sum_kernel(const float *__restrict__ part, int splits, in
 // in `mask`: the stride-2 dgrad phases without taps, all in one launch (float4)
 __global__ void phase_fill_kernel(int B, int OH, int OW, int C, int mask, const float *__restrict__ addend,
                                   float *__restrict__ out) {
+  pdl_wait_trigger();
   const int C4 = C / 4;
   const int64_t n = (int64_t)B * OH * OW * C4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -718,11 +718,11 @@ void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParam
   const int work = (P.M / BM) * (P.N / BN) * P.splits;
   const CUtensorMap to = out_map(P.out, OUT16, P);
   const CUtensorMap tw = P.splits > 1 ? ws_map(P.ws, P.N, (int64_t)P.splits * P.M) : to;
-  conv_tc_kernel<BN, STAGES, OUT16><<<std::min(work, kNumSMs), kThreads, smem, st>>>(ta, tb, to, tw, P);
+  launch_k(conv_tc_kernel<BN, STAGES, OUT16>, std::min(work, kNumSMs), kThreads, smem, st, ta, tb, to, tw, P);
   PETRA_LAUNCH_CHECK();
   if (P.splits > 1) {
     int64_t n = (int64_t)P.M * P.N / 4;
-    splitk_out_kernel<OUT16><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs), 256, 0, st>>>(P);
+    launch_k(splitk_out_kernel<OUT16>, (unsigned)std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs), 256, 0, st, P);
     PETRA_LAUNCH_CHECK();
   }
 }
@@ -857,7 +857,7 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_pad, const __
     }
   if (empty_mask) {
     int64_t cnt = (int64_t)g.B * g.H * g.W * (g.Ci / 4);
-    phase_fill_kernel<<<(unsigned)std::min<int64_t>(cdiv(cnt, 256), 8 * kNumSMs), 256, 0, st>>>(
+    launch_k(phase_fill_kernel, (unsigned)std::min<int64_t>(cdiv(cnt, 256), 8 * kNumSMs), 256, 0, st, 
         g.B, g.H, g.W, g.Ci, empty_mask, addend, dx);
     PETRA_LAUNCH_CHECK();
   }
@@ -885,7 +885,7 @@ template <int BN, int STAGES>
 void launch_wgrad(const CUtensorMap &tx, const CUtensorMap &tdz, const WgradParams &P, cudaStream_t st) {
   size_t smem = (size_t)STAGES * (2 * 64 * 64 * 2 + BN * 64 * 2) + 1024 + 256;  // attribute: conv_tc_prepare
   int work = P.n_mt * P.n_nt * P.splits;
-  wgrad_tc_kernel<BN, STAGES><<<std::min(work, kNumSMs), kThreads, smem, st>>>(tx, tdz, P);
+  launch_k(wgrad_tc_kernel<BN, STAGES>, std::min(work, kNumSMs), kThreads, smem, st, tx, tdz, P);
   PETRA_LAUNCH_CHECK();
 }
 
@@ -941,7 +941,7 @@ int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const 
 
 void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float eps, float *mean, float *invstd,
                             float *rmean, float *rvar, float mom, cudaStream_t st) {
-  stats_finalize_kernel<<<(unsigned)cdiv(N, 32), 1024, 0, st>>>(part, P, N, M, eps, mean, invstd, rmean, rvar, mom);
+  launch_k(stats_finalize_kernel, (unsigned)cdiv(N, 32), 1024, 0, st, part, P, N, M, eps, mean, invstd, rmean, rvar, mom);
   PETRA_LAUNCH_CHECK();
 }
 
@@ -960,7 +960,7 @@ CUtensorMap tma_map(const void *base, CUtensorMapDataType dt, int rank, const cu
 }
 
 void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st) {
-  splitk_sum_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st>>>(part, splits, n, out);
+  launch_k(splitk_sum_kernel, (unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st, part, splits, n, out);
   PETRA_LAUNCH_CHECK();
 }
 

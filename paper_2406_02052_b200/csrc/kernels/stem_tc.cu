@@ -5,13 +5,15 @@
 // with the implicit im2col A[m][kk] = bf16(x[b][s*ho+kh-p][s*wo+kw-p][c]) (0 outside).
 //
 // The TMA im2col boxes of conv_tc.cu need 64 channels per tap; a 3-channel image
-// (K = 147 for the ImageNet 7x7/s2 stem, 27 for the CIFAR 3x3 stem) has 3.  Here
-// the A operand is GATHERED: 8 producer warps build each 128 x 64 (fwd, K-major) or
-// 64 x 128 (wgrad, MN-major) bf16 tile straight from the fp32 NHWC input into the
-// 128B-swizzled smem layout UMMA reads (a per-kk offset table in smem, an unchecked
-// fast path for interior pixels), then publish it with fence.proxy.async + mbarrier.
-// No im2col tensor ever touches HBM; the fp32 -> bf16 conversion of the image is
-// fused into the gather.  The weights (fwd) sit in smem for the whole persistent CTA.
+// (the ImageNet 7x7/s2 stem, the CIFAR 3x3 stem) has 3.  Here the A operand is
+// GATHERED from a bf16 copy of the image padded to 4 channels (8 bytes per pixel,
+// image_to_bf16x4): the reduction index is laid out per kernel row as
+// kk = kh*S + kw*4 + c (S = k*4 rounded up to a power of two; zero weights on the
+// padding slots), so every 4 consecutive kk are one pixel = one 8-byte load.  8
+// producer warps build each 128 x 64 (fwd, K-major) or 64 x 128 (wgrad, MN-major)
+// bf16 tile in the 128B-swizzled smem layout UMMA reads (an unchecked fast path for
+// interior pixels), then publish it with fence.proxy.async + mbarrier.  No im2col
+// tensor ever touches HBM.  The weights (fwd) sit in smem for the whole persistent CTA.
 // Warp roles: 0-7 gather producers, 8-11 epilogue (TMEM lane quarters 0-3), 12 MMA.
 #include <cudaTypedefs.h>
 
@@ -31,30 +33,19 @@ constexpr uint32_t kATile = 128 * 64 * 2;  // 16 KB
 constexpr int kMaxKK = 256;
 
 struct StemParams {
-  const float *x;  // [B][H][W][Ci] fp32
-  const float *w;  // [Co][K] fp32 (forward)
+  const uint2 *xq;  // [B][H][W] x 4 bf16 (the image, channels zero-padded to 4)
+  const float *w;   // [Co][k][k][Ci] fp32 (forward)
   int B, H, W, Ci, k, s, p, Ho, Wo;
-  int M, K, N;
-  int KB;                              // forward: 64-wide K blocks
+  int M, K, N;                         // K = k*k*Ci (the weight layout)
+  int S, shS, Kp;                      // padded reduction: kk = kh*S + kw*4 + c, Kp = k*S
+  int KB;                              // forward: 64-wide blocks of Kp
   int n_mt, KBtot, kb_per_split, splits;  // wgrad: kk tiles of 128, pixel blocks of 64, split-K
   void *out;                           // fwd: z fp32 or bf16 (OUT16); wgrad: fp32
   float *stats;
 };
 
-// kk -> (input offset relative to the receptive-field corner, (kh << 16) | kw); -1 = zero pad
-__device__ void fill_table(const StemParams &P, int2 *tab, int n) {
-  for (int kk = threadIdx.x; kk < n; kk += blockDim.x) {
-    if (kk < P.K) {
-      const int tap = kk / P.Ci, c = kk % P.Ci, kh = tap / P.k, kw = tap % P.k;
-      tab[kk] = make_int2((kh * P.W + kw) * P.Ci + c, (kh << 16) | kw);
-    } else {
-      tab[kk] = make_int2(0, -1);
-    }
-  }
-}
-
 struct Pixel {
-  int64_t base;
+  int64_t base;  // pixel index of the receptive-field corner (b, hi0, wi0)
   int hi0, wi0;
   bool valid, interior;
 };
@@ -67,27 +58,29 @@ __device__ __forceinline__ Pixel pixel(const StemParams &P, int m) {
   q.hi0 = ho * P.s - P.p;
   q.wi0 = wo * P.s - P.p;
   q.interior = q.hi0 >= 0 && q.wi0 >= 0 && q.hi0 + P.k <= P.H && q.wi0 + P.k <= P.W;
-  q.base = (((int64_t)b * P.H + q.hi0) * P.W + q.wi0) * P.Ci;
+  q.base = ((int64_t)b * P.H + q.hi0) * P.W + q.wi0;
   return q;
 }
 
-__device__ __forceinline__ float gather1(const StemParams &P, const Pixel &q, int2 t) {
-  if (!q.valid || t.y < 0) return 0.f;
-  if (!q.interior) {
-    const int hi = q.hi0 + (t.y >> 16), wi = q.wi0 + (t.y & 0xffff);
-    if (hi < 0 || hi >= P.H || wi < 0 || wi >= P.W) return 0.f;
-  }
-  return __ldg(P.x + q.base + t.x);
+// kk -> weight index (kh*k + kw)*Ci + c, or -1 on a padding slot
+__device__ __forceinline__ int real_kk(const StemParams &P, int kk) {
+  const int kh = kk >> P.shS, j = kk & (P.S - 1), kw = j >> 2, c = j & 3;
+  return (kh < P.k && kw < P.k && c < P.Ci) ? (kh * P.k + kw) * P.Ci + c : -1;
 }
 
-// 32 consecutive kk of one pixel -> 16 packed bf16 pairs
-__device__ __forceinline__ void gather32(const StemParams &P, const int2 *tab, int kk0, const Pixel &q,
-                                         uint32_t (&pk)[16]) {
+// 32 consecutive kk of one output pixel = 8 pixels of the 4-channel image: 8-byte loads
+__device__ __forceinline__ void gather32(const StemParams &P, int kk0, const Pixel &q, uint32_t (&pk)[16]) {
 #pragma unroll
-  for (int e = 0; e < 32; e += 2) {
-    const float v0 = gather1(P, q, tab[kk0 + e]), v1 = gather1(P, q, tab[kk0 + e + 1]);
-    __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
-    pk[e >> 1] = *reinterpret_cast<uint32_t *>(&h);
+  for (int g = 0; g < 8; ++g) {
+    const int kk = kk0 + 4 * g;
+    const int kh = kk >> P.shS, kw = (kk & (P.S - 1)) >> 2;
+    uint2 u = make_uint2(0u, 0u);
+    if (q.valid && kh < P.k && kw < P.k) {
+      const int hi = q.hi0 + kh, wi = q.wi0 + kw;
+      if (q.interior || (hi >= 0 && hi < P.H && wi >= 0 && wi < P.W)) u = __ldg(P.xq + q.base + kh * P.W + kw);
+    }
+    pk[2 * g] = u.x;
+    pk[2 * g + 1] = u.y;
   }
 }
 
@@ -112,13 +105,11 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
   uint64_t *tfull = empty + kStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  int2 *tab = reinterpret_cast<int2 *>(tmem_slot + 4);
-  float *sstat = reinterpret_cast<float *>(tab + kMaxKK);  // [4][N][2]
+  float *sstat = reinterpret_cast<float *>(tmem_slot + 4);  // [4][N][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (int)cdiv(P.M, 128);
-  fill_table(P, tab, P.KB * 64);
-  // weights fp32 [Co][K] -> bf16 K-major swizzled tiles (zero beyond K)
+  // weights fp32 [Co][K] -> bf16 K-major swizzled tiles in the padded kk order
   const int kchunks = P.KB * 8;
   for (int i = threadIdx.x; i < BN * kchunks; i += blockDim.x) {
     const int n = i / kchunks, r = i % kchunks, kb = r >> 3, c = r & 7;
@@ -126,8 +117,9 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
       const int kk = kb * 64 + c * 8 + e;
-      const float v0 = kk < P.K ? P.w[(int64_t)n * P.K + kk] : 0.f;
-      const float v1 = kk + 1 < P.K ? P.w[(int64_t)n * P.K + kk + 1] : 0.f;
+      const int r0 = real_kk(P, kk), r1 = real_kk(P, kk + 1);
+      const float v0 = r0 >= 0 ? P.w[(int64_t)n * P.K + r0] : 0.f;
+      const float v1 = r1 >= 0 ? P.w[(int64_t)n * P.K + r1] : 0.f;
       __nv_bfloat162 h = __floats2bfloat162_rn(v0, v1);
       pk[e >> 1] = *reinterpret_cast<uint32_t *>(&h);
     }
@@ -160,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
       const Pixel q = pixel(P, t * 128 + row);
       for (int kb = 0; kb < P.KB; ++kb) {
         uint32_t pk[16];
-        gather32(P, tab, kb * 64 + half * 32, q, pk);  // loads in flight before the wait
+        gather32(P, kb * 64 + half * 32, q, pk);  // loads in flight before the wait
         tc::mbar_wait(&empty[stage], phase ^ 1);
         store_row_chunks(sA + stage * kATile, row, half * 4, pk);
         tc::fence_proxy_async_smem();
@@ -281,11 +273,9 @@ stem_wgrad_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constan
   uint64_t *tfull = empty + kStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  int2 *tab = reinterpret_cast<int2 *>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_work = P.n_mt * P.splits;
-  fill_table(P, tab, P.n_mt * 128);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full[s], kProducers + 1);  // + the expect_tx arrival of the dz TMA
@@ -315,7 +305,7 @@ stem_wgrad_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constan
       for (int kb = kb0; kb < kb1; ++kb) {
         const Pixel q = pixel(P, kb * 64 + r);
         uint32_t pk[16];
-        gather32(P, tab, kk0, q, pk);
+        gather32(P, kk0, q, pk);
         tc::mbar_wait(&empty[stage], phase ^ 1);
         uint8_t *sa = smem + stage * STAGE_BYTES;
         if (threadIdx.x == 0) {
@@ -367,13 +357,14 @@ stem_wgrad_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constan
       const int acc = it & 1;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
-      const int r = mt * 128 + row;
+      const int kk = mt * 128 + row;
+      const int r = kk < P.Kp ? real_kk(P, kk) : -1;  // padding slots of kk carry no weight
       float *o = static_cast<float *>(P.out) + (int64_t)sp * P.N * P.K;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         float v[16];
         tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
-        if (r < P.K) {
+        if (r >= 0) {
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) o[(int64_t)(c + jj) * P.K + r] = v[jj];
         }
@@ -397,21 +388,40 @@ StemParams base_params(const ConvGeom &g) {
   P.M = (int)g.M();
   P.K = g.K();
   P.N = g.Co;
-  P.KB = (int)cdiv(P.K, 64);
+  P.S = 4;
+  P.shS = 2;
+  while (P.S < 4 * g.k) {
+    P.S <<= 1;
+    ++P.shS;
+  }
+  P.Kp = g.k * P.S;
+  P.KB = (int)cdiv(P.Kp, 64);
   return P;
 }
 
-size_t fwd_smem(int BN, int KB) {
-  return 1024 + (size_t)kStages * kATile + (size_t)KB * BN * 128 + 256 + kMaxKK * 8 + (size_t)4 * BN * 2 * 4;
+int padded_k(const ConvGeom &g) { return base_params(g).Kp; }
+
+__global__ void image_to_bf16x4_kernel(const float *__restrict__ x, uint2 *__restrict__ xq, int64_t pixels, int C) {
+  pdl_wait_trigger();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pixels; i += (int64_t)gridDim.x * blockDim.x) {
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < C; ++c) v[c] = x[i * C + c];
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+    xq[i] = make_uint2(*reinterpret_cast<uint32_t *>(&a), *reinterpret_cast<uint32_t *>(&b));
+  }
 }
-size_t wgrad_smem(int BN) { return 1024 + (size_t)kStages * (kATile + BN * 128) + 256 + kMaxKK * 8; }
+
+size_t fwd_smem(int BN, int KB) {
+  return 1024 + (size_t)kStages * kATile + (size_t)KB * BN * 128 + 256 + (size_t)4 * BN * 2 * 4;
+}
+size_t wgrad_smem(int BN) { return 1024 + (size_t)kStages * (kATile + BN * 128) + 256; }
 
 struct WPlan {
   int n_mt, KBtot, kb_per_split, splits;
 };
 WPlan wplan(const ConvGeom &g) {
   WPlan w{};
-  w.n_mt = (int)cdiv(g.K(), 128);
+  w.n_mt = (int)cdiv(padded_k(g), 128);
   w.KBtot = (int)cdiv(g.M(), 64);
   const int want = std::max(1, std::min(w.KBtot, (int)cdiv(kNumSMs, w.n_mt)));
   w.kb_per_split = (int)cdiv(w.KBtot, want);
@@ -440,8 +450,17 @@ void stem_tc_prepare() {
 }
 
 bool stem_tc_supported(const ConvGeom &g) {
-  return g.Ci >= 1 && g.Ci < 64 && g.K() <= kMaxKK && g.Co % 64 == 0 && g.Co <= 256 &&
-         g.M() < ((int64_t)1 << 31) && g.Min() * g.Ci < ((int64_t)1 << 31);
+  return g.Ci >= 1 && g.Ci <= 4 && g.k <= 8 && padded_k(g) <= kMaxKK && g.Co % 64 == 0 && g.Co <= 256 &&
+         g.M() < ((int64_t)1 << 31) && g.Min() < ((int64_t)1 << 31);
+}
+
+size_t stem_operand_elems(const ConvGeom &g) { return (size_t)g.Min() * 4; }
+
+void image_to_bf16x4(const float *x, __nv_bfloat16 *xq, const ConvGeom &g, cudaStream_t st) {
+  const int64_t pix = g.Min();
+  launch_k(image_to_bf16x4_kernel, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(pix, 256), 8 * kNumSMs)),
+           256, 0, st, x, reinterpret_cast<uint2 *>(xq), pix, g.Ci);
+  PETRA_LAUNCH_CHECK();
 }
 
 size_t stem_tc_workspace(const ConvGeom &g) {
@@ -450,12 +469,12 @@ size_t stem_tc_workspace(const ConvGeom &g) {
   return w.splits > 1 ? (size_t)w.splits * g.Co * g.K() * sizeof(float) : 0;
 }
 
-int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, void *z, bool z_bf16, float *stats_part,
-                cudaStream_t st) {
+int stem_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *xq, const float *w, void *z, bool z_bf16,
+                float *stats_part, cudaStream_t st) {
   if (!stem_tc_supported(g)) throw PetraError(PETRA_E_UNSUPPORTED, "stem_fwd_tc: geometry");
   stem_tc_prepare();
   StemParams P = base_params(g);
-  P.x = x;
+  P.xq = reinterpret_cast<const uint2 *>(xq);
   P.w = w;
   P.out = z;
   P.stats = stats_part;
@@ -474,13 +493,13 @@ int stem_fwd_tc(const ConvGeom &g, const float *x, const float *w, void *z, bool
   return stats_part ? grid : 0;
 }
 
-void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const float *x, float *dw, float *ws,
+void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *xq, float *dw, float *ws,
                    cudaStream_t st) {
   if (!stem_tc_supported(g)) throw PetraError(PETRA_E_UNSUPPORTED, "stem_wgrad_tc: geometry");
   stem_tc_prepare();
   StemParams P = base_params(g);
   WPlan wp = wplan(g);
-  P.x = x;
+  P.xq = reinterpret_cast<const uint2 *>(xq);
   P.n_mt = wp.n_mt;
   P.KBtot = wp.KBtot;
   P.kb_per_split = wp.kb_per_split;

@@ -157,6 +157,34 @@ __device__ __forceinline__ void colsum16(float (&x)[16], int lane) {
   x[0] += __shfl_xor_sync(0xffffffffu, x[0], 1);
 }
 
+// BN statistics of a warp's 32 staged output rows (each 128 bytes: 64 bf16 or 32 fp32
+// values), read back from the epilogue staging buffer instead of reduced across lanes:
+// lane L owns 4-byte word L of every row -- columns 2L, 2L+1 (bf16) or column L (fp32)
+// -- and sums it over the 32 rows (conflict-free: for a fixed row the lanes read 32
+// distinct banks).  Row r starts at buf + r * pitch; SWZ: 16-byte chunks in the
+// 128B-swizzled order of a TMA box (chunk c of row r at (c ^ (r & 7)) * 16).
+template <bool BF16, bool SWZ>
+__device__ __forceinline__ void staged_colsums(const uint8_t *buf, int pitch, int lane, float (&s)[2],
+                                               float (&q)[2]) {
+  s[0] = s[1] = q[0] = q[1] = 0.f;
+#pragma unroll 8
+  for (int r = 0; r < 32; ++r) {
+    const int chunk = SWZ ? ((lane >> 2) ^ (r & 7)) : (lane >> 2);
+    const uint32_t w = *reinterpret_cast<const uint32_t *>(buf + r * pitch + chunk * 16 + 4 * (lane & 3));
+    if constexpr (BF16) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&w));
+      s[0] += f.x;
+      q[0] = fmaf(f.x, f.x, q[0]);
+      s[1] += f.y;
+      q[1] = fmaf(f.y, f.y, q[1]);
+    } else {
+      const float f = __uint_as_float(w);
+      s[0] += f;
+      q[0] = fmaf(f, f, q[0]);
+    }
+  }
+}
+
 }  // namespace tc
 
 // host: 2-D TMA map of a row-major bf16 matrix [rows][K], 128B swizzle, box (64 K, box_rows)

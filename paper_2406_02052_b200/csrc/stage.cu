@@ -135,11 +135,13 @@ void Stage::alloc_layer(Layer &L, bool inner) {
     const bool s1k3 = halo && !L.is_stem && L.g.k == 3 && L.g.s == 1;
     L.xpad = s1k3 && conv_tc_supported(L.g, 0) && conv_halo_eligible(L.g.B, L.g.H, L.g.W, L.g.Ci, L.g.Co);
     L.dzpad = s1k3 && conv_tc_supported(L.g, 1) && conv_halo_eligible(L.g.B, L.g.Ho, L.g.Wo, L.g.Co, L.g.Ci);
-    const int64_t nxb = L.xpad ? (int64_t)L.g.B * (L.g.H + 2) * (L.g.W + 2) * L.g.Ci : L.g.Min() * L.g.Ci;
+    const int64_t nxb = L.xpad ? (int64_t)L.g.B * (L.g.H + 2) * (L.g.W + 2) * L.g.Ci
+                        : (L.is_stem && stem_tc_supported(L.g)) ? (int64_t)stem_operand_elems(L.g)
+                                                                 : L.g.Min() * L.g.Ci;
     const int64_t ndz = L.dzpad ? (int64_t)L.g.B * (L.g.Ho + 2) * (L.g.Wo + 2) * L.g.Co : n;
     L.dzb = dalloc(ndz * sizeof(__nv_bfloat16));
     if (L.dzpad) PETRA_CUDA(cudaMemset(L.dzb->p, 0, ndz * sizeof(__nv_bfloat16)));  // borders stay zero
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < 2 && !L.operand_of; ++c) {
       L.xb_[c] = dalloc(nxb * sizeof(__nv_bfloat16));
       if (L.xpad) PETRA_CUDA(cudaMemset(L.xb_[c]->p, 0, nxb * sizeof(__nv_bfloat16)));
     }
@@ -265,6 +267,12 @@ void Stage::build() {
     for (size_t l = 0; l < u.phi.size(); ++l) alloc_layer(u.phi[l], l + 1 < u.phi.size());
     if (u.d.kind == PETRA_UNIT_DS) {
       alloc_layer(u.pa, false);
+      // P_b reads the same tensor as the branch's first conv (x[src]): one bf16 operand
+      // for both when neither uses the zero-bordered layout (written by the branch first)
+      Layer &f = u.phi[0];
+      if (tc_ && conv_tc_supported(u.pb.g, 0) && conv_tc_supported(f.g, 0) && !f.xpad && !f.is_stem &&
+          f.g.H == u.pb.g.H && f.g.W == u.pb.g.W && f.g.Ci == u.pb.g.Ci)
+        u.pb.operand_of = &f;
       alloc_layer(u.pb, false);
     }
   }
@@ -495,9 +503,14 @@ static double conv_bytes(const ConvGeom &g, int esz) {
 
 void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready) {
   const float *w = theta_->as<float>() + L.w_off;
-  if (tc_ && stem_tc_supported(L.g)) {  // few input channels: gathered im2col, fp32 x read directly
-    ProfScope ps("conv_fwd_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 4));
-    L.stats_rows() = stem_fwd_tc(L.g, x, w, L.z()->p, L.z16, reinterpret_cast<float *>(part()->p), st);
+  if (tc_ && stem_tc_supported(L.g)) {  // few input channels: gathered im2col from a 4-channel bf16 copy
+    {
+      ProfScope pc("cvt_bf16", st, 0.0, (4.0 * L.g.Ci + 8.0) * (double)L.g.Min());
+      image_to_bf16x4(x, L.xb()->as<__nv_bfloat16>(), L.g, st);
+    }
+    ProfScope ps("conv_fwd_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2));
+    L.stats_rows() = stem_fwd_tc(L.g, L.xb()->as<__nv_bfloat16>(), w, L.z()->p, L.z16,
+                                 reinterpret_cast<float *>(part()->p), st);
     return;
   }
   bool tc = tc_ && conv_tc_supported(L.g, 0);
@@ -519,7 +532,7 @@ void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   float *dw = grad_->as<float>() + L.w_off;
   if (tc_ && stem_tc_supported(L.g)) {
     ProfScope ps("conv_wgrad_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2));
-    stem_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), x, dw, wgrad_ws()->as<float>(), st);
+    stem_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.xb()->as<__nv_bfloat16>(), dw, wgrad_ws()->as<float>(), st);
     return;
   }
   bool tc = tc_ && conv_tc_supported(L.g, 2);
@@ -660,7 +673,7 @@ Bf16Out Stage::src_operand(Unit &n) {
 }
 
 void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep, cudaStream_t st, Bf16Out ob,
-                         bool src_ready) {
+                         bool src_ready, int ob_half) {
   const float *th = theta_->as<float>();
   switch (u.d.kind) {
     case PETRA_UNIT_REV: {
@@ -677,17 +690,18 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       branch_forward(u.phi, xs, keep, st);
       conv_fwd(u.pa, xd, st);
       layer_stats(u.pa, keep, st);
-      conv_fwd(u.pb, xs, st);
+      conv_fwd(u.pb, xs, st, u.pb.operand_of != nullptr);  // operand shared with the branch's first conv
       layer_stats(u.pb, keep, st);
       Layer &L = u.phi.back();
       int64_t M = L.g.M();
       int C = L.g.Co;
+      const Bf16Out od = ob_half == u.dst() ? ob : Bf16Out{}, os = ob_half == u.src() ? ob : Bf16Out{};
       apply_bn(M, C, u.pa.z()->p, u.pa.z16, C, 0, u.pa.mean()->as<float>(), u.pa.invstd()->as<float>(),
                              th + u.pa.g_off, th + u.pa.b_off, 0, 1.f, nullptr, out[u.dst()], nullptr, st);
-      apply_bn(M, C, L.z()->p, L.z16, C, 0, L.mean()->as<float>(), L.invstd()->as<float>(),
-                             th + L.g_off, th + L.b_off, 1, 1.f, out[u.dst()], out[u.dst()], nullptr, st);
+      apply_bn(M, C, L.z()->p, L.z16, C, 0, L.mean()->as<float>(), L.invstd()->as<float>(), th + L.g_off,
+               th + L.b_off, 1, 1.f, out[u.dst()], out[u.dst()], od.p, st, od.pH, od.pW);
       apply_bn(M, C, u.pb.z()->p, u.pb.z16, C, 0, u.pb.mean()->as<float>(), u.pb.invstd()->as<float>(),
-                             th + u.pb.g_off, th + u.pb.b_off, 0, 1.f, nullptr, out[u.src()], nullptr, st);
+               th + u.pb.g_off, th + u.pb.b_off, 0, 1.f, nullptr, out[u.src()], os.p, st, os.pH, os.pW);
       break;
     }
     case PETRA_UNIT_STEM: {
@@ -736,7 +750,7 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
         branch_forward(u.phi, xs, true, st);
         conv_fwd(u.pa, xd, st);
         layer_stats(u.pa, true, st);
-        conv_fwd(u.pb, xs, st);
+        conv_fwd(u.pb, xs, st, u.pb.operand_of != nullptr);
         layer_stats(u.pb, true, st);
       }
       const float *dyd = cur_d[u.dst()], *dys = cur_d[u.src()];
@@ -862,7 +876,12 @@ void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *
       int slot = push[i];
       copy_d2d(u.fifo.slot0[slot]->as<float>(), cur[0], u.in.numel(), st);
       if (u.d.kind == PETRA_UNIT_DS) copy_d2d(u.fifo.slot1[slot]->as<float>(), cur[1], u.in.numel(), st);
-      unit_forward(u, cur, tgt, keep, st);
+      // a DS unit writes the bf16 operand of the next reversible unit's src half too
+      Bf16Out ob = (u.d.kind == PETRA_UNIT_DS && i + 1 < n && units_[i + 1].d.kind == PETRA_UNIT_REV)
+                       ? src_operand(units_[i + 1]) : Bf16Out{};
+      const int obh = ob.p ? units_[i + 1].src() : -1;
+      unit_forward(u, cur, tgt, keep, st, ob, false, obh);
+      ready = ob.p != nullptr;
       cur[0] = tgt[0];
       cur[1] = tgt[1];
       ro[0] = ro[1] = false;

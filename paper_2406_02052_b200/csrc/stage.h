@@ -48,7 +48,8 @@ struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
   DevPtr &a() { return a_[*ctx]; }
   DevPtr &mean() { return mean_[*ctx]; }
   DevPtr &invstd() { return invstd_[*ctx]; }
-  DevPtr &xb() { return xb_[*ctx]; }
+  Layer *operand_of = nullptr;               // shares that layer's bf16 input operand (same input tensor)
+  DevPtr &xb() { return operand_of ? operand_of->xb() : xb_[*ctx]; }
   int &stats_rows() { return stats_rows_[*ctx]; }
   DevPtr dz, da, dzb;                        // backward-only workspace
   DevPtr w_bf16, wt_bf16;                    // bf16 shadows of the live weights
@@ -209,7 +210,7 @@ class Stage {
   Bf16Out src_operand(Unit &next);
 
   void unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep, cudaStream_t st, Bf16Out ob = {},
-                    bool src_ready = false);
+                    bool src_ready = false, int ob_half = -1);
   void unit_backward(Unit &u, bool recompute, const float *xin[2], const float *cur_x[2], float *out_x[2],
                      const float *cur_d[2], float *out_d[2], cudaStream_t st, Bf16Out ob = {},
                      bool src_ready = false);
