@@ -273,9 +273,22 @@ def run_ours(a):
     else:
         bound, peak, unit, ach = "hbm", peaks["hbm_gbs"], "GB/s", top["bytes"] / top["ms"] / 1e6
         peak_src = f"hbm_gbs ({src})"
+    traffic, traffic_src = None, None
+    tfile = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", f"traffic_{a.model}.json")
+    if os.path.exists(tfile) and prec == L.BF16_TC:
+        with open(tfile) as f:
+            tj = json.load(f)
+        if name in tj["categories"]:
+            traffic = round(tj["categories"][name]["bytes_per_launch"])
+            traffic_src = (f"dram__bytes_read.sum + dram__bytes_write.sum per logical launch, ncu launch list "
+                           f"({os.path.relpath(tfile)}; {tj['cache']})")
     roof = {"bound": bound, "kernel": name, "achieved": round(ach, 2), "peak": peak, "unit": unit,
-            "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_src,
-            "share_of_step": round(top["ms"] / tot, 3), "launches_per_step": top["launches"] / a.steps}
+            "frac": round(ach / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_bytes_per_launch": round(top["bytes"] / top["launches"]), "peak_source": peak_src,
+            "share_of_step": round(top["ms"] / tot, 3), "launches_per_step": top["launches"] / a.steps,
+            "method": ("profiled replay of K further steps with every stage and both directions serialised on "
+                       "the launch stream: CUDA events around each logical kernel time it alone (warm L2)"),
+            "serial_ms_per_step": round(tot / a.steps, 4)}
     kernels = [{"name": p["name"], "share": round(p["ms"] / tot, 3), "launches": p["launches"],
                 "ms_per_step": round(p["ms"] / a.steps, 4),
                 "tflops": round(p["flops"] / p["ms"] / 1e9, 2) if p["flops"] else None,

@@ -335,7 +335,7 @@ petra_status petra_conv_bench(int32_t mode, int32_t engine, const petra_conv_geo
 /* Which engine the library uses for a convolution pass at a given precision:
  * 0 = SIMT fp32, 1 = tcgen05 bf16 (operands rounded to bf16, fp32 accumulation) --
  * the TMA implicit GEMM for Ci, Co multiples of 64, or, for few input channels (the
- * stem: Ci < 64, k*k*Ci <= 256, Co in {64, 128, 256}; forward and wgrad), the
+ * stem: Ci <= 4, k <= 8, Co in {64, 128, 256}; forward and wgrad), the
  * gathered-im2col kernel. */
 int32_t petra_conv_engine(const petra_conv_geom *g, int32_t mode, int32_t precision);
 int64_t petra_launch_count(void);

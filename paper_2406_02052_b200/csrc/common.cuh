@@ -45,6 +45,8 @@ __device__ __forceinline__ void pdl_wait_trigger() {
 }
 
 bool pdl_enabled();
+// tuning knob from the environment (read once per name; default if unset)
+int env_int(const char *name, int dflt);
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {

@@ -80,7 +80,9 @@ inline RedGeom red_geom(int64_t M, int C, int RT) {
   }
   g.RG = RT / g.TPR;
   g.ctiles = (int)cdiv(C, g.CT);
-  int64_t want = std::max<int64_t>(1, kNumSMs / g.ctiles);  // one wave: few partials to merge
+  // one full-occupancy wave (2048 threads per SM): enough loads in flight per SM for
+  // small tensors, and few partials to merge
+  int64_t want = std::max<int64_t>(1, (int64_t)kNumSMs * (2048 / RT) / g.ctiles);
   g.nrb = (int)std::max<int64_t>(1, std::min<int64_t>(want, cdiv(M, 4 * g.RG)));
   g.rpb = cdiv(M, g.nrb);
   g.nrb = (int)cdiv(M, g.rpb);
@@ -272,22 +274,34 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
       mu[k] = mean[cz + k];
       be[k] = beta[cz + k];
     }
-    for (int64_t i = i0, m = i0 / C4; i < n; i += stride, m += dm) {
-      const float4 zv = ld4(z, m * ldz + cz);
-      float4 o;
-      float *op = &o.x;
+    // 4 rows per trip, all loads issued before any use (memory-level parallelism)
+    for (int64_t i = i0, m = i0 / C4; i < n; i += 4 * stride, m += 4 * dm) {
+      float4 zv[4], av[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float y = fmaf(a[k], f4(zv, k) - mu[k], be[k]);
-        if (relu) y = y > 0.f ? y : 0.f;
-        op[k] = sign * y;
+      for (int u = 0; u < 4; ++u) {
+        if (i + u * stride < n) {
+          zv[u] = ld4(z, (m + u * dm) * ldz + cz);
+          av[u] = acc ? ld4(acc, (m + u * dm) * C + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
-      if (acc) {
-        const float4 av = ld4(acc, m * C + c);
-        o.x += av.x; o.y += av.y; o.z += av.z; o.w += av.w;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i + u * stride >= n) break;
+        const int64_t mu_ = m + u * dm;
+        float4 o;
+        float *op = &o.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float y = fmaf(a[k], f4(zv[u], k) - mu[k], be[k]);
+          if (relu) y = y > 0.f ? y : 0.f;
+          op[k] = sign * y;
+        }
+        if (acc) {
+          o.x += av[u].x; o.y += av[u].y; o.z += av[u].z; o.w += av[u].w;
+        }
+        if (out) st4(out, mu_ * C + c, o);
+        if (out_bf16) st4(out_bf16, pad_row(mu_, pH, pW) * C + c, o);
       }
-      if (out) st4(out, m * C + c, o);
-      if (out_bf16) st4(out_bf16, pad_row(m, pH, pW) * C + c, o);
     }
     return;
   }
@@ -456,20 +470,31 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
       db[k] = dbeta[c + k] * invM;
       dg[k] = dgamma[c + k];
     }
-    for (int64_t i = i0, m = i0 / C4; i < n; i += stride, m += dm) {
-      const float4 zv = ld4(z, m * C + c);
-      float4 g4 = load_dy4(dy0, dy1, cs, C, m, c);
-      float4 o;
-      float *op = &o.x, *gp = &g4.x;
+    for (int64_t i = i0, m = i0 / C4; i < n; i += 4 * stride, m += 4 * dm) {  // 4 rows per trip
+      float4 zv[4], gv[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float xh = (f4(zv, k) - mu[k]) * is[k];
-        float g = gp[k];
-        if (relu && !(fmaf(ga[k], xh, be[k]) > 0.f)) g = 0.f;
-        op[k] = ga[k] * is[k] * (g - db[k] - xh * dg[k] * invM);
+      for (int u = 0; u < 4; ++u) {
+        if (i + u * stride < n) {
+          zv[u] = ld4(z, (m + u * dm) * C + c);
+          gv[u] = load_dy4(dy0, dy1, cs, C, m + u * dm, c);
+        }
       }
-      if (dz) st4(dz, m * C + c, o);
-      if (dz_bf16) st4(dz_bf16, pad_row(m, pH, pW) * C + c, o);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i + u * stride >= n) break;
+        const int64_t mu_ = m + u * dm;
+        float4 o;
+        float *op = &o.x, *gp = &gv[u].x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float xh = (f4(zv[u], k) - mu[k]) * is[k];
+          float g = gp[k];
+          if (relu && !(fmaf(ga[k], xh, be[k]) > 0.f)) g = 0.f;
+          op[k] = ga[k] * is[k] * (g - db[k] - xh * dg[k] * invM);
+        }
+        if (dz) st4(dz, mu_ * C + c, o);
+        if (dz_bf16) st4(dz_bf16, pad_row(mu_, pH, pW) * C + c, o);
+      }
     }
     return;
   }

@@ -24,7 +24,8 @@
 namespace petra {
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;                     // two epilogue warps per TMEM lane quarter
+constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr int kBoxMax = 256;                     // TMA box height limit (rows per halo load)
 constexpr uint32_t kRowPitch = 144;              // epilogue staging row pitch (bank spread)
 constexpr uint32_t kEpiWarp = 32 * kRowPitch;
@@ -70,8 +71,8 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint64_t *tfull = bempty + kMaxBStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  uint8_t *sepi = reinterpret_cast<uint8_t *>(afull) + 512;       // [4 warps][32 rows x 144 B]
-  float *sstat = reinterpret_cast<float *>(sepi + 4 * kEpiWarp);  // [4][N][2]
+  uint8_t *sepi = reinterpret_cast<uint8_t *>(afull) + 512;       // [8 warps][32 rows x 144 B]
+  float *sstat = reinterpret_cast<float *>(sepi + kEpiWarps * kEpiWarp);  // [4 lane quarters][N][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_nt = P.N / BN;
@@ -90,7 +91,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 4);
+      tc::mbar_init(&tempty[a], kEpiWarps);
     }
     tc::fence_mbar_init();
     tc::tma_prefetch(&tmA);
@@ -159,14 +160,16 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tc::umma_commit(&tfull[acc]);
       }
     }
-  } else {  // ---------------- epilogue warps 2..5
+  } else {  // ---------------- epilogue warps 2..9 (two per TMEM lane quarter, alternating column chunks)
     const int q = warp & 3;
+    const int hc = (warp - 2) >> 2;
     const int row = q * 32 + lane;
     float *my_stat = sstat + (size_t)q * P.N * 2;
-    uint8_t *ebuf = sepi + q * kEpiWarp;
-    if (P.stats)
-      for (int i = lane; i < 2 * P.N; i += 32) my_stat[i] = 0.f;
-    __syncwarp();
+    uint8_t *ebuf = sepi + (warp - 2) * kEpiWarp;
+    if (P.stats) {  // the two warps of a lane quarter share its (column-disjoint) sums
+      for (int i = (warp - 2) * 32 + lane; i < 8 * P.N; i += kEpiWarps * 32) sstat[i] = 0.f;
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+    }
     constexpr int ES = OUT16 ? 2 : 4;
     constexpr int CW = 128 / ES;  // columns per 128-byte chunk
     int it = 0;
@@ -184,7 +187,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int64_t opix = valid ? ((int64_t)b * P.H + hp - 1) * P.W + wp - 1 : -1;
         const float *arow = (valid && P.addend) ? P.addend + opix * P.N + nt * BN : nullptr;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += CW) {
+        for (int c = CW * hc; c < BN; c += 2 * CW) {
           float v[CW];
 #pragma unroll
           for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
@@ -252,9 +255,9 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
     if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       float *g = P.stats + (size_t)blockIdx.x * P.N * 2;
-      for (int i = q * 32 + lane; i < 2 * P.N; i += 128)
+      for (int i = (warp - 2) * 32 + lane; i < 2 * P.N; i += kEpiWarps * 32)
         g[i] = (sstat[i] + sstat[2 * P.N + i]) + (sstat[4 * P.N + i] + sstat[6 * P.N + i]);
     }
   }
@@ -265,7 +268,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 }
 
-size_t fixed_smem() { return 1024 + 512 + 4 * kEpiWarp + (size_t)kMaxStatN * 32; }
+size_t fixed_smem() { return 1024 + 512 + kEpiWarps * kEpiWarp + (size_t)kMaxStatN * 32; }
 // the halo of T tiles (128*T + 2*(W+3) rows) as equal TMA boxes of <= 256 rows, each a
 // multiple of 8 rows so every box starts 1 KB-aligned
 void halo_rows(int T, int W, int &box_rows, int &HR) {

@@ -9,7 +9,8 @@
 //
 // Design (B200-first):
 //  * persistent warp-specialised CTAs (one per SM): warp 0 = TMA producer, warp 1 =
-//    tcgen05.mma issuer (one thread) + TMEM owner, warps 2-5 = epilogue;
+//    tcgen05.mma issuer (one thread) + TMEM owner, warps 2-9 = epilogue (two warps per
+//    TMEM lane quarter, alternating 128-byte column chunks);
 //  * A (activations) is an implicit im2col: one 4-D TMA box per (tap, 64-channel
 //    block), coordinates shifted by the tap offset, stride s via TMA traversal
 //    strides, halo / padding from TMA's zero fill of out-of-bounds coordinates.  The
@@ -32,7 +33,9 @@ namespace petra {
 namespace {
 
 constexpr int BM = 128, BK = 64;
-constexpr int kThreads = 192;  // 6 warps
+constexpr int kThreads = 192;      // wgrad: 6 warps (producer, MMA, 4 epilogue)
+constexpr int kEpiWarps = 8;       // conv: two epilogue warps per TMEM lane quarter (column halves)
+constexpr int kConvThreads = (2 + kEpiWarps) * 32;
 constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr int kMaxTaps = 9;
 constexpr int kMaxStatN = 512;  // widest conv output with fused BN statistics
@@ -59,7 +62,7 @@ struct ConvTCParams {
 // fences, and lane 0 issues the TMA store while the warp fills the other buffer.
 // Out-of-bounds box elements (padding rows of the padded grid) are not written.
 constexpr uint32_t kEpiBuf = 32 * 128;
-constexpr uint32_t kEpiBytes = 4 * 2 * kEpiBuf;
+constexpr uint32_t kEpiBytes = kEpiWarps * 2 * kEpiBuf;
 
 // row `lane` of a 32 x 128 B swizzled box: 32 fp32 or 64 bf16 values
 template <bool BF16>
@@ -85,7 +88,7 @@ __device__ __forceinline__ void stage_row(uint8_t *buf, int lane, const float *v
 }
 
 template <int BN, int STAGES, bool OUT16>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kConvThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmW,
                const __grid_constant__ ConvTCParams P) {
@@ -99,8 +102,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  uint8_t *sepi = smem + STAGES * STAGE_BYTES + 1024;      // [4 warps][2][32 x 128 B] epilogue staging
-  float *sstat = reinterpret_cast<float *>(sepi + kEpiBytes);  // [4 warps][N][2] BN partial sums (fused stats)
+  uint8_t *sepi = smem + STAGES * STAGE_BYTES + 1024;      // [8 warps][2][32 x 128 B] epilogue staging
+  float *sstat = reinterpret_cast<float *>(sepi + kEpiBytes);  // [4 lane quarters][N][2] BN partial sums
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_n = P.N / BN;
@@ -124,7 +127,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 4);
+      tc::mbar_init(&tempty[a], kEpiWarps);
     }
     tc::fence_mbar_init();
     tc::tma_prefetch(&tmA);
@@ -185,14 +188,16 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else {  // ---------------- epilogue warps 2..5
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int q = warp & 3;             // TMEM lane quarter this warp may access
+    const int hc = (warp - 2) >> 2;     // column half: chunks hc, hc + 2, ... of each tile
     const int row = q * 32 + lane;
     float *my_stat = sstat + (size_t)q * P.N * 2;
-    uint8_t *ebuf = sepi + q * 2 * kEpiBuf;
+    uint8_t *ebuf = sepi + (warp - 2) * 2 * kEpiBuf;
     int eb = 0;  // staging buffer to fill next
-    if (P.stats)
-      for (int i = lane; i < 2 * P.N; i += 32) my_stat[i] = 0.f;
-    __syncwarp();
+    if (P.stats) {  // the two warps of a lane quarter share its (column-disjoint) sums
+      for (int i = (warp - 2) * 32 + lane; i < 8 * P.N; i += kEpiWarps * 32) sstat[i] = 0.f;
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+    }
     if (lane == 0) {
       tc::tma_prefetch(&tmO);
       tc::tma_prefetch(&tmW);
@@ -224,7 +229,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int m = mt * BM + row;
       if (P.splits > 1) {  // fp32 partial of this K split, GEMM-row order -> ws[split][M][N]
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 32 * hc; c < BN; c += 64) {
           float v[32];
           tc::tmem_ld16(trow + c, *reinterpret_cast<float(*)[16]>(v));
           tc::tmem_ld16(trow + c + 16, *reinterpret_cast<float(*)[16]>(v + 16));
@@ -245,7 +250,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int wb = m0w / GHW, wr = m0w % GHW, wi = wr / P.Wb, wj = wr % P.Wb;
         constexpr int CW = OUT16 ? 64 : 32;  // columns per 128-byte staged row
 #pragma unroll 1
-        for (int c = 0; c < BN; c += CW) {
+        for (int c = CW * hc; c < BN; c += 2 * CW) {
           float v[CW];
 #pragma unroll
           for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
@@ -283,9 +288,9 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     if (lane == 0) tc::bulk_wait_all();
     if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       float *g = P.stats + (size_t)blockIdx.x * P.N * 2;
-      for (int i = q * 32 + lane; i < 2 * P.N; i += 128)
+      for (int i = (warp - 2) * 32 + lane; i < 2 * P.N; i += kEpiWarps * 32)
         g[i] = (sstat[i] + sstat[2 * P.N + i]) + (sstat[4 * P.N + i] + sstat[6 * P.N + i]);
     }
   }
@@ -666,8 +671,9 @@ ConvPlan conv_plan(int M, int N, int KB) {
     if (mt * (N / bn) >= kNumSMs) break;
   }
   const int tiles = mt * (N / p.BN);
-  if (tiles * 4 < kNumSMs * 3) {  // under 75% of one wave: split K
-    int want = std::max(1, (kNumSMs + tiles / 2) / tiles);
+  static const int split_max = env_int("PETRA_SPLITK_MAX", 1 << 20);
+  if (tiles * 4 < kNumSMs * 3 && split_max > 1) {  // under 75% of one wave: split K
+    int want = std::max(1, std::min(split_max, (kNumSMs + tiles / 2) / tiles));
     want = std::min(want, std::max(1, KB / 4));  // at least 4 K-blocks per split
     p.kb_per_split = (int)cdiv(KB, want);
     p.splits = (int)cdiv(KB, p.kb_per_split);
@@ -706,7 +712,7 @@ CUtensorMap ws_map(float *ws, int N, int64_t rows) {
   return make_map(ws, 2, dims, st, box, el, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
-constexpr int conv_stages(int BN) { return BN == 256 ? 3 : (BN == 128 ? 5 : 6); }
+constexpr int conv_stages(int BN) { return BN == 256 ? 3 : (BN == 128 ? 4 : 6); }
 constexpr size_t conv_smem(int BN, size_t stat_bytes) {
   return 1024 + (size_t)conv_stages(BN) * (A_BYTES + BN * BK * 2) + 1024 + kEpiBytes + stat_bytes;
 }
@@ -718,7 +724,7 @@ void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParam
   const int work = (P.M / BM) * (P.N / BN) * P.splits;
   const CUtensorMap to = out_map(P.out, OUT16, P);
   const CUtensorMap tw = P.splits > 1 ? ws_map(P.ws, P.N, (int64_t)P.splits * P.M) : to;
-  launch_k(conv_tc_kernel<BN, STAGES, OUT16>, std::min(work, kNumSMs), kThreads, smem, st, ta, tb, to, tw, P);
+  launch_k(conv_tc_kernel<BN, STAGES, OUT16>, std::min(work, kNumSMs), kConvThreads, smem, st, ta, tb, to, tw, P);
   PETRA_LAUNCH_CHECK();
   if (P.splits > 1) {
     int64_t n = (int64_t)P.M * P.N / 4;
@@ -875,7 +881,8 @@ WgradPlan wgrad_plan(const ConvGeom &g) {
   w.t = tiling(g.B, g.Ho, g.Wo, 64);
   w.KBtot = (int)(w.t.M() / 64);
   int tiles = w.n_mt * w.n_nt;
-  int want = std::max(1, std::min(w.KBtot, (int)cdiv(kNumSMs, tiles)));
+  static const int ctas = env_int("PETRA_WGRAD_CTAS", kNumSMs);  // CTAs the split-K aims to fill
+  int want = std::max(1, std::min(w.KBtot, (int)cdiv(ctas, tiles)));
   w.kb_per_split = (int)cdiv(w.KBtot, want);
   w.splits = (int)cdiv(w.KBtot, w.kb_per_split);
   return w;

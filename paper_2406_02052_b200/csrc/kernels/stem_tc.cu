@@ -450,7 +450,7 @@ void stem_tc_prepare() {
 }
 
 bool stem_tc_supported(const ConvGeom &g) {
-  return g.Ci >= 1 && g.Ci <= 4 && g.k <= 8 && padded_k(g) <= kMaxKK && g.Co % 64 == 0 && g.Co <= 256 &&
+  return g.Ci >= 1 && g.Ci <= 4 && g.k <= 8 && padded_k(g) <= kMaxKK && (g.Co == 64 || g.Co == 128 || g.Co == 256) &&
          g.M() < ((int64_t)1 << 31) && g.Min() < ((int64_t)1 << 31);
 }
 

@@ -138,7 +138,7 @@ void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labe
   for (int j = 1; j <= J_; ++j) {
     if (!sched_.local(j)) continue;
     Stage &s = *stages_[j];
-    st = streams_[j];
+    st = Prof::enabled ? caller : streams_[j];  // profiled replay: one stream, kernels timed alone
     PETRA_CUDA(cudaStreamWaitEvent(st, start_, 0));
     const Schedule::Step &sp = steps[j];
     TickArgs a;

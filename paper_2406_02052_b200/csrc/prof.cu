@@ -15,6 +15,11 @@ std::vector<std::string> Prof::names;
 std::vector<cudaEvent_t> Prof::pool;
 static size_t g_pool_next = 0;
 
+int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char *e = getenv("PETRA_PDL");

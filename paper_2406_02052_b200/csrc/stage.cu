@@ -497,8 +497,14 @@ static void apply_bn(int64_t M, int C, const void *z, bool z16, int ldz, int zc0
 }
 
 static double conv_flops(const ConvGeom &g) { return 2.0 * (double)g.M() * g.Co * g.K(); }
-static double conv_bytes(const ConvGeom &g, int esz) {
-  return (double)esz * ((double)g.Min() * g.Ci + (double)g.Co * g.K()) + 4.0 * (double)g.M() * g.Co;
+// algorithmic HBM bytes of one convolution pass: operands once (elements of size esz),
+// the result once (out_es bytes per element) and the addend once (dgrad)
+enum { PASS_FWD = 0, PASS_DGRAD = 1, PASS_WGRAD = 2 };
+static double conv_bytes(const ConvGeom &g, int esz, int pass, int out_es, bool addend = false) {
+  const double x = (double)g.Min() * g.Ci, w = (double)g.Co * g.K(), z = (double)g.M() * g.Co;
+  if (pass == PASS_FWD) return esz * (x + w) + out_es * z;
+  if (pass == PASS_DGRAD) return esz * (z + w) + (out_es + (addend ? 4.0 : 0.0)) * x;
+  return esz * (x + z) + out_es * w;
 }
 
 void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready) {
@@ -508,7 +514,7 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
       ProfScope pc("cvt_bf16", st, 0.0, (4.0 * L.g.Ci + 8.0) * (double)L.g.Min());
       image_to_bf16x4(x, L.xb()->as<__nv_bfloat16>(), L.g, st);
     }
-    ProfScope ps("conv_fwd_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2));
+    ProfScope ps("conv_fwd_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2, PASS_FWD, L.z16 ? 2 : 4));
     L.stats_rows() = stem_fwd_tc(L.g, L.xb()->as<__nv_bfloat16>(), w, L.z()->p, L.z16,
                                  reinterpret_cast<float *>(part()->p), st);
     return;
@@ -519,7 +525,8 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
     if (L.xpad) f32_to_bf16_padded(x, L.xb()->as<__nv_bfloat16>(), L.g.B, L.g.H, L.g.W, L.g.Ci, st);
     else f32_to_bf16(x, L.xb()->as<__nv_bfloat16>(), L.g.Min() * L.g.Ci, st);
   }
-  ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
+  ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g),
+               conv_bytes(L.g, tc ? 2 : 4, PASS_FWD, L.z16 ? 2 : 4));
   if (tc) {
     L.stats_rows() = conv_fwd_tc(L.g, L.xb()->as<__nv_bfloat16>(), L.xpad, L.w_bf16->as<__nv_bfloat16>(), L.z()->p, L.z16,
                                wgrad_ws()->as<float>(), reinterpret_cast<float *>(part()->p), st);
@@ -531,12 +538,13 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
 void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   float *dw = grad_->as<float>() + L.w_off;
   if (tc_ && stem_tc_supported(L.g)) {
-    ProfScope ps("conv_wgrad_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2));
+    ProfScope ps("conv_wgrad_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2, PASS_WGRAD, 4));
     stem_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.xb()->as<__nv_bfloat16>(), dw, wgrad_ws()->as<float>(), st);
     return;
   }
   bool tc = tc_ && conv_tc_supported(L.g, 2);
-  ProfScope ps(tc ? "conv_wgrad_tc" : "conv_wgrad_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
+  ProfScope ps(tc ? "conv_wgrad_tc" : "conv_wgrad_simt", st, conv_flops(L.g),
+               conv_bytes(L.g, tc ? 2 : 4, PASS_WGRAD, 4));
   if (tc) {
     // L.xb holds bf16(x) from the conv_fwd of this tick (forward or recomputation);
     // L.dzb was written in bf16 by bn_bwd_dz
@@ -549,7 +557,8 @@ void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
 
 void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t st) {
   bool tc = tc_ && conv_tc_supported(L.g, 1);
-  ProfScope ps(tc ? "conv_dgrad_tc" : "conv_dgrad_simt", st, conv_flops(L.g), conv_bytes(L.g, tc ? 2 : 4));
+  ProfScope ps(tc ? "conv_dgrad_tc" : "conv_dgrad_simt", st, conv_flops(L.g),
+               conv_bytes(L.g, tc ? 2 : 4, PASS_DGRAD, 4, addend != nullptr));
   if (tc) {
     conv_dgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.wt_bf16->as<__nv_bfloat16>(), addend, out,
                   wgrad_ws()->as<float>(), st);
@@ -1067,9 +1076,10 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
     if (is_last_) {
       ctx_ = 0;
       enqueue_tail(a.x1, a.x2, a.labels, a.oxt[0], a.oxt[1], a.od[0], a.od[1], a.loss, push, pop, s);
-    } else if (fwd && bwd) {
+    } else if (fwd && bwd && !Prof::enabled) {
       // forward (theta^t, context 0) and backward (context 1) of different micro-batches
       // are independent until the update: run them on two streams, join, then update
+      // (a profiled replay serialises them so that each kernel's events time it alone)
       PETRA_CUDA(cudaEventRecord(fork_, s));
       PETRA_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
       ctx_ = 0;
@@ -1078,6 +1088,12 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
       enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, side_);
       PETRA_CUDA(cudaEventRecord(join_, side_));
       PETRA_CUDA(cudaStreamWaitEvent(s, join_, 0));
+      ctx_ = 0;
+    } else if (fwd && bwd) {
+      ctx_ = 0;
+      enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
+      ctx_ = 1;
+      enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, s);
       ctx_ = 0;
     } else if (fwd) {
       ctx_ = 0;
