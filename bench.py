@@ -148,7 +148,10 @@ def run_ours(a):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     H, classes = IMAGE[a.model]
     units = PM.revnet(a.model, H, classes)
-    counts = PM.partition(units, a.stages, a.batch, H, H, 3)
+    # one GPU: FLOP-balanced stages (all run concurrently); several: the comm-aware
+    # cost model (slowest GPU's compute + its cross-GPU message bytes / NVLink)
+    counts = (PM.partition(units, a.stages, a.batch, H, H, 3) if world == 1
+              else PM.partition_comm(units, a.stages, world, a.batch, H, H, 3))
     prec = L.BF16_TC if a.precision == "bf16" else L.FP32
     specs = PM.stage_specs(units, counts, a.batch, (H, H, 3), prec, WD[a.model])
     stage_rank = contiguous_stage_ranks(a.stages, world)
@@ -303,6 +306,7 @@ def run_ours(a):
            "config": {"workload": workload_name(a), "model": a.model, "global_batch": B, "micro_batch": B,
                       "image": [3, H, H], "classes": classes, "stages": J, "partition_units": counts,
                       "stage_rank": stage_rank, "parallelism": f"petra-stages{J}-over-{world}gpu",
+                      "partitioner": "flop-balanced" if world == 1 else "comm-aware cost model",
                       "precision_requested": a.precision, "lr": lr, "fill_ticks": 2 * J - 2,
                       "graph_capture_ticks": graph_cycle,
                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
@@ -366,6 +370,9 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
+    # at least one stage per GPU: J = max(--stages, world) (the paper's RevNets have
+    # 10-18 units, so J up to 8 always partitions)
+    a.stages = max(a.stages, a.gpus)
     if a.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     if a.impl == "reference":

@@ -47,6 +47,10 @@ __device__ __forceinline__ void pdl_wait_trigger() {
 bool pdl_enabled();
 // tuning knob from the environment (read once per name; default if unset)
 int env_int(const char *name, int dflt);
+// CTAs of a persistent conv kernel: min(work items, cap).  The stages of a tick and a
+// stage's two directions run concurrently, so a kernel that leaves SMs to its
+// neighbours raises the tick's throughput (measured); PETRA_CONV_CTAS.
+int conv_grid(int work);
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {

@@ -14,6 +14,8 @@
 // Deterministic: per-block fp64 partials, merged in a fixed order by the last
 // block to finish (atomic ticket after a fence) -- one launch per reduction, no
 // float atomics.  Streaming passes move 4 channels per thread (16-byte accesses).
+#include <type_traits>
+
 #include "../kernels.h"
 
 namespace petra {
@@ -52,10 +54,10 @@ inline int log2_or_neg(int v) {
 // row m of an H x W grid -> row of the zero-bordered (H+2) x (W+2) layout (pH <= 0: m)
 __device__ __forceinline__ int64_t pad_row(int64_t m, int pH, int pW) {
   if (pH <= 0) return m;
-  const int64_t hw = (int64_t)pH * pW;
-  const int64_t b = m / hw;
-  const int r = (int)(m - b * hw), h = r / pW, w = r - h * pW;
-  return (b * (pH + 2) + h + 1) * (pW + 2) + w + 1;
+  // 32-bit index math: the padded operand buffers hold < 2^31 rows (host-checked)
+  const int hw = pH * pW, mi = (int)m;
+  const int b = mi / hw, r = mi - b * hw, h = r / pW, w = r - h * pW;
+  return ((int64_t)b * (pH + 2) + h + 1) * (pW + 2) + w + 1;
 }
 
 // reduction blocks: one wave of NT-thread blocks (stats 1024, backward reduce 512:
@@ -80,9 +82,9 @@ inline RedGeom red_geom(int64_t M, int C, int RT) {
   }
   g.RG = RT / g.TPR;
   g.ctiles = (int)cdiv(C, g.CT);
-  // one full-occupancy wave (2048 threads per SM): enough loads in flight per SM for
-  // small tensors, and few partials to merge
-  int64_t want = std::max<int64_t>(1, (int64_t)kNumSMs * (2048 / RT) / g.ctiles);
+  // one wave: one block per SM (1024 / 512 threads, >= 64 KB of loads in flight), few
+  // partials to merge
+  int64_t want = std::max<int64_t>(1, (int64_t)kNumSMs / g.ctiles);
   g.nrb = (int)std::max<int64_t>(1, std::min<int64_t>(want, cdiv(M, 4 * g.RG)));
   g.rpb = cdiv(M, g.nrb);
   g.nrb = (int)cdiv(M, g.rpb);
@@ -255,56 +257,9 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
                                 const float *__restrict__ mean, const float *__restrict__ invstd,
                                 const float *__restrict__ gamma, const float *__restrict__ beta, int relu,
                                 float sign, const float *acc, TO *out, __nv_bfloat16 *out_bf16, int pH, int pW,
-                                int sh, int fixed) {
+                                int sh) {
   pdl_wait_trigger();
   const bool vec = (C % 4 == 0) && (ldz % 4 == 0) && (zc0 % 4 == 0);
-  if (vec && fixed) {
-    // the grid stride is a multiple of C/4: each thread keeps one 4-channel group,
-    // whose BN constants live in registers; rows advance by stride / (C/4)
-    const int C4 = C / 4;
-    const int64_t n = M * C4, stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i0 >= n) return;
-    const int c = (int)(i0 % C4) * 4, cz = zc0 + c;
-    const int64_t dm = stride / C4;
-    float a[4], mu[4], be[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      a[k] = gamma[cz + k] * invstd[cz + k];
-      mu[k] = mean[cz + k];
-      be[k] = beta[cz + k];
-    }
-    // 4 rows per trip, all loads issued before any use (memory-level parallelism)
-    for (int64_t i = i0, m = i0 / C4; i < n; i += 4 * stride, m += 4 * dm) {
-      float4 zv[4], av[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (i + u * stride < n) {
-          zv[u] = ld4(z, (m + u * dm) * ldz + cz);
-          av[u] = acc ? ld4(acc, (m + u * dm) * C + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (i + u * stride >= n) break;
-        const int64_t mu_ = m + u * dm;
-        float4 o;
-        float *op = &o.x;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          float y = fmaf(a[k], f4(zv[u], k) - mu[k], be[k]);
-          if (relu) y = y > 0.f ? y : 0.f;
-          op[k] = sign * y;
-        }
-        if (acc) {
-          o.x += av[u].x; o.y += av[u].y; o.z += av[u].z; o.w += av[u].w;
-        }
-        if (out) st4(out, mu_ * C + c, o);
-        if (out_bf16) st4(out_bf16, pad_row(mu_, pH, pW) * C + c, o);
-      }
-    }
-    return;
-  }
   if (vec) {
     const int C4 = C / 4;
     const int64_t n = M * C4;
@@ -341,6 +296,107 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
     if (acc) o += acc[i];
     if (out) stv(out, i, o);
     if (out_bf16) out_bf16[pad_row(m, pH, pW) * C + c] = __float2bfloat16_rn(o);
+  }
+}
+
+// Per-channel passes with one 4-channel group per thread: the grid stride is a
+// multiple of C/4 (chan_grid), so the BN constants of a thread live in registers and
+// rows advance by stride / (C/4); two rows per trip, loads issued before use.  Row
+// indices are 32-bit (M < 2^31, host-checked).
+template <typename TZ>
+__global__ void __launch_bounds__(256, 4) bn_apply_fixed_kernel(
+    int M, int C, const TZ *__restrict__ z, int ldz, int zc0, const float *__restrict__ mean,
+    const float *__restrict__ invstd, const float *__restrict__ gamma, const float *__restrict__ beta, int relu,
+    float sign, const float *__restrict__ acc, float *__restrict__ out, __nv_bfloat16 *__restrict__ out_bf16, int pH,
+    int pW) {
+  pdl_wait_trigger();
+  const int C4 = C / 4;
+  const int stride = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (t0 % C4) * 4, cz = zc0 + c;
+  const int dm = stride / C4;
+  float a[4], mu[4], be[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    a[k] = gamma[cz + k] * invstd[cz + k];
+    mu[k] = mean[cz + k];
+    be[k] = beta[cz + k];
+  }
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int m = t0 / C4; m < M; m += 2 * dm) {
+    const bool two = m + dm < M;
+    const float4 z0 = ld4(z, (int64_t)m * ldz + cz);
+    const float4 z1 = two ? ld4(z, (int64_t)(m + dm) * ldz + cz) : zero;
+    const float4 a0 = acc ? ld4(acc, (int64_t)m * C + c) : zero;
+    const float4 a1 = (acc && two) ? ld4(acc, (int64_t)(m + dm) * C + c) : zero;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (u && !two) break;
+      const int mm = m + u * dm;
+      const float4 zv = u ? z1 : z0, av = u ? a1 : a0;
+      float4 o;
+      float *op = &o.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float y = fmaf(a[k], f4(zv, k) - mu[k], be[k]);
+        if (relu) y = y > 0.f ? y : 0.f;
+        op[k] = sign * y;
+      }
+      o.x += av.x; o.y += av.y; o.z += av.z; o.w += av.w;
+      if (out) st4(out, (int64_t)mm * C + c, o);
+      if (out_bf16) st4(out_bf16, pad_row(mm, pH, pW) * C + c, o);
+    }
+  }
+}
+
+template <typename TZ>
+__global__ void __launch_bounds__(256, 4) bn_bwd_dz_fixed_kernel(
+    int M, int C, const TZ *__restrict__ z, const float *__restrict__ mean, const float *__restrict__ invstd,
+    const float *__restrict__ gamma, const float *__restrict__ beta, int relu, const float *__restrict__ dy,
+    const float *__restrict__ dgamma, const float *__restrict__ dbeta, float *__restrict__ dz,
+    __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW) {
+  pdl_wait_trigger();
+  const float invM = 1.0f / (float)M;
+  const int C4 = C / 4;
+  const int stride = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (t0 % C4) * 4;
+  const int dm = stride / C4;
+  float is[4], mu[4], ga[4], be[4], db[4], dg[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    is[k] = invstd[c + k];
+    mu[k] = mean[c + k];
+    ga[k] = gamma[c + k];
+    be[k] = beta[c + k];
+    db[k] = dbeta[c + k] * invM;
+    dg[k] = dgamma[c + k];
+  }
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int m = t0 / C4; m < M; m += 2 * dm) {
+    const bool two = m + dm < M;
+    const float4 z0 = ld4(z, (int64_t)m * C + c);
+    const float4 z1 = two ? ld4(z, (int64_t)(m + dm) * C + c) : zero;
+    const float4 g0 = ld4(dy, (int64_t)m * C + c);
+    const float4 g1 = two ? ld4(dy, (int64_t)(m + dm) * C + c) : zero;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (u && !two) break;
+      const int mm = m + u * dm;
+      const float4 zv = u ? z1 : z0;
+      float4 g4 = u ? g1 : g0;
+      float4 o;
+      float *op = &o.x, *gp = &g4.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float xh = (f4(zv, k) - mu[k]) * is[k];
+        float g = gp[k];
+        if (relu && !(fmaf(ga[k], xh, be[k]) > 0.f)) g = 0.f;
+        op[k] = ga[k] * is[k] * (g - db[k] - xh * dg[k] * invM);  // same rounding as bn_bwd_dz_kernel
+      }
+      if (dz) st4(dz, (int64_t)mm * C + c, o);
+      if (dz_bf16) st4(dz_bf16, pad_row(mm, pH, pW) * C + c, o);
+    }
   }
 }
 
@@ -449,55 +505,10 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
                                  const float *__restrict__ beta, int relu, const float *dy0, const float *dy1,
                                  int cs, const float *__restrict__ dgamma, const float *__restrict__ dbeta,
                                  float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW,
-                                 int sh, int fixed) {
+                                 int sh) {
   pdl_wait_trigger();
   const float invM = 1.0f / (float)M;
   const bool vec = (C % 4 == 0) && (dy1 == nullptr || cs % 4 == 0);
-  if (vec && fixed) {  // one 4-channel group per thread (see bn_apply_kernel)
-    const int C4 = C / 4;
-    const int64_t n = M * C4, stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i0 >= n) return;
-    const int c = (int)(i0 % C4) * 4;
-    const int64_t dm = stride / C4;
-    float is[4], mu[4], ga[4], be[4], db[4], dg[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      is[k] = invstd[c + k];
-      mu[k] = mean[c + k];
-      ga[k] = gamma[c + k];
-      be[k] = beta[c + k];
-      db[k] = dbeta[c + k] * invM;
-      dg[k] = dgamma[c + k];
-    }
-    for (int64_t i = i0, m = i0 / C4; i < n; i += 4 * stride, m += 4 * dm) {  // 4 rows per trip
-      float4 zv[4], gv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (i + u * stride < n) {
-          zv[u] = ld4(z, (m + u * dm) * C + c);
-          gv[u] = load_dy4(dy0, dy1, cs, C, m + u * dm, c);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (i + u * stride >= n) break;
-        const int64_t mu_ = m + u * dm;
-        float4 o;
-        float *op = &o.x, *gp = &gv[u].x;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float xh = (f4(zv[u], k) - mu[k]) * is[k];
-          float g = gp[k];
-          if (relu && !(fmaf(ga[k], xh, be[k]) > 0.f)) g = 0.f;
-          op[k] = ga[k] * is[k] * (g - db[k] - xh * dg[k] * invM);
-        }
-        if (dz) st4(dz, mu_ * C + c, o);
-        if (dz_bf16) st4(dz_bf16, pad_row(mu_, pH, pW) * C + c, o);
-      }
-    }
-    return;
-  }
   if (vec) {
     const int C4 = C / 4;
     const int64_t n = M * C4;
@@ -578,8 +589,13 @@ void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
               __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st) {
   const unsigned cg = (ldz % 4 == 0 && zc0 % 4 == 0) ? chan_grid(M, C) : 0;
-  launch_k(bn_apply_kernel<TZ, TO>, cg ? cg : ew_grid(M * C / 4), 256, 0, st, M, C, z, ldz, zc0, mean, invstd, gamma,
-           beta, relu, sign, acc, out, out_bf16, pH, pW, log2_or_neg(C / 4), cg ? 1 : 0);
+  if (cg && std::is_same<TO, float>::value && M < ((int64_t)1 << 31) / 4) {
+    launch_k(bn_apply_fixed_kernel<TZ>, cg, 256, 0, st, (int)M, C, z, ldz, zc0, mean, invstd, gamma, beta, relu, sign,
+             acc, reinterpret_cast<float *>(out), out_bf16, pH, pW);
+  } else {
+    launch_k(bn_apply_kernel<TZ, TO>, ew_grid(M * C / 4), 256, 0, st, M, C, z, ldz, zc0, mean, invstd, gamma, beta,
+             relu, sign, acc, out, out_bf16, pH, pW, log2_or_neg(C / 4));
+  }
   PETRA_LAUNCH_CHECK();
 }
 template void bn_apply<float, float>(int64_t, int, const float *, int, int, const float *, const float *,
@@ -613,9 +629,13 @@ template <typename TZ>
 void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *invstd, const float *gamma,
                const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
                const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, int pH, int pW, cudaStream_t st) {
-  const unsigned cg = (dy1 == nullptr || cs % 4 == 0) ? chan_grid(M, C) : 0;
-  launch_k(bn_bwd_dz_kernel<TZ>, cg ? cg : ew_grid(M * C / 4), 256, 0, st, M, C, z, mean, invstd, gamma, beta, relu,
-           dy0, dy1, cs, dgamma, dbeta, dz, dz_bf16, pH, pW, log2_or_neg(C / 4), cg ? 1 : 0);
+  const unsigned cg = dy1 == nullptr ? chan_grid(M, C) : 0;  // split halves (stem): generic pass
+  if (cg && M < ((int64_t)1 << 31) / 4)
+    launch_k(bn_bwd_dz_fixed_kernel<TZ>, cg, 256, 0, st, (int)M, C, z, mean, invstd, gamma, beta, relu, dy0, dgamma,
+             dbeta, dz, dz_bf16, pH, pW);
+  else
+    launch_k(bn_bwd_dz_kernel<TZ>, ew_grid(M * C / 4), 256, 0, st, M, C, z, mean, invstd, gamma, beta, relu, dy0, dy1,
+             cs, dgamma, dbeta, dz, dz_bf16, pH, pW, log2_or_neg(C / 4));
   PETRA_LAUNCH_CHECK();
 }
 template void bn_bwd_dz<float>(int64_t, int, const float *, const float *, const float *, const float *,

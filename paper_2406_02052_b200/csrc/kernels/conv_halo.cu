@@ -322,7 +322,7 @@ template <int BN, int T, bool OUT16>
 void launch(const CUtensorMap &ta, const CUtensorMap &tb, const HaloParams &P, cudaStream_t st) {
   const int work = (int)cdiv(P.Mp, 128 * T) * (P.N / BN);
   const size_t smem = fixed_smem() + 2 * (size_t)P.a_stage + (size_t)P.bstages * BN * 128;
-  launch_k(conv_halo_kernel<BN, T, OUT16>, std::min(work, kNumSMs), kThreads, smem, st, ta, tb, P);
+  launch_k(conv_halo_kernel<BN, T, OUT16>, conv_grid(work), kThreads, smem, st, ta, tb, P);
   PETRA_LAUNCH_CHECK();
 }
 
@@ -403,7 +403,7 @@ int conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_p
   if (out16) dispatch<true>(pl.BN, pl.T, ta, tb, P, st);
   else dispatch<false>(pl.BN, pl.T, ta, tb, P, st);
   const int work = (int)cdiv(P.Mp, 128 * pl.T) * (N / pl.BN);
-  return P.stats ? std::min(work, kNumSMs) : 0;
+  return P.stats ? conv_grid(work) : 0;
 }
 
 }  // namespace petra

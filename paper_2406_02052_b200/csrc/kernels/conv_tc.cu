@@ -671,7 +671,9 @@ ConvPlan conv_plan(int M, int N, int KB) {
     if (mt * (N / bn) >= kNumSMs) break;
   }
   const int tiles = mt * (N / p.BN);
-  static const int split_max = env_int("PETRA_SPLITK_MAX", 1 << 20);
+  // split-K off by default: under the tick's stream concurrency the split's partial
+  // traffic and second launch cost more than the SMs it fills (measured)
+  static const int split_max = env_int("PETRA_SPLITK_MAX", 1);
   if (tiles * 4 < kNumSMs * 3 && split_max > 1) {  // under 75% of one wave: split K
     int want = std::max(1, std::min(split_max, (kNumSMs + tiles / 2) / tiles));
     want = std::min(want, std::max(1, KB / 4));  // at least 4 K-blocks per split
@@ -724,7 +726,7 @@ void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParam
   const int work = (P.M / BM) * (P.N / BN) * P.splits;
   const CUtensorMap to = out_map(P.out, OUT16, P);
   const CUtensorMap tw = P.splits > 1 ? ws_map(P.ws, P.N, (int64_t)P.splits * P.M) : to;
-  launch_k(conv_tc_kernel<BN, STAGES, OUT16>, std::min(work, kNumSMs), kConvThreads, smem, st, ta, tb, to, tw, P);
+  launch_k(conv_tc_kernel<BN, STAGES, OUT16>, conv_grid(work), kConvThreads, smem, st, ta, tb, to, tw, P);
   PETRA_LAUNCH_CHECK();
   if (P.splits > 1) {
     int64_t n = (int64_t)P.M * P.N / 4;
@@ -797,7 +799,7 @@ int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const __nv_bf
   launch_any(ta, w, g.Co, g.K(), P, ws, out16, st);
   if (!P.stats) return 0;
   const int BN = conv_plan(P.M, P.N, P.ntaps * P.CB).BN;
-  return std::min((P.M / BM) * (P.N / BN) * P.splits, kNumSMs);  // partial rows written (one per CTA)
+  return conv_grid((P.M / BM) * (P.N / BN) * P.splits);  // partial rows written (one per CTA)
 }
 
 void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_pad, const __nv_bfloat16 *wt, const float *addend,
@@ -881,7 +883,7 @@ WgradPlan wgrad_plan(const ConvGeom &g) {
   w.t = tiling(g.B, g.Ho, g.Wo, 64);
   w.KBtot = (int)(w.t.M() / 64);
   int tiles = w.n_mt * w.n_nt;
-  static const int ctas = env_int("PETRA_WGRAD_CTAS", kNumSMs);  // CTAs the split-K aims to fill
+  static const int ctas = env_int("PETRA_WGRAD_CTAS", kNumSMs / 2);  // CTAs the split-K aims to fill
   int want = std::max(1, std::min(w.KBtot, (int)cdiv(ctas, tiles)));
   w.kb_per_split = (int)cdiv(w.KBtot, want);
   w.splits = (int)cdiv(w.KBtot, w.kb_per_split);

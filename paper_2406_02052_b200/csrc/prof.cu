@@ -20,6 +20,11 @@ int env_int(const char *name, int dflt) {
   return (e && *e) ? atoi(e) : dflt;
 }
 
+int conv_grid(int work) {
+  static const int cap = std::max(1, std::min(kNumSMs, env_int("PETRA_CONV_CTAS", kNumSMs)));
+  return std::max(1, std::min(work, cap));
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char *e = getenv("PETRA_PDL");

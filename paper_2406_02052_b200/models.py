@@ -157,6 +157,117 @@ def partition(units, J, batch=64, h=32, w=32, c=3):
     return counts
 
 
+# ---- cost model of a unit's tick (comm-aware partitioner)
+# Measured on B200 (profiles/r01, serialised replay): tensor-core convolutions run
+# at ~0.27 of the bf16 peak inside a tick, the streaming BN / coupling passes at
+# ~0.6 of HBM; a peer copy over NVLink 5 at 770 GB/s per direction (B200_PROFILING.md).
+TC_FLOPS = 0.27 * 1.37e15
+HBM_BPS = 0.6 * 6.46e12
+LINK_BPS = 7.7e11
+
+
+def unit_cost(units, batch, h, w, c):
+    """Modelled device seconds of one tick of each unit (forward + reconstruction +
+    VJP = 4x the forward conv FLOPs for reversible units, Table 1; the
+    same count for non-reversible units, which recompute from their buffer) plus its
+    streaming bytes: per half-coupling the forward reads src/dst and writes dst
+    (3 N fp32), the backward reads dst', src, d_dst, d_src and writes dst, d_src
+    (6 N), and every conv output is written and read in bf16 in the forward, the
+    recomputation and twice in the BN backward."""
+    macs = conv_macs(units, batch, h, w, c)
+    ins, _ = shapes(units, batch, h, w, c)
+    out = []
+    for u, m, (B, H, W, Cc) in zip(units, macs, ins):
+        flops = 4 * 2.0 * m
+        by = 0.0
+        if u.kind in (L.UNIT_REV, L.UNIT_DS):
+            n = B * H * W * Cc
+            by += 9 * 4.0 * n
+            HH, WW = H, W
+            for ci, co, k, s in u.layers:
+                HH, WW = _out(HH, k, s), _out(WW, k, s)
+                by += 4 * 2.0 * B * HH * WW * co
+        elif u.kind == L.UNIT_STEM:
+            ci, co, k, s = u.layers[0]
+            by += 4 * 2.0 * B * _out(H, k, s) * _out(W, k, s) * co + 3 * 4.0 * B * H * W * Cc
+        out.append(flops / TC_FLOPS + by / HBM_BPS)
+    return out
+
+
+def boundary_bytes(units, batch, h, w, c):
+    """Bytes crossing the cut in front of unit i per tick: the forward message
+    (2 fp32 halves) plus the backward message (x~ and delta: 4 halves)."""
+    ins, _ = shapes(units, batch, h, w, c)
+    return [6 * 4.0 * B * H * W * Cc for (B, H, W, Cc) in ins]
+
+
+def partition_comm(units, J, world, batch=64, h=32, w=32, c=3):
+    """Contiguous grouping of units into J stages on `world` GPUs (J/world
+    consecutive stages per GPU, contiguous_stage_ranks) minimising the slowest GPU:
+    max over GPUs of (its stages' modelled compute + the bytes of its cross-GPU cuts
+    / link).  Exact by dynamic programming over cut positions (units <= ~20)."""
+    cost = unit_cost(units, batch, h, w, c)
+    bnd = boundary_bytes(units, batch, h, w, c)
+    n = len(units)
+    if J > n:
+        raise ValueError(f"J={J} > {n} units")
+    base, rem = divmod(J, world)
+    per_gpu = [base + (1 if r < rem else 0) for r in range(world)]
+    pre = [0.0]
+    for x in cost:
+        pre.append(pre[-1] + x)
+    import functools
+
+    @functools.lru_cache(maxsize=None)
+    def best(i, g):
+        """(bottleneck, counts) for units i.. on GPUs g.. ; GPU g takes per_gpu[g] stages."""
+        if g == world:
+            return (0.0, ()) if i == n else (float("inf"), ())
+        k = per_gpu[g]
+        rest = sum(per_gpu[g + 1:])
+        res = (float("inf"), ())
+        for j in range(i + k, n - rest + 1):   # GPU g gets units i..j-1 (>= k of them)
+            comm = (bnd[i] if i > 0 else 0.0) + (bnd[j] if j < n else 0.0)
+            t = pre[j] - pre[i] + comm / LINK_BPS
+            tail, cnts = best(j, g + 1)
+            b = max(t, tail)
+            if b < res[0]:
+                res = (b, (j - i,) + cnts)
+        return res
+
+    _, per = best(0, 0)
+    # split each GPU's units into its stages, balancing modelled cost inside the GPU
+    counts, i = [], 0
+    for g, m in enumerate(per):
+        sub = units[i:i + m]
+        if per_gpu[g] == 1:
+            counts.append(m)
+        else:
+            cs = cost[i:i + m]
+            counts += _balance(cs, per_gpu[g])
+        i += m
+    return counts
+
+
+def _balance(cost, k):
+    """Contiguous split of a cost list into k non-empty groups minimising the maximum."""
+    n = len(cost)
+    import functools
+
+    @functools.lru_cache(maxsize=None)
+    def f(i, k):
+        if k == 1:
+            return (sum(cost[i:]), (n - i,))
+        res = (float("inf"), ())
+        for j in range(i + 1, n - k + 2):
+            tail = f(j, k - 1)
+            b = max(sum(cost[i:j]), tail[0])
+            if b < res[0]:
+                res = (b, (j - i,) + tail[1])
+        return res
+    return list(f(0, k)[1])
+
+
 @dataclass
 class StageSpec:
     units: list
