@@ -152,6 +152,13 @@ def _stage_tick(case, precision, exact_fwd):
     tol_g = tol
     if precision == L.BF16_TC and case in BF16_TIER:
         tol, tol_g = BF16_TIER[case]
+    elif precision == L.BF16_TC and sum(1 for u in units if not isinstance(u, StemUnit)) >= 2:
+        # reading c23: the second unit's backward runs on a RECONSTRUCTED fp32 half whose
+        # bf16 rounding can land on the other neighbour of the emulating oracle's; the
+        # ReLU mask that flips carries an O(1) dy.  Held to the north_star bf16 bar (2e-2)
+        # (measured: rev_basic_c128_16x16 bwd.d1 6.2e-3, grad.u0.w 9.6e-3 once the forward
+        # conv ran without split-K, i.e. with another fp32 summation order)
+        tol, tol_g = 2e-2, 2e-2
     xs = [synth.images(s, 0, i) for i, s in enumerate(in_shapes)]
     # ---- forward
     fo = ostage.forward(E.Fwd(0, xs, None))
