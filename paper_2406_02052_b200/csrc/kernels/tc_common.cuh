@@ -166,19 +166,33 @@ __device__ __forceinline__ void colsum16(float (&x)[16], int lane) {
 template <bool BF16, bool SWZ>
 __device__ __forceinline__ void staged_colsums(const uint8_t *buf, int pitch, int lane, float (&s)[2],
                                                float (&q)[2]) {
-  s[0] = s[1] = q[0] = q[1] = 0.f;
+  if constexpr (BF16) {
+    // packed fp32x2 adds / FMAs (sm_100 FADD2 / FFMA2), even and odd rows in separate
+    // accumulators (two dependency chains); bf16 -> fp32 is a 16-bit shift
+    float2 s0 = make_float2(0.f, 0.f), s1 = s0, q0 = s0, q1 = s0;
 #pragma unroll 8
-  for (int r = 0; r < 32; ++r) {
-    const int chunk = SWZ ? ((lane >> 2) ^ (r & 7)) : (lane >> 2);
-    const uint32_t w = *reinterpret_cast<const uint32_t *>(buf + r * pitch + chunk * 16 + 4 * (lane & 3));
-    if constexpr (BF16) {
-      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&w));
-      s[0] += f.x;
-      q[0] = fmaf(f.x, f.x, q[0]);
-      s[1] += f.y;
-      q[1] = fmaf(f.y, f.y, q[1]);
-    } else {
-      const float f = __uint_as_float(w);
+    for (int r = 0; r < 32; r += 2) {
+      const int c0 = SWZ ? ((lane >> 2) ^ (r & 7)) : (lane >> 2);
+      const int c1 = SWZ ? ((lane >> 2) ^ ((r + 1) & 7)) : (lane >> 2);
+      const uint32_t w0 = *reinterpret_cast<const uint32_t *>(buf + r * pitch + c0 * 16 + 4 * (lane & 3));
+      const uint32_t w1 = *reinterpret_cast<const uint32_t *>(buf + (r + 1) * pitch + c1 * 16 + 4 * (lane & 3));
+      const float2 f0 = make_float2(__uint_as_float(w0 << 16), __uint_as_float(w0 & 0xffff0000u));
+      const float2 f1 = make_float2(__uint_as_float(w1 << 16), __uint_as_float(w1 & 0xffff0000u));
+      s0 = __fadd2_rn(s0, f0);
+      q0 = __ffma2_rn(f0, f0, q0);
+      s1 = __fadd2_rn(s1, f1);
+      q1 = __ffma2_rn(f1, f1, q1);
+    }
+    s[0] = s0.x + s1.x;
+    s[1] = s0.y + s1.y;
+    q[0] = q0.x + q1.x;
+    q[1] = q0.y + q1.y;
+  } else {
+    s[0] = s[1] = q[0] = q[1] = 0.f;
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+      const int chunk = SWZ ? ((lane >> 2) ^ (r & 7)) : (lane >> 2);
+      const float f = *reinterpret_cast<const float *>(buf + r * pitch + chunk * 16 + 4 * (lane & 3));
       s[0] += f;
       q[0] = fmaf(f, f, q[0]);
     }

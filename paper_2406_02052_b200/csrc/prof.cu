@@ -21,7 +21,7 @@ int env_int(const char *name, int dflt) {
 }
 
 int conv_grid(int work) {
-  static const int cap = std::max(1, std::min(kNumSMs, env_int("PETRA_CONV_CTAS", kNumSMs)));
+  static const int cap = std::max(1, std::min(kNumSMs, env_int("PETRA_CONV_CTAS", 96)));
   return std::max(1, std::min(work, cap));
 }
 
