@@ -132,7 +132,8 @@ petra_status petra_stage_param_count(const petra_stage *s, size_t *n_params, siz
  *   optimizer  v, Delta (last backward) and the Delta_j accumulator (k > 1)
  *   shadows    bf16 copies of the live conv weights (tensor-core operands; a copy of
  *              the single live version, rewritten by every update, not a stash)
- *   fifo       input FIFO slots of the non-reversible units (capacity 2(J-j)+1)
+ *   fifo       input FIFO slots of the non-reversible units (capacity 2(J-j)+1): the fp32
+ *              input and, on the tensor-core path, its bf16 conv operands
  *   fifo_live  bytes of those slots holding an input right now
  *   workspace  everything else: per-layer conv outputs / BN statistics / operand
  *              copies of the tick, tail buffers

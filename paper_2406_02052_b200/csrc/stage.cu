@@ -141,7 +141,7 @@ void Stage::alloc_layer(Layer &L, bool inner) {
     const int64_t ndz = L.dzpad ? (int64_t)L.g.B * (L.g.Ho + 2) * (L.g.Wo + 2) * L.g.Co : n;
     L.dzb = dalloc(ndz * sizeof(__nv_bfloat16));
     if (L.dzpad) PETRA_CUDA(cudaMemset(L.dzb->p, 0, ndz * sizeof(__nv_bfloat16)));  // borders stay zero
-    for (int c = 0; c < 2 && !L.operand_of; ++c) {
+    for (int c = 0; c < 2 && !L.operand_of && !L.fifo_backed; ++c) {
       L.xb_[c] = dalloc(nxb * sizeof(__nv_bfloat16));
       if (L.xpad) PETRA_CUDA(cudaMemset(L.xb_[c]->p, 0, nxb * sizeof(__nv_bfloat16)));
     }
@@ -262,6 +262,16 @@ void Stage::build() {
   bufs_ = dalloc(std::max<int64_t>(1, n_buffers_) * sizeof(float));
   PETRA_CUDA(cudaMemset(grad_->p, 0, n_params_ * sizeof(float)));
 
+  // ---- bf16 operands of non-reversible units live in their FIFO slots (tensor-core
+  // path, plain layouts): converted once in the forward, reused by the recomputation
+  if (tc_ && desc_.precision == PETRA_BF16_TC) {
+    for (auto &u : units_) {
+      auto plain = [&](const Layer &L) { return conv_tc_supported(L.g, 0) && !(L.g.k == 3 && L.g.s == 1); };
+      if (u.d.kind == PETRA_UNIT_DS && plain(u.pa) && plain(u.phi[0]))
+        u.pa.fifo_backed = u.phi[0].fifo_backed = true;
+      if (u.d.kind == PETRA_UNIT_STEM && stem_tc_supported(u.phi[0].g)) u.phi[0].fifo_backed = true;
+    }
+  }
   // ---- workspace
   for (auto &u : units_) {
     for (size_t l = 0; l < u.phi.size(); ++l) alloc_layer(u.phi[l], l + 1 < u.phi.size());
@@ -328,6 +338,12 @@ void Stage::build() {
       for (int s = 0; s < u.fifo.cap; ++s) {
         u.fifo.slot0.push_back(dalloc(u.in.numel() * sizeof(float)));
         if (u.d.kind == PETRA_UNIT_DS) u.fifo.slot1.push_back(dalloc(u.in.numel() * sizeof(float)));
+        if (u.d.kind == PETRA_UNIT_DS && u.pa.fifo_backed) {
+          u.fifo.bslot0.push_back(dalloc(u.in.numel() * sizeof(__nv_bfloat16)));
+          u.fifo.bslot1.push_back(dalloc(u.in.numel() * sizeof(__nv_bfloat16)));
+        } else if (u.d.kind == PETRA_UNIT_STEM && u.phi[0].fifo_backed) {
+          u.fifo.bslot0.push_back(dalloc(stem_operand_elems(u.phi[0].g) * sizeof(__nv_bfloat16)));
+        }
       }
     }
   }
@@ -435,7 +451,9 @@ void Stage::memory(petra_memory_report *r) const {
     }
     uint64_t slot = 0, all = 0;
     for (size_t s = 0; s < u.fifo.slot0.size(); ++s) {
-      uint64_t one = b(u.fifo.slot0[s]) + (s < u.fifo.slot1.size() ? b(u.fifo.slot1[s]) : 0);
+      uint64_t one = b(u.fifo.slot0[s]) + (s < u.fifo.slot1.size() ? b(u.fifo.slot1[s]) : 0) +
+                     (s < u.fifo.bslot0.size() ? b(u.fifo.bslot0[s]) : 0) +
+                     (s < u.fifo.bslot1.size() ? b(u.fifo.bslot1[s]) : 0);
       all += one;
       slot = one;
     }
@@ -510,25 +528,25 @@ static double conv_bytes(const ConvGeom &g, int esz, int pass, int out_es, bool 
 void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready) {
   const float *w = theta_->as<float>() + L.w_off;
   if (tc_ && stem_tc_supported(L.g)) {  // few input channels: gathered im2col from a 4-channel bf16 copy
-    {
+    if (!x_bf16_ready) {
       ProfScope pc("cvt_bf16", st, 0.0, (4.0 * L.g.Ci + 8.0) * (double)L.g.Min());
-      image_to_bf16x4(x, L.xb()->as<__nv_bfloat16>(), L.g, st);
+      image_to_bf16x4(x, L.xbp(), L.g, st);
     }
     ProfScope ps("conv_fwd_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2, PASS_FWD, L.z16 ? 2 : 4));
-    L.stats_rows() = stem_fwd_tc(L.g, L.xb()->as<__nv_bfloat16>(), w, L.z()->p, L.z16,
+    L.stats_rows() = stem_fwd_tc(L.g, L.xbp(), w, L.z()->p, L.z16,
                                  reinterpret_cast<float *>(part()->p), st);
     return;
   }
   bool tc = tc_ && conv_tc_supported(L.g, 0);
   if (tc && !x_bf16_ready) {  // bf16 operand of a stream input (also read by the TC wgrad)
     ProfScope pc("cvt_bf16", st, 0.0, 6.0 * (double)L.g.Min() * L.g.Ci);
-    if (L.xpad) f32_to_bf16_padded(x, L.xb()->as<__nv_bfloat16>(), L.g.B, L.g.H, L.g.W, L.g.Ci, st);
-    else f32_to_bf16(x, L.xb()->as<__nv_bfloat16>(), L.g.Min() * L.g.Ci, st);
+    if (L.xpad) f32_to_bf16_padded(x, L.xbp(), L.g.B, L.g.H, L.g.W, L.g.Ci, st);
+    else f32_to_bf16(x, L.xbp(), L.g.Min() * L.g.Ci, st);
   }
   ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g),
                conv_bytes(L.g, tc ? 2 : 4, PASS_FWD, L.z16 ? 2 : 4));
   if (tc) {
-    L.stats_rows() = conv_fwd_tc(L.g, L.xb()->as<__nv_bfloat16>(), L.xpad, L.w_bf16->as<__nv_bfloat16>(), L.z()->p, L.z16,
+    L.stats_rows() = conv_fwd_tc(L.g, L.xbp(), L.xpad, L.w_bf16->as<__nv_bfloat16>(), L.z()->p, L.z16,
                                wgrad_ws()->as<float>(), reinterpret_cast<float *>(part()->p), st);
   } else {
     conv_fwd_simt(L.g, x, w, L.z()->as<float>(), st);
@@ -539,7 +557,7 @@ void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   float *dw = grad_->as<float>() + L.w_off;
   if (tc_ && stem_tc_supported(L.g)) {
     ProfScope ps("conv_wgrad_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2, PASS_WGRAD, 4));
-    stem_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.xb()->as<__nv_bfloat16>(), dw, wgrad_ws()->as<float>(), st);
+    stem_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.xbp(), dw, wgrad_ws()->as<float>(), st);
     return;
   }
   bool tc = tc_ && conv_tc_supported(L.g, 2);
@@ -548,7 +566,7 @@ void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   if (tc) {
     // L.xb holds bf16(x) from the conv_fwd of this tick (forward or recomputation);
     // L.dzb was written in bf16 by bn_bwd_dz
-    conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.xb()->as<__nv_bfloat16>(), L.xpad, dw,
+    conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.xbp(), L.xpad, dw,
                   wgrad_ws()->as<float>(), st);
   } else {
     conv_wgrad_simt(L.g, L.dz->as<float>(), x, dw, wgrad_ws()->as<float>(), st);
@@ -606,7 +624,7 @@ void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running
       const bool need32 = !ready || !conv_tc_supported(N.g, 2);
       apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(), L.invstd()->as<float>(),
                th + L.g_off, th + L.b_off, 1, 1.f, nullptr, need32 ? L.a()->as<float>() : nullptr,
-               ready ? N.xb()->as<__nv_bfloat16>() : nullptr, st, N.xpad ? N.g.H : 0, N.g.W);
+               ready ? N.xbp() : nullptr, st, N.xpad ? N.g.H : 0, N.g.W);
       x = L.a()->as<float>();
     }
   }
@@ -678,7 +696,19 @@ Bf16Out Stage::src_operand(Unit &n) {
   if (!tc_ || n.d.kind != PETRA_UNIT_REV) return {};
   Layer &L = n.phi[0];
   if (!conv_tc_supported(L.g, 0)) return {};
-  return Bf16Out{L.xb()->as<__nv_bfloat16>(), L.xpad ? L.g.H : 0, L.g.W};
+  return Bf16Out{L.xbp(), L.xpad ? L.g.H : 0, L.g.W};
+}
+
+// point the FIFO-backed layers of a non-reversible unit at the bf16 slots of `slot`
+void Stage::bind_fifo_operands(Unit &u, int slot) {
+  if (u.fifo.bslot0.empty()) return;
+  if (u.d.kind == PETRA_UNIT_STEM) {
+    u.phi[0].xb_ext = u.fifo.bslot0[slot]->as<__nv_bfloat16>();
+    return;
+  }
+  DevPtr *b[2] = {&u.fifo.bslot0[slot], &u.fifo.bslot1[slot]};
+  u.pa.xb_ext = (*b[u.dst()])->as<__nv_bfloat16>();      // P_a reads x[dst]
+  u.phi[0].xb_ext = (*b[u.src()])->as<__nv_bfloat16>();  // the branch (and P_b) read x[src]
 }
 
 void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep, cudaStream_t st, Bf16Out ob,
@@ -756,8 +786,8 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
     case PETRA_UNIT_DS: {
       const float *xd = xin[u.dst()], *xs = xin[u.src()];
       if (recompute) {
-        branch_forward(u.phi, xs, true, st);
-        conv_fwd(u.pa, xd, st);
+        branch_forward(u.phi, xs, true, st, src_ready);
+        conv_fwd(u.pa, xd, st, src_ready);
         layer_stats(u.pa, true, st);
         conv_fwd(u.pb, xs, st, u.pb.operand_of != nullptr);
         layer_stats(u.pb, true, st);
@@ -779,7 +809,7 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
       Layer &L = u.phi[0];
       const float *th = theta_->as<float>();
       if (recompute) {
-        conv_fwd(L, xin[0], st);
+        conv_fwd(L, xin[0], st, src_ready);
         layer_stats(L, true, st);
         if (u.d.maxpool) {
           // recompute the pre-pool activation and argmax (outputs go to scratch)
@@ -889,6 +919,7 @@ void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *
       Bf16Out ob = (u.d.kind == PETRA_UNIT_DS && i + 1 < n && units_[i + 1].d.kind == PETRA_UNIT_REV)
                        ? src_operand(units_[i + 1]) : Bf16Out{};
       const int obh = ob.p ? units_[i + 1].src() : -1;
+      bind_fifo_operands(u, slot);
       unit_forward(u, cur, tgt, keep, st, ob, false, obh);
       ready = ob.p != nullptr;
       cur[0] = tgt[0];
@@ -940,7 +971,8 @@ void Stage::enqueue_backward_walk(int last_unit, bool recompute, const float *cx
       float *td[2] = {nullptr, nullptr};
       if (u.d.kind == PETRA_UNIT_DS)
         for (int h = 0; h < 2; ++h) td[h] = u.bd[h] ? u.bd[h]->as<float>() : od[h];
-      unit_backward(u, recompute, xin, cx, nullptr, cd, td, st);
+      bind_fifo_operands(u, slot);  // the forward converted this micro-batch's input into the slot
+      unit_backward(u, recompute, xin, cx, nullptr, cd, td, st, Bf16Out{}, !u.fifo.bslot0.empty());
       cx[0] = xin[0];
       cx[1] = xin[1];
       rox[0] = rox[1] = true;  // FIFO memory: copied out at the end, never written

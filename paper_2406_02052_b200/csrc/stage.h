@@ -49,7 +49,13 @@ struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
   DevPtr &mean() { return mean_[*ctx]; }
   DevPtr &invstd() { return invstd_[*ctx]; }
   Layer *operand_of = nullptr;               // shares that layer's bf16 input operand (same input tensor)
+  bool fifo_backed = false;                  // its bf16 operand lives in the unit's FIFO slot (DS / stem)
+  __nv_bfloat16 *xb_ext = nullptr;           // ... bound to the slot of the tick being enqueued
   DevPtr &xb() { return operand_of ? operand_of->xb() : xb_[*ctx]; }
+  __nv_bfloat16 *xbp() {
+    if (operand_of) return operand_of->xbp();
+    return fifo_backed ? xb_ext : xb_[*ctx]->as<__nv_bfloat16>();
+  }
   int &stats_rows() { return stats_rows_[*ctx]; }
   DevPtr dz, da, dzb;                        // backward-only workspace
   DevPtr w_bf16, wt_bf16;                    // bf16 shadows of the live weights
@@ -62,6 +68,8 @@ struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
 struct Fifo {                // input buffer of a non-reversible unit (reading c5)
   int cap = 0, head = 0, size = 0;
   std::vector<DevPtr> slot0, slot1;   // one tensor (stem) or two halves (DS)
+  std::vector<DevPtr> bslot0, bslot1; // their bf16 conv operands (tensor-core path): converted once
+                                      // in the forward, read again by the backward's recomputation
   std::deque<uint64_t> ids;
   int peak = 0;
 };
@@ -214,6 +222,7 @@ class Stage {
   void unit_backward(Unit &u, bool recompute, const float *xin[2], const float *cur_x[2], float *out_x[2],
                      const float *cur_d[2], float *out_d[2], cudaStream_t st, Bf16Out ob = {},
                      bool src_ready = false);
+  void bind_fifo_operands(Unit &u, int slot);
 };
 
 }  // namespace petra

@@ -40,11 +40,14 @@ def test_stage_memory_categories(precision, k):
         # FIFO: capacity 2(J-j)+1 (1 in the final stage) copies of each non-reversible unit's input
         cap = spec.fifo_capacity if j < len(specs) else 1
         fifo = 0
+        tc = precision == L.BF16_TC
         for u, (B, H, W, C) in zip(us, ins[i0:i0 + counts[j - 1]]):
+            # fp32 input (+ its bf16 conv operands on the tensor-core path: the stem's
+            # 4-channel image copy, both DS halves)
             if u.kind == L.UNIT_STEM:
-                fifo += cap * B * H * W * C * 4
+                fifo += cap * B * H * W * (C * 4 + (4 * 2 if tc else 0))
             elif u.kind == L.UNIT_DS:
-                fifo += cap * 2 * B * H * W * C * 4
+                fifo += cap * 2 * B * H * W * C * (4 + (2 if tc else 0))
         assert m["fifo"] == fifo
         assert m["fifo_live"] == 0
         assert m["total"] == m["params"] + m["optimizer"] + m["shadows"] + m["fifo"] + m["workspace"]
