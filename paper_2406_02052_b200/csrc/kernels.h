@@ -19,14 +19,19 @@ void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *
 bool conv_tc_supported(const ConvGeom &g, int mode);   // mode 0 fwd, 1 dgrad, 2 wgrad
 void conv_tc_prepare();  // one-time kernel attributes (before any graph capture)
 size_t conv_tc_workspace(const ConvGeom &g, int mode);  // split-K workspace bytes
+// BN partial sums written by a conv epilogue: `rows` rows [rows][Co][2] (sum, sum of
+// squares), one per CTA; with `groups` > 1 the CTAs each own one of `groups` column
+// groups of Co/groups channels (CTA r: group r % groups) and write only those columns.
+// rows == 0: not fused (run bn_stats on z).
+struct StatsRows {
+  int rows = 0, groups = 1;
+};
 // z[m][co] = conv(x_bf16, w_bf16), stored fp32 or (z_bf16) bf16.  stats_part (nullable,
-// >= 148*Co*2 floats): the epilogue also writes BN partial sums of z as stored;
-// returns the number of partial rows to merge with bn_stats_from_partials (0 = not
-// fused, run bn_stats on z).
-int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,
+// >= 148*Co*2 floats): the epilogue also writes BN partial sums of z as stored.
+StatsRows conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,
                 bool z_bf16, float *ws, float *stats_part, cudaStream_t st);
-void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float eps, float *mean, float *invstd,
-                            float *rmean, float *rvar, float mom, cudaStream_t st);
+void bn_stats_from_partials(const float *part, StatsRows rows, int N, int64_t M, float eps, float *mean,
+                            float *invstd, float *rmean, float *rvar, float mom, cudaStream_t st);
 // dx (fp32) = addend + conv^T(dz_bf16, wT_bf16)
 void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_padded, const __nv_bfloat16 *wt,
                    const float *addend, float *dx, float *ws, cudaStream_t st);
@@ -36,8 +41,9 @@ void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_padded, c
 // halo kernel (conv_halo.cu): 3x3 stride-1 pass on a padded operand
 void conv_halo_prepare();
 bool conv_halo_eligible(int B, int H, int W, int Cred, int N);
-int conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad, const __nv_bfloat16 *wmat,
-                  const float *addend, void *out, bool out16, float *stats, cudaStream_t st);
+StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad,
+                        const __nv_bfloat16 *wmat, const float *addend, void *out, bool out16, float *stats,
+                        cudaStream_t st);
 
 // out[i] = sum over splits z of part[z * n + i], fixed order (deterministic)
 void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st);
@@ -56,8 +62,8 @@ size_t stem_operand_elems(const ConvGeom &g);  // bf16 elements of the 4-channel
 void image_to_bf16x4(const float *x, __nv_bfloat16 *xq, const ConvGeom &g, cudaStream_t st);
 // z = conv(xq, bf16(w)) stored fp32 or (z_bf16) bf16; w fp32 as stored; fused BN
 // partials as conv_fwd_tc
-int stem_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *xq, const float *w, void *z, bool z_bf16,
-                float *stats_part, cudaStream_t st);
+StatsRows stem_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *xq, const float *w, void *z, bool z_bf16,
+                      float *stats_part, cudaStream_t st);
 // dw (fp32) = sum_pixels dz_bf16 (x) xq
 void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *xq, float *dw, float *ws,
                    cudaStream_t st);
@@ -103,7 +109,8 @@ void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *thet
 void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int C, const float *w,
                            const float *bias, int N, const int32_t *labels, float *feat, float *logits,
                            float *dlogits, float *loss_row, float *dfeat, float *dw, float *db, float *d1,
-                           float *d2, float *loss, int *nonfinite, cudaStream_t st);
+                           float *d2, float *loss, int *nonfinite, float *fc_ws, int64_t fc_ws_floats,
+                           cudaStream_t st);
 void maxpool_fwd(const float *a, int B, int H, int W, int C, int Ho, int Wo, float *o1, float *o2, uint8_t *arg,
                  cudaStream_t st);
 void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, int H, int W, int C, int Ho, int Wo,

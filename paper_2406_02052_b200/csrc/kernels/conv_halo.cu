@@ -43,7 +43,8 @@ struct HaloParams {
   int lead, HR;            // halo rows before the tile group (Wp + 1); rows loaded per halo
   int box_rows;            // rows per TMA box (HR = boxes * box_rows, box_rows % 8 == 0)
   uint32_t a_stage;        // bytes per A stage (HR * 128)
-  int bstages;             // B ring depth
+  int bstages;             // B ring depth (resident: the CB * ntaps weight tiles, loaded once)
+  int resident;            // 1: the whole weight matrix of the (single) N tile stays in smem
   const float *addend;     // nullable, fp32 output only
   void *out;               // [B][H][W][N] fp32 or bf16
   float *stats;            // nullable: one BN partial row per CTA [grid][N][2]
@@ -64,7 +65,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   constexpr int ACC = T * BN;  // TMEM columns per accumulator set
   uint8_t *sA = smem;
   uint8_t *sB = sA + ASTAGES * P.a_stage;
-  uint64_t *afull = reinterpret_cast<uint64_t *>(sB + P.bstages * B_BYTES);
+  uint64_t *afull = reinterpret_cast<uint64_t *>(sB + P.bstages * B_BYTES);  // resident: bstages = CB*ntaps
   uint64_t *aempty = afull + ASTAGES;
   uint64_t *bfull = aempty + ASTAGES;
   uint64_t *bempty = bfull + kMaxBStages;
@@ -72,13 +73,13 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
   uint8_t *sepi = reinterpret_cast<uint8_t *>(afull) + 512;       // [8 warps][32 rows x 144 B]
-  float *sstat = reinterpret_cast<float *>(sepi + kEpiWarps * kEpiWarp);  // [4 lane quarters][N][2]
+  float *sstat = reinterpret_cast<float *>(sepi + kEpiWarps * kEpiWarp);  // [4 lane quarters][BN][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_nt = P.N / BN;
   const int n_work = (int)cdiv(P.Mp, 128 * T) * n_nt;
   const int GHW = P.Hp * P.Wp;
-  const int BS = P.bstages;
+  const int BS = P.resident ? 1 : P.bstages;  // resident: one barrier for the whole weight load
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ASTAGES; ++s) {
@@ -107,6 +108,12 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (lane == 0) {  // ---------------- TMA producer: halo per channel block, B per (channel block, tap)
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
+      if (P.resident) {  // every (channel block, tap) weight tile once, on bfull[0]
+        tc::mbar_arrive_expect_tx(&bfull[0], (uint32_t)P.CB * P.ntaps * B_BYTES);
+        for (int cb = 0; cb < P.CB; ++cb)
+          for (int t = 0; t < P.ntaps; ++t)
+            tc::tma_load_2d(sB + (cb * P.ntaps + t) * B_BYTES, &tmB, &bfull[0], P.wk[t] * P.Cred + cb * 64, 0);
+      }
       for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
         const int mg = w / n_nt, nt = w % n_nt;
         const int r0 = mg * 128 * T - P.lead;  // may be negative: TMA zero-fills
@@ -116,7 +123,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           for (int r = 0; r < P.HR; r += P.box_rows)  // equal boxes, 1 KB-aligned (swizzle-consistent)
             tc::tma_load_2d(sA + as * P.a_stage + r * 128, &tmA, &afull[as], cb * 64, r0 + r);
           if (++as == ASTAGES) { as = 0; aph ^= 1; }
-          for (int t = 0; t < P.ntaps; ++t) {
+          for (int t = 0; t < P.ntaps && !P.resident; ++t) {
             tc::mbar_wait(&bempty[bs], bph ^ 1);
             tc::mbar_arrive_expect_tx(&bfull[bs], B_BYTES);
             tc::tma_load_2d(sB + bs * B_BYTES, &tmB, &bfull[bs], P.wk[t] * P.Cred + cb * 64, nt * BN);
@@ -131,6 +138,10 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
       int it = 0;
+      if (P.resident) {
+        tc::mbar_wait(&bfull[0], 0);
+        tc::tc_fence_after();
+      }
       for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
         const int acc = it & 1;
         tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
@@ -141,9 +152,12 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           tc::tc_fence_after();
           const uint32_t abase = tc::smem_u32(sA + as * P.a_stage) + P.lead * 128;
           for (int t = 0; t < P.ntaps; ++t) {
-            tc::mbar_wait(&bfull[bs], bph);
-            tc::tc_fence_after();
-            const uint64_t bd = tc::sw128_desc(tc::smem_u32(sB + bs * B_BYTES), 16, 1024);
+            if (!P.resident) {
+              tc::mbar_wait(&bfull[bs], bph);
+              tc::tc_fence_after();
+            }
+            const int bslot = P.resident ? cb * P.ntaps + t : bs;
+            const uint64_t bd = tc::sw128_desc(tc::smem_u32(sB + bslot * B_BYTES), 16, 1024);
 #pragma unroll
             for (int tt = 0; tt < T; ++tt) {
               const uint64_t ad = tc::sw128_desc(abase + (tt * 128 + P.off[t]) * 128, 16, 1024);
@@ -151,8 +165,10 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               for (int k = 0; k < 4; ++k)
                 tc::umma_bf16(dtm + tt * BN, ad + 2 * k, bd + 2 * k, idesc, (cb > 0 || t > 0 || k > 0) ? 1u : 0u);
             }
-            tc::umma_commit(&bempty[bs]);
-            if (++bs == BS) { bs = 0; bph ^= 1; }
+            if (!P.resident) {
+              tc::umma_commit(&bempty[bs]);
+              if (++bs == BS) { bs = 0; bph ^= 1; }
+            }
           }
           tc::umma_commit(&aempty[as]);
           if (++as == ASTAGES) { as = 0; aph ^= 1; }
@@ -164,10 +180,10 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int q = warp & 3;
     const int hc = (warp - 2) >> 2;
     const int row = q * 32 + lane;
-    float *my_stat = sstat + (size_t)q * P.N * 2;
+    float *my_stat = sstat + (size_t)q * BN * 2;  // this CTA's N tile (fixed: grid % n_nt == 0)
     uint8_t *ebuf = sepi + (warp - 2) * kEpiWarp;
     if (P.stats) {  // the two warps of a lane quarter share its (column-disjoint) sums
-      for (int i = (warp - 2) * 32 + lane; i < 8 * P.N; i += kEpiWarps * 32) sstat[i] = 0.f;
+      for (int i = (warp - 2) * 32 + lane; i < 8 * BN; i += kEpiWarps * 32) sstat[i] = 0.f;
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
     }
     constexpr int ES = OUT16 ? 2 : 4;
@@ -239,7 +255,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (P.stats) {  // statistics of z as stored (reading c24), from the staged rows
             float s[2], sq[2];
             tc::staged_colsums<OUT16, false>(ebuf, kRowPitch, lane, s, sq);
-            const int col = nt * BN + c + (OUT16 ? 2 * lane : lane);
+            const int col = c + (OUT16 ? 2 * lane : lane);  // column within the N tile
             my_stat[2 * col] += s[0];
             my_stat[2 * col + 1] += sq[0];
             if (OUT16) {
@@ -256,9 +272,9 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      float *g = P.stats + (size_t)blockIdx.x * P.N * 2;
+      float *g = P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_nt) * BN) * 2;
       for (int i = (warp - 2) * 32 + lane; i < 2 * P.N; i += kEpiWarps * 32)
-        g[i] = (sstat[i] + sstat[2 * P.N + i]) + (sstat[4 * P.N + i] + sstat[6 * P.N + i]);
+        g[i] = (sstat[i] + sstat[2 * BN + i]) + (sstat[4 * BN + i] + sstat[6 * BN + i]);
     }
   }
   __syncthreads();
@@ -268,7 +284,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 }
 
-size_t fixed_smem() { return 1024 + 512 + kEpiWarps * kEpiWarp + (size_t)kMaxStatN * 32; }
+size_t fixed_smem() { return 1024 + 512 + kEpiWarps * kEpiWarp + (size_t)256 * 32; }  // stats: BN <= 256
 // the halo of T tiles (128*T + 2*(W+3) rows) as equal TMA boxes of <= 256 rows, each a
 // multiple of 8 rows so every box starts 1 KB-aligned
 void halo_rows(int T, int W, int &box_rows, int &HR) {
@@ -285,7 +301,7 @@ uint32_t a_stage_bytes(int T, int W) {
 
 struct HaloPlan {
   int BN, T, bstages;
-  bool ok;
+  bool ok, resident;
 };
 // Tile group T (weight reuse) and N tile: the largest T whose A halos fit next to >= 3
 // weight stages while the work items still fill 3/4 of a wave (measured: the weight
@@ -293,10 +309,27 @@ struct HaloPlan {
 // zero border adds > 35% rows, or that fill under 3/4 of a wave, stay on the split-K
 // path of conv_tc.cu.
 HaloPlan halo_plan(int B, int H, int W, int Cred, int N) {
-  HaloPlan p{0, 0, 0, false};
+  HaloPlan p{0, 0, 0, false, false};
   if (Cred % 64 || N % 64) return p;
   const int64_t Mp = (int64_t)B * (H + 2) * (W + 2);
   if (Mp >= ((int64_t)1 << 31) || Mp * 100 > (int64_t)B * H * W * 135) return p;
+  // Weight-resident plan: one N tile (BN = N <= 128) whose 9 * Cred x N weights stay in
+  // smem for the whole persistent CTA, so only the halos stream from L2 (~42 B/clk per
+  // SM on B200: the weight stream, not the MMA, bounds the streamed plan for C = 64).
+  static const bool resident_ok = env_int("PETRA_HALO_RESIDENT", 1) != 0;
+  if (resident_ok && N <= 128) {
+    const size_t wbytes = (size_t)9 * (Cred / 64) * N * 128;
+    for (int T : {4, 2, 1}) {
+      if (T * N * 2 > 512) continue;
+      if (fixed_smem() + 2 * (size_t)a_stage_bytes(T, W) + wbytes > kSmemLimit) continue;
+      if (cdiv(Mp, 128 * T) < (kNumSMs * 3 + 3) / 4) continue;
+      p.BN = N;
+      p.T = T;
+      p.bstages = 9 * (Cred / 64);
+      p.ok = p.resident = true;
+      return p;
+    }
+  }
   for (int pass = 0; pass < 1; ++pass) {
     const int64_t min_work = (kNumSMs * 3 + 3) / 4;
     for (int bn : {256, 128, 64}) {
@@ -318,11 +351,17 @@ HaloPlan halo_plan(int B, int H, int W, int Cred, int N) {
   return p;
 }
 
+// a multiple of the N-tile count: every CTA's work items share one N tile
+int halo_grid(int work, int n_nt) {
+  const int g = conv_grid(work);
+  return std::max(n_nt, g / n_nt * n_nt);
+}
+
 template <int BN, int T, bool OUT16>
 void launch(const CUtensorMap &ta, const CUtensorMap &tb, const HaloParams &P, cudaStream_t st) {
   const int work = (int)cdiv(P.Mp, 128 * T) * (P.N / BN);
   const size_t smem = fixed_smem() + 2 * (size_t)P.a_stage + (size_t)P.bstages * BN * 128;
-  launch_k(conv_halo_kernel<BN, T, OUT16>, conv_grid(work), kThreads, smem, st, ta, tb, P);
+  launch_k(conv_halo_kernel<BN, T, OUT16>, halo_grid(work, P.N / BN), kThreads, smem, st, ta, tb, P);
   PETRA_LAUNCH_CHECK();
 }
 
@@ -366,8 +405,9 @@ bool conv_halo_eligible(int B, int H, int W, int Cred, int N) { return halo_plan
 // out[b][h][w][n] (= addend +) sum_{tap, c} a_pad[b][h+kh][w+kw][c] * wmat[n][wk(tap)*Cred + c]
 // a_pad: [B][H+2][W+2][Cred] bf16 with zero borders; wmat: [N][9*Cred] bf16
 // (forward: x and w; stride-1 dgrad: dz and the flipped/transposed wT, same tap order).
-int conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad, const __nv_bfloat16 *wmat,
-                  const float *addend, void *out, bool out16, float *stats, cudaStream_t st) {
+StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad,
+                        const __nv_bfloat16 *wmat, const float *addend, void *out, bool out16, float *stats,
+                        cudaStream_t st) {
   const HaloPlan pl = halo_plan(B, H, W, Cred, N);
   if (!pl.ok) throw PetraError(PETRA_E_UNSUPPORTED, "conv_halo_run: geometry");
   if (out16 && addend) throw PetraError(PETRA_E_ARG, "conv_halo_run: addend needs an fp32 output");
@@ -391,9 +431,10 @@ int conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_p
   halo_rows(pl.T, W, P.box_rows, P.HR);
   P.a_stage = (uint32_t)P.HR * 128;
   P.bstages = pl.bstages;
+  P.resident = pl.resident ? 1 : 0;
   P.addend = addend;
   P.out = out;
-  P.stats = N <= kMaxStatN ? stats : nullptr;
+  P.stats = stats;
   cuuint64_t adims[2] = {(cuuint64_t)Cred, (cuuint64_t)P.Mp};
   cuuint64_t ast[1] = {(cuuint64_t)Cred * 2};
   cuuint32_t abox[2] = {64, (cuuint32_t)P.box_rows};
@@ -403,7 +444,11 @@ int conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_p
   if (out16) dispatch<true>(pl.BN, pl.T, ta, tb, P, st);
   else dispatch<false>(pl.BN, pl.T, ta, tb, P, st);
   const int work = (int)cdiv(P.Mp, 128 * pl.T) * (N / pl.BN);
-  return P.stats ? conv_grid(work) : 0;
+  if (!P.stats) return {};
+  StatsRows r;
+  r.groups = N / pl.BN;
+  r.rows = halo_grid(work, r.groups);
+  return r;
 }
 
 }  // namespace petra

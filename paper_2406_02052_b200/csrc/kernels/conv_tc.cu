@@ -103,7 +103,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
   uint8_t *sepi = smem + STAGES * STAGE_BYTES + 1024;      // [8 warps][2][32 x 128 B] epilogue staging
-  float *sstat = reinterpret_cast<float *>(sepi + kEpiBytes);  // [4 lane quarters][N][2] BN partial sums
+  float *sstat = reinterpret_cast<float *>(sepi + kEpiBytes);  // [4 lane quarters][BN][2] BN partial sums
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_n = P.N / BN;
@@ -191,11 +191,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int q = warp & 3;             // TMEM lane quarter this warp may access
     const int hc = (warp - 2) >> 2;     // column half: chunks hc, hc + 2, ... of each tile
     const int row = q * 32 + lane;
-    float *my_stat = sstat + (size_t)q * P.N * 2;
+    float *my_stat = sstat + (size_t)q * BN * 2;  // this CTA's N tile (fixed: grid % n_tiles_n == 0)
     uint8_t *ebuf = sepi + (warp - 2) * 2 * kEpiBuf;
     int eb = 0;  // staging buffer to fill next
     if (P.stats) {  // the two warps of a lane quarter share its (column-disjoint) sums
-      for (int i = (warp - 2) * 32 + lane; i < 8 * P.N; i += kEpiWarps * 32) sstat[i] = 0.f;
+      for (int i = (warp - 2) * 32 + lane; i < 8 * BN; i += kEpiWarps * 32) sstat[i] = 0.f;
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
     }
     if (lane == 0) {
@@ -272,7 +272,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (P.stats) {  // BN batch statistics of z as stored (reading c24), from the staged rows
             float s[2], sq[2];
             tc::staged_colsums<OUT16, true>(staged, 128, lane, s, sq);
-            const int col = nt * BN + c + (OUT16 ? 2 * lane : lane);
+            const int col = c + (OUT16 ? 2 * lane : lane);  // column within the N tile
             my_stat[2 * col] += s[0];
             my_stat[2 * col + 1] += sq[0];
             if (OUT16) {
@@ -289,9 +289,9 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (lane == 0) tc::bulk_wait_all();
     if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      float *g = P.stats + (size_t)blockIdx.x * P.N * 2;
-      for (int i = (warp - 2) * 32 + lane; i < 2 * P.N; i += kEpiWarps * 32)
-        g[i] = (sstat[i] + sstat[2 * P.N + i]) + (sstat[4 * P.N + i] + sstat[6 * P.N + i]);
+      float *g = P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2;
+      for (int i = (warp - 2) * 32 + lane; i < 2 * BN; i += kEpiWarps * 32)
+        g[i] = (sstat[i] + sstat[2 * BN + i]) + (sstat[4 * BN + i] + sstat[6 * BN + i]);
     }
   }
   __syncthreads();
@@ -305,8 +305,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 // block of 32 warps per 32 channels, warp w sums rows w, w+32, ... in fp64 (lane =
 // channel, coalesced), then warp 0 combines the 32 warp sums in a fixed order;
 // optional running-stat EMA (reading c9).
-__global__ void __launch_bounds__(1024) stats_finalize_kernel(const float *__restrict__ part, int P, int N, int64_t M,
-                                                              float eps, float *__restrict__ mean,
+__global__ void __launch_bounds__(1024) stats_finalize_kernel(const float *__restrict__ part, int P, int groups, int N,
+                                                              int64_t M, float eps, float *__restrict__ mean,
                                                               float *__restrict__ invstd, float *__restrict__ rmean,
                                                               float *__restrict__ rvar, float mom) {
   pdl_wait_trigger();
@@ -315,15 +315,17 @@ __global__ void __launch_bounds__(1024) stats_finalize_kernel(const float *__res
   const int c = blockIdx.x * 32 + lane;
   double a0 = 0, a1 = 0, b0 = 0, b1 = 0;
   if (c < N) {
-    int i = w;
-    for (; i + 32 < P; i += 64) {
-      const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)i * N + c) * 2);
-      const float2 v = *reinterpret_cast<const float2 *>(part + ((size_t)(i + 32) * N + c) * 2);
+    // rows of this column's group: r = grp, grp + groups, ... (n rows); warp w takes j = w, w + 32, ...
+    const int grp = c / (N / groups), n = (P - grp + groups - 1) / groups;
+    int j = w;
+    for (; j + 32 < n; j += 64) {
+      const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)(grp + j * groups) * N + c) * 2);
+      const float2 v = *reinterpret_cast<const float2 *>(part + ((size_t)(grp + (j + 32) * groups) * N + c) * 2);
       a0 += u.x; b0 += u.y;
       a1 += v.x; b1 += v.y;
     }
-    if (i < P) {
-      const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)i * N + c) * 2);
+    if (j < n) {
+      const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)(grp + j * groups) * N + c) * 2);
       a0 += u.x; b0 += u.y;
     }
   }
@@ -719,14 +721,22 @@ constexpr size_t conv_smem(int BN, size_t stat_bytes) {
   return 1024 + (size_t)conv_stages(BN) * (A_BYTES + BN * BK * 2) + 1024 + kEpiBytes + stat_bytes;
 }
 
+// grid of a conv kernel whose epilogue writes BN partials: a multiple of the N-tile
+// count, so every CTA's work items share one N tile (w = blockIdx + k * grid)
+int conv_stats_grid(int work, int n_tiles_n) {
+  const int g = conv_grid(work);
+  return std::max(n_tiles_n, g / n_tiles_n * n_tiles_n);
+}
+
 template <int BN, bool OUT16>
 void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P, cudaStream_t st) {
   constexpr int STAGES = conv_stages(BN);
-  const size_t smem = conv_smem(BN, P.stats ? (size_t)P.N * 32 : 0);  // attribute: conv_tc_prepare
+  const size_t smem = conv_smem(BN, P.stats ? (size_t)BN * 32 : 0);  // attribute: conv_tc_prepare
   const int work = (P.M / BM) * (P.N / BN) * P.splits;
+  const int grid = conv_stats_grid(work, P.N / BN);
   const CUtensorMap to = out_map(P.out, OUT16, P);
   const CUtensorMap tw = P.splits > 1 ? ws_map(P.ws, P.N, (int64_t)P.splits * P.M) : to;
-  launch_k(conv_tc_kernel<BN, STAGES, OUT16>, conv_grid(work), kConvThreads, smem, st, ta, tb, to, tw, P);
+  launch_k(conv_tc_kernel<BN, STAGES, OUT16>, grid, kConvThreads, smem, st, ta, tb, to, tw, P);
   PETRA_LAUNCH_CHECK();
   if (P.splits > 1) {
     int64_t n = (int64_t)P.M * P.N / 4;
@@ -746,7 +756,7 @@ void launch_any(const CUtensorMap &ta, const __nv_bfloat16 *w, int wrows, int wK
     P.splits = 1;
     P.kb_per_split = P.ntaps * P.CB;
   }
-  if (P.splits > 1 || P.N > kMaxStatN) P.stats = nullptr;  // stats need final z (split-K: standalone pass)
+  if (P.splits > 1) P.stats = nullptr;  // stats need final z (split-K: standalone pass)
   if (out16 && P.addend) throw PetraError(PETRA_E_ARG, "conv_tc: addend needs an fp32 output");
   CUtensorMap tb = mat_map(w, wrows, wK, pl.BN);
   if (out16) {
@@ -768,7 +778,8 @@ bool geom_ok(const ConvGeom &g) {
   return true;
 }
 
-int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const __nv_bfloat16 *w, void *out, bool out16,
+StatsRows run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const __nv_bfloat16 *w, void *out,
+                  bool out16,
             float *ws, float *stats, cudaStream_t st) {
   if (x_pad && g.k == 3 && g.s == 1 && conv_halo_eligible(g.B, g.H, g.W, g.Ci, g.Co))
     return conv_halo_run(g.B, g.H, g.W, g.Ci, g.Co, x, w, nullptr, out, out16, stats, st);
@@ -797,9 +808,12 @@ int run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const __nv_bf
   P.stats = stats;
   CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, t.Wb, t.R, t.NB, g.s, x_pad);
   launch_any(ta, w, g.Co, g.K(), P, ws, out16, st);
-  if (!P.stats) return 0;
+  if (!P.stats) return {};
   const int BN = conv_plan(P.M, P.N, P.ntaps * P.CB).BN;
-  return conv_grid((P.M / BM) * (P.N / BN) * P.splits);  // partial rows written (one per CTA)
+  StatsRows r;
+  r.groups = P.N / BN;
+  r.rows = conv_stats_grid((P.M / BM) * (P.N / BN) * P.splits, r.groups);  // one partial row per CTA
+  return r;
 }
 
 void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_pad, const __nv_bfloat16 *wt, const float *addend,
@@ -943,14 +957,15 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode) {
   return p.splits > 1 ? (size_t)p.splits * M * N * sizeof(float) : 0;
 }
 
-int conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,
+StatsRows conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,
                 bool z_bf16, float *ws, float *stats_part, cudaStream_t st) {
   return run_fwd(g, x, x_padded, w, z, z_bf16, ws, stats_part, st);
 }
 
-void bn_stats_from_partials(const float *part, int P, int N, int64_t M, float eps, float *mean, float *invstd,
-                            float *rmean, float *rvar, float mom, cudaStream_t st) {
-  launch_k(stats_finalize_kernel, (unsigned)cdiv(N, 32), 1024, 0, st, part, P, N, M, eps, mean, invstd, rmean, rvar, mom);
+void bn_stats_from_partials(const float *part, StatsRows rows, int N, int64_t M, float eps, float *mean,
+                            float *invstd, float *rmean, float *rvar, float mom, cudaStream_t st) {
+  launch_k(stats_finalize_kernel, (unsigned)cdiv(N, 32), 1024, 0, st, part, rows.rows, rows.groups, N, M, eps, mean,
+           invstd, rmean, rvar, mom);
   PETRA_LAUNCH_CHECK();
 }
 

@@ -101,20 +101,78 @@ __global__ void gap_kernel(const float *__restrict__ x1, const float *__restrict
   feat[(int64_t)b * 2 * C + c2] = s / (float)HW;
 }
 
-__global__ void fc_fwd_kernel(const float *__restrict__ feat, const float *__restrict__ w,
-                              const float *__restrict__ bias, int B, int Cin, int N, float *__restrict__ logits) {
+// Small fp32 GEMM of the classifier: C[m][n] = sum_k A(m, k) B(k, n) (+ bias[n]), with
+// A(m, k) = A[m*sam + k*sak] and B(k, n) = B[k*sbk + n*sbn] (the transposes of the FC
+// forward / weight gradient / input gradient).  16 x 32 output tiles, 128 threads of 2 x 2
+// outputs, K in chunks of 32 through shared memory; blockIdx.z = a K split of kspan
+// (partials to ws[z][M][N], summed in z order by fc_splitk_reduce: deterministic).  M =
+// batch is small: small tiles and split K keep enough blocks resident to hide latency.
+constexpr int GM = 16, GN = 32, GK = 32;
+__global__ void __launch_bounds__(128) fc_gemm_kernel(const float *__restrict__ A, int64_t sam, int64_t sak,
+                                                      const float *__restrict__ Bm, int64_t sbk, int64_t sbn,
+                                                      const float *__restrict__ bias, int M, int N, int K,
+                                                      int kspan, float *__restrict__ C) {
   pdl_wait_trigger();
-  // one warp per (b, n)
-  int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (gw >= B * N) return;
-  int b = gw / N, n = gw - b * N;
-  float s = 0.f;
-  for (int c = lane; c < Cin; c += 32) s = fmaf(feat[(int64_t)b * Cin + c], w[(int64_t)n * Cin + c], s);
+  __shared__ float sa[GK][GM + 1], sb[GK][GN + 1];
+  const int m0 = blockIdx.y * GM, n0 = blockIdx.x * GN;
+  const int kbeg = blockIdx.z * kspan, kend = min(K, kbeg + kspan);
+  C += (int64_t)blockIdx.z * M * N;
+  if (gridDim.z > 1) bias = nullptr;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 8 threads: cols 2tx.., rows 2ty..
+  float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+  for (int k0 = kbeg; k0 < kend; k0 += GK) {
+    // consecutive threads walk the operand's contiguous index (coalesced loads)
+    for (int i = threadIdx.x; i < GK * GM; i += 128) {
+      const bool kfast = sak == 1;
+      const int kk = kfast ? i % GK : i / GM, mm = kfast ? i / GK : i % GM, m = m0 + mm, k = k0 + kk;
+      sa[kk][mm] = (m < M && k < kend) ? A[m * sam + k * sak] : 0.f;
+    }
+    for (int i = threadIdx.x; i < GK * GN; i += 128) {
+      const bool kfast = sbk == 1;
+      const int kk = kfast ? i % GK : i / GN, nn = kfast ? i / GK : i % GN, n = n0 + nn, k = k0 + kk;
+      sb[kk][nn] = (n < N && k < kend) ? Bm[k * sbk + n * sbn] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < GK; ++kk) {
+      const float a0 = sa[kk][2 * ty], a1 = sa[kk][2 * ty + 1];
+      const float b0 = sb[kk][2 * tx], b1 = sb[kk][2 * tx + 1];
+      acc[0][0] = fmaf(a0, b0, acc[0][0]);
+      acc[0][1] = fmaf(a0, b1, acc[0][1]);
+      acc[1][0] = fmaf(a1, b0, acc[1][0]);
+      acc[1][1] = fmaf(a1, b1, acc[1][1]);
+    }
+    __syncthreads();
+  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) logits[(int64_t)b * N + n] = s + bias[n];
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int m = m0 + 2 * ty + i, n = n0 + 2 * tx + j;
+      if (m < M && n < N) C[(int64_t)m * N + n] = acc[i][j] + (bias ? bias[n] : 0.f);
+    }
 }
+
+__global__ void fc_splitk_reduce_kernel(const float *__restrict__ ws, int splits, int64_t n, int N,
+                                        const float *__restrict__ bias, float *__restrict__ C) {
+  pdl_wait_trigger();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += ws[(int64_t)z * n + i];
+    C[i] = s + (bias ? bias[i % N] : 0.f);
+  }
+}
+
+// bias gradient: db[n] = sum_b dlogits[b][n]
+__global__ void fc_bias_grad_kernel(const float *__restrict__ dlogits, int B, int N, float *__restrict__ db) {
+  pdl_wait_trigger();
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float s = 0.f;
+  for (int b = 0; b < B; ++b) s += dlogits[(int64_t)b * N + n];
+  db[n] = s;
+}
+
 
 __global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__restrict__ labels, int B, int N,
                           float *__restrict__ dlogits, float *__restrict__ loss_row) {
@@ -173,33 +231,7 @@ __global__ void loss_mean_kernel(const float *__restrict__ loss_row, int B, floa
   }
 }
 
-__global__ void fc_bwd_w_kernel(const float *__restrict__ dlogits, const float *__restrict__ feat, int B, int Cin,
-                                int N, float *__restrict__ dw, float *__restrict__ db) {
-  pdl_wait_trigger();
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < (int64_t)N * Cin) {
-    int n = (int)(i / Cin), c = (int)(i - (int64_t)n * Cin);
-    float s = 0.f;
-    for (int b = 0; b < B; ++b) s = fmaf(dlogits[(int64_t)b * N + n], feat[(int64_t)b * Cin + c], s);
-    dw[i] = s;
-  }
-  if (i < N) {
-    float s = 0.f;
-    for (int b = 0; b < B; ++b) s += dlogits[(int64_t)b * N + i];
-    db[i] = s;
-  }
-}
 
-__global__ void fc_bwd_x_kernel(const float *__restrict__ dlogits, const float *__restrict__ w, int B, int Cin,
-                                int N, float *__restrict__ dfeat) {
-  pdl_wait_trigger();
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)B * Cin) return;
-  int b = (int)(i / Cin), c = (int)(i - (int64_t)b * Cin);
-  float s = 0.f;
-  for (int n = 0; n < N; ++n) s = fmaf(dlogits[(int64_t)b * N + n], w[(int64_t)n * Cin + c], s);
-  dfeat[i] = s;
-}
 
 __global__ void gap_bwd_kernel(const float *__restrict__ dfeat, int B, int HW, int C, float *__restrict__ d1,
                                float *__restrict__ d2) {
@@ -373,21 +405,43 @@ void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *thet
 void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int C, const float *w,
                            const float *bias, int N, const int32_t *labels, float *feat, float *logits,
                            float *dlogits, float *loss_row, float *dfeat, float *dw, float *db, float *d1,
-                           float *d2, float *loss, int *nonfinite, cudaStream_t st) {
+                           float *d2, float *loss, int *nonfinite, float *fc_ws, int64_t fc_ws_floats,
+                           cudaStream_t st) {
   int Cin = 2 * C;
   launch_k(gap_kernel, dim3((unsigned)cdiv(Cin, 128), B), 128, 0, st, x1, x2, B, HW, C, feat);
   PETRA_LAUNCH_CHECK();
-  launch_k(fc_fwd_kernel, (unsigned)cdiv((int64_t)B * N * 32, 256), 256, 0, st, feat, w, bias, B, Cin, N, logits);
-  PETRA_LAUNCH_CHECK();
+  auto gemm = [&](const float *A, int64_t sam, int64_t sak, const float *Bm, int64_t sbk, int64_t sbn,
+                  const float *bs, int M, int Nn, int K, float *C) {
+    // split K until ~2048 blocks or 8 chunks per block, within the workspace
+    const int64_t tiles = cdiv(Nn, GN) * cdiv(M, GM);
+    int splits = 1;
+    while (splits < 64 && tiles * splits * 2 <= 2048 && cdiv(K, (int64_t)GK * splits * 2) >= 1 &&
+           (int64_t)(splits * 2) * M * Nn <= fc_ws_floats)
+      splits *= 2;
+    const int kspan = (int)(cdiv(cdiv(K, splits), GK) * GK);
+    splits = (int)cdiv(K, kspan);
+    launch_k(fc_gemm_kernel, dim3((unsigned)cdiv(Nn, GN), (unsigned)cdiv(M, GM), (unsigned)splits), 128, 0, st, A,
+             sam, sak, Bm, sbk, sbn, bs, M, Nn, K, kspan, splits > 1 ? fc_ws : C);
+    PETRA_LAUNCH_CHECK();
+    if (splits > 1) {
+      const int64_t n = (int64_t)M * Nn;
+      launch_k(fc_splitk_reduce_kernel, (unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st, fc_ws,
+               splits, n, Nn, bs, C);
+      PETRA_LAUNCH_CHECK();
+    }
+  };
+  // logits[b][n] = sum_c feat[b][c] w[n][c] + bias[n]
+  gemm(feat, Cin, 1, w, 1, Cin, bias, B, N, Cin, logits);
   launch_k(ce_kernel, B, 256, 0, st, logits, labels, B, N, dlogits, loss_row);
   PETRA_LAUNCH_CHECK();
   launch_k(loss_mean_kernel, 1, 32, 0, st, loss_row, B, loss, nonfinite);
   PETRA_LAUNCH_CHECK();
-  launch_k(fc_bwd_w_kernel, (unsigned)cdiv(std::max<int64_t>((int64_t)N * Cin, N), 256), 256, 0, st, dlogits, feat, B,
-                                                                                               Cin, N, dw, db);
+  // dw[n][c] = sum_b dlogits[b][n] feat[b][c];  db[n] = sum_b dlogits[b][n]
+  gemm(dlogits, 1, N, feat, Cin, 1, nullptr, N, Cin, B, dw);
+  launch_k(fc_bias_grad_kernel, (unsigned)cdiv(N, 256), 256, 0, st, dlogits, B, N, db);
   PETRA_LAUNCH_CHECK();
-  launch_k(fc_bwd_x_kernel, (unsigned)cdiv((int64_t)B * Cin, 256), 256, 0, st, dlogits, w, B, Cin, N, dfeat);
-  PETRA_LAUNCH_CHECK();
+  // dfeat[b][c] = sum_n dlogits[b][n] w[n][c]
+  gemm(dlogits, N, 1, w, Cin, 1, nullptr, B, Cin, N, dfeat);
   launch_k(gap_bwd_kernel, ew_grid((int64_t)B * HW * C), 256, 0, st, dfeat, B, HW, C, d1, d2);
   PETRA_LAUNCH_CHECK();
 }

@@ -469,8 +469,8 @@ size_t stem_tc_workspace(const ConvGeom &g) {
   return w.splits > 1 ? (size_t)w.splits * g.Co * g.K() * sizeof(float) : 0;
 }
 
-int stem_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *xq, const float *w, void *z, bool z_bf16,
-                float *stats_part, cudaStream_t st) {
+StatsRows stem_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *xq, const float *w, void *z, bool z_bf16,
+                      float *stats_part, cudaStream_t st) {
   if (!stem_tc_supported(g)) throw PetraError(PETRA_E_UNSUPPORTED, "stem_fwd_tc: geometry");
   stem_tc_prepare();
   StemParams P = base_params(g);
@@ -490,7 +490,9 @@ int stem_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *xq, const float *w, void
     else launch_k(stem_fwd_kernel<256, false>, grid, kThreads, smem, st, P);
   }
   PETRA_LAUNCH_CHECK();
-  return stats_part ? grid : 0;
+  StatsRows r;
+  r.rows = stats_part ? grid : 0;  // one N tile (BN = Co): every CTA writes all columns
+  return r;
 }
 
 void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat16 *xq, float *dw, float *ws,

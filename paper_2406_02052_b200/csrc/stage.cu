@@ -355,6 +355,8 @@ void Stage::build() {
     dlogits_ = dalloc((int64_t)B * t.d.classes * sizeof(float));
     lossrow_ = dalloc((int64_t)B * sizeof(float));
     dfeat_ = dalloc((int64_t)B * Cin * sizeof(float));
+    fc_ws_floats_ = 16 * (int64_t)B * std::max(Cin, t.d.classes);  // split-K partials of the FC GEMMs
+    fc_ws_ = dalloc(fc_ws_floats_ * sizeof(float));
     for (int h = 0; h < 2; ++h) tail_d_[h] = dalloc(t.in.numel() * sizeof(float));
   }
 
@@ -587,12 +589,12 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
 
 void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
   float *b = bufs_->as<float>();
-  if (L.stats_rows() > 0) {  // sums already produced by the tensor-core conv epilogue
-    ProfScope ps("bn_stats_merge", st, 0.0, 8.0 * L.stats_rows() * L.g.Co);
+  if (L.stats_rows().rows > 0) {  // sums already produced by the tensor-core conv epilogue
+    ProfScope ps("bn_stats_merge", st, 0.0, 8.0 * L.stats_rows().rows * L.g.Co / L.stats_rows().groups);
     bn_stats_from_partials(reinterpret_cast<const float *>(part()->p), L.stats_rows(), L.g.Co, L.g.M(), desc_.bn_eps,
                            L.mean()->as<float>(), L.invstd()->as<float>(), running ? b + L.rm_off : nullptr,
                            running ? b + L.rv_off : nullptr, desc_.bn_momentum, st);
-    L.stats_rows() = 0;
+    L.stats_rows() = StatsRows{};
     return;
   }
   ProfScope ps("bn_stats", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co);
@@ -1011,7 +1013,8 @@ void Stage::enqueue_tail(const float *x1, const float *x2, const int32_t *labels
     tail_forward_backward(cur[0], cur[1], desc_.batch, t.in.H * t.in.W, t.in.C, th + t.fc_w, th + t.fc_b,
                           t.d.classes, labels, feat_->as<float>(), logits_->as<float>(), dlogits_->as<float>(),
                           lossrow_->as<float>(), dfeat_->as<float>(), gr + t.fc_w, gr + t.fc_b,
-                          tail_d_[0]->as<float>(), tail_d_[1]->as<float>(), loss, nonfinite_->as<int>(), st);
+                          tail_d_[0]->as<float>(), tail_d_[1]->as<float>(), loss, nonfinite_->as<int>(),
+                          fc_ws_->as<float>(), fc_ws_floats_, st);
   }
   // the stage's own forward buffers and gradient buffers are written in place
   const float *cx[2] = {cur[0], cur[1]}, *cd[2] = {tail_d_[0]->as<float>(), tail_d_[1]->as<float>()};

@@ -42,7 +42,7 @@ struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
   // forward and the backward of a pipeline tick run concurrently on two streams, so
   // everything either writes has one copy per context; *ctx selects the live one.
   DevPtr z_[2], a_[2], mean_[2], invstd_[2], xb_[2];
-  int stats_rows_[2] = {0, 0};               // > 0: BN partials written by the conv epilogue
+  StatsRows stats_rows_[2];                  // rows > 0: BN partials written by the conv epilogue
   const int *ctx = nullptr;
   DevPtr &z() { return z_[*ctx]; }
   DevPtr &a() { return a_[*ctx]; }
@@ -56,7 +56,7 @@ struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
     if (operand_of) return operand_of->xbp();
     return fifo_backed ? xb_ext : xb_[*ctx]->as<__nv_bfloat16>();
   }
-  int &stats_rows() { return stats_rows_[*ctx]; }
+  StatsRows &stats_rows() { return stats_rows_[*ctx]; }
   DevPtr dz, da, dzb;                        // backward-only workspace
   DevPtr w_bf16, wt_bf16;                    // bf16 shadows of the live weights
   bool z16 = false;                          // z stored in bf16 (tensor-core conv output, reading c24)
@@ -170,7 +170,8 @@ class Stage {
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
   DevPtr nonfinite_;
   // tail workspace
-  DevPtr feat_, logits_, dlogits_, lossrow_, dfeat_, tail_d_[2];
+  DevPtr feat_, logits_, dlogits_, lossrow_, dfeat_, tail_d_[2], fc_ws_;
+  int64_t fc_ws_floats_ = 0;
   // bf16 shadows of stage-level stream halves (TC path)
   int64_t version_ = 0;                          // optimizer updates applied
   int64_t t_ = 1;                                // Alg. 1 step counter t (reading c12: starts at 1)
