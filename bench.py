@@ -194,6 +194,10 @@ def run_ours(a):
     # cost model (slowest GPU's compute + its cross-GPU message bytes / NVLink)
     counts = (PM.partition(units, a.stages, a.batch, H, H, 3) if world == 1
               else PM.partition_comm(units, a.stages, world, a.batch, H, H, 3))
+    if a.partition:  # explicit units per stage
+        counts = [int(x) for x in a.partition.split(",")]
+        if len(counts) != a.stages or sum(counts) != len(units):
+            raise SystemExit(f"--partition {a.partition}: need {a.stages} counts summing to {len(units)}")
     prec = L.BF16_TC if a.precision == "bf16" else L.FP32
     specs = PM.stage_specs(units, counts, a.batch, (H, H, 3), prec, WD[a.model])
     stage_rank = contiguous_stage_ranks(a.stages, world)
@@ -411,6 +415,7 @@ def main():
     ap.add_argument("--stages", type=int, default=4)
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", default="", help="units per stage, e.g. 5,4,5,4 (default: FLOP-balanced)")
     a = ap.parse_args()
     # at least one stage per GPU: J = max(--stages, world) (the paper's RevNets have
     # 10-18 units, so J up to 8 always partitions)
