@@ -159,33 +159,35 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
-        int mt, nt, sp, kb0, kb1;
-        decode(w, mt, nt, sp, kb0, kb1);
-        const int acc = it & 1;
-        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+  } else if (warp == 1) {  // ---------------- MMA issuer: warp-uniform loop, elected lane issues
+    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      int mt, nt, sp, kb0, kb1;
+      decode(w, mt, nt, sp, kb0, kb1);
+      const int acc = it & 1;
+      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      const uint32_t dtm = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        const uint32_t dtm = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          tc::mbar_wait(&full[stage], phase);
-          tc::tc_fence_after();
-          const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
-          const uint64_t ad = tc::sw128_desc(sa, 16, 1024);
-          const uint64_t bd = tc::sw128_desc(sa + A_BYTES, 16, 1024);
+        const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
+        const uint64_t ad = tc::sw128_desc(sa, 16, 1024);
+        const uint64_t bd = tc::sw128_desc(sa + A_BYTES, 16, 1024);
+        if (tc::elect_one()) {
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // advance 32 B (16 bf16) along K inside the swizzle row
             tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           tc::umma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc::umma_commit(&tfull[acc]);
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (tc::elect_one()) tc::umma_commit(&tfull[acc]);
+      __syncwarp();
     }
   } else {  // ---------------- epilogue warps 2..5
     const int q = warp & 3;             // TMEM lane quarter this warp may access
@@ -480,36 +482,38 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16(128, BN, 1, 1);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
-        int mt, nt, sp;
-        decode(w, mt, nt, sp);
-        const int kb0 = sp * P.kb_per_split, kb1 = min(P.KBtot, kb0 + P.kb_per_split);
-        const int acc = it & 1;
-        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+  } else if (warp == 1) {  // MMA issuer: warp-uniform loop, elected lane issues
+    constexpr uint32_t idesc = tc::idesc_bf16(128, BN, 1, 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      int mt, nt, sp;
+      decode(w, mt, nt, sp);
+      const int kb0 = sp * P.kb_per_split, kb1 = min(P.KBtot, kb0 + P.kb_per_split);
+      const int acc = it & 1;
+      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      const uint32_t dtm = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        const uint32_t dtm = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          tc::mbar_wait(&full[stage], phase);
-          tc::tc_fence_after();
-          const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
-          // MN-major: LBO = next 64-element MN block (8 KB), SBO = next 8 K-rows (1 KB)
-          const uint64_t ad = tc::sw128_desc(sa, HALF_A, 1024);
-          const uint64_t bd = tc::sw128_desc(sa + 2 * HALF_A, HALF_A, 1024);
+        const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
+        // MN-major: LBO = next 64-element MN block (8 KB), SBO = next 8 K-rows (1 KB)
+        const uint64_t ad = tc::sw128_desc(sa, HALF_A, 1024);
+        const uint64_t bd = tc::sw128_desc(sa + 2 * HALF_A, HALF_A, 1024);
+        if (tc::elect_one()) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)  // 16 pixels = 16 rows x 128 B = 2048 B per step
             tc::umma_bf16(dtm, ad + (uint64_t)(k * 2048 >> 4), bd + (uint64_t)(k * 2048 >> 4), idesc,
                           (kb > kb0 || k) ? 1u : 0u);
           tc::umma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc::umma_commit(&tfull[acc]);
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (tc::elect_one()) tc::umma_commit(&tfull[acc]);
+      __syncwarp();
     }
   } else {
     const int q = warp & 3;

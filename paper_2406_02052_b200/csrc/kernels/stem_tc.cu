@@ -160,29 +160,31 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 12) {  // ---------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16(128, BN, 0, 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-        const int acc = it & 1;
-        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+  } else if (warp == 12) {  // ---------------- MMA issuer: warp-uniform loop, elected lane issues
+    constexpr uint32_t idesc = tc::idesc_bf16(128, BN, 0, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      const uint32_t dtm = tmem_base + acc * BN;
+      for (int kb = 0; kb < P.KB; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        const uint32_t dtm = tmem_base + acc * BN;
-        for (int kb = 0; kb < P.KB; ++kb) {
-          tc::mbar_wait(&full[stage], phase);
-          tc::tc_fence_after();
-          const uint64_t ad = tc::sw128_desc(tc::smem_u32(sA + stage * kATile), 16, 1024);
-          const uint64_t bd = tc::sw128_desc(tc::smem_u32(sB + (size_t)kb * BN * 128), 16, 1024);
+        const uint64_t ad = tc::sw128_desc(tc::smem_u32(sA + stage * kATile), 16, 1024);
+        const uint64_t bd = tc::sw128_desc(tc::smem_u32(sB + (size_t)kb * BN * 128), 16, 1024);
+        if (tc::elect_one()) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
           tc::umma_commit(&empty[stage]);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        tc::umma_commit(&tfull[acc]);
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
+      if (tc::elect_one()) tc::umma_commit(&tfull[acc]);
+      __syncwarp();
     }
   } else {  // ---------------- epilogue warps 8..11
     const int q = warp & 3;
@@ -319,34 +321,36 @@ stem_wgrad_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constan
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 12) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16(128, BN, 1, 1);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
-        const int sp = w % P.splits;
-        const int kb0 = sp * P.kb_per_split, kb1 = min(P.KBtot, kb0 + P.kb_per_split);
-        const int acc = it & 1;
-        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+  } else if (warp == 12) {  // MMA issuer: warp-uniform loop, elected lane issues
+    constexpr uint32_t idesc = tc::idesc_bf16(128, BN, 1, 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      const int sp = w % P.splits;
+      const int kb0 = sp * P.kb_per_split, kb1 = min(P.KBtot, kb0 + P.kb_per_split);
+      const int acc = it & 1;
+      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      const uint32_t dtm = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        const uint32_t dtm = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          tc::mbar_wait(&full[stage], phase);
-          tc::tc_fence_after();
-          const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
-          const uint64_t ad = tc::sw128_desc(sa, 8192, 1024);
-          const uint64_t bd = tc::sw128_desc(sa + kATile, 8192, 1024);
+        const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
+        const uint64_t ad = tc::sw128_desc(sa, 8192, 1024);
+        const uint64_t bd = tc::sw128_desc(sa + kATile, 8192, 1024);
+        if (tc::elect_one()) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)  // 16 pixels = 16 rows x 128 B per step
             tc::umma_bf16(dtm, ad + (uint64_t)(k * 2048 >> 4), bd + (uint64_t)(k * 2048 >> 4), idesc,
                           (kb > kb0 || k) ? 1u : 0u);
           tc::umma_commit(&empty[stage]);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        tc::umma_commit(&tfull[acc]);
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
+      if (tc::elect_one()) tc::umma_commit(&tfull[acc]);
+      __syncwarp();
     }
   } else {
     const int q = warp & 3;

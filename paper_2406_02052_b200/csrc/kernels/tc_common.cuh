@@ -111,6 +111,19 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// one lane of a converged warp (the leader): tcgen05 ops are issued from warp-uniform
+// code under this predicate, as CUTLASS does.  Issuing them from a lone diverged lane
+// (if (lane == 0) { ... }) makes the compiler wrap every UTCHMMA in an
+// ELECT / R2UR.BROADCAST / BRA.U.ANY waterfall -- measured ~133 cycles per MMA whatever
+// its N (tools/micro/umma_rate.cu), 4x the 128x64x16 tensor-pipe time.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\telect.sync rx|px, 0xffffffff;\n\t@px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
