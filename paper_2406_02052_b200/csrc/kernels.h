@@ -25,11 +25,20 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode);  // split-K workspace byt
 // rows == 0: not fused (run bn_stats on z).
 struct StatsRows {
   int rows = 0, groups = 1;
+  bool finalized = false;  // mean / invstd (+ running stats) already written by the conv kernel
+};
+// BN finalize done inside a conv kernel by the last CTA of each N-tile group
+struct BnFinalize {
+  float *mean = nullptr, *invstd = nullptr;  // mean == nullptr: leave it to bn_stats_from_partials
+  float *rmean = nullptr, *rvar = nullptr;   // nullable: running-statistics EMA (recomputation only)
+  unsigned *ticket = nullptr;                // >= groups counters, zero between launches
+  float eps = 1e-5f, mom = 0.1f;
+  int64_t count = 0;                         // rows of z
 };
 // z[m][co] = conv(x_bf16, w_bf16), stored fp32 or (z_bf16) bf16.  stats_part (nullable,
 // >= 148*Co*2 floats): the epilogue also writes BN partial sums of z as stored.
 StatsRows conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,
-                bool z_bf16, float *ws, float *stats_part, cudaStream_t st);
+                bool z_bf16, float *ws, float *stats_part, cudaStream_t st, const BnFinalize *fin = nullptr);
 void bn_stats_from_partials(const float *part, StatsRows rows, int N, int64_t M, float eps, float *mean,
                             float *invstd, float *rmean, float *rvar, float mom, cudaStream_t st);
 // dx (fp32) = addend + conv^T(dz_bf16, wT_bf16)
@@ -43,7 +52,7 @@ void conv_halo_prepare();
 bool conv_halo_eligible(int B, int H, int W, int Cred, int N);
 StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad,
                         const __nv_bfloat16 *wmat, const float *addend, void *out, bool out16, float *stats,
-                        cudaStream_t st);
+                        cudaStream_t st, const BnFinalize *fin = nullptr);
 
 // out[i] = sum over splits z of part[z * n + i], fixed order (deterministic)
 void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st);

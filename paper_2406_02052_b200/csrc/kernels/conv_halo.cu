@@ -49,6 +49,7 @@ struct HaloParams {
   const float *addend;     // nullable, fp32 output only
   void *out;               // [B][H][W][N] fp32 or bf16
   float *stats;            // nullable: one BN partial row per CTA [grid][N][2]
+  tc::StatsFinalize fin;   // fin.mean != null: the last CTA of each N-tile group finalizes
 };
 
 // T consecutive 128-row M tiles share every B (weight) stage: the MMA warp applies one
@@ -284,6 +285,10 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       float *g = P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_nt) * BN) * 2;
       for (int i = (warp - 2) * 32 + lane; i < 2 * P.N; i += kEpiWarps * 32)
         g[i] = (sstat[i] + sstat[2 * BN + i]) + (sstat[4 * BN + i] + sstat[6 * BN + i]);
+      if (P.fin.mean) {  // last CTA of the group: mean / invstd (+ running stats) in-kernel
+        tc::finalize_group<kEpiWarps * 32, 1>(P.fin, P.stats, P.N, BN, n_nt, blockIdx.x % n_nt, (warp - 2) * 32 + lane,
+                                              reinterpret_cast<double *>(sepi), tmem_slot + 1);
+      }
     }
   }
   __syncthreads();
@@ -416,7 +421,7 @@ bool conv_halo_eligible(int B, int H, int W, int Cred, int N) { return halo_plan
 // (forward: x and w; stride-1 dgrad: dz and the flipped/transposed wT, same tap order).
 StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad,
                         const __nv_bfloat16 *wmat, const float *addend, void *out, bool out16, float *stats,
-                        cudaStream_t st) {
+                        cudaStream_t st, const BnFinalize *fin) {
   const HaloPlan pl = halo_plan(B, H, W, Cred, N);
   if (!pl.ok) throw PetraError(PETRA_E_UNSUPPORTED, "conv_halo_run: geometry");
   if (out16 && addend) throw PetraError(PETRA_E_ARG, "conv_halo_run: addend needs an fp32 output");
@@ -445,6 +450,10 @@ StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat1
   P.addend = addend;
   P.out = out;
   P.stats = stats;
+  if (stats && fin && fin->mean) {
+    P.fin = *fin;
+    P.fin.count = (int64_t)B * H * W;
+  }
   cuuint64_t adims[2] = {(cuuint64_t)Cred, (cuuint64_t)P.Mp};
   cuuint64_t ast[1] = {(cuuint64_t)Cred * 2};
   cuuint32_t abox[2] = {64, (cuuint32_t)P.box_rows};
@@ -458,6 +467,7 @@ StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat1
   StatsRows r;
   r.groups = N / pl.BN;
   r.rows = halo_grid(work, r.groups);
+  r.finalized = P.fin.mean != nullptr;
   return r;
 }
 

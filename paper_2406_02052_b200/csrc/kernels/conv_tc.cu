@@ -55,6 +55,7 @@ struct ConvTCParams {
   const float *addend;       // nullable (fp32 output only): out = addend + conv
   void *out;                 // [B*OH*OW][N], fp32 or bf16 (OUT16); written by TMA stores through tmO
   float *stats;              // nullable: per-(CTA, epilogue warp) BN partials [grid][4][N][2] (sum, sum sq)
+  tc::StatsFinalize fin;     // fin.mean != null: the last CTA of each N-tile group finalizes
 };
 
 // Epilogue staging: each epilogue warp owns two 4 KB buffers (32 rows x 128 B, the
@@ -294,6 +295,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       float *g = P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2;
       for (int i = (warp - 2) * 32 + lane; i < 2 * BN; i += kEpiWarps * 32)
         g[i] = (sstat[i] + sstat[2 * BN + i]) + (sstat[4 * BN + i] + sstat[6 * BN + i]);
+      if (P.fin.mean) {  // last CTA of the group: mean / invstd (+ running stats) in-kernel
+        tc::finalize_group<kEpiWarps * 32, 1>(P.fin, P.stats, P.N, BN, n_tiles_n, blockIdx.x % n_tiles_n,
+                                              (warp - 2) * 32 + lane, reinterpret_cast<double *>(sepi),
+                                              tmem_slot + 1);  // flag word next to the TMEM address
+      }
     }
   }
   __syncthreads();
@@ -760,7 +766,10 @@ void launch_any(const CUtensorMap &ta, const __nv_bfloat16 *w, int wrows, int wK
     P.splits = 1;
     P.kb_per_split = P.ntaps * P.CB;
   }
-  if (P.splits > 1) P.stats = nullptr;  // stats need final z (split-K: standalone pass)
+  if (P.splits > 1) {  // stats need final z (split-K: standalone pass)
+    P.stats = nullptr;
+    P.fin.mean = nullptr;
+  }
   if (out16 && P.addend) throw PetraError(PETRA_E_ARG, "conv_tc: addend needs an fp32 output");
   CUtensorMap tb = mat_map(w, wrows, wK, pl.BN);
   if (out16) {
@@ -783,10 +792,9 @@ bool geom_ok(const ConvGeom &g) {
 }
 
 StatsRows run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const __nv_bfloat16 *w, void *out,
-                  bool out16,
-            float *ws, float *stats, cudaStream_t st) {
+                  bool out16, float *ws, float *stats, cudaStream_t st, const BnFinalize *fin) {
   if (x_pad && g.k == 3 && g.s == 1 && conv_halo_eligible(g.B, g.H, g.W, g.Ci, g.Co))
-    return conv_halo_run(g.B, g.H, g.W, g.Ci, g.Co, x, w, nullptr, out, out16, stats, st);
+    return conv_halo_run(g.B, g.H, g.W, g.Ci, g.Co, x, w, nullptr, out, out16, stats, st, fin);
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
   ConvTCParams P{};
   P.M = (int)t.M();
@@ -810,6 +818,10 @@ StatsRows run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const _
   P.oss = 1;
   P.out = out;
   P.stats = stats;
+  if (stats && fin && fin->mean) {
+    P.fin = *fin;
+    P.fin.count = g.M();
+  }
   CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, t.Wb, t.R, t.NB, g.s, x_pad);
   launch_any(ta, w, g.Co, g.K(), P, ws, out16, st);
   if (!P.stats) return {};
@@ -817,6 +829,7 @@ StatsRows run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const _
   StatsRows r;
   r.groups = P.N / BN;
   r.rows = conv_stats_grid((P.M / BM) * (P.N / BN) * P.splits, r.groups);  // one partial row per CTA
+  r.finalized = P.fin.mean != nullptr;
   return r;
 }
 
@@ -962,8 +975,8 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode) {
 }
 
 StatsRows conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,
-                bool z_bf16, float *ws, float *stats_part, cudaStream_t st) {
-  return run_fwd(g, x, x_padded, w, z, z_bf16, ws, stats_part, st);
+                bool z_bf16, float *ws, float *stats_part, cudaStream_t st, const BnFinalize *fin) {
+  return run_fwd(g, x, x_padded, w, z, z_bf16, ws, stats_part, st, fin);
 }
 
 void bn_stats_from_partials(const float *part, StatsRows rows, int N, int64_t M, float eps, float *mean,

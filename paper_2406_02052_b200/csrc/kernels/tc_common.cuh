@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include "../kernels.h"
+
 namespace petra {
 namespace tc {
 
@@ -210,6 +212,64 @@ __device__ __forceinline__ void staged_colsums(const uint8_t *buf, int pitch, in
       q[0] = fmaf(f, f, q[0]);
     }
   }
+}
+
+// In-kernel BN finalize by the last CTA of an N-tile group (the conv epilogues).
+// Every CTA has written its partial row [N][2] (sum, sum of squares) for the BN columns
+// of its group `grp` (rows grp, grp + groups, ...; rows_g of them).  Called by the
+// NT epilogue threads (tid 0..NT-1) after a named barrier that follows those writes;
+// `bar` / NT name that barrier.  The CTA that takes the last ticket of the group
+// sums the group's rows in a fixed order (fp64; NT / BN row slices, combined in slice
+// order: deterministic), writes mean / invstd and, when rmean != null, the running
+// statistics (reading c9: biased variance for normalisation, unbiased for the EMA),
+// then resets the ticket for the next launch.  scratch: >= NT * 2 doubles of smem.
+using StatsFinalize = ::petra::BnFinalize;
+template <int NT, int BAR>
+__device__ __forceinline__ void finalize_group(const StatsFinalize &F, const float *part, int N, int BN, int groups,
+                                               int grp, int tid, double *scratch, unsigned *s_flag) {
+  const int rows_g = ((int)gridDim.x - grp + groups - 1) / groups;
+  __threadfence();  // this thread's part of the CTA's partial row, before the ticket
+  asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+  if (tid == 0) *s_flag = atomicAdd(&F.ticket[grp], 1u) == (unsigned)(rows_g - 1) ? 1u : 0u;
+  asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+  if (*s_flag == 0u) return;
+  __threadfence();  // the other CTAs' rows (they fenced before their tickets)
+  const int S = NT / BN > 0 ? NT / BN : 1;  // row slices per column
+  for (int c0 = 0; c0 < BN; c0 += NT / S) {
+    const int c = c0 + tid % (NT / S), sl = tid / (NT / S);
+    double s = 0.0, ss = 0.0;
+    if (c < BN && sl < S) {
+      const float *p = part + ((size_t)grp * N + (size_t)grp * BN + c) * 2;
+      for (int k = sl; k < rows_g; k += S) {
+        const float2 v = __ldcg(reinterpret_cast<const float2 *>(p + (size_t)k * groups * N * 2));
+        s += v.x;
+        ss += v.y;
+      }
+    }
+    scratch[2 * tid] = s;
+    scratch[2 * tid + 1] = ss;
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+    if (tid < NT / S && c0 + tid < BN) {
+      double a = 0.0, b = 0.0;
+      for (int k = 0; k < S; ++k) {
+        a += scratch[2 * (k * (NT / S) + tid)];
+        b += scratch[2 * (k * (NT / S) + tid) + 1];
+      }
+      const int col = grp * BN + c0 + tid;
+      const double M = (double)F.count, mu = a / M;
+      double var = b / M - mu * mu;
+      if (var < 0.0) var = 0.0;
+      F.mean[col] = (float)mu;
+      F.invstd[col] = (float)(1.0 / sqrt(var + (double)F.eps));
+      if (F.rmean) {
+        const double unb = F.count > 1 ? var * M / (M - 1.0) : var;
+        F.rmean[col] = (float)((1.0 - F.mom) * F.rmean[col] + F.mom * mu);
+        F.rvar[col] = (float)((1.0 - F.mom) * F.rvar[col] + F.mom * unb);
+      }
+    }
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+  }
+  if (tid == 0) F.ticket[grp] = 0u;
 }
 
 }  // namespace tc

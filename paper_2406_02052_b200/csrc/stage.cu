@@ -297,6 +297,8 @@ void Stage::build() {
   size_t max_ctr = 1;
   for (auto &p : layers) max_ctr = std::max(max_ctr, bn_counter_count(p.L->g.Co));
   for (int c = 0; c < 2; ++c) {
+    fin_ticket_[c] = dalloc(64 * sizeof(unsigned));  // conv-epilogue finalize tickets (<= 32 N-tile groups)
+    PETRA_CUDA(cudaMemset(fin_ticket_[c]->p, 0, 64 * sizeof(unsigned)));
     part_[c] = dalloc(std::max<size_t>(max_part, 16));
     counters_[c] = dalloc(max_ctr * sizeof(unsigned));
     PETRA_CUDA(cudaMemset(counters_[c]->p, 0, max_ctr * sizeof(unsigned)));
@@ -527,7 +529,7 @@ static double conv_bytes(const ConvGeom &g, int esz, int pass, int out_es, bool 
   return esz * (x + z) + out_es * w;
 }
 
-void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready) {
+void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready, bool running) {
   const float *w = theta_->as<float>() + L.w_off;
   if (tc_ && stem_tc_supported(L.g)) {  // few input channels: gathered im2col from a 4-channel bf16 copy
     if (!x_bf16_ready) {
@@ -548,8 +550,22 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
   ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g),
                conv_bytes(L.g, tc ? 2 : 4, PASS_FWD, L.z16 ? 2 : 4));
   if (tc) {
+    // PETRA_CONV_FINALIZE=1: BN statistics finalized by the conv's last CTA per N-tile
+    // group instead of a stats_finalize launch (measured slower under stage
+    // concurrency: R18 45.6k vs 47.0k samples/s -- the serial tail of the last CTA
+    // costs more than the small launch; off by default)
+    static const bool in_kernel = env_int("PETRA_CONV_FINALIZE", 0) != 0;
+    float *b = bufs_->as<float>();
+    BnFinalize fin;
+    fin.mean = in_kernel ? L.mean()->as<float>() : nullptr;
+    fin.invstd = L.invstd()->as<float>();
+    fin.rmean = running ? b + L.rm_off : nullptr;
+    fin.rvar = running ? b + L.rv_off : nullptr;
+    fin.ticket = fin_ticket_[ctx_]->as<unsigned>();
+    fin.eps = desc_.bn_eps;
+    fin.mom = desc_.bn_momentum;
     L.stats_rows() = conv_fwd_tc(L.g, L.xbp(), L.xpad, L.w_bf16->as<__nv_bfloat16>(), L.z()->p, L.z16,
-                               wgrad_ws()->as<float>(), reinterpret_cast<float *>(part()->p), st);
+                                 wgrad_ws()->as<float>(), reinterpret_cast<float *>(part()->p), st, &fin);
   } else {
     conv_fwd_simt(L.g, x, w, L.z()->as<float>(), st);
   }
@@ -589,6 +605,10 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
 
 void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
   float *b = bufs_->as<float>();
+  if (L.stats_rows().finalized) {  // mean / invstd (+ running stats) written by the conv kernel
+    L.stats_rows() = StatsRows{};
+    return;
+  }
   if (L.stats_rows().rows > 0) {  // sums already produced by the tensor-core conv epilogue
     ProfScope ps("bn_stats_merge", st, 0.0, 8.0 * L.stats_rows().rows * L.g.Co / L.stats_rows().groups);
     bn_stats_from_partials(reinterpret_cast<const float *>(part()->p), L.stats_rows(), L.g.Co, L.g.M(), desc_.bn_eps,
@@ -616,7 +636,7 @@ void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running
   bool ready = ready0;
   for (size_t l = 0; l < phi.size(); ++l) {
     Layer &L = phi[l];
-    conv_fwd(L, x, st, ready);
+    conv_fwd(L, x, st, ready, running);
     layer_stats(L, running, st);
     if (l + 1 < phi.size()) {
       // inner activation; its bf16 copy is written straight into the next layer's operand
@@ -729,9 +749,9 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       // y[dst] = P_a(x[dst]) + Phi_s(x[src]);  y[src] = P_b(x[src])
       const float *xd = cur[u.dst()], *xs = cur[u.src()];
       branch_forward(u.phi, xs, keep, st);
-      conv_fwd(u.pa, xd, st);
+      conv_fwd(u.pa, xd, st, false, keep);
       layer_stats(u.pa, keep, st);
-      conv_fwd(u.pb, xs, st, u.pb.operand_of != nullptr);  // operand shared with the branch's first conv
+      conv_fwd(u.pb, xs, st, u.pb.operand_of != nullptr, keep);  // operand shared with the branch's first conv
       layer_stats(u.pb, keep, st);
       Layer &L = u.phi.back();
       int64_t M = L.g.M();
@@ -747,7 +767,7 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
     }
     case PETRA_UNIT_STEM: {
       Layer &L = u.phi[0];
-      conv_fwd(L, cur[0], st);
+      conv_fwd(L, cur[0], st, false, keep);
       layer_stats(L, keep, st);
       int Ch = L.g.Co / 2;
       if (u.d.maxpool) {
@@ -789,9 +809,9 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
       const float *xd = xin[u.dst()], *xs = xin[u.src()];
       if (recompute) {
         branch_forward(u.phi, xs, true, st, src_ready);
-        conv_fwd(u.pa, xd, st, src_ready);
+        conv_fwd(u.pa, xd, st, src_ready, true);
         layer_stats(u.pa, true, st);
-        conv_fwd(u.pb, xs, st, u.pb.operand_of != nullptr);
+        conv_fwd(u.pb, xs, st, u.pb.operand_of != nullptr, true);
         layer_stats(u.pb, true, st);
       }
       const float *dyd = cur_d[u.dst()], *dys = cur_d[u.src()];
@@ -811,7 +831,7 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
       Layer &L = u.phi[0];
       const float *th = theta_->as<float>();
       if (recompute) {
-        conv_fwd(L, xin[0], st, src_ready);
+        conv_fwd(L, xin[0], st, src_ready, true);
         layer_stats(L, true, st);
         if (u.d.maxpool) {
           // recompute the pre-pool activation and argmax (outputs go to scratch)

@@ -161,7 +161,7 @@ class Stage {
   std::vector<SgdSeg> segs_;
   DevPtr segs_dev_;
   int64_t max_seg_ = 0;
-  DevPtr part_[2], wgrad_ws_[2], counters_[2];  // per context (see Layer)
+  DevPtr part_[2], wgrad_ws_[2], counters_[2], fin_ticket_[2];  // per context (see Layer)
   int ctx_ = 0;                                 // workspace context being enqueued
   DevPtr &part() { return part_[ctx_]; }
   DevPtr &wgrad_ws() { return wgrad_ws_[ctx_]; }
@@ -207,7 +207,7 @@ class Stage {
                     cudaStream_t st);
 
   // kernels of one layer / unit
-  void conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready = false);
+  void conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready = false, bool running = false);
   void conv_wgrad(Layer &L, const float *x, cudaStream_t st);
   void conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t st);
   void layer_stats(Layer &L, bool running, cudaStream_t st);
