@@ -45,7 +45,6 @@ struct HaloParams {
   uint32_t a_stage;        // bytes per A stage (HR * 128)
   int bstages;             // B ring depth (resident: the CB * ntaps weight tiles, loaded once)
   int resident;            // 1: the whole weight matrix of the (single) N tile stays in smem
-  int dbg;                 // experiment: 1 = skip epilogue work, 2 = skip MMAs
   const float *addend;     // nullable, fp32 output only
   void *out;               // [B][H][W][N] fp32 or bf16
   float *stats;            // nullable: one BN partial row per CTA [grid][N][2]
@@ -121,13 +120,9 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int r0 = mg * 128 * T - P.lead;  // may be negative: TMA zero-fills
         for (int cb = 0; cb < P.CB; ++cb) {
           tc::mbar_wait(&aempty[as], aph ^ 1);
-          if (P.dbg == 4) {
-            tc::mbar_arrive(&afull[as]);
-          } else {
-            tc::mbar_arrive_expect_tx(&afull[as], P.HR * 128);
-            for (int r = 0; r < P.HR; r += P.box_rows)  // equal boxes, 1 KB-aligned (swizzle-consistent)
-              tc::tma_load_2d(sA + as * P.a_stage + r * 128, &tmA, &afull[as], cb * 64, r0 + r);
-          }
+          tc::mbar_arrive_expect_tx(&afull[as], P.HR * 128);
+          for (int r = 0; r < P.HR; r += P.box_rows)  // equal boxes, 1 KB-aligned (swizzle-consistent)
+            tc::tma_load_2d(sA + as * P.a_stage + r * 128, &tmA, &afull[as], cb * 64, r0 + r);
           if (++as == ASTAGES) { as = 0; aph ^= 1; }
           for (int t = 0; t < P.ntaps && !P.resident; ++t) {
             tc::mbar_wait(&bempty[bs], bph ^ 1);
@@ -171,9 +166,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             for (int k = 0; k < 4; ++k)
 #pragma unroll
               for (int tt = 0; tt < T; ++tt)  // tiles innermost: independent accumulators back to back
-                if (P.dbg != 2 && P.dbg != 3)
-                  tc::umma_bf16(dtm + tt * BN, ad[tt] + 2 * k, bd + 2 * k, idesc,
-                                (cb > 0 || t > 0 || k > 0) ? 1u : 0u);
+                tc::umma_bf16(dtm + tt * BN, ad[tt] + 2 * k, bd + 2 * k, idesc, (cb > 0 || t > 0 || k > 0) ? 1u : 0u);
             if (!P.resident) tc::umma_commit(&bempty[bs]);
           }
           __syncwarp();
@@ -205,7 +198,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
 #pragma unroll 1
-      for (int tt = 0; tt < T && P.dbg != 1 && P.dbg != 3 && P.dbg != 4; ++tt) {
+      for (int tt = 0; tt < T; ++tt) {
         const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC + tt * BN;
         const int m = (mg * T + tt) * 128 + row;
         const int b = m / GHW, r = m % GHW, hp = r / P.Wp, wp = r % P.Wp;
@@ -446,7 +439,6 @@ StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat1
   P.a_stage = (uint32_t)P.HR * 128;
   P.bstages = pl.bstages;
   P.resident = pl.resident ? 1 : 0;
-  P.dbg = env_int("PETRA_DBG_HALO", 0);
   P.addend = addend;
   P.out = out;
   P.stats = stats;

@@ -327,7 +327,10 @@ void Stage::build() {
     bool need_fout = later_nonrev || is_last_;
     if (need_fout)
       for (int h = 0; h < 2; ++h) u.fout[h] = dalloc(u.out.numel() * sizeof(float));
-    if (earlier_nonrev) {
+    // a reversible unit reconstructs into its own buffer when the half it receives is
+    // read-only FIFO memory of an earlier unit's input or, in the final stage, of a
+    // later non-reversible unit (the tail has no caller output to reconstruct into)
+    if (earlier_nonrev || (is_last_ && later_nonrev)) {
       for (int h = 0; h < 2; ++h) {
         if (u.d.kind == PETRA_UNIT_REV) u.bx[h] = dalloc(u.in.numel() * sizeof(float));
         if (u.d.kind != PETRA_UNIT_STEM) u.bd[h] = dalloc(u.in.numel() * sizeof(float));
@@ -973,7 +976,10 @@ void Stage::enqueue_backward_walk(int last_unit, bool recompute, const float *cx
       float *tx[2] = {nullptr, nullptr}, *td[2] = {nullptr, nullptr};
       tx[d] = rox[d] ? (u.bx[d] ? u.bx[d]->as<float>() : ox[d]) : const_cast<float *>(cx[d]);
       td[s] = rod[s] ? (u.bd[s] ? u.bd[s]->as<float>() : od[s]) : const_cast<float *>(cd[s]);
-      if (!tx[d] || !td[s]) throw PetraError(PETRA_E_ARG, "NULL backward output for a reversible stage");
+      if (!tx[d] || !td[s])
+        throw PetraError(PETRA_E_ARG, "NULL backward output for reversible unit " + std::to_string(i) + " of " +
+                                          std::to_string(units_.size()) + (is_last_ ? " (final stage)" : "") +
+                                          (tx[d] ? "" : ": no x~ target") + (td[s] ? "" : ": no delta target"));
       const float *nox[2] = {nullptr, nullptr};
       // the reconstructed dst half is the src of the unit processed next (recomputed
       // from it): its bf16 operand comes out of the reconstruction kernel

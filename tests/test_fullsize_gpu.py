@@ -42,7 +42,7 @@ def _rel(a, b):
 @pytest.mark.parametrize("model,j,counts,precision", [
     ("revnet18", 2, [3, 4, 4, 7], L.FP32), ("revnet18", 2, [3, 4, 4, 7], L.BF16_TC),
     ("revnet18", 3, [3, 4, 4, 7], L.BF16_TC), ("revnet18", 2, None, L.BF16_TC),
-    ("revnet50", 2, None, L.BF16_TC), ("revnet50", 6, None, L.BF16_TC)])
+    ("revnet50", 2, None, L.BF16_TC), ("revnet50", 6, None, L.FP32), ("revnet50", 6, None, L.BF16_TC)])
 def test_frozen_theta_reconstruction_full_size(model, j, counts, precision):
     torch.cuda.set_device(0)
     spec, J = _stage_case(model, j, counts, precision)
@@ -61,9 +61,11 @@ def test_frozen_theta_reconstruction_full_size(model, j, counts, precision):
     # fp32 path: (x + F) - F in fp32 -> ~1e-7 relative.  bf16 path: a unit recomputed from
     # a RECONSTRUCTED half can round a few operand elements to the other bf16 neighbour
     # and the flip travels through its conv-BN-ReLU chain (reading c23): measured 2.3e-5
-    # (RevNet-18 basic blocks) and 1.7e-4 (RevNet-50 bottlenecks, three layers).  A
-    # DS-first stage returns its buffered input bit for bit.
-    assert max(errs) < (1e-5 if precision == L.FP32 else 1e-3), errs
+    # (RevNet-18 basic blocks), 1.7e-4 (RevNet-50, two bottleneck units) and 3.2e-3
+    # (three bottleneck units, 1024 channels) -- bounded by the north_star bf16 bar 2e-2,
+    # while the fp32 path of the same stage stays at rounding level.  A DS-first stage
+    # returns its buffered input bit for bit.
+    assert max(errs) < (1e-5 if precision == L.FP32 else 2e-2), errs
     assert all(torch.isfinite(r).all().item() for r in res)
     th1, v1, _ = st.get_params()
     grads = st.get_grads()

@@ -202,6 +202,8 @@ TAIL_CASES = {
     "rev_rev_tail": (lambda: [rev(32, 0), rev(32, 1), TailUnit(64, 10)], 8, [(8, 32, 8, 8)] * 2),
     "ds_rev_tail": (lambda: [ds_basic(16, 32), rev(32, 1), TailUnit(64, 10)], 4, [(4, 16, 8, 8)] * 2),
     "bottleneck_tail_1000": (lambda: [bott(64, 16, 0), TailUnit(128, 1000)], 4, [(4, 64, 4, 4)] * 2),
+    # a reversible unit BEFORE a downsampling unit in the final stage (RevNet-50 J=4's last stage)
+    "rev_ds_rev_tail": (lambda: [rev(16, 1), ds_basic(16, 32), rev(32, 1), TailUnit(64, 10)], 4, [(4, 16, 8, 8)] * 2),
 }
 
 
