@@ -54,6 +54,13 @@ StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat1
                         const __nv_bfloat16 *wmat, const float *addend, void *out, bool out16, float *stats,
                         cudaStream_t st, const BnFinalize *fin = nullptr);
 
+// wgrad of a 3x3 stride-1 layer on zero-bordered operands: one x-halo load per pixel block
+// serves all nine taps (conv_halo.cu)
+bool wgrad_halo_eligible(const ConvGeom &g);
+size_t wgrad_halo_workspace(const ConvGeom &g);
+void wgrad_halo_run(const ConvGeom &g, const __nv_bfloat16 *dz_pad, const __nv_bfloat16 *x_pad, float *dw, float *ws,
+                    cudaStream_t st);
+
 // out[i] = sum over splits z of part[z * n + i], fixed order (deterministic)
 void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st);
 

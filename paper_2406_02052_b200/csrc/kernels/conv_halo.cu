@@ -382,6 +382,176 @@ void dispatch(int BN, int T, const CUtensorMap &ta, const CUtensorMap &tb, const
   else launch<256, 1, OUT16>(ta, tb, P, st);
 }
 
+
+// ------------------------------------------------------------------ wgrad on the halo
+// dW[co][tap][ci] = sum_p x_pad[p + off(tap)][ci] * dz_pad[p][co] over the padded grid
+// positions p (border positions of dz_pad are zero, so they add nothing).  One CTA per
+// (64-channel block of x, 64-channel block of dz, K split of pixel blocks) keeps ALL
+// nine taps in TMEM: five accumulators of 128 rows x 64 columns, each M = 128 MMA
+// pairing two taps as the two 64-element MN blocks of its A operand -- both are
+// windows of ONE halo load of x (descriptor start = window of the first tap, LBO =
+// row distance to the second tap's window; the fifth pair repeats tap 7 and its first
+// half is discarded).  Per 64-pixel block the CTA loads the x halo once and the dz
+// tile once instead of a tap box per (tap, 64-channel block) and a dz tile per M tile.
+struct WHaloParams {
+  int Ci, Co, CB, n_nt, KBtot, kb_per_split, splits;
+  int lead, HR, box_rows;
+  int off[9];
+  int Mr;      // 9 * Ci
+  float *out;  // [splits][Co][Mr]
+};
+constexpr int kWStages = 4;
+constexpr int kWThreads = 192;
+__device__ __forceinline__ int tap_a(int i) { return i < 4 ? 2 * i : 7; }
+__device__ __forceinline__ int tap_b(int i) { return i < 4 ? 2 * i + 1 : 8; }
+
+__global__ void __launch_bounds__(kWThreads, 1)
+wgrad_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDZ,
+                  const __grid_constant__ WHaloParams P) {
+  pdl_wait_trigger();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t XB = (uint32_t)P.HR * 128, STAGE = XB + 8192;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kWStages * STAGE);
+  uint64_t *empty = full + kWStages;
+  uint64_t *tfull = empty + kWStages;
+  uint64_t *tempty = tfull + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_work = P.CB * P.n_nt * P.splits;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWStages; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(tfull, 1);
+    tc::mbar_init(tempty, 4);
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&tmX);
+    tc::tma_prefetch(&tmDZ);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  auto decode = [&](int w, int &cb, int &nt, int &kb0, int &kb1) {
+    const int sp = w % P.splits, r = w / P.splits;
+    nt = r % P.n_nt;
+    cb = r / P.n_nt;
+    kb0 = sp * P.kb_per_split;
+    kb1 = min(P.KBtot, kb0 + P.kb_per_split);
+  };
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer: x halo + dz tile per 64-pixel block
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        int cb, nt, kb0, kb1;
+        decode(w, cb, nt, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *sx = smem + stage * STAGE;
+          tc::mbar_arrive_expect_tx(&full[stage], STAGE);
+          const int p0 = kb * 64;
+          for (int r = 0; r < P.HR; r += P.box_rows)
+            tc::tma_load_2d(sx + r * 128, &tmX, &full[stage], cb * 64, p0 - P.lead + r);
+          tc::tma_load_2d(sx + XB, &tmDZ, &full[stage], nt * 64, p0);
+          if (++stage == kWStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {  // ---------------- MMA issuer (warp-uniform, elected lane)
+    constexpr uint32_t idesc = tc::idesc_bf16(128, 64, 1, 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      int cb, nt, kb0, kb1;
+      decode(w, cb, nt, kb0, kb1);
+      tc::mbar_wait(tempty, (it & 1) ^ 1);
+      tc::tc_fence_after();
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        const uint32_t sx = tc::smem_u32(smem + stage * STAGE);
+        const uint64_t bd = tc::sw128_desc(sx + XB, 8192, 1024);
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int i = 0; i < 5; ++i) {
+            const int ta = tap_a(i), tb = tap_b(i);
+            const uint64_t ad = tc::sw128_desc(sx + (P.lead + P.off[ta]) * 128, (P.off[tb] - P.off[ta]) * 128, 1024);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)  // 16 pixels = 16 rows x 128 B per step
+              tc::umma_bf16(tmem_base + i * 64, ad + (uint64_t)(k * 2048 >> 4), bd + (uint64_t)(k * 2048 >> 4),
+                            idesc, (kb > kb0 || k) ? 1u : 0u);
+          }
+          tc::umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == kWStages) { stage = 0; phase ^= 1; }
+      }
+      if (tc::elect_one()) tc::umma_commit(tfull);
+      __syncwarp();
+    }
+  } else {  // ---------------- epilogue warps 2..5: D rows (tap pair, ci) x 64 co -> out[split][co][tap*Ci + ci]
+    const int q = warp & 3;
+    const int row = q * 32 + lane, half = row >> 6, ci = row & 63;
+    int it = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      int cb, nt, kb0, kb1;
+      decode(w, cb, nt, kb0, kb1);
+      const int sp = w % P.splits;
+      tc::mbar_wait(tfull, it & 1);
+      tc::tc_fence_after();
+      float *o = P.out + ((size_t)sp * P.Co + nt * 64) * P.Mr;
+#pragma unroll 1
+      for (int i = 0; i < 5; ++i) {
+        const int tap = half ? tap_b(i) : tap_a(i);
+        const bool store = !(i == 4 && half == 0);  // the repeated tap 7
+        const int r = tap * P.Ci + cb * 64 + ci;
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 16) {
+          float v[16];
+          tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + i * 64 + c, v);
+          if (store) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) o[(size_t)(c + j) * P.Mr + r] = v[j];
+          }
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tempty);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem_base, 512);
+  }
+}
+
+struct WHaloPlan {
+  int HR, box_rows, splits, kb_per_split, KBtot;
+  size_t smem;
+};
+WHaloPlan whalo_plan(int B, int H, int W, int Ci, int Co) {
+  WHaloPlan p{};
+  const int need = 64 + 2 * (W + 3);
+  const int nbox = (int)cdiv(need, kBoxMax);
+  p.box_rows = (int)cdiv(cdiv(need, nbox), 8) * 8;
+  p.HR = nbox * p.box_rows;
+  const int64_t Mp = (int64_t)B * (H + 2) * (W + 2);
+  p.KBtot = (int)cdiv(Mp, 64);
+  const int items = (Ci / 64) * (Co / 64);
+  static const int ctas = env_int("PETRA_WGRAD_CTAS", 48);
+  const int want = std::max(1, std::min(p.KBtot, (int)cdiv(ctas, items)));
+  p.kb_per_split = (int)cdiv(p.KBtot, want);
+  p.splits = (int)cdiv(p.KBtot, p.kb_per_split);
+  p.smem = 1024 + (size_t)kWStages * ((size_t)p.HR * 128 + 8192) + 256;
+  return p;
+}
 }  // namespace
 
 void conv_halo_prepare() {
@@ -402,7 +572,59 @@ void conv_halo_prepare() {
     set((const void *)conv_halo_kernel<128, 2, true>);
     set((const void *)conv_halo_kernel<128, 1, true>);
     set((const void *)conv_halo_kernel<256, 1, true>);
+    set((const void *)wgrad_halo_kernel);
   });
+}
+
+bool wgrad_halo_eligible(const ConvGeom &g) {
+  if (g.k != 3 || g.s != 1 || g.Ci % 64 || g.Co % 64) return false;
+  const WHaloPlan p = whalo_plan(g.B, g.H, g.W, g.Ci, g.Co);
+  return p.smem <= kSmemLimit && (int64_t)g.B * (g.H + 2) * (g.W + 2) < ((int64_t)1 << 31);
+}
+
+size_t wgrad_halo_workspace(const ConvGeom &g) {
+  if (!wgrad_halo_eligible(g)) return 0;
+  const WHaloPlan p = whalo_plan(g.B, g.H, g.W, g.Ci, g.Co);
+  return p.splits > 1 ? (size_t)p.splits * g.Co * g.K() * sizeof(float) : 0;
+}
+
+// dw[co][kh][kw][ci] = sum over pixels of dz (x) x, both operands zero-bordered
+// [B][H+2][W+2][C] bf16 (3x3 stride 1); ws: wgrad_halo_workspace bytes
+void wgrad_halo_run(const ConvGeom &g, const __nv_bfloat16 *dz_pad, const __nv_bfloat16 *x_pad, float *dw, float *ws,
+                    cudaStream_t st) {
+  if (!wgrad_halo_eligible(g)) throw PetraError(PETRA_E_UNSUPPORTED, "wgrad_halo_run: geometry");
+  conv_halo_prepare();
+  const WHaloPlan pl = whalo_plan(g.B, g.H, g.W, g.Ci, g.Co);
+  WHaloParams P{};
+  P.Ci = g.Ci;
+  P.Co = g.Co;
+  P.CB = g.Ci / 64;
+  P.n_nt = g.Co / 64;
+  P.KBtot = pl.KBtot;
+  P.kb_per_split = pl.kb_per_split;
+  P.splits = pl.splits;
+  const int Wp = g.W + 2;
+  P.lead = Wp + 1;
+  P.HR = pl.HR;
+  P.box_rows = pl.box_rows;
+  for (int t = 0; t < 9; ++t) P.off[t] = (t / 3 - 1) * Wp + (t % 3 - 1);
+  P.Mr = g.K();
+  if (pl.splits > 1 && !ws) throw PetraError(PETRA_E_ARG, "wgrad_halo_run: workspace required");
+  P.out = pl.splits > 1 ? ws : dw;
+  const int64_t Mp = (int64_t)g.B * (g.H + 2) * Wp;
+  cuuint64_t xd[2] = {(cuuint64_t)g.Ci, (cuuint64_t)Mp};
+  cuuint64_t xs[1] = {(cuuint64_t)g.Ci * 2};
+  cuuint32_t xb[2] = {64, (cuuint32_t)pl.box_rows};
+  cuuint64_t dd[2] = {(cuuint64_t)g.Co, (cuuint64_t)Mp};
+  cuuint64_t ds[1] = {(cuuint64_t)g.Co * 2};
+  cuuint32_t dbx[2] = {64, 64};
+  cuuint32_t es[2] = {1, 1};
+  CUtensorMap tx = tma_map(x_pad, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xd, xs, xb, es);
+  CUtensorMap tdz = tma_map(dz_pad, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dd, ds, dbx, es);
+  const int work = P.CB * P.n_nt * P.splits;
+  launch_k(wgrad_halo_kernel, std::min(work, kNumSMs), kWThreads, pl.smem, st, tx, tdz, P);
+  PETRA_LAUNCH_CHECK();
+  if (pl.splits > 1) splitk_sum(ws, pl.splits, (int64_t)g.Co * g.K(), dw, st);
 }
 
 // a 3x3 stride-1 pass whose padded grid fills at least ~3/4 of a wave of work items

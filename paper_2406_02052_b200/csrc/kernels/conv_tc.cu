@@ -965,7 +965,8 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode) {
   if (!conv_tc_supported(g, mode)) return 0;
   if (mode == 2) {
     WgradPlan w = wgrad_plan(g);
-    return w.splits > 1 ? (size_t)w.splits * g.Co * g.K() * sizeof(float) : 0;
+    return std::max(w.splits > 1 ? (size_t)w.splits * g.Co * g.K() * sizeof(float) : (size_t)0,
+                    wgrad_halo_workspace(g));
   }
   const int N = mode == 0 ? g.Co : g.Ci;
   const int KB = (mode == 0 ? g.k * g.k * g.Ci : g.k * g.k * g.Co) / 64;  // upper bound (all taps)
@@ -1007,6 +1008,11 @@ void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream
 
 void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_padded, const __nv_bfloat16 *x,
                    bool x_padded, float *dw, float *ws, cudaStream_t st) {
+  static const bool halo = env_int("PETRA_WGRAD_HALO", 1) != 0;
+  if (halo && dz_padded && x_padded && wgrad_halo_eligible(g)) {
+    wgrad_halo_run(g, dz, x, dw, ws, st);
+    return;
+  }
   WgradPlan w = wgrad_plan(g);
   CUtensorMap tx = act_map(x, g.B, g.H, g.W, g.Ci, w.t.Wb, w.t.R, w.t.NB, g.s, x_padded);
   // dz [B][Ho][Wo][Co], box (64 ch, 64 padded pixels); padding pixels out of bounds -> 0
