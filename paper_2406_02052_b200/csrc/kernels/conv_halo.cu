@@ -119,13 +119,13 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int mg = w / n_nt, nt = w % n_nt;
         const int r0 = mg * 128 * T - P.lead;  // may be negative: TMA zero-fills
         for (int cb = 0; cb < P.CB; ++cb) {
-          tc::mbar_wait(&aempty[as], aph ^ 1);
+          tc::mbar_wait_idle(&aempty[as], aph ^ 1);
           tc::mbar_arrive_expect_tx(&afull[as], P.HR * 128);
           for (int r = 0; r < P.HR; r += P.box_rows)  // equal boxes, 1 KB-aligned (swizzle-consistent)
             tc::tma_load_2d(sA + as * P.a_stage + r * 128, &tmA, &afull[as], cb * 64, r0 + r);
           if (++as == ASTAGES) { as = 0; aph ^= 1; }
           for (int t = 0; t < P.ntaps && !P.resident; ++t) {
-            tc::mbar_wait(&bempty[bs], bph ^ 1);
+            tc::mbar_wait_idle(&bempty[bs], bph ^ 1);
             tc::mbar_arrive_expect_tx(&bfull[bs], B_BYTES);
             tc::tma_load_2d(sB + bs * B_BYTES, &tmB, &bfull[bs], P.wk[t] * P.Cred + cb * 64, nt * BN);
             if (++bs == BS) { bs = 0; bph ^= 1; }
@@ -144,7 +144,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
       const int acc = it & 1;
-      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::mbar_wait_idle(&tempty[acc], ((it >> 1) & 1) ^ 1);
       tc::tc_fence_after();
       const uint32_t dtm = tmem_base + acc * ACC;
       for (int cb = 0; cb < P.CB; ++cb) {
@@ -222,7 +222,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             for (int jj = 0; jj < CW; ++jj) v[jj] = 0.f;
           }
           // stage this lane's row (128 B) ...
-          uint8_t *rp = ebuf + lane * kRowPitch;
+          const uint32_t rp = tc::smem_u32(ebuf) + lane * kRowPitch;
 #pragma unroll
           for (int ch = 0; ch < 8; ++ch) {
             uint4 u;
@@ -241,7 +241,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               u = make_uint4(__float_as_uint(v[4 * ch]), __float_as_uint(v[4 * ch + 1]),
                              __float_as_uint(v[4 * ch + 2]), __float_as_uint(v[4 * ch + 3]));
             }
-            *reinterpret_cast<uint4 *>(rp + ch * 16) = u;
+            tc::sts128(rp + ch * 16, u);
           }
           __syncwarp();
           // ... and write the warp's 32 rows out: 8 lanes per 128-byte pixel chunk
@@ -250,7 +250,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const int idx = k * 32 + lane, rr = idx >> 3, piece = idx & 7;
             const int64_t op = __shfl_sync(0xffffffffu, opix, rr);
             if (op >= 0) {
-              const uint4 u = *reinterpret_cast<const uint4 *>(ebuf + rr * kRowPitch + piece * 16);
+              const uint4 u = tc::lds128(tc::smem_u32(ebuf) + rr * kRowPitch + piece * 16);
               char *dst = static_cast<char *>(P.out) + (op * P.N + nt * BN + c) * ES + piece * 16;
               *reinterpret_cast<uint4 *>(dst) = u;
             }
@@ -396,6 +396,7 @@ void dispatch(int BN, int T, const CUtensorMap &ta, const CUtensorMap &tb, const
 struct WHaloParams {
   int Ci, Co, CB, n_nt, KBtot, kb_per_split, splits;
   int lead, HR, box_rows;
+  int pb;      // pixels per block (64 or 128): pb / 16 MMA K steps per accumulator
   int off[9];
   int Mr;      // 9 * Ci
   float *out;  // [splits][Co][Mr]
@@ -411,7 +412,7 @@ wgrad_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   pdl_wait_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t XB = (uint32_t)P.HR * 128, STAGE = XB + 8192;
+  const uint32_t XB = (uint32_t)P.HR * 128, STAGE = XB + (uint32_t)P.pb * 128;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + kWStages * STAGE);
   uint64_t *empty = full + kWStages;
   uint64_t *tfull = empty + kWStages;
@@ -450,13 +451,13 @@ wgrad_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         int cb, nt, kb0, kb1;
         decode(w, cb, nt, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          tc::mbar_wait(&empty[stage], phase ^ 1);
+          tc::mbar_wait_idle(&empty[stage], phase ^ 1);
           uint8_t *sx = smem + stage * STAGE;
           tc::mbar_arrive_expect_tx(&full[stage], STAGE);
-          const int p0 = kb * 64;
+          const int p0 = kb * P.pb;
           for (int r = 0; r < P.HR; r += P.box_rows)
             tc::tma_load_2d(sx + r * 128, &tmX, &full[stage], cb * 64, p0 - P.lead + r);
-          tc::tma_load_2d(sx + XB, &tmDZ, &full[stage], nt * 64, p0);
+          for (int r = 0; r < P.pb; r += 64) tc::tma_load_2d(sx + XB + r * 128, &tmDZ, &full[stage], nt * 64, p0 + r);
           if (++stage == kWStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -469,20 +470,21 @@ wgrad_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
       int cb, nt, kb0, kb1;
       decode(w, cb, nt, kb0, kb1);
-      tc::mbar_wait(tempty, (it & 1) ^ 1);
+      tc::mbar_wait_idle(tempty, (it & 1) ^ 1);
       tc::tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
         const uint32_t sx = tc::smem_u32(smem + stage * STAGE);
         const uint64_t bd = tc::sw128_desc(sx + XB, 8192, 1024);
+        const int nk = P.pb >> 4;
         if (tc::elect_one()) {
 #pragma unroll
           for (int i = 0; i < 5; ++i) {
             const int ta = tap_a(i), tb = tap_b(i);
             const uint64_t ad = tc::sw128_desc(sx + (P.lead + P.off[ta]) * 128, (P.off[tb] - P.off[ta]) * 128, 1024);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)  // 16 pixels = 16 rows x 128 B per step
+#pragma unroll 1
+            for (int k = 0; k < nk; ++k)  // 16 pixels = 16 rows x 128 B per step
               tc::umma_bf16(tmem_base + i * 64, ad + (uint64_t)(k * 2048 >> 4), bd + (uint64_t)(k * 2048 >> 4),
                             idesc, (kb > kb0 || k) ? 1u : 0u);
           }
@@ -533,23 +535,25 @@ wgrad_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
 }
 
 struct WHaloPlan {
-  int HR, box_rows, splits, kb_per_split, KBtot;
+  int pb, HR, box_rows, splits, kb_per_split, KBtot;
   size_t smem;
 };
 WHaloPlan whalo_plan(int B, int H, int W, int Ci, int Co) {
   WHaloPlan p{};
-  const int need = 64 + 2 * (W + 3);
+  static const int pb_env = env_int("PETRA_WGRAD_HALO_PB", 128);
+  p.pb = pb_env == 128 ? 128 : 64;
+  const int need = p.pb + 2 * (W + 3);
   const int nbox = (int)cdiv(need, kBoxMax);
   p.box_rows = (int)cdiv(cdiv(need, nbox), 8) * 8;
   p.HR = nbox * p.box_rows;
   const int64_t Mp = (int64_t)B * (H + 2) * (W + 2);
-  p.KBtot = (int)cdiv(Mp, 64);
+  p.KBtot = (int)cdiv(Mp, p.pb);
   const int items = (Ci / 64) * (Co / 64);
-  static const int ctas = env_int("PETRA_WGRAD_CTAS", 48);
+  static const int ctas = env_int("PETRA_WGRAD_HALO_CTAS", 48);
   const int want = std::max(1, std::min(p.KBtot, (int)cdiv(ctas, items)));
   p.kb_per_split = (int)cdiv(p.KBtot, want);
   p.splits = (int)cdiv(p.KBtot, p.kb_per_split);
-  p.smem = 1024 + (size_t)kWStages * ((size_t)p.HR * 128 + 8192) + 256;
+  p.smem = 1024 + (size_t)kWStages * ((size_t)p.HR * 128 + (size_t)p.pb * 128) + 256;
   return p;
 }
 }  // namespace
@@ -607,6 +611,7 @@ void wgrad_halo_run(const ConvGeom &g, const __nv_bfloat16 *dz_pad, const __nv_b
   P.lead = Wp + 1;
   P.HR = pl.HR;
   P.box_rows = pl.box_rows;
+  P.pb = pl.pb;
   for (int t = 0; t < 9; ++t) P.off[t] = (t / 3 - 1) * Wp + (t % 3 - 1);
   P.Mr = g.K();
   if (pl.splits > 1 && !ws) throw PetraError(PETRA_E_ARG, "wgrad_halo_run: workspace required");

@@ -68,7 +68,7 @@ constexpr uint32_t kEpiBytes = kEpiWarps * 2 * kEpiBuf;
 // row `lane` of a 32 x 128 B swizzled box: 32 fp32 or 64 bf16 values
 template <bool BF16>
 __device__ __forceinline__ void stage_row(uint8_t *buf, int lane, const float *v) {
-  uint8_t *rowp = buf + lane * 128;
+  const uint32_t rowp = tc::smem_u32(buf) + lane * 128;
 #pragma unroll
   for (int ch = 0; ch < 8; ++ch) {
     uint4 u;
@@ -84,7 +84,7 @@ __device__ __forceinline__ void stage_row(uint8_t *buf, int lane, const float *v
       u = make_uint4(__float_as_uint(v[4 * ch]), __float_as_uint(v[4 * ch + 1]), __float_as_uint(v[4 * ch + 2]),
                      __float_as_uint(v[4 * ch + 3]));
     }
-    *reinterpret_cast<uint4 *>(rowp + ((ch ^ (lane & 7)) << 4)) = u;
+    tc::sts128(rowp + ((ch ^ (lane & 7)) << 4), u);
   }
 }
 
@@ -151,7 +151,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int b0 = m0 / GHW, i0 = (m0 % GHW) / P.Wb;
         for (int kb = kb0; kb < kb1; ++kb) {
           const int t = kb / P.CB, cb = kb % P.CB;
-          tc::mbar_wait(&empty[stage], phase ^ 1);
+          tc::mbar_wait_idle(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * STAGE_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
           tc::tma_load_4d(sa, &tmA, &full[stage], cb * BK, P.dw[t], P.s_in * i0 + P.dh[t], b0);
@@ -169,7 +169,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       int mt, nt, sp, kb0, kb1;
       decode(w, mt, nt, sp, kb0, kb1);
       const int acc = it & 1;
-      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::mbar_wait_idle(&tempty[acc], ((it >> 1) & 1) ^ 1);
       tc::tc_fence_after();
       const uint32_t dtm = tmem_base + acc * BN;
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -474,7 +474,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
         for (int kb = kb0; kb < kb1; ++kb) {
           const int p0 = kb * 64;
           const int b0 = p0 / GHW, i0 = (p0 % GHW) / P.Wb;
-          tc::mbar_wait(&empty[stage], phase ^ 1);
+          tc::mbar_wait_idle(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * STAGE_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], bytes);
           for (int j = 0; j < 2; ++j) {
@@ -498,7 +498,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
       decode(w, mt, nt, sp);
       const int kb0 = sp * P.kb_per_split, kb1 = min(P.KBtot, kb0 + P.kb_per_split);
       const int acc = it & 1;
-      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::mbar_wait_idle(&tempty[acc], ((it >> 1) & 1) ^ 1);
       tc::tc_fence_after();
       const uint32_t dtm = tmem_base + acc * BN;
       for (int kb = kb0; kb < kb1; ++kb) {

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
       for (int kb = 0; kb < P.KB; ++kb) {
         uint32_t pk[16];
         gather32(P, kb * 64 + half * 32, q, pk);  // loads in flight before the wait
-        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_wait_idle(&empty[stage], phase ^ 1);
         store_row_chunks(sA + stage * kATile, row, half * 4, pk);
         tc::fence_proxy_async_smem();
         tc::mbar_arrive(&full[stage]);
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
     int it = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
       const int acc = it & 1;
-      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::mbar_wait_idle(&tempty[acc], ((it >> 1) & 1) ^ 1);
       tc::tc_fence_after();
       const uint32_t dtm = tmem_base + acc * BN;
       for (int kb = 0; kb < P.KB; ++kb) {
@@ -308,7 +308,7 @@ stem_wgrad_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constan
         const Pixel q = pixel(P, kb * 64 + r);
         uint32_t pk[16];
         gather32(P, kk0, q, pk);
-        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_wait_idle(&empty[stage], phase ^ 1);
         uint8_t *sa = smem + stage * STAGE_BYTES;
         if (threadIdx.x == 0) {
           tc::mbar_arrive_expect_tx(&full[stage], B_BYTES);
@@ -330,7 +330,7 @@ stem_wgrad_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constan
       const int sp = w % P.splits;
       const int kb0 = sp * P.kb_per_split, kb1 = min(P.KBtot, kb0 + P.kb_per_split);
       const int acc = it & 1;
-      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc::mbar_wait_idle(&tempty[acc], ((it >> 1) & 1) ^ 1);
       tc::tc_fence_after();
       const uint32_t dtm = tmem_base + acc * BN;
       for (int kb = kb0; kb < kb1; ++kb) {

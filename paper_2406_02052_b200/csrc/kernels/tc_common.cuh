@@ -39,6 +39,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// wait for a phase of a pipeline barrier from a producer / MMA-issuer thread: the
+// suspend-time hint lets the hardware park the thread until the phase completes
+// instead of re-issuing try_wait (the polling loop otherwise takes issue slots from the
+// epilogue warps sharing its SM sub-partition)
+__device__ __forceinline__ void mbar_wait_idle(uint64_t *bar, uint32_t parity) {
+  uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(a),
+      "r"(parity), "r"(0x100000u)
+      : "memory");
+}
+
+// 32-bit shared-window accesses (avoid generic 64-bit address arithmetic)
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4 &v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
 // generic-proxy smem writes (st.shared) made visible to the async proxy (tcgen05.mma)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -185,12 +216,13 @@ __device__ __forceinline__ void staged_colsums(const uint8_t *buf, int pitch, in
     // packed fp32x2 adds / FMAs (sm_100 FADD2 / FFMA2), even and odd rows in separate
     // accumulators (two dependency chains); bf16 -> fp32 is a 16-bit shift
     float2 s0 = make_float2(0.f, 0.f), s1 = s0, q0 = s0, q1 = s0;
-#pragma unroll 8
+    const uint32_t base = smem_u32(buf) + 4 * (lane & 3);
+#pragma unroll
     for (int r = 0; r < 32; r += 2) {
       const int c0 = SWZ ? ((lane >> 2) ^ (r & 7)) : (lane >> 2);
       const int c1 = SWZ ? ((lane >> 2) ^ ((r + 1) & 7)) : (lane >> 2);
-      const uint32_t w0 = *reinterpret_cast<const uint32_t *>(buf + r * pitch + c0 * 16 + 4 * (lane & 3));
-      const uint32_t w1 = *reinterpret_cast<const uint32_t *>(buf + (r + 1) * pitch + c1 * 16 + 4 * (lane & 3));
+      const uint32_t w0 = lds32(base + r * pitch + c0 * 16);
+      const uint32_t w1 = lds32(base + (r + 1) * pitch + c1 * 16);
       const float2 f0 = make_float2(__uint_as_float(w0 << 16), __uint_as_float(w0 & 0xffff0000u));
       const float2 f1 = make_float2(__uint_as_float(w1 << 16), __uint_as_float(w1 & 0xffff0000u));
       s0 = __fadd2_rn(s0, f0);
@@ -204,10 +236,11 @@ __device__ __forceinline__ void staged_colsums(const uint8_t *buf, int pitch, in
     q[1] = q0.y + q1.y;
   } else {
     s[0] = s[1] = q[0] = q[1] = 0.f;
-#pragma unroll 8
+    const uint32_t base = smem_u32(buf) + 4 * (lane & 3);
+#pragma unroll
     for (int r = 0; r < 32; ++r) {
       const int chunk = SWZ ? ((lane >> 2) ^ (r & 7)) : (lane >> 2);
-      const float f = *reinterpret_cast<const float *>(buf + r * pitch + chunk * 16 + 4 * (lane & 3));
+      const float f = __uint_as_float(lds32(base + r * pitch + chunk * 16));
       s[0] += f;
       q[0] = fmaf(f, f, q[0]);
     }
