@@ -191,6 +191,12 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     constexpr int ES = OUT16 ? 2 : 4;
     constexpr int CW = 128 / ES;  // columns per 128-byte chunk
+    // per-lane sums of this warp's columns in registers (same additions, same order as a
+    // running smem sum)
+    constexpr int NCH = (BN + 2 * CW - 1) / (2 * CW);
+    float rs[NCH][2], rq[NCH][2];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) rs[k][0] = rs[k][1] = rq[k][0] = rq[k][1] = 0.f;
     int it = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
       const int mg = w / n_nt, nt = w % n_nt;
@@ -205,8 +211,10 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const bool valid = b < P.B && hp >= 1 && hp <= P.H && wp >= 1 && wp <= P.W;
         const int64_t opix = valid ? ((int64_t)b * P.H + hp - 1) * P.W + wp - 1 : -1;
         const float *arow = (valid && P.addend) ? P.addend + opix * P.N + nt * BN : nullptr;
-#pragma unroll 1
-        for (int c = CW * hc; c < BN; c += 2 * CW) {
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+          const int c = CW * hc + 2 * CW * k;
+          if (c >= BN) break;
           float v[CW];
 #pragma unroll
           for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
@@ -258,13 +266,10 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (P.stats) {  // statistics of z as stored (reading c24), from the staged rows
             float s[2], sq[2];
             tc::staged_colsums<OUT16, false>(ebuf, kRowPitch, lane, s, sq);
-            const int col = c + (OUT16 ? 2 * lane : lane);  // column within the N tile
-            my_stat[2 * col] += s[0];
-            my_stat[2 * col + 1] += sq[0];
-            if (OUT16) {
-              my_stat[2 * col + 2] += s[1];
-              my_stat[2 * col + 3] += sq[1];
-            }
+            rs[k][0] += s[0];
+            rq[k][0] += sq[0];
+            rs[k][1] += s[1];
+            rq[k][1] += sq[1];
           }
           __syncwarp();
         }
@@ -274,6 +279,18 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
     if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        const int c = CW * hc + 2 * CW * k;
+        if (c >= BN) break;
+        const int col = c + (OUT16 ? 2 * lane : lane);  // column within the N tile
+        my_stat[2 * col] = rs[k][0];
+        my_stat[2 * col + 1] = rq[k][0];
+        if (OUT16) {
+          my_stat[2 * col + 2] = rs[k][1];
+          my_stat[2 * col + 3] = rq[k][1];
+        }
+      }
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       float *g = P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_nt) * BN) * 2;
       for (int i = (warp - 2) * 32 + lane; i < 2 * P.N; i += kEpiWarps * 32)

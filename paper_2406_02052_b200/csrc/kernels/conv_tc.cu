@@ -221,6 +221,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if (lane == 0) tc::bulk_wait_read<1>();
       __syncwarp();
     };
+    // per-lane sums of this warp's columns (the CTA's N tile is fixed), tile after tile
+    // in registers -- the same additions, in the same order, as a running smem sum
+    constexpr int CW = OUT16 ? 64 : 32;  // columns per 128-byte staged row
+    constexpr int NCH = (BN + 2 * CW - 1) / (2 * CW);  // column chunks per warp per tile
+    float rs[NCH][2], rq[NCH][2];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) rs[k][0] = rs[k][1] = rq[k][0] = rq[k][1] = 0.f;
     int it = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
       int mt, nt, sp, kb0, kb1;
@@ -251,9 +258,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // TMA box origin of this warp's 32 rows in the (N, Gw, Gh, B) output view
         const int m0w = mt * BM + q * 32;
         const int wb = m0w / GHW, wr = m0w % GHW, wi = wr / P.Wb, wj = wr % P.Wb;
-        constexpr int CW = OUT16 ? 64 : 32;  // columns per 128-byte staged row
-#pragma unroll 1
-        for (int c = CW * hc; c < BN; c += 2 * CW) {
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+          const int c = CW * hc + 2 * CW * k;
+          if (c >= BN) break;
           float v[CW];
 #pragma unroll
           for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
@@ -275,13 +283,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (P.stats) {  // BN batch statistics of z as stored (reading c24), from the staged rows
             float s[2], sq[2];
             tc::staged_colsums<OUT16, true>(staged, 128, lane, s, sq);
-            const int col = c + (OUT16 ? 2 * lane : lane);  // column within the N tile
-            my_stat[2 * col] += s[0];
-            my_stat[2 * col + 1] += sq[0];
-            if (OUT16) {
-              my_stat[2 * col + 2] += s[1];
-              my_stat[2 * col + 3] += sq[1];
-            }
+            rs[k][0] += s[0];
+            rq[k][0] += sq[0];
+            rs[k][1] += s[1];
+            rq[k][1] += sq[1];
           }
         }
       }
@@ -291,6 +296,18 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     if (lane == 0) tc::bulk_wait_all();
     if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        const int c = CW * hc + 2 * CW * k;
+        if (c >= BN) break;
+        const int col = c + (OUT16 ? 2 * lane : lane);  // column within the N tile
+        my_stat[2 * col] = rs[k][0];
+        my_stat[2 * col + 1] = rq[k][0];
+        if (OUT16) {
+          my_stat[2 * col + 2] = rs[k][1];
+          my_stat[2 * col + 3] = rq[k][1];
+        }
+      }
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       float *g = P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2;
       for (int i = (warp - 2) * 32 + lane; i < 2 * BN; i += kEpiWarps * 32)
