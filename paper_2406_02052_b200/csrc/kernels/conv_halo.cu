@@ -55,7 +55,7 @@ struct HaloParams {
 // (tap, channel block) weight tile to all T tiles before releasing it, so the weight
 // bytes per output row drop T-fold; their accumulators sit side by side in TMEM.
 template <int BN, int T, bool OUT16>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(PETRA_CONV_MAXREG)
 conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ HaloParams P) {
   pdl_wait_trigger();
@@ -254,8 +254,8 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           __syncwarp();
           // ... and write the warp's 32 rows out: 8 lanes per 128-byte pixel chunk
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int idx = k * 32 + lane, rr = idx >> 3, piece = idx & 7;
+          for (int pc = 0; pc < 8; ++pc) {
+            const int idx = pc * 32 + lane, rr = idx >> 3, piece = idx & 7;
             const int64_t op = __shfl_sync(0xffffffffu, opix, rr);
             if (op >= 0) {
               const uint4 u = tc::lds128(tc::smem_u32(ebuf) + rr * kRowPitch + piece * 16);

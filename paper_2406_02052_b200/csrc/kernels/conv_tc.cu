@@ -89,7 +89,7 @@ __device__ __forceinline__ void stage_row(uint8_t *buf, int lane, const float *v
 }
 
 template <int BN, int STAGES, bool OUT16>
-__global__ void __launch_bounds__(kConvThreads, 1)
+__global__ void __maxnreg__(PETRA_CONV_MAXREG)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmW,
                const __grid_constant__ ConvTCParams P) {

@@ -54,6 +54,12 @@ __device__ __forceinline__ void mbar_wait_idle(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// register cap of the conv kernels (launch-time allocation decides which other
+// stages' kernels can share an SM with a conv CTA)
+#ifndef PETRA_CONV_MAXREG
+#define PETRA_CONV_MAXREG 128
+#endif
+
 // 32-bit shared-window accesses (avoid generic 64-bit address arithmetic)
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
