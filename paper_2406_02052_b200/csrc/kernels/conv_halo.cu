@@ -49,6 +49,7 @@ struct HaloParams {
   void *out;               // [B][H][W][N] fp32 or bf16
   float *stats;            // nullable: one BN partial row per CTA [grid][N][2]
   tc::StatsFinalize fin;   // fin.mean != null: the last CTA of each N-tile group finalizes
+  tc::FastDiv f_ghw, f_wp, f_nn;  // Hp * Wp, Wp, N / BN (set by launch)
 };
 
 // T consecutive 128-row M tiles share every B (weight) stage: the MMA warp applies one
@@ -80,6 +81,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int n_nt = P.N / BN;
   const int n_work = (int)cdiv(P.Mp, 128 * T) * n_nt;
   const int GHW = P.Hp * P.Wp;
+  const tc::FastDiv &f_ghw = P.f_ghw, &f_wp = P.f_wp, &f_nn = P.f_nn;
   const int BS = P.resident ? 1 : P.bstages;  // resident: one barrier for the whole weight load
 
   if (threadIdx.x == 0) {
@@ -116,7 +118,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             tc::tma_load_2d(sB + (cb * P.ntaps + t) * B_BYTES, &tmB, &bfull[0], P.wk[t] * P.Cred + cb * 64, 0);
       }
       for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const int mg = w / n_nt, nt = w % n_nt;
+        const int mg = tc::fdiv(w, f_nn), nt = w - mg * n_nt;
         const int r0 = mg * 128 * T - P.lead;  // may be negative: TMA zero-fills
         for (int cb = 0; cb < P.CB; ++cb) {
           tc::mbar_wait_idle(&aempty[as], aph ^ 1);
@@ -199,7 +201,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     for (int k = 0; k < NCH; ++k) rs[k][0] = rs[k][1] = rq[k][0] = rq[k][1] = 0.f;
     int it = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
-      const int mg = w / n_nt, nt = w % n_nt;
+      const int mg = tc::fdiv(w, f_nn), nt = w - mg * n_nt;
       const int acc = it & 1;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
@@ -207,7 +209,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       for (int tt = 0; tt < T; ++tt) {
         const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC + tt * BN;
         const int m = (mg * T + tt) * 128 + row;
-        const int b = m / GHW, r = m % GHW, hp = r / P.Wp, wp = r % P.Wp;
+        const int b = tc::fdiv(m, f_ghw), r = m - b * GHW, hp = tc::fdiv(r, f_wp), wp = r - hp * P.Wp;
         const bool valid = b < P.B && hp >= 1 && hp <= P.H && wp >= 1 && wp <= P.W;
         const int64_t opix = valid ? ((int64_t)b * P.H + hp - 1) * P.W + wp - 1 : -1;
         const float *arow = (valid && P.addend) ? P.addend + opix * P.N + nt * BN : nullptr;
@@ -382,7 +384,11 @@ int halo_grid(int work, int n_nt) {
 }
 
 template <int BN, int T, bool OUT16>
-void launch(const CUtensorMap &ta, const CUtensorMap &tb, const HaloParams &P, cudaStream_t st) {
+void launch(const CUtensorMap &ta, const CUtensorMap &tb, const HaloParams &P0, cudaStream_t st) {
+  HaloParams P = P0;
+  P.f_ghw = tc::fastdiv_make(P.Hp * P.Wp);
+  P.f_wp = tc::fastdiv_make(P.Wp);
+  P.f_nn = tc::fastdiv_make(P.N / BN);
   const int work = (int)cdiv(P.Mp, 128 * T) * (P.N / BN);
   const size_t smem = fixed_smem() + 2 * (size_t)P.a_stage + (size_t)P.bstages * BN * 128;
   launch_k(conv_halo_kernel<BN, T, OUT16>, halo_grid(work, P.N / BN), kThreads, smem, st, ta, tb, P);

@@ -56,6 +56,7 @@ struct ConvTCParams {
   void *out;                 // [B*OH*OW][N], fp32 or bf16 (OUT16); written by TMA stores through tmO
   float *stats;              // nullable: per-(CTA, epilogue warp) BN partials [grid][4][N][2] (sum, sum sq)
   tc::StatsFinalize fin;     // fin.mean != null: the last CTA of each N-tile group finalizes
+  tc::FastDiv f_sp, f_nt, f_ghw, f_wb;  // splits, N / BN, Hb * Wb, Wb (set by launch_conv)
 };
 
 // Epilogue staging: each epilogue warp owns two 4 KB buffers (32 rows x 128 B, the
@@ -111,12 +112,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int n_work = (P.M / BM) * n_tiles_n * P.splits;  // (m tile, n tile, K split)
   const int KB = P.ntaps * P.CB;
   const int GHW = P.Hb * P.Wb;  // padded grid
+  const tc::FastDiv &f_sp = P.f_sp, &f_nt = P.f_nt, &f_ghw = P.f_ghw, &f_wb = P.f_wb;
   // work item -> tile coordinates and K-block range
   auto decode = [&](int w, int &mt, int &nt, int &sp, int &kb0, int &kb1) {
-    sp = w % P.splits;
-    const int tile = w / P.splits;
-    mt = tile / n_tiles_n;
-    nt = tile % n_tiles_n;
+    const int tile = tc::fdiv(w, f_sp);
+    sp = w - tile * P.splits;
+    mt = tc::fdiv(tile, f_nt);
+    nt = tile - mt * n_tiles_n;
     kb0 = sp * P.kb_per_split;
     kb1 = min(KB, kb0 + P.kb_per_split);
   };
@@ -148,7 +150,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         int mt, nt, sp, kb0, kb1;
         decode(w, mt, nt, sp, kb0, kb1);
         const int m0 = mt * BM;
-        const int b0 = m0 / GHW, i0 = (m0 % GHW) / P.Wb;
+        const int b0 = tc::fdiv(m0, f_ghw), i0 = tc::fdiv(m0 - b0 * GHW, f_wb);
         for (int kb = kb0; kb < kb1; ++kb) {
           const int t = kb / P.CB, cb = kb % P.CB;
           tc::mbar_wait_idle(&empty[stage], phase ^ 1);
@@ -248,7 +250,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           flush(&tmW, nt * BN + c, sp * P.M + mt * BM + q * 32, 0, 0, false);
         }
       } else {
-        const int b = m / GHW, r = m % GHW, i = r / P.Wb, j = r % P.Wb;
+        const int b = tc::fdiv(m, f_ghw), r = m - b * GHW, i = tc::fdiv(r, f_wb), j = r - i * P.Wb;
         const bool valid = b < P.B && i < P.Gh && j < P.Gw;  // padding rows: computed, never stored
         const float *arow = nullptr;
         if (valid && P.addend) {
@@ -257,7 +259,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
         // TMA box origin of this warp's 32 rows in the (N, Gw, Gh, B) output view
         const int m0w = mt * BM + q * 32;
-        const int wb = m0w / GHW, wr = m0w % GHW, wi = wr / P.Wb, wj = wr % P.Wb;
+        const int wb = tc::fdiv(m0w, f_ghw), wr = m0w - wb * GHW, wi = tc::fdiv(wr, f_wb), wj = wr - wi * P.Wb;
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
           const int c = CW * hc + 2 * CW * k;
@@ -756,7 +758,12 @@ int conv_stats_grid(int work, int n_tiles_n) {
 }
 
 template <int BN, bool OUT16>
-void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P, cudaStream_t st) {
+void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P0, cudaStream_t st) {
+  ConvTCParams P = P0;
+  P.f_sp = tc::fastdiv_make(P.splits);
+  P.f_nt = tc::fastdiv_make(P.N / BN);
+  P.f_ghw = tc::fastdiv_make(P.Hb * P.Wb);
+  P.f_wb = tc::fastdiv_make(P.Wb);
   constexpr int STAGES = conv_stages(BN);
   const size_t smem = conv_smem(BN, P.stats ? (size_t)BN * 32 : 0);  // attribute: conv_tc_prepare
   const int work = (P.M / BM) * (P.N / BN) * P.splits;

@@ -60,6 +60,30 @@ __device__ __forceinline__ void mbar_wait_idle(uint64_t *bar, uint32_t parity) {
 #define PETRA_CONV_MAXREG 128
 #endif
 
+// division by a kernel-constant divisor as multiply-high + shift (round-up method,
+// exact for dividends < 2^31); the magic numbers travel in the kernel parameters
+struct FastDiv {
+  uint32_t d, m;
+  int s;  // -1: d == 1
+};
+inline FastDiv fastdiv_make(uint32_t d) {  // host: filled into the kernel parameters
+  FastDiv f;
+  f.d = d;
+  if (d <= 1) {
+    f.m = 0;
+    f.s = -1;
+  } else {
+    const int l = 32 - __builtin_clz(d - 1);  // ceil(log2 d)
+    f.m = (uint32_t)(((1ull << (31 + l)) + d - 1) / d);
+    f.s = l - 1;
+  }
+  return f;
+}
+__device__ __forceinline__ int fdiv(int n, const FastDiv &f) {
+  return f.s < 0 ? n : (int)(__umulhi((uint32_t)n, f.m) >> f.s);
+}
+__device__ __forceinline__ int fmod_(int n, int q, const FastDiv &f) { return n - q * (int)f.d; }
+
 // 32-bit shared-window accesses (avoid generic 64-bit address arithmetic)
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
