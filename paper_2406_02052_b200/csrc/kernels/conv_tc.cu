@@ -696,10 +696,13 @@ struct ConvPlan {
 ConvPlan conv_plan(int M, int N, int KB) {
   ConvPlan p{64, 1, KB};
   const int mt = M / BM;
+  // widest N tile that still leaves `want_tiles` tiles (wider tiles reuse each A tile
+  // over more columns: fewer operand bytes from L2 per MMA)
+  static const int want_tiles = env_int("PETRA_CONV_TILES", kNumSMs);
   for (int bn : {256, 128, 64}) {
     if (N % bn) continue;
     p.BN = bn;
-    if (mt * (N / bn) >= kNumSMs) break;
+    if (mt * (N / bn) >= want_tiles) break;
   }
   const int tiles = mt * (N / p.BN);
   // split-K off by default: under the tick's stream concurrency the split's partial
