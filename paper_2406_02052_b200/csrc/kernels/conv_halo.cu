@@ -295,7 +295,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       float *g = P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_nt) * BN) * 2;
-      for (int i = (warp - 2) * 32 + lane; i < 2 * P.N; i += kEpiWarps * 32)
+      for (int i = (warp - 2) * 32 + lane; i < 2 * BN; i += kEpiWarps * 32)
         g[i] = (sstat[i] + sstat[2 * BN + i]) + (sstat[4 * BN + i] + sstat[6 * BN + i]);
       if (P.fin.mean) {  // last CTA of the group: mean / invstd (+ running stats) in-kernel
         tc::finalize_group<kEpiWarps * 32, 1>(P.fin, P.stats, P.N, BN, n_nt, blockIdx.x % n_nt, (warp - 2) * 32 + lane,
@@ -338,7 +338,9 @@ HaloPlan halo_plan(int B, int H, int W, int Cred, int N) {
   HaloPlan p{0, 0, 0, false, false};
   if (Cred % 64 || N % 64) return p;
   const int64_t Mp = (int64_t)B * (H + 2) * (W + 2);
-  if (Mp >= ((int64_t)1 << 31) || Mp * 100 > (int64_t)B * H * W * 135) return p;
+  static const int max_pad = env_int("PETRA_HALO_MAX_PAD", 135);  // padded rows, % of real rows
+  static const int64_t min_work = env_int("PETRA_HALO_MIN_WORK", (kNumSMs * 3 + 3) / 4);
+  if (Mp >= ((int64_t)1 << 31) || Mp * 100 > (int64_t)B * H * W * max_pad) return p;
   // Weight-resident plan: one N tile (BN = N <= 128) whose 9 * Cred x N weights stay in
   // smem for the whole persistent CTA, so only the halos stream from L2 (~42 B/clk per
   // SM on B200: the weight stream, not the MMA, bounds the streamed plan for C = 64).
@@ -348,7 +350,7 @@ HaloPlan halo_plan(int B, int H, int W, int Cred, int N) {
     for (int T : {4, 2, 1}) {
       if (T * N * 2 > 512) continue;
       if (fixed_smem() + 2 * (size_t)a_stage_bytes(T, W) + wbytes > kSmemLimit) continue;
-      if (cdiv(Mp, 128 * T) < (kNumSMs * 3 + 3) / 4) continue;
+      if (cdiv(Mp, 128 * T) < min_work) continue;
       p.BN = N;
       p.T = T;
       p.bstages = 9 * (Cred / 64);
@@ -357,7 +359,6 @@ HaloPlan halo_plan(int B, int H, int W, int Cred, int N) {
     }
   }
   for (int pass = 0; pass < 1; ++pass) {
-    const int64_t min_work = (kNumSMs * 3 + 3) / 4;
     for (int bn : {256, 128, 64}) {
       if (N % bn) continue;
       for (int T : {4, 2, 1}) {
