@@ -14,9 +14,11 @@
 // Deterministic: per-block fp64 partials, merged in a fixed order by the last
 // block to finish (atomic ticket after a fence) -- one launch per reduction, no
 // float atomics.  Streaming passes move 4 channels per thread (16-byte accesses).
+#include <mutex>
 #include <type_traits>
 
 #include "../kernels.h"
+#include "tc_common.cuh"
 
 namespace petra {
 namespace {
@@ -400,6 +402,97 @@ __global__ void __launch_bounds__(256, 4) bn_bwd_dz_fixed_kernel(
   }
 }
 
+
+// ---------------------------------------------------------------- BN apply, bulk-staged
+// Same arithmetic as bn_apply_fixed_kernel (bitwise), different data movement: the
+// block streams whole-row chunks of z (and of the addend) into a two-stage shared-
+// memory ring with cp.async.bulk (one instruction per chunk, completion on an
+// mbarrier) and computes from shared memory, so the bytes in flight per SM are set
+// by the ring (2 x ~24 KB per block), not by the registers of the loading threads.
+constexpr int kBulkThreads = 256;
+constexpr int kBulkChunkBytes = 24576;
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+template <typename TZ>
+__global__ void __launch_bounds__(kBulkThreads) bn_apply_bulk_kernel(
+    int64_t M, int C, int R, const TZ *__restrict__ z, const float *__restrict__ mean,
+    const float *__restrict__ invstd, const float *__restrict__ gamma, const float *__restrict__ beta, int relu,
+    float sign, const float *__restrict__ acc, float *__restrict__ out, __nv_bfloat16 *__restrict__ out_bf16, int pH,
+    int pW) {
+  pdl_wait_trigger();
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t full[2];
+  const int C4 = C / 4, tid = threadIdx.x;
+  float4 *ca = reinterpret_cast<float4 *>(sm), *cm = ca + C4, *cb = cm + C4;
+  const uint32_t zb = (uint32_t)R * C * sizeof(TZ), ab = acc ? (uint32_t)R * C * 4 : 0;
+  uint8_t *ring = sm + (((size_t)3 * C4 * 16 + 127) & ~(size_t)127);
+  const uint32_t sbytes = (zb + ab + 127) & ~127u;
+  for (int g = tid; g < C4; g += kBulkThreads) {
+    float a[4], mu[4], be[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a[k] = gamma[4 * g + k] * invstd[4 * g + k];
+      mu[k] = mean[4 * g + k];
+      be[k] = beta[4 * g + k];
+    }
+    ca[g] = make_float4(a[0], a[1], a[2], a[3]);
+    cm[g] = make_float4(mu[0], mu[1], mu[2], mu[3]);
+    cb[g] = make_float4(be[0], be[1], be[2], be[3]);
+  }
+  if (tid == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t nch = (M + R - 1) / R;
+  auto issue = [&](int64_t ch, int s) {
+    const int64_t r0 = ch * R;
+    const uint32_t rows = (uint32_t)min((int64_t)R, M - r0);
+    const uint32_t bz = rows * C * (uint32_t)sizeof(TZ), ba = acc ? rows * C * 4 : 0;
+    tc::mbar_arrive_expect_tx(&full[s], bz + ba);
+    bulk_g2s(ring + s * sbytes, z + r0 * C, bz, &full[s]);
+    if (acc) bulk_g2s(ring + s * sbytes + zb, acc + r0 * C, ba, &full[s]);
+  };
+  uint32_t ph0 = 0, ph1 = 0;
+  int s = 0;
+  if (tid == 0 && (int64_t)blockIdx.x < nch) issue(blockIdx.x, 0);
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x, s ^= 1) {
+    if (tid == 0 && ch + gridDim.x < nch) issue(ch + gridDim.x, s ^ 1);  // its stage was released last iteration
+    tc::mbar_wait(&full[s], s ? ph1 : ph0);
+    if (s) ph1 ^= 1; else ph0 ^= 1;
+    const TZ *zs = reinterpret_cast<const TZ *>(ring + s * sbytes);
+    const float *as = reinterpret_cast<const float *>(ring + s * sbytes + zb);
+    const int64_t r0 = ch * R;
+    const int rows = (int)min((int64_t)R, M - r0);
+    const int n4 = rows * C4;
+    for (int e = tid; e < n4; e += kBulkThreads) {
+      const int r = e / C4, g = e - r * C4;
+      const float4 zv = ld4(zs, (int64_t)e * 4);
+      const float4 av = acc ? *reinterpret_cast<const float4 *>(as + (int64_t)e * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 a4 = ca[g], m4 = cm[g], b4 = cb[g];
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w}, mu[4] = {m4.x, m4.y, m4.z, m4.w}, be[4] = {b4.x, b4.y, b4.z, b4.w};
+      float4 o;
+      float *op = &o.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float y = fmaf(a[k], f4(zv, k) - mu[k], be[k]);
+        if (relu) y = y > 0.f ? y : 0.f;
+        op[k] = sign * y;
+      }
+      o.x += av.x; o.y += av.y; o.z += av.z; o.w += av.w;
+      const int64_t m = r0 + r;
+      if (out) st4(out, m * C + 4 * g, o);
+      if (out_bf16) st4(out_bf16, pad_row(m, pH, pW) * C + 4 * g, o);
+    }
+    __syncthreads();  // stage s fully read before it is refilled
+  }
+}
+
 // ---------------------------------------------------------------- backward reduce (+ reconstruction)
 template <typename TZ>
 __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
@@ -588,6 +681,29 @@ template <typename TZ, typename TO>
 void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean, const float *invstd,
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
               __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st) {
+  static const bool bulk_on = env_int("PETRA_BN_BULK", 1) != 0;
+  const bool aligned = ((uintptr_t)z % 16 == 0) && ((uintptr_t)acc % 16 == 0);
+  if (bulk_on && std::is_same<TO, float>::value && ldz == C && zc0 == 0 && C % 8 == 0 && C <= 4096 && aligned &&
+      M * C < ((int64_t)1 << 31)) {
+    const int es = (int)sizeof(TZ) + (acc ? 4 : 0);
+    static const int chunk = env_int("PETRA_BN_BULK_CHUNK", kBulkChunkBytes);
+    static const int bps = env_int("PETRA_BN_BULK_BPS", 4);
+    const int R = std::max(1, chunk / (C * es));
+    const size_t sbytes = ((size_t)R * C * es + 127) & ~(size_t)127;
+    const size_t smem = (((size_t)3 * (C / 4) * 16 + 127) & ~(size_t)127) + 2 * sbytes;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(bn_apply_bulk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(bn_apply_bulk_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+    });
+    const int64_t nch = (M + R - 1) / R;
+    const unsigned grid = (unsigned)std::min<int64_t>(nch, (int64_t)bps * kNumSMs);
+    launch_k(bn_apply_bulk_kernel<TZ>, grid, kBulkThreads, smem, st, M, C, R, z, mean, invstd, gamma, beta, relu,
+             sign, acc, reinterpret_cast<float *>(out), out_bf16, pH, pW);
+    PETRA_LAUNCH_CHECK();
+    return;
+  }
   const unsigned cg = (ldz % 4 == 0 && zc0 % 4 == 0) ? chan_grid(M, C) : 0;
   if (cg && std::is_same<TO, float>::value && M < ((int64_t)1 << 31) / 4) {
     launch_k(bn_apply_fixed_kernel<TZ>, cg, 256, 0, st, (int)M, C, z, ldz, zc0, mean, invstd, gamma, beta, relu, sign,
