@@ -493,6 +493,86 @@ __global__ void __launch_bounds__(kBulkThreads) bn_apply_bulk_kernel(
   }
 }
 
+
+// BN backward dz, bulk-staged like bn_apply_bulk_kernel (bitwise the arithmetic of
+// bn_bwd_dz_fixed_kernel): z and dy chunks through the smem ring.
+template <typename TZ>
+__global__ void __launch_bounds__(kBulkThreads) bn_bwd_dz_bulk_kernel(
+    int64_t M, int C, int R, const TZ *__restrict__ z, const float *__restrict__ mean,
+    const float *__restrict__ invstd, const float *__restrict__ gamma, const float *__restrict__ beta, int relu,
+    const float *__restrict__ dy, const float *__restrict__ dgamma, const float *__restrict__ dbeta,
+    float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW) {
+  pdl_wait_trigger();
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t full[2];
+  const int C4 = C / 4, tid = threadIdx.x;
+  const float invM = 1.0f / (float)M;
+  float4 *cis = reinterpret_cast<float4 *>(sm), *cmu = cis + C4, *cga = cmu + C4, *cbe = cga + C4, *cdb = cbe + C4,
+         *cdg = cdb + C4;
+  const uint32_t zb = (uint32_t)R * C * sizeof(TZ), yb = (uint32_t)R * C * 4;
+  uint8_t *ring = sm + (((size_t)6 * C4 * 16 + 127) & ~(size_t)127);
+  const uint32_t sbytes = (zb + yb + 127) & ~127u;
+  for (int g = tid; g < C4; g += kBulkThreads) {
+    const int c = 4 * g;
+    cis[g] = make_float4(invstd[c], invstd[c + 1], invstd[c + 2], invstd[c + 3]);
+    cmu[g] = make_float4(mean[c], mean[c + 1], mean[c + 2], mean[c + 3]);
+    cga[g] = make_float4(gamma[c], gamma[c + 1], gamma[c + 2], gamma[c + 3]);
+    cbe[g] = make_float4(beta[c], beta[c + 1], beta[c + 2], beta[c + 3]);
+    cdb[g] = make_float4(dbeta[c] * invM, dbeta[c + 1] * invM, dbeta[c + 2] * invM, dbeta[c + 3] * invM);
+    cdg[g] = make_float4(dgamma[c], dgamma[c + 1], dgamma[c + 2], dgamma[c + 3]);
+  }
+  if (tid == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t nch = (M + R - 1) / R;
+  auto issue = [&](int64_t ch, int s) {
+    const int64_t r0 = ch * R;
+    const uint32_t rows = (uint32_t)min((int64_t)R, M - r0);
+    const uint32_t bz = rows * C * (uint32_t)sizeof(TZ), by = rows * C * 4;
+    tc::mbar_arrive_expect_tx(&full[s], bz + by);
+    bulk_g2s(ring + s * sbytes, z + r0 * C, bz, &full[s]);
+    bulk_g2s(ring + s * sbytes + zb, dy + r0 * C, by, &full[s]);
+  };
+  uint32_t ph0 = 0, ph1 = 0;
+  int s = 0;
+  if (tid == 0 && (int64_t)blockIdx.x < nch) issue(blockIdx.x, 0);
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x, s ^= 1) {
+    if (tid == 0 && ch + gridDim.x < nch) issue(ch + gridDim.x, s ^ 1);
+    tc::mbar_wait(&full[s], s ? ph1 : ph0);
+    if (s) ph1 ^= 1; else ph0 ^= 1;
+    const TZ *zs = reinterpret_cast<const TZ *>(ring + s * sbytes);
+    const float *ys = reinterpret_cast<const float *>(ring + s * sbytes + zb);
+    const int64_t r0 = ch * R;
+    const int rows = (int)min((int64_t)R, M - r0);
+    const int n4 = rows * C4;
+    for (int e = tid; e < n4; e += kBulkThreads) {
+      const int r = e / C4, g = e - r * C4;
+      const float4 zv = ld4(zs, (int64_t)e * 4);
+      float4 g4 = *reinterpret_cast<const float4 *>(ys + (int64_t)e * 4);
+      const float4 i4 = cis[g], m4 = cmu[g], a4 = cga[g], b4 = cbe[g], d4 = cdb[g], e4 = cdg[g];
+      const float is[4] = {i4.x, i4.y, i4.z, i4.w}, mu[4] = {m4.x, m4.y, m4.z, m4.w},
+                  ga[4] = {a4.x, a4.y, a4.z, a4.w}, be[4] = {b4.x, b4.y, b4.z, b4.w},
+                  db[4] = {d4.x, d4.y, d4.z, d4.w}, dg[4] = {e4.x, e4.y, e4.z, e4.w};
+      float4 o;
+      float *op = &o.x, *gp = &g4.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float xh = (f4(zv, k) - mu[k]) * is[k];
+        float gk = gp[k];
+        if (relu && !(fmaf(ga[k], xh, be[k]) > 0.f)) gk = 0.f;
+        op[k] = ga[k] * is[k] * (gk - db[k] - xh * dg[k] * invM);  // same rounding as bn_bwd_dz_kernel
+      }
+      const int64_t m = r0 + r;
+      if (dz) st4(dz, m * C + 4 * g, o);
+      if (dz_bf16) st4(dz_bf16, pad_row(m, pH, pW) * C + 4 * g, o);
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- backward reduce (+ reconstruction)
 template <typename TZ>
 __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
@@ -682,8 +762,9 @@ void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
               __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st) {
   static const bool bulk_on = env_int("PETRA_BN_BULK", 1) != 0;
+  static const int bulk_maxc = env_int("PETRA_BN_BULK_MAXC", 4096);
   const bool aligned = ((uintptr_t)z % 16 == 0) && ((uintptr_t)acc % 16 == 0);
-  if (bulk_on && std::is_same<TO, float>::value && ldz == C && zc0 == 0 && C % 8 == 0 && C <= 4096 && aligned &&
+  if (bulk_on && std::is_same<TO, float>::value && ldz == C && zc0 == 0 && C % 8 == 0 && C <= bulk_maxc && aligned &&
       M * C < ((int64_t)1 << 31)) {
     const int es = (int)sizeof(TZ) + (acc ? 4 : 0);
     static const int chunk = env_int("PETRA_BN_BULK_CHUNK", kBulkChunkBytes);
@@ -745,6 +826,29 @@ template <typename TZ>
 void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *invstd, const float *gamma,
                const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
                const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, int pH, int pW, cudaStream_t st) {
+  static const bool bulk_on = env_int("PETRA_BN_BULK", 1) != 0;
+  static const int bulk_maxc = env_int("PETRA_BN_BULK_DZ_MAXC", 512);
+  if (bulk_on && dy1 == nullptr && C % 8 == 0 && C <= bulk_maxc && (uintptr_t)z % 16 == 0 && (uintptr_t)dy0 % 16 == 0 &&
+      M * C < ((int64_t)1 << 31)) {
+    const int es = (int)sizeof(TZ) + 4;
+    static const int chunk = env_int("PETRA_BN_BULK_CHUNK", kBulkChunkBytes);
+    static const int bps = env_int("PETRA_BN_BULK_BPS", 4);
+    const int R = std::max(1, chunk / (C * es));
+    const size_t sbytes = ((size_t)R * C * es + 127) & ~(size_t)127;
+    const size_t smem = (((size_t)6 * (C / 4) * 16 + 127) & ~(size_t)127) + 2 * sbytes;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(bn_bwd_dz_bulk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(bn_bwd_dz_bulk_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+    });
+    const int64_t nch = (M + R - 1) / R;
+    const unsigned grid = (unsigned)std::min<int64_t>(nch, (int64_t)bps * kNumSMs);
+    launch_k(bn_bwd_dz_bulk_kernel<TZ>, grid, kBulkThreads, smem, st, M, C, R, z, mean, invstd, gamma, beta, relu, dy0,
+             dgamma, dbeta, dz, dz_bf16, pH, pW);
+    PETRA_LAUNCH_CHECK();
+    return;
+  }
   const unsigned cg = dy1 == nullptr ? chan_grid(M, C) : 0;  // split halves (stem): generic pass
   if (cg && M < ((int64_t)1 << 31) / 4)
     launch_k(bn_bwd_dz_fixed_kernel<TZ>, cg, 256, 0, st, (int)M, C, z, mean, invstd, gamma, beta, relu, dy0, dgamma,
