@@ -19,6 +19,7 @@
 
 #include "../kernels.h"
 #include "tc_common.cuh"
+#include "tc_common.cuh"
 
 namespace petra {
 namespace {
@@ -671,6 +672,108 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
   if (t == 0) counter[blockIdx.y] = 0u;
 }
 
+
+// BN backward reduce, TMA-staged: per chunk of Rc rows the block's z / dy (/ dst_in)
+// tiles for its channel tile arrive by one 2-D TMA load each (box CT x Rc) into a
+// two-stage smem ring.  Every thread keeps the (rows, channels) it has in
+// bn_bwd_reduce_kernel and adds them in the same order (chunks are whole multiples of
+// the row-group count), so the sums -- and the partial rows / merge that follow -- are
+// bitwise those of the register-loading kernel.
+template <typename TZ>
+__global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
+    const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmY,
+    const __grid_constant__ CUtensorMap tmD, int64_t M, int C, int CT, int TPR, int RG, int64_t rpb, int nrb, int Rc,
+    const float *__restrict__ mean, const float *__restrict__ invstd, const float *__restrict__ gamma,
+    const float *__restrict__ beta, int relu, int has_dst, float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW,
+    double *__restrict__ part, unsigned *__restrict__ counter, float *__restrict__ dgamma,
+    float *__restrict__ dbeta) {
+  pdl_wait_trigger();
+  constexpr int RT = RT_BWD;
+  __shared__ double sh[RT][4];
+  __shared__ uint64_t full[2];
+  extern __shared__ __align__(128) uint8_t ring[];
+  const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
+  const int c0 = blockIdx.y * CT;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(M, r0 + rpb);
+  double sg[4] = {0, 0, 0, 0}, sgx[4] = {0, 0, 0, 0};
+  const int c = c0 + 4 * cj;
+  const bool mine = c < C && rgi < RG;
+  const uint32_t zb = (uint32_t)Rc * CT * sizeof(TZ), fb = (uint32_t)Rc * CT * 4;
+  const uint32_t sbytes = (zb + fb + (has_dst ? fb : 0) + 127) & ~127u;
+  if (t == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t nchunk = (r1 - r0 + Rc - 1) / Rc;
+  auto issue = [&](int64_t k, int s) {  // thread 0
+    const int y = (int)(r0 + k * Rc);
+    uint8_t *st = ring + s * sbytes;
+    tc::mbar_arrive_expect_tx(&full[s], zb + fb + (has_dst ? fb : 0));
+    tc::tma_load_2d(st, &tmZ, &full[s], c0, y);
+    tc::tma_load_2d(st + zb, &tmY, &full[s], c0, y);
+    if (has_dst) tc::tma_load_2d(st + zb + fb, &tmD, &full[s], c0, y);
+  };
+  float mu[4], is[4], ga[4], be[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    mu[k] = mine ? mean[c + k] : 0.f;
+    is[k] = mine ? invstd[c + k] : 0.f;
+    ga[k] = mine ? gamma[c + k] : 0.f;
+    be[k] = mine ? beta[c + k] : 0.f;
+  }
+  if (t == 0 && nchunk > 0) issue(0, 0);
+  uint32_t ph0 = 0, ph1 = 0;
+  int s = 0;
+  for (int64_t k = 0; k < nchunk; ++k, s ^= 1) {
+    if (t == 0 && k + 1 < nchunk) issue(k + 1, s ^ 1);  // its stage was released at the end of k-1
+    tc::mbar_wait(&full[s], s ? ph1 : ph0);
+    if (s) ph1 ^= 1; else ph0 ^= 1;
+    const int64_t a0 = r0 + k * Rc;
+    const int rows = (int)min((int64_t)Rc, r1 - a0);
+    const uint8_t *st = ring + s * sbytes;
+    if (mine) {
+      for (int i = rgi; i < rows; i += RG) {
+        const int64_t r = a0 + i;
+        const float4 zv = ld4(reinterpret_cast<const TZ *>(st), (int64_t)i * CT + 4 * cj);
+        float4 g4 = *reinterpret_cast<const float4 *>(st + zb + ((size_t)i * CT + 4 * cj) * 4);
+        float4 d4 = has_dst ? *reinterpret_cast<const float4 *>(st + zb + fb + ((size_t)i * CT + 4 * cj) * 4)
+                            : make_float4(0, 0, 0, 0);
+        float *gp = &g4.x, *dp = &d4.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float xh = (f4(zv, q) - mu[q]) * is[q];
+          float y = fmaf(ga[q], xh, be[q]);
+          float g = gp[q];
+          if (relu) {
+            if (!(y > 0.f)) g = 0.f;
+            y = y > 0.f ? y : 0.f;
+          }
+          dp[q] -= y;
+          sg[q] += (double)g;
+          sgx[q] += (double)g * (double)xh;
+        }
+        if (has_dst) {
+          st4(dst_out, r * C + c, d4);
+          if (dst_bf16) st4(dst_bf16, pad_row(r, pH, pW) * C + c, d4);
+        }
+      }
+    }
+    __syncthreads();  // stage s read by every thread before it is refilled
+  }
+  write_partial<RT>(sh, sg, sgx, true, TPR, RG, c0, C, part);
+  if (!last_block(counter, nrb)) return;
+  double a, b;
+  merge_tile<RT>(part, nrb, C, c0, CT, sh, a, b);
+  const int ch = c0 + t;
+  if (t < CT && ch < C) {
+    dbeta[ch] = (float)a;
+    dgamma[ch] = (float)b;
+  }
+  if (t == 0) counter[blockIdx.y] = 0u;
+}
+
 // ---------------------------------------------------------------- dz
 template <typename TZ>
 __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, const float *__restrict__ mean,
@@ -808,6 +911,28 @@ void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float
                    float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW, float *dgamma, float *dbeta,
                    double *part, unsigned *counter, cudaStream_t st) {
   RedGeom g = red_geom(M, C, RT_BWD);
+  static const bool tma_on = env_int("PETRA_BN_TMA_REDUCE", 1) != 0;
+  const bool aligned = (uintptr_t)z % 16 == 0 && (uintptr_t)dy0 % 16 == 0 && (uintptr_t)dst_in % 16 == 0;
+  if (tma_on && dy1 == nullptr && C % 8 == 0 && aligned && g.CT % 8 == 0 && M < ((int64_t)1 << 31)) {
+    const int es = (int)sizeof(TZ) + 4 + (dst_out ? 4 : 0);
+    const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (40960 / (g.CT * es)) / g.RG * g.RG));
+    const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(bn_bwd_reduce_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(bn_bwd_reduce_tma_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           160 * 1024);
+    });
+    const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const CUtensorMap tz = plain_map_2d(z, zt, (int)sizeof(TZ), M, C, g.CT, Rc);
+    const CUtensorMap ty = plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
+    const CUtensorMap td = dst_out ? plain_map_2d(dst_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc) : ty;
+    launch_k(bn_bwd_reduce_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 2 * sbytes, st, tz, ty, td, M, C, g.CT,
+             g.TPR, g.RG, g.rpb, g.nrb, Rc, mean, invstd, gamma, beta, relu, dst_out ? 1 : 0, dst_out, dst_bf16, pH,
+             pW, part, counter, dgamma, dbeta);
+    PETRA_LAUNCH_CHECK();
+    return;
+  }
   launch_k(bn_bwd_reduce_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 0, st, z, M, C, g.CT, g.TPR, g.RG, g.rpb, g.nrb, mean,
                                                                  invstd, gamma, beta, relu, dy0, dy1, cs, dst_in,
                                                                  dst_out, dst_bf16, pH, pW, part, counter, dgamma,

@@ -1028,6 +1028,23 @@ CUtensorMap tma_map(const void *base, CUtensorMapDataType dt, int rank, const cu
   return make_map(base, rank, dims, strides_bytes, box, es, dt);
 }
 
+// plain row-major [rows][cols] map without swizzle, box (box_cols, box_rows): the
+// staging of the BN passes (bn.cu)
+CUtensorMap plain_map_2d(const void *base, CUtensorMapDataType dt, int esize, int64_t rows, int cols, int box_cols,
+                         int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t st[1] = {(cuuint64_t)cols * esize};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, dt, 2, const_cast<void *>(base), dims, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw PetraError(PETRA_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+
 void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st) {
   launch_k(splitk_sum_kernel, (unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st, part, splits, n, out);
   PETRA_LAUNCH_CHECK();

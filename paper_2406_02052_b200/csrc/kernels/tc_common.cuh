@@ -342,5 +342,8 @@ CUtensorMap kmajor_map_bf16(const __nv_bfloat16 *m, int rows, int K, int box_row
 // host: any tiled TMA map with 128B swizzle (throws PetraError on failure)
 CUtensorMap tma_map(const void *base, CUtensorMapDataType dt, int rank, const cuuint64_t *dims,
                     const cuuint64_t *strides_bytes, const cuuint32_t *box, const cuuint32_t *es);
+// row-major [rows][cols] tensor map, no swizzle, box (box_cols, box_rows) (conv_tc.cu)
+CUtensorMap plain_map_2d(const void *base, CUtensorMapDataType dt, int esize, int64_t rows, int cols, int box_cols,
+                         int box_rows);
 
 }  // namespace petra
