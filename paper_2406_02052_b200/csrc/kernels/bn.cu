@@ -73,7 +73,7 @@ struct RedGeom {
   int CT, TPR, RG, ctiles, nrb;
   int64_t rpb;
 };
-inline RedGeom red_geom(int64_t M, int C, int RT) {
+inline RedGeom red_geom(int64_t M, int C, int RT, int per_sm = 1) {
   RedGeom g;
   if (C % 4 == 0) {
     g.CT = std::min(C, 128);
@@ -87,7 +87,7 @@ inline RedGeom red_geom(int64_t M, int C, int RT) {
   g.ctiles = (int)cdiv(C, g.CT);
   // one wave: one block per SM (1024 / 512 threads, >= 64 KB of loads in flight), few
   // partials to merge
-  int64_t want = std::max<int64_t>(1, (int64_t)kNumSMs / g.ctiles);
+  int64_t want = std::max<int64_t>(1, (int64_t)per_sm * kNumSMs / g.ctiles);
   g.nrb = (int)std::max<int64_t>(1, std::min<int64_t>(want, cdiv(M, 4 * g.RG)));
   g.rpb = cdiv(M, g.nrb);
   g.nrb = (int)cdiv(M, g.rpb);
@@ -404,171 +404,76 @@ __global__ void __launch_bounds__(256, 4) bn_bwd_dz_fixed_kernel(
 }
 
 
-// ---------------------------------------------------------------- BN apply, bulk-staged
-// Same arithmetic as bn_apply_fixed_kernel (bitwise), different data movement: the
-// block streams whole-row chunks of z (and of the addend) into a two-stage shared-
-// memory ring with cp.async.bulk (one instruction per chunk, completion on an
-// mbarrier) and computes from shared memory, so the bytes in flight per SM are set
-// by the ring (2 x ~24 KB per block), not by the registers of the loading threads.
-constexpr int kBulkThreads = 256;
-constexpr int kBulkChunkBytes = 24576;
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   tc::smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
-               : "memory");
-}
+// ---------------------------------------------------------------- TMA-staged BN passes
+// BN apply, TMA-staged per channel tile (bitwise the arithmetic of
+// bn_apply_fixed_kernel): thread (cj, rgi) keeps channels c0 + 4cj .. +3 and their
+// constants in registers; z (a [M][ldz] view starting at column zc0) and the addend
+// arrive per row chunk by 2-D TMA boxes into a two-stage smem ring.
 template <typename TZ>
-__global__ void __launch_bounds__(kBulkThreads) bn_apply_bulk_kernel(
-    int64_t M, int C, int R, const TZ *__restrict__ z, const float *__restrict__ mean,
+__global__ void __launch_bounds__(256) bn_apply_tma_kernel(
+    const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmA, int has_acc, int64_t M, int C,
+    int CT, int TPR, int RG, int64_t rpb, int Rc, int zc0, const float *__restrict__ mean,
     const float *__restrict__ invstd, const float *__restrict__ gamma, const float *__restrict__ beta, int relu,
-    float sign, const float *__restrict__ acc, float *__restrict__ out, __nv_bfloat16 *__restrict__ out_bf16, int pH,
-    int pW) {
+    float sign, float *__restrict__ out, __nv_bfloat16 *__restrict__ out_bf16, int pH, int pW) {
   pdl_wait_trigger();
-  extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t full[2];
-  const int C4 = C / 4, tid = threadIdx.x;
-  float4 *ca = reinterpret_cast<float4 *>(sm), *cm = ca + C4, *cb = cm + C4;
-  const uint32_t zb = (uint32_t)R * C * sizeof(TZ), ab = acc ? (uint32_t)R * C * 4 : 0;
-  uint8_t *ring = sm + (((size_t)3 * C4 * 16 + 127) & ~(size_t)127);
+  extern __shared__ __align__(128) uint8_t ring[];
+  const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
+  const int c0 = blockIdx.y * CT;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(M, r0 + rpb);
+  const int c = c0 + 4 * cj;
+  const bool mine = c < C && rgi < RG;
+  const uint32_t zb = (uint32_t)Rc * CT * sizeof(TZ), ab = has_acc ? (uint32_t)Rc * CT * 4 : 0;
   const uint32_t sbytes = (zb + ab + 127) & ~127u;
-  for (int g = tid; g < C4; g += kBulkThreads) {
-    float a[4], mu[4], be[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      a[k] = gamma[4 * g + k] * invstd[4 * g + k];
-      mu[k] = mean[4 * g + k];
-      be[k] = beta[4 * g + k];
-    }
-    ca[g] = make_float4(a[0], a[1], a[2], a[3]);
-    cm[g] = make_float4(mu[0], mu[1], mu[2], mu[3]);
-    cb[g] = make_float4(be[0], be[1], be[2], be[3]);
-  }
-  if (tid == 0) {
+  if (t == 0) {
     tc::mbar_init(&full[0], 1);
     tc::mbar_init(&full[1], 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
-  const int64_t nch = (M + R - 1) / R;
-  auto issue = [&](int64_t ch, int s) {
-    const int64_t r0 = ch * R;
-    const uint32_t rows = (uint32_t)min((int64_t)R, M - r0);
-    const uint32_t bz = rows * C * (uint32_t)sizeof(TZ), ba = acc ? rows * C * 4 : 0;
-    tc::mbar_arrive_expect_tx(&full[s], bz + ba);
-    bulk_g2s(ring + s * sbytes, z + r0 * C, bz, &full[s]);
-    if (acc) bulk_g2s(ring + s * sbytes + zb, acc + r0 * C, ba, &full[s]);
+  float a[4], mu[4], be[4];  // BN constants of z's columns zc0 + c .. (the split-halves view)
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    a[k] = mine ? gamma[zc0 + c + k] * invstd[zc0 + c + k] : 0.f;
+    mu[k] = mine ? mean[zc0 + c + k] : 0.f;
+    be[k] = mine ? beta[zc0 + c + k] : 0.f;
+  }
+  const int64_t nchunk = (r1 - r0 + Rc - 1) / Rc;
+  auto issue = [&](int64_t k, int s) {
+    const int y = (int)(r0 + k * Rc);
+    uint8_t *st = ring + s * sbytes;
+    tc::mbar_arrive_expect_tx(&full[s], zb + ab);
+    tc::tma_load_2d(st, &tmZ, &full[s], c0, y);
+    if (has_acc) tc::tma_load_2d(st + zb, &tmA, &full[s], c0, y);
   };
+  if (t == 0 && nchunk > 0) issue(0, 0);
   uint32_t ph0 = 0, ph1 = 0;
   int s = 0;
-  if (tid == 0 && (int64_t)blockIdx.x < nch) issue(blockIdx.x, 0);
-  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x, s ^= 1) {
-    if (tid == 0 && ch + gridDim.x < nch) issue(ch + gridDim.x, s ^ 1);  // its stage was released last iteration
+  for (int64_t k = 0; k < nchunk; ++k, s ^= 1) {
+    if (t == 0 && k + 1 < nchunk) issue(k + 1, s ^ 1);
     tc::mbar_wait(&full[s], s ? ph1 : ph0);
     if (s) ph1 ^= 1; else ph0 ^= 1;
-    const TZ *zs = reinterpret_cast<const TZ *>(ring + s * sbytes);
-    const float *as = reinterpret_cast<const float *>(ring + s * sbytes + zb);
-    const int64_t r0 = ch * R;
-    const int rows = (int)min((int64_t)R, M - r0);
-    const int n4 = rows * C4;
-    for (int e = tid; e < n4; e += kBulkThreads) {
-      const int r = e / C4, g = e - r * C4;
-      const float4 zv = ld4(zs, (int64_t)e * 4);
-      const float4 av = acc ? *reinterpret_cast<const float4 *>(as + (int64_t)e * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 a4 = ca[g], m4 = cm[g], b4 = cb[g];
-      const float a[4] = {a4.x, a4.y, a4.z, a4.w}, mu[4] = {m4.x, m4.y, m4.z, m4.w}, be[4] = {b4.x, b4.y, b4.z, b4.w};
-      float4 o;
-      float *op = &o.x;
+    const int64_t a0 = r0 + k * Rc;
+    const int rows = (int)min((int64_t)Rc, r1 - a0);
+    const uint8_t *st = ring + s * sbytes;
+    if (mine) {
+      for (int i = rgi; i < rows; i += RG) {
+        const int64_t m = a0 + i;
+        const float4 zv = ld4(reinterpret_cast<const TZ *>(st), (int64_t)i * CT + 4 * cj);
+        const float4 av = has_acc ? *reinterpret_cast<const float4 *>(st + zb + ((size_t)i * CT + 4 * cj) * 4)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 o;
+        float *op = &o.x;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float y = fmaf(a[k], f4(zv, k) - mu[k], be[k]);
-        if (relu) y = y > 0.f ? y : 0.f;
-        op[k] = sign * y;
+        for (int q = 0; q < 4; ++q) {
+          float y = fmaf(a[q], f4(zv, q) - mu[q], be[q]);
+          if (relu) y = y > 0.f ? y : 0.f;
+          op[q] = sign * y;
+        }
+        o.x += av.x; o.y += av.y; o.z += av.z; o.w += av.w;
+        if (out) st4(out, m * C + c, o);
+        if (out_bf16) st4(out_bf16, pad_row(m, pH, pW) * C + c, o);
       }
-      o.x += av.x; o.y += av.y; o.z += av.z; o.w += av.w;
-      const int64_t m = r0 + r;
-      if (out) st4(out, m * C + 4 * g, o);
-      if (out_bf16) st4(out_bf16, pad_row(m, pH, pW) * C + 4 * g, o);
-    }
-    __syncthreads();  // stage s fully read before it is refilled
-  }
-}
-
-
-// BN backward dz, bulk-staged like bn_apply_bulk_kernel (bitwise the arithmetic of
-// bn_bwd_dz_fixed_kernel): z and dy chunks through the smem ring.
-template <typename TZ>
-__global__ void __launch_bounds__(kBulkThreads) bn_bwd_dz_bulk_kernel(
-    int64_t M, int C, int R, const TZ *__restrict__ z, const float *__restrict__ mean,
-    const float *__restrict__ invstd, const float *__restrict__ gamma, const float *__restrict__ beta, int relu,
-    const float *__restrict__ dy, const float *__restrict__ dgamma, const float *__restrict__ dbeta,
-    float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW) {
-  pdl_wait_trigger();
-  extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ uint64_t full[2];
-  const int C4 = C / 4, tid = threadIdx.x;
-  const float invM = 1.0f / (float)M;
-  float4 *cis = reinterpret_cast<float4 *>(sm), *cmu = cis + C4, *cga = cmu + C4, *cbe = cga + C4, *cdb = cbe + C4,
-         *cdg = cdb + C4;
-  const uint32_t zb = (uint32_t)R * C * sizeof(TZ), yb = (uint32_t)R * C * 4;
-  uint8_t *ring = sm + (((size_t)6 * C4 * 16 + 127) & ~(size_t)127);
-  const uint32_t sbytes = (zb + yb + 127) & ~127u;
-  for (int g = tid; g < C4; g += kBulkThreads) {
-    const int c = 4 * g;
-    cis[g] = make_float4(invstd[c], invstd[c + 1], invstd[c + 2], invstd[c + 3]);
-    cmu[g] = make_float4(mean[c], mean[c + 1], mean[c + 2], mean[c + 3]);
-    cga[g] = make_float4(gamma[c], gamma[c + 1], gamma[c + 2], gamma[c + 3]);
-    cbe[g] = make_float4(beta[c], beta[c + 1], beta[c + 2], beta[c + 3]);
-    cdb[g] = make_float4(dbeta[c] * invM, dbeta[c + 1] * invM, dbeta[c + 2] * invM, dbeta[c + 3] * invM);
-    cdg[g] = make_float4(dgamma[c], dgamma[c + 1], dgamma[c + 2], dgamma[c + 3]);
-  }
-  if (tid == 0) {
-    tc::mbar_init(&full[0], 1);
-    tc::mbar_init(&full[1], 1);
-    tc::fence_mbar_init();
-  }
-  __syncthreads();
-  const int64_t nch = (M + R - 1) / R;
-  auto issue = [&](int64_t ch, int s) {
-    const int64_t r0 = ch * R;
-    const uint32_t rows = (uint32_t)min((int64_t)R, M - r0);
-    const uint32_t bz = rows * C * (uint32_t)sizeof(TZ), by = rows * C * 4;
-    tc::mbar_arrive_expect_tx(&full[s], bz + by);
-    bulk_g2s(ring + s * sbytes, z + r0 * C, bz, &full[s]);
-    bulk_g2s(ring + s * sbytes + zb, dy + r0 * C, by, &full[s]);
-  };
-  uint32_t ph0 = 0, ph1 = 0;
-  int s = 0;
-  if (tid == 0 && (int64_t)blockIdx.x < nch) issue(blockIdx.x, 0);
-  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x, s ^= 1) {
-    if (tid == 0 && ch + gridDim.x < nch) issue(ch + gridDim.x, s ^ 1);
-    tc::mbar_wait(&full[s], s ? ph1 : ph0);
-    if (s) ph1 ^= 1; else ph0 ^= 1;
-    const TZ *zs = reinterpret_cast<const TZ *>(ring + s * sbytes);
-    const float *ys = reinterpret_cast<const float *>(ring + s * sbytes + zb);
-    const int64_t r0 = ch * R;
-    const int rows = (int)min((int64_t)R, M - r0);
-    const int n4 = rows * C4;
-    for (int e = tid; e < n4; e += kBulkThreads) {
-      const int r = e / C4, g = e - r * C4;
-      const float4 zv = ld4(zs, (int64_t)e * 4);
-      float4 g4 = *reinterpret_cast<const float4 *>(ys + (int64_t)e * 4);
-      const float4 i4 = cis[g], m4 = cmu[g], a4 = cga[g], b4 = cbe[g], d4 = cdb[g], e4 = cdg[g];
-      const float is[4] = {i4.x, i4.y, i4.z, i4.w}, mu[4] = {m4.x, m4.y, m4.z, m4.w},
-                  ga[4] = {a4.x, a4.y, a4.z, a4.w}, be[4] = {b4.x, b4.y, b4.z, b4.w},
-                  db[4] = {d4.x, d4.y, d4.z, d4.w}, dg[4] = {e4.x, e4.y, e4.z, e4.w};
-      float4 o;
-      float *op = &o.x, *gp = &g4.x;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float xh = (f4(zv, k) - mu[k]) * is[k];
-        float gk = gp[k];
-        if (relu && !(fmaf(ga[k], xh, be[k]) > 0.f)) gk = 0.f;
-        op[k] = ga[k] * is[k] * (gk - db[k] - xh * dg[k] * invM);  // same rounding as bn_bwd_dz_kernel
-      }
-      const int64_t m = r0 + r;
-      if (dz) st4(dz, m * C + 4 * g, o);
-      if (dz_bf16) st4(dz_bf16, pad_row(m, pH, pW) * C + 4 * g, o);
     }
     __syncthreads();
   }
@@ -774,6 +679,84 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
   if (t == 0) counter[blockIdx.y] = 0u;
 }
 
+
+// BN backward dz, TMA-staged per channel tile (bitwise the arithmetic of
+// bn_bwd_dz_fixed_kernel): thread (cj, rgi) keeps channels c0 + 4cj .. +3 and their
+// constants in registers and takes rows rgi, rgi + RG, ... of each chunk; the z / dy
+// tiles (box CT x Rc) arrive by TMA into a two-stage smem ring.
+template <typename TZ>
+__global__ void __launch_bounds__(256) bn_bwd_dz_tma_kernel(
+    const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmY, int64_t M, int C, int CT,
+    int TPR, int RG, int64_t rpb, int Rc, const float *__restrict__ mean, const float *__restrict__ invstd,
+    const float *__restrict__ gamma, const float *__restrict__ beta, int relu, const float *__restrict__ dgamma,
+    const float *__restrict__ dbeta, float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW) {
+  pdl_wait_trigger();
+  __shared__ uint64_t full[2];
+  extern __shared__ __align__(128) uint8_t ring[];
+  const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
+  const int c0 = blockIdx.y * CT;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(M, r0 + rpb);
+  const int c = c0 + 4 * cj;
+  const bool mine = c < C && rgi < RG;
+  const float invM = 1.0f / (float)M;
+  const uint32_t zb = (uint32_t)Rc * CT * sizeof(TZ), fb = (uint32_t)Rc * CT * 4;
+  const uint32_t sbytes = (zb + fb + 127) & ~127u;
+  if (t == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  float is[4], mu[4], ga[4], be[4], db[4], dg[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    is[k] = mine ? invstd[c + k] : 0.f;
+    mu[k] = mine ? mean[c + k] : 0.f;
+    ga[k] = mine ? gamma[c + k] : 0.f;
+    be[k] = mine ? beta[c + k] : 0.f;
+    db[k] = mine ? dbeta[c + k] * invM : 0.f;
+    dg[k] = mine ? dgamma[c + k] : 0.f;
+  }
+  const int64_t nchunk = (r1 - r0 + Rc - 1) / Rc;
+  auto issue = [&](int64_t k, int s) {
+    const int y = (int)(r0 + k * Rc);
+    uint8_t *st = ring + s * sbytes;
+    tc::mbar_arrive_expect_tx(&full[s], zb + fb);
+    tc::tma_load_2d(st, &tmZ, &full[s], c0, y);
+    tc::tma_load_2d(st + zb, &tmY, &full[s], c0, y);
+  };
+  if (t == 0 && nchunk > 0) issue(0, 0);
+  uint32_t ph0 = 0, ph1 = 0;
+  int s = 0;
+  for (int64_t k = 0; k < nchunk; ++k, s ^= 1) {
+    if (t == 0 && k + 1 < nchunk) issue(k + 1, s ^ 1);
+    tc::mbar_wait(&full[s], s ? ph1 : ph0);
+    if (s) ph1 ^= 1; else ph0 ^= 1;
+    const int64_t a0 = r0 + k * Rc;
+    const int rows = (int)min((int64_t)Rc, r1 - a0);
+    const uint8_t *st = ring + s * sbytes;
+    if (mine) {
+      for (int i = rgi; i < rows; i += RG) {
+        const int64_t m = a0 + i;
+        const float4 zv = ld4(reinterpret_cast<const TZ *>(st), (int64_t)i * CT + 4 * cj);
+        float4 g4 = *reinterpret_cast<const float4 *>(st + zb + ((size_t)i * CT + 4 * cj) * 4);
+        float4 o;
+        float *op = &o.x, *gp = &g4.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float xh = (f4(zv, q) - mu[q]) * is[q];
+          float g = gp[q];
+          if (relu && !(fmaf(ga[q], xh, be[q]) > 0.f)) g = 0.f;
+          op[q] = ga[q] * is[q] * (g - db[q] - xh * dg[q] * invM);  // same rounding as bn_bwd_dz_kernel
+        }
+        if (dz) st4(dz, m * C + c, o);
+        if (dz_bf16) st4(dz_bf16, pad_row(m, pH, pW) * C + c, o);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- dz
 template <typename TZ>
 __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, const float *__restrict__ mean,
@@ -864,27 +847,26 @@ template <typename TZ, typename TO>
 void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean, const float *invstd,
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
               __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st) {
-  static const bool bulk_on = env_int("PETRA_BN_BULK", 1) != 0;
-  static const int bulk_maxc = env_int("PETRA_BN_BULK_MAXC", 4096);
-  const bool aligned = ((uintptr_t)z % 16 == 0) && ((uintptr_t)acc % 16 == 0);
-  if (bulk_on && std::is_same<TO, float>::value && ldz == C && zc0 == 0 && C % 8 == 0 && C <= bulk_maxc && aligned &&
-      M * C < ((int64_t)1 << 31)) {
+  static const bool tma_on = env_int("PETRA_BN_TMA_APPLY", 1) != 0;
+  if (tma_on && std::is_same<TO, float>::value && C % 8 == 0 && (uintptr_t)(z + zc0) % 16 == 0 &&
+      ((size_t)ldz * sizeof(TZ)) % 16 == 0 && (uintptr_t)acc % 16 == 0 && M < ((int64_t)1 << 31)) {
+    RedGeom g = red_geom(M, C, 256, 4);
     const int es = (int)sizeof(TZ) + (acc ? 4 : 0);
-    static const int chunk = env_int("PETRA_BN_BULK_CHUNK", kBulkChunkBytes);
-    static const int bps = env_int("PETRA_BN_BULK_BPS", 4);
-    const int R = std::max(1, chunk / (C * es));
-    const size_t sbytes = ((size_t)R * C * es + 127) & ~(size_t)127;
-    const size_t smem = (((size_t)3 * (C / 4) * 16 + 127) & ~(size_t)127) + 2 * sbytes;
+    const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (24576 / (g.CT * es)) / g.RG * g.RG));
+    const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
     static std::once_flag once;
     std::call_once(once, [] {
-      cudaFuncSetAttribute(bn_apply_bulk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(bn_apply_bulk_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           200 * 1024);
+      cudaFuncSetAttribute(bn_apply_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(bn_apply_tma_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           160 * 1024);
     });
-    const int64_t nch = (M + R - 1) / R;
-    const unsigned grid = (unsigned)std::min<int64_t>(nch, (int64_t)bps * kNumSMs);
-    launch_k(bn_apply_bulk_kernel<TZ>, grid, kBulkThreads, smem, st, M, C, R, z, mean, invstd, gamma, beta, relu,
-             sign, acc, reinterpret_cast<float *>(out), out_bf16, pH, pW);
+    const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    // z: [M][C] view of a [M][ldz] buffer from column zc0
+    const CUtensorMap tz = plain_map_2d_strided(z + zc0, zt, (int)sizeof(TZ), M, C, ldz, g.CT, Rc);
+    const CUtensorMap ta = acc ? plain_map_2d(acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc) : tz;
+    launch_k(bn_apply_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), 256, 2 * sbytes, st, tz, ta, acc ? 1 : 0, M, C, g.CT,
+             g.TPR, g.RG, g.rpb, Rc, zc0, mean, invstd, gamma, beta, relu, sign, reinterpret_cast<float *>(out), out_bf16,
+             pH, pW);
     PETRA_LAUNCH_CHECK();
     return;
   }
@@ -951,26 +933,24 @@ template <typename TZ>
 void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *invstd, const float *gamma,
                const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
                const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, int pH, int pW, cudaStream_t st) {
-  static const bool bulk_on = env_int("PETRA_BN_BULK", 1) != 0;
-  static const int bulk_maxc = env_int("PETRA_BN_BULK_DZ_MAXC", 512);
-  if (bulk_on && dy1 == nullptr && C % 8 == 0 && C <= bulk_maxc && (uintptr_t)z % 16 == 0 && (uintptr_t)dy0 % 16 == 0 &&
-      M * C < ((int64_t)1 << 31)) {
+  static const bool tma_on = env_int("PETRA_BN_TMA_DZ", 1) != 0;
+  if (tma_on && dy1 == nullptr && C % 8 == 0 && (uintptr_t)z % 16 == 0 && (uintptr_t)dy0 % 16 == 0 &&
+      M < ((int64_t)1 << 31)) {
+    RedGeom g = red_geom(M, C, 256, 4);
     const int es = (int)sizeof(TZ) + 4;
-    static const int chunk = env_int("PETRA_BN_BULK_CHUNK", kBulkChunkBytes);
-    static const int bps = env_int("PETRA_BN_BULK_BPS", 4);
-    const int R = std::max(1, chunk / (C * es));
-    const size_t sbytes = ((size_t)R * C * es + 127) & ~(size_t)127;
-    const size_t smem = (((size_t)6 * (C / 4) * 16 + 127) & ~(size_t)127) + 2 * sbytes;
+    const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (24576 / (g.CT * es)) / g.RG * g.RG));
+    const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
     static std::once_flag once;
     std::call_once(once, [] {
-      cudaFuncSetAttribute(bn_bwd_dz_bulk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(bn_bwd_dz_bulk_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           200 * 1024);
+      cudaFuncSetAttribute(bn_bwd_dz_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(bn_bwd_dz_tma_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           160 * 1024);
     });
-    const int64_t nch = (M + R - 1) / R;
-    const unsigned grid = (unsigned)std::min<int64_t>(nch, (int64_t)bps * kNumSMs);
-    launch_k(bn_bwd_dz_bulk_kernel<TZ>, grid, kBulkThreads, smem, st, M, C, R, z, mean, invstd, gamma, beta, relu, dy0,
-             dgamma, dbeta, dz, dz_bf16, pH, pW);
+    const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const CUtensorMap tz = plain_map_2d(z, zt, (int)sizeof(TZ), M, C, g.CT, Rc);
+    const CUtensorMap ty = plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
+    launch_k(bn_bwd_dz_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), 256, 2 * sbytes, st, tz, ty, M, C, g.CT, g.TPR, g.RG,
+             g.rpb, Rc, mean, invstd, gamma, beta, relu, dgamma, dbeta, dz, dz_bf16, pH, pW);
     PETRA_LAUNCH_CHECK();
     return;
   }

@@ -1032,9 +1032,14 @@ CUtensorMap tma_map(const void *base, CUtensorMapDataType dt, int rank, const cu
 // staging of the BN passes (bn.cu)
 CUtensorMap plain_map_2d(const void *base, CUtensorMapDataType dt, int esize, int64_t rows, int cols, int box_cols,
                          int box_rows) {
+  return plain_map_2d_strided(base, dt, esize, rows, cols, cols, box_cols, box_rows);
+}
+// the same over a [rows][ld] buffer (first `cols` columns from base)
+CUtensorMap plain_map_2d_strided(const void *base, CUtensorMapDataType dt, int esize, int64_t rows, int cols, int ld,
+                                 int box_cols, int box_rows) {
   CUtensorMap m;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t st[1] = {(cuuint64_t)cols * esize};
+  cuuint64_t st[1] = {(cuuint64_t)ld * esize};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, dt, 2, const_cast<void *>(base), dims, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -345,5 +345,7 @@ CUtensorMap tma_map(const void *base, CUtensorMapDataType dt, int rank, const cu
 // row-major [rows][cols] tensor map, no swizzle, box (box_cols, box_rows) (conv_tc.cu)
 CUtensorMap plain_map_2d(const void *base, CUtensorMapDataType dt, int esize, int64_t rows, int cols, int box_cols,
                          int box_rows);
+CUtensorMap plain_map_2d_strided(const void *base, CUtensorMapDataType dt, int esize, int64_t rows, int cols, int ld,
+                                 int box_cols, int box_rows);
 
 }  // namespace petra
