@@ -15,9 +15,9 @@ MAIN = {  # category -> (main-kernel regex, helper-kernel regex)
     "conv_dgrad_tc": (r"(conv_tc_kernel|conv_halo_kernel)<\d+, \d+, 0>", r"splitk_out_kernel<0>|phase_fill"),
     "conv_wgrad_tc": (r"wgrad_tc_kernel|wgrad_halo_kernel", r"splitk_sum_kernel"),
     "conv_fwd_stem_tc": (r"stem_fwd_kernel", None),
-    "bn_apply": (r"bn_apply(_fixed)?_kernel", None),
-    "bn_bwd_reduce": (r"bn_bwd_reduce_kernel", None),
-    "bn_bwd_dz": (r"bn_bwd_dz(_fixed)?_kernel", None),
+    "bn_apply": (r"bn_apply(_fixed|_tma)?_kernel", None),
+    "bn_bwd_reduce": (r"bn_bwd_reduce(_tma)?_kernel", None),
+    "bn_bwd_dz": (r"bn_bwd_dz(_fixed|_tma)?_kernel", None),
     "bn_stats_merge": (r"stats_finalize_kernel", None),
     "sgd_update": (r"sgd_kernel", None),
     "cvt_bf16": (r"f32_to_bf16|image_to_bf16x4", None),
