@@ -364,8 +364,18 @@ __global__ void maxpool_bwd_v4_kernel(const float4 *__restrict__ d1, const float
 
 __global__ void f32_to_bf16_kernel(const float *__restrict__ x, __nv_bfloat16 *__restrict__ y, int64_t n) {
   pdl_wait_trigger();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = __float2bfloat16_rn(x[i]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((n & 3) == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)y & 7) == 0) {  // 16-byte loads, 8-byte stores
+    const float4 *x4 = reinterpret_cast<const float4 *>(x);
+    uint2 *y4 = reinterpret_cast<uint2 *>(y);
+    for (int64_t i = t0; i < n / 4; i += stride) {
+      const float4 v = x4[i];
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+      y4[i] = make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+    }
+    return;
+  }
+  for (int64_t i = t0; i < n; i += stride) y[i] = __float2bfloat16_rn(x[i]);
 }
 
 // interior of a zero-bordered [B][H+2][W+2][C] bf16 buffer (C % 4 == 0)
@@ -480,7 +490,8 @@ void f32_to_bf16_padded(const float *x, __nv_bfloat16 *y, int B, int H, int W, i
 }
 
 void f32_to_bf16(const float *x, __nv_bfloat16 *y, int64_t n, cudaStream_t st) {
-  launch_k(f32_to_bf16_kernel, ew_grid(n), 256, 0, st, x, y, n);
+  const bool v4 = (n & 3) == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)y & 7) == 0;
+  launch_k(f32_to_bf16_kernel, ew_grid(v4 ? n / 4 : n), 256, 0, st, x, y, n);
   PETRA_LAUNCH_CHECK();
 }
 
