@@ -382,18 +382,18 @@ __global__ void f32_to_bf16_kernel(const float *__restrict__ x, __nv_bfloat16 *_
 __global__ void f32_to_bf16_padded_kernel(const float4 *__restrict__ x, uint2 *__restrict__ y, int B, int H, int W,
                                           int C4) {
   pdl_wait_trigger();
-  const int64_t n = (int64_t)B * H * W * C4;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C4);
-    const int64_t m = i / C4;
-    const int w = (int)(m % W);
-    const int64_t r = m / W;
-    const int h = (int)(r % H);
-    const int64_t b = r / H;
-    const float4 v = x[i];
-    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-    y[((b * (H + 2) + h + 1) * (W + 2) + w + 1) * C4 + c] =
-        make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+  // one pixel row (b, h) per block iteration: W * C4 contiguous float4 in, the same run
+  // of uint2 out one padded pixel in (no per-element index divisions)
+  const int rowlen = W * C4;
+  for (int r = blockIdx.x; r < B * H; r += gridDim.x) {
+    const int b = r / H, h = r - b * H;
+    const float4 *src = x + (int64_t)r * rowlen;
+    uint2 *dst = y + (((int64_t)b * (H + 2) + h + 1) * (W + 2) + 1) * C4;
+    for (int j = threadIdx.x; j < rowlen; j += blockDim.x) {
+      const float4 v = src[j];
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+      dst[j] = make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+    }
   }
 }
 
@@ -484,7 +484,7 @@ void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, in
 
 void f32_to_bf16_padded(const float *x, __nv_bfloat16 *y, int B, int H, int W, int C, cudaStream_t st) {
   const int C4 = C / 4;
-  launch_k(f32_to_bf16_padded_kernel, ew_grid((int64_t)B * H * W * C4), 256, 0, st, 
+  launch_k(f32_to_bf16_padded_kernel, (unsigned)std::min<int64_t>((int64_t)B * H, 16 * kNumSMs), 256, 0, st, 
       reinterpret_cast<const float4 *>(x), reinterpret_cast<uint2 *>(y), B, H, W, C4);
   PETRA_LAUNCH_CHECK();
 }
