@@ -587,7 +587,8 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
 template <typename TZ>
 __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
     const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmY,
-    const __grid_constant__ CUtensorMap tmD, int64_t M, int C, int CT, int TPR, int RG, int64_t rpb, int nrb, int Rc,
+    const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmY1, int cs, int64_t M, int C,
+    int CT, int TPR, int RG, int64_t rpb, int nrb, int Rc,
     const float *__restrict__ mean, const float *__restrict__ invstd, const float *__restrict__ gamma,
     const float *__restrict__ beta, int relu, int has_dst, float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW,
     double *__restrict__ part, unsigned *__restrict__ counter, float *__restrict__ dgamma,
@@ -617,7 +618,12 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
     uint8_t *st = ring + s * sbytes;
     tc::mbar_arrive_expect_tx(&full[s], zb + fb + (has_dst ? fb : 0));
     tc::tma_load_2d(st, &tmZ, &full[s], c0, y);
-    tc::tma_load_2d(st + zb, &tmY, &full[s], c0, y);
+    if (cs) {  // split halves (the stem): [Rc][cs] from dy0, then [Rc][C - cs] from dy1 (one tile = all C)
+      tc::tma_load_2d(st + zb, &tmY, &full[s], 0, y);
+      tc::tma_load_2d(st + zb + (size_t)Rc * cs * 4, &tmY1, &full[s], 0, y);
+    } else {
+      tc::tma_load_2d(st + zb, &tmY, &full[s], c0, y);
+    }
     if (has_dst) tc::tma_load_2d(st + zb + fb, &tmD, &full[s], c0, y);
   };
   float mu[4], is[4], ga[4], be[4];
@@ -642,7 +648,10 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
       for (int i = rgi; i < rows; i += RG) {
         const int64_t r = a0 + i;
         const float4 zv = ld4(reinterpret_cast<const TZ *>(st), (int64_t)i * CT + 4 * cj);
-        float4 g4 = *reinterpret_cast<const float4 *>(st + zb + ((size_t)i * CT + 4 * cj) * 4);
+        const size_t yo = !cs ? (size_t)i * CT + 4 * cj
+                              : (4 * cj < cs ? (size_t)i * cs + 4 * cj
+                                             : (size_t)Rc * cs + (size_t)i * (C - cs) + 4 * cj - cs);
+        float4 g4 = *reinterpret_cast<const float4 *>(st + zb + yo * 4);
         float4 d4 = has_dst ? *reinterpret_cast<const float4 *>(st + zb + fb + ((size_t)i * CT + 4 * cj) * 4)
                             : make_float4(0, 0, 0, 0);
         float *gp = &g4.x, *dp = &d4.x;
@@ -686,8 +695,8 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
 // tiles (box CT x Rc) arrive by TMA into a two-stage smem ring.
 template <typename TZ>
 __global__ void __launch_bounds__(256) bn_bwd_dz_tma_kernel(
-    const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmY, int64_t M, int C, int CT,
-    int TPR, int RG, int64_t rpb, int Rc, const float *__restrict__ mean, const float *__restrict__ invstd,
+    const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmY,
+    const __grid_constant__ CUtensorMap tmY1, int cs, int64_t M, int C, int CT, int TPR, int RG, int64_t rpb, int Rc, const float *__restrict__ mean, const float *__restrict__ invstd,
     const float *__restrict__ gamma, const float *__restrict__ beta, int relu, const float *__restrict__ dgamma,
     const float *__restrict__ dbeta, float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW) {
   pdl_wait_trigger();
@@ -723,7 +732,12 @@ __global__ void __launch_bounds__(256) bn_bwd_dz_tma_kernel(
     uint8_t *st = ring + s * sbytes;
     tc::mbar_arrive_expect_tx(&full[s], zb + fb);
     tc::tma_load_2d(st, &tmZ, &full[s], c0, y);
-    tc::tma_load_2d(st + zb, &tmY, &full[s], c0, y);
+    if (cs) {  // split halves: see bn_bwd_reduce_tma_kernel
+      tc::tma_load_2d(st + zb, &tmY, &full[s], 0, y);
+      tc::tma_load_2d(st + zb + (size_t)Rc * cs * 4, &tmY1, &full[s], 0, y);
+    } else {
+      tc::tma_load_2d(st + zb, &tmY, &full[s], c0, y);
+    }
   };
   if (t == 0 && nchunk > 0) issue(0, 0);
   uint32_t ph0 = 0, ph1 = 0;
@@ -739,7 +753,10 @@ __global__ void __launch_bounds__(256) bn_bwd_dz_tma_kernel(
       for (int i = rgi; i < rows; i += RG) {
         const int64_t m = a0 + i;
         const float4 zv = ld4(reinterpret_cast<const TZ *>(st), (int64_t)i * CT + 4 * cj);
-        float4 g4 = *reinterpret_cast<const float4 *>(st + zb + ((size_t)i * CT + 4 * cj) * 4);
+        const size_t yo = !cs ? (size_t)i * CT + 4 * cj
+                              : (4 * cj < cs ? (size_t)i * cs + 4 * cj
+                                             : (size_t)Rc * cs + (size_t)i * (C - cs) + 4 * cj - cs);
+        float4 g4 = *reinterpret_cast<const float4 *>(st + zb + yo * 4);
         float4 o;
         float *op = &o.x, *gp = &g4.x;
 #pragma unroll
@@ -894,8 +911,11 @@ void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float
                    double *part, unsigned *counter, cudaStream_t st) {
   RedGeom g = red_geom(M, C, RT_BWD);
   static const bool tma_on = env_int("PETRA_BN_TMA_REDUCE", 1) != 0;
-  const bool aligned = (uintptr_t)z % 16 == 0 && (uintptr_t)dy0 % 16 == 0 && (uintptr_t)dst_in % 16 == 0;
-  if (tma_on && dy1 == nullptr && C % 8 == 0 && aligned && g.CT % 8 == 0 && M < ((int64_t)1 << 31)) {
+  const bool aligned = (uintptr_t)z % 16 == 0 && (uintptr_t)dy0 % 16 == 0 && (uintptr_t)dst_in % 16 == 0 &&
+                       (uintptr_t)dy1 % 16 == 0;
+  // split dy halves (the stem): one channel tile covering both (same geometry as the register kernel)
+  const bool split_ok = dy1 == nullptr || (g.ctiles == 1 && cs % 4 == 0 && (C - cs) % 4 == 0 && cs > 0 && cs < C);
+  if (tma_on && split_ok && C % 8 == 0 && aligned && g.CT % 8 == 0 && M < ((int64_t)1 << 31)) {
     const int es = (int)sizeof(TZ) + 4 + (dst_out ? 4 : 0);
     const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (40960 / (g.CT * es)) / g.RG * g.RG));
     const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
@@ -907,9 +927,13 @@ void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float
     });
     const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const CUtensorMap tz = plain_map_2d(z, zt, (int)sizeof(TZ), M, C, g.CT, Rc);
-    const CUtensorMap ty = plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
+    const int s0 = dy1 ? cs : 0;
+    const CUtensorMap ty = dy1 ? plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, cs, cs, Rc)
+                               : plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
+    const CUtensorMap ty1 = dy1 ? plain_map_2d(dy1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C - cs, C - cs, Rc) : ty;
     const CUtensorMap td = dst_out ? plain_map_2d(dst_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc) : ty;
-    launch_k(bn_bwd_reduce_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 2 * sbytes, st, tz, ty, td, M, C, g.CT,
+    launch_k(bn_bwd_reduce_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 2 * sbytes, st, tz, ty, td, ty1, s0, M, C,
+             g.CT,
              g.TPR, g.RG, g.rpb, g.nrb, Rc, mean, invstd, gamma, beta, relu, dst_out ? 1 : 0, dst_out, dst_bf16, pH,
              pW, part, counter, dgamma, dbeta);
     PETRA_LAUNCH_CHECK();
@@ -934,9 +958,11 @@ void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *in
                const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
                const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, int pH, int pW, cudaStream_t st) {
   static const bool tma_on = env_int("PETRA_BN_TMA_DZ", 1) != 0;
-  if (tma_on && dy1 == nullptr && C % 8 == 0 && (uintptr_t)z % 16 == 0 && (uintptr_t)dy0 % 16 == 0 &&
-      M < ((int64_t)1 << 31)) {
-    RedGeom g = red_geom(M, C, 256, 4);
+  const RedGeom gs = red_geom(M, C, 256, 4);
+  const bool split_ok = dy1 == nullptr || (gs.ctiles == 1 && cs % 4 == 0 && (C - cs) % 4 == 0 && cs > 0 && cs < C);
+  if (tma_on && split_ok && C % 8 == 0 && (uintptr_t)z % 16 == 0 && (uintptr_t)dy0 % 16 == 0 &&
+      (uintptr_t)dy1 % 16 == 0 && M < ((int64_t)1 << 31)) {
+    const RedGeom &g = gs;
     const int es = (int)sizeof(TZ) + 4;
     const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (24576 / (g.CT * es)) / g.RG * g.RG));
     const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
@@ -948,8 +974,12 @@ void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *in
     });
     const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const CUtensorMap tz = plain_map_2d(z, zt, (int)sizeof(TZ), M, C, g.CT, Rc);
-    const CUtensorMap ty = plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
-    launch_k(bn_bwd_dz_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), 256, 2 * sbytes, st, tz, ty, M, C, g.CT, g.TPR, g.RG,
+    const int s0 = dy1 ? cs : 0;
+    const CUtensorMap ty = dy1 ? plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, cs, cs, Rc)
+                               : plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
+    const CUtensorMap ty1 = dy1 ? plain_map_2d(dy1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C - cs, C - cs, Rc) : ty;
+    launch_k(bn_bwd_dz_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), 256, 2 * sbytes, st, tz, ty, ty1, s0, M, C, g.CT, g.TPR,
+             g.RG,
              g.rpb, Rc, mean, invstd, gamma, beta, relu, dgamma, dbeta, dz, dz_bf16, pH, pW);
     PETRA_LAUNCH_CHECK();
     return;
