@@ -93,7 +93,7 @@ template <int BN, int STAGES, bool OUT16>
 __global__ void __maxnreg__(PETRA_CONV_MAXREG)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmW,
-               const __grid_constant__ ConvTCParams P) {
+               const __grid_constant__ CUtensorMap tmAdd, const __grid_constant__ ConvTCParams P) {
   pdl_wait_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -104,6 +104,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint64_t *abar = reinterpret_cast<uint64_t *>(tmem_slot + 2);  // per epilogue warp: addend box loads
   uint8_t *sepi = smem + STAGES * STAGE_BYTES + 1024;      // [8 warps][2][32 x 128 B] epilogue staging
   float *sstat = reinterpret_cast<float *>(sepi + kEpiBytes);  // [4 lane quarters][BN][2] BN partial sums
 
@@ -132,6 +133,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], kEpiWarps);
     }
+    for (int a = 0; a < kEpiWarps; ++a) tc::mbar_init(&abar[a], 1);
     tc::fence_mbar_init();
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
@@ -230,6 +232,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     float rs[NCH][2], rq[NCH][2];
 #pragma unroll
     for (int k = 0; k < NCH; ++k) rs[k][0] = rs[k][1] = rq[k][0] = rq[k][1] = 0.f;
+    uint32_t aph = 0;  // phase of this warp's addend barrier
     int it = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
       int mt, nt, sp, kb0, kb1;
@@ -252,11 +255,6 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       } else {
         const int b = tc::fdiv(m, f_ghw), r = m - b * GHW, i = tc::fdiv(r, f_wb), j = r - i * P.Wb;
         const bool valid = b < P.B && i < P.Gh && j < P.Gw;  // padding rows: computed, never stored
-        const float *arow = nullptr;
-        if (valid && P.addend) {
-          const int64_t opix = ((int64_t)b * P.OH + i * P.oss + P.ph) * P.OW + j * P.oss + P.pw;
-          arow = P.addend + opix * P.N + nt * BN;
-        }
         // TMA box origin of this warp's 32 rows in the (N, Gw, Gh, B) output view
         const int m0w = mt * BM + q * 32;
         const int wb = tc::fdiv(m0w, f_ghw), wr = m0w - wb * GHW, wi = tc::fdiv(wr, f_wb), wj = wr - wi * P.Wb;
@@ -267,12 +265,24 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           float v[CW];
 #pragma unroll
           for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
-          if (arow) {
-#pragma unroll
-            for (int jj = 0; jj < CW; jj += 4) {
-              float4 a4 = *reinterpret_cast<const float4 *>(arow + c + jj);
-              v[jj] += a4.x; v[jj + 1] += a4.y; v[jj + 2] += a4.z; v[jj + 3] += a4.w;
+          if (!OUT16 && P.addend) {  // the addend box (same geometry as the store box) by TMA into the buffer
+            acquire();
+            if (lane == 0) {
+              tc::mbar_arrive_expect_tx(&abar[warp - 2], kEpiBuf);
+              tc::tma_load_4d(ebuf + eb * kEpiBuf, &tmAdd, &abar[warp - 2], nt * BN + c, wj, wi, wb);
             }
+            tc::mbar_wait(&abar[warp - 2], aph);
+            aph ^= 1;
+            const uint32_t rowp = tc::smem_u32(ebuf + eb * kEpiBuf) + lane * 128;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              const uint4 u = tc::lds128(rowp + ((ch ^ (lane & 7)) << 4));
+              v[4 * ch] += __uint_as_float(u.x);
+              v[4 * ch + 1] += __uint_as_float(u.y);
+              v[4 * ch + 2] += __uint_as_float(u.z);
+              v[4 * ch + 3] += __uint_as_float(u.w);
+            }
+            __syncwarp();  // every lane has read its row before stage_row overwrites the buffer
           }
           if (!valid) {  // padding row: never stored (outside the TMA box), zero for the statistics
 #pragma unroll
@@ -773,7 +783,9 @@ void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParam
   const int grid = conv_stats_grid(work, P.N / BN);
   const CUtensorMap to = out_map(P.out, OUT16, P);
   const CUtensorMap tw = P.splits > 1 ? ws_map(P.ws, P.N, (int64_t)P.splits * P.M) : to;
-  launch_k(conv_tc_kernel<BN, STAGES, OUT16>, grid, kConvThreads, smem, st, ta, tb, to, tw, P);
+  // the addend in the output's geometry (fp32 outputs only)
+  const CUtensorMap tad = (!OUT16 && P.addend) ? out_map(const_cast<float *>(P.addend), false, P) : to;
+  launch_k(conv_tc_kernel<BN, STAGES, OUT16>, grid, kConvThreads, smem, st, ta, tb, to, tw, tad, P);
   PETRA_LAUNCH_CHECK();
   if (P.splits > 1) {
     int64_t n = (int64_t)P.M * P.N / 4;
