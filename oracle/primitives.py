@@ -19,20 +19,60 @@ import numpy as np
 BN_EPS = 1e-5        # reading c9 (paper silent; PyTorch default)
 BN_MOMENTUM = 0.1    # reading c9
 
-# Operand-precision emulation (reading c22).  The paper fixes no
-# precision; the oracle is exact fp64 by default.  A test that compares a kernel
-# computing a convolution on rounded operands (bf16 tensor cores) may install
-# rounding functions here so that the ReLU masks -- integer decisions taken from
-# floating point -- are decided on the same rounded operands on both sides.
-# Each entry: None (exact) or f(array, pass_name, geometry) -> rounded array,
-# geometry = (B, H, W, Ci, Co, k, stride).  Products/sums stay fp64.  "fwd_out" is
-# applied to the convolution's result (a kernel that stores z in bf16, reading c24).
-OPERAND_ROUND = {"fwd": None, "dgrad": None, "wgrad": None, "fwd_out": None}
+# The arithmetic of the bf16 tensor-core path (reading c22).  The paper
+# fixes no precision (it trains in PyTorch's default fp32); north_star
+# asks for bf16 tensor-core convolutions.  The oracle is exact fp64 by default.  Under
+# ``bf16_convolutions()`` it follows ONE rule, stated here and in DESIGN.md, that
+# names the rounding points of that path without asking the code under test:
+#
+#   R1  every convolution pass -- forward (and the recomputation), dgrad, wgrad --
+#       rounds BOTH of its operands to bf16 (round-to-nearest-even of the fp32
+#       value, :func:`bf16_round`) and then accumulates exactly;
+#   R2  the forward result z is rounded to bf16 before BatchNorm reads it
+#       (statistics, normalisation and the backward all see the rounded z);
+#   R3  nothing else is rounded: streams, messages, BN, ReLU, the coupling add /
+#       subtract, dgrad / wgrad results, the classifier and the optimizer stay exact.
+#
+# The ReLU masks are integers decided from floating point; under this rule both
+# sides decide them on the same rounded operands (up to accumulation order).
+_MODE = {"bf16": False}
 
 
-def _rnd(kind, a, geom):
-    f = OPERAND_ROUND[kind]
-    return a if f is None else f(a, kind, geom)
+class bf16_convolutions:
+    """Context manager: the oracle follows rules R1-R3 above while it is active."""
+
+    def __enter__(self):
+        self.prev = _MODE["bf16"]
+        _MODE["bf16"] = True
+        return self
+
+    def __exit__(self, *exc):
+        _MODE["bf16"] = self.prev
+
+
+def bf16_round(a):
+    """Round to bfloat16 (8 significand bits, 8 exponent bits; IEEE round to nearest,
+    ties to even), through fp32 (device operands are fp32 values), returned as fp64.
+
+    Written from the definition: a finite fp32 value v with binary exponent
+    e = floor(log2|v|) (clamped to -126, the subnormal range) lies on the bf16 grid
+    of spacing ulp = 2^(e-7); v/ulp is rounded half-to-even; results of magnitude
+    >= 2^128 overflow to inf.  NaN and inf pass through."""
+    v = np.asarray(a, np.float32).astype(np.float64)
+    out = v.copy()
+    fin = np.isfinite(v) & (v != 0)
+    e = np.frexp(v[fin])[1] - 1.0            # v = m * 2^e, 1 <= |m| < 2 (exact)
+    e = np.maximum(e, -126.0)
+    ulp = np.exp2(e - 7.0)
+    r = np.round(v[fin] / ulp) * ulp        # numpy rounds half to even
+    r[np.abs(r) >= 2.0 ** 128] = np.inf * np.sign(r[np.abs(r) >= 2.0 ** 128])
+    out[fin] = r
+    return out
+
+
+def _op(a):
+    """A convolution operand / forward result under the active precision (R1, R2)."""
+    return bf16_round(a) if _MODE["bf16"] else a
 
 
 # --------------------------------------------------------------------------- conv
@@ -61,14 +101,13 @@ def conv2d(x, w, stride=1, pad=0):
     if C != C2 or k != k2:
         raise ValueError(f"conv2d shape mismatch x{x.shape} w{w.shape}")
     Ho, Wo = conv_out_size(H, k, stride, pad), conv_out_size(W, k, stride, pad)
-    geom = (B, H, W, C, O, k, stride)
-    x, w = _rnd("fwd", x, geom), _rnd("fwd", w, geom)
+    x, w = _op(x), _op(w)                                  # R1
     xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
     out = np.zeros((B, O, Ho, Wo))
     for kh, kw, view in _taps(xp, k, stride, Ho, Wo):
         # sum over c of view[b,c,i,j] * w[o,c,kh,kw]  -> [B,Ho,Wo,O]
         out += np.tensordot(view, w[:, :, kh, kw], axes=([1], [1])).transpose(0, 3, 1, 2)
-    return _rnd("fwd_out", out, geom)
+    return _op(out)                                        # R2
 
 
 def conv2d_vjp(x, w, stride, pad, dout, need_dx=True):
@@ -80,9 +119,8 @@ def conv2d_vjp(x, w, stride, pad, dout, need_dx=True):
     B, C, H, W = x.shape
     O, _, k, _ = w.shape
     Ho, Wo = dout.shape[2], dout.shape[3]
-    geom = (B, H, W, C, O, k, stride)
-    xw, dw_out = _rnd("wgrad", x, geom), _rnd("wgrad", dout, geom)
-    dd_out, wd = _rnd("dgrad", dout, geom), _rnd("dgrad", w, geom)
+    xw, dw_out = _op(x), _op(dout)                         # R1 (wgrad operands)
+    dd_out, wd = _op(dout), _op(w)                         # R1 (dgrad operands)
     xp = np.pad(xw, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
     dxp = np.zeros_like(xp) if need_dx else None
     dw = np.zeros_like(w)
@@ -136,9 +174,23 @@ def bn_train_vjp(cache, gamma, dout):
 
 
 # --------------------------------------------------------------------------- relu / pool
+# ReLU-mask instrumentation for the bf16 flip-floor derivation (DESIGN.md reading
+# c25).  ``MASKS["record"]``: a list that receives every mask decided; ``MASKS["replay"]``:
+# a list of masks consumed in order instead of deciding them (the same code path run
+# twice calls relu in the same order).  Both None (the default): plain ReLU.
+MASKS = {"record": None, "replay": None}
+
+
 def relu(a):
     """ReLU with mask a > 0 (reading c19: derivative 0 at 0)."""
     mask = a > 0
+    if MASKS["replay"] is not None:
+        m = MASKS["replay"].pop(0)
+        if m.shape != mask.shape:
+            raise ValueError(f"mask replay out of order: {m.shape} vs {mask.shape}")
+        mask = m
+    if MASKS["record"] is not None:
+        MASKS["record"].append(mask.copy())
     return np.where(mask, a, 0.0), mask
 
 

@@ -6,11 +6,14 @@
 namespace petra {
 
 // ---------------------------------------------------------------- SIMT fp32 convolutions
-void conv_fwd_simt(const ConvGeom &g, const float *x, const float *w, float *z, cudaStream_t st);
+// bf16 = true: operands rounded to bf16 on load and the forward z on store (the
+// bf16 path's rule for every convolution pass, reading c22)
+void conv_fwd_simt(const ConvGeom &g, const float *x, const float *w, float *z, cudaStream_t st, bool bf16 = false);
 void conv_dgrad_simt(const ConvGeom &g, const float *dz, const float *w, const float *addend, float *dx,
-                     cudaStream_t st);
+                     cudaStream_t st, bool bf16 = false);
 size_t conv_wgrad_simt_workspace(const ConvGeom &g);
-void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *dw, float *ws, cudaStream_t st);
+void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *dw, float *ws, cudaStream_t st,
+                     bool bf16 = false);
 
 // ---------------------------------------------------------------- tcgen05 bf16 convolutions
 // bf16 activation operands are [B][H][W][C], or -- "padded" -- [B][H+2][W+2][C] with

@@ -1,8 +1,12 @@
 // conv_simt.cu -- fp32 SIMT implicit-GEMM convolutions (forward, dgrad, wgrad).
 //
 // The fp32 parity path (PETRA_FP32): TF32 tensor cores cannot meet rel 1e-4
-// (10-bit mantissa), so these run on the FFMA pipe.  They also serve the stem
-// (C_in = 3) on the bf16 path.  NHWC activations, weights [Co][k][k][Ci].
+// (10-bit mantissa), so these run on the FFMA pipe.  On the bf16 path they serve
+// the geometries the tensor-core kernels do not take (channel counts that are not
+// multiples of 64, the MLP's linear layers): there (RND = true) every operand is
+// rounded to bf16 on load and the forward result z to bf16 on store, so every
+// convolution pass of PETRA_BF16_TC follows one rule whichever engine runs it
+// (reading c22).  NHWC activations, weights [Co][k][k][Ci].
 //
 //   forward : z[m][co]   = sum_{kh,kw,ci} x[b][ho*s+kh-p][wo*s+kw-p][ci] * w[co][kh][kw][ci]
 //   dgrad   : dx[m'][ci] = sum_{kh,kw,co} dz[b][(h+p-kh)/s][(w+p-kw)/s][co] * w[co][kh][kw][ci]
@@ -18,7 +22,13 @@ namespace {
 constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
 enum { FWD = 0, DGRAD = 1, WGRAD = 2 };
 
-template <int MODE>
+// round-to-nearest-even to bf16, kept in an fp32 register (reading c22)
+template <bool RND>
+__device__ __forceinline__ float opnd(float v) {
+  return RND ? __bfloat162float(__float2bfloat16_rn(v)) : v;
+}
+
+template <int MODE, bool RND>
 __global__ void __launch_bounds__(NT)
 conv_simt_kernel(ConvGeom g, const float *__restrict__ asrc, const float *__restrict__ bsrc,
                  float *__restrict__ out, const float *__restrict__ addend,
@@ -70,7 +80,7 @@ conv_simt_kernel(ConvGeom g, const float *__restrict__ asrc, const float *__rest
           if (hi >= 0 && hi < g.H && wi >= 0 && wi < g.W)
             v = asrc[(((int64_t)ab * g.H + hi) * g.W + wi) * g.Ci + ci];
         }
-        As[a_kq + i][a_row] = v;
+        As[a_kq + i][a_row] = opnd<RND>(v);
       }
     } else if (MODE == DGRAD) {
 #pragma unroll
@@ -86,7 +96,7 @@ conv_simt_kernel(ConvGeom g, const float *__restrict__ asrc, const float *__rest
             if (ho < g.Ho && wo < g.Wo) v = asrc[(((int64_t)ab * g.Ho + ho) * g.Wo + wo) * g.Co + co];
           }
         }
-        As[a_kq + i][a_row] = v;
+        As[a_kq + i][a_row] = opnd<RND>(v);
       }
     } else {  // WGRAD: A[m=co][kk=pixel] = dz[pixel][co]
       const int kl = t >> 4, mq = (t & 15) * 4;
@@ -94,7 +104,7 @@ conv_simt_kernel(ConvGeom g, const float *__restrict__ asrc, const float *__rest
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         int64_t m = m0 + mq + i;
-        As[kl][mq + i] = (kk < kend && m < M) ? asrc[kk * g.Co + m] : 0.f;
+        As[kl][mq + i] = (kk < kend && m < M) ? opnd<RND>(asrc[kk * g.Co + m]) : 0.f;
       }
     }
     // ---------------- B tile -> Bs[kk][n]
@@ -104,7 +114,7 @@ conv_simt_kernel(ConvGeom g, const float *__restrict__ asrc, const float *__rest
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         int64_t kk = k0 + kq + i;
-        Bs[kq + i][nl] = (n < N && kk < kend) ? bsrc[(int64_t)n * K + kk] : 0.f;
+        Bs[kq + i][nl] = (n < N && kk < kend) ? opnd<RND>(bsrc[(int64_t)n * K + kk]) : 0.f;
       }
     } else if (MODE == DGRAD) {
       const int kl = t >> 4, nq = (t & 15) * 4;
@@ -115,7 +125,7 @@ conv_simt_kernel(ConvGeom g, const float *__restrict__ asrc, const float *__rest
       for (int i = 0; i < 4; ++i) {
         int n = n0 + nq + i;
         Bs[kl][nq + i] = (kk < kend && n < N)
-                             ? bsrc[((int64_t)co * g.k * g.k + tap) * g.Ci + n] : 0.f;
+                             ? opnd<RND>(bsrc[((int64_t)co * g.k * g.k + tap) * g.Ci + n]) : 0.f;
       }
     } else {  // WGRAD: B[kk=pixel][n=(kh,kw,ci)] = x[...]
       const int kl = t >> 4, nq = (t & 15) * 4;
@@ -139,7 +149,7 @@ conv_simt_kernel(ConvGeom g, const float *__restrict__ asrc, const float *__rest
           if (hi >= 0 && hi < g.H && wi >= 0 && wi < g.W)
             v = bsrc[(((int64_t)b * g.H + hi) * g.W + wi) * g.Ci + ci];
         }
-        Bs[kl][nq + i] = v;
+        Bs[kl][nq + i] = opnd<RND>(v);
       }
     }
     __syncthreads();
@@ -167,7 +177,7 @@ conv_simt_kernel(ConvGeom g, const float *__restrict__ asrc, const float *__rest
       if (n >= N) continue;
       float v = acc[i][j];
       if (addend) v += addend[m * N + n];
-      out[m * N + n] = v;
+      out[m * N + n] = MODE == FWD ? opnd<RND>(v) : v;
     }
   }
 }
@@ -185,19 +195,21 @@ __global__ void splitk_reduce_kernel(const float *__restrict__ part, int splits,
 
 }  // namespace
 
-void conv_fwd_simt(const ConvGeom &g, const float *x, const float *w, float *z, cudaStream_t st) {
+void conv_fwd_simt(const ConvGeom &g, const float *x, const float *w, float *z, cudaStream_t st, bool bf16) {
   int64_t M = g.M();
   dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(g.Co, BN), 1);
-  launch_k(conv_simt_kernel<FWD>, grid, NT, 0, st, g, x, w, z, nullptr, M, g.Co, g.K(), g.K());
+  launch_k(bf16 ? conv_simt_kernel<FWD, true> : conv_simt_kernel<FWD, false>, grid, NT, 0, st, g, x, w, z, nullptr,
+           M, g.Co, g.K(), g.K());
   PETRA_LAUNCH_CHECK();
 }
 
 void conv_dgrad_simt(const ConvGeom &g, const float *dz, const float *w, const float *addend,
-                     float *dx, cudaStream_t st) {
+                     float *dx, cudaStream_t st, bool bf16) {
   int64_t M = g.Min();
   int64_t K = (int64_t)g.k * g.k * g.Co;
   dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(g.Ci, BN), 1);
-  launch_k(conv_simt_kernel<DGRAD>, grid, NT, 0, st, g, dz, w, dx, addend, M, g.Ci, K, K);
+  launch_k(bf16 ? conv_simt_kernel<DGRAD, true> : conv_simt_kernel<DGRAD, false>, grid, NT, 0, st, g, dz, w, dx,
+           addend, M, g.Ci, K, K);
   PETRA_LAUNCH_CHECK();
 }
 
@@ -209,7 +221,8 @@ size_t conv_wgrad_simt_workspace(const ConvGeom &g) {
 }
 
 void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *dw, float *ws,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool bf16) {
+  auto kern = bf16 ? conv_simt_kernel<WGRAD, true> : conv_simt_kernel<WGRAD, false>;
   int64_t M = g.Co, N = g.K(), K = g.M();
   int64_t tiles = cdiv(M, BM) * cdiv(N, BN);
   int splits = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(2 * kNumSMs, tiles), cdiv(K, 256)));
@@ -217,11 +230,11 @@ void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *
   splits = (int)cdiv(K, kchunk);
   dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN), splits);
   if (splits == 1) {
-    launch_k(conv_simt_kernel<WGRAD>, grid, NT, 0, st, g, dz, x, dw, nullptr, M, (int)N, K, kchunk);
+    launch_k(kern, grid, NT, 0, st, g, dz, x, dw, nullptr, M, (int)N, K, kchunk);
     PETRA_LAUNCH_CHECK();
     return;
   }
-  launch_k(conv_simt_kernel<WGRAD>, grid, NT, 0, st, g, dz, x, ws, nullptr, M, (int)N, K, kchunk);
+  launch_k(kern, grid, NT, 0, st, g, dz, x, ws, nullptr, M, (int)N, K, kchunk);
   PETRA_LAUNCH_CHECK();
   int64_t n = M * N;
   launch_k(splitk_reduce_kernel, (unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st, 

@@ -570,7 +570,7 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
     L.stats_rows() = conv_fwd_tc(L.g, L.xbp(), L.xpad, L.w_bf16->as<__nv_bfloat16>(), L.z()->p, L.z16,
                                  wgrad_ws()->as<float>(), reinterpret_cast<float *>(part()->p), st, &fin);
   } else {
-    conv_fwd_simt(L.g, x, w, L.z()->as<float>(), st);
+    conv_fwd_simt(L.g, x, w, L.z()->as<float>(), st, tc_);
   }
 }
 
@@ -590,7 +590,7 @@ void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
     conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.xbp(), L.xpad, dw,
                   wgrad_ws()->as<float>(), st);
   } else {
-    conv_wgrad_simt(L.g, L.dz->as<float>(), x, dw, wgrad_ws()->as<float>(), st);
+    conv_wgrad_simt(L.g, L.dz->as<float>(), x, dw, wgrad_ws()->as<float>(), st, tc_);
   }
 }
 
@@ -602,7 +602,7 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
     conv_dgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.wt_bf16->as<__nv_bfloat16>(), addend, out,
                   wgrad_ws()->as<float>(), st);
   } else {
-    conv_dgrad_simt(L.g, L.dz->as<float>(), theta_->as<float>() + L.w_off, addend, out, st);
+    conv_dgrad_simt(L.g, L.dz->as<float>(), theta_->as<float>() + L.w_off, addend, out, st, tc_);
   }
 }
 

@@ -94,36 +94,13 @@ def rand_params(units, seed):
     return units
 
 
-def bf16_round(a):
-    """Round to bfloat16 (round-to-nearest-even) through fp32, as the kernels do."""
-    f = np.ascontiguousarray(np.asarray(a, np.float32))
-    u = f.view(np.uint32).astype(np.uint64)
-    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
-    return u.astype(np.uint32).view(np.float32).astype(np.float64)
-
-
-class bf16_emulation:
-    """Context manager: make the oracle round conv operands to bf16 exactly where
-    libpetra runs that convolution pass on the tcgen05 engine (reading c22), and the
-    forward result z too, which that engine stores in bf16 (reading c24)."""
-
-    def __enter__(self):
-        import ctypes as C
-        from oracle import primitives as OP
-        self.OP = OP
-        self.saved = dict(OP.OPERAND_ROUND)
-        cache = {}
-
-        def hook(a, kind, geom):
-            mode = {"fwd": 0, "dgrad": 1, "wgrad": 2, "fwd_out": 0}[kind]
-            key = (mode, geom)
-            if key not in cache:
-                g = L.PetraConvGeom(*geom)
-                cache[key] = L.lib().petra_conv_engine(C.byref(g), mode, L.BF16_TC) == 1
-            return bf16_round(a) if cache[key] else a
-        for k in OP.OPERAND_ROUND:
-            OP.OPERAND_ROUND[k] = hook
-        return self
-
-    def __exit__(self, *exc):
-        self.OP.OPERAND_ROUND.update(self.saved)
+def elementwise(got, want):
+    """Element-wise view of a comparison (per-tensor norms hide a wrong
+    row): max |err| / max |want|, and the fraction of elements whose error exceeds
+    1e-2 of the tensor's rms ("outliers")."""
+    a, b = np.asarray(got, np.float64).ravel(), np.asarray(want, np.float64).ravel()
+    err = np.abs(a - b)
+    rms = np.sqrt(np.mean(b * b)) if b.size else 0.0
+    mx = float(err.max() / max(np.abs(b).max(), 1e-30)) if b.size else 0.0
+    out = float(np.mean(err > 1e-2 * max(rms, 1e-30))) if b.size else 0.0
+    return mx, out
