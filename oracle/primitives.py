@@ -35,7 +35,16 @@ BN_MOMENTUM = 0.1    # reading c9
 #
 # The ReLU masks are integers decided from floating point; under this rule both
 # sides decide them on the same rounded operands (up to accumulation order).
-_MODE = {"bf16": False}
+#
+# ``fp32_accumulation()`` (reading c25) changes the rounding, not the
+# arithmetic: every convolution accumulates in fp32 (numpy's float32 contraction, a
+# summation order of its own) and the tensors a device keeps in fp32 -- the stream
+# halves after each coupling add / subtract, BN-ReLU activations, gradient sums -- are
+# rounded to fp32 where they are produced (:func:`stored`).  It is not a model of any
+# kernel; the tests use it to MEASURE how far an implementation of the same arithmetic
+# that differs only in its rounding lands from the oracle -- through the ReLU masks
+# such rounding moves.
+_MODE = {"bf16": False, "acc32": False}
 
 
 class bf16_convolutions:
@@ -48,6 +57,27 @@ class bf16_convolutions:
 
     def __exit__(self, *exc):
         _MODE["bf16"] = self.prev
+
+
+class fp32_accumulation:
+    """Context manager: convolutions accumulate in fp32 while it is active (c25)."""
+
+    def __enter__(self):
+        self.prev = _MODE["acc32"]
+        _MODE["acc32"] = True
+        return self
+
+    def __exit__(self, *exc):
+        _MODE["acc32"] = self.prev
+
+
+def _acc():
+    return np.float32 if _MODE["acc32"] else np.float64
+
+
+def stored(a):
+    """A tensor the device keeps in fp32: rounded to fp32 under fp32_accumulation()."""
+    return np.asarray(a, np.float32).astype(np.float64) if _MODE["acc32"] else a
 
 
 def bf16_round(a):
@@ -103,10 +133,13 @@ def conv2d(x, w, stride=1, pad=0):
     Ho, Wo = conv_out_size(H, k, stride, pad), conv_out_size(W, k, stride, pad)
     x, w = _op(x), _op(w)                                  # R1
     xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
-    out = np.zeros((B, O, Ho, Wo))
+    dt = _acc()
+    xp, w = xp.astype(dt, copy=False), w.astype(dt, copy=False)
+    out = np.zeros((B, O, Ho, Wo), dt)
     for kh, kw, view in _taps(xp, k, stride, Ho, Wo):
         # sum over c of view[b,c,i,j] * w[o,c,kh,kw]  -> [B,Ho,Wo,O]
         out += np.tensordot(view, w[:, :, kh, kw], axes=([1], [1])).transpose(0, 3, 1, 2)
+    out = out.astype(np.float64, copy=False)
     return _op(out)                                        # R2
 
 
@@ -122,16 +155,19 @@ def conv2d_vjp(x, w, stride, pad, dout, need_dx=True):
     xw, dw_out = _op(x), _op(dout)                         # R1 (wgrad operands)
     dd_out, wd = _op(dout), _op(w)                         # R1 (dgrad operands)
     xp = np.pad(xw, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
-    dxp = np.zeros_like(xp) if need_dx else None
-    dw = np.zeros_like(w)
+    dt = _acc()
+    xp, dw_out = xp.astype(dt, copy=False), dw_out.astype(dt, copy=False)
+    dd_out, wd = dd_out.astype(dt, copy=False), wd.astype(dt, copy=False)
+    dxp = np.zeros(xp.shape, dt) if need_dx else None
+    dw = np.zeros(w.shape, dt)
     for kh, kw, view in _taps(xp, k, stride, Ho, Wo):
         dw[:, :, kh, kw] = np.tensordot(dw_out, view, axes=([0, 2, 3], [0, 2, 3]))
         if need_dx:
             contrib = np.tensordot(dd_out, wd[:, :, kh, kw], axes=([1], [0]))  # [B,Ho,Wo,C]
             dxp[:, :, kh:kh + stride * (Ho - 1) + 1:stride,
                 kw:kw + stride * (Wo - 1) + 1:stride] += contrib.transpose(0, 3, 1, 2)
-    dx = dxp[:, :, pad:pad + H, pad:pad + W].copy() if need_dx else None
-    return dx, dw
+    dx = dxp[:, :, pad:pad + H, pad:pad + W].astype(np.float64) if need_dx else None
+    return dx, dw.astype(np.float64, copy=False)
 
 
 # --------------------------------------------------------------------------- batch norm
@@ -174,16 +210,21 @@ def bn_train_vjp(cache, gamma, dout):
 
 
 # --------------------------------------------------------------------------- relu / pool
-# ReLU-mask instrumentation for the bf16 flip-floor derivation (DESIGN.md reading
-# c25).  ``MASKS["record"]``: a list that receives every mask decided; ``MASKS["replay"]``:
-# a list of masks consumed in order instead of deciding them (the same code path run
-# twice calls relu in the same order).  Both None (the default): plain ReLU.
-MASKS = {"record": None, "replay": None}
+# ReLU-mask instrumentation for the flip-floor derivation (reading c25).
+# ``MASKS["record"]``: a list that receives every mask decided; ``MASKS["replay"]``: a
+# list of masks consumed in order instead of deciding them (the same code path run
+# twice calls relu in the same order); ``MASKS["band"]``: tau -- every decision whose
+# pre-activation lies within tau * rms(a) of zero is taken the other way.  All None
+# (the default): plain ReLU.
+MASKS = {"record": None, "replay": None, "band": None}
 
 
 def relu(a):
     """ReLU with mask a > 0 (reading c19: derivative 0 at 0)."""
     mask = a > 0
+    if MASKS["band"] is not None:
+        near = np.abs(a) <= MASKS["band"] * np.sqrt(np.mean(a * a))
+        mask = mask ^ near
     if MASKS["replay"] is not None:
         m = MASKS["replay"].pop(0)
         if m.shape != mask.shape:

@@ -49,13 +49,13 @@ class ConvBN:
         mask = None
         if self.act:
             y, mask = P.relu(y)
-        return y, (x, bc, mask)
+        return P.stored(y), (x, bc, mask)
 
     def vjp(self, cache, dout, need_dx=True):
         x, bc, mask = cache
         g = dout * mask if self.act else dout
         dz, dgamma, dbeta = P.bn_train_vjp(bc, self.gamma, g)
-        dx, dw = P.conv2d_vjp(x, self.w, self.stride, self.pad, dz, need_dx)
+        dx, dw = P.conv2d_vjp(x, self.w, self.stride, self.pad, P.stored(dz), need_dx)
         return dx, [dw, dgamma, dbeta]
 
     def flops_fwd(self, x_shape):
@@ -130,19 +130,19 @@ class RevUnit:
     def forward_graph(self, xs, update_stats=False):
         out, caches = self.phi.forward(xs[self.src], update_stats)
         ys = list(xs)
-        ys[self.dst] = xs[self.dst] + out
+        ys[self.dst] = P.stored(xs[self.dst] + out)
         return ys, caches
 
     def reconstruct(self, ys):
         out, caches = self.phi.forward(ys[self.src], update_stats=True)
         xs = list(ys)
-        xs[self.dst] = ys[self.dst] - out
+        xs[self.dst] = P.stored(ys[self.dst] - out)
         return xs, caches
 
     def vjp(self, caches, ds):
         dsrc, grads = self.phi.vjp(caches, ds[self.dst])
         out = list(ds)
-        out[self.src] = ds[self.src] + dsrc   # delta of dst passes through unchanged
+        out[self.src] = P.stored(ds[self.src] + dsrc)   # delta of dst passes through unchanged
         return out, grads
 
     def flops_fwd(self, shapes):
@@ -177,7 +177,7 @@ class DSUnit:
         pa_out, c_pa = self.pa.forward(xs[self.dst], update_stats)
         pb_out, c_pb = self.pb.forward(xs[self.src], update_stats)
         ys = [None, None]
-        ys[self.dst] = pa_out + phi_out
+        ys[self.dst] = P.stored(pa_out + phi_out)
         ys[self.src] = pb_out
         return ys, (c_phi, c_pa, c_pb)
 
@@ -189,7 +189,7 @@ class DSUnit:
         out = [None, None]
         if need_dx:
             out[self.dst] = d_dst
-            out[self.src] = d_src_phi + d_src_pb
+            out[self.src] = P.stored(d_src_phi + d_src_pb)
         return out, g_phi + g_pa + g_pb
 
     def flops_fwd(self, shapes):

@@ -21,6 +21,7 @@ initial state and is compared with these three records.
 """
 from __future__ import annotations
 
+import contextlib
 import copy
 import functools
 
@@ -36,6 +37,27 @@ WORKLOADS = {
     "r18_b64_j4": ("revnet18", 32, 10, 64, [5, 4, 4, 5], 5e-4),
 }
 LR = 0.025  # PAPER.md:256, 0.1 * 64 / 256 at k = 1
+# the fp32 rounding band of a mask decision (reading c25): 4 sigma of the rounding
+# error of a K-term fp32 dot product relative to its rms, u * sqrt(K) with
+# u = 2^-24 and K up to 4608 (RevNet's 3x3 x 512): 4 * 6e-8 * 68 = 1.6e-5 -> 2e-5
+BAND_FP32 = 2e-5
+
+
+@contextlib.contextmanager
+def oracle_mode(bf16=False, acc32=False, band=None):
+    """The oracle's arithmetic for one run: rules R1-R3 (bf16), fp32 rounding (acc32),
+    mask decisions in the fp32 band flipped (band)."""
+    with contextlib.ExitStack() as st:
+        if bf16:
+            st.enter_context(OP.bf16_convolutions())
+        if acc32:
+            st.enter_context(OP.fp32_accumulation())
+        prev = OP.MASKS["band"]
+        OP.MASKS["band"] = band
+        try:
+            yield
+        finally:
+            OP.MASKS["band"] = prev
 
 
 def init_units(model, H, classes, seed=1):
@@ -118,7 +140,7 @@ def chain(workload="r18_b64_j4"):
         fwd_out[j] = stages[j - 1].forward(E.Fwd(0, x_in[j], lab)).xs
         OP.MASKS["record"] = None
         x_in[j + 1] = fwd_out[j]
-    recs = {"exact": {}, "bf16": {}, "pinned": {}}
+    recs = {"exact": {}}
     OP.MASKS["record"] = masks[J].setdefault("fwd", [])
     loss, bo = stages[J - 1].tail_step(E.Fwd(0, x_in[J], lab))
     OP.MASKS["record"] = None
@@ -134,26 +156,41 @@ def chain(workload="r18_b64_j4"):
             bwd_in[j - 1] = (b.xs, b.ds)
     inputs = {j: (x_in[j], lab, *(bwd_in[j] if j < J else (None, None))) for j in range(1, J + 1)}
 
-    # bf16 rule (its masks recorded) and bf16 rule with the exact masks replayed,
-    # stage by stage on the same inputs
-    bmasks = {j: {} for j in range(1, J + 1)}
-    for mode in ("bf16", "pinned"):
+    # the other oracle runs, stage by stage on the same inputs (masks recorded, or
+    # replayed for "pinned"):
+    #   bf16         rules R1-R3                         (the bf16 path's arithmetic)
+    #   pinned       rules R1-R3 with the exact masks     (c25: the floor is the flips)
+    #   *_acc32      convolutions accumulated / tensors stored in fp32 (c25: another rounding)
+    #   *_band       every decision within the fp32 rounding band of zero flipped (c25)
+    runs = {"bf16": (True, False, None), "pinned": (True, False, None), "exact_acc32": (False, True, None),
+            "bf16_acc32": (True, True, None), "exact_band": (False, False, BAND_FP32),
+            "bf16_band": (True, False, BAND_FP32)}
+    mrec = {m: {j: {} for j in range(1, J + 1)} for m in runs}
+    for mode, (b16, a32, band) in runs.items():
+        recs.setdefault(mode, {})
         units = copy.deepcopy(units0)
         groups = OM.group(units, counts)
         for j in range(1, J + 1):
             s = E.Stage(groups[j - 1], opt, j, J)
             s.lr = LR
-            m = ("replay", masks[j]) if mode == "pinned" else ("record", bmasks[j])
-            with OP.bf16_convolutions():
+            m = ("replay", masks[j]) if mode == "pinned" else ("record", mrec[mode][j])
+            with oracle_mode(b16, a32, band):
                 recs[mode][j] = _tick(s, j, J, *inputs[j], masks=m)
-    # mask decisions that differ between the exact and the bf16-rule oracle, per
-    # stage: (flipped, total)
-    flips = {}
-    for j in range(1, J + 1):
-        f = n = 0
-        for kind in bmasks[j]:
-            for a, b in zip(bmasks[j][kind], masks[j][kind]):
-                f += int(np.count_nonzero(a != b))
-                n += a.size
-        flips[j] = (f, n)
+    mrec["exact"] = masks
+
+    def count(a, b):
+        out = {}
+        for j in range(1, J + 1):
+            f = n = 0
+            for kind in mrec[a][j]:
+                for x, y in zip(mrec[a][j][kind], mrec[b][j][kind]):
+                    f += int(np.count_nonzero(x != y))
+                    n += x.size
+            out[j] = (f, n)
+        return out
+
+    # mask decisions that differ, per stage: (flipped, total)
+    flips = {"bf16_vs_exact": count("bf16", "exact"), "exact_acc32_vs_exact": count("exact_acc32", "exact"),
+             "bf16_acc32_vs_bf16": count("bf16_acc32", "bf16"), "exact_band_vs_exact": count("exact_band", "exact"),
+             "bf16_band_vs_bf16": count("bf16_band", "bf16")}
     return units0, counts, inputs, recs, flips

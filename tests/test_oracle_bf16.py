@@ -118,9 +118,11 @@ def test_c25_decomposition_small_revnet18_chain():
     from tests.gpu_harness import rel
     FO.WORKLOADS.setdefault("r18_b4_j4", ("revnet18", 32, 10, 4, [5, 4, 4, 5], 5e-4))
     units0, counts, inputs, recs, flips = FO.chain("r18_b4_j4")
-    total_f = sum(f for f, _ in flips.values())
-    total_n = sum(n for _, n in flips.values())
-    assert 1e-5 < total_f / total_n < 1e-2, flips
+    frac = {k: sum(f for f, _ in v.values()) / sum(n for _, n in v.values()) for k, v in flips.items()}
+    assert 1e-5 < frac["bf16_vs_exact"] < 1e-2, flips
+    # another summation order of the same arithmetic moves far fewer decisions
+    assert frac["exact_acc32_vs_exact"] < frac["bf16_vs_exact"] / 20, frac
+    assert frac["bf16_acc32_vs_bf16"] < frac["bf16_vs_exact"] / 5, frac
     for j in range(1, len(counts) + 1):
         ex, bq, pq = recs["exact"][j], recs["bf16"][j], recs["pinned"][j]
         for key in ("fwd", "xt", "d"):

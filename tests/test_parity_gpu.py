@@ -2,7 +2,6 @@
 identical seeded inputs and parameters.  Tolerances (north_star): rel 1e-4 for
 the fp32 path, rel 2e-2 for the bf16 tensor-core path (tests/parity_rule.py),
 integer schedule reports bit-exact."""
-import contextlib
 
 import numpy as np
 import pytest
@@ -10,10 +9,10 @@ import pytest
 import synth
 from oracle import engine as E
 from oracle import models as OM
-from oracle import primitives as OP
 from oracle.units import Branch, ConvBN, DSUnit, RevUnit, StemUnit, TailUnit
 from tests.gpu_harness import (nchw, nhwc, oracle_to_product_units, pack_like, pack_params, per_tensor_rel,
                                rand_params, rel)
+from tests import fullsize_oracle as FO
 from tests.parity_rule import Report
 
 pytestmark = pytest.mark.gpu
@@ -94,9 +93,8 @@ STAGE_CASES = {
 }
 
 
-def _oracle_stage_tick(make, B, in_shapes, bf16):
-    """The oracle's single tick of a non-final stage on the test's inputs: exact, or
-    under rules R1-R3 (oracle.primitives.bf16_convolutions, reading c22)."""
+def _oracle_stage_tick(make, B, in_shapes, bf16, acc32=False, band=None):
+    """The oracle's single tick of a non-final stage on the test's inputs."""
     units = make()
     rand_params(units, 3)
     ostage = E.Stage(units, E.OptConfig(), 1, 2)
@@ -106,7 +104,7 @@ def _oracle_stage_tick(make, B, in_shapes, bf16):
     # message for both oracles and the GPU), random delta
     xt = [a + 0.05 * synth.normal(a.shape, 7, h) for h, a in enumerate(_exact_fwd(make, B, in_shapes))]
     dd = [synth.normal(a.shape, 8, h) for h, a in enumerate(xt)]
-    with (OP.bf16_convolutions() if bf16 else contextlib.nullcontext()):
+    with FO.oracle_mode(bf16, acc32, band):
         fo = ostage.forward(E.Fwd(0, xs, None))
         bo = ostage.backward(E.Bwd(0, xt, dd))
     th, bf = pack_params(units)
@@ -146,6 +144,8 @@ def test_stage_tick_parity(case, precision):
     bf16 = precision == L.BF16_TC
     ex = _oracle_stage_tick(make, B, in_shapes, False)
     bq = _oracle_stage_tick(make, B, in_shapes, True) if bf16 else None
+    alts = [_oracle_stage_tick(make, B, in_shapes, bf16, acc32=True),
+            _oracle_stage_tick(make, B, in_shapes, bf16, band=FO.BAND_FP32)]
     units = make()
     stem = isinstance(units[0], StemUnit)
     in_hwc = tuple(np.array(in_shapes[0])[[2, 3, 1]])
@@ -169,13 +169,14 @@ def test_stage_tick_parity(case, precision):
     if not stem:
         for h in range(2):
             rep.add(f"bwd.xt{h + 1}", nchw(host(in_half[h])), ex["xt"][h], b_("xt", h))
-            rep.add(f"bwd.d{h + 1}", nchw(host(in_half[2 + h])), ex["d"][h], b_("d", h), gated=True)
+            rep.add(f"bwd.d{h + 1}", nchw(host(in_half[2 + h])), ex["d"][h], b_("d", h), gated=True,
+                    alt=[a["d"][h] for a in alts])
     g = st.get_grads()
     th, v, bf = st.get_params()
     for name, a, b in _slices(units):
-        rep.add("grad." + name, g[a:b], ex["grads"][a:b], bq["grads"][a:b] if bf16 else None, gated=True)
-        rep.add("theta." + name, th[a:b], ex["theta"][a:b], bq["theta"][a:b] if bf16 else None)
-        rep.add("v." + name, v[a:b], ex["v"][a:b], bq["v"][a:b] if bf16 else None, gated=True)
+        for key, got in (("grads", g), ("theta", th), ("v", v)):
+            rep.add(f"{key}.{name}", got[a:b], ex[key][a:b], bq[key][a:b] if bf16 else None, gated=True,
+                    alt=[x[key][a:b] for x in alts])
     rep.add("running", bf, ex["buffers"], b_("buffers"))
     print(rep.text())
     assert rep.ok, "\n" + rep.text()
@@ -194,14 +195,14 @@ TAIL_CASES = {
 }
 
 
-def _oracle_tail(make, B, in_shapes, bf16):
+def _oracle_tail(make, B, in_shapes, bf16, acc32=False, band=None):
     units = make()
     rand_params(units, 3)
     ostage = E.Stage(units, E.OptConfig(), 2, 2)
     ostage.lr = 0.1
     xs = [synth.images(s, 0, i) for i, s in enumerate(in_shapes)]
     lab = synth.labels(B, units[-1].classes, 0, 0)
-    with (OP.bf16_convolutions() if bf16 else contextlib.nullcontext()):
+    with FO.oracle_mode(bf16, acc32, band):
         loss, bo = ostage.tail_step(E.Fwd(0, xs, lab))
     th, bf = pack_params(units)
     return {"xs": xs, "lab": lab, "loss": loss, "d": bo.ds, "grads": pack_like(units, ostage.last_grads),
@@ -216,6 +217,8 @@ def test_tail_stage_parity(case, precision):
     bf16 = precision == L.BF16_TC
     ex = _oracle_tail(make, B, in_shapes, False)
     bq = _oracle_tail(make, B, in_shapes, True) if bf16 else None
+    alts = [_oracle_tail(make, B, in_shapes, bf16, acc32=True),
+            _oracle_tail(make, B, in_shapes, bf16, band=FO.BAND_FP32)]
     units = make()
     in_hwc = tuple(np.array(in_shapes[0])[[2, 3, 1]])
     st = make_pair(units, B, in_hwc, precision)
@@ -230,12 +233,14 @@ def test_tail_stage_parity(case, precision):
         # the tail returns the received input unchanged (reading c7): bit-exact copy
         rep.add(f"xt{h + 1}", nchw(host(outs[h])), ex["xs"][h].astype(np.float32),
                 ex["xs"][h].astype(np.float32) if bf16 else None, tol=0.0)
-        rep.add(f"d{h + 1}", nchw(host(outs[2 + h])), ex["d"][h], bq["d"][h] if bf16 else None, gated=True)
+        rep.add(f"d{h + 1}", nchw(host(outs[2 + h])), ex["d"][h], bq["d"][h] if bf16 else None, gated=True,
+                alt=[a["d"][h] for a in alts])
     g = st.get_grads()
     th, v, bf = st.get_params()
     for name, a, b in _slices(units):
-        rep.add("grad." + name, g[a:b], ex["grads"][a:b], bq["grads"][a:b] if bf16 else None, gated=True)
-        rep.add("theta." + name, th[a:b], ex["theta"][a:b], bq["theta"][a:b] if bf16 else None)
+        for key, got in (("grads", g), ("theta", th), ("v", v)):
+            rep.add(f"{key}.{name}", got[a:b], ex[key][a:b], bq[key][a:b] if bf16 else None, gated=True,
+                    alt=[x[key][a:b] for x in alts])
     rep.add("running", bf, ex["buffers"], bq["buffers"] if bf16 else None)
     print(rep.text())
     assert rep.ok, "\n" + rep.text()
