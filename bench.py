@@ -177,8 +177,8 @@ def run_ours(a):
     import torch
     import torch.distributed as dist
 
-    from paper_2406_02052_b200 import Pipeline, _lib as L, models as PM
-    from paper_2406_02052_b200.dist import Transport, contiguous_stage_ranks
+    from paper_2406_02052_b200 import Pipeline, petra, _lib as L, models as PM
+    from paper_2406_02052_b200.dist import contiguous_stage_ranks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -201,8 +201,12 @@ def run_ours(a):
     prec = L.BF16_TC if a.precision == "bf16" else L.FP32
     specs = PM.stage_specs(units, counts, a.batch, (H, H, 3), prec, WD[a.model])
     stage_rank = contiguous_stage_ranks(a.stages, world)
-    pipe = Pipeline(specs, stage_rank, rank, world, seed=1)
-    tr = Transport(pipe) if world > 1 else None
+    if world > 1:  # the library moves the messages: ncclSend / ncclRecv on its own comm streams
+        nid = [petra.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        pipe = Pipeline(specs, stage_rank, rank, world, seed=1, transport="nccl", nccl_id=nid[0], join_comm=True)
+    else:
+        pipe = Pipeline(specs, stage_rank, rank, world, seed=1)
     J, B = a.stages, a.batch
     dev = torch.device("cuda", local)
     gen = torch.Generator(device=dev).manual_seed(0)
@@ -226,12 +230,12 @@ def run_ours(a):
         if ev:
             ev[0].record(st)
         h0 = time.perf_counter()
+        # at N > 1 the tick's neighbour exchange is inside the events: the pipeline joins
+        # the caller's stream to it (join_comm), after overlapping it with the tick's compute
         pipe.tick(t, True, xs[i] if owns_first else None, ys[i] if owns_first else None, lr, loss, report=False)
         if ev:
             host_ms.append((time.perf_counter() - h0) * 1e3)
             ev[1].record(st)
-        if tr:
-            tr.exchange(t)
         t += 1
 
     # fill the pipeline (2J-2 ticks), then one full cycle of CUDA-graph keys (a stage's
@@ -283,8 +287,6 @@ def run_ours(a):
             dy.copy_(hy[i], non_blocking=True)
         pipe.tick(t, True, dx if owns_first else None, dy if owns_first else None, lr, loss, report=False)
         hl.copy_(loss, non_blocking=True)
-        if tr:
-            tr.exchange(t)
         t += 1
     e1.record(st)
     torch.cuda.synchronize()

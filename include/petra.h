@@ -51,9 +51,9 @@ typedef enum {
   PETRA_E_ODD_CHANNELS = 3, /* a two-stream activation needs an even channel count */
   PETRA_E_EMPTY_BUFFER = 4, /* non-reversible backward with an empty FIFO: schedule bug          */
   PETRA_E_ORDER = 5,        /* backward mb id is not the FIFO head / ids not monotone            */
-  PETRA_E_NONFINITE = 6,    /* NaN/Inf loss (latched device flag, reported by get_params)        */
+  PETRA_E_NONFINITE = 6,    /* NaN/Inf loss or Delta (latched device flag, reported by get_params) */
   PETRA_E_CUDA = 7,         /* CUDA runtime error or no device                                   */
-  PETRA_E_NCCL = 8,         /* reserved (transport runs in the caller, see petra_pipeline_comm)  */
+  PETRA_E_NCCL = 8,         /* NCCL unavailable (libnccl.so.2 not loadable) or an NCCL call failed */
   PETRA_E_OOM = 9,          /* device allocation failed                                          */
   PETRA_E_UNSUPPORTED = 10  /* configuration not implemented                                     */
 } petra_status;
@@ -213,17 +213,54 @@ petra_status petra_stage_tail(petra_stage *s, uint64_t mb_id,
  * runs tick t of every local stage (forward then backward, both at theta^t,
  * then the update; reading c8).  Mailboxes are double-buffered: a message
  * produced at tick t is consumed at t+1 (PAPER.md:131-134 superscripts).
- * Same-rank neighbours hand messages over by pointer; for cross-rank
- * neighbours the caller moves the bytes listed by petra_pipeline_comm() after
- * each tick (NCCL send/recv on its own stream via torch.distributed).
+ * Same-rank neighbours hand messages over by pointer.  Cross-rank neighbours
+ * exchange only with their neighbours ("each stage ...
+ * communicates only with its neighbours"; Alg. 1 Send/Receive):
+ * forward messages (x1, x2, labels) to rank+1, backward messages (x~1, x~2, d1,
+ * d2; 2x the forward bytes) to rank-1.  The transport moves them:
+ *
+ *   PETRA_TRANSPORT_NONE   the caller moves the bytes petra_pipeline_comm() lists
+ *                          after each tick (world == 1 needs nothing);
+ *   PETRA_TRANSPORT_NCCL   the library: ncclSend / ncclRecv on two library-owned
+ *                          streams (one per direction), one NCCL group per
+ *                          direction and tick.  The forward group of tick t is
+ *                          issued when the last local stage's FORWARD of tick t is
+ *                          done, so it overlaps that tick's backwards; the
+ *                          backward group when the first local stage's backward is
+ *                          done.  At tick t+1 only the stage that consumes a
+ *                          received message waits for it (external event nodes in
+ *                          the stage's CUDA graph); the others start at once.
+ *                          nccl_id: 128 bytes from petra_nccl_unique_id() on rank 0,
+ *                          given to every rank (e.g. via torch.distributed);
+ *   PETRA_TRANSPORT_LOCAL  the same schedule, events and overlap for `world`
+ *                          pipelines of ONE process on one device (a test
+ *                          transport): ranks find each other by `local_group`
+ *                          and the sender copies into the receiver's buffer
+ *                          (cudaMemcpyAsync on its comm stream).  The host must
+ *                          run tick t of every rank before tick t+1 of any.
+ *
+ * With a library transport, petra_pipeline_tick joins the caller's stream to the
+ * tick's exchange (join_comm != 0, the default: a per-tick device timer then
+ * includes the communication) or leaves it running under the next tick
+ * (join_comm == 0).
  */
+typedef enum { PETRA_TRANSPORT_NONE = 0, PETRA_TRANSPORT_NCCL = 1, PETRA_TRANSPORT_LOCAL = 2 } petra_transport;
+
 typedef struct {
   int32_t n_stages;                /* J                                                */
   const petra_stage_desc *stages;  /* all J stage descriptors (every rank passes all)  */
   const int32_t *stage_rank;       /* rank owning stage j (contiguous, non-decreasing) */
   int32_t rank, world;
   uint64_t seed;                   /* stage j is created with seed + j                 */
+  int32_t transport;               /* petra_transport                                  */
+  const unsigned char *nccl_id;    /* NCCL: 128 bytes (petra_nccl_unique_id)           */
+  int64_t local_group;             /* LOCAL: nonzero key shared by the ranks           */
+  int32_t join_comm;               /* library transports: see above (1 = default)      */
 } petra_pipeline_desc;
+
+/* NCCL unique id for PETRA_TRANSPORT_NCCL (call on rank 0, share with all ranks).
+ * Errors: PETRA_E_NCCL (libnccl.so.2 not loadable), PETRA_E_ARG (NULL). */
+petra_status petra_nccl_unique_id(unsigned char out[128]);
 
 typedef struct petra_pipeline petra_pipeline;
 

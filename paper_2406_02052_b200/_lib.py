@@ -59,10 +59,14 @@ class PetraTickReport(C.Structure):
                 ("param_version", C.c_int64 * MAX_STAGES), ("fifo_depth", C.c_int64 * MAX_STAGES)]
 
 
+TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1, 2
+
+
 class PetraPipelineDesc(C.Structure):
     _fields_ = [("n_stages", C.c_int32), ("stages", C.POINTER(PetraStageDesc)),
                 ("stage_rank", C.POINTER(C.c_int32)), ("rank", C.c_int32), ("world", C.c_int32),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("transport", C.c_int32), ("nccl_id", C.c_void_p),
+                ("local_group", C.c_int64), ("join_comm", C.c_int32)]
 
 
 class PetraCommEntry(C.Structure):
@@ -112,6 +116,7 @@ SIGS = {
     "petra_stage_tail": (C.c_int, [P, U64, VP, VP, VP, F32, VP, VP, VP, VP, VP, VP]),
     "petra_pipeline_create": (C.c_int, [C.POINTER(PetraPipelineDesc), C.POINTER(P)]),
     "petra_pipeline_destroy": (C.c_int, [P]),
+    "petra_nccl_unique_id": (C.c_int, [VP]),
     "petra_pipeline_stage": (C.c_int, [P, I32, C.POINTER(P)]),
     "petra_pipeline_tick": (C.c_int, [P, I64, I32, VP, VP, F32, VP, VP, C.POINTER(PetraTickReport)]),
     "petra_pipeline_comm": (C.c_int, [P, I64, C.POINTER(PetraCommPlan)]),

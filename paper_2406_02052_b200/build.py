@@ -21,8 +21,24 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libpetra.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_include():
+    """nccl.h of the NCCL PyTorch ships (the one loaded at run time), else the system's.
+    Only the header is needed: libnccl.so.2 is dlopen'ed (csrc/nccl_dl.cpp)."""
+    try:
+        import nvidia.nccl as nv
+        for base in list(getattr(nv, "__path__", [])):
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    return "/usr/include"
+
+
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-                "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+                "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include()]
 
 
 def sources():
@@ -65,7 +81,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if log:
                 print(f"== {os.path.basename(s)}\n{log}")
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcuda"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcuda", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -191,6 +191,16 @@ petra_status petra_pipeline_create(const petra_pipeline_desc *d, petra_pipeline 
   });
 }
 
+petra_status petra_nccl_unique_id(unsigned char out[128]) {
+  if (!out) return fail(PETRA_E_ARG, "NULL argument");
+  return guard([&] {
+    ncclUniqueId id;
+    PETRA_NCCL(petra::nccl().GetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
 petra_status petra_pipeline_destroy(petra_pipeline *p) {
   return guard([&] { delete p; });
 }

@@ -1,11 +1,32 @@
-// pipeline.cu -- the stages of one rank, their double-buffered mailboxes and the
-// per-tick driver (product code).  Cross-rank bytes are moved by the caller
-// (NCCL send/recv through torch.distributed) from the plan of petra_pipeline_comm.
+// pipeline.cu -- the stages of one rank, their double-buffered mailboxes, the
+// per-tick driver and the neighbour exchange (product code).
+//
+// Exchange (library transports, include/petra.h "pipeline"): two comm streams, one
+// per direction.  Tick t (parity p, q = p ^ 1):
+//   stage j0 (first local, j0 > 1) forward  waits  recv_done(FWD, q)  (message of tick t-1)
+//   stage j1 (last local,  j1 < J) forward  waits  cdone[FWD][p]      (its send of t-2 released
+//                                                                      fwd_[j1][p])
+//   stage j1 backward                       waits  recv_done(BWD, q)
+//   stage j0 backward                       waits  cdone[BWD][p]      (bwd_[j0][p] released)
+// and every stage records fdone / bdone (its forward / backward part) and tdone (its
+// whole tick) per parity.  After enqueuing the stages, the FWD comm stream waits for
+// fdone[j1][p] (the message is final) and tdone[j0][q] (ghost_fwd[p] was last read at
+// t-1), moves the forward messages, records cdone[FWD][p]; the BWD stream likewise
+// with bdone[j0][p] and tdone[j1][q].  So the forward exchange of tick t runs under
+// that tick's backwards, and at tick t+1 only the stages that consume a received
+// message wait for it.
 #include "pipeline.h"
 
 #include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
 
 namespace petra {
+
+// LOCAL transport: the pipelines of one process that form one group, by rank
+static std::mutex g_hub_mu;
+static std::map<int64_t, std::vector<Pipeline *>> g_hub;
 
 static bool has_stem(const petra_stage_desc &d) { return d.n_units > 0 && d.units[0].kind == PETRA_UNIT_STEM; }
 
@@ -28,9 +49,18 @@ static std::vector<int> accum_ks(const petra_pipeline_desc &d) {
 Pipeline::Pipeline(const petra_pipeline_desc &d)
     : J_(d.n_stages),
       rank_(d.rank),
+      world_(d.world),
+      transport_(d.transport),
+      group_(d.local_group),
+      join_comm_(d.join_comm != 0),
       sched_(d.n_stages, std::vector<int>(d.stage_rank, d.stage_rank + d.n_stages), nonrev_counts(d), d.rank,
              accum_ks(d)) {
   if (J_ < 1 || J_ > PETRA_MAX_STAGES) throw PetraError(PETRA_E_ARG, "n_stages out of range");
+  if (world_ < 1 || rank_ < 0 || rank_ >= world_) throw PetraError(PETRA_E_ARG, "rank / world out of range");
+  if (transport_ < PETRA_TRANSPORT_NONE || transport_ > PETRA_TRANSPORT_LOCAL)
+    throw PetraError(PETRA_E_ARG, "unknown transport");
+  if (transport_ == PETRA_TRANSPORT_NCCL && !d.nccl_id) throw PetraError(PETRA_E_ARG, "NCCL transport needs nccl_id");
+  if (transport_ == PETRA_TRANSPORT_LOCAL && group_ == 0) throw PetraError(PETRA_E_ARG, "LOCAL transport needs local_group");
   stages_.resize(J_ + 2);
   fwd_.resize(J_ + 2);
   bwd_.resize(J_ + 2);
@@ -84,6 +114,49 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
       for (int k = 0; k < 4; ++k) ghost_bwd_[p].x[k] = dalloc(out.numel() * sizeof(float));
     }
   }
+  if (lib_transport()) {
+    fdone_.assign(J_ + 2, {nullptr, nullptr});
+    bdone_.assign(J_ + 2, {nullptr, nullptr});
+    tdone_.assign(J_ + 2, {nullptr, nullptr});
+    for (int j = j0; j <= j1; ++j)
+      for (int p = 0; p < 2; ++p) {
+        PETRA_CUDA(cudaEventCreateWithFlags(&fdone_[j][p], cudaEventDisableTiming));
+        PETRA_CUDA(cudaEventCreateWithFlags(&bdone_[j][p], cudaEventDisableTiming));
+        PETRA_CUDA(cudaEventCreateWithFlags(&tdone_[j][p], cudaEventDisableTiming));
+      }
+    for (int dir = 0; dir < 2; ++dir) {
+      PETRA_CUDA(cudaStreamCreateWithFlags(&cs_[dir], cudaStreamNonBlocking));
+      for (int p = 0; p < 2; ++p) PETRA_CUDA(cudaEventCreateWithFlags(&cdone_[dir][p], cudaEventDisableTiming));
+    }
+  }
+  if (transport_ == PETRA_TRANSPORT_NCCL) {
+    ncclUniqueId id;
+    std::memcpy(&id, d.nccl_id, sizeof(id));
+    PETRA_NCCL(nccl().CommInitRank(&nccl_comm_, world_, id, rank_));
+  } else if (transport_ == PETRA_TRANSPORT_LOCAL) {
+    std::lock_guard<std::mutex> lk(g_hub_mu);
+    auto &v = g_hub[group_];
+    if ((int)v.size() < world_) v.resize(world_, nullptr);
+    if (v[rank_]) throw PetraError(PETRA_E_ARG, "LOCAL transport: rank already registered in this group");
+    v[rank_] = this;
+  }
+}
+
+Pipeline *Pipeline::peer(int rank) const {
+  std::lock_guard<std::mutex> lk(g_hub_mu);
+  auto it = g_hub.find(group_);
+  if (it == g_hub.end() || rank >= (int)it->second.size() || !it->second[rank])
+    throw PetraError(PETRA_E_ARG, "LOCAL transport: rank " + std::to_string(rank) + " has no pipeline in the group");
+  return it->second[rank];
+}
+
+// the event that completes when the message of direction `dir` produced at a tick of
+// parity `parity` has arrived in this rank's ghost buffer
+cudaEvent_t Pipeline::recv_done(int dir, int parity) const {
+  if (transport_ == PETRA_TRANSPORT_NCCL) return cdone_[dir][parity];  // this rank's own receive
+  // LOCAL: the sender pushed it on its comm stream
+  const int src = dir == DIR_FWD ? sched_.rank_of(sched_.first_local() - 1) : sched_.rank_of(sched_.last_local() + 1);
+  return peer(src)->cdone_[dir][parity];
 }
 
 cudaEvent_t Pipeline::ev() {
@@ -118,6 +191,28 @@ int Pipeline::stage_ms(float *ms, int n) {
 }
 
 Pipeline::~Pipeline() {
+  if (transport_ == PETRA_TRANSPORT_LOCAL) {
+    std::lock_guard<std::mutex> lk(g_hub_mu);
+    auto it = g_hub.find(group_);
+    if (it != g_hub.end()) {
+      if (rank_ < (int)it->second.size() && it->second[rank_] == this) it->second[rank_] = nullptr;
+      bool empty = true;
+      for (auto *q : it->second) empty &= q == nullptr;
+      if (empty) g_hub.erase(it);
+    }
+  }
+  for (int dir = 0; dir < 2; ++dir)
+    if (cs_[dir]) cudaStreamSynchronize(cs_[dir]);
+  if (nccl_comm_) nccl().CommDestroy(nccl_comm_);
+  for (int dir = 0; dir < 2; ++dir) {
+    if (cs_[dir]) cudaStreamDestroy(cs_[dir]);
+    for (int p = 0; p < 2; ++p)
+      if (cdone_[dir][p]) cudaEventDestroy(cdone_[dir][p]);
+  }
+  for (auto *v : {&fdone_, &bdone_, &tdone_})
+    for (auto &pr : *v)
+      for (cudaEvent_t e : pr)
+        if (e) cudaEventDestroy(e);
   for (auto e : ev_pool_) cudaEventDestroy(e);
   for (auto s : streams_)
     if (s) cudaStreamDestroy(s);
@@ -187,6 +282,19 @@ void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labe
       }
     }
     if (j == J_) a.loss = loss;
+    if (lib_transport()) {  // cross-rank synchronisation points (header comment)
+      const int j0 = sched_.first_local(), j1 = sched_.last_local();
+      if (a.fwd) {
+        if (j == j0 && j > 1) a.wait_f[0] = recv_done(DIR_FWD, q);
+        if (j == j1 && j < J_) a.wait_f[1] = cdone_[DIR_FWD][p];
+        a.done_f = fdone_[j][p];
+      }
+      if (a.bwd) {
+        if (j == j1 && j < J_) a.wait_b[0] = recv_done(DIR_BWD, q);
+        if (j == j0 && j > 1) a.wait_b[1] = cdone_[DIR_BWD][p];
+        a.done_b = bdone_[j][p];
+      }
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timing_) {
       e0 = ev();
@@ -199,10 +307,16 @@ void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labe
       tev_[j].push_back({e0, e1});
     }
     PETRA_CUDA(cudaEventRecord(done_[j], st));
+    if (lib_transport()) PETRA_CUDA(cudaEventRecord(tdone_[j][p], st));
   }
   if (timing_) ++timed_ticks_;
+  std::vector<bool> used(2, false);
+  if (lib_transport()) exchange(t, used);
   for (int j = 1; j <= J_; ++j)  // join: the caller's stream sees the whole tick
     if (sched_.local(j)) PETRA_CUDA(cudaStreamWaitEvent(caller, done_[j], 0));
+  if (join_comm_)
+    for (int dir = 0; dir < 2; ++dir)
+      if (used[dir]) PETRA_CUDA(cudaStreamWaitEvent(caller, cdone_[dir][p], 0));
   if (rep) {
     rep->tick = t;
     rep->n_stages = J_;
@@ -212,6 +326,61 @@ void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labe
       rep->param_version[j - 1] = ver[j];
       rep->fifo_depth[j - 1] = fifo[j];
     }
+  }
+}
+
+void Pipeline::exchange(int64_t t, std::vector<bool> &used) {
+  const int p = (int)(t & 1), q = p ^ 1;
+  const int j0 = sched_.first_local(), j1 = sched_.last_local();
+  std::vector<Schedule::Comm> msgs = sched_.comm(t);
+  for (int dir = 0; dir < 2; ++dir) {
+    std::vector<const Schedule::Comm *> ops;
+    for (const Schedule::Comm &c : msgs)
+      if (c.kind == (dir == DIR_FWD ? Schedule::MSG_FWD : Schedule::MSG_BWD)) ops.push_back(&c);
+    if (ops.empty()) continue;
+    used[dir] = true;
+    cudaStream_t cs = cs_[dir];
+    for (const Schedule::Comm *c : ops) {
+      if (c->send) {  // the message is final when the sending part of the stage is done
+        PETRA_CUDA(cudaStreamWaitEvent(cs, dir == DIR_FWD ? fdone_[j1][p] : bdone_[j0][p], 0));
+      } else {        // this rank's ghost buffer of parity p was last read at tick t-1
+        PETRA_CUDA(cudaStreamWaitEvent(cs, dir == DIR_FWD ? tdone_[j0][q] : tdone_[j1][q], 0));
+      }
+    }
+    ProfScope ps(dir == DIR_FWD ? "exchange_fwd" : "exchange_bwd", cs, 0.0, 0.0);
+    if (transport_ == PETRA_TRANSPORT_NCCL) {
+      const NcclApi &nc = nccl();
+      PETRA_NCCL(nc.GroupStart());
+      for (const Schedule::Comm *c : ops) {
+        Msg &m = dir == DIR_FWD ? (c->send ? fwd_[j1][p] : ghost_fwd_[p]) : (c->send ? bwd_[j0][p] : ghost_bwd_[p]);
+        const int n = dir == DIR_FWD ? 2 : 4;
+        for (int k = 0; k <= n; ++k) {
+          const DevPtr &b = k < n ? m.x[k] : m.labels;
+          if (!b) continue;
+          if (c->send) PETRA_NCCL(nc.Send(b->p, b->bytes, ncclUint8, c->peer, nccl_comm_, cs));
+          else PETRA_NCCL(nc.Recv(b->p, b->bytes, ncclUint8, c->peer, nccl_comm_, cs));
+        }
+      }
+      PETRA_NCCL(nc.GroupEnd());
+    } else {  // LOCAL: push into the receiver's ghost buffer once it released it
+      for (const Schedule::Comm *c : ops) {
+        if (!c->send) continue;
+        Pipeline *pr = peer(c->peer);
+        const int rj = dir == DIR_FWD ? pr->sched_.first_local() : pr->sched_.last_local();
+        PETRA_CUDA(cudaStreamWaitEvent(cs, pr->tdone_[rj][q], 0));
+        Msg &src = dir == DIR_FWD ? fwd_[j1][p] : bwd_[j0][p];
+        Msg &dst = dir == DIR_FWD ? pr->ghost_fwd_[p] : pr->ghost_bwd_[p];
+        const int n = dir == DIR_FWD ? 2 : 4;
+        for (int k = 0; k <= n; ++k) {
+          const DevPtr &a = k < n ? src.x[k] : src.labels;
+          const DevPtr &b = k < n ? dst.x[k] : dst.labels;
+          if (!a || !b) continue;
+          if (a->bytes != b->bytes) throw PetraError(PETRA_E_SHAPE, "LOCAL transport: message sizes differ");
+          PETRA_CUDA(cudaMemcpyAsync(b->p, a->p, a->bytes, cudaMemcpyDeviceToDevice, cs));
+        }
+      }
+    }
+    PETRA_CUDA(cudaEventRecord(cdone_[dir][p], cs));
   }
 }
 

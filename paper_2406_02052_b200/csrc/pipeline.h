@@ -1,8 +1,10 @@
-// pipeline.h -- stages of one rank + mailboxes (product code).
+// pipeline.h -- stages of one rank, mailboxes and the neighbour exchange (product code).
 #pragma once
+#include <array>
 #include <memory>
 #include <vector>
 
+#include "nccl_dl.h"
 #include "schedule.h"
 #include "stage.h"
 
@@ -16,6 +18,7 @@ struct Msg {
 class Pipeline {
  public:
   explicit Pipeline(const petra_pipeline_desc &d);
+  ~Pipeline();
   Stage *stage(int j) { return (j >= 1 && j <= J_) ? stages_[j].get() : nullptr; }
   void tick(int64_t t, bool inject, const float *x0, const int32_t *labels, float lr, float *loss, cudaStream_t st,
             petra_tick_report *rep);
@@ -24,7 +27,11 @@ class Pipeline {
   int stage_ms(float *ms, int n);
 
  private:
-  int J_, rank_;
+  enum { DIR_FWD = 0, DIR_BWD = 1 };
+  int J_, rank_, world_;
+  int transport_ = PETRA_TRANSPORT_NONE;
+  int64_t group_ = 0;
+  bool join_comm_ = true;
   Schedule sched_;
   std::vector<petra_stage_desc> descs_;
   std::vector<std::unique_ptr<Stage>> stages_;
@@ -44,8 +51,19 @@ class Pipeline {
   int timed_ticks_ = 0;
   cudaEvent_t ev();
 
- public:
-  ~Pipeline();
+  // ---- library transports (NCCL, LOCAL)
+  ncclComm_t nccl_comm_ = nullptr;
+  cudaStream_t cs_[2] = {nullptr, nullptr};               // comm stream per direction
+  cudaEvent_t cdone_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [dir][parity]: exchange done
+  // per local stage and parity: forward part done, backward part done, whole tick done
+  std::vector<std::array<cudaEvent_t, 2>> fdone_, bdone_, tdone_;
+  bool lib_transport() const { return transport_ != PETRA_TRANSPORT_NONE; }
+  Pipeline *peer(int rank) const;          // LOCAL: the pipeline of another rank
+  cudaEvent_t recv_done(int dir, int parity) const;
+  void exchange(int64_t t, std::vector<bool> &used);
+
+  Msg &ghost_fwd(int p) { return ghost_fwd_[p]; }
+  Msg &ghost_bwd(int p) { return ghost_bwd_[p]; }
 };
 
 }  // namespace petra

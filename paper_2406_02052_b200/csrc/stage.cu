@@ -1133,10 +1133,24 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
   if (!fwd && !bwd) return;
   if (bwd) upload_lr(lr, st);
   const int mode = bwd ? next_update_mode() : SGD_PLAIN;
+  bool capturing = false;
+  // external synchronisation points (TickArgs::wait_* / done_*): plain event waits and
+  // records when enqueued directly, external event nodes when captured into the graph
+  auto wait_on = [&](cudaStream_t s, const cudaEvent_t (&evs)[2]) {
+    for (cudaEvent_t e : evs)
+      if (e) PETRA_CUDA(cudaStreamWaitEvent(s, e, capturing ? cudaEventWaitExternal : cudaEventWaitDefault));
+  };
+  auto record = [&](cudaEvent_t e, cudaStream_t s) {
+    if (e) PETRA_CUDA(cudaEventRecordWithFlags(e, s, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+  };
   auto enqueue = [&](cudaStream_t s) {
     if (is_last_) {
       ctx_ = 0;
+      wait_on(s, a.wait_f);
+      wait_on(s, a.wait_b);
       enqueue_tail(a.x1, a.x2, a.labels, a.oxt[0], a.oxt[1], a.od[0], a.od[1], a.loss, push, pop, s);
+      record(a.done_f, s);
+      record(a.done_b, s);
     } else if (fwd && bwd && !Prof::enabled) {
       // forward (theta^t, context 0) and backward (context 1) of different micro-batches
       // are independent until the update: run them on two streams, join, then update
@@ -1144,24 +1158,29 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
       PETRA_CUDA(cudaEventRecord(fork_, s));
       PETRA_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
       ctx_ = 0;
+      wait_on(s, a.wait_f);
       enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
+      record(a.done_f, s);
       ctx_ = 1;
+      wait_on(side_, a.wait_b);
       enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, side_);
+      record(a.done_b, side_);
       PETRA_CUDA(cudaEventRecord(join_, side_));
       PETRA_CUDA(cudaStreamWaitEvent(s, join_, 0));
       ctx_ = 0;
-    } else if (fwd && bwd) {
-      ctx_ = 0;
-      enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
-      ctx_ = 1;
-      enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, s);
-      ctx_ = 0;
-    } else if (fwd) {
-      ctx_ = 0;
-      enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
     } else {
-      ctx_ = 1;
-      enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, s);
+      if (fwd) {
+        ctx_ = 0;
+        wait_on(s, a.wait_f);
+        enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
+        record(a.done_f, s);
+      }
+      if (bwd) {
+        ctx_ = 1;
+        wait_on(s, a.wait_b);
+        enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, s);
+        record(a.done_b, s);
+      }
       ctx_ = 0;
     }
     if (bwd) enqueue_update(mode, s);
@@ -1173,7 +1192,9 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
     for (const void *p : {(const void *)a.x1, (const void *)a.x2, (const void *)a.labels, (const void *)a.o[0],
                           (const void *)a.o[1], (const void *)a.xt[0], (const void *)a.xt[1], (const void *)a.d[0],
                           (const void *)a.d[1], (const void *)a.oxt[0], (const void *)a.oxt[1],
-                          (const void *)a.od[0], (const void *)a.od[1], (const void *)a.loss})
+                          (const void *)a.od[0], (const void *)a.od[1], (const void *)a.loss,
+                          (const void *)a.wait_f[0], (const void *)a.wait_f[1], (const void *)a.wait_b[0],
+                          (const void *)a.wait_b[1], (const void *)a.done_f, (const void *)a.done_b})
       key.push_back((uintptr_t)p);
     for (int v : push) key.push_back((uintptr_t)(v + 1));
     for (int v : pop) key.push_back((uintptr_t)(v + 1));
@@ -1182,9 +1203,12 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
       const int64_t n0 = Prof::launches.load();
       cudaGraph_t g = nullptr;
       PETRA_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+      capturing = true;
       try {
         enqueue(st);
+        capturing = false;
       } catch (...) {
+        capturing = false;
         cudaStreamEndCapture(st, &g);
         if (g) cudaGraphDestroy(g);
         throw;

@@ -111,6 +111,12 @@ struct TickArgs {
   float *oxt[2] = {nullptr, nullptr};        // backward output x~_{j-1}
   float *od[2] = {nullptr, nullptr};         // backward output delta_j
   float *loss = nullptr;                     // tail only
+  // cross-rank synchronisation set by the pipeline's transport: the forward (backward)
+  // part waits on wait_f (wait_b) -- a received message, a send buffer released -- and
+  // records done_f (done_b) when its messages are final.  Inside the stage's CUDA graph
+  // they are external event nodes (cudaEventWaitExternal / cudaEventRecordExternal).
+  cudaEvent_t wait_f[2] = {nullptr, nullptr}, wait_b[2] = {nullptr, nullptr};
+  cudaEvent_t done_f = nullptr, done_b = nullptr;
 };
 
 struct CachedGraph {

@@ -112,14 +112,21 @@ def report_dict(rep: L.PetraTickReport):
 class Pipeline:
     """petra_pipeline_* : the stages of this rank with double-buffered mailboxes."""
 
-    def __init__(self, specs, stage_rank=None, rank=0, world=1, seed=0):
+    def __init__(self, specs, stage_rank=None, rank=0, world=1, seed=0, transport="none", nccl_id=None,
+                 local_group=0, join_comm=True):
+        """transport: "none" (world 1, or the caller moves petra_pipeline_comm's bytes),
+        "nccl" (the library's ncclSend/ncclRecv; nccl_id = nccl_unique_id() of rank 0),
+        "local" (ranks = pipelines of this process sharing local_group; a test transport)."""
         J = len(specs)
         self.J = J
         self._keep = [s.to_c() for s in specs]
         descs = (L.PetraStageDesc * J)(*[d for d, _ in self._keep])
         sr = (C.c_int32 * J)(*(stage_rank or [0] * J))
+        tr = {"none": L.TRANSPORT_NONE, "nccl": L.TRANSPORT_NCCL, "local": L.TRANSPORT_LOCAL}[transport]
+        self._nid = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         pd = L.PetraPipelineDesc(J, C.cast(descs, C.POINTER(L.PetraStageDesc)), C.cast(sr, C.POINTER(C.c_int32)),
-                                 rank, world, seed)
+                                 rank, world, seed, tr, C.cast(self._nid, C.c_void_p) if self._nid else None,
+                                 int(local_group), int(bool(join_comm)))
         self._descs, self._sr = descs, sr
         h = C.c_void_p()
         L.call("petra_pipeline_create", C.byref(pd), C.byref(h))
@@ -163,6 +170,13 @@ class Pipeline:
         plan = L.PetraCommPlan()
         L.call("petra_pipeline_comm", self.h, t, C.byref(plan))
         return [(plan.e[i].peer, plan.e[i].send, plan.e[i].ptr, plan.e[i].bytes) for i in range(plan.n)]
+
+
+def nccl_unique_id() -> bytes:
+    """petra_nccl_unique_id: 128 bytes for PETRA_TRANSPORT_NCCL (create on rank 0, share)."""
+    buf = C.create_string_buffer(128)
+    L.call("petra_nccl_unique_id", buf)
+    return buf.raw
 
 
 class Schedule:
