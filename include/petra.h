@@ -370,6 +370,18 @@ petra_status petra_conv_run(int32_t mode, int32_t engine, const petra_conv_geom 
  * bit 1: forward with the BN statistics fused into the epilogue (as a stage runs it). */
 petra_status petra_conv_bench(int32_t mode, int32_t engine, const petra_conv_geom *g, int32_t flags,
                               int32_t iters, float *avg_ms);
+/* Kernel-level test hook of the fused BN statistics: one tensor-core
+ * forward convolution with z stored in bf16 and the batch statistics fused into its
+ * epilogue, exactly as a stage runs it (engine 1: plain operand, the stem's gathered
+ * im2col for Ci <= 4; engine 2: zero-bordered operand, the halo kernel where eligible),
+ * then the library's merge.  Each CTA keeps per column the shifted sums of its valid rows
+ * (shift = the mean of its first tile) and writes (count, mean, M2); the merge combines
+ * them over CTAs with Chan's pairwise update in fp64 in a fixed order.  Outputs (host):
+ * z[B*Ho*Wo][Co] (the stored bf16 values as fp32), mean[Co] and the biased variance
+ * var[Co] the library normalises with.  Synchronous.  Errors: PETRA_E_ARG,
+ * PETRA_E_UNSUPPORTED (no tensor-core path / no fused statistics), PETRA_E_CUDA. */
+petra_status petra_conv_bn_stats(const petra_conv_geom *g, int32_t engine, const float *x, const float *w,
+                                 float *z, float *mean, float *var);
 /* Which engine the library uses for a convolution pass at a given precision:
  * 0 = SIMT fp32, 1 = tcgen05 bf16 (operands rounded to bf16, fp32 accumulation) --
  * the TMA implicit GEMM for Ci, Co multiples of 64, or, for few input channels (the

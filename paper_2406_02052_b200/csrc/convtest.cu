@@ -1,6 +1,7 @@
 // convtest.cu -- petra_conv_run: one convolution pass on host buffers (kernel-level tests).
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <functional>
 #include <vector>
 
@@ -14,7 +15,7 @@ namespace {
 // `iters` further passes (CUDA events; operands prepared once, outside the timing)
 petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a, const float *b,
                  const float *addend, float *out, int iters = 0, float *ms = nullptr, bool out16 = false,
-                 bool stats = false) {
+                 bool stats = false, float *mean_out = nullptr, float *var_out = nullptr) {
   using namespace petra;
   ConvGeom g = make_geom(pg->batch, pg->h, pg->w, pg->cin, pg->cout, pg->ksize, pg->stride);
   int64_t nx = g.Min() * g.Ci, nz = g.M() * g.Co, nw = (int64_t)g.Co * g.K();
@@ -32,7 +33,8 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     PETRA_CUDA(cudaMemcpy(dadd->p, addend, no * 4, cudaMemcpyHostToDevice));
   }
   cudaStream_t st = nullptr;
-  DevPtr ab, bb, ws, part = dalloc((size_t)kNumSMs * 4 * g.Co * 2 * sizeof(float));
+  DevPtr ab, bb, ws, part = dalloc((size_t)kNumSMs * 4 * (g.Co * 2 + 1) * sizeof(float));
+  StatsRows rows;
   float *stats_part = stats ? part->as<float>() : nullptr;
   const bool a_pad = padded, b_pad = padded && mode == 2;
   std::function<void()> launch;
@@ -42,7 +44,7 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
       ab = dalloc(stem_operand_elems(g) * 2);
       launch = [&] {
         image_to_bf16x4(da->as<float>(), ab->as<__nv_bfloat16>(), g, st);
-        stem_fwd_tc(g, ab->as<__nv_bfloat16>(), db->as<float>(), dout->p, out16, stats_part, st);
+        rows = stem_fwd_tc(g, ab->as<__nv_bfloat16>(), db->as<float>(), dout->p, out16, stats_part, st);
       };
     } else {
       ab = dalloc(na * 2);
@@ -89,8 +91,8 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     ws = dalloc(std::max<size_t>(16, conv_tc_workspace(g, mode)));
     launch = [&] {
       if (mode == 0)
-        conv_fwd_tc(g, ab->as<__nv_bfloat16>(), a_pad, bb->as<__nv_bfloat16>(), dout->p, out16, ws->as<float>(),
-                    stats_part, st);
+        rows = conv_fwd_tc(g, ab->as<__nv_bfloat16>(), a_pad, bb->as<__nv_bfloat16>(), dout->p, out16,
+                           ws->as<float>(), stats_part, st);
       else if (mode == 1)
         conv_dgrad_tc(g, ab->as<__nv_bfloat16>(), a_pad, bb->as<__nv_bfloat16>(),
                       addend ? dadd->as<float>() : nullptr, dout->as<float>(), ws->as<float>(), st);
@@ -115,7 +117,26 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
-  if (out) PETRA_CUDA(cudaMemcpy(out, dout->p, no * 4, cudaMemcpyDeviceToHost));
+  if (mean_out && var_out) {  // the library's BN batch statistics of z as stored (eps = 0: invstd^-2 = var)
+    if (rows.rows == 0) throw PetraError(PETRA_E_UNSUPPORTED, "no fused statistics for this geometry");
+    DevPtr dm = dalloc(g.Co * 4), di = dalloc(g.Co * 4);
+    bn_stats_from_partials(part->as<float>(), rows, g.Co, g.M(), 0.f, dm->as<float>(), di->as<float>(), nullptr,
+                           nullptr, 0.1f, st);
+    std::vector<float> inv(g.Co);
+    PETRA_CUDA(cudaMemcpy(mean_out, dm->p, g.Co * 4, cudaMemcpyDeviceToHost));
+    PETRA_CUDA(cudaMemcpy(inv.data(), di->p, g.Co * 4, cudaMemcpyDeviceToHost));
+    for (int c = 0; c < g.Co; ++c) var_out[c] = 1.f / (inv[c] * inv[c]);
+  }
+  if (out && out16) {  // bf16 z -> fp32
+    std::vector<uint16_t> h(no);
+    PETRA_CUDA(cudaMemcpy(h.data(), dout->p, no * 2, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < no; ++i) {
+      const uint32_t u = (uint32_t)h[i] << 16;
+      std::memcpy(out + i, &u, 4);
+    }
+  } else if (out) {
+    PETRA_CUDA(cudaMemcpy(out, dout->p, no * 4, cudaMemcpyDeviceToHost));
+  }
   return PETRA_OK;
 }
 }  // namespace
@@ -125,6 +146,19 @@ extern "C" petra_status petra_conv_run(int32_t mode, int32_t engine, const petra
   if (!g || !a || !b || !out || mode < 0 || mode > 2 || engine < 0 || engine > 2) return PETRA_E_ARG;
   try {
     return run(mode, engine, g, a, b, addend, out);
+  } catch (const petra::PetraError &e) {
+    return e.status;
+  } catch (...) {
+    cudaGetLastError();
+    return PETRA_E_CUDA;
+  }
+}
+
+extern "C" petra_status petra_conv_bn_stats(const petra_conv_geom *g, int32_t engine, const float *x,
+                                            const float *w, float *z, float *mean, float *var) {
+  if (!g || !x || !w || !z || !mean || !var || engine < 1 || engine > 2) return PETRA_E_ARG;
+  try {
+    return run(0, engine, g, x, w, nullptr, z, 0, nullptr, true, true, mean, var);
   } catch (const petra::PetraError &e) {
     return e.status;
   } catch (...) {

@@ -22,26 +22,18 @@ void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *
 bool conv_tc_supported(const ConvGeom &g, int mode);   // mode 0 fwd, 1 dgrad, 2 wgrad
 void conv_tc_prepare();  // one-time kernel attributes (before any graph capture)
 size_t conv_tc_workspace(const ConvGeom &g, int mode);  // split-K workspace bytes
-// BN partial sums written by a conv epilogue: `rows` rows [rows][Co][2] (sum, sum of
-// squares), one per CTA; with `groups` > 1 the CTAs each own one of `groups` column
-// groups of Co/groups channels (CTA r: group r % groups) and write only those columns.
-// rows == 0: not fused (run bn_stats on z).
+// BN partial statistics written by a conv epilogue: `rows` rows [rows][Co][2] of
+// (mean, M2) over the CTA's valid output rows, one row per CTA, followed by the rows'
+// counts (float[rows] at part + rows * Co * 2); with `groups` > 1 the CTAs each own one
+// of `groups` column groups of Co/groups channels (CTA r: group r % groups) and write
+// only those columns.  rows == 0: not fused (run bn_stats on z).
 struct StatsRows {
   int rows = 0, groups = 1;
-  bool finalized = false;  // mean / invstd (+ running stats) already written by the conv kernel
-};
-// BN finalize done inside a conv kernel by the last CTA of each N-tile group
-struct BnFinalize {
-  float *mean = nullptr, *invstd = nullptr;  // mean == nullptr: leave it to bn_stats_from_partials
-  float *rmean = nullptr, *rvar = nullptr;   // nullable: running-statistics EMA (recomputation only)
-  unsigned *ticket = nullptr;                // >= groups counters, zero between launches
-  float eps = 1e-5f, mom = 0.1f;
-  int64_t count = 0;                         // rows of z
 };
 // z[m][co] = conv(x_bf16, w_bf16), stored fp32 or (z_bf16) bf16.  stats_part (nullable,
-// >= 148*Co*2 floats): the epilogue also writes BN partial sums of z as stored.
+// >= 148*(Co*2+1) floats): the epilogue also writes BN partial statistics of z as stored.
 StatsRows conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,
-                bool z_bf16, float *ws, float *stats_part, cudaStream_t st, const BnFinalize *fin = nullptr);
+                bool z_bf16, float *ws, float *stats_part, cudaStream_t st);
 void bn_stats_from_partials(const float *part, StatsRows rows, int N, int64_t M, float eps, float *mean,
                             float *invstd, float *rmean, float *rvar, float mom, cudaStream_t st);
 // dx (fp32) = addend + conv^T(dz_bf16, wT_bf16)
@@ -55,7 +47,7 @@ void conv_halo_prepare();
 bool conv_halo_eligible(int B, int H, int W, int Cred, int N);
 StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad,
                         const __nv_bfloat16 *wmat, const float *addend, void *out, bool out16, float *stats,
-                        cudaStream_t st, const BnFinalize *fin = nullptr);
+                        cudaStream_t st);
 
 // wgrad of a 3x3 stride-1 layer on zero-bordered operands: one x-halo load per pixel block
 // serves all nine taps (conv_halo.cu)

@@ -47,8 +47,7 @@ struct HaloParams {
   int resident;            // 1: the whole weight matrix of the (single) N tile stays in smem
   const float *addend;     // nullable, fp32 output only
   void *out;               // [B][H][W][N] fp32 or bf16
-  float *stats;            // nullable: one BN partial row per CTA [grid][N][2]
-  tc::StatsFinalize fin;   // fin.mean != null: the last CTA of each N-tile group finalizes
+  float *stats;            // nullable: one BN partial row per CTA [grid][N][2] (mean, M2) + float[grid] counts
   tc::FastDiv f_ghw, f_wp, f_nn;  // Hp * Wp, Wp, N / BN (set by launch)
 };
 
@@ -75,7 +74,8 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
   uint8_t *sepi = reinterpret_cast<uint8_t *>(afull) + 512;       // [8 warps][32 rows x 144 B]
-  float *sstat = reinterpret_cast<float *>(sepi + kEpiWarps * kEpiWarp);  // [4 lane quarters][BN][2]
+  float *sstat = reinterpret_cast<float *>(sepi + kEpiWarps * kEpiWarp);  // [4 lane quarters][BN][2] (mean, M2)
+  int *scnt = reinterpret_cast<int *>(sstat + 8 * BN);                     // [4 lane quarters] valid rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_nt = P.N / BN;
@@ -187,18 +187,14 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int row = q * 32 + lane;
     float *my_stat = sstat + (size_t)q * BN * 2;  // this CTA's N tile (fixed: grid % n_nt == 0)
     uint8_t *ebuf = sepi + (warp - 2) * kEpiWarp;
-    if (P.stats) {  // the two warps of a lane quarter share its (column-disjoint) sums
-      for (int i = (warp - 2) * 32 + lane; i < 8 * BN; i += kEpiWarps * 32) sstat[i] = 0.f;
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-    }
     constexpr int ES = OUT16 ? 2 : 4;
     constexpr int CW = 128 / ES;  // columns per 128-byte chunk
-    // per-lane sums of this warp's columns in registers (same additions, same order as a
-    // running smem sum)
+    // per-lane shifted statistics of this warp's columns in registers (tc::ColStats)
     constexpr int NCH = (BN + 2 * CW - 1) / (2 * CW);
-    float rs[NCH][2], rq[NCH][2];
+    tc::ColStats cst[NCH];
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) rs[k][0] = rs[k][1] = rq[k][0] = rq[k][1] = 0.f;
+    for (int k = 0; k < NCH; ++k) tc::colstats_zero(cst[k]);
+    int nrows = 0;  // valid rows of this warp's tiles so far (warp-uniform)
     int it = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
       const int mg = tc::fdiv(w, f_nn), nt = w - mg * n_nt;
@@ -213,6 +209,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const bool valid = b < P.B && hp >= 1 && hp <= P.H && wp >= 1 && wp <= P.W;
         const int64_t opix = valid ? ((int64_t)b * P.H + hp - 1) * P.W + wp - 1 : -1;
         const float *arow = (valid && P.addend) ? P.addend + opix * P.N + nt * BN : nullptr;
+        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
           const int c = CW * hc + 2 * CW * k;
@@ -265,42 +262,36 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               *reinterpret_cast<uint4 *>(dst) = u;
             }
           }
-          if (P.stats) {  // statistics of z as stored (reading c24), from the staged rows
-            float s[2], sq[2];
-            tc::staged_colsums<OUT16, false>(ebuf, kRowPitch, lane, s, sq);
-            rs[k][0] += s[0];
-            rq[k][0] += sq[0];
-            rs[k][1] += s[1];
-            rq[k][1] += sq[1];
-          }
+          if (P.stats)  // statistics of z as stored (reading c24), from the staged rows
+            tc::colstats_tile<OUT16, false>(ebuf, kRowPitch, lane, vmask, nrows, cst[k]);
           __syncwarp();
         }
+        nrows += __popc(vmask);
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
-    if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
+    if (P.stats) {  // this CTA's partial row: the 4 lane quarters merged (Chan) in a fixed order
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
         const int c = CW * hc + 2 * CW * k;
         if (c >= BN) break;
         const int col = c + (OUT16 ? 2 * lane : lane);  // column within the N tile
-        my_stat[2 * col] = rs[k][0];
-        my_stat[2 * col + 1] = rq[k][0];
+        const float2 a = tc::colstats_final(cst[k], 0, nrows);
+        my_stat[2 * col] = a.x;
+        my_stat[2 * col + 1] = a.y;
         if (OUT16) {
-          my_stat[2 * col + 2] = rs[k][1];
-          my_stat[2 * col + 3] = rq[k][1];
+          const float2 b = tc::colstats_final(cst[k], 1, nrows);
+          my_stat[2 * col + 2] = b.x;
+          my_stat[2 * col + 3] = b.y;
         }
       }
+      if (hc == 0 && lane == 0) scnt[q] = nrows;
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      float *g = P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_nt) * BN) * 2;
-      for (int i = (warp - 2) * 32 + lane; i < 2 * BN; i += kEpiWarps * 32)
-        g[i] = (sstat[i] + sstat[2 * BN + i]) + (sstat[4 * BN + i] + sstat[6 * BN + i]);
-      if (P.fin.mean) {  // last CTA of the group: mean / invstd (+ running stats) in-kernel
-        tc::finalize_group<kEpiWarps * 32, 1>(P.fin, P.stats, P.N, BN, n_nt, blockIdx.x % n_nt, (warp - 2) * 32 + lane,
-                                              reinterpret_cast<double *>(sepi), tmem_slot + 1);
-      }
+      tc::cta_stats_row(sstat, scnt, BN, (warp - 2) * 32 + lane, kEpiWarps * 32,
+                        P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_nt) * BN) * 2,
+                        P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
     }
   }
   __syncthreads();
@@ -310,7 +301,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 }
 
-size_t fixed_smem() { return 1024 + 512 + kEpiWarps * kEpiWarp + (size_t)256 * 32; }  // stats: BN <= 256
+size_t fixed_smem() { return 1024 + 512 + kEpiWarps * kEpiWarp + (size_t)256 * 32 + 16; }  // stats: BN <= 256
 // the halo of T tiles (128*T + 2*(W+3) rows) as equal TMA boxes of <= 256 rows, each a
 // multiple of 8 rows so every box starts 1 KB-aligned
 void halo_rows(int T, int W, int &box_rows, int &HR) {
@@ -665,7 +656,7 @@ bool conv_halo_eligible(int B, int H, int W, int Cred, int N) { return halo_plan
 // (forward: x and w; stride-1 dgrad: dz and the flipped/transposed wT, same tap order).
 StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat16 *a_pad,
                         const __nv_bfloat16 *wmat, const float *addend, void *out, bool out16, float *stats,
-                        cudaStream_t st, const BnFinalize *fin) {
+                        cudaStream_t st) {
   const HaloPlan pl = halo_plan(B, H, W, Cred, N);
   if (!pl.ok) throw PetraError(PETRA_E_UNSUPPORTED, "conv_halo_run: geometry");
   if (out16 && addend) throw PetraError(PETRA_E_ARG, "conv_halo_run: addend needs an fp32 output");
@@ -693,10 +684,6 @@ StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat1
   P.addend = addend;
   P.out = out;
   P.stats = stats;
-  if (stats && fin && fin->mean) {
-    P.fin = *fin;
-    P.fin.count = (int64_t)B * H * W;
-  }
   cuuint64_t adims[2] = {(cuuint64_t)Cred, (cuuint64_t)P.Mp};
   cuuint64_t ast[1] = {(cuuint64_t)Cred * 2};
   cuuint32_t abox[2] = {64, (cuuint32_t)P.box_rows};
@@ -710,7 +697,6 @@ StatsRows conv_halo_run(int B, int H, int W, int Cred, int N, const __nv_bfloat1
   StatsRows r;
   r.groups = N / pl.BN;
   r.rows = halo_grid(work, r.groups);
-  r.finalized = P.fin.mean != nullptr;
   return r;
 }
 

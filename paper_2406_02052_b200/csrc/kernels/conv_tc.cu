@@ -54,8 +54,8 @@ struct ConvTCParams {
   float *ws;
   const float *addend;       // nullable (fp32 output only): out = addend + conv
   void *out;                 // [B*OH*OW][N], fp32 or bf16 (OUT16); written by TMA stores through tmO
-  float *stats;              // nullable: per-(CTA, epilogue warp) BN partials [grid][4][N][2] (sum, sum sq)
-  tc::StatsFinalize fin;     // fin.mean != null: the last CTA of each N-tile group finalizes
+  float *stats;              // nullable: BN partials, one row per CTA: [grid][N][2] (mean, M2) of the CTA's
+                             // N tile columns, then float[grid] row counts (kernels.h StatsRows)
   tc::FastDiv f_sp, f_nt, f_ghw, f_wb;  // splits, N / BN, Hb * Wb, Wb (set by launch_conv)
 };
 
@@ -106,7 +106,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
   uint64_t *abar = reinterpret_cast<uint64_t *>(tmem_slot + 2);  // per epilogue warp: addend box loads
   uint8_t *sepi = smem + STAGES * STAGE_BYTES + 1024;      // [8 warps][2][32 x 128 B] epilogue staging
-  float *sstat = reinterpret_cast<float *>(sepi + kEpiBytes);  // [4 lane quarters][BN][2] BN partial sums
+  float *sstat = reinterpret_cast<float *>(sepi + kEpiBytes);  // [4 lane quarters][BN][2] (mean, M2)
+  int *scnt = reinterpret_cast<int *>(sstat + 8 * BN);           // [4 lane quarters] valid rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_n = P.N / BN;
@@ -201,10 +202,6 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     float *my_stat = sstat + (size_t)q * BN * 2;  // this CTA's N tile (fixed: grid % n_tiles_n == 0)
     uint8_t *ebuf = sepi + (warp - 2) * 2 * kEpiBuf;
     int eb = 0;  // staging buffer to fill next
-    if (P.stats) {  // the two warps of a lane quarter share its (column-disjoint) sums
-      for (int i = (warp - 2) * 32 + lane; i < 8 * BN; i += kEpiWarps * 32) sstat[i] = 0.f;
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-    }
     if (lane == 0) {
       tc::tma_prefetch(&tmO);
       tc::tma_prefetch(&tmW);
@@ -225,13 +222,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if (lane == 0) tc::bulk_wait_read<1>();
       __syncwarp();
     };
-    // per-lane sums of this warp's columns (the CTA's N tile is fixed), tile after tile
-    // in registers -- the same additions, in the same order, as a running smem sum
+    // per-lane shifted statistics of this warp's columns (the CTA's N tile is fixed),
+    // tile after tile in registers (tc::ColStats)
     constexpr int CW = OUT16 ? 64 : 32;  // columns per 128-byte staged row
     constexpr int NCH = (BN + 2 * CW - 1) / (2 * CW);  // column chunks per warp per tile
-    float rs[NCH][2], rq[NCH][2];
+    tc::ColStats cst[NCH];
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) rs[k][0] = rs[k][1] = rq[k][0] = rq[k][1] = 0.f;
+    for (int k = 0; k < NCH; ++k) tc::colstats_zero(cst[k]);
+    int nrows = 0;  // valid rows of this warp's tiles so far (warp-uniform)
     uint32_t aph = 0;  // phase of this warp's addend barrier
     int it = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
@@ -258,6 +256,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // TMA box origin of this warp's 32 rows in the (N, Gw, Gh, B) output view
         const int m0w = mt * BM + q * 32;
         const int wb = tc::fdiv(m0w, f_ghw), wr = m0w - wb * GHW, wi = tc::fdiv(wr, f_wb), wj = wr - wi * P.Wb;
+        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
           const int c = CW * hc + 2 * CW * k;
@@ -292,43 +291,36 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           uint8_t *staged = ebuf + eb * kEpiBuf;
           stage_row<OUT16>(staged, lane, v);
           flush(&tmO, nt * BN + c, wj, wi, wb, true);
-          if (P.stats) {  // BN batch statistics of z as stored (reading c24), from the staged rows
-            float s[2], sq[2];
-            tc::staged_colsums<OUT16, true>(staged, 128, lane, s, sq);
-            rs[k][0] += s[0];
-            rq[k][0] += sq[0];
-            rs[k][1] += s[1];
-            rq[k][1] += sq[1];
-          }
+          if (P.stats)  // BN batch statistics of z as stored (reading c24), from the staged rows
+            tc::colstats_tile<OUT16, true>(staged, 128, lane, vmask, nrows, cst[k]);
         }
+        nrows += __popc(vmask);
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
     if (lane == 0) tc::bulk_wait_all();
-    if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
+    if (P.stats) {  // this CTA's partial row: the 4 lane quarters merged (Chan) in a fixed order
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
         const int c = CW * hc + 2 * CW * k;
         if (c >= BN) break;
         const int col = c + (OUT16 ? 2 * lane : lane);  // column within the N tile
-        my_stat[2 * col] = rs[k][0];
-        my_stat[2 * col + 1] = rq[k][0];
+        const float2 a = tc::colstats_final(cst[k], 0, nrows);
+        my_stat[2 * col] = a.x;
+        my_stat[2 * col + 1] = a.y;
         if (OUT16) {
-          my_stat[2 * col + 2] = rs[k][1];
-          my_stat[2 * col + 3] = rq[k][1];
+          const float2 b = tc::colstats_final(cst[k], 1, nrows);
+          my_stat[2 * col + 2] = b.x;
+          my_stat[2 * col + 3] = b.y;
         }
       }
+      if (hc == 0 && lane == 0) scnt[q] = nrows;
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      float *g = P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2;
-      for (int i = (warp - 2) * 32 + lane; i < 2 * BN; i += kEpiWarps * 32)
-        g[i] = (sstat[i] + sstat[2 * BN + i]) + (sstat[4 * BN + i] + sstat[6 * BN + i]);
-      if (P.fin.mean) {  // last CTA of the group: mean / invstd (+ running stats) in-kernel
-        tc::finalize_group<kEpiWarps * 32, 1>(P.fin, P.stats, P.N, BN, n_tiles_n, blockIdx.x % n_tiles_n,
-                                              (warp - 2) * 32 + lane, reinterpret_cast<double *>(sepi),
-                                              tmem_slot + 1);  // flag word next to the TMEM address
-      }
+      tc::cta_stats_row(sstat, scnt, BN, (warp - 2) * 32 + lane, kEpiWarps * 32,
+                        P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2,
+                        P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
     }
   }
   __syncthreads();
@@ -338,50 +330,59 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
 }
 
-// BN statistics from the fused partials part[P][N][2] (one row per conv CTA): a
-// block of 32 warps per 32 channels, warp w sums rows w, w+32, ... in fp64 (lane =
-// channel, coalesced), then warp 0 combines the 32 warp sums in a fixed order;
-// optional running-stat EMA (reading c9).
-__global__ void __launch_bounds__(1024) stats_finalize_kernel(const float *__restrict__ part, int P, int groups, int N,
-                                                              int64_t M, float eps, float *__restrict__ mean,
-                                                              float *__restrict__ invstd, float *__restrict__ rmean,
-                                                              float *__restrict__ rvar, float mom) {
+// BN statistics from the fused partials part[P][N][2] = (mean, M2) per conv CTA and the
+// rows' counts cnt[P] (at part + P * N * 2).  A block of 8 warps per 32 channels (lane =
+// channel, coalesced); warp w takes rows w, w + 8, ... and accumulates in fp64, shifted by
+// the group's first row mean m0:  A = sum n_r (m_r - m0),  B = sum n_r (m_r - m0)^2,
+// W = sum M2_r, n = sum n_r  (the pairwise / Chan combination of (count, mean, M2)
+// triples written as sums: M2 = W + B - A^2 / n); the 8 warp results are added in warp
+// order (deterministic).  Biased variance for the normalisation, unbiased for the
+// running-stat EMA (reading c9).
+__global__ void __launch_bounds__(256) stats_finalize_kernel(const float *__restrict__ part, int P, int groups, int N,
+                                                             int64_t M, float eps, float *__restrict__ mean,
+                                                             float *__restrict__ invstd, float *__restrict__ rmean,
+                                                             float *__restrict__ rvar, float mom) {
   pdl_wait_trigger();
-  __shared__ double sh[2][32][33];
+  __shared__ double sh[4][8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
-  double a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+  const float *cnt = part + (size_t)P * N * 2;
+  double A = 0, Bq = 0, Wm = 0, n = 0, m0 = 0;
   if (c < N) {
-    // rows of this column's group: r = grp, grp + groups, ... (n rows); warp w takes j = w, w + 32, ...
-    const int grp = c / (N / groups), n = (P - grp + groups - 1) / groups;
-    int j = w;
-    for (; j + 32 < n; j += 64) {
-      const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)(grp + j * groups) * N + c) * 2);
-      const float2 v = *reinterpret_cast<const float2 *>(part + ((size_t)(grp + (j + 32) * groups) * N + c) * 2);
-      a0 += u.x; b0 += u.y;
-      a1 += v.x; b1 += v.y;
-    }
-    if (j < n) {
-      const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)(grp + j * groups) * N + c) * 2);
-      a0 += u.x; b0 += u.y;
+    // rows of this column's group: r = grp, grp + groups, ... (nr rows)
+    const int grp = c / (N / groups), nr = (P - grp + groups - 1) / groups;
+    m0 = part[((size_t)grp * N + c) * 2];
+    for (int j = w; j < nr; j += 8) {
+      const int r = grp + j * groups;
+      const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)r * N + c) * 2);
+      const double nr_ = cnt[r], d = (double)u.x - m0;
+      A += nr_ * d;
+      Bq += nr_ * d * d;
+      Wm += u.y;
+      n += nr_;
     }
   }
-  sh[0][w][lane] = a0 + a1;
-  sh[1][w][lane] = b0 + b1;
+  sh[0][w][lane] = A;
+  sh[1][w][lane] = Bq;
+  sh[2][w][lane] = Wm;
+  sh[3][w][lane] = n;
   __syncthreads();
   if (w == 0 && c < N) {
-    double s = 0, ss = 0;
-    for (int k = 0; k < 32; ++k) {
-      s += sh[0][k][lane];
-      ss += sh[1][k][lane];
+    A = Bq = Wm = n = 0;
+    for (int k = 0; k < 8; ++k) {
+      A += sh[0][k][lane];
+      Bq += sh[1][k][lane];
+      Wm += sh[2][k][lane];
+      n += sh[3][k][lane];
     }
-    double mu = s / (double)M;
-    double var = ss / (double)M - mu * mu;
-    if (var < 0.0) var = 0.0;
+    const double mu = n > 0 ? m0 + A / n : 0.0;
+    double M2 = n > 0 ? Wm + Bq - A * A / n : 0.0;
+    if (M2 < 0.0) M2 = 0.0;
+    const double var = M > 0 ? M2 / (double)M : 0.0;  // n == M: every valid output row once
     mean[c] = (float)mu;
     invstd[c] = (float)(1.0 / sqrt(var + (double)eps));
     if (rmean) {
-      double unb = M > 1 ? var * (double)M / (double)(M - 1) : var;
+      const double unb = M > 1 ? M2 / (double)(M - 1) : var;
       rmean[c] = (float)((1.0 - mom) * rmean[c] + mom * mu);
       rvar[c] = (float)((1.0 - mom) * rvar[c] + mom * unb);
     }
@@ -778,7 +779,7 @@ void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParam
   P.f_ghw = tc::fastdiv_make(P.Hb * P.Wb);
   P.f_wb = tc::fastdiv_make(P.Wb);
   constexpr int STAGES = conv_stages(BN);
-  const size_t smem = conv_smem(BN, P.stats ? (size_t)BN * 32 : 0);  // attribute: conv_tc_prepare
+  const size_t smem = conv_smem(BN, P.stats ? (size_t)BN * 32 + 16 : 0);  // attribute: conv_tc_prepare
   const int work = (P.M / BM) * (P.N / BN) * P.splits;
   const int grid = conv_stats_grid(work, P.N / BN);
   const CUtensorMap to = out_map(P.out, OUT16, P);
@@ -805,10 +806,7 @@ void launch_any(const CUtensorMap &ta, const __nv_bfloat16 *w, int wrows, int wK
     P.splits = 1;
     P.kb_per_split = P.ntaps * P.CB;
   }
-  if (P.splits > 1) {  // stats need final z (split-K: standalone pass)
-    P.stats = nullptr;
-    P.fin.mean = nullptr;
-  }
+  if (P.splits > 1) P.stats = nullptr;  // stats need final z (split-K: standalone pass)
   if (out16 && P.addend) throw PetraError(PETRA_E_ARG, "conv_tc: addend needs an fp32 output");
   CUtensorMap tb = mat_map(w, wrows, wK, pl.BN);
   if (out16) {
@@ -831,9 +829,9 @@ bool geom_ok(const ConvGeom &g) {
 }
 
 StatsRows run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const __nv_bfloat16 *w, void *out,
-                  bool out16, float *ws, float *stats, cudaStream_t st, const BnFinalize *fin) {
+                  bool out16, float *ws, float *stats, cudaStream_t st) {
   if (x_pad && g.k == 3 && g.s == 1 && conv_halo_eligible(g.B, g.H, g.W, g.Ci, g.Co))
-    return conv_halo_run(g.B, g.H, g.W, g.Ci, g.Co, x, w, nullptr, out, out16, stats, st, fin);
+    return conv_halo_run(g.B, g.H, g.W, g.Ci, g.Co, x, w, nullptr, out, out16, stats, st);
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
   ConvTCParams P{};
   P.M = (int)t.M();
@@ -857,10 +855,6 @@ StatsRows run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const _
   P.oss = 1;
   P.out = out;
   P.stats = stats;
-  if (stats && fin && fin->mean) {
-    P.fin = *fin;
-    P.fin.count = g.M();
-  }
   CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, t.Wb, t.R, t.NB, g.s, x_pad);
   launch_any(ta, w, g.Co, g.K(), P, ws, out16, st);
   if (!P.stats) return {};
@@ -868,7 +862,6 @@ StatsRows run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const _
   StatsRows r;
   r.groups = P.N / BN;
   r.rows = conv_stats_grid((P.M / BM) * (P.N / BN) * P.splits, r.groups);  // one partial row per CTA
-  r.finalized = P.fin.mean != nullptr;
   return r;
 }
 
@@ -975,7 +968,7 @@ void conv_tc_prepare() {
   std::call_once(once, [] {
     auto set = [](const void *f, int BN) {
       PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)conv_smem(BN, kMaxStatN * 32)));
+                                      (int)conv_smem(BN, kMaxStatN * 32 + 16)));
     };
     set((const void *)conv_tc_kernel<256, conv_stages(256), false>, 256);
     set((const void *)conv_tc_kernel<128, conv_stages(128), false>, 128);
@@ -1015,13 +1008,13 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode) {
 }
 
 StatsRows conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,
-                bool z_bf16, float *ws, float *stats_part, cudaStream_t st, const BnFinalize *fin) {
-  return run_fwd(g, x, x_padded, w, z, z_bf16, ws, stats_part, st, fin);
+                bool z_bf16, float *ws, float *stats_part, cudaStream_t st) {
+  return run_fwd(g, x, x_padded, w, z, z_bf16, ws, stats_part, st);
 }
 
 void bn_stats_from_partials(const float *part, StatsRows rows, int N, int64_t M, float eps, float *mean,
                             float *invstd, float *rmean, float *rvar, float mom, cudaStream_t st) {
-  launch_k(stats_finalize_kernel, (unsigned)cdiv(N, 32), 1024, 0, st, part, rows.rows, rows.groups, N, M, eps, mean,
+  launch_k(stats_finalize_kernel, (unsigned)cdiv(N, 32), 256, 0, st, part, rows.rows, rows.groups, N, M, eps, mean,
            invstd, rmean, rvar, mom);
   PETRA_LAUNCH_CHECK();
 }

@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
   uint64_t *tfull = empty + kStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  float *sstat = reinterpret_cast<float *>(tmem_slot + 4);  // [4][N][2]
+  float *sstat = reinterpret_cast<float *>(tmem_slot + 4);  // [4 quarters][N][3] (shift k, S, Q), then [4][N][2]
+  int *scnt = reinterpret_cast<int *>(sstat + 4 * 3 * P.N);  // [4 quarters] valid rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (int)cdiv(P.M, 128);
@@ -189,10 +190,14 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
   } else {  // ---------------- epilogue warps 8..11
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    float *my_stat = sstat + (size_t)q * P.N * 2;
+    // shifted statistics per column of this quarter's rows (tc::ColStats, kept in smem
+    // here: the lanes of a warp hold rows, colsum16 reduces them): k = mean of the first
+    // tile with valid rows, S = sum (z - k), Q = sum (z - k)^2 over valid rows
+    float *my_stat = sstat + (size_t)q * P.N * 3;
     if (P.stats)
-      for (int i = lane; i < 2 * P.N; i += 32) my_stat[i] = 0.f;
+      for (int i = lane; i < 3 * P.N; i += 32) my_stat[i] = 0.f;
     __syncwarp();
+    int nrows = 0;
     int it = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -200,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
       tc::tc_fence_after();
       const int m = t * 128 + row;
       const bool valid = m < P.M;
+      const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         float v[16];
@@ -228,28 +234,64 @@ __global__ void __launch_bounds__(kThreads, 1) stem_fwd_kernel(const __grid_cons
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
         }
-        if (P.stats) {
-          float sq[16];
+        if (P.stats && nvalid > 0) {
+          if (nrows == 0) {  // first tile: the shifts are the first valid row's values
+            const int r0 = __ffs(__ballot_sync(0xffffffffu, valid)) - 1;
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) sq[jj] = v[jj] * v[jj];
-          tc::colsum16(v, lane);
+            for (int jj = 0; jj < 16; ++jj) {
+              const float k0 = __shfl_sync(0xffffffffu, v[jj], r0);
+              if (lane == 0) my_stat[3 * (c + jj)] = k0;
+            }
+            __syncwarp();
+          }
+          float d[16], sq[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            d[jj] = valid ? v[jj] - my_stat[3 * (c + jj)] : 0.f;
+            sq[jj] = d[jj] * d[jj];
+          }
+          tc::colsum16(d, lane);
           tc::colsum16(sq, lane);
+          __syncwarp();
           if (!(lane & 1)) {
             const int col = c + (lane >> 1);
-            my_stat[2 * col] += v[0];
-            my_stat[2 * col + 1] += sq[0];
+            my_stat[3 * col + 1] += d[0];
+            my_stat[3 * col + 2] += sq[0];
           }
+          __syncwarp();
         }
       }
+      nrows += nvalid;
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
-    if (P.stats) {  // this CTA's partial row: the 4 warps' sums combined in a fixed order
+    if (P.stats) {  // this CTA's partial row: the 4 quarters' (count, mean, M2) merged (Chan) in order
+      const float inv = nrows > 0 ? 1.f / (float)nrows : 0.f;
+      float mu[8], m2[8];  // this warp's quarter, columns lane, lane + 32, ... (N <= 256)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int col = lane + 32 * r;
+        if (col < P.N) {
+          const float k = my_stat[3 * col], S = my_stat[3 * col + 1], Q = my_stat[3 * col + 2];
+          mu[r] = nrows > 0 ? k + S * inv : 0.f;
+          m2[r] = nrows > 0 ? fmaxf(fmaf(-S * inv, S, Q), 0.f) : 0.f;
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // every quarter has read its (k, S, Q)
+      float *fin = sstat;  // reuse as [4][N][2] (mean, M2)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int col = lane + 32 * r;
+        if (col < P.N) {
+          fin[(q * P.N + col) * 2] = mu[r];
+          fin[(q * P.N + col) * 2 + 1] = m2[r];
+        }
+      }
+      if (lane == 0) scnt[q] = nrows;
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      float *g = P.stats + (size_t)blockIdx.x * P.N * 2;
-      for (int i = q * 32 + lane; i < 2 * P.N; i += 128)
-        g[i] = (sstat[i] + sstat[2 * P.N + i]) + (sstat[4 * P.N + i] + sstat[6 * P.N + i]);
+      tc::cta_stats_row(fin, scnt, P.N, q * 32 + lane, 128, P.stats + (size_t)blockIdx.x * P.N * 2,
+                        P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
     }
   }
   __syncthreads();
@@ -416,7 +458,7 @@ __global__ void image_to_bf16x4_kernel(const float *__restrict__ x, uint2 *__res
 }
 
 size_t fwd_smem(int BN, int KB) {
-  return 1024 + (size_t)kStages * kATile + (size_t)KB * BN * 128 + 256 + (size_t)4 * BN * 2 * 4;
+  return 1024 + (size_t)kStages * kATile + (size_t)KB * BN * 128 + 256 + (size_t)4 * BN * 3 * 4 + 16;
 }
 size_t wgrad_smem(int BN) { return 1024 + (size_t)kStages * (kATile + BN * 128) + 256; }
 

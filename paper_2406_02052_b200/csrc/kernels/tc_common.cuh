@@ -236,16 +236,18 @@ __device__ __forceinline__ void colsum16(float (&x)[16], int lane) {
 // BN statistics of a warp's 32 staged output rows (each 128 bytes: 64 bf16 or 32 fp32
 // values), read back from the epilogue staging buffer instead of reduced across lanes:
 // lane L owns 4-byte word L of every row -- columns 2L, 2L+1 (bf16) or column L (fp32)
-// -- and sums it over the 32 rows (conflict-free: for a fixed row the lanes read 32
-// distinct banks).  Row r starts at buf + r * pitch; SWZ: 16-byte chunks in the
-// 128B-swizzled order of a TMA box (chunk c of row r at (c ^ (r & 7)) * 16).
+// -- and sums (z - k) and (z - k)^2 over the 32 rows, k = the lane's per-column shift
+// (conflict-free: for a fixed row the lanes read 32 distinct banks).  Row r starts at
+// buf + r * pitch; SWZ: 16-byte chunks in the 128B-swizzled order of a TMA box (chunk
+// c of row r at (c ^ (r & 7)) * 16).
 template <bool BF16, bool SWZ>
-__device__ __forceinline__ void staged_colsums(const uint8_t *buf, int pitch, int lane, float (&s)[2],
-                                               float (&q)[2]) {
+__device__ __forceinline__ void staged_colsums(const uint8_t *buf, int pitch, int lane, const float (&k)[2],
+                                               float (&s)[2], float (&q)[2]) {
   if constexpr (BF16) {
     // packed fp32x2 adds / FMAs (sm_100 FADD2 / FFMA2), even and odd rows in separate
     // accumulators (two dependency chains); bf16 -> fp32 is a 16-bit shift
     float2 s0 = make_float2(0.f, 0.f), s1 = s0, q0 = s0, q1 = s0;
+    const float2 nk = make_float2(-k[0], -k[1]);
     const uint32_t base = smem_u32(buf) + 4 * (lane & 3);
 #pragma unroll
     for (int r = 0; r < 32; r += 2) {
@@ -253,8 +255,8 @@ __device__ __forceinline__ void staged_colsums(const uint8_t *buf, int pitch, in
       const int c1 = SWZ ? ((lane >> 2) ^ ((r + 1) & 7)) : (lane >> 2);
       const uint32_t w0 = lds32(base + r * pitch + c0 * 16);
       const uint32_t w1 = lds32(base + (r + 1) * pitch + c1 * 16);
-      const float2 f0 = make_float2(__uint_as_float(w0 << 16), __uint_as_float(w0 & 0xffff0000u));
-      const float2 f1 = make_float2(__uint_as_float(w1 << 16), __uint_as_float(w1 & 0xffff0000u));
+      const float2 f0 = __fadd2_rn(make_float2(__uint_as_float(w0 << 16), __uint_as_float(w0 & 0xffff0000u)), nk);
+      const float2 f1 = __fadd2_rn(make_float2(__uint_as_float(w1 << 16), __uint_as_float(w1 & 0xffff0000u)), nk);
       s0 = __fadd2_rn(s0, f0);
       q0 = __ffma2_rn(f0, f0, q0);
       s1 = __fadd2_rn(s1, f1);
@@ -270,69 +272,82 @@ __device__ __forceinline__ void staged_colsums(const uint8_t *buf, int pitch, in
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
       const int chunk = SWZ ? ((lane >> 2) ^ (r & 7)) : (lane >> 2);
-      const float f = __uint_as_float(lds32(base + r * pitch + chunk * 16));
+      const float f = __uint_as_float(lds32(base + r * pitch + chunk * 16)) - k[0];
       s[0] += f;
       q[0] = fmaf(f, f, q[0]);
     }
   }
 }
 
-// In-kernel BN finalize by the last CTA of an N-tile group (the conv epilogues).
-// Every CTA has written its partial row [N][2] (sum, sum of squares) for the BN columns
-// of its group `grp` (rows grp, grp + groups, ...; rows_g of them).  Called by the
-// NT epilogue threads (tid 0..NT-1) after a named barrier that follows those writes;
-// `bar` / NT name that barrier.  The CTA that takes the last ticket of the group
-// sums the group's rows in a fixed order (fp64; NT / BN row slices, combined in slice
-// order: deterministic), writes mean / invstd and, when rmean != null, the running
-// statistics (reading c9: biased variance for normalisation, unbiased for the EMA),
-// then resets the ticket for the next launch.  scratch: >= NT * 2 doubles of smem.
-using StatsFinalize = ::petra::BnFinalize;
-template <int NT, int BAR>
-__device__ __forceinline__ void finalize_group(const StatsFinalize &F, const float *part, int N, int BN, int groups,
-                                               int grp, int tid, double *scratch, unsigned *s_flag) {
-  const int rows_g = ((int)gridDim.x - grp + groups - 1) / groups;
-  __threadfence();  // this thread's part of the CTA's partial row, before the ticket
-  asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
-  if (tid == 0) *s_flag = atomicAdd(&F.ticket[grp], 1u) == (unsigned)(rows_g - 1) ? 1u : 0u;
-  asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
-  if (*s_flag == 0u) return;
-  __threadfence();  // the other CTAs' rows (they fenced before their tickets)
-  const int S = NT / BN > 0 ? NT / BN : 1;  // row slices per column
-  for (int c0 = 0; c0 < BN; c0 += NT / S) {
-    const int c = c0 + tid % (NT / S), sl = tid / (NT / S);
-    double s = 0.0, ss = 0.0;
-    if (c < BN && sl < S) {
-      const float *p = part + ((size_t)grp * N + (size_t)grp * BN + c) * 2;
-      for (int k = sl; k < rows_g; k += S) {
-        const float2 v = __ldcg(reinterpret_cast<const float2 *>(p + (size_t)k * groups * N * 2));
-        s += v.x;
-        ss += v.y;
-      }
+// BN batch statistics in the conv epilogues: every lane keeps, for
+// its (up to two) columns, the shifted sums S = sum (z - k), Q = sum (z - k)^2 over the
+// valid rows of the tiles it has seen, with k = the column's value in the first valid
+// row it saw (the shifted-data algorithm: no cancellation between E[z^2] and mean^2 --
+// a sample of the column is within a few standard deviations of its mean).  Padding
+// rows are staged as exact zeros; their (0 - k) terms are removed.  At the end:
+// n (warp-uniform), mean = k + S / n, M2 = Q - S^2 / n -- the (count, mean, M2) triple
+// the CTA merges over its lane quarters and the finalize merges over CTAs.
+struct ColStats {
+  float k[2], s[2], q[2];
+};
+__device__ __forceinline__ void colstats_zero(ColStats &c) {
+  c.k[0] = c.k[1] = c.s[0] = c.s[1] = c.q[0] = c.q[1] = 0.f;
+}
+// add one staged 32-row tile whose valid rows are the set bits of vmask (warp-uniform);
+// n = valid rows seen so far
+template <bool BF16, bool SWZ>
+__device__ __forceinline__ void colstats_tile(const uint8_t *buf, int pitch, int lane, uint32_t vmask, int n,
+                                              ColStats &c) {
+  if (vmask == 0u) return;
+  if (n == 0) {  // the shift: this lane's word in the first valid row
+    const int r = __ffs(vmask) - 1;
+    const int chunk = SWZ ? ((lane >> 2) ^ (r & 7)) : (lane >> 2);
+    const uint32_t w = lds32(smem_u32(buf) + r * pitch + chunk * 16 + 4 * (lane & 3));
+    if constexpr (BF16) {
+      c.k[0] = __uint_as_float(w << 16);
+      c.k[1] = __uint_as_float(w & 0xffff0000u);
+    } else {
+      c.k[0] = __uint_as_float(w);
     }
-    scratch[2 * tid] = s;
-    scratch[2 * tid + 1] = ss;
-    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
-    if (tid < NT / S && c0 + tid < BN) {
-      double a = 0.0, b = 0.0;
-      for (int k = 0; k < S; ++k) {
-        a += scratch[2 * (k * (NT / S) + tid)];
-        b += scratch[2 * (k * (NT / S) + tid) + 1];
-      }
-      const int col = grp * BN + c0 + tid;
-      const double M = (double)F.count, mu = a / M;
-      double var = b / M - mu * mu;
-      if (var < 0.0) var = 0.0;
-      F.mean[col] = (float)mu;
-      F.invstd[col] = (float)(1.0 / sqrt(var + (double)F.eps));
-      if (F.rmean) {
-        const double unb = F.count > 1 ? var * M / (M - 1.0) : var;
-        F.rmean[col] = (float)((1.0 - F.mom) * F.rmean[col] + F.mom * mu);
-        F.rvar[col] = (float)((1.0 - F.mom) * F.rvar[col] + F.mom * unb);
-      }
-    }
-    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
   }
-  if (tid == 0) F.ticket[grp] = 0u;
+  float s[2], q[2];
+  staged_colsums<BF16, SWZ>(buf, pitch, lane, c.k, s, q);
+  const float pad = (float)(32 - __popc(vmask));
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    c.s[j] += fmaf(pad, c.k[j], s[j]);
+    c.q[j] += fmaf(-pad * c.k[j], c.k[j], q[j]);
+  }
+}
+// (mean, M2) of column j after n valid rows
+__device__ __forceinline__ float2 colstats_final(const ColStats &c, int j, int n) {
+  if (n == 0) return make_float2(0.f, 0.f);
+  const float inv = 1.f / (float)n;
+  return make_float2(c.k[j] + c.s[j] * inv, fmaxf(fmaf(-c.s[j] * inv, c.s[j], c.q[j]), 0.f));
+}
+// Chan's merge of (nb, mb, M2b) into (n, m, M2)
+template <typename T>
+__device__ __forceinline__ void chan_merge(T &n, T &m, T &M2, T nb, T mb, T M2b) {
+  if (nb <= T(0)) return;
+  const T nn = n + nb, d = mb - m;
+  m += d * (nb / nn);
+  M2 += M2b + d * d * (n * nb / nn);
+  n = nn;
+}
+// A CTA's partial statistics row from its 4 lane quarters: sq[quarter][BN][2] holds
+// (mean, M2) per column, cnt[quarter] the quarter's valid-row count; merged in quarter
+// order and written as (mean, M2) to row[BN][2] (global), the count to *row_n.
+__device__ __forceinline__ void cta_stats_row(const float *sq, const int *cnt, int BN, int tid, int nthreads,
+                                              float *row, float *row_n) {
+  for (int c = tid; c < BN; c += nthreads) {
+    float n = 0.f, m = 0.f, M2 = 0.f;
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq)
+      chan_merge(n, m, M2, (float)cnt[qq], sq[(qq * BN + c) * 2], sq[(qq * BN + c) * 2 + 1]);
+    row[2 * c] = m;
+    row[2 * c + 1] = M2;
+  }
+  if (tid == 0) *row_n = (float)(cnt[0] + cnt[1] + cnt[2] + cnt[3]);
 }
 
 }  // namespace tc

@@ -288,7 +288,7 @@ void Stage::build() {
   }
   for (auto &p : layers) {
     max_part = std::max(max_part, bn_partial_bytes(p.L->g.M(), p.L->g.Co));
-    max_part = std::max(max_part, (size_t)kNumSMs * 4 * p.L->g.Co * 2 * sizeof(float));  // fused conv stats
+    max_part = std::max(max_part, (size_t)kNumSMs * 4 * (p.L->g.Co * 2 + 1) * sizeof(float));  // fused conv stats
     max_ws = std::max(max_ws, conv_wgrad_simt_workspace(p.L->g));
     if (tc_)
       for (int mode = 0; mode < 3; ++mode) max_ws = std::max(max_ws, conv_tc_workspace(p.L->g, mode));
@@ -297,8 +297,6 @@ void Stage::build() {
   size_t max_ctr = 1;
   for (auto &p : layers) max_ctr = std::max(max_ctr, bn_counter_count(p.L->g.Co));
   for (int c = 0; c < 2; ++c) {
-    fin_ticket_[c] = dalloc(64 * sizeof(unsigned));  // conv-epilogue finalize tickets (<= 32 N-tile groups)
-    PETRA_CUDA(cudaMemset(fin_ticket_[c]->p, 0, 64 * sizeof(unsigned)));
     part_[c] = dalloc(std::max<size_t>(max_part, 16));
     counters_[c] = dalloc(max_ctr * sizeof(unsigned));
     PETRA_CUDA(cudaMemset(counters_[c]->p, 0, max_ctr * sizeof(unsigned)));
@@ -553,22 +551,8 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
   ProfScope ps(tc ? "conv_fwd_tc" : "conv_fwd_simt", st, conv_flops(L.g),
                conv_bytes(L.g, tc ? 2 : 4, PASS_FWD, L.z16 ? 2 : 4));
   if (tc) {
-    // PETRA_CONV_FINALIZE=1: BN statistics finalized by the conv's last CTA per N-tile
-    // group instead of a stats_finalize launch (measured slower under stage
-    // concurrency: R18 45.6k vs 47.0k samples/s -- the serial tail of the last CTA
-    // costs more than the small launch; off by default)
-    static const bool in_kernel = env_int("PETRA_CONV_FINALIZE", 0) != 0;
-    float *b = bufs_->as<float>();
-    BnFinalize fin;
-    fin.mean = in_kernel ? L.mean()->as<float>() : nullptr;
-    fin.invstd = L.invstd()->as<float>();
-    fin.rmean = running ? b + L.rm_off : nullptr;
-    fin.rvar = running ? b + L.rv_off : nullptr;
-    fin.ticket = fin_ticket_[ctx_]->as<unsigned>();
-    fin.eps = desc_.bn_eps;
-    fin.mom = desc_.bn_momentum;
     L.stats_rows() = conv_fwd_tc(L.g, L.xbp(), L.xpad, L.w_bf16->as<__nv_bfloat16>(), L.z()->p, L.z16,
-                                 wgrad_ws()->as<float>(), reinterpret_cast<float *>(part()->p), st, &fin);
+                                 wgrad_ws()->as<float>(), reinterpret_cast<float *>(part()->p), st);
   } else {
     conv_fwd_simt(L.g, x, w, L.z()->as<float>(), st, tc_);
   }
@@ -608,10 +592,6 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
 
 void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
   float *b = bufs_->as<float>();
-  if (L.stats_rows().finalized) {  // mean / invstd (+ running stats) written by the conv kernel
-    L.stats_rows() = StatsRows{};
-    return;
-  }
   if (L.stats_rows().rows > 0) {  // sums already produced by the tensor-core conv epilogue
     ProfScope ps("bn_stats_merge", st, 0.0, 8.0 * L.stats_rows().rows * L.g.Co / L.stats_rows().groups);
     bn_stats_from_partials(reinterpret_cast<const float *>(part()->p), L.stats_rows(), L.g.Co, L.g.M(), desc_.bn_eps,

@@ -167,7 +167,7 @@ class Stage {
   std::vector<SgdSeg> segs_;
   DevPtr segs_dev_;
   int64_t max_seg_ = 0;
-  DevPtr part_[2], wgrad_ws_[2], counters_[2], fin_ticket_[2];  // per context (see Layer)
+  DevPtr part_[2], wgrad_ws_[2], counters_[2];  // per context (see Layer)
   int ctx_ = 0;                                 // workspace context being enqueued
   DevPtr &part() { return part_[ctx_]; }
   DevPtr &wgrad_ws() { return wgrad_ws_[ctx_]; }
