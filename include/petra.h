@@ -109,6 +109,18 @@ typedef struct {
 
 typedef struct petra_stage petra_stage;
 
+/* Device memory the library allocates (parameters, optimizer slots, FIFOs, workspace,
+ * mailboxes) comes from cudaMalloc / cudaFree, or, once installed, from the caller's
+ * allocator -- e.g. PyTorch's caching allocator, so a training process has one pool.
+ * alloc(bytes, device, ctx) returns a device pointer on `device` (the current device
+ * when the object is created) or NULL (-> PETRA_E_OOM); release(ptr, device, ctx) frees
+ * it.  A buffer is released through the allocator that made it, so installing another
+ * one (or NULL, NULL to return to cudaMalloc) affects only objects created afterwards.
+ * Process-wide; call it while no other thread creates library objects.
+ * Errors: PETRA_E_ARG (exactly one of alloc / release NULL). */
+petra_status petra_set_allocator(void *(*alloc)(size_t bytes, int32_t device, void *ctx),
+                                 void (*release)(void *ptr, int32_t device, void *ctx), void *ctx);
+
 /* Create a stage on the current CUDA device.  Parameters are initialised from
  * `seed` (Kaiming-uniform conv/linear weights, gamma=1, beta=0, bias=0,
  * running mean 0 / var 1, momentum 0); callers that need identical values on

@@ -117,6 +117,7 @@ SIGS = {
     "petra_pipeline_create": (C.c_int, [C.POINTER(PetraPipelineDesc), C.POINTER(P)]),
     "petra_pipeline_destroy": (C.c_int, [P]),
     "petra_nccl_unique_id": (C.c_int, [VP]),
+    "petra_set_allocator": (C.c_int, [VP, VP, VP]),
     "petra_pipeline_stage": (C.c_int, [P, I32, C.POINTER(P)]),
     "petra_pipeline_tick": (C.c_int, [P, I64, I32, VP, VP, F32, VP, VP, C.POINTER(PetraTickReport)]),
     "petra_pipeline_comm": (C.c_int, [P, I64, C.POINTER(PetraCommPlan)]),

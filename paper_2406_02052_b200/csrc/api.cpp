@@ -137,10 +137,12 @@ petra_status petra_stage_get_params(petra_stage *s, float *theta, float *v, floa
   if (!s) return fail(PETRA_E_ARG, "NULL stage");
   petra_status st = guard([&] { s->s->get_params(theta, v, bufs); });
   if (st != PETRA_OK) return st;
-  bool nf = false;
+  int nf = 0;
   st = guard([&] { nf = s->s->nonfinite(); });
   if (st != PETRA_OK) return st;
-  if (nf) return fail(PETRA_E_NONFINITE, "non-finite loss was produced");
+  if (nf) return fail(PETRA_E_NONFINITE, std::string("non-finite ") + ((nf & 1) ? "loss " : "") +
+                                             ((nf & 2) ? "Delta (a gradient fed to the update) " : "") +
+                                             "was produced");
   return PETRA_OK;
 }
 
@@ -189,6 +191,16 @@ petra_status petra_pipeline_create(const petra_pipeline_desc *d, petra_pipeline 
     }
     *out = h.release();
   });
+}
+
+petra_status petra_set_allocator(void *(*alloc)(size_t bytes, int32_t device, void *ctx),
+                                 void (*release)(void *ptr, int32_t device, void *ctx), void *ctx) {
+  if ((alloc == nullptr) != (release == nullptr)) return fail(PETRA_E_ARG, "alloc and release go together");
+  petra::Allocator &a = petra::allocator();
+  a.alloc = reinterpret_cast<void *(*)(size_t, int, void *)>(alloc);
+  a.release = reinterpret_cast<void (*)(void *, int, void *)>(release);
+  a.ctx = ctx;
+  return PETRA_OK;
 }
 
 petra_status petra_nccl_unique_id(unsigned char out[128]) {

@@ -116,7 +116,7 @@ struct SgdSeg {
 enum { SGD_PLAIN = 0, SGD_ACCUMULATE = 1, SGD_ACC_UPDATE = 2 };
 void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *theta, float *v, const float *grad,
                 float *acc, int k, int mode, const float *lr_dev, float mom, float wd, int nesterov, cudaStream_t st,
-                bool shadow_only);
+                bool shadow_only, int *nonfinite);  // nonfinite: device flag set (2) by a NaN / Inf in Delta
 void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int C, const float *w,
                            const float *bias, int N, const int32_t *labels, float *feat, float *logits,
                            float *dlogits, float *loss_row, float *dfeat, float *dw, float *db, float *d1,

@@ -822,6 +822,9 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
   }
 }
 
+// a byte offset inside a TMA ring stage that can start a tensor-copy destination
+inline bool ring_aligned(size_t bytes) { return bytes % 128 == 0; }
+
 inline unsigned ew_grid(int64_t n) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs));
 }
@@ -871,21 +874,25 @@ void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean
     const int es = (int)sizeof(TZ) + (acc ? 4 : 0);
     const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (24576 / (g.CT * es)) / g.RG * g.RG));
     const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
-    static std::once_flag once;
-    std::call_once(once, [] {
-      cudaFuncSetAttribute(bn_apply_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(bn_apply_tma_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           160 * 1024);
-    });
-    const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    // z: [M][C] view of a [M][ldz] buffer from column zc0
-    const CUtensorMap tz = plain_map_2d_strided(z + zc0, zt, (int)sizeof(TZ), M, C, ldz, g.CT, Rc);
-    const CUtensorMap ta = acc ? plain_map_2d(acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc) : tz;
-    launch_k(bn_apply_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), 256, 2 * sbytes, st, tz, ta, acc ? 1 : 0, M, C, g.CT,
-             g.TPR, g.RG, g.rpb, Rc, zc0, mean, invstd, gamma, beta, relu, sign, reinterpret_cast<float *>(out), out_bf16,
-             pH, pW);
-    PETRA_LAUNCH_CHECK();
-    return;
+    // every TMA destination inside a ring stage must be 128-byte aligned (else the register kernel)
+    const bool ring_ok = ring_aligned((size_t)Rc * g.CT * sizeof(TZ)) && g.CT % 8 == 0;
+    if (ring_ok) {
+      static std::once_flag once;
+      std::call_once(once, [] {
+        cudaFuncSetAttribute(bn_apply_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(bn_apply_tma_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             160 * 1024);
+      });
+      const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+      // z: [M][C] view of a [M][ldz] buffer from column zc0
+      const CUtensorMap tz = plain_map_2d_strided(z + zc0, zt, (int)sizeof(TZ), M, C, ldz, g.CT, Rc);
+      const CUtensorMap ta = acc ? plain_map_2d(acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc) : tz;
+      launch_k(bn_apply_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), 256, 2 * sbytes, st, tz, ta, acc ? 1 : 0, M, C, g.CT,
+               g.TPR, g.RG, g.rpb, Rc, zc0, mean, invstd, gamma, beta, relu, sign, reinterpret_cast<float *>(out), out_bf16,
+               pH, pW);
+      PETRA_LAUNCH_CHECK();
+      return;
+    }
   }
   const unsigned cg = (ldz % 4 == 0 && zc0 % 4 == 0) ? chan_grid(M, C) : 0;
   if (cg && std::is_same<TO, float>::value && M < ((int64_t)1 << 31) / 4) {
@@ -919,25 +926,30 @@ void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float
     const int es = (int)sizeof(TZ) + 4 + (dst_out ? 4 : 0);
     const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (40960 / (g.CT * es)) / g.RG * g.RG));
     const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
-    static std::once_flag once;
-    std::call_once(once, [] {
-      cudaFuncSetAttribute(bn_bwd_reduce_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(bn_bwd_reduce_tma_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           160 * 1024);
-    });
-    const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    const CUtensorMap tz = plain_map_2d(z, zt, (int)sizeof(TZ), M, C, g.CT, Rc);
-    const int s0 = dy1 ? cs : 0;
-    const CUtensorMap ty = dy1 ? plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, cs, cs, Rc)
-                               : plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
-    const CUtensorMap ty1 = dy1 ? plain_map_2d(dy1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C - cs, C - cs, Rc) : ty;
-    const CUtensorMap td = dst_out ? plain_map_2d(dst_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc) : ty;
-    launch_k(bn_bwd_reduce_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 2 * sbytes, st, tz, ty, td, ty1, s0, M, C,
-             g.CT,
-             g.TPR, g.RG, g.rpb, g.nrb, Rc, mean, invstd, gamma, beta, relu, dst_out ? 1 : 0, dst_out, dst_bf16, pH,
-             pW, part, counter, dgamma, dbeta);
-    PETRA_LAUNCH_CHECK();
-    return;
+    // every TMA destination inside a ring stage must be 128-byte aligned (else the register kernel)
+    const bool ring_ok = ring_aligned((size_t)Rc * g.CT * sizeof(TZ)) && ring_aligned((size_t)Rc * g.CT * 4) &&
+                         (!dy1 || ring_aligned((size_t)Rc * cs * 4));
+    if (ring_ok) {
+      static std::once_flag once;
+      std::call_once(once, [] {
+        cudaFuncSetAttribute(bn_bwd_reduce_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(bn_bwd_reduce_tma_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             160 * 1024);
+      });
+      const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+      const CUtensorMap tz = plain_map_2d(z, zt, (int)sizeof(TZ), M, C, g.CT, Rc);
+      const int s0 = dy1 ? cs : 0;
+      const CUtensorMap ty = dy1 ? plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, cs, cs, Rc)
+                                 : plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
+      const CUtensorMap ty1 = dy1 ? plain_map_2d(dy1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C - cs, C - cs, Rc) : ty;
+      const CUtensorMap td = dst_out ? plain_map_2d(dst_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc) : ty;
+      launch_k(bn_bwd_reduce_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 2 * sbytes, st, tz, ty, td, ty1, s0, M, C,
+               g.CT,
+               g.TPR, g.RG, g.rpb, g.nrb, Rc, mean, invstd, gamma, beta, relu, dst_out ? 1 : 0, dst_out, dst_bf16, pH,
+               pW, part, counter, dgamma, dbeta);
+      PETRA_LAUNCH_CHECK();
+      return;
+    }
   }
   launch_k(bn_bwd_reduce_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 0, st, z, M, C, g.CT, g.TPR, g.RG, g.rpb, g.nrb, mean,
                                                                  invstd, gamma, beta, relu, dy0, dy1, cs, dst_in,
@@ -966,23 +978,28 @@ void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *in
     const int es = (int)sizeof(TZ) + 4;
     const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (24576 / (g.CT * es)) / g.RG * g.RG));
     const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
-    static std::once_flag once;
-    std::call_once(once, [] {
-      cudaFuncSetAttribute(bn_bwd_dz_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(bn_bwd_dz_tma_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           160 * 1024);
-    });
-    const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    const CUtensorMap tz = plain_map_2d(z, zt, (int)sizeof(TZ), M, C, g.CT, Rc);
-    const int s0 = dy1 ? cs : 0;
-    const CUtensorMap ty = dy1 ? plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, cs, cs, Rc)
-                               : plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
-    const CUtensorMap ty1 = dy1 ? plain_map_2d(dy1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C - cs, C - cs, Rc) : ty;
-    launch_k(bn_bwd_dz_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), 256, 2 * sbytes, st, tz, ty, ty1, s0, M, C, g.CT, g.TPR,
-             g.RG,
-             g.rpb, Rc, mean, invstd, gamma, beta, relu, dgamma, dbeta, dz, dz_bf16, pH, pW);
-    PETRA_LAUNCH_CHECK();
-    return;
+    // every TMA destination inside a ring stage must be 128-byte aligned (else the register kernel)
+    const bool ring_ok = ring_aligned((size_t)Rc * g.CT * sizeof(TZ)) && g.CT % 8 == 0 &&
+                         (!dy1 || ring_aligned((size_t)Rc * cs * 4));
+    if (ring_ok) {
+      static std::once_flag once;
+      std::call_once(once, [] {
+        cudaFuncSetAttribute(bn_bwd_dz_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(bn_bwd_dz_tma_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             160 * 1024);
+      });
+      const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+      const CUtensorMap tz = plain_map_2d(z, zt, (int)sizeof(TZ), M, C, g.CT, Rc);
+      const int s0 = dy1 ? cs : 0;
+      const CUtensorMap ty = dy1 ? plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, cs, cs, Rc)
+                                 : plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
+      const CUtensorMap ty1 = dy1 ? plain_map_2d(dy1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C - cs, C - cs, Rc) : ty;
+      launch_k(bn_bwd_dz_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), 256, 2 * sbytes, st, tz, ty, ty1, s0, M, C, g.CT, g.TPR,
+               g.RG,
+               g.rpb, Rc, mean, invstd, gamma, beta, relu, dgamma, dbeta, dz, dz_bf16, pH, pW);
+      PETRA_LAUNCH_CHECK();
+      return;
+    }
   }
   const unsigned cg = dy1 == nullptr ? chan_grid(M, C) : 0;  // split halves (stem): generic pass
   if (cg && M < ((int64_t)1 << 31) / 4)

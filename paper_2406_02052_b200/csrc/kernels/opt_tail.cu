@@ -18,7 +18,7 @@ __global__ void __launch_bounds__(256) sgd_kernel(const SgdSeg *__restrict__ seg
                                                   float *__restrict__ v, const float *__restrict__ grad,
                                                   float *__restrict__ acc, float inv_k, int mode,
                                                   const float *__restrict__ lr_dev, float mom, float wd, int nesterov,
-                                                  int shadow_only) {
+                                                  int shadow_only, int *__restrict__ nonfinite) {
   pdl_wait_trigger();
   // mode (Alg. 1 lines 19-22):  SGD_PLAIN   k = 1, update with Delta;
   // SGD_ACCUMULATE  acc += Delta/k, no update;  SGD_ACC_UPDATE  update with acc + Delta/k, acc = 0
@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(256) sgd_kernel(const SgdSeg *__restrict__ seg
     float th = theta[o];
     if (shadow_only) return th;
     float d = grad[o];
+    if (!isfinite(d)) atomicOr(nonfinite, 2);  // latched (bit 1: Delta); reported by petra_stage_get_params
     if (mode == SGD_ACC_UPDATE) {
       d = fmaf(d, inv_k, acc[o]);
       acc[o] = 0.f;
@@ -44,8 +45,11 @@ __global__ void __launch_bounds__(256) sgd_kernel(const SgdSeg *__restrict__ seg
   };
   if (mode == SGD_ACCUMULATE) {  // Delta_j += Delta / k; theta (and its shadows) unchanged
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sg.count;
-         i += (int64_t)gridDim.x * blockDim.x)
-      acc[sg.offset + i] += grad[sg.offset + i] * inv_k;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const float d = grad[sg.offset + i];
+      if (!isfinite(d)) atomicOr(nonfinite, 2);
+      acc[sg.offset + i] += d * inv_k;
+    }
     return;
   }
   if (sg.wt_bf16) {
@@ -227,7 +231,7 @@ __global__ void loss_mean_kernel(const float *__restrict__ loss_row, int B, floa
     for (int b = 0; b < B; ++b) s += loss_row[b];
     float l = (float)(s / B);
     if (loss) *loss = l;
-    if (!isfinite(l)) *nonfinite = 1;
+    if (!isfinite(l)) atomicOr(nonfinite, 1);  // latched (bit 0: loss)
   }
 }
 
@@ -405,10 +409,10 @@ inline unsigned ew_grid(int64_t n) {
 
 void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *theta, float *v, const float *grad,
                 float *acc, int k, int mode, const float *lr_dev, float mom, float wd, int nesterov, cudaStream_t st,
-                bool shadow_only) {
+                bool shadow_only, int *nonfinite) {
   dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(max_count, 256), 2 * kNumSMs)), nseg);
   launch_k(sgd_kernel, grid, 256, 0, st, segs_dev, theta, v, grad, acc, 1.f / (float)k, mode, lr_dev, mom, wd, nesterov,
-                                           shadow_only ? 1 : 0);
+           shadow_only ? 1 : 0, nonfinite);
   PETRA_LAUNCH_CHECK();
 }
 

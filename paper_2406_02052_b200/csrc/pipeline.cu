@@ -191,6 +191,7 @@ int Pipeline::stage_ms(float *ms, int n) {
 }
 
 Pipeline::~Pipeline() {
+  cudaDeviceSynchronize();  // mailboxes and ghost buffers may still be in use (see ~Stage)
   if (transport_ == PETRA_TRANSPORT_LOCAL) {
     std::lock_guard<std::mutex> lk(g_hub_mu);
     auto it = g_hub.find(group_);
@@ -225,6 +226,7 @@ static float *fp(const DevPtr &p) { return p ? p->as<float>() : nullptr; }
 
 void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labels, float lr, float *loss,
                     cudaStream_t st, petra_tick_report *rep) {
+  NvtxRange tick_range("petra tick %lld (rank %d)", (long long)t, rank_);
   std::vector<int64_t> ver, fifo;
   std::vector<Schedule::Step> steps = sched_.tick(t, inject, &ver, &fifo);
   const int p = (int)(t & 1), q = p ^ 1;
@@ -301,7 +303,10 @@ void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labe
       e1 = ev();
       PETRA_CUDA(cudaEventRecord(e0, st));
     }
-    s.tick(a, lr, st, graphs_);
+    {
+      NvtxRange r("stage %d: fwd mb %lld, bwd mb %lld", j, (long long)sp.fwd_mb, (long long)sp.bwd_mb);
+      s.tick(a, lr, st, graphs_);
+    }
     if (timing_) {
       PETRA_CUDA(cudaEventRecord(e1, st));
       tev_[j].push_back({e0, e1});
@@ -347,6 +352,7 @@ void Pipeline::exchange(int64_t t, std::vector<bool> &used) {
         PETRA_CUDA(cudaStreamWaitEvent(cs, dir == DIR_FWD ? tdone_[j0][q] : tdone_[j1][q], 0));
       }
     }
+    NvtxRange nr(dir == DIR_FWD ? "exchange fwd (x1, x2, labels -> rank+1)" : "exchange bwd (x~, delta -> rank-1)");
     ProfScope ps(dir == DIR_FWD ? "exchange_fwd" : "exchange_bwd", cs, 0.0, 0.0);
     if (transport_ == PETRA_TRANSPORT_NCCL) {
       const NcclApi &nc = nccl();

@@ -4,12 +4,32 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <string>
 #include <vector>
 
 namespace petra {
+
+// NVTX range (header-only NVTX v3: a no-op unless a tool such as nsys is attached).
+// The library marks each pipeline tick, each stage's tick inside it and each exchange
+// direction, so an nsys timeline shows per stage and phase where the time goes and how
+// the exchange overlaps the compute.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  template <typename... A>
+  NvtxRange(const char *fmt, A... a) {
+    char buf[96];
+    std::snprintf(buf, sizeof(buf), fmt, a...);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 struct Prof {
   static std::atomic<int64_t> launches;  // every kernel launch of the library

@@ -26,9 +26,27 @@ namespace petra {
 // bytes allocated by the stage under construction (Stage::memory)
 static thread_local size_t *g_alloc_acc = nullptr;
 
+// device allocator (petra_set_allocator): cudaMalloc / cudaFree unless the caller installed
+// its own (e.g. PyTorch's caching allocator); a buffer remembers who allocated it
+Allocator &allocator() {
+  static Allocator a;
+  return a;
+}
+
 DevBuf::DevBuf(size_t n) : bytes(n) {
   if (n == 0) return;
   if (g_alloc_acc) *g_alloc_acc += n;
+  const Allocator a = allocator();
+  if (a.alloc) {
+    int dev = 0;
+    PETRA_CUDA(cudaGetDevice(&dev));
+    p = a.alloc(n, dev, a.ctx);
+    if (!p) throw PetraError(PETRA_E_OOM, "installed allocator returned NULL for " + std::to_string(n) + " bytes");
+    release = a.release;
+    ctx = a.ctx;
+    device = dev;
+    return;
+  }
   cudaError_t e = cudaMalloc(&p, n);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -36,7 +54,9 @@ DevBuf::DevBuf(size_t n) : bytes(n) {
   }
 }
 DevBuf::~DevBuf() {
-  if (p) cudaFree(p);
+  if (!p) return;
+  if (release) release(p, device, ctx);
+  else cudaFree(p);
 }
 DevPtr dalloc(size_t bytes) { return DevPtr(new DevBuf(bytes)); }
 
@@ -80,6 +100,9 @@ Stage::Stage(const petra_stage_desc &desc, uint64_t seed) : desc_(desc) {
 }
 
 Stage::~Stage() {
+  // the device may still run this stage's work; its buffers go back to an allocator
+  // (cudaFree, or a caller's caching pool that would hand them out again at once)
+  cudaDeviceSynchronize();
   for (auto &kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
   if (side_) cudaStreamDestroy(side_);
   if (fork_) cudaEventDestroy(fork_);
@@ -417,7 +440,8 @@ void Stage::set_params(const float *theta, const float *v, const float *bufs) {
     PETRA_CUDA(cudaMemcpy(bufs_->p, bufs, n_buffers_ * sizeof(float), cudaMemcpyHostToDevice));
   if (tc_ && theta) {
     sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
-               grad_->as<float>(), nullptr, 1, SGD_PLAIN, nullptr, 0.f, 0.f, 1, nullptr, /*shadow_only=*/true);
+               grad_->as<float>(), nullptr, 1, SGD_PLAIN, nullptr, 0.f, 0.f, 1, nullptr, /*shadow_only=*/true,
+               nonfinite_->as<int>());
     PETRA_CUDA(cudaDeviceSynchronize());
   }
 }
@@ -435,11 +459,11 @@ void Stage::get_grads(float *delta) {
   PETRA_CUDA(cudaMemcpy(delta, grad_->p, n_params_ * sizeof(float), cudaMemcpyDeviceToHost));
 }
 
-bool Stage::nonfinite() {
+int Stage::nonfinite() {
   int h = 0;
   PETRA_CUDA(cudaDeviceSynchronize());
   PETRA_CUDA(cudaMemcpy(&h, nonfinite_->p, sizeof(int), cudaMemcpyDeviceToHost));
-  return h != 0;
+  return h;
 }
 
 void Stage::memory(petra_memory_report *r) const {
@@ -501,7 +525,7 @@ void Stage::enqueue_update(int mode, cudaStream_t st) {
                (mode == SGD_PLAIN ? 20.0 : mode == SGD_ACCUMULATE ? 12.0 : 28.0) * (double)n_params_);
   sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
              grad_->as<float>(), acc_ ? acc_->as<float>() : nullptr, desc_.accumulation_k, mode, lr_dev_->as<float>(),
-             desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false);
+             desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false, nonfinite_->as<int>());
 }
 
 // ------------------------------------------------------------------ layer kernels
@@ -1046,6 +1070,7 @@ static void check_lr(float lr) {
 }
 
 void Stage::forward(uint64_t mb, const float *x1, const float *x2, float *o1, float *o2, cudaStream_t st) {
+  NvtxRange nr("stage forward mb %llu", (unsigned long long)mb);
   if (is_last_) throw PetraError(PETRA_E_ARG, "the final stage runs petra_stage_tail");
   check_fwd(mb, x1, x2);
   if (!o1 || !o2) throw PetraError(PETRA_E_ARG, "NULL output pointer");
@@ -1060,6 +1085,7 @@ void Stage::forward(uint64_t mb, const float *x1, const float *x2, float *o1, fl
 
 void Stage::backward(uint64_t mb, const float *xt1, const float *xt2, const float *d1, const float *d2,
                      float *oxt1, float *oxt2, float *od1, float *od2, float lr, cudaStream_t st) {
+  NvtxRange nr("stage backward mb %llu", (unsigned long long)mb);
   if (is_last_) throw PetraError(PETRA_E_ARG, "the final stage runs petra_stage_tail");
   if (!xt1 || !xt2 || !d1 || !d2) throw PetraError(PETRA_E_ARG, "NULL backward input");
   check_lr(lr);
@@ -1077,6 +1103,7 @@ void Stage::backward(uint64_t mb, const float *xt1, const float *xt2, const floa
 
 void Stage::tail(uint64_t mb, const float *x1, const float *x2, const int32_t *labels, float lr, float *oxt1,
                  float *oxt2, float *od1, float *od2, float *loss, cudaStream_t st) {
+  NvtxRange nr("stage tail mb %llu", (unsigned long long)mb);
   if (!is_last_) throw PetraError(PETRA_E_ARG, "petra_stage_tail on a stage without a tail unit");
   if (!labels) throw PetraError(PETRA_E_ARG, "NULL labels");
   check_fwd(mb, x1, x2);

@@ -12,10 +12,21 @@
 
 namespace petra {
 
+// device allocator installed with petra_set_allocator (alloc == null: cudaMalloc)
+struct Allocator {
+  void *(*alloc)(size_t, int, void *) = nullptr;
+  void (*release)(void *, int, void *) = nullptr;
+  void *ctx = nullptr;
+};
+Allocator &allocator();
+
 // device allocation owned by a stage
 struct DevBuf {
   void *p = nullptr;
   size_t bytes = 0;
+  void (*release)(void *, int, void *) = nullptr;  // the allocator that made it (null: cudaFree)
+  void *ctx = nullptr;
+  int device = 0;
   DevBuf() = default;
   explicit DevBuf(size_t n);
   ~DevBuf();
@@ -151,7 +162,7 @@ class Stage {
   void get_params(float *theta, float *v, float *bufs);
   void set_params(const float *theta, const float *v, const float *bufs);
   void get_grads(float *delta);
-  bool nonfinite();
+  int nonfinite();  // latched device flags: bit 0 loss, bit 1 Delta (NaN / Inf)
   cudaStream_t last_stream() const { return last_stream_; }
 
  private:

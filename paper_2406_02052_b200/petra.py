@@ -172,6 +172,32 @@ class Pipeline:
         return [(plan.e[i].peer, plan.e[i].send, plan.e[i].ptr, plan.e[i].bytes) for i in range(plan.n)]
 
 
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
+_RELEASE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.c_void_p)
+_allocator_keep = []
+
+
+def use_torch_allocator(enable: bool = True):
+    """petra_set_allocator with PyTorch's caching allocator (enable) or cudaMalloc (not):
+    the library's parameters, FIFOs and workspace then live in torch's pool."""
+    import torch
+    if not enable:
+        L.call("petra_set_allocator", None, None, None)
+        return
+
+    def alloc(n, dev, ctx):
+        try:
+            return int(torch.cuda.caching_allocator_alloc(int(n), int(dev)))
+        except Exception:
+            return None
+
+    def release(p, dev, ctx):
+        torch.cuda.caching_allocator_delete(int(p))
+    fa, fr = _ALLOC_FN(alloc), _RELEASE_FN(release)
+    _allocator_keep[:] = [fa, fr]  # the library holds raw pointers to the callbacks
+    L.call("petra_set_allocator", C.cast(fa, C.c_void_p), C.cast(fr, C.c_void_p), None)
+
+
 def nccl_unique_id() -> bytes:
     """petra_nccl_unique_id: 128 bytes for PETRA_TRANSPORT_NCCL (create on rank 0, share)."""
     buf = C.create_string_buffer(128)

@@ -135,3 +135,13 @@ def test_partition_is_flop_balanced():
         per.append(sum(cost[i:i + c]))
         i += c
     assert max(per) <= 1.25 * sum(cost) / 4
+
+
+def test_set_allocator_argument_checks():
+    """petra_set_allocator: alloc and release go together; (NULL, NULL) restores cudaMalloc.
+    Host-only (no device work)."""
+    import ctypes as C
+    from paper_2406_02052_b200 import _lib as L
+    fa = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)(lambda n, d, c: None)
+    assert L.lib().petra_set_allocator(C.cast(fa, C.c_void_p), None, None) == 1  # PETRA_E_ARG
+    assert L.lib().petra_set_allocator(None, None, None) == 0
