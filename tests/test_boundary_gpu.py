@@ -19,14 +19,19 @@ def _stage(precision=L.BF16_TC, B=4):
     return st
 
 
+_MB = [0]
+
+
 def _tick(st, B=4, scale=1.0):
+    mb = _MB[0]
+    _MB[0] += 1
     g = torch.Generator(device="cuda").manual_seed(0)
     x = [torch.randn(B, 8, 8, 64, device="cuda", generator=g) for _ in range(2)]
     o = [torch.empty_like(x[0]) for _ in range(2)]
-    st.forward(0, x[0], x[1], o[0], o[1])
+    st.forward(mb, x[0], x[1], o[0], o[1])
     d = [torch.randn(B, 8, 8, 64, device="cuda", generator=g) * scale for _ in range(2)]
     r = [torch.empty_like(x[0]) for _ in range(4)]
-    st.backward(0, o[0], o[1], d[0], d[1], *r, 0.01)
+    st.backward(mb, o[0], o[1], d[0], d[1], *r, 0.01)
     torch.cuda.synchronize()
 
 
