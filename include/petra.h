@@ -105,7 +105,18 @@ typedef struct {
                                       Delta_mb / k every backward; Nesterov update with Delta_j and
                                       reset when t mod k == 0 (t counts backwards from 1)           */
   int32_t fifo_capacity;           /* non-reversible input FIFO depth; >= 2(J-j)+1 (Table 1)   */
+  int32_t compare_buffers;         /* 0 for PETRA.  Table 3 comparison modes (PAPER.md:310-330,
+                                      memory measurement only; the numerics stay PETRA's):
+                                      bit 0 (PETRA_CMP_INPUTS): the stage also buffers the input
+                                      of each of its fifo_capacity in-flight micro-batches, as a
+                                      delayed-gradient method must (a device copy every forward;
+                                      nothing extra when its first unit is non-reversible: its
+                                      FIFO holds them already);
+                                      bit 1 (PETRA_CMP_STASH): weight stashing -- fifo_capacity-1
+                                      = 2(J-j) extra fp32 copies of theta, one written every
+                                      forward (PipeDream)                                        */
 } petra_stage_desc;
+enum { PETRA_CMP_INPUTS = 1, PETRA_CMP_STASH = 2 };
 
 typedef struct petra_stage petra_stage;
 
@@ -149,10 +160,12 @@ petra_status petra_stage_param_count(const petra_stage *s, size_t *n_params, siz
  *   fifo_live  bytes of those slots holding an input right now
  *   workspace  everything else: per-layer conv outputs / BN statistics / operand
  *              copies of the tick, tail buffers
+ *   cmp_inputs, cmp_stash  the comparison buffers of petra_stage_desc.compare_buffers
  *   total      sum of the above categories (fifo_live excluded)
  * Host-only, no synchronisation.  Errors: PETRA_E_ARG (NULL). */
 typedef struct {
   uint64_t total, params, optimizer, shadows, fifo, fifo_live, workspace;
+  uint64_t cmp_inputs, cmp_stash;  /* compare_buffers modes: the extra input ring / theta stash */
 } petra_memory_report;
 petra_status petra_stage_memory(const petra_stage *s, petra_memory_report *out);
 
@@ -257,6 +270,18 @@ petra_status petra_stage_tail(petra_stage *s, uint64_t mb_id,
  * (join_comm == 0).
  */
 typedef enum { PETRA_TRANSPORT_NONE = 0, PETRA_TRANSPORT_NCCL = 1, PETRA_TRANSPORT_LOCAL = 2 } petra_transport;
+/* Message format at stage boundaries ("doubles the cost of
+ * backward communications"):
+ *   PETRA_WIRE_FP32  messages are the fp32 stream values (default; the inversion
+ *                    reconstructs x~ from exactly what the next stage computed);
+ *   PETRA_WIRE_BF16  every message a stage sends (x1, x2 forward; x~1, x~2, d1, d2
+ *                    backward) is rounded to bf16 (round-to-nearest-even) by the producing
+ *                    stage before it is declared final, at EVERY stage boundary whatever the
+ *                    rank layout (so the numerics do not depend on it), and cross-rank
+ *                    transfers carry 2-byte elements: half the NVLink bytes.  Stage 1's
+ *                    injected input is not a message and is not rounded.  The error this
+ *                    adds is measured in DESIGN.md (section 9, "bf16 wire"). */
+typedef enum { PETRA_WIRE_FP32 = 0, PETRA_WIRE_BF16 = 1 } petra_wire;
 
 typedef struct {
   int32_t n_stages;                /* J                                                */
@@ -268,6 +293,7 @@ typedef struct {
   const unsigned char *nccl_id;    /* NCCL: 128 bytes (petra_nccl_unique_id)           */
   int64_t local_group;             /* LOCAL: nonzero key shared by the ranks           */
   int32_t join_comm;               /* library transports: see above (1 = default)      */
+  int32_t wire;                    /* petra_wire: message format at stage boundaries   */
 } petra_pipeline_desc;
 
 /* NCCL unique id for PETRA_TRANSPORT_NCCL (call on rank 0, share with all ranks).

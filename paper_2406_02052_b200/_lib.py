@@ -19,6 +19,7 @@ MAX_COMM = 16
 
 FP32, BF16_TC = 0, 1
 UNIT_REV, UNIT_DS, UNIT_STEM, UNIT_TAIL = 0, 1, 2, 3
+CMP_INPUTS, CMP_STASH = 1, 2  # petra_stage_desc.compare_buffers (Table 3 comparison modes)
 T_CONV_W, T_BN_GAMMA, T_BN_BETA, T_FC_W, T_FC_B, T_BN_RMEAN, T_BN_RVAR = range(7)
 STATUS = {0: "PETRA_OK", 1: "PETRA_E_ARG", 2: "PETRA_E_SHAPE", 3: "PETRA_E_ODD_CHANNELS",
           4: "PETRA_E_EMPTY_BUFFER", 5: "PETRA_E_ORDER", 6: "PETRA_E_NONFINITE", 7: "PETRA_E_CUDA",
@@ -40,7 +41,7 @@ class PetraStageDesc(C.Structure):
                 ("batch", C.c_int32), ("in_h", C.c_int32), ("in_w", C.c_int32), ("in_c", C.c_int32),
                 ("precision", C.c_int32), ("momentum", C.c_float), ("weight_decay", C.c_float),
                 ("bn_momentum", C.c_float), ("bn_eps", C.c_float), ("nesterov", C.c_int32),
-                ("accumulation_k", C.c_int32), ("fifo_capacity", C.c_int32)]
+                ("accumulation_k", C.c_int32), ("fifo_capacity", C.c_int32), ("compare_buffers", C.c_int32)]
 
 
 class PetraTensorInfo(C.Structure):
@@ -50,7 +51,7 @@ class PetraTensorInfo(C.Structure):
 
 class PetraMemoryReport(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("total", "params", "optimizer", "shadows", "fifo", "fifo_live",
-                                          "workspace")]
+                                          "workspace", "cmp_inputs", "cmp_stash")]
 
 
 class PetraTickReport(C.Structure):
@@ -66,7 +67,7 @@ class PetraPipelineDesc(C.Structure):
     _fields_ = [("n_stages", C.c_int32), ("stages", C.POINTER(PetraStageDesc)),
                 ("stage_rank", C.POINTER(C.c_int32)), ("rank", C.c_int32), ("world", C.c_int32),
                 ("seed", C.c_uint64), ("transport", C.c_int32), ("nccl_id", C.c_void_p),
-                ("local_group", C.c_int64), ("join_comm", C.c_int32)]
+                ("local_group", C.c_int64), ("join_comm", C.c_int32), ("wire", C.c_int32)]
 
 
 class PetraCommEntry(C.Structure):

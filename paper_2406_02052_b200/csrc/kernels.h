@@ -80,6 +80,18 @@ void stem_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, const __nv_bfloat
                    cudaStream_t st);
 
 // ---------------------------------------------------------------- batch norm / coupling
+// BN statistics still to be merged from a conv epilogue's partial rows (StatsRows at
+// `part`): the consuming BN pass (apply, backward reduce) merges the rows of its channel
+// tile in its prologue instead of a separate stats_finalize launch.  Block 0 of each
+// channel tile writes mean / invstd to global (for later passes) and, when rmean is set,
+// applies the running-statistics update.  part == nullptr: mean / invstd are final.
+struct StatsFold {
+  const float *part = nullptr;
+  int rows = 0, groups = 1, N = 0;  // partial rows, column groups, channels of the conv output
+  int64_t M = 0;                    // valid output rows (the statistics' count)
+  float eps = 1e-5f, mom = 0.1f;
+  float *rmean = nullptr, *rvar = nullptr;
+};
 size_t bn_partial_bytes(int64_t M, int C);
 size_t bn_counter_count(int C);  // zero-initialised unsigned counters a reduction needs
 template <typename TZ>
@@ -87,15 +99,16 @@ void bn_stats(const TZ *z, int64_t M, int C, float eps, float *mean, float *invs
               float mom, double *part, unsigned *counter, cudaStream_t st);
 // out_bf16 (nullable) is written padded when pH > 0: rows m = (b*pH + h)*pW + w go to the
 // interior of a zero-bordered [B][pH+2][pW+2][C] buffer
+// fold (nullable): statistics of z's columns [zc0, zc0 + C) still to be merged (StatsFold)
 template <typename TZ, typename TO>
 void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean, const float *invstd,
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
-              __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st);
+              __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st, const StatsFold *fold = nullptr);
 template <typename TZ>
 void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float *invstd, const float *gamma,
                    const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dst_in,
                    float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW, float *dgamma, float *dbeta,
-                   double *part, unsigned *counter, cudaStream_t st);
+                   double *part, unsigned *counter, cudaStream_t st, const StatsFold *fold = nullptr);
 // dz (fp32, nullable) and/or its bf16 copy (nullable: the tensor-core operand; padded
 // as in bn_apply when pH > 0)
 template <typename TZ>
@@ -127,6 +140,9 @@ void maxpool_fwd(const float *a, int B, int H, int W, int C, int Ho, int Wo, flo
 void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, int H, int W, int C, int Ho, int Wo,
                  float *da, cudaStream_t st);
 void f32_to_bf16(const float *x, __nv_bfloat16 *y, int64_t n, cudaStream_t st);
+void bf16_to_f32(const __nv_bfloat16 *x, float *y, int64_t n, cudaStream_t st);
+// x = float(bf16_rn(x)): the pipeline's bf16 wire format (petra_pipeline_desc.wire)
+void round_bf16_inplace(float *x, int64_t n, cudaStream_t st);
 // y = bf16(x) into the interior of a zero-bordered [B][H+2][W+2][C] buffer
 void f32_to_bf16_padded(const float *x, __nv_bfloat16 *y, int B, int H, int W, int C, cudaStream_t st);
 

@@ -404,6 +404,68 @@ __global__ void __launch_bounds__(256, 4) bn_bwd_dz_fixed_kernel(
 }
 
 
+// ---------------------------------------------------------------- statistics fold
+// Merge of a conv epilogue's BN partial rows (StatsFold; layout kernels.h StatsRows) for
+// channels [cb, cb + CT) of the conv output, in the prologue of the consuming BN pass
+// (instead of a stats_finalize launch).  Eight threads per channel (thread bits 0-2) take
+// rows j, j + 8, ... of the channel's column group and accumulate in fp64, shifted by the
+// group's first row mean m0:  A = sum n_r (m_r - m0),  B = sum n_r (m_r - m0)^2,
+// W = sum M2_r,  n = sum n_r;  the eight are combined by a fixed xor tree (deterministic).
+// mean = m0 + A / n, M2 = W + B - A^2 / n (the pairwise / Chan combination of (count,
+// mean, M2) triples written as sums); biased variance M2 / M for the normalisation,
+// unbiased M2 / (M - 1) for the running EMA (reading c9).  Results go to s_mu / s_is;
+// `writer` (block 0 of the channel tile) also stores mean / invstd and updates the
+// running statistics.  Ends with __syncthreads.  blockDim.x must be a multiple of 32.
+__device__ void fold_stats(const StatsFold &f, int cb, int CT, float *s_mu, float *s_is, bool writer,
+                           float *__restrict__ mean, float *__restrict__ invstd) {
+  const int t = threadIdx.x;
+  const float *cnt = f.part + (size_t)f.rows * f.N * 2;
+  const int gsz = f.N / f.groups;
+  for (int base = 0; base < CT * 8; base += blockDim.x) {  // same trip count in every thread
+    const int slot = base + t, cl = slot >> 3, sub = slot & 7, c = cb + cl;
+    double A = 0, Bq = 0, Wm = 0, n = 0, m0 = 0;
+    if (cl < CT) {
+      const int grp = c / gsz, nr = (f.rows - grp + f.groups - 1) / f.groups;
+      m0 = f.part[((size_t)grp * f.N + c) * 2];
+      for (int j = sub; j < nr; j += 8) {
+        const int r = grp + j * f.groups;
+        const float2 u = __ldcg(reinterpret_cast<const float2 *>(f.part + ((size_t)r * f.N + c) * 2));
+        const double nr_ = __ldcg(cnt + r), d = (double)u.x - m0;
+        A += nr_ * d;
+        Bq += nr_ * d * d;
+        Wm += u.y;
+        n += nr_;
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      A += __shfl_xor_sync(0xffffffffu, A, o);
+      Bq += __shfl_xor_sync(0xffffffffu, Bq, o);
+      Wm += __shfl_xor_sync(0xffffffffu, Wm, o);
+      n += __shfl_xor_sync(0xffffffffu, n, o);
+    }
+    if (cl < CT && sub == 0) {
+      const double mu = n > 0 ? m0 + A / n : 0.0;
+      double M2 = n > 0 ? Wm + Bq - A * A / n : 0.0;
+      if (M2 < 0.0) M2 = 0.0;
+      const double var = f.M > 0 ? M2 / (double)f.M : 0.0;  // n == M: every valid output row once
+      const float is = (float)(1.0 / sqrt(var + (double)f.eps));
+      s_mu[cl] = (float)mu;
+      s_is[cl] = is;
+      if (writer) {
+        mean[c] = (float)mu;
+        invstd[c] = is;
+        if (f.rmean) {
+          const double unb = f.M > 1 ? M2 / (double)(f.M - 1) : var;
+          f.rmean[c] = (float)((1.0 - f.mom) * f.rmean[c] + f.mom * mu);
+          f.rvar[c] = (float)((1.0 - f.mom) * f.rvar[c] + f.mom * unb);
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- TMA-staged BN passes
 // BN apply, TMA-staged per channel tile (bitwise the arithmetic of
 // bn_apply_fixed_kernel): thread (cj, rgi) keeps channels c0 + 4cj .. +3 and their
@@ -414,9 +476,11 @@ __global__ void __launch_bounds__(256) bn_apply_tma_kernel(
     const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmA, int has_acc, int64_t M, int C,
     int CT, int TPR, int RG, int64_t rpb, int Rc, int zc0, const float *__restrict__ mean,
     const float *__restrict__ invstd, const float *__restrict__ gamma, const float *__restrict__ beta, int relu,
-    float sign, float *__restrict__ out, __nv_bfloat16 *__restrict__ out_bf16, int pH, int pW) {
+    float sign, float *__restrict__ out, __nv_bfloat16 *__restrict__ out_bf16, int pH, int pW,
+    const StatsFold fold) {
   pdl_wait_trigger();
   __shared__ uint64_t full[2];
+  __shared__ float s_mu[128], s_is[128];
   extern __shared__ __align__(128) uint8_t ring[];
   const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
   const int c0 = blockIdx.y * CT;
@@ -431,13 +495,6 @@ __global__ void __launch_bounds__(256) bn_apply_tma_kernel(
     tc::fence_mbar_init();
   }
   __syncthreads();
-  float a[4], mu[4], be[4];  // BN constants of z's columns zc0 + c .. (the split-halves view)
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    a[k] = mine ? gamma[zc0 + c + k] * invstd[zc0 + c + k] : 0.f;
-    mu[k] = mine ? mean[zc0 + c + k] : 0.f;
-    be[k] = mine ? beta[zc0 + c + k] : 0.f;
-  }
   const int64_t nchunk = (r1 - r0 + Rc - 1) / Rc;
   auto issue = [&](int64_t k, int s) {
     const int y = (int)(r0 + k * Rc);
@@ -446,7 +503,18 @@ __global__ void __launch_bounds__(256) bn_apply_tma_kernel(
     tc::tma_load_2d(st, &tmZ, &full[s], c0, y);
     if (has_acc) tc::tma_load_2d(st + zb, &tmA, &full[s], c0, y);
   };
-  if (t == 0 && nchunk > 0) issue(0, 0);
+  if (t == 0 && nchunk > 0) issue(0, 0);  // the first chunk streams in while the statistics merge
+  if (fold.part)  // this tile's statistics from the conv epilogue's partial rows
+    fold_stats(fold, zc0 + c0, min(CT, C - c0), s_mu, s_is, blockIdx.x == 0, const_cast<float *>(mean),
+               const_cast<float *>(invstd));
+  float a[4], mu[4], be[4];  // BN constants of z's columns zc0 + c .. (the split-halves view)
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float is = !mine ? 0.f : fold.part ? s_is[4 * cj + k] : invstd[zc0 + c + k];
+    a[k] = mine ? gamma[zc0 + c + k] * is : 0.f;
+    mu[k] = !mine ? 0.f : fold.part ? s_mu[4 * cj + k] : mean[zc0 + c + k];
+    be[k] = mine ? beta[zc0 + c + k] : 0.f;
+  }
   uint32_t ph0 = 0, ph1 = 0;
   int s = 0;
   for (int64_t k = 0; k < nchunk; ++k, s ^= 1) {
@@ -592,11 +660,12 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
     const float *__restrict__ mean, const float *__restrict__ invstd, const float *__restrict__ gamma,
     const float *__restrict__ beta, int relu, int has_dst, float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW,
     double *__restrict__ part, unsigned *__restrict__ counter, float *__restrict__ dgamma,
-    float *__restrict__ dbeta) {
+    float *__restrict__ dbeta, const StatsFold fold) {
   pdl_wait_trigger();
   constexpr int RT = RT_BWD;
   __shared__ double sh[RT][4];
   __shared__ uint64_t full[2];
+  __shared__ float s_mu[128], s_is[128];
   extern __shared__ __align__(128) uint8_t ring[];
   const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
   const int c0 = blockIdx.y * CT;
@@ -626,15 +695,18 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
     }
     if (has_dst) tc::tma_load_2d(st + zb + fb, &tmD, &full[s], c0, y);
   };
+  if (t == 0 && nchunk > 0) issue(0, 0);  // the first chunk streams in while the statistics merge
+  if (fold.part)
+    fold_stats(fold, c0, min(CT, C - c0), s_mu, s_is, blockIdx.x == 0, const_cast<float *>(mean),
+               const_cast<float *>(invstd));
   float mu[4], is[4], ga[4], be[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    mu[k] = mine ? mean[c + k] : 0.f;
-    is[k] = mine ? invstd[c + k] : 0.f;
+    mu[k] = !mine ? 0.f : fold.part ? s_mu[4 * cj + k] : mean[c + k];
+    is[k] = !mine ? 0.f : fold.part ? s_is[4 * cj + k] : invstd[c + k];
     ga[k] = mine ? gamma[c + k] : 0.f;
     be[k] = mine ? beta[c + k] : 0.f;
   }
-  if (t == 0 && nchunk > 0) issue(0, 0);
   uint32_t ph0 = 0, ph1 = 0;
   int s = 0;
   for (int64_t k = 0; k < nchunk; ++k, s ^= 1) {
@@ -843,6 +915,14 @@ inline unsigned chan_grid(int64_t M, int C) {
   return (unsigned)std::max<int64_t>(q, g / q * q);
 }
 
+// the fold as a separate stats_finalize launch (the passes without a fused prologue)
+void finalize_fold(const StatsFold &f, float *mean, float *invstd, cudaStream_t st) {
+  StatsRows r;
+  r.rows = f.rows;
+  r.groups = f.groups;
+  bn_stats_from_partials(f.part, r, f.N, f.M, f.eps, mean, invstd, f.rmean, f.rvar, f.mom, st);
+}
+
 }  // namespace
 
 size_t bn_partial_bytes(int64_t M, int C) {
@@ -866,7 +946,7 @@ template void bn_stats<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int, float
 template <typename TZ, typename TO>
 void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean, const float *invstd,
               const float *gamma, const float *beta, int relu, float sign, const float *acc, TO *out,
-              __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st) {
+              __nv_bfloat16 *out_bf16, int pH, int pW, cudaStream_t st, const StatsFold *fold) {
   static const bool tma_on = env_int("PETRA_BN_TMA_APPLY", 1) != 0;
   if (tma_on && std::is_same<TO, float>::value && C % 8 == 0 && (uintptr_t)(z + zc0) % 16 == 0 &&
       ((size_t)ldz * sizeof(TZ)) % 16 == 0 && (uintptr_t)acc % 16 == 0 && M < ((int64_t)1 << 31)) {
@@ -889,11 +969,12 @@ void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean
       const CUtensorMap ta = acc ? plain_map_2d(acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc) : tz;
       launch_k(bn_apply_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), 256, 2 * sbytes, st, tz, ta, acc ? 1 : 0, M, C, g.CT,
                g.TPR, g.RG, g.rpb, Rc, zc0, mean, invstd, gamma, beta, relu, sign, reinterpret_cast<float *>(out), out_bf16,
-               pH, pW);
+               pH, pW, fold ? *fold : StatsFold{});
       PETRA_LAUNCH_CHECK();
       return;
     }
   }
+  if (fold) finalize_fold(*fold, const_cast<float *>(mean), const_cast<float *>(invstd), st);  // the register kernels read final statistics
   const unsigned cg = (ldz % 4 == 0 && zc0 % 4 == 0) ? chan_grid(M, C) : 0;
   if (cg && std::is_same<TO, float>::value && M < ((int64_t)1 << 31) / 4) {
     launch_k(bn_apply_fixed_kernel<TZ>, cg, 256, 0, st, (int)M, C, z, ldz, zc0, mean, invstd, gamma, beta, relu, sign,
@@ -906,16 +987,17 @@ void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean
 }
 template void bn_apply<float, float>(int64_t, int, const float *, int, int, const float *, const float *,
                                      const float *, const float *, int, float, const float *, float *,
-                                     __nv_bfloat16 *, int, int, cudaStream_t);
+                                     __nv_bfloat16 *, int, int, cudaStream_t, const StatsFold *);
 template void bn_apply<__nv_bfloat16, float>(int64_t, int, const __nv_bfloat16 *, int, int, const float *,
                                              const float *, const float *, const float *, int, float,
-                                             const float *, float *, __nv_bfloat16 *, int, int, cudaStream_t);
+                                             const float *, float *, __nv_bfloat16 *, int, int, cudaStream_t,
+                                             const StatsFold *);
 
 template <typename TZ>
 void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float *invstd, const float *gamma,
                    const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dst_in,
                    float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW, float *dgamma, float *dbeta,
-                   double *part, unsigned *counter, cudaStream_t st) {
+                   double *part, unsigned *counter, cudaStream_t st, const StatsFold *fold) {
   RedGeom g = red_geom(M, C, RT_BWD);
   static const bool tma_on = env_int("PETRA_BN_TMA_REDUCE", 1) != 0;
   const bool aligned = (uintptr_t)z % 16 == 0 && (uintptr_t)dy0 % 16 == 0 && (uintptr_t)dst_in % 16 == 0 &&
@@ -946,11 +1028,12 @@ void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float
       launch_k(bn_bwd_reduce_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 2 * sbytes, st, tz, ty, td, ty1, s0, M, C,
                g.CT,
                g.TPR, g.RG, g.rpb, g.nrb, Rc, mean, invstd, gamma, beta, relu, dst_out ? 1 : 0, dst_out, dst_bf16, pH,
-               pW, part, counter, dgamma, dbeta);
+               pW, part, counter, dgamma, dbeta, fold ? *fold : StatsFold{});
       PETRA_LAUNCH_CHECK();
       return;
     }
   }
+  if (fold) finalize_fold(*fold, const_cast<float *>(mean), const_cast<float *>(invstd), st);
   launch_k(bn_bwd_reduce_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 0, st, z, M, C, g.CT, g.TPR, g.RG, g.rpb, g.nrb, mean,
                                                                  invstd, gamma, beta, relu, dy0, dy1, cs, dst_in,
                                                                  dst_out, dst_bf16, pH, pW, part, counter, dgamma,
@@ -959,11 +1042,12 @@ void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float
 }
 template void bn_bwd_reduce<float>(const float *, int64_t, int, const float *, const float *, const float *,
                                    const float *, int, const float *, const float *, int, const float *, float *,
-                                   __nv_bfloat16 *, int, int, float *, float *, double *, unsigned *, cudaStream_t);
+                                   __nv_bfloat16 *, int, int, float *, float *, double *, unsigned *, cudaStream_t,
+                                   const StatsFold *);
 template void bn_bwd_reduce<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int, const float *, const float *,
                                            const float *, const float *, int, const float *, const float *, int,
                                            const float *, float *, __nv_bfloat16 *, int, int, float *, float *,
-                                           double *, unsigned *, cudaStream_t);
+                                           double *, unsigned *, cudaStream_t, const StatsFold *);
 
 template <typename TZ>
 void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *invstd, const float *gamma,

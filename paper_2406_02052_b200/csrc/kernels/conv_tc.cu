@@ -352,7 +352,28 @@ __global__ void __launch_bounds__(256) stats_finalize_kernel(const float *__rest
     // rows of this column's group: r = grp, grp + groups, ... (nr rows)
     const int grp = c / (N / groups), nr = (P - grp + groups - 1) / groups;
     m0 = part[((size_t)grp * N + c) * 2];
-    for (int j = w; j < nr; j += 8) {
+    int j = w;
+    // four rows' loads in flight before their (in-order) accumulation: the merge is
+    // L2-latency bound
+    for (; j + 24 < nr; j += 32) {
+      float2 u[4];
+      float cn[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = grp + (j + 8 * k) * groups;
+        u[k] = *reinterpret_cast<const float2 *>(part + ((size_t)r * N + c) * 2);
+        cn[k] = cnt[r];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double nr_ = cn[k], d = (double)u[k].x - m0;
+        A += nr_ * d;
+        Bq += nr_ * d * d;
+        Wm += u[k].y;
+        n += nr_;
+      }
+    }
+    for (; j < nr; j += 8) {
       const int r = grp + j * groups;
       const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)r * N + c) * 2);
       const double nr_ = cnt[r], d = (double)u.x - m0;
@@ -581,6 +602,47 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+// out[i] = sum over splits z of part[z * n + i], float4 columns: a block takes 32 float4
+// columns, its 8 warps take splits w, w + 8, ... (up to four 16-byte loads in flight per
+// thread before the adds), and the 8 warp sums are added in warp order through smem --
+// a fixed order (deterministic) with every split of a column read in one round trip
+// per four splits per warp instead of per four splits per thread
+__global__ void __launch_bounds__(256) splitk_sum4_kernel(const float4 *__restrict__ part, int splits, int64_t n4,
+                                                         float4 *__restrict__ out) {
+  pdl_wait_trigger();
+  __shared__ float4 sh[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < n4) {
+    const float4 *p = part + i;
+    int z = w;
+    for (; z + 24 < splits; z += 32) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcg(p + (int64_t)(z + 8 * u) * n4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+      }
+    }
+    for (; z < splits; z += 8) {
+      const float4 v = __ldcg(p + (int64_t)z * n4);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+  }
+  sh[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && i < n4) {
+    float4 s = sh[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+      s.x += sh[k][lane].x; s.y += sh[k][lane].y; s.z += sh[k][lane].z; s.w += sh[k][lane].w;
+    }
+    out[i] = s;
   }
 }
 
@@ -1056,6 +1118,14 @@ CUtensorMap plain_map_2d_strided(const void *base, CUtensorMapDataType dt, int e
 
 
 void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st) {
+  static const bool v4 = env_int("PETRA_SPLITK_V4", 1) != 0;
+  if (v4 && n % 4 == 0 && (uintptr_t)part % 16 == 0 && (uintptr_t)out % 16 == 0) {
+    const int64_t n4 = n / 4;
+    launch_k(splitk_sum4_kernel, (unsigned)cdiv(n4, 32), 256, 0, st, reinterpret_cast<const float4 *>(part), splits, n4,
+             reinterpret_cast<float4 *>(out));
+    PETRA_LAUNCH_CHECK();
+    return;
+  }
   launch_k(splitk_sum_kernel, (unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st, part, splits, n, out);
   PETRA_LAUNCH_CHECK();
 }

@@ -382,6 +382,31 @@ __global__ void f32_to_bf16_kernel(const float *__restrict__ x, __nv_bfloat16 *_
   for (int64_t i = t0; i < n; i += stride) y[i] = __float2bfloat16_rn(x[i]);
 }
 
+// bf16 wire format of the pipeline messages: x = float(bf16_rn(x)) in place (mode 0),
+// or the exact widening y = float(x_bf16) (mode 1, unpacking a received message)
+__global__ void round_bf16_kernel(float *__restrict__ x, int64_t n) {
+  pdl_wait_trigger();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((n & 3) == 0 && ((uintptr_t)x & 15) == 0) {
+    float4 *x4 = reinterpret_cast<float4 *>(x);
+    for (int64_t i = t0; i < n / 4; i += stride) {
+      float4 v = x4[i];
+      v.x = __bfloat162float(__float2bfloat16_rn(v.x));
+      v.y = __bfloat162float(__float2bfloat16_rn(v.y));
+      v.z = __bfloat162float(__float2bfloat16_rn(v.z));
+      v.w = __bfloat162float(__float2bfloat16_rn(v.w));
+      x4[i] = v;
+    }
+    return;
+  }
+  for (int64_t i = t0; i < n; i += stride) x[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
+}
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16 *__restrict__ x, float *__restrict__ y, int64_t n) {
+  pdl_wait_trigger();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < n; i += stride) y[i] = __bfloat162float(x[i]);
+}
+
 // interior of a zero-bordered [B][H+2][W+2][C] bf16 buffer (C % 4 == 0)
 __global__ void f32_to_bf16_padded_kernel(const float4 *__restrict__ x, uint2 *__restrict__ y, int B, int H, int W,
                                           int C4) {
@@ -490,6 +515,17 @@ void f32_to_bf16_padded(const float *x, __nv_bfloat16 *y, int B, int H, int W, i
   const int C4 = C / 4;
   launch_k(f32_to_bf16_padded_kernel, (unsigned)std::min<int64_t>((int64_t)B * H, 16 * kNumSMs), 256, 0, st, 
       reinterpret_cast<const float4 *>(x), reinterpret_cast<uint2 *>(y), B, H, W, C4);
+  PETRA_LAUNCH_CHECK();
+}
+
+void round_bf16_inplace(float *x, int64_t n, cudaStream_t st) {
+  const bool v4 = (n & 3) == 0 && ((uintptr_t)x & 15) == 0;
+  launch_k(round_bf16_kernel, ew_grid(v4 ? n / 4 : n), 256, 0, st, x, n);
+  PETRA_LAUNCH_CHECK();
+}
+
+void bf16_to_f32(const __nv_bfloat16 *x, float *y, int64_t n, cudaStream_t st) {
+  launch_k(bf16_to_f32_kernel, ew_grid(n), 256, 0, st, x, y, n);
   PETRA_LAUNCH_CHECK();
 }
 

@@ -53,6 +53,7 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
       transport_(d.transport),
       group_(d.local_group),
       join_comm_(d.join_comm != 0),
+      wire_(d.wire),
       sched_(d.n_stages, std::vector<int>(d.stage_rank, d.stage_rank + d.n_stages), nonrev_counts(d), d.rank,
              accum_ks(d)) {
   if (J_ < 1 || J_ > PETRA_MAX_STAGES) throw PetraError(PETRA_E_ARG, "n_stages out of range");
@@ -61,6 +62,7 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
     throw PetraError(PETRA_E_ARG, "unknown transport");
   if (transport_ == PETRA_TRANSPORT_NCCL && !d.nccl_id) throw PetraError(PETRA_E_ARG, "NCCL transport needs nccl_id");
   if (transport_ == PETRA_TRANSPORT_LOCAL && group_ == 0) throw PetraError(PETRA_E_ARG, "LOCAL transport needs local_group");
+  if (wire_ != PETRA_WIRE_FP32 && wire_ != PETRA_WIRE_BF16) throw PetraError(PETRA_E_ARG, "unknown wire format");
   stages_.resize(J_ + 2);
   fwd_.resize(J_ + 2);
   bwd_.resize(J_ + 2);
@@ -112,6 +114,20 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
     if (j1 < J_) {
       const Shape &out = stages_[j1]->out_shape();
       for (int k = 0; k < 4; ++k) ghost_bwd_[p].x[k] = dalloc(out.numel() * sizeof(float));
+    }
+  }
+  if (lib_transport() && wire_ == PETRA_WIRE_BF16) {  // 2-byte images of the cross-rank messages
+    for (int p = 0; p < 2; ++p) {
+      if (j1 < J_) {  // forward send of j1, backward receive for j1
+        const int64_t n = stages_[j1]->out_shape().numel();
+        for (int k = 0; k < 2; ++k) wsend_[DIR_FWD][p].x[k] = dalloc(n * sizeof(__nv_bfloat16));
+        for (int k = 0; k < 4; ++k) wrecv_[DIR_BWD][p].x[k] = dalloc(n * sizeof(__nv_bfloat16));
+      }
+      if (j0 > 1) {  // forward receive for j0, backward send of j0
+        const int64_t n = stages_[j0]->in_shape().numel();
+        for (int k = 0; k < 2; ++k) wrecv_[DIR_FWD][p].x[k] = dalloc(n * sizeof(__nv_bfloat16));
+        for (int k = 0; k < 4; ++k) wsend_[DIR_BWD][p].x[k] = dalloc(n * sizeof(__nv_bfloat16));
+      }
     }
   }
   if (lib_transport()) {
@@ -284,6 +300,7 @@ void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labe
       }
     }
     if (j == J_) a.loss = loss;
+    a.round_msgs = wire_ == PETRA_WIRE_BF16;
     if (lib_transport()) {  // cross-rank synchronisation points (header comment)
       const int j0 = sched_.first_local(), j1 = sched_.last_local();
       if (a.fwd) {
@@ -354,20 +371,38 @@ void Pipeline::exchange(int64_t t, std::vector<bool> &used) {
     }
     NvtxRange nr(dir == DIR_FWD ? "exchange fwd (x1, x2, labels -> rank+1)" : "exchange bwd (x~, delta -> rank-1)");
     ProfScope ps(dir == DIR_FWD ? "exchange_fwd" : "exchange_bwd", cs, 0.0, 0.0);
+    const bool w16 = wire_ == PETRA_WIRE_BF16;
+    const int nt = dir == DIR_FWD ? 2 : 4;  // message tensors (labels travel as int32)
     if (transport_ == PETRA_TRANSPORT_NCCL) {
       const NcclApi &nc = nccl();
+      if (w16)  // pack: the values are bf16-exact (rounded by the producing stage)
+        for (const Schedule::Comm *c : ops)
+          if (c->send) {
+            Msg &m = dir == DIR_FWD ? fwd_[j1][p] : bwd_[j0][p];
+            for (int k = 0; k < nt; ++k)
+              f32_to_bf16(m.x[k]->as<float>(), wsend_[dir][p].x[k]->as<__nv_bfloat16>(),
+                          (int64_t)(m.x[k]->bytes / sizeof(float)), cs);
+          }
       PETRA_NCCL(nc.GroupStart());
       for (const Schedule::Comm *c : ops) {
         Msg &m = dir == DIR_FWD ? (c->send ? fwd_[j1][p] : ghost_fwd_[p]) : (c->send ? bwd_[j0][p] : ghost_bwd_[p]);
-        const int n = dir == DIR_FWD ? 2 : 4;
-        for (int k = 0; k <= n; ++k) {
-          const DevPtr &b = k < n ? m.x[k] : m.labels;
+        Msg &wm = c->send ? wsend_[dir][p] : wrecv_[dir][p];
+        for (int k = 0; k <= nt; ++k) {
+          const DevPtr &b = k < nt ? (w16 ? wm.x[k] : m.x[k]) : m.labels;
           if (!b) continue;
           if (c->send) PETRA_NCCL(nc.Send(b->p, b->bytes, ncclUint8, c->peer, nccl_comm_, cs));
           else PETRA_NCCL(nc.Recv(b->p, b->bytes, ncclUint8, c->peer, nccl_comm_, cs));
         }
       }
       PETRA_NCCL(nc.GroupEnd());
+      if (w16)  // unpack into the fp32 ghost buffers (exact widening)
+        for (const Schedule::Comm *c : ops)
+          if (!c->send) {
+            Msg &g = dir == DIR_FWD ? ghost_fwd_[p] : ghost_bwd_[p];
+            for (int k = 0; k < nt; ++k)
+              bf16_to_f32(wrecv_[dir][p].x[k]->as<__nv_bfloat16>(), g.x[k]->as<float>(),
+                          (int64_t)(g.x[k]->bytes / sizeof(float)), cs);
+          }
     } else {  // LOCAL: push into the receiver's ghost buffer once it released it
       for (const Schedule::Comm *c : ops) {
         if (!c->send) continue;
@@ -376,12 +411,19 @@ void Pipeline::exchange(int64_t t, std::vector<bool> &used) {
         PETRA_CUDA(cudaStreamWaitEvent(cs, pr->tdone_[rj][q], 0));
         Msg &src = dir == DIR_FWD ? fwd_[j1][p] : bwd_[j0][p];
         Msg &dst = dir == DIR_FWD ? pr->ghost_fwd_[p] : pr->ghost_bwd_[p];
-        const int n = dir == DIR_FWD ? 2 : 4;
-        for (int k = 0; k <= n; ++k) {
-          const DevPtr &a = k < n ? src.x[k] : src.labels;
-          const DevPtr &b = k < n ? dst.x[k] : dst.labels;
+        for (int k = 0; k <= nt; ++k) {
+          const DevPtr &a = k < nt ? src.x[k] : src.labels;
+          const DevPtr &b = k < nt ? dst.x[k] : dst.labels;
           if (!a || !b) continue;
           if (a->bytes != b->bytes) throw PetraError(PETRA_E_SHAPE, "LOCAL transport: message sizes differ");
+          if (w16 && k < nt) {  // the same 2-byte wire as NCCL: pack, move, widen
+            const DevPtr &ws = wsend_[dir][p].x[k], &wr = pr->wrecv_[dir][p].x[k];
+            const int64_t n = (int64_t)(a->bytes / sizeof(float));
+            f32_to_bf16(a->as<float>(), ws->as<__nv_bfloat16>(), n, cs);
+            PETRA_CUDA(cudaMemcpyAsync(wr->p, ws->p, ws->bytes, cudaMemcpyDeviceToDevice, cs));
+            bf16_to_f32(wr->as<__nv_bfloat16>(), b->as<float>(), n, cs);
+            continue;
+          }
           PETRA_CUDA(cudaMemcpyAsync(b->p, a->p, a->bytes, cudaMemcpyDeviceToDevice, cs));
         }
       }

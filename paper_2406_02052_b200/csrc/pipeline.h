@@ -32,6 +32,10 @@ class Pipeline {
   int transport_ = PETRA_TRANSPORT_NONE;
   int64_t group_ = 0;
   bool join_comm_ = true;
+  int wire_ = PETRA_WIRE_FP32;
+  // bf16 wire: 2-byte images of the cross-rank messages ([dir][parity]; send = this rank's
+  // outgoing message, recv = the incoming one before it is widened into the ghost buffer)
+  Msg wsend_[2][2], wrecv_[2][2];
   Schedule sched_;
   std::vector<petra_stage_desc> descs_;
   std::vector<std::unique_ptr<Stage>> stages_;

@@ -107,6 +107,9 @@ Stage::~Stage() {
   if (side_) cudaStreamDestroy(side_);
   if (fork_) cudaEventDestroy(fork_);
   if (join_) cudaEventDestroy(join_);
+  if (wg_) cudaStreamDestroy(wg_);
+  if (wg_fork_) cudaEventDestroy(wg_fork_);
+  if (wg_join_) cudaEventDestroy(wg_join_);
   if (lr_host_) cudaFreeHost(lr_host_);
 }
 
@@ -175,7 +178,7 @@ void Stage::build() {
   const int B = desc_.batch;
   Shape cur{B, desc_.in_h, desc_.in_w, desc_.in_c};
   in_ = cur;
-  size_t max_part = 0, max_ws = 0;
+  size_t max_part = 0, max_spart = 0, max_ws = 0;
   std::vector<std::vector<Layer *>> unit_layers(units_.size());
   struct Pending {
     Layer *L;
@@ -311,7 +314,7 @@ void Stage::build() {
   }
   for (auto &p : layers) {
     max_part = std::max(max_part, bn_partial_bytes(p.L->g.M(), p.L->g.Co));
-    max_part = std::max(max_part, (size_t)kNumSMs * 4 * (p.L->g.Co * 2 + 1) * sizeof(float));  // fused conv stats
+    max_spart = std::max(max_spart, (size_t)kNumSMs * 4 * (p.L->g.Co * 2 + 1) * sizeof(float));  // fused conv stats
     max_ws = std::max(max_ws, conv_wgrad_simt_workspace(p.L->g));
     if (tc_)
       for (int mode = 0; mode < 3; ++mode) max_ws = std::max(max_ws, conv_tc_workspace(p.L->g, mode));
@@ -321,6 +324,7 @@ void Stage::build() {
   for (auto &p : layers) max_ctr = std::max(max_ctr, bn_counter_count(p.L->g.Co));
   for (int c = 0; c < 2; ++c) {
     part_[c] = dalloc(std::max<size_t>(max_part, 16));
+    spart_[c] = dalloc(std::max<size_t>(max_spart, 16));
     counters_[c] = dalloc(max_ctr * sizeof(unsigned));
     PETRA_CUDA(cudaMemset(counters_[c]->p, 0, max_ctr * sizeof(unsigned)));
     wgrad_ws_[c] = dalloc(std::max<size_t>(max_ws, 16));
@@ -328,6 +332,21 @@ void Stage::build() {
   PETRA_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
   PETRA_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
   PETRA_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
+  if (tc_ && env_int("PETRA_WGRAD_STREAM", 1)) {
+    PETRA_CUDA(cudaStreamCreateWithFlags(&wg_, cudaStreamNonBlocking));
+    PETRA_CUDA(cudaEventCreateWithFlags(&wg_fork_, cudaEventDisableTiming));
+    PETRA_CUDA(cudaEventCreateWithFlags(&wg_join_, cudaEventDisableTiming));
+    wg_ws_ = dalloc(std::max<size_t>(max_ws, 16));
+  }
+  // Table 3 comparison buffers (memory measurement; numerics unchanged)
+  if (desc_.compare_buffers & PETRA_CMP_INPUTS) {
+    const bool own_fifo = !units_.empty() && units_[0].d.kind != PETRA_UNIT_REV;  // PETRA buffers these already
+    if (!own_fifo)
+      for (int s = 0; s < std::max(1, desc_.fifo_capacity); ++s)
+        for (int h = 0; h < 2; ++h) cmp_in_[h].push_back(dalloc(in_.numel() * sizeof(float)));
+  }
+  if (desc_.compare_buffers & PETRA_CMP_STASH)
+    for (int s = 0; s < desc_.fifo_capacity - 1; ++s) cmp_stash_.push_back(dalloc(theta_->bytes));
   lr_dev_ = dalloc(sizeof(float));
   PETRA_CUDA(cudaMallocHost(&lr_host_, kLrRing * sizeof(float)));
   if (tc_) conv_tc_prepare();
@@ -489,8 +508,11 @@ void Stage::memory(petra_memory_report *r) const {
     r->fifo += all;
     r->fifo_live += slot * (uint64_t)u.fifo.size;
   }
+  for (int h = 0; h < 2; ++h)
+    for (auto &p : cmp_in_[h]) r->cmp_inputs += b(p);
+  for (auto &p : cmp_stash_) r->cmp_stash += b(p);
   r->total = alloc_bytes_;
-  r->workspace = r->total - r->params - r->optimizer - r->shadows - r->fifo;
+  r->workspace = r->total - r->params - r->optimizer - r->shadows - r->fifo - r->cmp_inputs - r->cmp_stash;
 }
 
 int Stage::fifo_depth() const {
@@ -532,15 +554,15 @@ void Stage::enqueue_update(int mode, cudaStream_t st) {
 static void apply_bn(int64_t M, int C, const void *z, bool z16, int ldz, int zc0, const float *mean,
                      const float *invstd, const float *gamma, const float *beta, int relu, float sign,
                      const float *acc, float *out, __nv_bfloat16 *out_bf16, cudaStream_t st, int pH = 0,
-                     int pW = 0) {
+                     int pW = 0, const StatsFold *fold = nullptr) {
   ProfScope ps("bn_apply", st, 0.0,
                (double)M * C * ((z16 ? 2.0 : 4.0) + (acc ? 4.0 : 0.0) + (out ? 4.0 : 0.0) + (out_bf16 ? 2.0 : 0.0)));
   if (z16)
     bn_apply<__nv_bfloat16, float>(M, C, static_cast<const __nv_bfloat16 *>(z), ldz, zc0, mean, invstd, gamma, beta,
-                                   relu, sign, acc, out, out_bf16, pH, pW, st);
+                                   relu, sign, acc, out, out_bf16, pH, pW, st, fold);
   else
     bn_apply<float, float>(M, C, static_cast<const float *>(z), ldz, zc0, mean, invstd, gamma, beta, relu, sign, acc,
-                           out, out_bf16, pH, pW, st);
+                           out, out_bf16, pH, pW, st, fold);
 }
 
 static double conv_flops(const ConvGeom &g) { return 2.0 * (double)g.M() * g.Co * g.K(); }
@@ -555,6 +577,7 @@ static double conv_bytes(const ConvGeom &g, int esz, int pass, int out_es, bool 
 }
 
 void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_ready, bool running) {
+  flush_fold(st);  // this conv's epilogue rewrites the context's partial rows
   const float *w = theta_->as<float>() + L.w_off;
   if (tc_ && stem_tc_supported(L.g)) {  // few input channels: gathered im2col from a 4-channel bf16 copy
     if (!x_bf16_ready) {
@@ -563,7 +586,7 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
     }
     ProfScope ps("conv_fwd_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2, PASS_FWD, L.z16 ? 2 : 4));
     L.stats_rows() = stem_fwd_tc(L.g, L.xbp(), w, L.z()->p, L.z16,
-                                 reinterpret_cast<float *>(part()->p), st);
+                                 reinterpret_cast<float *>(spart()->p), st);
     return;
   }
   bool tc = tc_ && conv_tc_supported(L.g, 0);
@@ -576,27 +599,47 @@ void Stage::conv_fwd(Layer &L, const float *x, cudaStream_t st, bool x_bf16_read
                conv_bytes(L.g, tc ? 2 : 4, PASS_FWD, L.z16 ? 2 : 4));
   if (tc) {
     L.stats_rows() = conv_fwd_tc(L.g, L.xbp(), L.xpad, L.w_bf16->as<__nv_bfloat16>(), L.z()->p, L.z16,
-                                 wgrad_ws()->as<float>(), reinterpret_cast<float *>(part()->p), st);
+                                 wgrad_ws()->as<float>(), reinterpret_cast<float *>(spart()->p), st);
   } else {
     conv_fwd_simt(L.g, x, w, L.z()->as<float>(), st, tc_);
   }
 }
 
+// the wgrads' stream back into `st` (before the update reads Delta)
+void Stage::join_wgrads(cudaStream_t st) {
+  if (!wg_active_) return;
+  PETRA_CUDA(cudaEventRecord(wg_join_, wg_));
+  PETRA_CUDA(cudaStreamWaitEvent(st, wg_join_, 0));
+  wg_active_ = false;
+}
+
 void Stage::conv_wgrad(Layer &L, const float *x, cudaStream_t st) {
   float *dw = grad_->as<float>() + L.w_off;
-  if (tc_ && stem_tc_supported(L.g)) {
+  const bool stem = tc_ && stem_tc_supported(L.g);
+  bool tc = tc_ && conv_tc_supported(L.g, 2);
+  float *ws = wgrad_ws()->as<float>();
+  // tensor-core wgrads read only the bf16 operands (L.xbp, L.dzb), which nothing later in
+  // the walk rewrites: off the critical path onto the wgrad stream (not in a profiled,
+  // serialised replay; SIMT wgrads read the fp32 input, which a later reconstruction may
+  // overwrite in place, and stay on `st`)
+  if ((stem || tc) && wg_ && !Prof::enabled) {
+    PETRA_CUDA(cudaEventRecord(wg_fork_, st));
+    PETRA_CUDA(cudaStreamWaitEvent(wg_, wg_fork_, 0));
+    st = wg_;
+    ws = wg_ws_->as<float>();
+    wg_active_ = true;
+  }
+  if (stem) {
     ProfScope ps("conv_wgrad_stem_tc", st, conv_flops(L.g), conv_bytes(L.g, 2, PASS_WGRAD, 4));
-    stem_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.xbp(), dw, wgrad_ws()->as<float>(), st);
+    stem_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.xbp(), dw, ws, st);
     return;
   }
-  bool tc = tc_ && conv_tc_supported(L.g, 2);
   ProfScope ps(tc ? "conv_wgrad_tc" : "conv_wgrad_simt", st, conv_flops(L.g),
                conv_bytes(L.g, tc ? 2 : 4, PASS_WGRAD, 4));
   if (tc) {
     // L.xb holds bf16(x) from the conv_fwd of this tick (forward or recomputation);
     // L.dzb was written in bf16 by bn_bwd_dz
-    conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.xbp(), L.xpad, dw,
-                  wgrad_ws()->as<float>(), st);
+    conv_wgrad_tc(L.g, L.dzb->as<__nv_bfloat16>(), L.dzpad, L.xbp(), L.xpad, dw, ws, st);
   } else {
     conv_wgrad_simt(L.g, L.dz->as<float>(), x, dw, wgrad_ws()->as<float>(), st, tc_);
   }
@@ -614,14 +657,53 @@ void Stage::conv_dgrad(Layer &L, const float *addend, float *out, cudaStream_t s
   }
 }
 
+// Statistics of a conv output whose epilogue wrote partial rows are merged by the BN
+// pass that consumes them (StatsFold, the pass's prologue); a fold not consumed before
+// the next conv epilogue of the context rewrites the rows is launched on its own.
+void Stage::flush_fold(cudaStream_t st) {
+  Layer *L = pending_[ctx_];
+  if (!L) return;
+  pending_[ctx_] = nullptr;
+  StatsFold &f = L->fold();
+  if (!f.part) return;
+  ProfScope ps("bn_stats_merge", st, 0.0, 8.0 * f.rows * L->g.Co / f.groups);
+  StatsRows r;
+  r.rows = f.rows;
+  r.groups = f.groups;
+  bn_stats_from_partials(f.part, r, f.N, f.M, f.eps, L->mean()->as<float>(), L->invstd()->as<float>(), f.rmean,
+                         f.rvar, f.mom, st);
+  f = StatsFold{};
+}
+
+const StatsFold *Stage::take_fold(Layer &L) {
+  if (pending_[ctx_] != &L || !L.fold().part) return nullptr;
+  pending_[ctx_] = nullptr;
+  fold_tmp_[ctx_] = L.fold();
+  L.fold() = StatsFold{};
+  return &fold_tmp_[ctx_];
+}
+
 void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
   float *b = bufs_->as<float>();
   if (L.stats_rows().rows > 0) {  // sums already produced by the tensor-core conv epilogue
-    ProfScope ps("bn_stats_merge", st, 0.0, 8.0 * L.stats_rows().rows * L.g.Co / L.stats_rows().groups);
-    bn_stats_from_partials(reinterpret_cast<const float *>(part()->p), L.stats_rows(), L.g.Co, L.g.M(), desc_.bn_eps,
-                           L.mean()->as<float>(), L.invstd()->as<float>(), running ? b + L.rm_off : nullptr,
-                           running ? b + L.rv_off : nullptr, desc_.bn_momentum, st);
+    flush_fold(st);
+    StatsFold f;
+    f.part = reinterpret_cast<const float *>(spart()->p);
+    f.rows = L.stats_rows().rows;
+    f.groups = L.stats_rows().groups;
+    f.N = L.g.Co;
+    f.M = L.g.M();
+    f.eps = desc_.bn_eps;
+    f.mom = desc_.bn_momentum;
+    f.rmean = running ? b + L.rm_off : nullptr;
+    f.rvar = running ? b + L.rv_off : nullptr;
+    L.fold() = f;
     L.stats_rows() = StatsRows{};
+    pending_[ctx_] = &L;
+    // off by default: every block of the consuming pass merging the partial rows of its
+    // channel tile costs more than the launch it saves (measured)
+    static const bool fold_on = env_int("PETRA_STATS_FOLD", 0) != 0;
+    if (!fold_on) flush_fold(st);
     return;
   }
   ProfScope ps("bn_stats", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co);
@@ -653,7 +735,7 @@ void Stage::branch_forward(std::vector<Layer> &phi, const float *x, bool running
       const bool need32 = !ready || !conv_tc_supported(N.g, 2);
       apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(), L.invstd()->as<float>(),
                th + L.g_off, th + L.b_off, 1, 1.f, nullptr, need32 ? L.a()->as<float>() : nullptr,
-               ready ? N.xbp() : nullptr, st, N.xpad ? N.g.H : 0, N.g.W);
+               ready ? N.xbp() : nullptr, st, N.xpad ? N.g.H : 0, N.g.W, take_fold(L));
       x = L.a()->as<float>();
     }
   }
@@ -667,17 +749,19 @@ void Stage::layer_bwd(Layer &L, const float *dy0, const float *dy1, int cs, cons
   const float *th = theta_->as<float>();
   float *gr = grad_->as<float>();
   double n = (double)L.g.M() * L.g.Co;
+  const StatsFold *fold = take_fold(L);
   {
   ProfScope ps("bn_bwd_reduce", st, 0.0, n * ((L.z16 ? 2.0 : 4.0) + 4.0 + (dst_out ? 8.0 : 0.0) + (ob.p ? 2.0 : 0.0)));
   if (L.z16)
     bn_bwd_reduce<__nv_bfloat16>(L.z()->as<__nv_bfloat16>(), L.g.M(), L.g.Co, L.mean()->as<float>(),
                                  L.invstd()->as<float>(), th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs,
                                  dst_in, dst_out, ob.p, ob.pH, ob.pW, gr + L.g_off, gr + L.b_off,
-                                 part()->as<double>(), counters()->as<unsigned>(), st);
+                                 part()->as<double>(), counters()->as<unsigned>(), st, fold);
   else
     bn_bwd_reduce<float>(L.z()->as<float>(), L.g.M(), L.g.Co, L.mean()->as<float>(), L.invstd()->as<float>(),
                          th + L.g_off, th + L.b_off, L.relu ? 1 : 0, dy0, dy1, cs, dst_in, dst_out, ob.p, ob.pH,
-                         ob.pW, gr + L.g_off, gr + L.b_off, part()->as<double>(), counters()->as<unsigned>(), st);
+                         ob.pW, gr + L.g_off, gr + L.b_off, part()->as<double>(), counters()->as<unsigned>(), st,
+                         fold);
   }
   // dz in bf16 for tensor-core dgrad / wgrad, in fp32 only if a SIMT pass consumes it
   // (the stem has no dgrad: its input is data)
@@ -749,7 +833,7 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       branch_forward(u.phi, cur[u.src()], keep, st, src_ready);
       Layer &L = u.phi.back();
       apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(), L.invstd()->as<float>(),
-               th + L.g_off, th + L.b_off, 1, 1.f, cur[u.dst()], out[u.dst()], ob.p, st, ob.pH, ob.pW);
+               th + L.g_off, th + L.b_off, 1, 1.f, cur[u.dst()], out[u.dst()], ob.p, st, ob.pH, ob.pW, take_fold(L));
       break;
     }
     case PETRA_UNIT_DS: {
@@ -765,11 +849,13 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       int C = L.g.Co;
       const Bf16Out od = ob_half == u.dst() ? ob : Bf16Out{}, os = ob_half == u.src() ? ob : Bf16Out{};
       apply_bn(M, C, u.pa.z()->p, u.pa.z16, C, 0, u.pa.mean()->as<float>(), u.pa.invstd()->as<float>(),
-                             th + u.pa.g_off, th + u.pa.b_off, 0, 1.f, nullptr, out[u.dst()], nullptr, st);
+                             th + u.pa.g_off, th + u.pa.b_off, 0, 1.f, nullptr, out[u.dst()], nullptr, st, 0, 0,
+                             take_fold(u.pa));
       apply_bn(M, C, L.z()->p, L.z16, C, 0, L.mean()->as<float>(), L.invstd()->as<float>(), th + L.g_off,
-               th + L.b_off, 1, 1.f, out[u.dst()], out[u.dst()], od.p, st, od.pH, od.pW);
+               th + L.b_off, 1, 1.f, out[u.dst()], out[u.dst()], od.p, st, od.pH, od.pW, take_fold(L));
       apply_bn(M, C, u.pb.z()->p, u.pb.z16, C, 0, u.pb.mean()->as<float>(), u.pb.invstd()->as<float>(),
-               th + u.pb.g_off, th + u.pb.b_off, 0, 1.f, nullptr, out[u.src()], os.p, st, os.pH, os.pW);
+               th + u.pb.g_off, th + u.pb.b_off, 0, 1.f, nullptr, out[u.src()], os.p, st, os.pH, os.pW,
+               take_fold(u.pb));
       break;
     }
     case PETRA_UNIT_STEM: {
@@ -780,11 +866,12 @@ void Stage::unit_forward(Unit &u, const float *cur[2], float *out[2], bool keep,
       if (u.d.maxpool) {
         apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(),
                                L.invstd()->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
-                               u.pool_a()->as<float>(), nullptr, st);
+                               u.pool_a()->as<float>(), nullptr, st, 0, 0, take_fold(L));
         ProfScope ps("maxpool", st, 0.0, 4.0 * (double)L.g.M() * L.g.Co * 1.25);
         maxpool_fwd(u.pool_a()->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, out[0], out[1],
                     u.pool_arg()->as<uint8_t>(), st);
       } else {
+        flush_fold(st);  // two passes over halves of the channels: final statistics first
         for (int h = 0; h < 2; ++h)
           apply_bn(L.g.M(), Ch, L.z()->p, L.z16, L.g.Co, h * Ch, L.mean()->as<float>(),
                                  L.invstd()->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr, out[h],
@@ -844,7 +931,7 @@ void Stage::unit_backward(Unit &u, bool recompute, const float *xin[2], const fl
           // recompute the pre-pool activation and argmax (outputs go to scratch)
           apply_bn(L.g.M(), L.g.Co, L.z()->p, L.z16, L.g.Co, 0, L.mean()->as<float>(),
                                  L.invstd()->as<float>(), th + L.g_off, th + L.b_off, 1, 1.f, nullptr,
-                                 u.pool_a()->as<float>(), nullptr, st);
+                                 u.pool_a()->as<float>(), nullptr, st, 0, 0, take_fold(L));
           maxpool_fwd(u.pool_a()->as<float>(), L.g.B, L.g.Ho, L.g.Wo, L.g.Co, u.out.H, u.out.W, L.dz->as<float>(),
                       L.dz->as<float>() + u.out.numel(), u.pool_arg()->as<uint8_t>(), st);
         }
@@ -918,8 +1005,23 @@ std::vector<int> Stage::take_pop(uint64_t mb) {
 // later units work in place.  Caller inputs are never written.  keep = final stage
 // (running stats updated in this single forward, reading c10; outputs stay in the
 // stage's buffers for its own backward).
+// comparison buffers of this forward (slot n_fwd_ of each ring): the received input and
+// theta^t, as a delayed-gradient method with weight stashing would keep them
+void Stage::enqueue_compare(const float *x1, const float *x2, cudaStream_t st) {
+  if (!cmp_in_[0].empty()) {
+    const size_t s = (size_t)(n_fwd_ % (int64_t)cmp_in_[0].size());
+    copy_d2d(cmp_in_[0][s]->as<float>(), x1, in_.numel(), st);
+    copy_d2d(cmp_in_[1][s]->as<float>(), x2, in_.numel(), st);
+  }
+  if (!cmp_stash_.empty()) {
+    const size_t s = (size_t)(n_fwd_ % (int64_t)cmp_stash_.size());
+    copy_d2d(cmp_stash_[s]->as<float>(), theta_->as<float>(), (int64_t)(theta_->bytes / sizeof(float)), st);
+  }
+}
+
 void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *o2, const std::vector<int> &push,
                             bool keep, const float **fin, cudaStream_t st) {
+  enqueue_compare(x1, x2, st);
   const float *cur[2] = {x1, x2};
   bool ro[2] = {true, true};
   float *outs[2] = {o1, o2};
@@ -956,6 +1058,7 @@ void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *
       ro[0] = ro[1] = false;
     }
   }
+  flush_fold(st);
   if (fin) {
     fin[0] = cur[0];
     fin[1] = cur[1];
@@ -1021,6 +1124,8 @@ void Stage::enqueue_backward(const float *xt1, const float *xt2, const float *d1
   bool rox[2] = {true, true}, rod[2] = {true, true};
   float *ox[2] = {oxt1, oxt2}, *od[2] = {od1, od2};
   enqueue_backward_walk((int)units_.size() - 1, true, cx, cd, rox, rod, ox, od, pop, st);
+  flush_fold(st);
+  join_wgrads(st);
   if (!stem_first())
     for (int h = 0; h < 2; ++h) {
       if (ox[h]) copy_d2d(ox[h], cx[h], in_.numel(), st);
@@ -1051,6 +1156,7 @@ void Stage::enqueue_tail(const float *x1, const float *x2, const int32_t *labels
   bool rox[2] = {false, false}, rod[2] = {false, false};
   float *ox[2] = {nullptr, nullptr}, *od[2] = {nullptr, nullptr};
   enqueue_backward_walk((int)units_.size() - 2, false, cx, cd, rox, rod, ox, od, pop, st);
+  join_wgrads(st);
   if (!stem_first()) {
     copy_d2d(oxt1, x1, in_.numel(), st);
     copy_d2d(oxt2, x2, in_.numel(), st);
@@ -1150,12 +1256,26 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
   auto record = [&](cudaEvent_t e, cudaStream_t s) {
     if (e) PETRA_CUDA(cudaEventRecordWithFlags(e, s, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
   };
+  // bf16 wire format: round the messages of this tick before they are declared final
+  auto round_fwd = [&](cudaStream_t s) {
+    if (!a.round_msgs) return;
+    for (int h = 0; h < 2; ++h)
+      if (a.o[h]) round_bf16_inplace(a.o[h], out_.numel(), s);
+  };
+  auto round_bwd = [&](cudaStream_t s) {
+    if (!a.round_msgs || stem_first()) return;
+    for (int h = 0; h < 2; ++h) {
+      if (a.oxt[h]) round_bf16_inplace(a.oxt[h], in_.numel(), s);
+      if (a.od[h]) round_bf16_inplace(a.od[h], in_.numel(), s);
+    }
+  };
   auto enqueue = [&](cudaStream_t s) {
     if (is_last_) {
       ctx_ = 0;
       wait_on(s, a.wait_f);
       wait_on(s, a.wait_b);
       enqueue_tail(a.x1, a.x2, a.labels, a.oxt[0], a.oxt[1], a.od[0], a.od[1], a.loss, push, pop, s);
+      round_bwd(s);
       record(a.done_f, s);
       record(a.done_b, s);
     } else if (fwd && bwd && !Prof::enabled) {
@@ -1167,10 +1287,12 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
       ctx_ = 0;
       wait_on(s, a.wait_f);
       enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
+      round_fwd(s);
       record(a.done_f, s);
       ctx_ = 1;
       wait_on(side_, a.wait_b);
       enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, side_);
+      round_bwd(side_);
       record(a.done_b, side_);
       PETRA_CUDA(cudaEventRecord(join_, side_));
       PETRA_CUDA(cudaStreamWaitEvent(s, join_, 0));
@@ -1180,12 +1302,14 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
         ctx_ = 0;
         wait_on(s, a.wait_f);
         enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
+        round_fwd(s);
         record(a.done_f, s);
       }
       if (bwd) {
         ctx_ = 1;
         wait_on(s, a.wait_b);
         enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, s);
+        round_bwd(s);
         record(a.done_b, s);
       }
       ctx_ = 0;
@@ -1195,7 +1319,7 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
   if (!use_graph || Prof::enabled) {
     enqueue(st);
   } else {
-    std::vector<uintptr_t> key = {(uintptr_t)fwd, (uintptr_t)bwd, (uintptr_t)mode};
+    std::vector<uintptr_t> key = {(uintptr_t)fwd, (uintptr_t)bwd, (uintptr_t)mode, (uintptr_t)a.round_msgs};
     for (const void *p : {(const void *)a.x1, (const void *)a.x2, (const void *)a.labels, (const void *)a.o[0],
                           (const void *)a.o[1], (const void *)a.xt[0], (const void *)a.xt[1], (const void *)a.d[0],
                           (const void *)a.d[1], (const void *)a.oxt[0], (const void *)a.oxt[1],
@@ -1204,6 +1328,8 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
                           (const void *)a.wait_b[1], (const void *)a.done_f, (const void *)a.done_b})
       key.push_back((uintptr_t)p);
     for (int v : push) key.push_back((uintptr_t)(v + 1));
+    if (fwd && !cmp_in_[0].empty()) key.push_back((uintptr_t)(n_fwd_ % (int64_t)cmp_in_[0].size()) + 1);
+    if (fwd && !cmp_stash_.empty()) key.push_back((uintptr_t)(n_fwd_ % (int64_t)cmp_stash_.size()) + 1);
     for (int v : pop) key.push_back((uintptr_t)(v + 1));
     auto it = graphs_.find(key);
     if (it == graphs_.end()) {

@@ -68,6 +68,8 @@ struct Layer {               // conv(no bias) -> BN(train) [-> ReLU]
     return fifo_backed ? xb_ext : xb_[*ctx]->as<__nv_bfloat16>();
   }
   StatsRows &stats_rows() { return stats_rows_[*ctx]; }
+  StatsFold fold_[2];                        // part != null: statistics left for the consuming BN pass
+  StatsFold &fold() { return fold_[*ctx]; }
   DevPtr dz, da, dzb;                        // backward-only workspace
   DevPtr w_bf16, wt_bf16;                    // bf16 shadows of the live weights
   bool z16 = false;                          // z stored in bf16 (tensor-core conv output, reading c24)
@@ -128,6 +130,9 @@ struct TickArgs {
   // they are external event nodes (cudaEventWaitExternal / cudaEventRecordExternal).
   cudaEvent_t wait_f[2] = {nullptr, nullptr}, wait_b[2] = {nullptr, nullptr};
   cudaEvent_t done_f = nullptr, done_b = nullptr;
+  // bf16 wire format (petra_pipeline_desc.wire): the messages this tick produces (forward
+  // outputs, backward x~ and delta) are rounded to bf16 in place before done_f / done_b
+  bool round_msgs = false;
 };
 
 struct CachedGraph {
@@ -178,13 +183,26 @@ class Stage {
   std::vector<SgdSeg> segs_;
   DevPtr segs_dev_;
   int64_t max_seg_ = 0;
-  DevPtr part_[2], wgrad_ws_[2], counters_[2];  // per context (see Layer)
+  DevPtr part_[2], spart_[2], wgrad_ws_[2], counters_[2];  // per context (see Layer)
   int ctx_ = 0;                                 // workspace context being enqueued
   DevPtr &part() { return part_[ctx_]; }
+  DevPtr &spart() { return spart_[ctx_]; }   // BN partial rows of the conv epilogues
+  Layer *pending_[2] = {nullptr, nullptr};    // layer whose statistics fold is not consumed yet
+  void flush_fold(cudaStream_t st);           // launch the pending fold as stats_finalize
+  const StatsFold *take_fold(Layer &L);       // the fold for L's consuming pass (cleared)
+  StatsFold fold_tmp_[2];
   DevPtr &wgrad_ws() { return wgrad_ws_[ctx_]; }
   DevPtr &counters() { return counters_[ctx_]; }
   cudaStream_t side_ = nullptr;                 // the backward's stream (fork / join per tick)
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
+  // tensor-core wgrads on their own stream: a layer's dW is needed only by the update, so
+  // the wgrad leaves the critical dz -> dgrad -> BN chain of the backward walk (joined
+  // before the update); own split-K workspace
+  cudaStream_t wg_ = nullptr;
+  cudaEvent_t wg_fork_ = nullptr, wg_join_ = nullptr;
+  DevPtr wg_ws_;
+  bool wg_active_ = false;
+  void join_wgrads(cudaStream_t st);
   DevPtr nonfinite_;
   // tail workspace
   DevPtr feat_, logits_, dlogits_, lossrow_, dfeat_, tail_d_[2], fc_ws_;
@@ -193,6 +211,11 @@ class Stage {
   int64_t version_ = 0;                          // optimizer updates applied
   int64_t t_ = 1;                                // Alg. 1 step counter t (reading c12: starts at 1)
   int64_t n_fwd_ = 0, n_bwd_ = 0;
+  // Table 3 comparison buffers (petra_stage_desc.compare_buffers): a ring of stage inputs
+  // (delayed-gradient input buffer) and a ring of theta copies (weight stash), one slot
+  // written per forward
+  std::vector<DevPtr> cmp_in_[2], cmp_stash_;
+  void enqueue_compare(const float *x1, const float *x2, cudaStream_t st);
   bool have_last_fwd_ = false;
   uint64_t last_fwd_mb_ = 0;
   cudaStream_t last_stream_ = nullptr;

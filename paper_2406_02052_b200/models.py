@@ -280,6 +280,7 @@ class StageSpec:
     bn_eps: float = 1e-5
     fifo_capacity: int = 1
     accumulation_k: int = 1   # Alg. 1 lines 19-23
+    compare_buffers: int = 0  # Table 3 comparison modes (petra.h PETRA_CMP_INPUTS / PETRA_CMP_STASH)
 
     def to_c(self):
         arr = (L.PetraUnit * len(self.units))(*[u.to_c() for u in self.units])
@@ -290,6 +291,7 @@ class StageSpec:
         d.precision, d.momentum, d.weight_decay = self.precision, self.momentum, self.weight_decay
         d.bn_momentum, d.bn_eps, d.nesterov, d.accumulation_k = self.bn_momentum, self.bn_eps, 1, self.accumulation_k
         d.fifo_capacity = self.fifo_capacity
+        d.compare_buffers = self.compare_buffers
         return d, arr   # keep arr alive with d
 
 

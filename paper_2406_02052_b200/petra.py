@@ -113,10 +113,11 @@ class Pipeline:
     """petra_pipeline_* : the stages of this rank with double-buffered mailboxes."""
 
     def __init__(self, specs, stage_rank=None, rank=0, world=1, seed=0, transport="none", nccl_id=None,
-                 local_group=0, join_comm=True):
+                 local_group=0, join_comm=True, wire="fp32"):
         """transport: "none" (world 1, or the caller moves petra_pipeline_comm's bytes),
         "nccl" (the library's ncclSend/ncclRecv; nccl_id = nccl_unique_id() of rank 0),
-        "local" (ranks = pipelines of this process sharing local_group; a test transport)."""
+        "local" (ranks = pipelines of this process sharing local_group; a test transport).
+        wire: "fp32" or "bf16" (petra_wire: messages rounded to bf16 at every stage boundary)."""
         J = len(specs)
         self.J = J
         self._keep = [s.to_c() for s in specs]
@@ -126,7 +127,7 @@ class Pipeline:
         self._nid = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         pd = L.PetraPipelineDesc(J, C.cast(descs, C.POINTER(L.PetraStageDesc)), C.cast(sr, C.POINTER(C.c_int32)),
                                  rank, world, seed, tr, C.cast(self._nid, C.c_void_p) if self._nid else None,
-                                 int(local_group), int(bool(join_comm)))
+                                 int(local_group), int(bool(join_comm)), {"fp32": 0, "bf16": 1}[wire])
         self._descs, self._sr = descs, sr
         h = C.c_void_p()
         L.call("petra_pipeline_create", C.byref(pd), C.byref(h))

@@ -76,3 +76,56 @@ def test_fifo_live_bytes_follow_pushes():
     torch.cuda.synchronize()
     assert st.memory()["fifo_live"] == per
     st.close()
+
+
+def test_compare_buffers_measured_and_numerics_unchanged():
+    """Table 3 comparison modes (petra_stage_desc.compare_buffers): the
+    input ring holds fifo_capacity stage inputs (only for stages whose first unit is
+    reversible: PETRA's own FIFO holds the others), the weight stash fifo_capacity - 1 =
+    2(J-j) fp32 copies of theta; both are written every forward, and the trajectory stays
+    PETRA's bitwise (theta, v and the losses equal the plain run's)."""
+    import numpy as np
+    from paper_2406_02052_b200 import Pipeline
+    from paper_2406_02052_b200 import models as PM2
+    torch.cuda.set_device(0)
+    units = PM2.revnet("revnet18", 32, 10)
+    counts = [5, 4, 4, 5]
+    J, B = 4, 8
+    out = {}
+    for mode in (0, L.CMP_INPUTS | L.CMP_STASH):
+        specs = PM2.stage_specs(units, counts, B, (32, 32, 3), L.BF16_TC)
+        for sp in specs:
+            sp.compare_buffers = mode
+        pipe = Pipeline(specs, [0] * J, 0, 1, seed=3)
+        gen = torch.Generator(device="cuda").manual_seed(0)
+        loss = torch.zeros(1, device="cuda")
+        losses = []
+        for t in range(2 * J + 3):
+            x = torch.randn((B, 32, 32, 3), generator=gen, device="cuda")
+            y = torch.randint(0, 10, (B,), generator=gen, device="cuda", dtype=torch.int32)
+            pipe.tick(t, True, x, y, 0.025, loss, report=False)
+            torch.cuda.synchronize()
+            losses.append(loss.item())
+        mem = {j: s.memory() for j, s in pipe.stages.items()}
+        prm = {j: s.get_params() for j, s in pipe.stages.items()}
+        nparams = {j: s.n_params for j, s in pipe.stages.items()}
+        pipe.close()
+        out[mode] = (losses, prm, mem, nparams)
+    l0, p0, m0, _ = out[0]
+    l1, p1, m1, npar = out[L.CMP_INPUTS | L.CMP_STASH]
+    assert l0 == l1
+    for j in p0:
+        for a, b in zip(p0[j], p1[j]):
+            assert np.array_equal(a, b), j
+    in_shapes = PM2.shapes(units, B, 32, 32, 3)[0]
+    i0 = 0
+    for j in range(1, J + 1):
+        cap = 2 * (J - j) + 1
+        first = units[i0]
+        Bq, H, W, C = in_shapes[i0]
+        exp_in = 0 if first.kind != L.UNIT_REV else cap * 2 * Bq * H * W * C * 4
+        assert m1[j]["cmp_inputs"] == exp_in, j
+        assert m1[j]["cmp_stash"] == (cap - 1) * npar[j] * 4, j
+        assert m0[j]["cmp_inputs"] == 0 and m0[j]["cmp_stash"] == 0
+        assert m1[j]["total"] - m0[j]["total"] == exp_in + (cap - 1) * npar[j] * 4, j
+        i0 += counts[j - 1]

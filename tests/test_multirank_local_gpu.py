@@ -30,7 +30,7 @@ from paper_2406_02052_b200.dist import contiguous_stage_ranks  # noqa: E402
 _group = itertools.count(1)
 
 
-def _run(world, precision, join_comm, n_mb=6, B=8, counts=(5, 4, 4, 5), lr=0.025):
+def _run(world, precision, join_comm, n_mb=6, B=8, counts=(5, 4, 4, 5), lr=0.025, wire="fp32"):
     torch.cuda.set_device(0)
     units = rand_params(OM.build_revnet("revnet18", 32, 10), 5)
     groups = OM.group(units, list(counts))
@@ -40,7 +40,7 @@ def _run(world, precision, join_comm, n_mb=6, B=8, counts=(5, 4, 4, 5), lr=0.025
     sr = contiguous_stage_ranks(J, world)
     gid = next(_group)
     pipes = [Pipeline(specs, sr, r, world, seed=0, transport="local" if world > 1 else "none", local_group=gid,
-                      join_comm=join_comm) for r in range(world)]
+                      join_comm=join_comm, wire=wire) for r in range(world)]
     for p in pipes:
         for j, s in p.stages.items():
             th, bf = init[j - 1]
@@ -96,3 +96,27 @@ def test_uneven_rank_layout_and_single_stage_ranks():
     for j in ref_p:
         for a, b in zip(p[j], ref_p[j]):
             assert np.array_equal(a, b), j
+
+
+@pytest.mark.parametrize("precision", [L.FP32, L.BF16_TC], ids=["fp32", "bf16"])
+def test_bf16_wire_rank_layout_independent(precision):
+    """petra_wire PETRA_WIRE_BF16: every message is
+    rounded to bf16 by its producer at every stage boundary, and cross-rank transfers
+    carry the 2-byte images -- so world 2 / 4 stay BITWISE equal to world 1 under the
+    same wire, while the bf16 wire itself differs from the fp32 wire (the rounding took
+    place) by about the bf16 unit roundoff per message."""
+    ref_l, ref_p, ref_r = _run(1, precision, True, wire="bf16")
+    assert len(ref_l) == 6 and all(np.isfinite(v) for v in ref_l.values())
+    for world in (2, 4):
+        l, p, r = _run(world, precision, True, wire="bf16")
+        assert r == ref_r and l == ref_l, world
+        for j in ref_p:
+            for a, b in zip(p[j], ref_p[j]):
+                assert np.array_equal(a, b), (world, j)
+    f_l, f_p, _ = _run(1, precision, True, wire="fp32")
+    th_b = np.concatenate([ref_p[j][0] for j in sorted(ref_p)])
+    th_f = np.concatenate([f_p[j][0] for j in sorted(f_p)])
+    rel = np.linalg.norm(th_b - th_f) / np.linalg.norm(th_f)
+    assert 0.0 < rel < 1e-2, rel
+    for m in ref_l:
+        assert abs(ref_l[m] - f_l[m]) <= 2e-2 * abs(f_l[m]), (m, ref_l[m], f_l[m])
