@@ -233,6 +233,23 @@ petra_status petra_stage_tail(petra_stage *s, uint64_t mb_id,
                               float lr, float *xt1_in, float *xt2_in, float *d1_in, float *d2_in,
                               float *loss_dev, void *stream);
 
+/* Evaluation forward (the running statistics of batch normalisation "are
+ * then used during model evaluation"): every unit of a NON-final stage
+ * with BN normalising by the running mean / variance (invstd = 1/sqrt(var + eps)); nothing
+ * is pushed on the FIFOs, no statistics or parameters change.  Layout as
+ * petra_stage_forward (x2 NULL for a stem-first stage).  Must not overlap a training
+ * forward of the same stage (it uses the forward workspace); non-reversible units need a
+ * free FIFO slot (drain the pipeline first).  Enqueued on `stream`.
+ * Errors: PETRA_E_ARG, PETRA_E_CUDA. */
+petra_status petra_stage_eval(petra_stage *s, const float *x1_in, const float *x2_in, float *x1_out, float *x2_out,
+                              void *stream);
+/* Final stage: evaluation forward, then the classifier; adds to *correct_dev (device int32)
+ * the number of rows whose first-index argmax logit equals the label and writes the
+ * batch-mean cross-entropy to *loss_dev (device float).  labels_dev: int32[B].
+ * Errors: PETRA_E_ARG, PETRA_E_CUDA. */
+petra_status petra_stage_eval_tail(petra_stage *s, const float *x1_in, const float *x2_in, const int32_t *labels_dev,
+                                   int32_t *correct_dev, float *loss_dev, void *stream);
+
 /* ------------------------------------------------------------------ pipeline
  * One process (rank) owns a contiguous block of stages.  petra_pipeline_tick
  * runs tick t of every local stage (forward then backward, both at theta^t,

@@ -107,6 +107,8 @@ SIGS = {
     "petra_stage_output_shape": (C.c_int, [P, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32), C.POINTER(I32)]),
     "petra_stage_param_count": (C.c_int, [P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "petra_stage_memory": (C.c_int, [P, C.POINTER(PetraMemoryReport)]),
+    "petra_stage_eval": (C.c_int, [P, VP, VP, VP, VP, VP]),
+    "petra_stage_eval_tail": (C.c_int, [P, VP, VP, VP, VP, VP, VP]),
     "petra_stage_num_tensors": (C.c_int, [P, C.POINTER(I32)]),
     "petra_stage_tensor_info": (C.c_int, [P, I32, C.POINTER(PetraTensorInfo)]),
     "petra_stage_get_params": (C.c_int, [P, VP, VP, VP]),

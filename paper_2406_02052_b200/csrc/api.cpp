@@ -176,6 +176,17 @@ petra_status petra_stage_tail(petra_stage *s, uint64_t mb, const float *x1, cons
   return guard([&] { s->s->tail(mb, x1, x2, labels, lr, oxt1, oxt2, od1, od2, loss, (cudaStream_t)stream); });
 }
 
+petra_status petra_stage_eval(petra_stage *s, const float *x1, const float *x2, float *o1, float *o2, void *stream) {
+  if (!s) return fail(PETRA_E_ARG, "NULL stage");
+  return guard([&] { s->s->eval(x1, x2, o1, o2, (cudaStream_t)stream); });
+}
+
+petra_status petra_stage_eval_tail(petra_stage *s, const float *x1, const float *x2, const int32_t *labels,
+                                   int32_t *correct, float *loss, void *stream) {
+  if (!s) return fail(PETRA_E_ARG, "NULL stage");
+  return guard([&] { s->s->eval_tail(x1, x2, labels, correct, loss, (cudaStream_t)stream); });
+}
+
 petra_status petra_pipeline_create(const petra_pipeline_desc *d, petra_pipeline **out) {
   if (!d || !out || !d->stages || !d->stage_rank) return fail(PETRA_E_ARG, "NULL argument");
   return guard([&] {

@@ -54,16 +54,22 @@ int conv_grid(int work);
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  // the stream's priority on the launch itself, so a captured graph's kernel nodes keep it
+  // (the stage's backward stream outranks its forward; the wgrad stream ranks lowest)
+  int prio = 0;
+  cudaStreamGetPriority(st, &prio);
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = prio;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   PETRA_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 

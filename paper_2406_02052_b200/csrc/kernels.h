@@ -134,7 +134,10 @@ void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int 
                            const float *bias, int N, const int32_t *labels, float *feat, float *logits,
                            float *dlogits, float *loss_row, float *dfeat, float *dw, float *db, float *d1,
                            float *d2, float *loss, int *nonfinite, float *fc_ws, int64_t fc_ws_floats,
-                           cudaStream_t st);
+                           cudaStream_t st, int *correct = nullptr);  // correct: evaluation only (count += argmax == y)
+// BN constants from the running statistics (evaluation): mean = rm, invstd = 1/sqrt(rv + eps)
+void bn_running_constants(const float *rm, const float *rv, int C, float eps, float *mean, float *invstd,
+                          cudaStream_t st);
 void maxpool_fwd(const float *a, int B, int H, int W, int C, int Ho, int Wo, float *o1, float *o2, uint8_t *arg,
                  cudaStream_t st);
 void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, int H, int W, int C, int Ho, int Wo,

@@ -923,7 +923,23 @@ void finalize_fold(const StatsFold &f, float *mean, float *invstd, cudaStream_t 
   bn_stats_from_partials(f.part, r, f.N, f.M, f.eps, mean, invstd, f.rmean, f.rvar, f.mom, st);
 }
 
+__global__ void running_constants_kernel(const float *__restrict__ rm, const float *__restrict__ rv, int C, float eps,
+                                         float *__restrict__ mean, float *__restrict__ invstd) {
+  pdl_wait_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) {
+    mean[c] = rm[c];
+    invstd[c] = (float)(1.0 / sqrt((double)rv[c] + (double)eps));
+  }
+}
+
 }  // namespace
+
+void bn_running_constants(const float *rm, const float *rv, int C, float eps, float *mean, float *invstd,
+                          cudaStream_t st) {
+  launch_k(running_constants_kernel, (unsigned)cdiv(C, 256), 256, 0, st, rm, rv, C, eps, mean, invstd);
+  PETRA_LAUNCH_CHECK();
+}
 
 size_t bn_partial_bytes(int64_t M, int C) {
   return (size_t)std::max(red_geom(M, C, RT_STATS).nrb, red_geom(M, C, RT_BWD).nrb) * C * 2 * sizeof(double);

@@ -15,7 +15,9 @@
 // 32 rows in smem and writes them out coalesced (8 lanes per 128-byte pixel chunk).
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <mutex>
+#include <vector>
 
 #include "../errors.h"
 #include "../kernels.h"
@@ -49,7 +51,16 @@ struct HaloParams {
   void *out;               // [B][H][W][N] fp32 or bf16
   float *stats;            // nullable: one BN partial row per CTA [grid][N][2] (mean, M2) + float[grid] counts
   tc::FastDiv f_ghw, f_wp, f_nn;  // Hp * Wp, Wp, N / BN (set by launch)
+  int rs;                  // epilogue row split allowed (PETRA_EPI_RS)
+  unsigned long long *tl;  // nullable: per-CTA timeline (PETRA_TIMELINE=1 debug runs, kTl slots per CTA)
 };
+// timeline slots (clock64 per CTA): 0 entry, 1 setup done, 2 weights resident, 3 exit,
+// 4 + 4i: item i MMA start (operands + accumulator ready), MMAs issued, epilogue (warp 2)
+// start, epilogue end
+constexpr int kTl = 64;
+__device__ __forceinline__ void tl_mark(unsigned long long *tl, int slot) {
+  if (tl && slot < kTl) tl[(size_t)blockIdx.x * kTl + slot] = clock64();
+}
 
 // T consecutive 128-row M tiles share every B (weight) stage: the MMA warp applies one
 // (tap, channel block) weight tile to all T tiles before releasing it, so the weight
@@ -74,8 +85,16 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
   uint8_t *sepi = reinterpret_cast<uint8_t *>(afull) + 512;       // [8 warps][32 rows x 144 B]
-  float *sstat = reinterpret_cast<float *>(sepi + kEpiWarps * kEpiWarp);  // [4 lane quarters][BN][2] (mean, M2)
-  int *scnt = reinterpret_cast<int *>(sstat + 8 * BN);                     // [4 lane quarters] valid rows
+  // Epilogue work split: two warps per TMEM lane quarter.  A row of BN outputs wider than
+  // one 128-byte chunk is split by column chunks (hc = chunk parity); a row that fits in
+  // one chunk (BN = 64, bf16 out) is not split -- the two warps take alternate tiles of the
+  // item (T >= 2) or alternate items (T == 1, each its own TMEM accumulator), so all eight
+  // warps work (RS: rows split).
+  const bool RS = BN * (OUT16 ? 2 : 4) <= 128 && P.rs;  // (P.rs: PETRA_EPI_RS, default on)
+  const bool RS_ITEMS = RS && T == 1;   // alternate items: 4 warps release each accumulator
+  const int NSLOT = RS ? 8 : 4;          // statistics slots: per warp (RS) or per lane quarter
+  float *sstat = reinterpret_cast<float *>(sepi + kEpiWarps * kEpiWarp);  // [NSLOT][BN][2] (mean, M2)
+  int *scnt = reinterpret_cast<int *>(sstat + NSLOT * BN * 2);              // [NSLOT] valid rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_nt = P.N / BN;
@@ -83,6 +102,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int GHW = P.Hp * P.Wp;
   const tc::FastDiv &f_ghw = P.f_ghw, &f_wp = P.f_wp, &f_nn = P.f_nn;
   const int BS = P.resident ? 1 : P.bstages;  // resident: one barrier for the whole weight load
+  if (threadIdx.x == 0) tl_mark(P.tl, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ASTAGES; ++s) {
@@ -95,7 +115,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], kEpiWarps);
+      tc::mbar_init(&tempty[a], RS_ITEMS ? kEpiWarps / 2 : kEpiWarps);
     }
     tc::fence_mbar_init();
     tc::tma_prefetch(&tmA);
@@ -106,6 +126,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) tl_mark(P.tl, 1);
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer: halo per channel block, B per (channel block, tap)
@@ -144,6 +165,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       tc::mbar_wait(&bfull[0], 0);
       tc::tc_fence_after();
     }
+    if (lane == 0) tl_mark(P.tl, 2);
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
       const int acc = it & 1;
       tc::mbar_wait_idle(&tempty[acc], ((it >> 1) & 1) ^ 1);
@@ -152,6 +174,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       for (int cb = 0; cb < P.CB; ++cb) {
         tc::mbar_wait(&afull[as], aph);
         tc::tc_fence_after();
+        if (cb == 0 && lane == 0) tl_mark(P.tl, 4 + 4 * it);
         const uint32_t abase = tc::smem_u32(sA + as * P.a_stage) + P.lead * 128;
         for (int t = 0; t < P.ntaps; ++t) {
           if (!P.resident) {
@@ -180,12 +203,14 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       if (tc::elect_one()) tc::umma_commit(&tfull[acc]);
       __syncwarp();
+      if (lane == 0) tl_mark(P.tl, 5 + 4 * it);
     }
   } else {  // ---------------- epilogue warps 2..9 (two per TMEM lane quarter, alternating column chunks)
     const int q = warp & 3;
     const int hc = (warp - 2) >> 2;
     const int row = q * 32 + lane;
-    float *my_stat = sstat + (size_t)q * BN * 2;  // this CTA's N tile (fixed: grid % n_nt == 0)
+    const int slot = RS ? warp - 2 : q;
+    float *my_stat = sstat + (size_t)slot * BN * 2;  // this CTA's N tile (fixed: grid % n_nt == 0)
     uint8_t *ebuf = sepi + (warp - 2) * kEpiWarp;
     constexpr int ES = OUT16 ? 2 : 4;
     constexpr int CW = 128 / ES;  // columns per 128-byte chunk
@@ -199,10 +224,12 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
       const int mg = tc::fdiv(w, f_nn), nt = w - mg * n_nt;
       const int acc = it & 1;
+      if (RS_ITEMS && acc != hc) continue;  // the other warp of this lane quarter takes it
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
+      if (warp == 2 && lane == 0) tl_mark(P.tl, 6 + 4 * it);
 #pragma unroll 1
-      for (int tt = 0; tt < T; ++tt) {
+      for (int tt = (RS && !RS_ITEMS) ? hc : 0; tt < T; tt += (RS && !RS_ITEMS) ? 2 : 1) {
         const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * ACC + tt * BN;
         const int m = (mg * T + tt) * 128 + row;
         const int b = tc::fdiv(m, f_ghw), r = m - b * GHW, hp = tc::fdiv(r, f_wp), wp = r - hp * P.Wp;
@@ -212,7 +239,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
-          const int c = CW * hc + 2 * CW * k;
+          const int c = RS ? 0 : CW * hc + 2 * CW * k;
           if (c >= BN) break;
           float v[CW];
 #pragma unroll
@@ -271,11 +298,12 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      if (warp == 2 && lane == 0) tl_mark(P.tl, 7 + 4 * it);
     }
-    if (P.stats) {  // this CTA's partial row: the 4 lane quarters merged (Chan) in a fixed order
+    if (P.stats) {  // this CTA's partial row: the slots merged (Chan) in a fixed order
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
-        const int c = CW * hc + 2 * CW * k;
+        const int c = RS ? 0 : CW * hc + 2 * CW * k;
         if (c >= BN) break;
         const int col = c + (OUT16 ? 2 * lane : lane);  // column within the N tile
         const float2 a = tc::colstats_final(cst[k], 0, nrows);
@@ -287,21 +315,27 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           my_stat[2 * col + 3] = b.y;
         }
       }
-      if (hc == 0 && lane == 0) scnt[q] = nrows;
+      if ((RS || hc == 0) && lane == 0) scnt[slot] = nrows;
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      tc::cta_stats_row(sstat, scnt, BN, (warp - 2) * 32 + lane, kEpiWarps * 32,
-                        P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_nt) * BN) * 2,
-                        P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
+      if (RS)
+        tc::cta_stats_row<8>(sstat, scnt, BN, (warp - 2) * 32 + lane, kEpiWarps * 32,
+                          P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_nt) * BN) * 2,
+                          P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
+      else
+        tc::cta_stats_row<4>(sstat, scnt, BN, (warp - 2) * 32 + lane, kEpiWarps * 32,
+                          P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_nt) * BN) * 2,
+                          P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) tl_mark(P.tl, 3);
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem_base, 2 * ACC);
   }
 }
 
-size_t fixed_smem() { return 1024 + 512 + kEpiWarps * kEpiWarp + (size_t)256 * 32 + 16; }  // stats: BN <= 256
+size_t fixed_smem() { return 1024 + 512 + kEpiWarps * kEpiWarp + (size_t)256 * 32 + 64; }  // stats: BN*NSLOT <= 1024
 // the halo of T tiles (128*T + 2*(W+3) rows) as equal TMA boxes of <= 256 rows, each a
 // multiple of 8 rows so every box starts 1 KB-aligned
 void halo_rows(int T, int W, int &box_rows, int &HR) {
@@ -381,10 +415,35 @@ void launch(const CUtensorMap &ta, const CUtensorMap &tb, const HaloParams &P0, 
   P.f_ghw = tc::fastdiv_make(P.Hp * P.Wp);
   P.f_wp = tc::fastdiv_make(P.Wp);
   P.f_nn = tc::fastdiv_make(P.N / BN);
+  static const int rs_on = env_int("PETRA_EPI_RS", 1);
+  P.rs = rs_on;
   const int work = (int)cdiv(P.Mp, 128 * T) * (P.N / BN);
   const size_t smem = fixed_smem() + 2 * (size_t)P.a_stage + (size_t)P.bstages * BN * 128;
-  launch_k(conv_halo_kernel<BN, T, OUT16>, halo_grid(work, P.N / BN), kThreads, smem, st, ta, tb, P);
+  static const bool tl_on = env_int("PETRA_TIMELINE", 0) != 0;  // debug: per-CTA timeline to stderr
+  const int grid = halo_grid(work, P.N / BN);
+  static unsigned long long *tl_buf = nullptr;
+  if (tl_on) {
+    if (!tl_buf) PETRA_CUDA(cudaMalloc(&tl_buf, (size_t)kNumSMs * kTl * sizeof(unsigned long long)));
+    PETRA_CUDA(cudaMemsetAsync(tl_buf, 0, (size_t)kNumSMs * kTl * sizeof(unsigned long long), st));
+    P.tl = tl_buf;
+  }
+  launch_k(conv_halo_kernel<BN, T, OUT16>, grid, kThreads, smem, st, ta, tb, P);
   PETRA_LAUNCH_CHECK();
+  if (tl_on) {
+    std::vector<unsigned long long> h((size_t)grid * kTl);
+    PETRA_CUDA(cudaStreamSynchronize(st));
+    PETRA_CUDA(cudaMemcpy(h.data(), tl_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "timeline conv_halo_kernel<%d,%d,%d> grid %d work %d (cycles from CTA entry)\n", BN, T, (int)OUT16,
+            grid, work);
+    for (int c = 0; c < grid; ++c) {
+      const unsigned long long *r = &h[(size_t)c * kTl], t0 = r[0];
+      auto d = [&](int i) { return r[i] ? (long long)(r[i] - t0) : -1LL; };
+      fprintf(stderr, "cta %3d setup %6lld wres %6lld exit %6lld |", c, d(1), d(2), d(3));
+      for (int i = 0; 4 + 4 * i + 3 < kTl && r[4 + 4 * i]; ++i)
+        fprintf(stderr, " [%lld %lld %lld %lld]", d(4 + 4 * i), d(5 + 4 * i), d(6 + 4 * i), d(7 + 4 * i));
+      fprintf(stderr, "\n");
+    }
+  }
 }
 
 template <bool OUT16>

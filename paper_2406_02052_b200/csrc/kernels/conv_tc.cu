@@ -57,6 +57,7 @@ struct ConvTCParams {
   float *stats;              // nullable: BN partials, one row per CTA: [grid][N][2] (mean, M2) of the CTA's
                              // N tile columns, then float[grid] row counts (kernels.h StatsRows)
   tc::FastDiv f_sp, f_nt, f_ghw, f_wb;  // splits, N / BN, Hb * Wb, Wb (set by launch_conv)
+  int rs;                    // epilogue row split allowed (PETRA_EPI_RS)
 };
 
 // Epilogue staging: each epilogue warp owns two 4 KB buffers (32 rows x 128 B, the
@@ -89,7 +90,13 @@ __device__ __forceinline__ void stage_row(uint8_t *buf, int lane, const float *v
   }
 }
 
-template <int BN, int STAGES, bool OUT16>
+// KG: 64-channel blocks per pipeline stage.  TMA serves about one copy per ~300 cycles
+// per SM whatever its size up to 32 KB (tools/micro/tma_burst.cu, profiles/r02/tuning/
+// tma_burst.txt), so a stage fetches KG blocks of the same tap with ONE A copy (a 5-D
+// im2col box whose outermost dimension is the channel block) and ONE B copy (a 3-D box
+// over KG consecutive k-blocks of the weight matrix): KG consecutive [rows][128 B] slabs
+// each, the layout the MMAs read one k-block at a time.
+template <int BN, int STAGES, bool OUT16, int KG>
 __global__ void __maxnreg__(PETRA_CONV_MAXREG)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmW,
@@ -98,7 +105,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t B_BYTES = BN * BK * 2;
-  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t STAGE_BYTES = KG * (A_BYTES + B_BYTES);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
   uint64_t *empty = full + STAGES;
   uint64_t *tfull = empty + STAGES;
@@ -106,8 +113,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
   uint64_t *abar = reinterpret_cast<uint64_t *>(tmem_slot + 2);  // per epilogue warp: addend box loads
   uint8_t *sepi = smem + STAGES * STAGE_BYTES + 1024;      // [8 warps][2][32 x 128 B] epilogue staging
-  float *sstat = reinterpret_cast<float *>(sepi + kEpiBytes);  // [4 lane quarters][BN][2] (mean, M2)
-  int *scnt = reinterpret_cast<int *>(sstat + 8 * BN);           // [4 lane quarters] valid rows
+  // two epilogue warps per TMEM lane quarter: split by 128-byte column chunks, or -- when a
+  // row is a single chunk (BN = 64, bf16 out: RS) -- by work item (each warp of the pair
+  // owns one of the two TMEM accumulators), so that all eight warps work
+  const bool RS = BN * (OUT16 ? 2 : 4) <= 128 && P.rs;  // (P.rs: PETRA_EPI_RS, default on)
+  const int NSLOT = RS ? 8 : 4;  // statistics slots: per warp (RS) or per lane quarter
+  float *sstat = reinterpret_cast<float *>(sepi + kEpiBytes);  // [NSLOT][BN][2] (mean, M2)
+  int *scnt = reinterpret_cast<int *>(sstat + NSLOT * BN * 2);   // [NSLOT] valid rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_n = P.N / BN;
@@ -132,7 +144,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], kEpiWarps);
+      tc::mbar_init(&tempty[a], RS ? kEpiWarps / 2 : kEpiWarps);
     }
     for (int a = 0; a < kEpiWarps; ++a) tc::mbar_init(&abar[a], 1);
     tc::fence_mbar_init();
@@ -154,13 +166,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         decode(w, mt, nt, sp, kb0, kb1);
         const int m0 = mt * BM;
         const int b0 = tc::fdiv(m0, f_ghw), i0 = tc::fdiv(m0 - b0 * GHW, f_wb);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += KG) {  // KG blocks of one tap (CB % KG == 0)
           const int t = kb / P.CB, cb = kb % P.CB;
           tc::mbar_wait_idle(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * STAGE_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tc::tma_load_4d(sa, &tmA, &full[stage], cb * BK, P.dw[t], P.s_in * i0 + P.dh[t], b0);
-          tc::tma_load_2d(sa + A_BYTES, &tmB, &full[stage], P.wk[t] * P.Cred + cb * BK, nt * BN);
+          tc::tma_load_5d(sa, &tmA, &full[stage], 0, P.dw[t], P.s_in * i0 + P.dh[t], b0, cb);
+          tc::tma_load_3d(sa + KG * A_BYTES, &tmB, &full[stage], 0, nt * BN, P.wk[t] * P.CB + cb);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -177,16 +189,19 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       tc::mbar_wait_idle(&tempty[acc], ((it >> 1) & 1) ^ 1);
       tc::tc_fence_after();
       const uint32_t dtm = tmem_base + acc * BN;
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int kb = kb0; kb < kb1; kb += KG) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
         const uint32_t sa = tc::smem_u32(smem + stage * STAGE_BYTES);
-        const uint64_t ad = tc::sw128_desc(sa, 16, 1024);
-        const uint64_t bd = tc::sw128_desc(sa + A_BYTES, 16, 1024);
         if (tc::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)  // advance 32 B (16 bf16) along K inside the swizzle row
-            tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          for (int g = 0; g < KG; ++g) {
+            const uint64_t ad = tc::sw128_desc(sa + g * A_BYTES, 16, 1024);
+            const uint64_t bd = tc::sw128_desc(sa + KG * A_BYTES + g * B_BYTES, 16, 1024);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)  // advance 32 B (16 bf16) along K inside the swizzle row
+              tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || g > 0 || k > 0) ? 1u : 0u);
+          }
           tc::umma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -199,7 +214,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int q = warp & 3;             // TMEM lane quarter this warp may access
     const int hc = (warp - 2) >> 2;     // column half: chunks hc, hc + 2, ... of each tile
     const int row = q * 32 + lane;
-    float *my_stat = sstat + (size_t)q * BN * 2;  // this CTA's N tile (fixed: grid % n_tiles_n == 0)
+    const int slot = RS ? warp - 2 : q;
+    float *my_stat = sstat + (size_t)slot * BN * 2;  // this CTA's N tile (fixed: grid % n_tiles_n == 0)
     uint8_t *ebuf = sepi + (warp - 2) * 2 * kEpiBuf;
     int eb = 0;  // staging buffer to fill next
     if (lane == 0) {
@@ -236,13 +252,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       int mt, nt, sp, kb0, kb1;
       decode(w, mt, nt, sp, kb0, kb1);
       const int acc = it & 1;
+      if (RS && acc != hc) continue;  // the other warp of this lane quarter takes this item
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::tc_fence_after();
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       const int m = mt * BM + row;
       if (P.splits > 1) {  // fp32 partial of this K split, GEMM-row order -> ws[split][M][N]
 #pragma unroll 1
-        for (int c = 32 * hc; c < BN; c += 64) {
+        for (int c = RS ? 0 : 32 * hc; c < BN; c += RS ? 32 : 64) {
           float v[32];
           tc::tmem_ld16(trow + c, *reinterpret_cast<float(*)[16]>(v));
           tc::tmem_ld16(trow + c + 16, *reinterpret_cast<float(*)[16]>(v + 16));
@@ -259,7 +276,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
-          const int c = CW * hc + 2 * CW * k;
+          const int c = RS ? 0 : CW * hc + 2 * CW * k;
           if (c >= BN) break;
           float v[CW];
 #pragma unroll
@@ -301,10 +318,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
     if (lane == 0) tc::bulk_wait_all();
-    if (P.stats) {  // this CTA's partial row: the 4 lane quarters merged (Chan) in a fixed order
+    if (P.stats) {  // this CTA's partial row: the slots merged (Chan) in a fixed order
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
-        const int c = CW * hc + 2 * CW * k;
+        const int c = RS ? 0 : CW * hc + 2 * CW * k;
         if (c >= BN) break;
         const int col = c + (OUT16 ? 2 * lane : lane);  // column within the N tile
         const float2 a = tc::colstats_final(cst[k], 0, nrows);
@@ -316,11 +333,16 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           my_stat[2 * col + 3] = b.y;
         }
       }
-      if (hc == 0 && lane == 0) scnt[q] = nrows;
+      if ((RS || hc == 0) && lane == 0) scnt[slot] = nrows;
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      tc::cta_stats_row(sstat, scnt, BN, (warp - 2) * 32 + lane, kEpiWarps * 32,
-                        P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2,
-                        P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
+      if (RS)
+        tc::cta_stats_row<8>(sstat, scnt, BN, (warp - 2) * 32 + lane, kEpiWarps * 32,
+                             P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2,
+                             P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
+      else
+        tc::cta_stats_row<4>(sstat, scnt, BN, (warp - 2) * 32 + lane, kEpiWarps * 32,
+                             P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2,
+                             P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
     }
   }
   __syncthreads();
@@ -458,6 +480,8 @@ struct WgradParams {
   int KBtot;              // pixel blocks of 64 (padded grid)
   int kb_per_split;
   int n_mt, n_nt, splits;
+  int xg;                 // 2: both 64-row halves of an M tile are consecutive channel blocks of one
+                          // tap (Ci % 128 == 0): ONE 2-block x copy; 1: a copy per half
   float *out;             // [splits][N][Mr]
 };
 
@@ -522,19 +546,20 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
           ci0j[j] = r % P.Ci;
         }
         const uint32_t bytes = (valid[1] ? 2 : 1) * HALF_A + B_BYTES;
+        // TMA serves ~one copy per ~300 cycles per SM whatever its size (tma_burst.cu):
+        // the x halves in one 2-block copy when they share a tap, dz in one BN/64-block copy
         for (int kb = kb0; kb < kb1; ++kb) {
           const int p0 = kb * 64;
           const int b0 = p0 / GHW, i0 = (p0 % GHW) / P.Wb;
           tc::mbar_wait_idle(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * STAGE_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], bytes);
-          for (int j = 0; j < 2; ++j) {
+          for (int j = 0; j < 2; j += P.xg) {
             if (!valid[j]) continue;
             const int kh = tapj[j] / P.k, kw = tapj[j] % P.k;
-            tc::tma_load_4d(sa + j * HALF_A, &tmX, &full[stage], ci0j[j], kw - P.p, P.s * i0 + kh - P.p, b0);
+            tc::tma_load_5d(sa + j * HALF_A, &tmX, &full[stage], 0, kw - P.p, P.s * i0 + kh - P.p, b0, ci0j[j] / 64);
           }
-          for (int nb = 0; nb < BN / 64; ++nb)
-            tc::tma_load_4d(sa + 2 * HALF_A + nb * HALF_A, &tmDZ, &full[stage], nt * BN + nb * 64, 0, i0, b0);
+          tc::tma_load_5d(sa + 2 * HALF_A, &tmDZ, &full[stage], 0, 0, i0, b0, nt * (BN / 64));
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -719,6 +744,30 @@ CUtensorMap act_map(const __nv_bfloat16 *x, int B, int H, int W, int C, int Gw, 
   return make_map(base, 4, dims, st, box, es);
 }
 
+// the same activation view with the 64-channel block as an outermost fifth dimension
+// (stride 128 B): a box of kg blocks lands as kg consecutive 128-row slabs (conv_tc_kernel)
+CUtensorMap act_map5(const __nv_bfloat16 *x, int B, int H, int W, int C, int Gw, int R, int NB, int s, int kg,
+                     bool padded = false) {
+  const int P = padded ? 1 : 0;
+  const __nv_bfloat16 *base = x + (padded ? ((int64_t)(W + 2) + 1) * C : 0);
+  cuuint64_t dims[5] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B, (cuuint64_t)C / 64};
+  cuuint64_t st[4] = {(cuuint64_t)C * 2, (cuuint64_t)(W + 2 * P) * C * 2,
+                      (cuuint64_t)(H + 2 * P) * (W + 2 * P) * C * 2, 128};
+  cuuint32_t box[5] = {64, (cuuint32_t)(Gw * s), (cuuint32_t)(R * s), (cuuint32_t)NB, (cuuint32_t)kg};
+  cuuint32_t es[5] = {1, (cuuint32_t)s, (cuuint32_t)s, 1, 1};
+  return make_map(base, 5, dims, st, box, es);
+}
+
+// K-major matrix [rows][K] bf16 as (64, rows, K / 64 blocks), box (64, box_rows, kg): kg
+// consecutive k-blocks per copy, landing as kg [box_rows][128 B] slabs
+CUtensorMap mat_map3(const __nv_bfloat16 *w, int rows, int K, int box_rows, int kg) {
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)K / 64};
+  cuuint64_t st[2] = {(cuuint64_t)K * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)kg};
+  cuuint32_t es[3] = {1, 1, 1};
+  return make_map(w, 3, dims, st, box, es);
+}
+
 // K-major matrix [rows][K] bf16, box (64 K, box_rows)
 CUtensorMap mat_map(const __nv_bfloat16 *w, int rows, int K, int box_rows) {
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
@@ -821,9 +870,20 @@ CUtensorMap ws_map(float *ws, int N, int64_t rows) {
   return make_map(ws, 2, dims, st, box, el, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
-constexpr int conv_stages(int BN) { return BN == 256 ? 3 : (BN == 128 ? 4 : 6); }
-constexpr size_t conv_smem(int BN, size_t stat_bytes) {
-  return 1024 + (size_t)conv_stages(BN) * (A_BYTES + BN * BK * 2) + 1024 + kEpiBytes + stat_bytes;
+// the epilogue's statistics slots: [NSLOT][BN][2] floats + NSLOT counts (conv_tc_kernel RS)
+constexpr size_t conv_stat_bytes(int BN, bool OUT16) {
+  return (size_t)(BN * (OUT16 ? 2 : 4) <= 128 ? 8 : 4) * BN * 8 + 32;
+}
+// ring depth: about 144 / 128 KB of operands in flight
+constexpr int conv_stages(int BN, int KG = 1) { return (BN == 256 ? 3 : (BN == 128 ? 4 : 6)) / KG; }
+constexpr size_t conv_smem(int BN, int KG, size_t stat_bytes) {
+  return 1024 + (size_t)conv_stages(BN, KG) * KG * (A_BYTES + BN * BK * 2) + 1024 + kEpiBytes + stat_bytes;
+}
+// channel blocks per stage: 2 where the N tile is narrow (the copies, not the MMAs, bound
+// those tiles) and the reduction has an even number of 64-channel blocks per tap
+int conv_kg(int BN, int CB, int splits) {
+  static const int kmax = env_int("PETRA_CONV_KG", 1);  // 2 measured ~1% slower in the step (DESIGN 7)
+  return (kmax >= 2 && BN <= 128 && CB % 2 == 0 && splits == 1) ? 2 : 1;
 }
 
 // grid of a conv kernel whose epilogue writes BN partials: a multiple of the N-tile
@@ -833,22 +893,24 @@ int conv_stats_grid(int work, int n_tiles_n) {
   return std::max(n_tiles_n, g / n_tiles_n * n_tiles_n);
 }
 
-template <int BN, bool OUT16>
+template <int BN, bool OUT16, int KG>
 void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P0, cudaStream_t st) {
   ConvTCParams P = P0;
   P.f_sp = tc::fastdiv_make(P.splits);
   P.f_nt = tc::fastdiv_make(P.N / BN);
   P.f_ghw = tc::fastdiv_make(P.Hb * P.Wb);
   P.f_wb = tc::fastdiv_make(P.Wb);
-  constexpr int STAGES = conv_stages(BN);
-  const size_t smem = conv_smem(BN, P.stats ? (size_t)BN * 32 + 16 : 0);  // attribute: conv_tc_prepare
+  static const int rs_on = env_int("PETRA_EPI_RS", 1);
+  P.rs = rs_on;
+  constexpr int STAGES = conv_stages(BN, KG);
+  const size_t smem = conv_smem(BN, KG, P.stats ? conv_stat_bytes(BN, OUT16) : 0);  // attribute: conv_tc_prepare
   const int work = (P.M / BM) * (P.N / BN) * P.splits;
   const int grid = conv_stats_grid(work, P.N / BN);
   const CUtensorMap to = out_map(P.out, OUT16, P);
   const CUtensorMap tw = P.splits > 1 ? ws_map(P.ws, P.N, (int64_t)P.splits * P.M) : to;
   // the addend in the output's geometry (fp32 outputs only)
   const CUtensorMap tad = (!OUT16 && P.addend) ? out_map(const_cast<float *>(P.addend), false, P) : to;
-  launch_k(conv_tc_kernel<BN, STAGES, OUT16>, grid, kConvThreads, smem, st, ta, tb, to, tw, tad, P);
+  launch_k(conv_tc_kernel<BN, STAGES, OUT16, KG>, grid, kConvThreads, smem, st, ta, tb, to, tw, tad, P);
   PETRA_LAUNCH_CHECK();
   if (P.splits > 1) {
     int64_t n = (int64_t)P.M * P.N / 4;
@@ -857,28 +919,51 @@ void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParam
   }
 }
 
-// tensor maps are built per launch (host-side, ~1 us); B's box height = BN
-void launch_any(const CUtensorMap &ta, const __nv_bfloat16 *w, int wrows, int wK, ConvTCParams &P, float *ws,
-                bool out16, cudaStream_t st) {
-  ConvPlan pl = conv_plan(P.M, P.N, P.ntaps * P.CB);
+// The plan of one conv GEMM launch: N tile, K split, channel blocks per stage
+struct LaunchPlan {
+  ConvPlan pl;
+  int kg;
+};
+LaunchPlan launch_plan(const ConvTCParams &P, float *ws) {
+  LaunchPlan L;
+  L.pl = conv_plan(P.M, P.N, P.ntaps * P.CB);
+  if (L.pl.splits > 1 && !ws) {
+    L.pl.splits = 1;
+    L.pl.kb_per_split = P.ntaps * P.CB;
+  }
+  L.kg = conv_kg(L.pl.BN, P.CB, L.pl.splits);
+  return L;
+}
+
+// tensor maps are built per launch (host-side, ~1 us); B's box = (64, BN, kg); `ta` was
+// built with the same kg (act_map5)
+void launch_any(const CUtensorMap &ta, const LaunchPlan &L, const __nv_bfloat16 *w, int wrows, int wK,
+                ConvTCParams &P, float *ws, bool out16, cudaStream_t st) {
+  const ConvPlan &pl = L.pl;
   P.splits = pl.splits;
   P.kb_per_split = pl.kb_per_split;
   P.ws = ws;
-  if (pl.splits > 1 && !ws) {
-    P.splits = 1;
-    P.kb_per_split = P.ntaps * P.CB;
-  }
   if (P.splits > 1) P.stats = nullptr;  // stats need final z (split-K: standalone pass)
   if (out16 && P.addend) throw PetraError(PETRA_E_ARG, "conv_tc: addend needs an fp32 output");
-  CUtensorMap tb = mat_map(w, wrows, wK, pl.BN);
+  CUtensorMap tb = mat_map3(w, wrows, wK, pl.BN, L.kg);
+  if (L.kg == 2) {
+    if (out16) {
+      if (pl.BN == 128) launch_conv<128, true, 2>(ta, tb, P, st);
+      else launch_conv<64, true, 2>(ta, tb, P, st);
+    } else {
+      if (pl.BN == 128) launch_conv<128, false, 2>(ta, tb, P, st);
+      else launch_conv<64, false, 2>(ta, tb, P, st);
+    }
+    return;
+  }
   if (out16) {
-    if (pl.BN == 256) launch_conv<256, true>(ta, tb, P, st);
-    else if (pl.BN == 128) launch_conv<128, true>(ta, tb, P, st);
-    else launch_conv<64, true>(ta, tb, P, st);
+    if (pl.BN == 256) launch_conv<256, true, 1>(ta, tb, P, st);
+    else if (pl.BN == 128) launch_conv<128, true, 1>(ta, tb, P, st);
+    else launch_conv<64, true, 1>(ta, tb, P, st);
   } else {
-    if (pl.BN == 256) launch_conv<256, false>(ta, tb, P, st);
-    else if (pl.BN == 128) launch_conv<128, false>(ta, tb, P, st);
-    else launch_conv<64, false>(ta, tb, P, st);
+    if (pl.BN == 256) launch_conv<256, false, 1>(ta, tb, P, st);
+    else if (pl.BN == 128) launch_conv<128, false, 1>(ta, tb, P, st);
+    else launch_conv<64, false, 1>(ta, tb, P, st);
   }
 }
 
@@ -917,10 +1002,11 @@ StatsRows run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const _
   P.oss = 1;
   P.out = out;
   P.stats = stats;
-  CUtensorMap ta = act_map(x, g.B, g.H, g.W, g.Ci, t.Wb, t.R, t.NB, g.s, x_pad);
-  launch_any(ta, w, g.Co, g.K(), P, ws, out16, st);
+  const LaunchPlan L = launch_plan(P, ws);
+  CUtensorMap ta = act_map5(x, g.B, g.H, g.W, g.Ci, t.Wb, t.R, t.NB, g.s, L.kg, x_pad);
+  launch_any(ta, L, w, g.Co, g.K(), P, ws, out16, st);
   if (!P.stats) return {};
-  const int BN = conv_plan(P.M, P.N, P.ntaps * P.CB).BN;
+  const int BN = L.pl.BN;
   StatsRows r;
   r.groups = P.N / BN;
   r.rows = conv_stats_grid((P.M / BM) * (P.N / BN) * P.splits, r.groups);  // one partial row per CTA
@@ -936,7 +1022,6 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_pad, const __
     return;
   }
   Tiling t = tiling(g.B, g.Ho, g.Wo, BM);
-  CUtensorMap ta = act_map(dz, g.B, g.Ho, g.Wo, g.Co, t.Wb, t.R, t.NB, 1, dz_pad);
   ConvTCParams P{};
   P.M = (int)t.M();
   P.N = g.Ci;
@@ -961,7 +1046,9 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_pad, const __
       P.wk[tap] = tap;
     }
     P.oss = 1;
-    launch_any(ta, wt, g.Ci, wK, P, ws, false, st);
+    const LaunchPlan L = launch_plan(P, ws);
+    CUtensorMap ta = act_map5(dz, g.B, g.Ho, g.Wo, g.Co, t.Wb, t.R, t.NB, 1, L.kg, dz_pad);
+    launch_any(ta, L, wt, g.Ci, wK, P, ws, false, st);
     return;
   }
   // stride 2: phase (ph, pw) of dx gets the taps with kh = ph + p (mod 2), kw = pw + p (mod 2);
@@ -986,7 +1073,9 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_pad, const __
       P.ntaps = n;
       P.ph = ph;
       P.pw = pw;
-      launch_any(ta, wt, g.Ci, wK, P, ws, false, st);
+      const LaunchPlan L = launch_plan(P, ws);
+      CUtensorMap ta = act_map5(dz, g.B, g.Ho, g.Wo, g.Co, t.Wb, t.R, t.NB, 1, L.kg, dz_pad);
+      launch_any(ta, L, wt, g.Ci, wK, P, ws, false, st);
     }
   if (empty_mask) {
     int64_t cnt = (int64_t)g.B * g.H * g.W * (g.Ci / 4);
@@ -1028,16 +1117,21 @@ void launch_wgrad(const CUtensorMap &tx, const CUtensorMap &tdz, const WgradPara
 void conv_tc_prepare() {
   static std::once_flag once;
   std::call_once(once, [] {
-    auto set = [](const void *f, int BN) {
+    auto set = [](const void *f, int BN, int KG) {
       PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)conv_smem(BN, kMaxStatN * 32 + 16)));
+                                      (int)conv_smem(BN, KG, std::max(conv_stat_bytes(BN, true),
+                                                                      conv_stat_bytes(BN, false)))));
     };
-    set((const void *)conv_tc_kernel<256, conv_stages(256), false>, 256);
-    set((const void *)conv_tc_kernel<128, conv_stages(128), false>, 128);
-    set((const void *)conv_tc_kernel<64, conv_stages(64), false>, 64);
-    set((const void *)conv_tc_kernel<256, conv_stages(256), true>, 256);
-    set((const void *)conv_tc_kernel<128, conv_stages(128), true>, 128);
-    set((const void *)conv_tc_kernel<64, conv_stages(64), true>, 64);
+    set((const void *)conv_tc_kernel<256, conv_stages(256), false, 1>, 256, 1);
+    set((const void *)conv_tc_kernel<128, conv_stages(128), false, 1>, 128, 1);
+    set((const void *)conv_tc_kernel<64, conv_stages(64), false, 1>, 64, 1);
+    set((const void *)conv_tc_kernel<256, conv_stages(256), true, 1>, 256, 1);
+    set((const void *)conv_tc_kernel<128, conv_stages(128), true, 1>, 128, 1);
+    set((const void *)conv_tc_kernel<64, conv_stages(64), true, 1>, 64, 1);
+    set((const void *)conv_tc_kernel<128, conv_stages(128, 2), false, 2>, 128, 2);
+    set((const void *)conv_tc_kernel<64, conv_stages(64, 2), false, 2>, 64, 2);
+    set((const void *)conv_tc_kernel<128, conv_stages(128, 2), true, 2>, 128, 2);
+    set((const void *)conv_tc_kernel<64, conv_stages(64, 2), true, 2>, 64, 2);
     auto setw = [](const void *f, int STAGES, int BN) {
       size_t smem = (size_t)STAGES * (2 * 64 * 64 * 2 + BN * 64 * 2) + 1024 + 256;
       PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1138,9 +1232,12 @@ void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_padded, c
     return;
   }
   WgradPlan w = wgrad_plan(g);
-  CUtensorMap tx = act_map(x, g.B, g.H, g.W, g.Ci, w.t.Wb, w.t.R, w.t.NB, g.s, x_padded);
-  // dz [B][Ho][Wo][Co], box (64 ch, 64 padded pixels); padding pixels out of bounds -> 0
-  CUtensorMap tdz = act_map(dz, g.B, g.Ho, g.Wo, g.Co, w.t.Wb, w.t.R, w.t.NB, 1, dz_padded);
+  static const bool xg_on = env_int("PETRA_WGRAD_XG", 1) != 0;
+  const int xg = (xg_on && g.Ci % 128 == 0) ? 2 : 1;
+  CUtensorMap tx = act_map5(x, g.B, g.H, g.W, g.Ci, w.t.Wb, w.t.R, w.t.NB, g.s, xg, x_padded);
+  // dz [B][Ho][Wo][Co], box (64 ch, 64 padded pixels, BN / 64 channel blocks); padding
+  // pixels out of bounds -> 0
+  CUtensorMap tdz = act_map5(dz, g.B, g.Ho, g.Wo, g.Co, w.t.Wb, w.t.R, w.t.NB, 1, w.BN / 64, dz_padded);
   WgradParams P{};
   P.Mr = g.K();
   P.N = g.Co;
@@ -1155,6 +1252,7 @@ void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_padded, c
   P.n_mt = w.n_mt;
   P.n_nt = w.n_nt;
   P.splits = w.splits;
+  P.xg = xg;
   P.out = w.splits > 1 ? ws : dw;
   if (w.BN == 256) launch_wgrad<256, 3>(tx, tdz, P, st);
   else if (w.BN == 128) launch_wgrad<128, 4>(tx, tdz, P, st);

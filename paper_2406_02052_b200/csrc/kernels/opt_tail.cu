@@ -9,6 +9,8 @@
 // tail: GAP over H,W of concat(x1,x2), Linear + bias,
 //          batch-mean softmax cross-entropy, its VJP; deterministic reductions.
 // maxpool 3x3/s2/p1 with first-index ties.
+#include <cmath>
+
 #include "../kernels.h"
 
 namespace petra {
@@ -441,11 +443,54 @@ void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *thet
   PETRA_LAUNCH_CHECK();
 }
 
+// Evaluation of the classifier (the running statistics "are then used
+// during model evaluation"): per row, the CE loss and whether the first-index argmax of
+// the logits equals the label; correct counts are integer atomics (exact)
+__global__ void eval_rows_kernel(const float *__restrict__ logits, const int32_t *__restrict__ labels, int B, int N,
+                                 float *__restrict__ loss_row, int *__restrict__ correct) {
+  pdl_wait_trigger();
+  __shared__ float sm[32];
+  __shared__ int si[32];
+  const int b = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+  const float *z = logits + (size_t)b * N;
+  float m = -INFINITY;
+  int im = N;
+  for (int n = t; n < N; n += blockDim.x)
+    if (z[n] > m) { m = z[n]; im = n; }
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, im, o);
+    if (m2 > m || (m2 == m && i2 < im)) { m = m2; im = i2; }
+  }
+  if (lane == 0) { sm[w] = m; si[w] = im; }
+  __syncthreads();
+  if (t == 0) {
+    for (int k = 1; k < nw; ++k)
+      if (sm[k] > sm[0] || (sm[k] == sm[0] && si[k] < si[0])) { sm[0] = sm[k]; si[0] = si[k]; }
+  }
+  __syncthreads();
+  m = sm[0];
+  const int arg = si[0];
+  float e = 0.f;
+  for (int n = t; n < N; n += blockDim.x) e += expf(z[n] - m);
+  for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  __syncthreads();
+  if (lane == 0) sm[w] = e;
+  __syncthreads();
+  if (t == 0) {
+    float tot = 0.f;
+    for (int k = 0; k < nw; ++k) tot += sm[k];
+    const int y = labels[b];
+    loss_row[b] = logf(tot) + m - z[y];
+    if (arg == y) atomicAdd(correct, 1);
+  }
+}
+
 void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int C, const float *w,
                            const float *bias, int N, const int32_t *labels, float *feat, float *logits,
                            float *dlogits, float *loss_row, float *dfeat, float *dw, float *db, float *d1,
                            float *d2, float *loss, int *nonfinite, float *fc_ws, int64_t fc_ws_floats,
-                           cudaStream_t st) {
+                           cudaStream_t st, int *correct) {
   int Cin = 2 * C;
   launch_k(gap_kernel, dim3((unsigned)cdiv(Cin, 128), B), 128, 0, st, x1, x2, B, HW, C, feat);
   PETRA_LAUNCH_CHECK();
@@ -471,6 +516,13 @@ void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int 
   };
   // logits[b][n] = sum_c feat[b][c] w[n][c] + bias[n]
   gemm(feat, Cin, 1, w, 1, Cin, bias, B, N, Cin, logits);
+  if (correct) {  // evaluation: loss and correct count only (no gradients)
+    launch_k(eval_rows_kernel, B, 256, 0, st, logits, labels, B, N, loss_row, correct);
+    PETRA_LAUNCH_CHECK();
+    launch_k(loss_mean_kernel, 1, 32, 0, st, loss_row, B, loss, nonfinite);
+    PETRA_LAUNCH_CHECK();
+    return;
+  }
   launch_k(ce_kernel, B, 256, 0, st, logits, labels, B, N, dlogits, loss_row);
   PETRA_LAUNCH_CHECK();
   launch_k(loss_mean_kernel, 1, 32, 0, st, loss_row, B, loss, nonfinite);

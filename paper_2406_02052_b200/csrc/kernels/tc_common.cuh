@@ -125,6 +125,22 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *m, uin
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *m, uint64_t *bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *m, uint64_t *bar, int c0, int c1, int c2,
+                                            int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
 // TMA stores (smem -> global, bulk-group completion; out-of-bounds elements are skipped)
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *m, const void *src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -334,20 +350,27 @@ __device__ __forceinline__ void chan_merge(T &n, T &m, T &M2, T nb, T mb, T M2b)
   M2 += M2b + d * d * (n * nb / nn);
   n = nn;
 }
-// A CTA's partial statistics row from its 4 lane quarters: sq[quarter][BN][2] holds
-// (mean, M2) per column, cnt[quarter] the quarter's valid-row count; merged in quarter
-// order and written as (mean, M2) to row[BN][2] (global), the count to *row_n.
+// A CTA's partial statistics row from its NQ slots (4 lane quarters, or 8 epilogue warps
+// when the warps split rows): sq[slot][BN][2] holds (mean, M2) per column, cnt[slot] the
+// slot's valid-row count; merged in slot order and written as (mean, M2) to row[BN][2]
+// (global), the count to *row_n.
+template <int NQ = 4>
 __device__ __forceinline__ void cta_stats_row(const float *sq, const int *cnt, int BN, int tid, int nthreads,
                                               float *row, float *row_n) {
   for (int c = tid; c < BN; c += nthreads) {
     float n = 0.f, m = 0.f, M2 = 0.f;
 #pragma unroll
-    for (int qq = 0; qq < 4; ++qq)
+    for (int qq = 0; qq < NQ; ++qq)
       chan_merge(n, m, M2, (float)cnt[qq], sq[(qq * BN + c) * 2], sq[(qq * BN + c) * 2 + 1]);
     row[2 * c] = m;
     row[2 * c + 1] = M2;
   }
-  if (tid == 0) *row_n = (float)(cnt[0] + cnt[1] + cnt[2] + cnt[3]);
+  if (tid == 0) {
+    int t = 0;
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) t += cnt[qq];
+    *row_n = (float)t;
+  }
 }
 
 }  // namespace tc

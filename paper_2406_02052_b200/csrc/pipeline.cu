@@ -89,8 +89,14 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
   if (j1 < 1) throw PetraError(PETRA_E_ARG, "rank owns no stage");
   streams_.assign(J_ + 2, nullptr);
   done_.assign(J_ + 2, nullptr);
+  // stage streams rank between a stage's backward stream (highest) and its wgrad stream
+  // (lowest) when stream priorities are on (stage.cu, PETRA_STREAM_PRIO)
+  int prio_lo = 0, prio_hi = 0;
+  PETRA_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  const bool prio_on = env_int("PETRA_STREAM_PRIO", 1) != 0;
   for (int j = j0; j <= j1; ++j) {
-    PETRA_CUDA(cudaStreamCreateWithFlags(&streams_[j], cudaStreamNonBlocking));
+    if (prio_on) PETRA_CUDA(cudaStreamCreateWithPriority(&streams_[j], cudaStreamNonBlocking, (prio_lo + prio_hi) / 2));
+    else PETRA_CUDA(cudaStreamCreateWithFlags(&streams_[j], cudaStreamNonBlocking));
     PETRA_CUDA(cudaEventCreateWithFlags(&done_[j], cudaEventDisableTiming));
   }
   PETRA_CUDA(cudaEventCreateWithFlags(&start_, cudaEventDisableTiming));

@@ -329,11 +329,19 @@ void Stage::build() {
     PETRA_CUDA(cudaMemset(counters_[c]->p, 0, max_ctr * sizeof(unsigned)));
     wgrad_ws_[c] = dalloc(std::max<size_t>(max_ws, 16));
   }
-  PETRA_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  // stream priorities (PETRA_STREAM_PRIO=1): the backward -- a stage's longer half, on the
+  // tick's critical path -- outranks the forward; the wgrads (needed only by the update)
+  // rank lowest; the block scheduler then hands freed SMs to the critical work first
+  static const bool prio_on = env_int("PETRA_STREAM_PRIO", 1) != 0;
+  int prio_lo = 0, prio_hi = 0;
+  PETRA_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  if (prio_on) PETRA_CUDA(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, prio_hi));
+  else PETRA_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
   PETRA_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
   PETRA_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
   if (tc_ && env_int("PETRA_WGRAD_STREAM", 1)) {
-    PETRA_CUDA(cudaStreamCreateWithFlags(&wg_, cudaStreamNonBlocking));
+    if (prio_on) PETRA_CUDA(cudaStreamCreateWithPriority(&wg_, cudaStreamNonBlocking, prio_lo));
+    else PETRA_CUDA(cudaStreamCreateWithFlags(&wg_, cudaStreamNonBlocking));
     PETRA_CUDA(cudaEventCreateWithFlags(&wg_fork_, cudaEventDisableTiming));
     PETRA_CUDA(cudaEventCreateWithFlags(&wg_join_, cudaEventDisableTiming));
     wg_ws_ = dalloc(std::max<size_t>(max_ws, 16));
@@ -351,6 +359,8 @@ void Stage::build() {
   PETRA_CUDA(cudaMallocHost(&lr_host_, kLrRing * sizeof(float)));
   if (tc_) conv_tc_prepare();
   nonfinite_ = dalloc(sizeof(int));
+  evalflag_ = dalloc(sizeof(int));  // the evaluation tail's non-finite flag (not latched)
+  PETRA_CUDA(cudaMemset(evalflag_->p, 0, sizeof(int)));
   PETRA_CUDA(cudaMemset(nonfinite_->p, 0, sizeof(int)));
 
   // ---- output-target planning (see header of forward/backward)
@@ -685,6 +695,12 @@ const StatsFold *Stage::take_fold(Layer &L) {
 
 void Stage::layer_stats(Layer &L, bool running, cudaStream_t st) {
   float *b = bufs_->as<float>();
+  if (eval_) {  // evaluation: normalise by the running statistics
+    L.stats_rows() = StatsRows{};
+    bn_running_constants(b + L.rm_off, b + L.rv_off, L.g.Co, desc_.bn_eps, L.mean()->as<float>(),
+                         L.invstd()->as<float>(), st);
+    return;
+  }
   if (L.stats_rows().rows > 0) {  // sums already produced by the tensor-core conv epilogue
     flush_fold(st);
     StatsFold f;
@@ -1008,6 +1024,7 @@ std::vector<int> Stage::take_pop(uint64_t mb) {
 // comparison buffers of this forward (slot n_fwd_ of each ring): the received input and
 // theta^t, as a delayed-gradient method with weight stashing would keep them
 void Stage::enqueue_compare(const float *x1, const float *x2, cudaStream_t st) {
+  if (eval_) return;
   if (!cmp_in_[0].empty()) {
     const size_t s = (size_t)(n_fwd_ % (int64_t)cmp_in_[0].size());
     copy_d2d(cmp_in_[0][s]->as<float>(), x1, in_.numel(), st);
@@ -1044,8 +1061,10 @@ void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *
     } else {
       ready = false;
       int slot = push[i];
-      copy_d2d(u.fifo.slot0[slot]->as<float>(), cur[0], u.in.numel(), st);
-      if (u.d.kind == PETRA_UNIT_DS) copy_d2d(u.fifo.slot1[slot]->as<float>(), cur[1], u.in.numel(), st);
+      if (!eval_) {  // an evaluation forward keeps nothing for a backward
+        copy_d2d(u.fifo.slot0[slot]->as<float>(), cur[0], u.in.numel(), st);
+        if (u.d.kind == PETRA_UNIT_DS) copy_d2d(u.fifo.slot1[slot]->as<float>(), cur[1], u.in.numel(), st);
+      }
       // a DS unit writes the bf16 operand of the next reversible unit's src half too
       Bf16Out ob = (u.d.kind == PETRA_UNIT_DS && i + 1 < n && units_[i + 1].d.kind == PETRA_UNIT_REV)
                        ? src_operand(units_[i + 1]) : Bf16Out{};
@@ -1163,6 +1182,62 @@ void Stage::enqueue_tail(const float *x1, const float *x2, const int32_t *labels
     copy_d2d(od1, cd[0], in_.numel(), st);
     copy_d2d(od2, cd[1], in_.numel(), st);
   }
+}
+
+// ---- evaluation (the running statistics of batch normalisation "are then
+// used during model evaluation"): the forward of every unit with BN on the running
+// statistics; nothing is pushed, updated or counted.  Non-reversible units stage their
+// bf16 operand in the next free FIFO slot (peeked, not reserved).
+std::vector<int> Stage::peek_push() const {
+  std::vector<int> slots(units_.size(), -1);
+  for (size_t i = 0; i < units_.size(); ++i) {
+    const Fifo &f = units_[i].fifo;
+    if (units_[i].d.kind == PETRA_UNIT_DS || units_[i].d.kind == PETRA_UNIT_STEM) {
+      if (f.size >= f.cap) throw PetraError(PETRA_E_ARG, "evaluation needs a free FIFO slot (drain the pipeline)");
+      slots[i] = (f.head + f.size) % f.cap;
+    }
+  }
+  return slots;
+}
+
+void Stage::eval(const float *x1, const float *x2, float *o1, float *o2, cudaStream_t st) {
+  NvtxRange nr("stage eval");
+  if (is_last_) throw PetraError(PETRA_E_ARG, "the final stage runs petra_stage_eval_tail");
+  if (!x1 || (!stem_first() && !x2) || !o1 || !o2) throw PetraError(PETRA_E_ARG, "NULL activation pointer");
+  std::vector<int> push = peek_push();
+  ctx_ = 0;
+  eval_ = true;
+  try {
+    enqueue_forward(x1, x2, o1, o2, push, false, nullptr, st);
+  } catch (...) {
+    eval_ = false;
+    throw;
+  }
+  eval_ = false;
+}
+
+void Stage::eval_tail(const float *x1, const float *x2, const int32_t *labels, int *correct, float *loss,
+                      cudaStream_t st) {
+  NvtxRange nr("stage eval tail");
+  if (!is_last_) throw PetraError(PETRA_E_ARG, "petra_stage_eval_tail on a stage without a tail unit");
+  if (!x1 || (!stem_first() && !x2) || !labels || !correct || !loss) throw PetraError(PETRA_E_ARG, "NULL argument");
+  std::vector<int> push = peek_push();
+  ctx_ = 0;
+  eval_ = true;
+  try {
+    const float *cur[2];
+    enqueue_forward(x1, x2, nullptr, nullptr, push, false, cur, st);
+    Unit &t = units_.back();
+    const float *th = theta_->as<float>();
+    tail_forward_backward(cur[0], cur[1], desc_.batch, t.in.H * t.in.W, t.in.C, th + t.fc_w, th + t.fc_b,
+                          t.d.classes, labels, feat_->as<float>(), logits_->as<float>(), dlogits_->as<float>(),
+                          lossrow_->as<float>(), nullptr, nullptr, nullptr, nullptr, nullptr, loss,
+                          evalflag_->as<int>(), fc_ws_->as<float>(), fc_ws_floats_, st, correct);
+  } catch (...) {
+    eval_ = false;
+    throw;
+  }
+  eval_ = false;
 }
 
 // ---- public entry points (standalone stages: direct enqueue)

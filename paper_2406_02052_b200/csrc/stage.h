@@ -160,6 +160,9 @@ class Stage {
   void forward(uint64_t mb, const float *x1, const float *x2, float *o1, float *o2, cudaStream_t st);
   void backward(uint64_t mb, const float *xt1, const float *xt2, const float *d1, const float *d2, float *oxt1,
                 float *oxt2, float *od1, float *od2, float lr, cudaStream_t st);
+  // evaluation forward (BN on the running statistics, no FIFO push, no state change)
+  void eval(const float *x1, const float *x2, float *o1, float *o2, cudaStream_t st);
+  void eval_tail(const float *x1, const float *x2, const int32_t *labels, int *correct, float *loss, cudaStream_t st);
   void tail(uint64_t mb, const float *x1, const float *x2, const int32_t *labels, float lr, float *oxt1,
             float *oxt2, float *od1, float *od2, float *loss, cudaStream_t st);
   void tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph);
@@ -204,6 +207,7 @@ class Stage {
   bool wg_active_ = false;
   void join_wgrads(cudaStream_t st);
   DevPtr nonfinite_;
+  DevPtr evalflag_;
   // tail workspace
   DevPtr feat_, logits_, dlogits_, lossrow_, dfeat_, tail_d_[2], fc_ws_;
   int64_t fc_ws_floats_ = 0;
@@ -211,6 +215,8 @@ class Stage {
   int64_t version_ = 0;                          // optimizer updates applied
   int64_t t_ = 1;                                // Alg. 1 step counter t (reading c12: starts at 1)
   int64_t n_fwd_ = 0, n_bwd_ = 0;
+  bool eval_ = false;                          // enqueuing an evaluation forward
+  std::vector<int> peek_push() const;          // FIFO slots an evaluation forward may use (not reserved)
   // Table 3 comparison buffers (petra_stage_desc.compare_buffers): a ring of stage inputs
   // (delayed-gradient input buffer) and a ring of theta copies (weight stash), one slot
   // written per forward

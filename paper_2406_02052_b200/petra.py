@@ -102,6 +102,15 @@ class Stage:
         L.call("petra_stage_tail", self.h, mb, _ptr(x1), _ptr(x2), _ptr(labels), float(lr), _ptr(oxt1),
                _ptr(oxt2), _ptr(od1), _ptr(od2), _ptr(loss), _stream(stream))
 
+    def eval(self, x1, x2, o1, o2, stream=None):
+        """petra_stage_eval: forward with BN on the running statistics (no state change)."""
+        L.call("petra_stage_eval", self.h, _ptr(x1), _ptr(x2), _ptr(o1), _ptr(o2), _stream(stream))
+
+    def eval_tail(self, x1, x2, labels, correct, loss, stream=None):
+        """petra_stage_eval_tail: evaluation forward + classifier; correct (int32[1]) += hits."""
+        L.call("petra_stage_eval_tail", self.h, _ptr(x1), _ptr(x2), _ptr(labels), _ptr(correct), _ptr(loss),
+               _stream(stream))
+
 
 def report_dict(rep: L.PetraTickReport):
     J = rep.n_stages
