@@ -391,7 +391,10 @@ void Stage::build() {
     if (u.d.kind == PETRA_UNIT_DS || u.d.kind == PETRA_UNIT_STEM) {
       u.fifo.cap = is_last_ ? 1 : cap;
       for (int s = 0; s < u.fifo.cap; ++s) {
-        u.fifo.slot0.push_back(dalloc(u.in.numel() * sizeof(float)));
+        // the stem's fp32 input is needed only by SIMT passes: with its bf16 operand in the
+        // slot (tensor cores) and no backward message (stage 1 sends none), it is not kept
+        if (!(u.d.kind == PETRA_UNIT_STEM && u.phi[0].fifo_backed))
+          u.fifo.slot0.push_back(dalloc(u.in.numel() * sizeof(float)));
         if (u.d.kind == PETRA_UNIT_DS) u.fifo.slot1.push_back(dalloc(u.in.numel() * sizeof(float)));
         if (u.d.kind == PETRA_UNIT_DS && u.pa.fifo_backed) {
           u.fifo.bslot0.push_back(dalloc(u.in.numel() * sizeof(__nv_bfloat16)));
@@ -508,8 +511,9 @@ void Stage::memory(petra_memory_report *r) const {
       layer(u.pb);
     }
     uint64_t slot = 0, all = 0;
-    for (size_t s = 0; s < u.fifo.slot0.size(); ++s) {
-      uint64_t one = b(u.fifo.slot0[s]) + (s < u.fifo.slot1.size() ? b(u.fifo.slot1[s]) : 0) +
+    for (size_t s = 0; s < (size_t)u.fifo.cap; ++s) {
+      uint64_t one = (s < u.fifo.slot0.size() ? b(u.fifo.slot0[s]) : 0) +
+                     (s < u.fifo.slot1.size() ? b(u.fifo.slot1[s]) : 0) +
                      (s < u.fifo.bslot0.size() ? b(u.fifo.bslot0[s]) : 0) +
                      (s < u.fifo.bslot1.size() ? b(u.fifo.bslot1[s]) : 0);
       all += one;
@@ -1044,10 +1048,19 @@ void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *
   float *outs[2] = {o1, o2};
   const int n = (int)units_.size() - (is_last_ ? 1 : 0);
   bool ready = false;  // bf16 operand of this unit's src already written by its producer
+  static const bool in_place_push = env_int("PETRA_PUSH_IN_PLACE", 1) != 0;
   for (int i = 0; i < n; ++i) {
     Unit &u = units_[i];
     float *tgt[2];
     for (int h = 0; h < 2; ++h) tgt[h] = u.fout[h] ? u.fout[h]->as<float>() : outs[h];
+    // the units before a DS unit write its input straight into the DS's FIFO slot of this
+    // micro-batch (the slot the DS forward would copy it into: the copy becomes a no-op)
+    int nx = i + 1;
+    while (nx < n && units_[nx].d.kind == PETRA_UNIT_REV) ++nx;
+    if (in_place_push && nx < n && units_[nx].d.kind == PETRA_UNIT_DS && push[nx] >= 0) {
+      tgt[0] = units_[nx].fifo.slot0[push[nx]]->as<float>();
+      tgt[1] = units_[nx].fifo.slot1[push[nx]]->as<float>();
+    }
     if (u.d.kind == PETRA_UNIT_REV) {
       float *o[2] = {nullptr, nullptr};
       int d = u.dst();
@@ -1061,7 +1074,7 @@ void Stage::enqueue_forward(const float *x1, const float *x2, float *o1, float *
     } else {
       ready = false;
       int slot = push[i];
-      if (!eval_) {  // an evaluation forward keeps nothing for a backward
+      if (!eval_ && !u.fifo.slot0.empty()) {  // an evaluation forward keeps nothing for a backward
         copy_d2d(u.fifo.slot0[slot]->as<float>(), cur[0], u.in.numel(), st);
         if (u.d.kind == PETRA_UNIT_DS) copy_d2d(u.fifo.slot1[slot]->as<float>(), cur[1], u.in.numel(), st);
       }
@@ -1120,7 +1133,7 @@ void Stage::enqueue_backward_walk(int last_unit, bool recompute, const float *cx
     } else {
       ready = false;
       int slot = pop[i];
-      const float *xin[2] = {u.fifo.slot0[slot]->as<float>(),
+      const float *xin[2] = {u.fifo.slot0.empty() ? nullptr : u.fifo.slot0[slot]->as<float>(),
                              u.d.kind == PETRA_UNIT_DS ? u.fifo.slot1[slot]->as<float>() : nullptr};
       float *td[2] = {nullptr, nullptr};
       if (u.d.kind == PETRA_UNIT_DS)

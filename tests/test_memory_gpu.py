@@ -42,10 +42,10 @@ def test_stage_memory_categories(precision, k):
         fifo = 0
         tc = precision == L.BF16_TC
         for u, (B, H, W, C) in zip(us, ins[i0:i0 + counts[j - 1]]):
-            # fp32 input (+ its bf16 conv operands on the tensor-core path: the stem's
-            # 4-channel image copy, both DS halves)
-            if u.kind == L.UNIT_STEM:
-                fifo += cap * B * H * W * (C * 4 + (4 * 2 if tc else 0))
+            # fp32 input (+ its bf16 conv operands on the tensor-core path: both DS halves;
+            # the stem keeps only its 4-channel bf16 image copy there)
+            if u.kind == L.UNIT_STEM:  # tensor cores: the 4-channel bf16 copy only (no fp32 kept)
+                fifo += cap * B * H * W * (4 * 2 if tc else C * 4)
             elif u.kind == L.UNIT_DS:
                 fifo += cap * 2 * B * H * W * C * (4 + (2 if tc else 0))
         assert m["fifo"] == fifo
