@@ -88,7 +88,10 @@ inline RedGeom red_geom(int64_t M, int C, int RT, int per_sm = 1) {
   // one wave: one block per SM (1024 / 512 threads, >= 64 KB of loads in flight), few
   // partials to merge
   int64_t want = std::max<int64_t>(1, (int64_t)per_sm * kNumSMs / g.ctiles);
-  g.nrb = (int)std::max<int64_t>(1, std::min<int64_t>(want, cdiv(M, 4 * g.RG)));
+  // at least `min_rows` rows per block (PETRA_BN_MIN_ROWS, default 128; at least 4 row groups): small
+  // tensors otherwise spread over hundreds of blocks of a few rows each
+  static const int min_rows = env_int("PETRA_BN_MIN_ROWS", 128);  // 128: R18 +2.9 % (DESIGN 7)
+  g.nrb = (int)std::max<int64_t>(1, std::min<int64_t>(want, cdiv(M, std::max(4 * g.RG, min_rows))));
   g.rpb = cdiv(M, g.nrb);
   g.nrb = (int)cdiv(M, g.rpb);
   return g;

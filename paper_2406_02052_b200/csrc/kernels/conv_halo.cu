@@ -243,7 +243,7 @@ conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (c >= BN) break;
           float v[CW];
 #pragma unroll
-          for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
+          tc::tmem_ld16xN<CW / 16>(trow + c, v);
           if (arow) {
 #pragma unroll
             for (int jj = 0; jj < CW; jj += 4) {
@@ -586,13 +586,12 @@ wgrad_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         const int tap = half ? tap_b(i) : tap_a(i);
         const bool store = !(i == 4 && half == 0);  // the repeated tap 7
         const int r = tap * P.Ci + cb * 64 + ci;
-#pragma unroll 1
-        for (int c = 0; c < 64; c += 16) {
-          float v[16];
-          tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + i * 64 + c, v);
+        {
+          float v[64];
+          tc::tmem_ld16xN<4>(tmem_base + ((uint32_t)(q * 32) << 16) + i * 64, v);
           if (store) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) o[(size_t)(c + j) * P.Mr + r] = v[j];
+            for (int j = 0; j < 64; ++j) o[(size_t)j * P.Mr + r] = v[j];
           }
         }
       }

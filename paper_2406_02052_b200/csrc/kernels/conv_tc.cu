@@ -261,8 +261,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll 1
         for (int c = RS ? 0 : 32 * hc; c < BN; c += RS ? 32 : 64) {
           float v[32];
-          tc::tmem_ld16(trow + c, *reinterpret_cast<float(*)[16]>(v));
-          tc::tmem_ld16(trow + c + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+          tc::tmem_ld16xN<2>(trow + c, v);
           acquire();
           stage_row<false>(ebuf + eb * kEpiBuf, lane, v);
           flush(&tmW, nt * BN + c, sp * P.M + mt * BM + q * 32, 0, 0, false);
@@ -280,7 +279,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (c >= BN) break;
           float v[CW];
 #pragma unroll
-          for (int h = 0; h < CW; h += 16) tc::tmem_ld16(trow + c + h, *reinterpret_cast<float(*)[16]>(v + h));
+          tc::tmem_ld16xN<CW / 16>(trow + c, v);
           if (!OUT16 && P.addend) {  // the addend box (same geometry as the store box) by TMA into the buffer
             acquire();
             if (lane == 0) {
@@ -610,12 +609,12 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__
       const int r = mt * 128 + row;
       float *o = P.out + (int64_t)sp * P.N * P.Mr;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        float v[16];
-        tc::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+      for (int c = 0; c < BN; c += 64) {
+        float v[64];
+        tc::tmem_ld16xN<4>(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
         if (r < P.Mr) {
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) o[(int64_t)(nt * BN + c + jj) * P.Mr + r] = v[jj];
+          for (int jj = 0; jj < 64; ++jj) o[(int64_t)(nt * BN + c + jj) * P.Mr + r] = v[jj];
         }
       }
       tc::tc_fence_before();

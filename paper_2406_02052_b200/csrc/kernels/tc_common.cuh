@@ -232,6 +232,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// NC consecutive 16-column chunks with ONE wait: the tcgen05.ld's go out back to back
+// and their latencies overlap.  Every chunk's registers are threaded through an empty asm
+// that follows the (volatile) wait, so no use of them can be scheduled before it.
+template <int NC>
+__device__ __forceinline__ void tmem_ld16xN(uint32_t taddr, float *v) {
+  uint32_t r[NC][16];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[c][0]), "=r"(r[c][1]), "=r"(r[c][2]), "=r"(r[c][3]), "=r"(r[c][4]), "=r"(r[c][5]), "=r"(r[c][6]), "=r"(r[c][7]), "=r"(r[c][8]), "=r"(r[c][9]), "=r"(r[c][10]), "=r"(r[c][11]), "=r"(r[c][12]), "=r"(r[c][13]), "=r"(r[c][14]), "=r"(r[c][15])
+                 : "r"(taddr + 16 * c));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    asm volatile("" : "+r"(r[c][0]), "+r"(r[c][1]), "+r"(r[c][2]), "+r"(r[c][3]), "+r"(r[c][4]), "+r"(r[c][5]), "+r"(r[c][6]), "+r"(r[c][7]), "+r"(r[c][8]), "+r"(r[c][9]), "+r"(r[c][10]), "+r"(r[c][11]), "+r"(r[c][12]), "+r"(r[c][13]), "+r"(r[c][14]), "+r"(r[c][15]));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[16 * c + i] = __uint_as_float(r[c][i]);
+  }
+}
+
 // Column sums of a 32-row x 16-column fragment held one row per lane: butterfly
 // transpose-reduce (8+4+2+1+1 shuffles).  Afterwards lane L holds the sum over the
 // 32 rows of column (L >> 1) in x[0] (lanes 2k, 2k+1 both).
