@@ -1,6 +1,7 @@
 // kernels.h -- launchers of the PETRA B200 kernels (internal C++ interface, not the ABI).
 #pragma once
 #include <algorithm>
+#include <vector>
 #include "common.cuh"
 
 namespace petra {
@@ -124,12 +125,19 @@ struct SgdSeg {
   __nv_bfloat16 *w_bf16;         // nullable: bf16 shadow [Co][k][k][Ci]
   __nv_bfloat16 *wt_bf16;        // nullable: dgrad operand [Ci][k][k][Co], taps flipped
 };
+// work item of the update: a 32 x 32 tile (lo = tile index) of a conv weight with bf16
+// shadows, or elements [lo, hi) of another tensor (built once per stage: sgd_chunks)
+struct SgdChunk {
+  int seg;
+  int64_t lo, hi;
+};
+std::vector<SgdChunk> sgd_chunks(const std::vector<SgdSeg> &segs);
 // lr_dev: device scalar (written per tick from pinned host memory, so a captured
 // CUDA graph replays with the current learning rate)
 enum { SGD_PLAIN = 0, SGD_ACCUMULATE = 1, SGD_ACC_UPDATE = 2 };
-void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *theta, float *v, const float *grad,
-                float *acc, int k, int mode, const float *lr_dev, float mom, float wd, int nesterov, cudaStream_t st,
-                bool shadow_only, int *nonfinite);  // nonfinite: device flag set (2) by a NaN / Inf in Delta
+void sgd_update(const SgdSeg *segs_dev, int nseg, const SgdChunk *chunks_dev, int nchunks, float *theta, float *v,
+                const float *grad, float *acc, int k, int mode, const float *lr_dev, float mom, float wd, int nesterov,
+                cudaStream_t st, bool shadow_only, int *nonfinite);  // nonfinite: device flag set (2) by a NaN / Inf in Delta
 void tail_forward_backward(const float *x1, const float *x2, int B, int HW, int C, const float *w,
                            const float *bias, int N, const int32_t *labels, float *feat, float *logits,
                            float *dlogits, float *loss_row, float *dfeat, float *dw, float *db, float *d1,

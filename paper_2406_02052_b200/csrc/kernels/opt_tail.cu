@@ -16,56 +16,67 @@
 namespace petra {
 namespace {
 
-__global__ void __launch_bounds__(256) sgd_kernel(const SgdSeg *__restrict__ segs, float *__restrict__ theta,
-                                                  float *__restrict__ v, const float *__restrict__ grad,
-                                                  float *__restrict__ acc, float inv_k, int mode,
-                                                  const float *__restrict__ lr_dev, float mom, float wd, int nesterov,
-                                                  int shadow_only, int *__restrict__ nonfinite) {
+// One launch over the whole stage: a work item is a 32(co) x 32(ci) tile of one tap of a
+// conv weight with bf16 shadows, or a run of up to 1024 elements of any other tensor
+// (kernels.h SgdChunk, built once per stage); blocks stride over the items, so small
+// tensors (BN gamma / beta, biases) cost one item instead of a grid row of idle blocks.
+__global__ void __launch_bounds__(256) sgd_kernel(const SgdSeg *__restrict__ segs, const SgdChunk *__restrict__ chunks,
+                                                  int nchunks, float *__restrict__ theta, float *__restrict__ v,
+                                                  const float *__restrict__ grad, float *__restrict__ acc, float inv_k,
+                                                  int mode, const float *__restrict__ lr_dev, float mom, float wd,
+                                                  int nesterov, int shadow_only, int *__restrict__ nonfinite) {
   pdl_wait_trigger();
   // mode (Alg. 1 lines 19-22):  SGD_PLAIN   k = 1, update with Delta;
   // SGD_ACCUMULATE  acc += Delta/k, no update;  SGD_ACC_UPDATE  update with acc + Delta/k, acc = 0
-  const SgdSeg sg = segs[blockIdx.y];
-  if (shadow_only && !sg.w_bf16) return;
-  const float lam = sg.decay ? wd : 0.f;
-  const float lr = shadow_only ? 0.f : *lr_dev;  // device-resident: graph replays read the tick's lr
-  // theta[o] after this tick's update (or unchanged for shadow_only)
-  auto update = [&](int64_t o) -> float {
-    float th = theta[o];
-    if (shadow_only) return th;
-    float d = grad[o];
-    if (!isfinite(d)) atomicOr(nonfinite, 2);  // latched (bit 1: Delta); reported by petra_stage_get_params
-    if (mode == SGD_ACC_UPDATE) {
-      d = fmaf(d, inv_k, acc[o]);
-      acc[o] = 0.f;
-    }
-    const float g = fmaf(lam, th, d);
-    const float vv = fmaf(mom, v[o], g);
-    v[o] = vv;
-    th -= lr * (nesterov ? fmaf(mom, vv, g) : vv);
-    theta[o] = th;
-    return th;
-  };
-  if (mode == SGD_ACCUMULATE) {  // Delta_j += Delta / k; theta (and its shadows) unchanged
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sg.count;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      const float d = grad[sg.offset + i];
+  const float lr_all = shadow_only ? 0.f : *lr_dev;  // device-resident: graph replays read the tick's lr
+  __shared__ __nv_bfloat16 tile[32][33];
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const SgdChunk ch = chunks[c];
+    const SgdSeg sg = segs[ch.seg];
+    if (shadow_only && !sg.w_bf16) continue;  // block-uniform
+    const float lam = sg.decay ? wd : 0.f;
+    const float lr = lr_all;
+    // theta[o] after this tick's update (or unchanged for shadow_only)
+    auto update = [&](int64_t o) -> float {
+      float th = theta[o];
+      if (shadow_only) return th;
+      float d = grad[o];
+      if (!isfinite(d)) atomicOr(nonfinite, 2);  // latched (bit 1: Delta); reported by petra_stage_get_params
+      if (mode == SGD_ACC_UPDATE) {
+        d = fmaf(d, inv_k, acc[o]);
+        acc[o] = 0.f;
+      }
+      const float g = fmaf(lam, th, d);
+      const float vv = fmaf(mom, v[o], g);
+      v[o] = vv;
+      th -= lr * (nesterov ? fmaf(mom, vv, g) : vv);
+      theta[o] = th;
+      return th;
+    };
+    auto accumulate = [&](int64_t o) {  // Delta_j += Delta / k; theta (and its shadows) unchanged
+      const float d = grad[o];
       if (!isfinite(d)) atomicOr(nonfinite, 2);
-      acc[sg.offset + i] += d * inv_k;
-    }
-    return;
-  }
-  if (sg.wt_bf16) {
-    // conv weight [Co][kh][kw][Ci] in 32(co) x 32(ci) tiles of one tap: theta, v and
-    // the bf16 copy w_bf16 (same order) are read / written along ci, the dgrad operand
-    // wT[ci][tap'][co] = w[co][tap][ci] (tap' = k*k-1-tap, flipped) along co through
-    // a shared-memory transpose -- every global access coalesced
-    __shared__ __nv_bfloat16 tile[32][33];
-    const int taps = sg.k * sg.k;
-    const int nco = (sg.co + 31) / 32, nci = (sg.ci + 31) / 32;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int t = blockIdx.x; t < taps * nco * nci; t += gridDim.x) {
+      acc[o] += d * inv_k;
+    };
+    if (sg.wt_bf16) {
+      // conv weight [Co][kh][kw][Ci], tile ch.lo = (tap, co block, ci block): theta, v and
+      // the bf16 copy w_bf16 (same order) are read / written along ci, the dgrad operand
+      // wT[ci][tap'][co] = w[co][tap][ci] (tap' = k*k-1-tap, flipped) along co through a
+      // shared-memory transpose -- every global access coalesced
+      const int taps = sg.k * sg.k;
+      const int nco = (sg.co + 31) / 32, nci = (sg.ci + 31) / 32;
+      const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+      const int t = (int)ch.lo;
       const int cib = t % nci, r = t / nci, cob = r % nco, tap = r / nco;
       const int ci = cib * 32 + tx;
+      if (mode == SGD_ACCUMULATE) {  // block-uniform
+#pragma unroll
+        for (int rr = ty; rr < 32; rr += 8) {
+          const int co = cob * 32 + rr;
+          if (co < sg.co && ci < sg.ci) accumulate(sg.offset + ((int64_t)co * taps + tap) * sg.ci + ci);
+        }
+        continue;
+      }
 #pragma unroll
       for (int rr = ty; rr < 32; rr += 8) {
         const int co = cob * 32 + rr;
@@ -84,12 +95,16 @@ __global__ void __launch_bounds__(256) sgd_kernel(const SgdSeg *__restrict__ seg
         if (co < sg.co && cj < sg.ci) sg.wt_bf16[((int64_t)cj * taps + (taps - 1 - tap)) * sg.co + co] = tile[tx][rr];
       }
       __syncthreads();
+      continue;
     }
-    return;
-  }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sg.count; i += (int64_t)gridDim.x * blockDim.x) {
-    const float th = update(sg.offset + i);
-    if (sg.w_bf16) sg.w_bf16[i] = __float2bfloat16_rn(th);
+    for (int64_t i = ch.lo + threadIdx.x; i < ch.hi; i += blockDim.x) {
+      if (mode == SGD_ACCUMULATE) {
+        accumulate(sg.offset + i);
+        continue;
+      }
+      const float th = update(sg.offset + i);
+      if (sg.w_bf16) sg.w_bf16[i] = __float2bfloat16_rn(th);
+    }
   }
 }
 
@@ -434,12 +449,26 @@ inline unsigned ew_grid(int64_t n) {
 
 }  // namespace
 
-void sgd_update(const SgdSeg *segs_dev, int nseg, int64_t max_count, float *theta, float *v, const float *grad,
-                float *acc, int k, int mode, const float *lr_dev, float mom, float wd, int nesterov, cudaStream_t st,
-                bool shadow_only, int *nonfinite) {
-  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(max_count, 256), 2 * kNumSMs)), nseg);
-  launch_k(sgd_kernel, grid, 256, 0, st, segs_dev, theta, v, grad, acc, 1.f / (float)k, mode, lr_dev, mom, wd, nesterov,
-           shadow_only ? 1 : 0, nonfinite);
+std::vector<SgdChunk> sgd_chunks(const std::vector<SgdSeg> &segs) {
+  std::vector<SgdChunk> out;
+  for (int s = 0; s < (int)segs.size(); ++s) {
+    const SgdSeg &g = segs[s];
+    if (g.wt_bf16) {
+      const int64_t tiles = (int64_t)g.k * g.k * ((g.co + 31) / 32) * ((g.ci + 31) / 32);
+      for (int64_t t = 0; t < tiles; ++t) out.push_back({s, t, t + 1});
+    } else {
+      for (int64_t lo = 0; lo < g.count; lo += 1024) out.push_back({s, lo, std::min<int64_t>(g.count, lo + 1024)});
+    }
+  }
+  return out;
+}
+
+void sgd_update(const SgdSeg *segs_dev, int nseg, const SgdChunk *chunks_dev, int nchunks, float *theta, float *v,
+                const float *grad, float *acc, int k, int mode, const float *lr_dev, float mom, float wd, int nesterov,
+                cudaStream_t st, bool shadow_only, int *nonfinite) {
+  const unsigned grid = (unsigned)std::max(1, std::min(nchunks, 8 * kNumSMs));
+  launch_k(sgd_kernel, grid, 256, 0, st, segs_dev, chunks_dev, nchunks, theta, v, grad, acc, 1.f / (float)k, mode,
+           lr_dev, mom, wd, nesterov, shadow_only ? 1 : 0, nonfinite);
   PETRA_LAUNCH_CHECK();
 }
 

@@ -442,6 +442,10 @@ void Stage::build() {
   }
   segs_dev_ = dalloc(segs_.size() * sizeof(SgdSeg));
   PETRA_CUDA(cudaMemcpy(segs_dev_->p, segs_.data(), segs_.size() * sizeof(SgdSeg), cudaMemcpyHostToDevice));
+  const std::vector<SgdChunk> chunks = sgd_chunks(segs_);
+  n_chunks_ = (int)chunks.size();
+  chunks_dev_ = dalloc(std::max<size_t>(1, chunks.size()) * sizeof(SgdChunk));
+  PETRA_CUDA(cudaMemcpy(chunks_dev_->p, chunks.data(), chunks.size() * sizeof(SgdChunk), cudaMemcpyHostToDevice));
 }
 
 void Stage::init_params(uint64_t seed) {
@@ -471,7 +475,8 @@ void Stage::set_params(const float *theta, const float *v, const float *bufs) {
   if (bufs && n_buffers_)
     PETRA_CUDA(cudaMemcpy(bufs_->p, bufs, n_buffers_ * sizeof(float), cudaMemcpyHostToDevice));
   if (tc_ && theta) {
-    sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
+    sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), chunks_dev_->as<SgdChunk>(), n_chunks_, theta_->as<float>(),
+               v_->as<float>(),
                grad_->as<float>(), nullptr, 1, SGD_PLAIN, nullptr, 0.f, 0.f, 1, nullptr, /*shadow_only=*/true,
                nonfinite_->as<int>());
     PETRA_CUDA(cudaDeviceSynchronize());
@@ -559,7 +564,8 @@ void Stage::advance_step(int mode) {
 void Stage::enqueue_update(int mode, cudaStream_t st) {
   ProfScope ps("sgd_update", st, 0.0,
                (mode == SGD_PLAIN ? 20.0 : mode == SGD_ACCUMULATE ? 12.0 : 28.0) * (double)n_params_);
-  sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), max_seg_, theta_->as<float>(), v_->as<float>(),
+  sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), chunks_dev_->as<SgdChunk>(), n_chunks_, theta_->as<float>(),
+               v_->as<float>(),
              grad_->as<float>(), acc_ ? acc_->as<float>() : nullptr, desc_.accumulation_k, mode, lr_dev_->as<float>(),
              desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false, nonfinite_->as<int>());
 }

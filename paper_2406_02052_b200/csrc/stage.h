@@ -186,6 +186,8 @@ class Stage {
   std::vector<SgdSeg> segs_;
   DevPtr segs_dev_;
   int64_t max_seg_ = 0;
+  DevPtr chunks_dev_;   // SgdChunk work items of the update (sgd_chunks)
+  int n_chunks_ = 0;
   DevPtr part_[2], spart_[2], wgrad_ws_[2], counters_[2];  // per context (see Layer)
   int ctx_ = 0;                                 // workspace context being enqueued
   DevPtr &part() { return part_[ctx_]; }
