@@ -54,13 +54,43 @@ inline int log2_or_neg(int v) {
   while ((1 << s) < v) ++s;
   return s;
 }
-// row m of an H x W grid -> row of the zero-bordered (H+2) x (W+2) layout (pH <= 0: m)
-__device__ __forceinline__ int64_t pad_row(int64_t m, int pH, int pW) {
-  if (pH <= 0) return m;
+// row m of an H x W grid -> row of the zero-bordered (H+2) x (W+2) layout (pH <= 0: m).
+// The two divisions are multiply-high with magic numbers computed once per thread
+// (PadMap): an integer division costs ~25 instructions, and these kernels run one per
+// row of four channels -- ncu showed them instruction-bound (issue 54 %) on it.
+struct PadMap {
+  tc::FastDiv fhw, fw;
+  int pH, pW;
+};
+__device__ __forceinline__ tc::FastDiv fastdiv_dev(uint32_t d) {
+  tc::FastDiv f;
+  f.d = d;
+  if (d <= 1) {
+    f.m = 0;
+    f.s = -1;
+  } else {
+    const int l = 32 - __clz(d - 1);  // ceil(log2 d)
+    f.m = (uint32_t)(((1ull << (31 + l)) + d - 1) / d);
+    f.s = l - 1;
+  }
+  return f;
+}
+__device__ __forceinline__ PadMap pad_map(int pH, int pW) {
+  PadMap p;
+  p.pH = pH;
+  p.pW = pW;
+  if (pH > 0) {
+    p.fhw = fastdiv_dev((uint32_t)(pH * pW));
+    p.fw = fastdiv_dev((uint32_t)pW);
+  }
+  return p;
+}
+__device__ __forceinline__ int64_t pad_row(int64_t m, const PadMap &p) {
+  if (p.pH <= 0) return m;
   // 32-bit index math: the padded operand buffers hold < 2^31 rows (host-checked)
-  const int hw = pH * pW, mi = (int)m;
-  const int b = mi / hw, r = mi - b * hw, h = r / pW, w = r - h * pW;
-  return ((int64_t)b * (pH + 2) + h + 1) * (pW + 2) + w + 1;
+  const int mi = (int)m;
+  const int b = tc::fdiv(mi, p.fhw), r = mi - b * (int)p.fhw.d, h = tc::fdiv(r, p.fw), w = r - h * p.pW;
+  return ((int64_t)b * (p.pH + 2) + h + 1) * (p.pW + 2) + w + 1;
 }
 
 // reduction blocks: one wave of NT-thread blocks (stats 1024, backward reduce 512:
@@ -265,6 +295,7 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
                                 float sign, const float *acc, TO *out, __nv_bfloat16 *out_bf16, int pH, int pW,
                                 int sh) {
   pdl_wait_trigger();
+  const PadMap pm = pad_map(pH, pW);
   const bool vec = (C % 4 == 0) && (ldz % 4 == 0) && (zc0 % 4 == 0);
   if (vec) {
     const int C4 = C / 4;
@@ -287,7 +318,7 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
         o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
       }
       if (out) st4(out, m * C + c, o);
-      if (out_bf16) st4(out_bf16, pad_row(m, pH, pW) * C + c, o);
+      if (out_bf16) st4(out_bf16, pad_row(m, pm) * C + c, o);
     }
     return;
   }
@@ -301,7 +332,7 @@ __global__ void bn_apply_kernel(int64_t M, int C, const TZ *__restrict__ z, int 
     float o = sign * y;
     if (acc) o += acc[i];
     if (out) stv(out, i, o);
-    if (out_bf16) out_bf16[pad_row(m, pH, pW) * C + c] = __float2bfloat16_rn(o);
+    if (out_bf16) out_bf16[pad_row(m, pm) * C + c] = __float2bfloat16_rn(o);
   }
 }
 
@@ -316,6 +347,7 @@ __global__ void __launch_bounds__(256, 4) bn_apply_fixed_kernel(
     float sign, const float *__restrict__ acc, float *__restrict__ out, __nv_bfloat16 *__restrict__ out_bf16, int pH,
     int pW) {
   pdl_wait_trigger();
+  const PadMap pm = pad_map(pH, pW);
   const int C4 = C / 4;
   const int stride = gridDim.x * blockDim.x;
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -350,7 +382,7 @@ __global__ void __launch_bounds__(256, 4) bn_apply_fixed_kernel(
       }
       o.x += av.x; o.y += av.y; o.z += av.z; o.w += av.w;
       if (out) st4(out, (int64_t)mm * C + c, o);
-      if (out_bf16) st4(out_bf16, pad_row(mm, pH, pW) * C + c, o);
+      if (out_bf16) st4(out_bf16, pad_row(mm, pm) * C + c, o);
     }
   }
 }
@@ -362,6 +394,7 @@ __global__ void __launch_bounds__(256, 4) bn_bwd_dz_fixed_kernel(
     const float *__restrict__ dgamma, const float *__restrict__ dbeta, float *__restrict__ dz,
     __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW) {
   pdl_wait_trigger();
+  const PadMap pm = pad_map(pH, pW);
   const float invM = 1.0f / (float)M;
   const int C4 = C / 4;
   const int stride = gridDim.x * blockDim.x;
@@ -401,7 +434,7 @@ __global__ void __launch_bounds__(256, 4) bn_bwd_dz_fixed_kernel(
         op[k] = ga[k] * is[k] * (g - db[k] - xh * dg[k] * invM);  // same rounding as bn_bwd_dz_kernel
       }
       if (dz) st4(dz, (int64_t)mm * C + c, o);
-      if (dz_bf16) st4(dz_bf16, pad_row(mm, pH, pW) * C + c, o);
+      if (dz_bf16) st4(dz_bf16, pad_row(mm, pm) * C + c, o);
     }
   }
 }
@@ -482,6 +515,7 @@ __global__ void __launch_bounds__(256) bn_apply_tma_kernel(
     float sign, float *__restrict__ out, __nv_bfloat16 *__restrict__ out_bf16, int pH, int pW,
     const StatsFold fold) {
   pdl_wait_trigger();
+  const PadMap pm = pad_map(pH, pW);
   __shared__ uint64_t full[2];
   __shared__ float s_mu[128], s_is[128];
   extern __shared__ __align__(128) uint8_t ring[];
@@ -543,7 +577,7 @@ __global__ void __launch_bounds__(256) bn_apply_tma_kernel(
         }
         o.x += av.x; o.y += av.y; o.z += av.z; o.w += av.w;
         if (out) st4(out, m * C + c, o);
-        if (out_bf16) st4(out_bf16, pad_row(m, pH, pW) * C + c, o);
+        if (out_bf16) st4(out_bf16, pad_row(m, pm) * C + c, o);
       }
     }
     __syncthreads();
@@ -559,6 +593,7 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
     float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW, double *__restrict__ part,
     unsigned *__restrict__ counter, float *__restrict__ dgamma, float *__restrict__ dbeta) {
   pdl_wait_trigger();
+  const PadMap pm = pad_map(pH, pW);
   constexpr int RT = RT_BWD;
   __shared__ double sh[RT][4];
   const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
@@ -594,7 +629,7 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
         }
         if (dst_out) {
           st4(dst_out, r * C + c, d4);
-          if (dst_bf16) st4(dst_bf16, pad_row(r, pH, pW) * C + c, d4);
+          if (dst_bf16) st4(dst_bf16, pad_row(r, pm) * C + c, d4);
         }
       };
       int64_t r = r0 + rgi;
@@ -629,7 +664,7 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
         if (dst_out) {
           float o = dst_in[r * C + c] - y;
           dst_out[r * C + c] = o;
-          if (dst_bf16) dst_bf16[pad_row(r, pH, pW) * C + c] = __float2bfloat16_rn(o);
+          if (dst_bf16) dst_bf16[pad_row(r, pm) * C + c] = __float2bfloat16_rn(o);
         }
         sg[0] += (double)g;
         sgx[0] += (double)g * (double)xh;
@@ -665,6 +700,7 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
     double *__restrict__ part, unsigned *__restrict__ counter, float *__restrict__ dgamma,
     float *__restrict__ dbeta, const StatsFold fold) {
   pdl_wait_trigger();
+  const PadMap pm = pad_map(pH, pW);
   constexpr int RT = RT_BWD;
   __shared__ double sh[RT][4];
   __shared__ uint64_t full[2];
@@ -745,7 +781,7 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
         }
         if (has_dst) {
           st4(dst_out, r * C + c, d4);
-          if (dst_bf16) st4(dst_bf16, pad_row(r, pH, pW) * C + c, d4);
+          if (dst_bf16) st4(dst_bf16, pad_row(r, pm) * C + c, d4);
         }
       }
     }
@@ -775,6 +811,7 @@ __global__ void __launch_bounds__(256) bn_bwd_dz_tma_kernel(
     const float *__restrict__ gamma, const float *__restrict__ beta, int relu, const float *__restrict__ dgamma,
     const float *__restrict__ dbeta, float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW) {
   pdl_wait_trigger();
+  const PadMap pm = pad_map(pH, pW);
   __shared__ uint64_t full[2];
   extern __shared__ __align__(128) uint8_t ring[];
   const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
@@ -842,7 +879,7 @@ __global__ void __launch_bounds__(256) bn_bwd_dz_tma_kernel(
           op[q] = ga[q] * is[q] * (g - db[q] - xh * dg[q] * invM);  // same rounding as bn_bwd_dz_kernel
         }
         if (dz) st4(dz, m * C + c, o);
-        if (dz_bf16) st4(dz_bf16, pad_row(m, pH, pW) * C + c, o);
+        if (dz_bf16) st4(dz_bf16, pad_row(m, pm) * C + c, o);
       }
     }
     __syncthreads();
@@ -858,6 +895,7 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
                                  float *__restrict__ dz, __nv_bfloat16 *__restrict__ dz_bf16, int pH, int pW,
                                  int sh) {
   pdl_wait_trigger();
+  const PadMap pm = pad_map(pH, pW);
   const float invM = 1.0f / (float)M;
   const bool vec = (C % 4 == 0) && (dy1 == nullptr || cs % 4 == 0);
   if (vec) {
@@ -879,7 +917,7 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
         op[k] = gamma[c + k] * is * (g - dbeta[c + k] * invM - xh * dgamma[c + k] * invM);
       }
       if (dz) st4(dz, m * C + c, o);
-      if (dz_bf16) st4(dz_bf16, pad_row(m, pH, pW) * C + c, o);
+      if (dz_bf16) st4(dz_bf16, pad_row(m, pm) * C + c, o);
     }
     return;
   }
@@ -893,7 +931,7 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
     if (relu && !(fmaf(gamma[c], xh, beta[c]) > 0.f)) g = 0.f;
     float v = gamma[c] * is * (g - dbeta[c] * invM - xh * dgamma[c] * invM);
     if (dz) stv(dz, i, v);
-    if (dz_bf16) dz_bf16[pad_row(m, pH, pW) * C + c] = __float2bfloat16_rn(v);
+    if (dz_bf16) dz_bf16[pad_row(m, pm) * C + c] = __float2bfloat16_rn(v);
   }
 }
 

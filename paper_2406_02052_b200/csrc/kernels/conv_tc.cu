@@ -692,14 +692,22 @@ __global__ void splitk_sum_kernel(const float *__restrict__ part, int splits, in
 __global__ void phase_fill_kernel(int B, int OH, int OW, int C, int mask, const float *__restrict__ addend,
                                   float *__restrict__ out) {
   pdl_wait_trigger();
-  const int C4 = C / 4;
-  const int64_t n = (int64_t)B * OH * OW * C4;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t pix = i / C4;
-    int w = (int)(pix % OW), h = (int)((pix / OW) % OH);
-    if (!((mask >> ((h & 1) * 2 + (w & 1))) & 1)) continue;
-    float4 v = addend ? reinterpret_cast<const float4 *>(addend)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    reinterpret_cast<float4 *>(out)[i] = v;
+  // one pixel row (b, h) per block iteration, rows without a masked phase skipped whole;
+  // (w, c) from the thread index by a shift when C / 4 is a power of two (no 64-bit
+  // divisions per element)
+  const int C4 = C / 4, rowlen = OW * C4;
+  const int sh = (C4 & (C4 - 1)) == 0 ? __ffs(C4) - 1 : -1;
+  for (int row = blockIdx.x; row < B * OH; row += gridDim.x) {
+    const int h = row % OH;
+    const int m = (mask >> ((h & 1) * 2)) & 3;  // phases (h, w even) / (h, w odd) of this row
+    if (!m) continue;
+    const float4 *a = addend ? reinterpret_cast<const float4 *>(addend) + (int64_t)row * rowlen : nullptr;
+    float4 *o = reinterpret_cast<float4 *>(out) + (int64_t)row * rowlen;
+    for (int j = threadIdx.x; j < rowlen; j += blockDim.x) {
+      const int w = sh >= 0 ? j >> sh : j / C4;
+      if (!((m >> (w & 1)) & 1)) continue;
+      o[j] = a ? a[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
 }
 
@@ -1077,8 +1085,7 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_pad, const __
       launch_any(ta, L, wt, g.Ci, wK, P, ws, false, st);
     }
   if (empty_mask) {
-    int64_t cnt = (int64_t)g.B * g.H * g.W * (g.Ci / 4);
-    launch_k(phase_fill_kernel, (unsigned)std::min<int64_t>(cdiv(cnt, 256), 8 * kNumSMs), 256, 0, st, 
+    launch_k(phase_fill_kernel, (unsigned)std::min<int64_t>((int64_t)g.B * g.H, 16 * kNumSMs), 256, 0, st, 
         g.B, g.H, g.W, g.Ci, empty_mask, addend, dx);
     PETRA_LAUNCH_CHECK();
   }
@@ -1096,7 +1103,7 @@ WgradPlan wgrad_plan(const ConvGeom &g) {
   w.t = tiling(g.B, g.Ho, g.Wo, 64);
   w.KBtot = (int)(w.t.M() / 64);
   int tiles = w.n_mt * w.n_nt;
-  static const int ctas = env_int("PETRA_WGRAD_CTAS", 24);  // CTAs the split-K aims to fill
+  static const int ctas = env_int("PETRA_WGRAD_CTAS", 48);  // CTAs the split-K aims to fill
   int want = std::max(1, std::min(w.KBtot, (int)cdiv(ctas, tiles)));
   w.kb_per_split = (int)cdiv(w.KBtot, want);
   w.splits = (int)cdiv(w.KBtot, w.kb_per_split);

@@ -327,30 +327,37 @@ __global__ void maxpool_bwd_kernel(const float *__restrict__ d1, const float *__
 
 // vectorised variants (C % 8 == 0, 32-bit indexing): one thread = 4 channels of one
 // pixel, float4 loads/stores, the 4 argmax bytes as one 32-bit word
+// one output pixel row (b, ho) per block iteration: threads walk (wo, c) with a shift when
+// C4 is a power of two (no per-element 32-bit divisions)
 __global__ void maxpool_fwd_v4_kernel(const float4 *__restrict__ a, int B, int H, int W, int C4, int Ho, int Wo,
                                       float4 *__restrict__ o1, float4 *__restrict__ o2, uchar4 *__restrict__ arg) {
   pdl_wait_trigger();
-  const int n = B * Ho * Wo * C4, Ch4 = C4 / 2;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int c = i % C4, pix = i / C4, wo = pix % Wo, r = pix / Wo, ho = r % Ho, b = r / Ho;
-    float4 best = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-    uchar4 bi = make_uchar4(0, 0, 0, 0);
+  const int Ch4 = C4 / 2, rowlen = Wo * C4;
+  const int sh = (C4 & (C4 - 1)) == 0 ? __ffs(C4) - 1 : -1;
+  for (int row = blockIdx.x; row < B * Ho; row += gridDim.x) {
+    const int b = row / Ho, ho = row - b * Ho;
+    for (int j = threadIdx.x; j < rowlen; j += blockDim.x) {
+      const int wo = sh >= 0 ? j >> sh : j / C4, c = j - wo * C4;
+      float4 best = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      uchar4 bi = make_uchar4(0, 0, 0, 0);
 #pragma unroll
-    for (int kh = 0; kh < 3; ++kh)
+      for (int kh = 0; kh < 3; ++kh)
 #pragma unroll
-      for (int kw = 0; kw < 3; ++kw) {
-        const int h = ho * 2 + kh - 1, w = wo * 2 + kw - 1;
-        if (h < 0 || h >= H || w < 0 || w >= W) continue;
-        const float4 v = a[((b * H + h) * W + w) * C4 + c];
-        const unsigned char t = (unsigned char)(kh * 3 + kw);
-        if (v.x > best.x) { best.x = v.x; bi.x = t; }  // strict >: first index wins ties
-        if (v.y > best.y) { best.y = v.y; bi.y = t; }
-        if (v.z > best.z) { best.z = v.z; bi.z = t; }
-        if (v.w > best.w) { best.w = v.w; bi.w = t; }
-      }
-    arg[i] = bi;
-    if (c < Ch4) o1[pix * Ch4 + c] = best;
-    else o2[pix * Ch4 + c - Ch4] = best;
+        for (int kw = 0; kw < 3; ++kw) {
+          const int h = ho * 2 + kh - 1, w = wo * 2 + kw - 1;
+          if (h < 0 || h >= H || w < 0 || w >= W) continue;
+          const float4 v = a[((b * H + h) * W + w) * C4 + c];
+          const unsigned char t = (unsigned char)(kh * 3 + kw);
+          if (v.x > best.x) { best.x = v.x; bi.x = t; }  // strict >: first index wins ties
+          if (v.y > best.y) { best.y = v.y; bi.y = t; }
+          if (v.z > best.z) { best.z = v.z; bi.z = t; }
+          if (v.w > best.w) { best.w = v.w; bi.w = t; }
+        }
+      const int pix = row * Wo + wo;
+      arg[pix * C4 + c] = bi;
+      if (c < Ch4) o1[pix * Ch4 + c] = best;
+      else o2[pix * Ch4 + c - Ch4] = best;
+    }
   }
 }
 
@@ -358,28 +365,33 @@ __global__ void maxpool_bwd_v4_kernel(const float4 *__restrict__ d1, const float
                                       const uchar4 *__restrict__ arg, int B, int H, int W, int C4, int Ho, int Wo,
                                       float4 *__restrict__ da) {
   pdl_wait_trigger();
-  const int n = B * H * W * C4, Ch4 = C4 / 2;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int c = i % C4, pix = i / C4, w = pix % W, r = pix / W, h = r % H, b = r / H;
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    // output windows (ho, wo) with 2*ho-1 <= h <= 2*ho+1, in increasing (ho, wo) order
-    for (int ho = h / 2; ho <= min(Ho - 1, (h + 1) / 2); ++ho) {
-      const int kh = h - (ho * 2 - 1);
-      if (kh < 0 || kh > 2) continue;
-      for (int wo = w / 2; wo <= min(Wo - 1, (w + 1) / 2); ++wo) {
-        const int kw = w - (wo * 2 - 1);
-        if (kw < 0 || kw > 2) continue;
-        const int op = (b * Ho + ho) * Wo + wo;
-        const uchar4 g = arg[op * C4 + c];
-        const float4 d = c < Ch4 ? d1[op * Ch4 + c] : d2[op * Ch4 + c - Ch4];
-        const unsigned char t = (unsigned char)(kh * 3 + kw);
-        if (g.x == t) s.x += d.x;
-        if (g.y == t) s.y += d.y;
-        if (g.z == t) s.z += d.z;
-        if (g.w == t) s.w += d.w;
+  // one input pixel row (b, h) per block iteration (as the forward: no per-element divisions)
+  const int Ch4 = C4 / 2, rowlen = W * C4;
+  const int sh = (C4 & (C4 - 1)) == 0 ? __ffs(C4) - 1 : -1;
+  for (int row = blockIdx.x; row < B * H; row += gridDim.x) {
+    const int b = row / H, h = row - b * H;
+    for (int j = threadIdx.x; j < rowlen; j += blockDim.x) {
+      const int w = sh >= 0 ? j >> sh : j / C4, c = j - w * C4;
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      // output windows (ho, wo) with 2*ho-1 <= h <= 2*ho+1, in increasing (ho, wo) order
+      for (int ho = h / 2; ho <= min(Ho - 1, (h + 1) / 2); ++ho) {
+        const int kh = h - (ho * 2 - 1);
+        if (kh < 0 || kh > 2) continue;
+        for (int wo = w / 2; wo <= min(Wo - 1, (w + 1) / 2); ++wo) {
+          const int kw = w - (wo * 2 - 1);
+          if (kw < 0 || kw > 2) continue;
+          const int op = (b * Ho + ho) * Wo + wo;
+          const uchar4 g = arg[op * C4 + c];
+          const float4 d = c < Ch4 ? d1[op * Ch4 + c] : d2[op * Ch4 + c - Ch4];
+          const unsigned char t = (unsigned char)(kh * 3 + kw);
+          if (g.x == t) s.x += d.x;
+          if (g.y == t) s.y += d.y;
+          if (g.z == t) s.z += d.z;
+          if (g.w == t) s.w += d.w;
+        }
       }
+      da[(int64_t)row * rowlen + j] = s;
     }
-    da[i] = s;
   }
 }
 
@@ -570,7 +582,7 @@ void maxpool_fwd(const float *a, int B, int H, int W, int C, int Ho, int Wo, flo
                  cudaStream_t st) {
   if (C % 8 == 0 && (int64_t)B * H * W * C < ((int64_t)1 << 31)) {
     const int C4 = C / 4;
-    launch_k(maxpool_fwd_v4_kernel, ew_grid((int64_t)B * Ho * Wo * C4), 256, 0, st, 
+    launch_k(maxpool_fwd_v4_kernel, (unsigned)std::min<int64_t>((int64_t)B * Ho, 16 * kNumSMs), 256, 0, st, 
         reinterpret_cast<const float4 *>(a), B, H, W, C4, Ho, Wo, reinterpret_cast<float4 *>(o1),
         reinterpret_cast<float4 *>(o2), reinterpret_cast<uchar4 *>(arg));
   } else {
@@ -583,7 +595,7 @@ void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, in
                  float *da, cudaStream_t st) {
   if (C % 8 == 0 && (int64_t)B * H * W * C < ((int64_t)1 << 31)) {
     const int C4 = C / 4;
-    launch_k(maxpool_bwd_v4_kernel, ew_grid((int64_t)B * H * W * C4), 256, 0, st, 
+    launch_k(maxpool_bwd_v4_kernel, (unsigned)std::min<int64_t>((int64_t)B * H, 16 * kNumSMs), 256, 0, st, 
         reinterpret_cast<const float4 *>(d1), reinterpret_cast<const float4 *>(d2),
         reinterpret_cast<const uchar4 *>(arg), B, H, W, C4, Ho, Wo, reinterpret_cast<float4 *>(da));
   } else {
