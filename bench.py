@@ -270,24 +270,46 @@ def measure(model, stages, batch, precision, steps, warmup, world, rank, local, 
            "host_enqueue_ms_per_step": round(statistics.median(host_ms), 4) if host_ms else None,
            "gpu_launches": launches, "clocks": clk, "prec": prec, "H": H, "classes": classes}
 
-    # ---- e2e through the public API: pinned host inputs copied in, loss read back, every step
+    # ---- e2e through the public API: pinned host inputs copied in, loss read back, every step.
+    # The input copy of step k+1 runs on a copy stream under step k (double-buffered device
+    # inputs, as a training loop's prefetching loader does); every copy is inside the events.
     if e2e:
         hx = [x.cpu().pin_memory() for x in xs[:4]]
         hy = [y.cpu().pin_memory() for y in ys[:4]]
         hl = torch.zeros(1).pin_memory()
-        dx = torch.empty_like(xs[0])
-        dy = torch.empty_like(ys[0])
+        dx = [torch.empty_like(xs[0]) for _ in range(2)]
+        dy = [torch.empty_like(ys[0]) for _ in range(2)]
+        cs = torch.cuda.Stream()
+        copied = [torch.cuda.Event() for _ in range(2)]
+        used = [torch.cuda.Event() for _ in range(2)]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+        def stage_in(k):  # H2D of step k's inputs into buffer k % 2 (after step k-2 released it)
+            b = k % 2
+            with torch.cuda.stream(cs):
+                if k >= 2:
+                    cs.wait_event(used[b])
+                dx[b].copy_(hx[(t0 + k) % 4], non_blocking=True)
+                dy[b].copy_(hy[(t0 + k) % 4], non_blocking=True)
+                copied[b].record(cs)
+
+        t0 = t
         e0.record(st)
+        cs.wait_event(e0)
+        if owns_first:
+            stage_in(0)
         for k in range(steps):
-            i = t % 4
+            b = k % 2
             if owns_first:
-                dx.copy_(hx[i], non_blocking=True)
-                dy.copy_(hy[i], non_blocking=True)
-            pipe.tick(t, True, dx if owns_first else None, dy if owns_first else None, lr, loss, report=False)
+                if k + 1 < steps:
+                    stage_in(k + 1)
+                st.wait_event(copied[b])
+            pipe.tick(t, True, dx[b] if owns_first else None, dy[b] if owns_first else None, lr, loss, report=False)
+            if owns_first:
+                used[b].record(st)
             hl.copy_(loss, non_blocking=True)
             t += 1
         e1.record(st)

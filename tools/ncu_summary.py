@@ -4,11 +4,12 @@ rows = list(csv.reader(open(sys.argv[1])))
 hdr = next(i for i, r in enumerate(rows) if r and r[0] == 'ID')
 h = rows[hdr]; data = rows[hdr + 1:]
 ki, vi, ui = h.index('Kernel Name'), h.index('Metric Value'), h.index('Metric Unit')
+mi = h.index('Metric Name')
 scale = {'nsecond': 1e-3, 'ns': 1e-3, 'usecond': 1.0, 'us': 1.0, 'msecond': 1e3, 'ms': 1e3, 'second': 1e6, 's': 1e6}
 skip = int(sys.argv[2]) if len(sys.argv) > 2 else 0   # drop the first N launches (setup)
 agg = collections.defaultdict(lambda: [0, 0.0])
 for r in data[skip:]:
-    if len(r) <= vi:
+    if len(r) <= vi or r[mi] != 'gpu__time_duration.sum':  # other metrics of a multi-metric list
         continue
     name = r[ki].split('(')[0].replace('void ', '')
     name = name.replace('petra::<unnamed>::', '')
