@@ -96,6 +96,7 @@ __device__ __forceinline__ int64_t pad_row(int64_t m, const PadMap &p) {
 // reduction blocks: one wave of NT-thread blocks (stats 1024, backward reduce 512:
 // >= 64 KB of loads in flight per SM)
 constexpr int RT_STATS = 1024, RT_BWD = 512;
+constexpr int kMaxRing = 4;  // deepest TMA ring of the BN passes
 
 // Reduction geometry: a block covers a tile of CT channels (TPR threads per row,
 // 4 channels each; RG = 256/TPR row groups) and a contiguous chunk of rpb rows.
@@ -685,8 +686,9 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_kernel(
 
 
 // BN backward reduce, TMA-staged: per chunk of Rc rows the block's z / dy (/ dst_in)
-// tiles for its channel tile arrive by one 2-D TMA load each (box CT x Rc) into a
-// two-stage smem ring.  Every thread keeps the (rows, channels) it has in
+// tiles for its channel tile arrive by one 2-D TMA load each (box CT x Rc) into an
+// S-stage smem ring (S - 1 chunks in flight while one is computed; one block per SM, so
+// the ring depth is what covers the DRAM latency).  Every thread keeps the (rows, channels) it has in
 // bn_bwd_reduce_kernel and adds them in the same order (chunks are whole multiples of
 // the row-group count), so the sums -- and the partial rows / merge that follow -- are
 // bitwise those of the register-loading kernel.
@@ -694,7 +696,7 @@ template <typename TZ>
 __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
     const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmY,
     const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmY1, int cs, int64_t M, int C,
-    int CT, int TPR, int RG, int64_t rpb, int nrb, int Rc,
+    int CT, int TPR, int RG, int64_t rpb, int nrb, int Rc, int S,
     const float *__restrict__ mean, const float *__restrict__ invstd, const float *__restrict__ gamma,
     const float *__restrict__ beta, int relu, int has_dst, float *dst_out, __nv_bfloat16 *dst_bf16, int pH, int pW,
     double *__restrict__ part, unsigned *__restrict__ counter, float *__restrict__ dgamma,
@@ -703,7 +705,7 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
   const PadMap pm = pad_map(pH, pW);
   constexpr int RT = RT_BWD;
   __shared__ double sh[RT][4];
-  __shared__ uint64_t full[2];
+  __shared__ uint64_t full[kMaxRing];  // S <= kMaxRing stages in flight (one block per SM)
   __shared__ float s_mu[128], s_is[128];
   extern __shared__ __align__(128) uint8_t ring[];
   const int t = threadIdx.x, cj = t % TPR, rgi = t / TPR;
@@ -715,8 +717,7 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
   const uint32_t zb = (uint32_t)Rc * CT * sizeof(TZ), fb = (uint32_t)Rc * CT * 4;
   const uint32_t sbytes = (zb + fb + (has_dst ? fb : 0) + 127) & ~127u;
   if (t == 0) {
-    tc::mbar_init(&full[0], 1);
-    tc::mbar_init(&full[1], 1);
+    for (int q = 0; q < S; ++q) tc::mbar_init(&full[q], 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
@@ -734,7 +735,8 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
     }
     if (has_dst) tc::tma_load_2d(st + zb + fb, &tmD, &full[s], c0, y);
   };
-  if (t == 0 && nchunk > 0) issue(0, 0);  // the first chunk streams in while the statistics merge
+  if (t == 0)  // the first S-1 chunks stream in while the statistics merge
+    for (int q = 0; q < S - 1 && q < nchunk; ++q) issue(q, q);
   if (fold.part)
     fold_stats(fold, c0, min(CT, C - c0), s_mu, s_is, blockIdx.x == 0, const_cast<float *>(mean),
                const_cast<float *>(invstd));
@@ -746,12 +748,13 @@ __global__ void __launch_bounds__(RT_BWD) bn_bwd_reduce_tma_kernel(
     ga[k] = mine ? gamma[c + k] : 0.f;
     be[k] = mine ? beta[c + k] : 0.f;
   }
-  uint32_t ph0 = 0, ph1 = 0;
+  uint32_t phases = 0;  // bit q: parity of stage q's next completion
   int s = 0;
-  for (int64_t k = 0; k < nchunk; ++k, s ^= 1) {
-    if (t == 0 && k + 1 < nchunk) issue(k + 1, s ^ 1);  // its stage was released at the end of k-1
-    tc::mbar_wait(&full[s], s ? ph1 : ph0);
-    if (s) ph1 ^= 1; else ph0 ^= 1;
+  for (int64_t k = 0; k < nchunk; ++k, s = (s + 1 == S) ? 0 : s + 1) {
+    // chunk k + S - 1 goes into the stage chunk k - 1 released at the end of the last iteration
+    if (t == 0 && k + S - 1 < nchunk) issue(k + S - 1, (int)((k + S - 1) % S));
+    tc::mbar_wait(&full[s], (phases >> s) & 1u);
+    phases ^= 1u << s;
     const int64_t a0 = r0 + k * Rc;
     const int rows = (int)min((int64_t)Rc, r1 - a0);
     const uint8_t *st = ring + s * sbytes;
@@ -1065,15 +1068,18 @@ void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float
     const int es = (int)sizeof(TZ) + 4 + (dst_out ? 4 : 0);
     const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (40960 / (g.CT * es)) / g.RG * g.RG));
     const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
+    // ring depth: one block per SM, so the stages in flight are what hides the DRAM latency
+    static const int ring = std::max(2, std::min(kMaxRing, env_int("PETRA_BN_REDUCE_STAGES", 4)));
+    const int S = (size_t)ring * sbytes <= 180 * 1024 ? ring : 2;
     // every TMA destination inside a ring stage must be 128-byte aligned (else the register kernel)
     const bool ring_ok = ring_aligned((size_t)Rc * g.CT * sizeof(TZ)) && ring_aligned((size_t)Rc * g.CT * 4) &&
                          (!dy1 || ring_aligned((size_t)Rc * cs * 4));
     if (ring_ok) {
       static std::once_flag once;
       std::call_once(once, [] {
-        cudaFuncSetAttribute(bn_bwd_reduce_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(bn_bwd_reduce_tma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 184 * 1024);
         cudaFuncSetAttribute(bn_bwd_reduce_tma_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             160 * 1024);
+                             184 * 1024);
       });
       const CUtensorMapDataType zt = sizeof(TZ) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
       const CUtensorMap tz = plain_map_2d(z, zt, (int)sizeof(TZ), M, C, g.CT, Rc);
@@ -1082,9 +1088,9 @@ void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float
                                  : plain_map_2d(dy0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc);
       const CUtensorMap ty1 = dy1 ? plain_map_2d(dy1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C - cs, C - cs, Rc) : ty;
       const CUtensorMap td = dst_out ? plain_map_2d(dst_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, C, g.CT, Rc) : ty;
-      launch_k(bn_bwd_reduce_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, 2 * sbytes, st, tz, ty, td, ty1, s0, M, C,
+      launch_k(bn_bwd_reduce_tma_kernel<TZ>, dim3(g.nrb, g.ctiles), RT_BWD, S * sbytes, st, tz, ty, td, ty1, s0, M, C,
                g.CT,
-               g.TPR, g.RG, g.rpb, g.nrb, Rc, mean, invstd, gamma, beta, relu, dst_out ? 1 : 0, dst_out, dst_bf16, pH,
+               g.TPR, g.RG, g.rpb, g.nrb, Rc, S, mean, invstd, gamma, beta, relu, dst_out ? 1 : 0, dst_out, dst_bf16, pH,
                pW, part, counter, dgamma, dbeta, fold ? *fold : StatsFold{});
       PETRA_LAUNCH_CHECK();
       return;
