@@ -1069,7 +1069,7 @@ void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float
     const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (40960 / (g.CT * es)) / g.RG * g.RG));
     const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
     // ring depth: one block per SM, so the stages in flight are what hides the DRAM latency
-    static const int ring = std::max(2, std::min(kMaxRing, env_int("PETRA_BN_REDUCE_STAGES", 4)));
+    static const int ring = std::max(2, std::min(kMaxRing, env_int("PETRA_BN_REDUCE_STAGES", 2)));
     const int S = (size_t)ring * sbytes <= 180 * 1024 ? ring : 2;
     // every TMA destination inside a ring stage must be 128-byte aligned (else the register kernel)
     const bool ring_ok = ring_aligned((size_t)Rc * g.CT * sizeof(TZ)) && ring_aligned((size_t)Rc * g.CT * 4) &&

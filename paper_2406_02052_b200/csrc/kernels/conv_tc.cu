@@ -896,7 +896,10 @@ int conv_kg(int BN, int CB, int splits) {
 // grid of a conv kernel whose epilogue writes BN partials: a multiple of the N-tile
 // count, so every CTA's work items share one N tile (w = blockIdx + k * grid)
 int conv_stats_grid(int work, int n_tiles_n) {
-  const int g = conv_grid(work);
+  // PETRA_CONV_TC_CTAS (default: the common cap) for the im2col kernel alone: its small-M
+  // layers (few tiles, long K loops) are the ones a wider grid speeds up
+  static const int tc_cap = env_int("PETRA_CONV_TC_CTAS", 0);
+  const int g = tc_cap > 0 ? std::max(1, std::min({work, tc_cap, kNumSMs})) : conv_grid(work);
   return std::max(n_tiles_n, g / n_tiles_n * n_tiles_n);
 }
 

@@ -30,6 +30,8 @@ CASES = {
     # DS unit: projections without ReLU, strided operand views
     "ds_rev": (lambda: [DSUnit(0, Branch([ConvBN(64, 128, 3, 2)]), ConvBN(64, 128, 1, 2, relu=False),
                                ConvBN(64, 128, 1, 2, relu=False)), rev(128, 1)], 6, (14, 14, 64), L.BF16_TC),
+    # ImageNet-style stem: 7x7 / 2 conv + BN-ReLU + 3x3 / 2 max-pool, then a reversible unit
+    "stem_maxpool": (lambda: [StemUnit(3, 128, 7, 2, True), rev(64, 0)], 2, (32, 32, 3), L.BF16_TC),
 }
 
 
@@ -59,6 +61,11 @@ def main(case, out):
     if not stem:
         for k in range(4):
             arrs[f"r{k}"] = res[k].cpu().numpy()
+    # the evaluation forward (BN on the running statistics) of the same stage
+    oe = [torch.empty(st.out_shape, device="cuda") for _ in range(2)]
+    st.eval(xs[0], None if stem else xs[1], oe[0], oe[1])
+    torch.cuda.synchronize()
+    arrs["eval0"], arrs["eval1"] = oe[0].cpu().numpy(), oe[1].cpu().numpy()
     np.savez(out, **arrs)
 
 

@@ -1,7 +1,8 @@
 """Small-shape workload for tests/test_sanitizer_gpu.py (run under compute-sanitizer):
 the tcgen05 / TMEM / TMA convolution kernels (conv_tc forward / dgrad / wgrad, the halo
 forward / dgrad / wgrad, the stem), the fused BN statistics, and one bf16 stage tick
-(TMA-staged BN apply / backward-reduce / dz, the update) through the C ABI."""
+(TMA-staged BN apply / backward-reduce / dz, the update, the max-pool stem, the evaluation
+forward) through the C ABI."""
 import ctypes as C
 import os
 import sys
@@ -50,6 +51,7 @@ def main():
     with tempfile.TemporaryDirectory() as d:
         W.main("stem_rev_ragged", os.path.join(d, "a.npz"))
         W.main("ds_rev", os.path.join(d, "b.npz"))
+        W.main("stem_maxpool", os.path.join(d, "c.npz"))
     torch.cuda.synchronize()
     print("sanitizer target done")
 
