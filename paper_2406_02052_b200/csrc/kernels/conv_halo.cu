@@ -473,8 +473,13 @@ struct WHaloParams {
   int pb;      // pixels per block (64 or 128): pb / 16 MMA K steps per accumulator
   int off[9];
   int Mr;      // 9 * Ci
-  float *out;  // [splits][Co][Mr]
+  int cs;      // > 1: clusters of cs consecutive K splits of one item reduce their partials
+               // through distributed shared memory (single pass: one work item per CTA)
+  float *out;  // [splits / cs][Co][Mr]
 };
+// the cluster-reduction tile: accumulators 0-3 (taps 0-7, 128 rows) and the tap-8 half of
+// accumulator 4, fp32 [acc][64 co][128 rows] (the last one rows 64..127 only)
+constexpr int kWTileFloats = 4 * 64 * 128 + 64 * 64;
 constexpr int kWStages = 4;
 constexpr int kWThreads = 192;
 __device__ __forceinline__ int tap_a(int i) { return i < 4 ? 2 * i : 7; }
@@ -580,6 +585,27 @@ wgrad_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const int sp = w % P.splits;
       tc::mbar_wait(tfull, it & 1);
       tc::tc_fence_after();
+      if (P.cs > 1) {  // stage the partial in this CTA's (idle) operand ring for the cluster
+        float *tile = reinterpret_cast<float *>(smem);
+#pragma unroll 1
+        for (int i = 0; i < 5; ++i) {
+          if (i == 4 && half == 0) continue;  // the repeated tap 7
+          float v[64];
+          if (kb1 > kb0) {
+            tc::tmem_ld16xN<4>(tmem_base + ((uint32_t)(q * 32) << 16) + i * 64, v);
+          } else {  // an empty (padding) split: nothing was accumulated
+#pragma unroll
+            for (int j = 0; j < 64; ++j) v[j] = 0.f;
+          }
+          float *t = tile + (i < 4 ? (size_t)i * 64 * 128 : (size_t)4 * 64 * 128 - 64);  // i = 4: rows 64..127
+#pragma unroll
+          for (int j = 0; j < 64; ++j) t[(size_t)j * (i < 4 ? 128 : 64) + row] = v[j];
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tempty);
+        continue;
+      }
       float *o = P.out + ((size_t)sp * P.Co + nt * 64) * P.Mr;
 #pragma unroll 1
       for (int i = 0; i < 5; ++i) {
@@ -605,10 +631,50 @@ wgrad_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem_base, 512);
   }
+  if (P.cs > 1) {
+    // every CTA of the cluster staged its split's partial; CTA `rank` sums slice `rank` of
+    // the tile over the cluster's CTAs in rank order (deterministic) and writes it to the
+    // cluster's partial (or dw when one cluster covers all splits)
+    tc::cluster_sync();
+    const uint32_t rank = tc::cluster_ctarank();
+    int cb, nt, kb0, kb1;
+    decode(blockIdx.x, cb, nt, kb0, kb1);
+    const int grp = (blockIdx.x % P.splits) / P.cs;
+    float *o = P.out + ((size_t)grp * P.Co + nt * 64) * P.Mr;
+    const uint32_t tbase = tc::smem_u32(smem);
+    const int per = kWTileFloats / P.cs;  // a multiple of 4 for cs in {2, 4, 8}
+    const int g0 = (int)rank * per / 4, g1 = g0 + per / 4;
+    for (int gq = g0 + (int)threadIdx.x; gq < g1; gq += blockDim.x) {
+      float4 part[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)  // every rank's four floats in flight at once ...
+        if (r < P.cs) part[r] = tc::ld_dsmem_f32x4(tbase + 16u * (uint32_t)gq, (uint32_t)r);
+      float4 sum = part[0];
+#pragma unroll
+      for (int r = 1; r < 8; ++r)  // ... then added in rank order (deterministic)
+        if (r < P.cs) {
+          sum.x += part[r].x; sum.y += part[r].y; sum.z += part[r].z; sum.w += part[r].w;
+        }
+      const int e = 4 * gq;
+      int i, c, rw;
+      if (e < 4 * 64 * 128) {
+        i = e >> 13;
+        c = (e >> 7) & 63;
+        rw = e & 127;
+      } else {
+        i = 4;
+        c = (e - 4 * 64 * 128) >> 6;
+        rw = 64 + ((e - 4 * 64 * 128) & 63);
+      }
+      const int hf = rw >> 6, tap = hf ? tap_b(i) : tap_a(i);  // four consecutive rows of one half
+      *reinterpret_cast<float4 *>(o + (size_t)c * P.Mr + tap * P.Ci + cb * 64 + (rw & 63)) = sum;
+    }
+    tc::cluster_sync();  // the peers have read this CTA's tile
+  }
 }
 
 struct WHaloPlan {
-  int pb, HR, box_rows, splits, kb_per_split, KBtot;
+  int pb, HR, box_rows, splits, kb_per_split, KBtot, cs;
   size_t smem;
 };
 WHaloPlan whalo_plan(int B, int H, int W, int Ci, int Co) {
@@ -626,7 +692,20 @@ WHaloPlan whalo_plan(int B, int H, int W, int Ci, int Co) {
   const int want = std::max(1, std::min(p.KBtot, (int)cdiv(ctas, items)));
   p.kb_per_split = (int)cdiv(p.KBtot, want);
   p.splits = (int)cdiv(p.KBtot, p.kb_per_split);
-  p.smem = 1024 + (size_t)kWStages * ((size_t)p.HR * 128 + (size_t)p.pb * 128) + 256;
+  const size_t ring = (size_t)kWStages * ((size_t)p.HR * 128 + (size_t)p.pb * 128);
+  p.smem = 1024 + ring + 256;
+  // cluster reduction of the K splits (PETRA_WGRAD_CLUSTER=8; off by default): one pass (every
+  // CTA one work item), the partial tile fits in the operand ring; splits padded to a
+  // multiple of the cluster with empty splits
+  static const int cl = env_int("PETRA_WGRAD_CLUSTER", 1);  // 8 measured 2.4 % slower (DESIGN 7)
+  p.cs = 1;
+  if (cl > 1 && p.splits >= cl && ring >= (size_t)kWTileFloats * 4) {
+    const int padded = (int)cdiv(p.splits, cl) * cl;
+    if ((int64_t)items * padded <= kNumSMs) {
+      p.cs = cl;
+      p.splits = padded;
+    }
+  }
   return p;
 }
 }  // namespace
@@ -662,7 +741,8 @@ bool wgrad_halo_eligible(const ConvGeom &g) {
 size_t wgrad_halo_workspace(const ConvGeom &g) {
   if (!wgrad_halo_eligible(g)) return 0;
   const WHaloPlan p = whalo_plan(g.B, g.H, g.W, g.Ci, g.Co);
-  return p.splits > 1 ? (size_t)p.splits * g.Co * g.K() * sizeof(float) : 0;
+  const int parts = p.splits / p.cs;
+  return parts > 1 ? (size_t)parts * g.Co * g.K() * sizeof(float) : 0;
 }
 
 // dw[co][kh][kw][ci] = sum over pixels of dz (x) x, both operands zero-bordered
@@ -687,8 +767,10 @@ void wgrad_halo_run(const ConvGeom &g, const __nv_bfloat16 *dz_pad, const __nv_b
   P.pb = pl.pb;
   for (int t = 0; t < 9; ++t) P.off[t] = (t / 3 - 1) * Wp + (t % 3 - 1);
   P.Mr = g.K();
-  if (pl.splits > 1 && !ws) throw PetraError(PETRA_E_ARG, "wgrad_halo_run: workspace required");
-  P.out = pl.splits > 1 ? ws : dw;
+  P.cs = pl.cs;
+  const int parts = pl.splits / pl.cs;  // partials left for splitk_sum
+  if (parts > 1 && !ws) throw PetraError(PETRA_E_ARG, "wgrad_halo_run: workspace required");
+  P.out = parts > 1 ? ws : dw;
   const int64_t Mp = (int64_t)g.B * (g.H + 2) * Wp;
   cuuint64_t xd[2] = {(cuuint64_t)g.Ci, (cuuint64_t)Mp};
   cuuint64_t xs[1] = {(cuuint64_t)g.Ci * 2};
@@ -700,9 +782,10 @@ void wgrad_halo_run(const ConvGeom &g, const __nv_bfloat16 *dz_pad, const __nv_b
   CUtensorMap tx = tma_map(x_pad, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xd, xs, xb, es);
   CUtensorMap tdz = tma_map(dz_pad, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dd, ds, dbx, es);
   const int work = P.CB * P.n_nt * P.splits;
-  launch_k(wgrad_halo_kernel, std::min(work, kNumSMs), kWThreads, pl.smem, st, tx, tdz, P);
+  if (pl.cs > 1) launch_k_cluster(wgrad_halo_kernel, work, kWThreads, pl.smem, st, pl.cs, tx, tdz, P);
+  else launch_k(wgrad_halo_kernel, std::min(work, kNumSMs), kWThreads, pl.smem, st, tx, tdz, P);
   PETRA_LAUNCH_CHECK();
-  if (pl.splits > 1) splitk_sum(ws, pl.splits, (int64_t)g.Co * g.K(), dw, st);
+  if (parts > 1) splitk_sum(ws, parts, (int64_t)g.Co * g.K(), dw, st);
 }
 
 // a 3x3 stride-1 pass whose padded grid fills at least ~3/4 of a wave of work items

@@ -100,6 +100,30 @@ __device__ __forceinline__ void sts128(uint32_t addr, const uint4 &v) {
                : "memory");
 }
 
+// ---------------------------------------------------------------- clusters (distributed shared memory)
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// every thread of every CTA of the cluster: release this CTA's smem writes, acquire the peers'
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// four floats of CTA `rank`'s shared memory at the (16-byte aligned) address `saddr` has in
+// this CTA.  Volatile (kept after the cluster barrier); the caller issues all ranks' loads
+// before the first add, so they are in flight together.
+__device__ __forceinline__ float4 ld_dsmem_f32x4(uint32_t saddr, uint32_t rank) {
+  uint32_t remote;
+  float4 v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(saddr), "r"(rank));
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(remote)
+               : "memory");
+  return v;
+}
+
 // generic-proxy smem writes (st.shared) made visible to the async proxy (tcgen05.mma)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
