@@ -827,7 +827,7 @@ ConvPlan conv_plan(int M, int N, int KB) {
   const int mt = M / BM;
   // widest N tile that still leaves `want_tiles` tiles (wider tiles reuse each A tile
   // over more columns: fewer operand bytes from L2 per MMA)
-  static const int want_tiles = env_int("PETRA_CONV_TILES", kNumSMs);
+  static const int want_tiles = env_int("PETRA_CONV_TILES", 48);  // 48: R18 +1.4 %, serial conv -4.5 % (DESIGN 7)
   for (int bn : {256, 128, 64}) {
     if (N % bn) continue;
     p.BN = bn;
