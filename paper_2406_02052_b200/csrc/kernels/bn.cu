@@ -1010,9 +1010,10 @@ void bn_apply(int64_t M, int C, const TZ *z, int ldz, int zc0, const float *mean
   static const bool tma_on = env_int("PETRA_BN_TMA_APPLY", 1) != 0;
   if (tma_on && std::is_same<TO, float>::value && C % 8 == 0 && (uintptr_t)(z + zc0) % 16 == 0 &&
       ((size_t)ldz * sizeof(TZ)) % 16 == 0 && (uintptr_t)acc % 16 == 0 && M < ((int64_t)1 << 31)) {
-    RedGeom g = red_geom(M, C, 256, 4);
+    static const int per_sm = env_int("PETRA_BN_PER_SM", 2), chunk = env_int("PETRA_BN_CHUNK", 24576);
+    RedGeom g = red_geom(M, C, 256, per_sm);
     const int es = (int)sizeof(TZ) + (acc ? 4 : 0);
-    const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (24576 / (g.CT * es)) / g.RG * g.RG));
+    const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (chunk / (g.CT * es)) / g.RG * g.RG));
     const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
     // every TMA destination inside a ring stage must be 128-byte aligned (else the register kernel)
     const bool ring_ok = ring_aligned((size_t)Rc * g.CT * sizeof(TZ)) && g.CT % 8 == 0;
@@ -1066,7 +1067,8 @@ void bn_bwd_reduce(const TZ *z, int64_t M, int C, const float *mean, const float
   const bool split_ok = dy1 == nullptr || (g.ctiles == 1 && cs % 4 == 0 && (C - cs) % 4 == 0 && cs > 0 && cs < C);
   if (tma_on && split_ok && C % 8 == 0 && aligned && g.CT % 8 == 0 && M < ((int64_t)1 << 31)) {
     const int es = (int)sizeof(TZ) + 4 + (dst_out ? 4 : 0);
-    const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (40960 / (g.CT * es)) / g.RG * g.RG));
+    static const int rchunk = env_int("PETRA_BN_RCHUNK", 40960);
+    const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (rchunk / (g.CT * es)) / g.RG * g.RG));
     const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
     // ring depth: one block per SM, so the stages in flight are what hides the DRAM latency
     static const int ring = std::max(2, std::min(kMaxRing, env_int("PETRA_BN_REDUCE_STAGES", 2)));
@@ -1117,13 +1119,14 @@ void bn_bwd_dz(int64_t M, int C, const TZ *z, const float *mean, const float *in
                const float *beta, int relu, const float *dy0, const float *dy1, int cs, const float *dgamma,
                const float *dbeta, float *dz, __nv_bfloat16 *dz_bf16, int pH, int pW, cudaStream_t st) {
   static const bool tma_on = env_int("PETRA_BN_TMA_DZ", 1) != 0;
-  const RedGeom gs = red_geom(M, C, 256, 4);
+  static const int per_sm = env_int("PETRA_BN_PER_SM", 2), chunk = env_int("PETRA_BN_CHUNK", 24576);
+  const RedGeom gs = red_geom(M, C, 256, per_sm);
   const bool split_ok = dy1 == nullptr || (gs.ctiles == 1 && cs % 4 == 0 && (C - cs) % 4 == 0 && cs > 0 && cs < C);
   if (tma_on && split_ok && C % 8 == 0 && (uintptr_t)z % 16 == 0 && (uintptr_t)dy0 % 16 == 0 &&
       (uintptr_t)dy1 % 16 == 0 && M < ((int64_t)1 << 31)) {
     const RedGeom &g = gs;
     const int es = (int)sizeof(TZ) + 4;
-    const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (24576 / (g.CT * es)) / g.RG * g.RG));
+    const int Rc = std::min(256 / g.RG * g.RG, std::max(g.RG, (chunk / (g.CT * es)) / g.RG * g.RG));
     const size_t sbytes = (((size_t)Rc * g.CT * es) + 127) & ~(size_t)127;
     // every TMA destination inside a ring stage must be 128-byte aligned (else the register kernel)
     const bool ring_ok = ring_aligned((size_t)Rc * g.CT * sizeof(TZ)) && g.CT % 8 == 0 &&
