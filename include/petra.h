@@ -443,6 +443,13 @@ petra_status petra_conv_bn_stats(const petra_conv_geom *g, int32_t engine, const
  * stem: Ci <= 4, k <= 8, Co in {64, 128, 256}; forward and wgrad), the
  * gathered-im2col kernel. */
 int32_t petra_conv_engine(const petra_conv_geom *g, int32_t mode, int32_t precision);
+/* The tcgen05 im2col kernel's launch plan for a forward (mode 0) or stride-1 dgrad
+ * (mode 1) pass of the geometry (host only, no device work): plan[0] = N tile BN,
+ * plan[1] = K splits, plan[2] = cluster size (> 1: the splits of a tile are the CTAs
+ * of one thread-block cluster reduced through distributed shared memory -- DESIGN.md 7
+ * "Cluster split-K").  Errors: PETRA_E_ARG (NULL, bad mode), PETRA_E_UNSUPPORTED (no
+ * tensor-core im2col path for the pass). */
+petra_status petra_conv_plan(const petra_conv_geom *g, int32_t mode, int32_t *plan);
 int64_t petra_launch_count(void);
 petra_status petra_profile(int32_t enable);
 petra_status petra_profile_read(petra_prof_entry *out, int32_t cap, int32_t *n);

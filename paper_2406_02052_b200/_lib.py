@@ -132,6 +132,7 @@ SIGS = {
     "petra_conv_run": (C.c_int, [I32, I32, C.POINTER(PetraConvGeom), VP, VP, VP, VP]),
     "petra_conv_engine": (C.c_int32, [C.POINTER(PetraConvGeom), I32, I32]),
     "petra_conv_bn_stats": (C.c_int, [C.POINTER(PetraConvGeom), I32, VP, VP, VP, VP, VP]),
+    "petra_conv_plan": (C.c_int, [C.POINTER(PetraConvGeom), I32, C.POINTER(I32)]),
     "petra_conv_bench": (I32, [I32, I32, C.POINTER(PetraConvGeom), I32, I32, C.POINTER(C.c_float)]),
     "petra_launch_count": (C.c_int64, []),
     "petra_profile": (C.c_int, [I32]),

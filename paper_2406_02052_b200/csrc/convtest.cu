@@ -198,3 +198,13 @@ extern "C" int32_t petra_conv_engine(const petra_conv_geom *pg, int32_t mode, in
   if (petra::conv_tc_supported(g, mode)) return 1;
   return (mode != 1 && petra::stem_tc_supported(g)) ? 1 : 0;
 }
+
+extern "C" petra_status petra_conv_plan(const petra_conv_geom *pg, int32_t mode, int32_t *plan) {
+  if (!pg || !plan || (mode != 0 && mode != 1)) return PETRA_E_ARG;
+  petra::ConvGeom g = petra::make_geom(pg->batch, pg->h, pg->w, pg->cin, pg->cout, pg->ksize, pg->stride);
+  if (!petra::conv_tc_supported(g, mode) || (mode == 1 && g.s != 1)) return PETRA_E_UNSUPPORTED;
+  int out[3];
+  petra::conv_tc_plan_info(g, mode, out);
+  for (int i = 0; i < 3; ++i) plan[i] = out[i];
+  return PETRA_OK;
+}

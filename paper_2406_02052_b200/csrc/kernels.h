@@ -23,6 +23,7 @@ void conv_wgrad_simt(const ConvGeom &g, const float *dz, const float *x, float *
 bool conv_tc_supported(const ConvGeom &g, int mode);   // mode 0 fwd, 1 dgrad, 2 wgrad
 void conv_tc_prepare();  // one-time kernel attributes (before any graph capture)
 size_t conv_tc_workspace(const ConvGeom &g, int mode);  // split-K workspace bytes
+void conv_tc_plan_info(const ConvGeom &g, int mode, int *out);  // {BN, splits, cluster size}
 // BN partial statistics written by a conv epilogue: `rows` rows [rows][Co][2] of
 // (mean, M2) over the CTA's valid output rows, one row per CTA, followed by the rows'
 // counts (float[rows] at part + rows * Co * 2); with `groups` > 1 the CTAs each own one

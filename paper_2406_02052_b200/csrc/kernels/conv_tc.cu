@@ -51,6 +51,9 @@ struct ConvTCParams {
   int s_in;                  // A row coordinate = s_in * grid_row + dh
   int OH, OW, oss, ph, pw;   // grid (i, j) -> output pixel (i*oss+ph, j*oss+pw) of an OH x OW image
   int splits, kb_per_split;  // split-K (small-M layers): splits > 1 -> partials into ws[split][M][N]
+  int cs;                    // > 1: cluster split-K -- the `splits` (= cs) K slices of a tile are the cs
+                             // CTAs of one thread-block cluster, one work item per CTA; partials are
+                             // reduced on chip through distributed shared memory (no ws, no 2nd launch)
   float *ws;
   const float *addend;       // nullable (fp32 output only): out = addend + conv
   void *out;                 // [B*OH*OW][N], fp32 or bf16 (OUT16); written by TMA stores through tmO
@@ -238,6 +241,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if (lane == 0) tc::bulk_wait_read<1>();
       __syncwarp();
     };
+    if (P.cs > 1) {
+      // cluster split-K, one item per CTA: the accumulator is pushed to its row owners after
+      // the kernel's __syncthreads and the first cluster barrier (every CTA's MMAs are done,
+      // so every operand ring is free to receive)
+      tc::mbar_wait(&tfull[0], 0);
+      tc::tc_fence_after();
+    } else {
     // per-lane shifted statistics of this warp's columns (the CTA's N tile is fixed),
     // tile after tile in registers (tc::ColStats)
     constexpr int CW = OUT16 ? 64 : 32;  // columns per 128-byte staged row
@@ -343,11 +353,156 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                              P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2,
                              P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
     }
+    }  // P.cs == 1
   }
   __syncthreads();
+  if (P.cs > 1) {
+    // Cluster reduction.  CTA `rank` owns rows [rank * 128 / cs, (rank + 1) * 128 / cs) of the
+    // tile (4 / cs groups of 32 rows).  Every CTA PUSHES its accumulator rows to their owner
+    // with remote stores (st.shared::cluster: posted, no round-trip latency per access --
+    // pulling with ld.shared::cluster measured latency-bound, ~2x slower than no split),
+    // into the owner's operand ring as [source rank][owned row][BN] fp32, 16-byte chunks
+    // XOR-swizzled by row & 7.  After the second barrier the owner sums its rows over the
+    // sources in rank order (deterministic) from its own shared memory and runs the
+    // epilogue on them (addend, TMA store, BN statistics: one partial row per CTA).
+    tc::cluster_sync();  // every CTA's MMAs are complete: the rings are free
+    if (warp >= 2) {
+      const int q = warp & 3, hc = (warp - 2) >> 2, row = q * 32 + lane;
+      const int rpo = BM / P.cs;  // rows per owner
+      const int owner = row / rpo, lrow = row - owner * rpo;
+      const uint32_t me = tc::cluster_ctarank();
+      const uint32_t dst = tc::mapa(tc::smem_u32(smem) + (uint32_t)((int)me * rpo + lrow) * BN * 4, (uint32_t)owner);
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int c = 32 * hc; c < BN; c += 64) {
+        float v[32];
+        tc::tmem_ld16xN<2>(trow + c, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          tc::st_dsmem_f32x4(dst + ((uint32_t)(((c >> 2) + i) ^ (lrow & 7)) << 4),
+                             make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+      }
+      tc::tc_fence_before();
+    }
+  }
+  if (P.cs > 1) __syncthreads();
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem_base, 2 * BN);
+  }
+  if (P.cs > 1) {
+    tc::cluster_sync();  // every push has landed
+    if (warp >= 2) {
+      const int e = warp - 2;
+      const int rank = (int)tc::cluster_ctarank();
+      int mt, nt, sp, kb0, kb1;
+      decode(blockIdx.x, mt, nt, sp, kb0, kb1);
+      const int ng = 4 / P.cs;                // 32-row groups of this rank
+      constexpr int CW = OUT16 ? 64 : 32;    // columns per 128-byte staged row
+      constexpr int NCHK = BN / CW;
+      uint8_t *ebuf = sepi + e * 2 * kEpiBuf;
+      int eb = 0;
+      uint32_t aph = 0;
+      const uint32_t tile = tc::smem_u32(smem);
+      if (lane == 0) tc::tma_prefetch(&tmO);
+#pragma unroll 1
+      for (int u = e; u < ng * NCHK; u += kEpiWarps) {
+        const int g = u % ng, k = u / ng;
+        const int r0 = (rank * ng + g) * 32, r = r0 + lane;  // tile rows of this unit / lane
+        const int m = mt * BM + r;
+        const int b = tc::fdiv(m, f_ghw), rr = m - b * GHW, i = tc::fdiv(rr, f_wb), j = rr - i * P.Wb;
+        const bool valid = b < P.B && i < P.Gh && j < P.Gw;
+        const int m0w = mt * BM + r0;
+        const int wb = tc::fdiv(m0w, f_ghw), wr = m0w - wb * GHW, wi = tc::fdiv(wr, f_wb), wj = wr - wi * P.Wb;
+        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+        float v[CW];
+        const int lr = r - rank * BM / P.cs;  // owned row index
+        const uint32_t src0 = tile + (uint32_t)lr * BN * 4, sstride = (uint32_t)(BM / P.cs) * BN * 4;
+#pragma unroll
+        for (int c4 = 0; c4 < CW / 4; ++c4) {
+          const uint32_t a = src0 + ((uint32_t)(((k * CW) >> 2) + c4) ^ (uint32_t)(lr & 7)) * 16u;
+          uint4 pr[4];
+#pragma unroll
+          for (int q2 = 0; q2 < 4; ++q2)  // the sources' partials, added in rank order
+            if (q2 < P.cs) pr[q2] = tc::lds128(a + (uint32_t)q2 * sstride);
+          float4 sum = make_float4(__uint_as_float(pr[0].x), __uint_as_float(pr[0].y), __uint_as_float(pr[0].z),
+                                   __uint_as_float(pr[0].w));
+#pragma unroll
+          for (int q2 = 1; q2 < 4; ++q2)
+            if (q2 < P.cs) {
+              sum.x += __uint_as_float(pr[q2].x);
+              sum.y += __uint_as_float(pr[q2].y);
+              sum.z += __uint_as_float(pr[q2].z);
+              sum.w += __uint_as_float(pr[q2].w);
+            }
+          v[4 * c4] = sum.x;
+          v[4 * c4 + 1] = sum.y;
+          v[4 * c4 + 2] = sum.z;
+          v[4 * c4 + 3] = sum.w;
+        }
+        if (!OUT16 && P.addend) {  // the addend box (the store box's geometry) by TMA
+          if (lane == 0) tc::bulk_wait_read<1>();
+          __syncwarp();
+          if (lane == 0) {
+            tc::mbar_arrive_expect_tx(&abar[e], kEpiBuf);
+            tc::tma_load_4d(ebuf + eb * kEpiBuf, &tmAdd, &abar[e], nt * BN + k * CW, wj, wi, wb);
+          }
+          tc::mbar_wait(&abar[e], aph);
+          aph ^= 1;
+          const uint32_t sp_ = tc::smem_u32(ebuf + eb * kEpiBuf) + lane * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            const uint4 w4 = tc::lds128(sp_ + ((ch ^ (lane & 7)) << 4));
+            v[4 * ch] += __uint_as_float(w4.x);
+            v[4 * ch + 1] += __uint_as_float(w4.y);
+            v[4 * ch + 2] += __uint_as_float(w4.z);
+            v[4 * ch + 3] += __uint_as_float(w4.w);
+          }
+          __syncwarp();
+        }
+        if (!valid) {
+#pragma unroll
+          for (int jj = 0; jj < CW; ++jj) v[jj] = 0.f;
+        }
+        if (lane == 0) tc::bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t *staged = ebuf + eb * kEpiBuf;
+        stage_row<OUT16>(staged, lane, v);
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tc::tma_store_4d(&tmO, staged, nt * BN + k * CW, wj, wi, wb);
+          tc::bulk_commit();
+        }
+        eb ^= 1;
+        if (P.stats) {  // this unit's 32 rows x CW columns into the statistics slot of group g
+          tc::ColStats cst;
+          tc::colstats_zero(cst);
+          tc::colstats_tile<OUT16, true>(staged, 128, lane, vmask, 0, cst);
+          const int nv = __popc(vmask);
+          const int col = k * CW + (OUT16 ? 2 * lane : lane);
+          float *slot = sstat + (size_t)g * BN * 2;
+          const float2 a0 = tc::colstats_final(cst, 0, nv);
+          slot[2 * col] = a0.x;
+          slot[2 * col + 1] = a0.y;
+          if (OUT16) {
+            const float2 a1 = tc::colstats_final(cst, 1, nv);
+            slot[2 * col + 2] = a1.x;
+            slot[2 * col + 3] = a1.y;
+          }
+          if (k == 0 && lane == 0) scnt[g] = nv;
+        }
+      }
+      if (lane == 0) tc::bulk_wait_all();
+      if (P.stats) {
+        if (e == 0 && lane >= ng && lane < 4) scnt[lane] = 0;  // slots of no rows
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        const int ridx = sp * (P.M / BM) * n_tiles_n + mt * n_tiles_n + nt;  // ridx % n_tiles_n == nt
+        tc::cta_stats_row<4>(sstat, scnt, BN, e * 32 + lane, kEpiWarps * 32,
+                             P.stats + ((size_t)ridx * P.N + (size_t)nt * BN) * 2,
+                             P.stats + (size_t)gridDim.x * P.N * 2 + ridx);
+      }
+    }
   }
 }
 
@@ -820,10 +975,14 @@ int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64); }
 // N tile and K split for a conv GEMM: the largest N tile that still fills a wave
 // of SMs; below that, BN = 64 and a split of K (deterministic workspace reduction).
 struct ConvPlan {
-  int BN, splits, kb_per_split;
+  int BN, splits, kb_per_split, cs;
 };
+// Operand cycles of one CTA streaming `kb` k-blocks of a 128 x bn tile: the SM's TMA fill
+// rate (~40 B/clk measured on the conv kernels: 24-48 KB per k-block in 600-1200 cycles,
+// DESIGN.md 7) bounds these small-tile layers, not the MMAs.
+static double operand_cycles(int kb, int bn) { return kb * (double)(A_BYTES + bn * BK * 2) / 40.0; }
 ConvPlan conv_plan(int M, int N, int KB) {
-  ConvPlan p{64, 1, KB};
+  ConvPlan p{64, 1, KB, 1};
   const int mt = M / BM;
   // widest N tile that still leaves `want_tiles` tiles (wider tiles reuse each A tile
   // over more columns: fewer operand bytes from L2 per MMA)
@@ -842,6 +1001,34 @@ ConvPlan conv_plan(int M, int N, int KB) {
     want = std::min(want, std::max(1, KB / 4));  // at least 4 K-blocks per split
     p.kb_per_split = (int)cdiv(KB, want);
     p.splits = (int)cdiv(KB, p.kb_per_split);
+  }
+  // Cluster split-K for few-tile, long-K layers (R18 layers 3-4, R50 layer 4): a tile's K
+  // range over cs CTAs of one cluster, reduced through DSMEM in the same kernel.  Chosen
+  // when the modelled time (one CTA's operand stream + the cluster reduction) beats the
+  // plain plan's by 20 %; the N tile is re-picked for it (wider tiles: fewer operand bytes).
+  // off by default: R18 -11 % in the step (the clusters' co-scheduling under the tick's
+  // stream concurrency), mixed alone (DESIGN.md 7 "Cluster split-K")
+  static const int cs_on = env_int("PETRA_CONV_CS", 0);
+  static const int cs_ctas = std::min(kNumSMs, env_int("PETRA_CONV_CS_CTAS", 128));
+  if (cs_on && p.splits == 1) {
+    const double t0 = (double)cdiv(tiles, conv_grid(tiles)) * operand_cycles(KB, p.BN);
+    double best = 0.8 * t0;
+    for (int bn : {256, 128, 64}) {
+      if (N % bn) continue;
+      const int t = mt * (N / bn);
+      for (int cs : {4, 2}) {
+        if (KB % cs || KB / cs < 4 || t * cs > cs_ctas) continue;
+        // reduction: (cs-1)/cs of the fp32 tile pushed to the peers at ~20 B/clk (DSMEM,
+        // B300_MICROARCH.md)
+        const double e = operand_cycles(KB / cs, bn) + (double)(cs - 1) * BM * bn * 4 / cs / 20.0;
+        if (e < best) {
+          best = e;
+          p.BN = bn;
+          p.cs = p.splits = cs;
+          p.kb_per_split = KB / cs;
+        }
+      }
+    }
   }
   return p;
 }
@@ -915,11 +1102,17 @@ void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParam
   constexpr int STAGES = conv_stages(BN, KG);
   const size_t smem = conv_smem(BN, KG, P.stats ? conv_stat_bytes(BN, OUT16) : 0);  // attribute: conv_tc_prepare
   const int work = (P.M / BM) * (P.N / BN) * P.splits;
-  const int grid = conv_stats_grid(work, P.N / BN);
   const CUtensorMap to = out_map(P.out, OUT16, P);
-  const CUtensorMap tw = P.splits > 1 ? ws_map(P.ws, P.N, (int64_t)P.splits * P.M) : to;
   // the addend in the output's geometry (fp32 outputs only)
   const CUtensorMap tad = (!OUT16 && P.addend) ? out_map(const_cast<float *>(P.addend), false, P) : to;
+  if (P.cs > 1) {  // cluster split-K: one work item per CTA, clusters of cs consecutive CTAs
+    launch_k_cluster(conv_tc_kernel<BN, STAGES, OUT16, KG>, dim3(work), dim3(kConvThreads), smem, st, P.cs, ta, tb,
+                     to, to, tad, P);
+    PETRA_LAUNCH_CHECK();
+    return;
+  }
+  const int grid = conv_stats_grid(work, P.N / BN);
+  const CUtensorMap tw = P.splits > 1 ? ws_map(P.ws, P.N, (int64_t)P.splits * P.M) : to;
   launch_k(conv_tc_kernel<BN, STAGES, OUT16, KG>, grid, kConvThreads, smem, st, ta, tb, to, tw, tad, P);
   PETRA_LAUNCH_CHECK();
   if (P.splits > 1) {
@@ -937,7 +1130,7 @@ struct LaunchPlan {
 LaunchPlan launch_plan(const ConvTCParams &P, float *ws) {
   LaunchPlan L;
   L.pl = conv_plan(P.M, P.N, P.ntaps * P.CB);
-  if (L.pl.splits > 1 && !ws) {
+  if (L.pl.splits > 1 && L.pl.cs == 1 && !ws) {
     L.pl.splits = 1;
     L.pl.kb_per_split = P.ntaps * P.CB;
   }
@@ -952,8 +1145,9 @@ void launch_any(const CUtensorMap &ta, const LaunchPlan &L, const __nv_bfloat16 
   const ConvPlan &pl = L.pl;
   P.splits = pl.splits;
   P.kb_per_split = pl.kb_per_split;
+  P.cs = pl.cs;
   P.ws = ws;
-  if (P.splits > 1) P.stats = nullptr;  // stats need final z (split-K: standalone pass)
+  if (P.splits > 1 && P.cs == 1) P.stats = nullptr;  // stats need final z (split-K: standalone pass)
   if (out16 && P.addend) throw PetraError(PETRA_E_ARG, "conv_tc: addend needs an fp32 output");
   CUtensorMap tb = mat_map3(w, wrows, wK, pl.BN, L.kg);
   if (L.kg == 2) {
@@ -1019,7 +1213,8 @@ StatsRows run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const _
   const int BN = L.pl.BN;
   StatsRows r;
   r.groups = P.N / BN;
-  r.rows = conv_stats_grid((P.M / BM) * (P.N / BN) * P.splits, r.groups);  // one partial row per CTA
+  const int work = (P.M / BM) * (P.N / BN) * P.splits;
+  r.rows = L.pl.cs > 1 ? work : conv_stats_grid(work, r.groups);  // one partial row per CTA
   return r;
 }
 
@@ -1169,7 +1364,18 @@ size_t conv_tc_workspace(const ConvGeom &g, int mode) {
   const int KB = (mode == 0 ? g.k * g.k * g.Ci : g.k * g.k * g.Co) / 64;  // upper bound (all taps)
   const int64_t M = tiling(g.B, g.Ho, g.Wo, BM).M();
   ConvPlan p = conv_plan((int)M, N, KB);
-  return p.splits > 1 ? (size_t)p.splits * M * N * sizeof(float) : 0;
+  return (p.splits > 1 && p.cs == 1) ? (size_t)p.splits * M * N * sizeof(float) : 0;
+}
+
+// the im2col kernel's plan for a forward (mode 0) or stride-1 dgrad (mode 1) pass:
+// out = {BN, K splits, cluster size}
+void conv_tc_plan_info(const ConvGeom &g, int mode, int *out) {
+  const int N = mode == 0 ? g.Co : g.Ci;
+  const int KB = (mode == 0 ? g.k * g.k * g.Ci : g.k * g.k * g.Co) / 64;
+  const ConvPlan p = conv_plan((int)tiling(g.B, g.Ho, g.Wo, BM).M(), N, KB);
+  out[0] = p.BN;
+  out[1] = p.splits;
+  out[2] = p.cs;
 }
 
 StatsRows conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,

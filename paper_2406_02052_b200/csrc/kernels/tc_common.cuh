@@ -124,6 +124,19 @@ __device__ __forceinline__ float4 ld_dsmem_f32x4(uint32_t saddr, uint32_t rank) 
   return v;
 }
 
+// the shared::cluster address of `saddr` (this CTA's) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(saddr), "r"(rank));
+  return remote;
+}
+// posted 16-byte store into a cluster peer's shared memory (address from mapa)
+__device__ __forceinline__ void st_dsmem_f32x4(uint32_t raddr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(raddr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
 // generic-proxy smem writes (st.shared) made visible to the async proxy (tcgen05.mma)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

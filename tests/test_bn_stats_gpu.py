@@ -25,6 +25,11 @@ GEOMS = {
     "r50_l1_1x1_64to256": ((64, 56, 56, 64, 256, 1, 1), 1),
     "r50_stem_7x7s2": ((64, 224, 224, 3, 128, 7, 2), 1),
     "r18_l1_3x3_64_halo": ((64, 32, 32, 64, 64, 3, 1), 2),
+    # cluster split-K plans (partials reduced through DSMEM, one statistics row per CTA)
+    "r18_l3_3x3_256_cs": ((64, 8, 8, 256, 256, 3, 1), 1),
+    "r18_l4_3x3_512_cs": ((64, 4, 4, 512, 512, 3, 1), 1),
+    "r50_l4_3x3_512_cs": ((64, 7, 7, 512, 512, 3, 1), 1),
+    "r50_l4_1x1_2048to512_cs": ((64, 7, 7, 2048, 512, 1, 1), 1),
 }
 
 

@@ -3,6 +3,7 @@
   * tcgen05 bf16 kernels vs the SIMT kernels on bf16-exact inputs: every product
     is exact in fp32 on both, so only the summation order differs (rel 1e-5)."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -52,6 +53,11 @@ GEOMS = [  # (B, H, W, Ci, Co, k, stride)
     (2, 28, 28, 128, 256, 1, 2), (3, 14, 14, 256, 512, 3, 2), (1, 12, 20, 64, 64, 3, 1),
     (2, 14, 14, 128, 64, 1, 1), (2, 14, 14, 64, 64, 3, 1), (2, 14, 14, 64, 128, 1, 1),
 ]
+# the benchmark's few-tile, long-K layers at b64 (cluster split-K plans): R18 layers 3, 4;
+# R50 layer 4 (7x7 grid: masked padding rows) 3x3 and 1x1
+CS_GEOMS = [(64, 8, 8, 256, 256, 3, 1), (64, 4, 4, 512, 512, 3, 1), (64, 7, 7, 512, 512, 3, 1),
+            (64, 7, 7, 2048, 512, 1, 1)]
+GEOMS += CS_GEOMS
 SIMT_GEOMS = GEOMS[:2] + [(2, 9, 7, 3, 16, 3, 1), (2, 10, 10, 16, 32, 3, 2), (2, 9, 9, 8, 12, 1, 2),
                           (2, 15, 15, 3, 8, 7, 2)]
 
@@ -132,3 +138,14 @@ def test_tc_padded_operands_vs_simt(geom, mode):
     ref = conv_run(mode, 0, geom, a, b, addend)
     got = conv_run(mode, 2, geom, a, b, addend)
     assert rel(got, ref) < 1e-5, rel(got, ref)
+
+
+@pytest.mark.parametrize("geom,mode", [(g, m) for g in CS_GEOMS for m in (0, 1) if not (g[3] == 2048 and m == 1)])
+@pytest.mark.skipif(os.environ.get("PETRA_CONV_CS", "0") != "1", reason="cluster split-K off (PETRA_CONV_CS)")
+def test_cluster_split_plan(geom, mode):
+    """With PETRA_CONV_CS=1 the few-tile layers take the cluster split-K plan (so the parity
+    tests above cover it: tests/test_cluster_split_gpu.py reruns them in that mode)."""
+    plan = (C.c_int32 * 3)()
+    L.call("petra_conv_plan", C.byref(L.PetraConvGeom(*geom)), mode, plan)
+    BN, splits, cs = plan
+    assert cs in (2, 4) and splits == cs, tuple(plan)

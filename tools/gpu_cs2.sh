@@ -1,0 +1,7 @@
+O=gpurun_out/cs3; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 600 python -m pytest tests/test_kernels_gpu.py tests/test_bn_stats_gpu.py -x -q -k "cluster or stats or tc_conv" > $O/pytest_k.log 2>&1
+tail -3 $O/pytest_k.log
+for cfg in "PETRA_CONV_CS=0" "PETRA_CONV_CS=1"; do env $cfg python tools/cs_sweep.py >> $O/sweep.txt 2>&1; done
+cat $O/sweep.txt
+bash tools/ab.sh cs3ab "PETRA_CONV_CS=0" "PETRA_CONV_CS=1" "PETRA_CONV_CS=0" "PETRA_CONV_CS=1"
