@@ -447,7 +447,8 @@ int32_t petra_conv_engine(const petra_conv_geom *g, int32_t mode, int32_t precis
  * (mode 1) pass of the geometry (host only, no device work): plan[0] = N tile BN,
  * plan[1] = K splits, plan[2] = cluster size (> 1: the splits of a tile are the CTAs
  * of one thread-block cluster reduced through distributed shared memory -- DESIGN.md 7
- * "Cluster split-K").  Errors: PETRA_E_ARG (NULL, bad mode), PETRA_E_UNSUPPORTED (no
+ * "Cluster split-K"; -2: CTA pairs, M = 256 tiles on cta_group::2 UMMAs -- DESIGN.md 7
+ * "CTA pairs").  Errors: PETRA_E_ARG (NULL, bad mode), PETRA_E_UNSUPPORTED (no
  * tensor-core im2col path for the pass). */
 petra_status petra_conv_plan(const petra_conv_geom *g, int32_t mode, int32_t *plan);
 int64_t petra_launch_count(void);

@@ -99,7 +99,13 @@ __device__ __forceinline__ void stage_row(uint8_t *buf, int lane, const float *v
 // im2col box whose outermost dimension is the channel block) and ONE B copy (a 3-D box
 // over KG consecutive k-blocks of the weight matrix): KG consecutive [rows][128 B] slabs
 // each, the layout the MMAs read one k-block at a time.
-template <int BN, int STAGES, bool OUT16, int KG>
+//
+// PAIR: the CTAs of a cluster of 2 run M = 256 tiles with cta_group::2 UMMAs (DESIGN.md 7
+// "CTA pairs"): CTA r computes M tile 2 * mp + r of a pair tile mp and loads only ITS 128 A
+// rows and half (BN / 2 rows) of the weight tile -- the MMA reads the other half from the
+// peer -- so an SM streams A + B / 2 instead of A + B per k-block (-25 % at BN = 128, -33 %
+// at BN = 256); rank 0 issues the MMAs, both epilogues drain their own TMEM rows.
+template <int BN, int STAGES, bool OUT16, int KG, bool PAIR = false>
 __global__ void __maxnreg__(PETRA_CONV_MAXREG)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmW,
@@ -107,7 +113,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   pdl_wait_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr uint32_t B_BYTES = BN * BK * 2;
+  constexpr uint32_t B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // this CTA's rows of the weight tile
   constexpr uint32_t STAGE_BYTES = KG * (A_BYTES + B_BYTES);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
   uint64_t *empty = full + STAGES;
@@ -126,12 +132,26 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_n = P.N / BN;
-  const int n_work = (P.M / BM) * n_tiles_n * P.splits;  // (m tile, n tile, K split)
+  // (m tile, n tile, K split); PAIR: (m pair tile, n tile), pair p = blockIdx.x / 2 takes
+  // items p, p + gridDim.x / 2, ...
+  const int n_work = PAIR ? ((P.M / BM + 1) / 2) * n_tiles_n : (P.M / BM) * n_tiles_n * P.splits;
+  const int rank2 = PAIR ? (int)(blockIdx.x & 1) : 0;
+  const int w_first = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int w_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int KB = P.ntaps * P.CB;
   const int GHW = P.Hb * P.Wb;  // padded grid
   const tc::FastDiv &f_sp = P.f_sp, &f_nt = P.f_nt, &f_ghw = P.f_ghw, &f_wb = P.f_wb;
   // work item -> tile coordinates and K-block range
   auto decode = [&](int w, int &mt, int &nt, int &sp, int &kb0, int &kb1) {
+    if constexpr (PAIR) {  // this CTA's M tile of pair tile w / n_tiles_n
+      const int mp = tc::fdiv(w, f_nt);
+      nt = w - mp * n_tiles_n;
+      mt = 2 * mp + rank2;
+      sp = 0;
+      kb0 = 0;
+      kb1 = KB;
+      return;
+    }
     const int tile = tc::fdiv(w, f_sp);
     sp = w - tile * P.splits;
     mt = tc::fdiv(tile, f_nt);
@@ -147,16 +167,21 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], RS ? kEpiWarps / 2 : kEpiWarps);
+      // PAIR: the leader's MMA waits for both CTAs' epilogue warps
+      tc::mbar_init(&tempty[a], (PAIR ? 2 : 1) * (RS ? kEpiWarps / 2 : kEpiWarps));
     }
     for (int a = 0; a < kEpiWarps; ++a) tc::mbar_init(&abar[a], 1);
     tc::fence_mbar_init();
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
   }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) {
+    if constexpr (PAIR) tc::tmem_alloc2(tmem_slot, 2 * BN);
+    else tc::tmem_alloc(tmem_slot, 2 * BN);
+  }
   tc::tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) tc::cluster_sync();  // the peer's barriers exist before any remote arrival
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -164,7 +189,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      for (int w = w_first; w < n_work; w += w_step) {
         int mt, nt, sp, kb0, kb1;
         decode(w, mt, nt, sp, kb0, kb1);
         const int m0 = mt * BM;
@@ -173,19 +198,27 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const int t = kb / P.CB, cb = kb % P.CB;
           tc::mbar_wait_idle(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * STAGE_BYTES;
-          tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tc::tma_load_5d(sa, &tmA, &full[stage], 0, P.dw[t], P.s_in * i0 + P.dh[t], b0, cb);
-          tc::tma_load_3d(sa + KG * A_BYTES, &tmB, &full[stage], 0, nt * BN, P.wk[t] * P.CB + cb);
+          if constexpr (PAIR) {  // both CTAs' bytes credited to the leader's full barrier
+            const uint32_t lb = tc::leader_bar(&full[stage]);
+            if (rank2 == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+            tc::tma_load_5d_pair(sa, &tmA, lb, 0, P.dw[t], P.s_in * i0 + P.dh[t], b0, cb);
+            tc::tma_load_3d_pair(sa + KG * A_BYTES, &tmB, lb, 0, nt * BN + rank2 * (BN / 2), P.wk[t] * P.CB + cb);
+          } else {
+            tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            tc::tma_load_5d(sa, &tmA, &full[stage], 0, P.dw[t], P.s_in * i0 + P.dh[t], b0, cb);
+            tc::tma_load_3d(sa + KG * A_BYTES, &tmB, &full[stage], 0, nt * BN, P.wk[t] * P.CB + cb);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {  // ---------------- MMA issuer: warp-uniform loop, elected lane issues
-    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
+    constexpr uint32_t idesc = tc::idesc_bf16(PAIR ? 2 * BM : BM, BN, 0, 0);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+    const int w_end = (PAIR && rank2 != 0) ? 0 : n_work;  // a pair's MMAs are the leader's
+    for (int w = w_first; w < w_end; w += w_step, ++it) {
       int mt, nt, sp, kb0, kb1;
       decode(w, mt, nt, sp, kb0, kb1);
       const int acc = it & 1;
@@ -202,15 +235,23 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const uint64_t ad = tc::sw128_desc(sa + g * A_BYTES, 16, 1024);
             const uint64_t bd = tc::sw128_desc(sa + KG * A_BYTES + g * B_BYTES, 16, 1024);
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)  // advance 32 B (16 bf16) along K inside the swizzle row
-              tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || g > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {  // advance 32 B (16 bf16) along K inside the swizzle row
+              if constexpr (PAIR)
+                tc::umma_bf16_pair(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || g > 0 || k > 0) ? 1u : 0u);
+              else
+                tc::umma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || g > 0 || k > 0) ? 1u : 0u);
+            }
           }
-          tc::umma_commit(&empty[stage]);
+          if constexpr (PAIR) tc::umma_commit_pair(&empty[stage]);
+          else tc::umma_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (tc::elect_one()) tc::umma_commit(&tfull[acc]);
+      if (tc::elect_one()) {
+        if constexpr (PAIR) tc::umma_commit_pair(&tfull[acc]);
+        else tc::umma_commit(&tfull[acc]);
+      }
       __syncwarp();
     }
   } else {  // ---------------- epilogue warps 2..5
@@ -258,7 +299,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     int nrows = 0;  // valid rows of this warp's tiles so far (warp-uniform)
     uint32_t aph = 0;  // phase of this warp's addend barrier
     int it = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+    for (int w = w_first; w < n_work; w += w_step, ++it) {
       int mt, nt, sp, kb0, kb1;
       decode(w, mt, nt, sp, kb0, kb1);
       const int acc = it & 1;
@@ -324,9 +365,15 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) tc::mbar_arrive_remote(&tempty[acc], 0);  // the leader's MMA reuses both
+        else tc::mbar_arrive(&tempty[acc]);
+      }
     }
     if (lane == 0) tc::bulk_wait_all();
+    // the CTA's statistics row: blockIdx.x (its N tile is blockIdx.x % n_tiles_n), or for a
+    // pair rank * (pairs) + pair (its N tile is pair % n_tiles_n: pairs % n_tiles_n == 0)
+    const int srow = PAIR ? rank2 * w_step + w_first : (int)blockIdx.x;
     if (P.stats) {  // this CTA's partial row: the slots merged (Chan) in a fixed order
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
@@ -346,12 +393,12 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       if (RS)
         tc::cta_stats_row<8>(sstat, scnt, BN, (warp - 2) * 32 + lane, kEpiWarps * 32,
-                             P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2,
-                             P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
+                             P.stats + ((size_t)srow * P.N + (size_t)(srow % n_tiles_n) * BN) * 2,
+                             P.stats + (size_t)gridDim.x * P.N * 2 + srow);
       else
         tc::cta_stats_row<4>(sstat, scnt, BN, (warp - 2) * 32 + lane, kEpiWarps * 32,
-                             P.stats + ((size_t)blockIdx.x * P.N + (size_t)(blockIdx.x % n_tiles_n) * BN) * 2,
-                             P.stats + (size_t)gridDim.x * P.N * 2 + blockIdx.x);
+                             P.stats + ((size_t)srow * P.N + (size_t)(srow % n_tiles_n) * BN) * 2,
+                             P.stats + (size_t)gridDim.x * P.N * 2 + srow);
     }
     }  // P.cs == 1
   }
@@ -386,9 +433,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
   }
   if (P.cs > 1) __syncthreads();
+  if constexpr (PAIR) tc::cluster_sync();  // the leader's last MMAs / the peer's arrivals are done
   if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem_base, 2 * BN);
+    if constexpr (PAIR) tc::tmem_dealloc2(tmem_base, 2 * BN);
+    else tc::tmem_dealloc(tmem_base, 2 * BN);
   }
   if (P.cs > 1) {
     tc::cluster_sync();  // every push has landed
@@ -976,13 +1025,14 @@ int pick_bn(int N) { return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64); }
 // of SMs; below that, BN = 64 and a split of K (deterministic workspace reduction).
 struct ConvPlan {
   int BN, splits, kb_per_split, cs;
+  bool pair;  // CTA pairs (cta_group::2, M = 256 tiles)
 };
 // Operand cycles of one CTA streaming `kb` k-blocks of a 128 x bn tile: the SM's TMA fill
 // rate (~40 B/clk measured on the conv kernels: 24-48 KB per k-block in 600-1200 cycles,
 // DESIGN.md 7) bounds these small-tile layers, not the MMAs.
 static double operand_cycles(int kb, int bn) { return kb * (double)(A_BYTES + bn * BK * 2) / 40.0; }
 ConvPlan conv_plan(int M, int N, int KB) {
-  ConvPlan p{64, 1, KB, 1};
+  ConvPlan p{64, 1, KB, 1, false};
   const int mt = M / BM;
   // widest N tile that still leaves `want_tiles` tiles (wider tiles reuse each A tile
   // over more columns: fewer operand bytes from L2 per MMA)
@@ -1010,6 +1060,11 @@ ConvPlan conv_plan(int M, int N, int KB) {
   // stream concurrency), mixed alone (DESIGN.md 7 "Cluster split-K")
   static const int cs_on = env_int("PETRA_CONV_CS", 0);
   static const int cs_ctas = std::min(kNumSMs, env_int("PETRA_CONV_CS_CTAS", 128));
+  // CTA pairs for the N >= 128 tiles: an SM then streams A + B / 2 per k-block.  Off by
+  // default: exact, but no layer ran faster alone and the 1x1 K = 64 layers 1.6x slower
+  // (profiles/r02/tuning/cta_pairs.txt, DESIGN.md 7 "CTA pairs")
+  static const int pair_on = env_int("PETRA_CONV_PAIR", 0);
+  if (pair_on && p.splits == 1 && p.BN >= 128) p.pair = true;
   if (cs_on && p.splits == 1) {
     const double t0 = (double)cdiv(tiles, conv_grid(tiles)) * operand_cycles(KB, p.BN);
     double best = 0.8 * t0;
@@ -1026,6 +1081,7 @@ ConvPlan conv_plan(int M, int N, int KB) {
           p.BN = bn;
           p.cs = p.splits = cs;
           p.kb_per_split = KB / cs;
+          p.pair = false;
         }
       }
     }
@@ -1069,9 +1125,14 @@ constexpr size_t conv_stat_bytes(int BN, bool OUT16) {
   return (size_t)(BN * (OUT16 ? 2 : 4) <= 128 ? 8 : 4) * BN * 8 + 32;
 }
 // ring depth: about 144 / 128 KB of operands in flight
-constexpr int conv_stages(int BN, int KG = 1) { return (BN == 256 ? 3 : (BN == 128 ? 4 : 6)) / KG; }
-constexpr size_t conv_smem(int BN, int KG, size_t stat_bytes) {
-  return 1024 + (size_t)conv_stages(BN, KG) * KG * (A_BYTES + BN * BK * 2) + 1024 + kEpiBytes + stat_bytes;
+constexpr int conv_stages(int BN, int KG = 1, bool pair = false) {
+  // a pair's stage holds KG x (A + B / 2): 4 x 32 KB (BN = 256) / 6 x 24 KB (BN = 128), KG = 2: 2 x 64 KB /
+  // 3 x 48 KB
+  return pair ? (BN == 256 ? 4 : 6) / KG : (BN == 256 ? 3 : (BN == 128 ? 4 : 6)) / KG;
+}
+constexpr size_t conv_smem(int BN, int KG, size_t stat_bytes, bool pair = false) {
+  return 1024 + (size_t)conv_stages(BN, KG, pair) * KG * (A_BYTES + (pair ? BN / 2 : BN) * BK * 2) + 1024 +
+         kEpiBytes + stat_bytes;
 }
 // channel blocks per stage: 2 where the N tile is narrow (the copies, not the MMAs, bound
 // those tiles) and the reduction has an even number of 64-channel blocks per tap
@@ -1090,7 +1151,14 @@ int conv_stats_grid(int work, int n_tiles_n) {
   return std::max(n_tiles_n, g / n_tiles_n * n_tiles_n);
 }
 
-template <int BN, bool OUT16, int KG>
+// CTAs of a pair-tile grid: pairs a multiple of the N-tile count (every CTA keeps one N
+// tile: its statistics row), under the common cap
+int conv_pair_grid(int pair_work, int n_tiles_n) {
+  const int pairs = std::max(1, std::min(pair_work, conv_grid(pair_work * 2) / 2));
+  return 2 * std::max(n_tiles_n, pairs / n_tiles_n * n_tiles_n);
+}
+
+template <int BN, bool OUT16, int KG, bool PAIR = false>
 void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParams &P0, cudaStream_t st) {
   ConvTCParams P = P0;
   P.f_sp = tc::fastdiv_make(P.splits);
@@ -1099,9 +1167,18 @@ void launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvTCParam
   P.f_wb = tc::fastdiv_make(P.Wb);
   static const int rs_on = env_int("PETRA_EPI_RS", 1);
   P.rs = rs_on;
-  constexpr int STAGES = conv_stages(BN, KG);
-  const size_t smem = conv_smem(BN, KG, P.stats ? conv_stat_bytes(BN, OUT16) : 0);  // attribute: conv_tc_prepare
+  constexpr int STAGES = conv_stages(BN, KG, PAIR);
+  const size_t smem = conv_smem(BN, KG, P.stats ? conv_stat_bytes(BN, OUT16) : 0, PAIR);  // attribute: conv_tc_prepare
   const int work = (P.M / BM) * (P.N / BN) * P.splits;
+  if constexpr (PAIR) {
+    const CUtensorMap to = out_map(P.out, OUT16, P);
+    const CUtensorMap tad = (!OUT16 && P.addend) ? out_map(const_cast<float *>(P.addend), false, P) : to;
+    const int grid = conv_pair_grid(((P.M / BM + 1) / 2) * (P.N / BN), P.N / BN);
+    launch_k_cluster(conv_tc_kernel<BN, STAGES, OUT16, KG, true>, dim3(grid), dim3(kConvThreads), smem, st, 2, ta, tb,
+                     to, to, tad, P);
+    PETRA_LAUNCH_CHECK();
+    return;
+  }
   const CUtensorMap to = out_map(P.out, OUT16, P);
   // the addend in the output's geometry (fp32 outputs only)
   const CUtensorMap tad = (!OUT16 && P.addend) ? out_map(const_cast<float *>(P.addend), false, P) : to;
@@ -1134,7 +1211,8 @@ LaunchPlan launch_plan(const ConvTCParams &P, float *ws) {
     L.pl.splits = 1;
     L.pl.kb_per_split = P.ntaps * P.CB;
   }
-  L.kg = conv_kg(L.pl.BN, P.CB, L.pl.splits);
+  static const int pair_kg = env_int("PETRA_CONV_PAIR_KG", 2);
+  L.kg = L.pl.pair ? ((pair_kg == 2 && P.CB % 2 == 0) ? 2 : 1) : conv_kg(L.pl.BN, P.CB, L.pl.splits);
   return L;
 }
 
@@ -1149,7 +1227,27 @@ void launch_any(const CUtensorMap &ta, const LaunchPlan &L, const __nv_bfloat16 
   P.ws = ws;
   if (P.splits > 1 && P.cs == 1) P.stats = nullptr;  // stats need final z (split-K: standalone pass)
   if (out16 && P.addend) throw PetraError(PETRA_E_ARG, "conv_tc: addend needs an fp32 output");
-  CUtensorMap tb = mat_map3(w, wrows, wK, pl.BN, L.kg);
+  CUtensorMap tb = mat_map3(w, wrows, wK, pl.pair ? pl.BN / 2 : pl.BN, L.kg);  // a pair CTA loads BN / 2 rows
+  if (pl.pair) {
+    if (L.kg == 2) {
+      if (out16) {
+        if (pl.BN == 256) launch_conv<256, true, 2, true>(ta, tb, P, st);
+        else launch_conv<128, true, 2, true>(ta, tb, P, st);
+      } else {
+        if (pl.BN == 256) launch_conv<256, false, 2, true>(ta, tb, P, st);
+        else launch_conv<128, false, 2, true>(ta, tb, P, st);
+      }
+      return;
+    }
+    if (out16) {
+      if (pl.BN == 256) launch_conv<256, true, 1, true>(ta, tb, P, st);
+      else launch_conv<128, true, 1, true>(ta, tb, P, st);
+    } else {
+      if (pl.BN == 256) launch_conv<256, false, 1, true>(ta, tb, P, st);
+      else launch_conv<128, false, 1, true>(ta, tb, P, st);
+    }
+    return;
+  }
   if (L.kg == 2) {
     if (out16) {
       if (pl.BN == 128) launch_conv<128, true, 2>(ta, tb, P, st);
@@ -1214,7 +1312,9 @@ StatsRows run_fwd(const ConvGeom &g, const __nv_bfloat16 *x, bool x_pad, const _
   StatsRows r;
   r.groups = P.N / BN;
   const int work = (P.M / BM) * (P.N / BN) * P.splits;
-  r.rows = L.pl.cs > 1 ? work : conv_stats_grid(work, r.groups);  // one partial row per CTA
+  r.rows = L.pl.cs > 1 ? work
+           : L.pl.pair ? conv_pair_grid(((P.M / BM + 1) / 2) * r.groups, r.groups)
+                       : conv_stats_grid(work, r.groups);  // one partial row per CTA
   return r;
 }
 
@@ -1336,6 +1436,19 @@ void conv_tc_prepare() {
     set((const void *)conv_tc_kernel<64, conv_stages(64, 2), false, 2>, 64, 2);
     set((const void *)conv_tc_kernel<128, conv_stages(128, 2), true, 2>, 128, 2);
     set((const void *)conv_tc_kernel<64, conv_stages(64, 2), true, 2>, 64, 2);
+    auto set2 = [](const void *f, int BN, int KG) {
+      PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)conv_smem(BN, KG, std::max(conv_stat_bytes(BN, true),
+                                                                      conv_stat_bytes(BN, false)), true)));
+    };
+    set2((const void *)conv_tc_kernel<256, conv_stages(256, 1, true), false, 1, true>, 256, 1);
+    set2((const void *)conv_tc_kernel<128, conv_stages(128, 1, true), false, 1, true>, 128, 1);
+    set2((const void *)conv_tc_kernel<256, conv_stages(256, 1, true), true, 1, true>, 256, 1);
+    set2((const void *)conv_tc_kernel<128, conv_stages(128, 1, true), true, 1, true>, 128, 1);
+    set2((const void *)conv_tc_kernel<256, conv_stages(256, 2, true), false, 2, true>, 256, 2);
+    set2((const void *)conv_tc_kernel<128, conv_stages(128, 2, true), false, 2, true>, 128, 2);
+    set2((const void *)conv_tc_kernel<256, conv_stages(256, 2, true), true, 2, true>, 256, 2);
+    set2((const void *)conv_tc_kernel<128, conv_stages(128, 2, true), true, 2, true>, 128, 2);
     auto setw = [](const void *f, int STAGES, int BN) {
       size_t smem = (size_t)STAGES * (2 * 64 * 64 * 2 + BN * 64 * 2) + 1024 + 256;
       PETRA_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1375,7 +1488,7 @@ void conv_tc_plan_info(const ConvGeom &g, int mode, int *out) {
   const ConvPlan p = conv_plan((int)tiling(g.B, g.Ho, g.Wo, BM).M(), N, KB);
   out[0] = p.BN;
   out[1] = p.splits;
-  out[2] = p.cs;
+  out[2] = p.pair ? -2 : p.cs;
 }
 
 StatsRows conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, const __nv_bfloat16 *w, void *z,

@@ -141,11 +141,15 @@ def test_tc_padded_operands_vs_simt(geom, mode):
 
 
 @pytest.mark.parametrize("geom,mode", [(g, m) for g in CS_GEOMS for m in (0, 1) if not (g[3] == 2048 and m == 1)])
-@pytest.mark.skipif(os.environ.get("PETRA_CONV_CS", "0") != "1", reason="cluster split-K off (PETRA_CONV_CS)")
-def test_cluster_split_plan(geom, mode):
-    """With PETRA_CONV_CS=1 the few-tile layers take the cluster split-K plan (so the parity
-    tests above cover it: tests/test_cluster_split_gpu.py reruns them in that mode)."""
+@pytest.mark.skipif(os.environ.get("PETRA_CONV_CS", "0") != "1" and os.environ.get("PETRA_CONV_PAIR", "0") != "1",
+                    reason="default plans (tests/test_conv_modes_gpu.py sets the modes)")
+def test_conv_mode_plan(geom, mode):
+    """Under PETRA_CONV_CS=1 the few-tile layers take the cluster split-K plan; under
+    PETRA_CONV_PAIR=1 every N >= 128 tile runs on CTA pairs (plan[2] == -2)."""
     plan = (C.c_int32 * 3)()
     L.call("petra_conv_plan", C.byref(L.PetraConvGeom(*geom)), mode, plan)
     BN, splits, cs = plan
-    assert cs in (2, 4) and splits == cs, tuple(plan)
+    if os.environ.get("PETRA_CONV_CS", "0") == "1":
+        assert cs in (2, 4) and splits == cs, tuple(plan)
+    else:
+        assert (cs == -2) == (BN >= 128) and splits == 1, tuple(plan)
