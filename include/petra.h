@@ -421,8 +421,10 @@ petra_status petra_conv_run(int32_t mode, int32_t engine, const petra_conv_geom 
                             const float *b, const float *addend, float *out);
 /* Kernel benchmark: one convolution pass (as petra_conv_run, on seeded random device
  * inputs) repeated `iters` times after one warm-up; *avg_ms = mean device time per pass
- * (CUDA events).  flags bit 0: forward output z in bf16 (the tensor-core stage layout);
- * bit 1: forward with the BN statistics fused into the epilogue (as a stage runs it). */
+ * (CUDA events around one CUDA-graph replay of the `iters` passes, so host-side launch
+ * and tensor-map encoding time is excluded).  flags bit 0: forward output z in bf16 (the
+ * tensor-core stage layout); bit 1: forward with the BN statistics fused into the
+ * epilogue (as a stage runs it); bit 2: time direct launches instead of the graph. */
 petra_status petra_conv_bench(int32_t mode, int32_t engine, const petra_conv_geom *g, int32_t flags,
                               int32_t iters, float *avg_ms);
 /* Kernel-level test hook of the fused BN statistics: one tensor-core

@@ -39,6 +39,8 @@ def _nccl_include():
 
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
                 "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include()]
+# compile-time experiment switches (e.g. -DPETRA_EPI_NBUF=1); use with --force
+FLAGS += os.environ.get("PETRA_NVCC_FLAGS", "").split()
 
 
 def sources():

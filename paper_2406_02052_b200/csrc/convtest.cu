@@ -15,7 +15,8 @@ namespace {
 // `iters` further passes (CUDA events; operands prepared once, outside the timing)
 petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a, const float *b,
                  const float *addend, float *out, int iters = 0, float *ms = nullptr, bool out16 = false,
-                 bool stats = false, float *mean_out = nullptr, float *var_out = nullptr) {
+                 bool stats = false, float *mean_out = nullptr, float *var_out = nullptr,
+                 bool direct_launches = false) {
   using namespace petra;
   ConvGeom g = make_geom(pg->batch, pg->h, pg->w, pg->cin, pg->cout, pg->ksize, pg->stride);
   int64_t nx = g.Min() * g.Ci, nz = g.M() * g.Co, nw = (int64_t)g.Co * g.K();
@@ -32,7 +33,15 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     dadd = dalloc(no * 4);
     PETRA_CUDA(cudaMemcpy(dadd->p, addend, no * 4, cudaMemcpyHostToDevice));
   }
+  PETRA_CUDA(cudaDeviceSynchronize());  // pageable copies land before the non-blocking stream reads them
+  // a capturable stream: the timed loop replays as one CUDA graph (no host encode / launch
+  // time between the passes -- device time of back-to-back passes)
   cudaStream_t st = nullptr;
+  PETRA_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } st_guard{st};
   DevPtr ab, bb, ws, part = dalloc((size_t)kNumSMs * 4 * (g.Co * 2 + 1) * sizeof(float));
   StatsRows rows;
   float *stats_part = stats ? part->as<float>() : nullptr;
@@ -71,8 +80,8 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     const int64_t nb_buf = b_pad ? (int64_t)g.B * (g.H + 2) * (g.W + 2) * g.Ci : nb;
     ab = dalloc(na_buf * 2);
     bb = dalloc(nb_buf * 2);
-    PETRA_CUDA(cudaMemset(ab->p, 0, na_buf * 2));
-    PETRA_CUDA(cudaMemset(bb->p, 0, nb_buf * 2));
+    PETRA_CUDA(cudaMemsetAsync(ab->p, 0, na_buf * 2, st));  // on st: it does not order with the legacy stream
+    PETRA_CUDA(cudaMemsetAsync(bb->p, 0, nb_buf * 2, st));
     if (a_pad) f32_to_bf16_padded(da->as<float>(), ab->as<__nv_bfloat16>(), g.B, aH, aW, aC, st);
     else f32_to_bf16(da->as<float>(), ab->as<__nv_bfloat16>(), na, st);
     if (mode == 1) {  // flipped / transposed weights wT[ci][kh'][kw'][co] = w[co][k-1-kh'][k-1-kw'][ci]
@@ -85,6 +94,7 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
               wt[(((int64_t)ci * k + (k - 1 - kh)) * k + (k - 1 - kw)) * g.Co + co] =
                   b[(((int64_t)co * k + kh) * k + kw) * g.Ci + ci];
       PETRA_CUDA(cudaMemcpy(db->p, wt.data(), nb * 4, cudaMemcpyHostToDevice));
+      PETRA_CUDA(cudaDeviceSynchronize());
     }
     if (b_pad) f32_to_bf16_padded(db->as<float>(), bb->as<__nv_bfloat16>(), g.B, g.H, g.W, g.Ci, st);
     else f32_to_bf16(db->as<float>(), bb->as<__nv_bfloat16>(), nb, st);
@@ -107,8 +117,21 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     cudaEvent_t e0, e1;
     PETRA_CUDA(cudaEventCreate(&e0));
     PETRA_CUDA(cudaEventCreate(&e1));
+    cudaGraphExec_t gx = nullptr;
+    if (!direct_launches) {
+      cudaGraph_t gr;
+      PETRA_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      for (int i = 0; i < iters; ++i) launch();
+      PETRA_CUDA(cudaStreamEndCapture(st, &gr));
+      PETRA_CUDA(cudaGraphInstantiate(&gx, gr, 0));
+      cudaGraphDestroy(gr);
+      PETRA_CUDA(cudaGraphLaunch(gx, st));  // warm replay
+      PETRA_CUDA(cudaStreamSynchronize(st));
+    }
     PETRA_CUDA(cudaEventRecord(e0, st));
-    for (int i = 0; i < iters; ++i) launch();
+    if (gx) PETRA_CUDA(cudaGraphLaunch(gx, st));
+    else
+      for (int i = 0; i < iters; ++i) launch();
     PETRA_CUDA(cudaEventRecord(e1, st));
     PETRA_CUDA(cudaEventSynchronize(e1));
     float t = 0.f;
@@ -116,13 +139,16 @@ petra_status run(int mode, int engine, const petra_conv_geom *pg, const float *a
     *ms = t / iters;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (gx) cudaGraphExecDestroy(gx);
   }
+  PETRA_CUDA(cudaStreamSynchronize(st));
   if (mean_out && var_out) {  // the library's BN batch statistics of z as stored (eps = 0: invstd^-2 = var)
     if (rows.rows == 0) throw PetraError(PETRA_E_UNSUPPORTED, "no fused statistics for this geometry");
     DevPtr dm = dalloc(g.Co * 4), di = dalloc(g.Co * 4);
     bn_stats_from_partials(part->as<float>(), rows, g.Co, g.M(), 0.f, dm->as<float>(), di->as<float>(), nullptr,
                            nullptr, 0.1f, st);
     std::vector<float> inv(g.Co);
+    PETRA_CUDA(cudaStreamSynchronize(st));
     PETRA_CUDA(cudaMemcpy(mean_out, dm->p, g.Co * 4, cudaMemcpyDeviceToHost));
     PETRA_CUDA(cudaMemcpy(inv.data(), di->p, g.Co * 4, cudaMemcpyDeviceToHost));
     for (int c = 0; c < g.Co; ++c) var_out[c] = 1.f / (inv[c] * inv[c]);
@@ -183,7 +209,7 @@ extern "C" petra_status petra_conv_bench(int32_t mode, int32_t engine, const pet
     for (auto &v : a) v = rnd();
     for (auto &v : b) v = rnd() * 0.05f;
     return run(mode, engine, g, a.data(), b.data(), nullptr, nullptr, iters, avg_ms, (flags & 1) != 0,
-               (flags & 2) != 0);
+               (flags & 2) != 0, nullptr, nullptr, (flags & 4) != 0);
   } catch (const petra::PetraError &e) {
     return e.status;
   } catch (...) {

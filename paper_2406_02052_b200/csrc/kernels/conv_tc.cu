@@ -68,7 +68,13 @@ struct ConvTCParams {
 // fences, and lane 0 issues the TMA store while the warp fills the other buffer.
 // Out-of-bounds box elements (padding rows of the padded grid) are not written.
 constexpr uint32_t kEpiBuf = 32 * 128;
-constexpr uint32_t kEpiBytes = kEpiWarps * 2 * kEpiBuf;
+// staging buffers per epilogue warp (PETRA_EPI_NBUF=1: one, and its 32 KB go to the operand
+// ring -- a deeper ring for the latency-bound small-tile convs)
+#ifndef PETRA_EPI_NBUF
+#define PETRA_EPI_NBUF 2
+#endif
+constexpr int kEpiNBuf = PETRA_EPI_NBUF;
+constexpr uint32_t kEpiBytes = kEpiWarps * kEpiNBuf * kEpiBuf;
 
 // row `lane` of a 32 x 128 B swizzled box: 32 fp32 or 64 bf16 values
 template <bool BF16>
@@ -260,7 +266,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int row = q * 32 + lane;
     const int slot = RS ? warp - 2 : q;
     float *my_stat = sstat + (size_t)slot * BN * 2;  // this CTA's N tile (fixed: grid % n_tiles_n == 0)
-    uint8_t *ebuf = sepi + (warp - 2) * 2 * kEpiBuf;
+    uint8_t *ebuf = sepi + (warp - 2) * kEpiNBuf * kEpiBuf;
     int eb = 0;  // staging buffer to fill next
     if (lane == 0) {
       tc::tma_prefetch(&tmO);
@@ -275,11 +281,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         else tc::tma_store_2d(map, ebuf + eb * kEpiBuf, c0, c1);
         tc::bulk_commit();
       }
-      eb ^= 1;
+      eb = (eb + 1) % kEpiNBuf;
     };
     // before overwriting buffer eb: its previous store (two chunks ago) has read smem
     auto acquire = [&]() {
-      if (lane == 0) tc::bulk_wait_read<1>();
+      if (lane == 0) tc::bulk_wait_read<kEpiNBuf - 1>();
       __syncwarp();
     };
     if (P.cs > 1) {
@@ -449,7 +455,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int ng = 4 / P.cs;                // 32-row groups of this rank
       constexpr int CW = OUT16 ? 64 : 32;    // columns per 128-byte staged row
       constexpr int NCHK = BN / CW;
-      uint8_t *ebuf = sepi + e * 2 * kEpiBuf;
+      uint8_t *ebuf = sepi + e * kEpiNBuf * kEpiBuf;
       int eb = 0;
       uint32_t aph = 0;
       const uint32_t tile = tc::smem_u32(smem);
@@ -490,7 +496,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           v[4 * c4 + 3] = sum.w;
         }
         if (!OUT16 && P.addend) {  // the addend box (the store box's geometry) by TMA
-          if (lane == 0) tc::bulk_wait_read<1>();
+          if (lane == 0) tc::bulk_wait_read<kEpiNBuf - 1>();
           __syncwarp();
           if (lane == 0) {
             tc::mbar_arrive_expect_tx(&abar[e], kEpiBuf);
@@ -513,7 +519,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int jj = 0; jj < CW; ++jj) v[jj] = 0.f;
         }
-        if (lane == 0) tc::bulk_wait_read<1>();
+        if (lane == 0) tc::bulk_wait_read<kEpiNBuf - 1>();
         __syncwarp();
         uint8_t *staged = ebuf + eb * kEpiBuf;
         stage_row<OUT16>(staged, lane, v);
@@ -523,7 +529,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           tc::tma_store_4d(&tmO, staged, nt * BN + k * CW, wj, wi, wb);
           tc::bulk_commit();
         }
-        eb ^= 1;
+        eb = (eb + 1) % kEpiNBuf;
         if (P.stats) {  // this unit's 32 rows x CW columns into the statistics slot of group g
           tc::ColStats cst;
           tc::colstats_zero(cst);
@@ -563,12 +569,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 // triples written as sums: M2 = W + B - A^2 / n); the 8 warp results are added in warp
 // order (deterministic).  Biased variance for the normalisation, unbiased for the
 // running-stat EMA (reading c9).
-__global__ void __launch_bounds__(256) stats_finalize_kernel(const float *__restrict__ part, int P, int groups, int N,
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) stats_finalize_kernel(const float *__restrict__ part, int P, int groups, int N,
                                                              int64_t M, float eps, float *__restrict__ mean,
                                                              float *__restrict__ invstd, float *__restrict__ rmean,
                                                              float *__restrict__ rvar, float mom) {
   pdl_wait_trigger();
-  __shared__ double sh[4][8][33];
+  __shared__ double sh[4][NW][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   const float *cnt = part + (size_t)P * N * 2;
@@ -580,12 +587,12 @@ __global__ void __launch_bounds__(256) stats_finalize_kernel(const float *__rest
     int j = w;
     // four rows' loads in flight before their (in-order) accumulation: the merge is
     // L2-latency bound
-    for (; j + 24 < nr; j += 32) {
+    for (; j + 3 * NW < nr; j += 4 * NW) {
       float2 u[4];
       float cn[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int r = grp + (j + 8 * k) * groups;
+        const int r = grp + (j + NW * k) * groups;
         u[k] = *reinterpret_cast<const float2 *>(part + ((size_t)r * N + c) * 2);
         cn[k] = cnt[r];
       }
@@ -598,7 +605,7 @@ __global__ void __launch_bounds__(256) stats_finalize_kernel(const float *__rest
         n += nr_;
       }
     }
-    for (; j < nr; j += 8) {
+    for (; j < nr; j += NW) {
       const int r = grp + j * groups;
       const float2 u = *reinterpret_cast<const float2 *>(part + ((size_t)r * N + c) * 2);
       const double nr_ = cnt[r], d = (double)u.x - m0;
@@ -615,7 +622,7 @@ __global__ void __launch_bounds__(256) stats_finalize_kernel(const float *__rest
   __syncthreads();
   if (w == 0 && c < N) {
     A = Bq = Wm = n = 0;
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < NW; ++k) {
       A += sh[0][k][lane];
       Bq += sh[1][k][lane];
       Wm += sh[2][k][lane];
@@ -1060,6 +1067,7 @@ ConvPlan conv_plan(int M, int N, int KB) {
   // stream concurrency), mixed alone (DESIGN.md 7 "Cluster split-K")
   static const int cs_on = env_int("PETRA_CONV_CS", 0);
   static const int cs_ctas = std::min(kNumSMs, env_int("PETRA_CONV_CS_CTAS", 128));
+  static const int cs_bn = env_int("PETRA_CONV_CS_BN", 256);  // widest N tile split over a cluster
   // CTA pairs for the N >= 128 tiles: an SM then streams A + B / 2 per k-block.  Off by
   // default: exact, but no layer ran faster alone and the 1x1 K = 64 layers 1.6x slower
   // (profiles/r02/tuning/cta_pairs.txt, DESIGN.md 7 "CTA pairs")
@@ -1072,7 +1080,7 @@ ConvPlan conv_plan(int M, int N, int KB) {
       if (N % bn) continue;
       const int t = mt * (N / bn);
       for (int cs : {4, 2}) {
-        if (KB % cs || KB / cs < 4 || t * cs > cs_ctas) continue;
+        if (KB % cs || KB / cs < 4 || t * cs > cs_ctas || bn > cs_bn) continue;
         // reduction: (cs-1)/cs of the fp32 tile pushed to the peers at ~20 B/clk (DSMEM,
         // B300_MICROARCH.md)
         const double e = operand_cycles(KB / cs, bn) + (double)(cs - 1) * BM * bn * 4 / cs / 20.0;
@@ -1128,7 +1136,8 @@ constexpr size_t conv_stat_bytes(int BN, bool OUT16) {
 constexpr int conv_stages(int BN, int KG = 1, bool pair = false) {
   // a pair's stage holds KG x (A + B / 2): 4 x 32 KB (BN = 256) / 6 x 24 KB (BN = 128), KG = 2: 2 x 64 KB /
   // 3 x 48 KB
-  return pair ? (BN == 256 ? 4 : 6) / KG : (BN == 256 ? 3 : (BN == 128 ? 4 : 6)) / KG;
+  return pair ? (BN == 256 ? 4 : 6) / KG
+              : (kEpiNBuf == 1 ? (BN == 256 ? 3 : (BN == 128 ? 5 : 7)) : (BN == 256 ? 3 : (BN == 128 ? 4 : 6))) / KG;
 }
 constexpr size_t conv_smem(int BN, int KG, size_t stat_bytes, bool pair = false) {
   return 1024 + (size_t)conv_stages(BN, KG, pair) * KG * (A_BYTES + (pair ? BN / 2 : BN) * BK * 2) + 1024 +
@@ -1498,8 +1507,15 @@ StatsRows conv_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *x, bool x_padded, 
 
 void bn_stats_from_partials(const float *part, StatsRows rows, int N, int64_t M, float eps, float *mean,
                             float *invstd, float *rmean, float *rvar, float mom, cudaStream_t st) {
-  launch_k(stats_finalize_kernel, (unsigned)cdiv(N, 32), 256, 0, st, part, rows.rows, rows.groups, N, M, eps, mean,
-           invstd, rmean, rvar, mom);
+  // warps per 32 channels: each warp merges rows w, w + NW, ... (four loads in flight), so the
+  // L2 round trips per launch are ~rows / (4 NW)
+  static const int nw = env_int("PETRA_FINALIZE_WARPS", 8);
+  if (nw >= 32)
+    launch_k(stats_finalize_kernel<32>, (unsigned)cdiv(N, 32), 1024, 0, st, part, rows.rows, rows.groups, N, M, eps,
+             mean, invstd, rmean, rvar, mom);
+  else
+    launch_k(stats_finalize_kernel<8>, (unsigned)cdiv(N, 32), 256, 0, st, part, rows.rows, rows.groups, N, M, eps,
+             mean, invstd, rmean, rvar, mom);
   PETRA_LAUNCH_CHECK();
 }
 

@@ -43,14 +43,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 // suspend-time hint lets the hardware park the thread until the phase completes
 // instead of re-issuing try_wait (the polling loop otherwise takes issue slots from the
 // epilogue warps sharing its SM sub-partition)
+#ifndef PETRA_WAIT_HINT
+#define PETRA_WAIT_HINT 0x100000u
+#endif
 __device__ __forceinline__ void mbar_wait_idle(uint64_t *bar, uint32_t parity) {
+  if constexpr (PETRA_WAIT_HINT == 0u) {  // experiment switch: plain try_wait polling
+    mbar_wait(bar, parity);
+    return;
+  }
   uint32_t a = smem_u32(bar);
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(a),
-      "r"(parity), "r"(0x100000u)
+      "r"(parity), "r"(PETRA_WAIT_HINT)
       : "memory");
 }
 
