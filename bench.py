@@ -332,6 +332,7 @@ def measure(model, stages, batch, precision, steps, warmup, world, rank, local, 
     for _ in range(steps):
         tick()
     prof = L.profile_read()
+    recs = L.profile_records()
     L.profile(False)
     pipe.close()
     peaks, src = load_peaks()
@@ -361,9 +362,20 @@ def measure(model, stages, batch, precision, steps, warmup, world, rank, local, 
             traffic = round(tj["categories"][name]["bytes_per_launch"])
             traffic_src = (f"dram__bytes_read.sum + dram__bytes_write.sum per logical launch, ncu launch list "
                            f"({os.path.relpath(tfile, ROOT)}; {tj['cache']})")
+    # per-launch roofline of the dominant category: each logical launch's own bound,
+    # max(flops / tensor peak, bytes / HBM peak) (its 1x1 K = 64 convolutions are HBM-bound,
+    # the 3x3 ones tensor-bound), summed and divided by the measured time
+    mine = [r for r in recs if r["name"] == name]
+    t_roof = sum(max(r["flops"] / (peaks["bf16_tflops"] * 1e9), r["bytes"] / (peaks["hbm_gbs"] * 1e6)) for r in mine)
+    t_meas = sum(r["ms"] for r in mine)
+    n_hbm = sum(1 for r in mine if r["bytes"] / peaks["hbm_gbs"] * 1e3 > r["flops"] / peaks["bf16_tflops"])
     out["roofline"] = {
         "bound": bound, "kernel": name, "achieved": round(ach, 2), "peak": peak, "unit": unit,
         "frac": round(ach / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+        "frac_of_launch_rooflines": round(t_roof / t_meas, 4) if t_meas > 0 else None,
+        "launch_rooflines": (f"sum over the category's {len(mine)} launches of max(algorithmic flops / "
+                             f"{peaks['bf16_tflops']} TFLOP/s, algorithmic bytes / {peaks['hbm_gbs']} GB/s) = "
+                             f"{t_roof:.4f} ms over {t_meas:.4f} ms measured; {n_hbm} launches HBM-bound"),
         "algorithmic_bytes_per_launch": round(top["bytes"] / top["launches"]), "peak_source": peak_src,
         "share_of_step": round(top["ms"] / tot, 3), "launches_per_step": top["launches"] / steps,
         "method": ("profiled replay of K further steps with every stage and both directions serialised on "

@@ -456,6 +456,19 @@ petra_status petra_conv_plan(const petra_conv_geom *g, int32_t mode, int32_t *pl
 int64_t petra_launch_count(void);
 petra_status petra_profile(int32_t enable);
 petra_status petra_profile_read(petra_prof_entry *out, int32_t cap, int32_t *n);
+/* The same profile per logical kernel, in enqueue order: category index (the order of
+ * petra_profile_read's categories before it drops empty ones is the order of first use;
+ * `name` repeats it), event time, algorithmic flops and bytes of that one launch -- for a
+ * roofline per launch (each launch's own bound, max(flops / tensor peak, bytes / HBM peak)).
+ * Writes min(cap, records) entries, *n = the number of records.  Errors: PETRA_E_ARG (NULL),
+ * PETRA_E_CUDA. */
+typedef struct {
+  char name[32];
+  float ms;
+  double flops;
+  double bytes;
+} petra_prof_record;
+petra_status petra_profile_records(petra_prof_record *out, int32_t cap, int32_t *n);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -137,6 +137,7 @@ SIGS = {
     "petra_launch_count": (C.c_int64, []),
     "petra_profile": (C.c_int, [I32]),
     "petra_profile_read": (C.c_int, [C.POINTER(PetraProfEntry), I32, C.POINTER(I32)]),
+    "petra_profile_records": (C.c_int, [VP, I32, C.POINTER(I32)]),
 }
 
 
@@ -146,6 +147,21 @@ def launch_count() -> int:
 
 def profile(enable: bool):
     call("petra_profile", int(bool(enable)))
+
+
+class PetraProfRecord(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("ms", C.c_float), ("flops", C.c_double), ("bytes", C.c_double)]
+
+
+def profile_records():
+    """Per logical kernel of the profiled replay: name, event ms, algorithmic flops and bytes."""
+    n = C.c_int32()
+    one = (PetraProfRecord * 1)()
+    call("petra_profile_records", C.cast(one, C.c_void_p), 0, C.byref(n))
+    arr = (PetraProfRecord * max(1, n.value))()
+    call("petra_profile_records", C.cast(arr, C.c_void_p), n.value, C.byref(n))
+    return [dict(name=arr[i].name.decode(), ms=arr[i].ms, flops=arr[i].flops, bytes=arr[i].bytes)
+            for i in range(n.value)]
 
 
 def profile_read():

@@ -257,7 +257,11 @@ void Pipeline::tick(int64_t t, bool inject, const float *x0, const int32_t *labe
   for (int j = 1; j <= J_; ++j) {
     if (!sched_.local(j)) continue;
     Stage &s = *stages_[j];
-    st = Prof::enabled ? caller : streams_[j];  // profiled replay: one stream, kernels timed alone
+    // profiled replay: every local stage on ONE of the pipeline's (capturable, non-blocking)
+    // streams, so kernels run and are timed alone
+    int jl = 1;
+    while (!sched_.local(jl)) ++jl;
+    st = Prof::enabled ? streams_[jl] : streams_[j];
     PETRA_CUDA(cudaStreamWaitEvent(st, start_, 0));
     const Schedule::Step &sp = steps[j];
     TickArgs a;

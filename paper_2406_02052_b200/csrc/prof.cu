@@ -89,4 +89,21 @@ petra_status petra_profile_read(petra_prof_entry *out, int32_t cap, int32_t *n) 
   *n = k;
   return PETRA_OK;
 }
+
+petra_status petra_profile_records(petra_prof_record *out, int32_t cap, int32_t *n) {
+  if (!out || !n) return PETRA_E_ARG;
+  if (cudaDeviceSynchronize() != cudaSuccess) return PETRA_E_CUDA;
+  int k = 0;
+  for (auto &r : Prof::recs) {
+    if (k >= cap) break;
+    petra_prof_record &o = out[k++];
+    std::memset(&o, 0, sizeof(o));
+    std::strncpy(o.name, Prof::names[r.cat].c_str(), sizeof(o.name) - 1);
+    cudaEventElapsedTime(&o.ms, r.a, r.b);
+    o.flops = r.flops;
+    o.bytes = r.bytes;
+  }
+  *n = (int32_t)Prof::recs.size();
+  return PETRA_OK;
+}
 }

@@ -57,12 +57,20 @@ struct ProfScope {
     cat = Prof::category(name);
     a = Prof::ev();
     b = Prof::ev();
-    cudaEventRecord(a, st);
+    record(a);
   }
   ~ProfScope() {
     if (cat < 0) return;
-    cudaEventRecord(b, st);
+    record(b);
     Prof::recs.push_back({cat, a, b, flops, bytes});
+  }
+  // inside a stream capture (the profiled replay runs each stage tick as a one-off graph, so
+  // the host's launch work is not between the two events) the record must be an event node
+  void record(cudaEvent_t e) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else cudaEventRecord(e, st);
   }
 };
 

@@ -104,6 +104,7 @@ Stage::~Stage() {
   // (cudaFree, or a caller's caching pool that would hand them out again at once)
   cudaDeviceSynchronize();
   for (auto &kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
+  for (auto ex : prof_execs_) cudaGraphExecDestroy(ex);
   if (side_) cudaStreamDestroy(side_);
   if (fork_) cudaEventDestroy(fork_);
   if (join_) cudaEventDestroy(join_);
@@ -1410,8 +1411,32 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
     }
     if (bwd) enqueue_update(mode, s);
   };
-  if (!use_graph || Prof::enabled) {
+  if (!use_graph) {
     enqueue(st);
+  } else if (Prof::enabled) {
+    // profiled replay: this tick as a one-off graph (its kernels and the ProfScope event
+    // nodes), so each kernel's event pair brackets device work only, not the host's tensor-map
+    // encoding and launch calls (a kernel shorter than its host enqueue would otherwise be
+    // timed at the host's pace)
+    cudaGraph_t g = nullptr;
+    PETRA_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    capturing = true;
+    try {
+      enqueue(st);
+      capturing = false;
+    } catch (...) {
+      capturing = false;
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    PETRA_CUDA(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t ex = nullptr;
+    cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    PETRA_CUDA(e);
+    PETRA_CUDA(cudaGraphLaunch(ex, st));
+    prof_execs_.push_back(ex);  // released by the destructor (after its device sync)
   } else {
     std::vector<uintptr_t> key = {(uintptr_t)fwd, (uintptr_t)bwd, (uintptr_t)mode, (uintptr_t)a.round_msgs};
     for (const void *p : {(const void *)a.x1, (const void *)a.x2, (const void *)a.labels, (const void *)a.o[0],

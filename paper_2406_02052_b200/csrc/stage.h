@@ -237,6 +237,7 @@ class Stage {
   float *lr_host_ = nullptr;
   uint64_t lr_next_ = 0;
   std::map<std::vector<uintptr_t>, CachedGraph> graphs_;
+  std::vector<cudaGraphExec_t> prof_execs_;  // one-off graphs of the profiled replay
   void upload_lr(float lr, cudaStream_t st);
   int next_update_mode() const;
   void advance_step(int mode);

@@ -11,9 +11,10 @@ import re
 import sys
 
 MAIN = {  # category -> (main-kernel regex, helper-kernel regex)
-    "conv_fwd_tc": (r"(conv_tc_kernel|conv_halo_kernel)<\d+, \d+, 1>", r"splitk_out_kernel<1>"),
-    "conv_dgrad_tc": (r"(conv_tc_kernel|conv_halo_kernel)<\d+, \d+, 0>", r"splitk_out_kernel<0>|phase_fill"),
-    "conv_wgrad_tc": (r"wgrad_tc_kernel|wgrad_halo_kernel", r"splitk_sum_kernel"),
+    # third template argument = OUT16 (conv_tc_kernel<BN, STAGES, OUT16, KG, PAIR>, conv_halo_kernel<BN, T, OUT16>)
+    "conv_fwd_tc": (r"(conv_tc_kernel|conv_halo_kernel)<\d+, \d+, 1[,>]", r"splitk_out_kernel<1>"),
+    "conv_dgrad_tc": (r"(conv_tc_kernel|conv_halo_kernel)<\d+, \d+, 0[,>]", r"splitk_out_kernel<0>|phase_fill"),
+    "conv_wgrad_tc": (r"wgrad_tc_kernel|wgrad_halo_kernel", r"splitk_sum4?_kernel"),
     "conv_fwd_stem_tc": (r"stem_fwd_kernel", None),
     "bn_apply": (r"bn_apply(_fixed|_tma)?_kernel", None),
     "bn_bwd_reduce": (r"bn_bwd_reduce(_tma)?_kernel", None),
