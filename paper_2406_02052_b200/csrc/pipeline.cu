@@ -96,11 +96,13 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
   const bool prio_on = env_int("PETRA_STREAM_PRIO", 1) != 0;
   // the final stage runs forward, loss and backward as ONE chain on its stage stream (no
   // backward side stream): PETRA_TAIL_PRIO=1 gives that stream the backward streams' rank
-  const bool tail_hi = env_int("PETRA_TAIL_PRIO", 1) != 0;  // R18 +2.4 % (profiles/r02/tuning/tail_priority.txt)
+  // (2: one rank below the backward streams)
+  const int tail_p = env_int("PETRA_TAIL_PRIO", 1);  // R18 +2.4 % (profiles/r02/tuning/tail_priority.txt)
+  const int tail_rank = tail_p == 1 ? prio_hi : (tail_p == 2 ? std::min(prio_lo, prio_hi + 1) : (prio_lo + prio_hi) / 2);
   for (int j = j0; j <= j1; ++j) {
     if (prio_on)
       PETRA_CUDA(cudaStreamCreateWithPriority(&streams_[j], cudaStreamNonBlocking,
-                                              (tail_hi && j == J_) ? prio_hi : (prio_lo + prio_hi) / 2));
+                                              j == J_ ? tail_rank : (prio_lo + prio_hi) / 2));
     else PETRA_CUDA(cudaStreamCreateWithFlags(&streams_[j], cudaStreamNonBlocking));
     PETRA_CUDA(cudaEventCreateWithFlags(&done_[j], cudaEventDisableTiming));
   }

@@ -341,7 +341,10 @@ void Stage::build() {
   PETRA_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
   PETRA_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
   if (tc_ && env_int("PETRA_WGRAD_STREAM", 1)) {
-    if (prio_on) PETRA_CUDA(cudaStreamCreateWithPriority(&wg_, cudaStreamNonBlocking, prio_lo));
+    // PETRA_WGRAD_PRIO: 0 lowest (default), 1 the forward's rank, 2 the backward's
+    static const int wprio = env_int("PETRA_WGRAD_PRIO", 0);
+    const int wp = wprio >= 2 ? prio_hi : (wprio == 1 ? (prio_lo + prio_hi) / 2 : prio_lo);
+    if (prio_on) PETRA_CUDA(cudaStreamCreateWithPriority(&wg_, cudaStreamNonBlocking, wp));
     else PETRA_CUDA(cudaStreamCreateWithFlags(&wg_, cudaStreamNonBlocking));
     PETRA_CUDA(cudaEventCreateWithFlags(&wg_fork_, cudaEventDisableTiming));
     PETRA_CUDA(cudaEventCreateWithFlags(&wg_join_, cudaEventDisableTiming));
