@@ -14,6 +14,8 @@
 //   update                 PAPER.md:135, 256 (Nesterov 0.9, wd exclusions)
 #include "stage.h"
 
+#include <algorithm>
+
 #include <cstdlib>
 
 #include <cmath>
@@ -108,6 +110,8 @@ Stage::~Stage() {
   if (side_) cudaStreamDestroy(side_);
   if (fork_) cudaEventDestroy(fork_);
   if (join_) cudaEventDestroy(join_);
+  if (eu_b_) cudaEventDestroy(eu_b_);
+  if (fwd_done_) cudaEventDestroy(fwd_done_);
   if (wg_) cudaStreamDestroy(wg_);
   if (wg_fork_) cudaEventDestroy(wg_fork_);
   if (wg_join_) cudaEventDestroy(wg_join_);
@@ -340,6 +344,8 @@ void Stage::build() {
   else PETRA_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
   PETRA_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
   PETRA_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
+  PETRA_CUDA(cudaEventCreateWithFlags(&eu_b_, cudaEventDisableTiming));
+  PETRA_CUDA(cudaEventCreateWithFlags(&fwd_done_, cudaEventDisableTiming));
   if (tc_ && env_int("PETRA_WGRAD_STREAM", 1)) {
     // PETRA_WGRAD_PRIO: 0 lowest (default), 1 the forward's rank, 2 the backward's
     static const int wprio = env_int("PETRA_WGRAD_PRIO", 0);
@@ -448,6 +454,28 @@ void Stage::build() {
   PETRA_CUDA(cudaMemcpy(segs_dev_->p, segs_.data(), segs_.size() * sizeof(SgdSeg), cudaMemcpyHostToDevice));
   const std::vector<SgdChunk> chunks = sgd_chunks(segs_);
   n_chunks_ = (int)chunks.size();
+  {  // per-unit chunk ranges (segments follow tensors_ order; chunks follow segments)
+    std::vector<int> seg_unit;
+    for (auto &t : tensors_)
+      if (t.kind <= PETRA_T_FC_B) seg_unit.push_back(t.unit);
+    const int nu = (int)units_.size();
+    unit_chunk_lo_.assign(nu, 0);
+    unit_chunk_hi_.assign(nu, 0);
+    std::vector<int> seen(nu, 0);
+    early_ok_ = (int)seg_unit.size() == (int)segs_.size();
+    int prev = -1;
+    for (int c = 0; c < n_chunks_ && early_ok_; ++c) {
+      const int u = seg_unit[chunks[c].seg];
+      if (u < 0 || u >= nu) { early_ok_ = false; break; }
+      if (u != prev) {
+        if (seen[u]) early_ok_ = false;  // a unit's items must be one contiguous range
+        seen[u] = 1;
+        unit_chunk_lo_[u] = c;
+        prev = u;
+      }
+      unit_chunk_hi_[u] = c + 1;
+    }
+  }
   chunks_dev_ = dalloc(std::max<size_t>(1, chunks.size()) * sizeof(SgdChunk));
   PETRA_CUDA(cudaMemcpy(chunks_dev_->p, chunks.data(), chunks.size() * sizeof(SgdChunk), cudaMemcpyHostToDevice));
 }
@@ -572,6 +600,46 @@ void Stage::enqueue_update(int mode, cudaStream_t st) {
                v_->as<float>(),
              grad_->as<float>(), acc_ ? acc_->as<float>() : nullptr, desc_.accumulation_k, mode, lr_dev_->as<float>(),
              desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false, nonfinite_->as<int>());
+}
+
+// unit `u`'s update on the wgrad stream, ordered after everything `st` (the backward
+// stream) has enqueued so far -- the unit's dgrad, BN-backward sums and SIMT wgrads -- its
+// tensor-core wgrads (already on the wgrad stream) and, once, this tick's forward
+void Stage::early_update(int u, cudaStream_t st) {
+  if (!eu_.active || u < 0 || u >= (int)eu_.done.size() || unit_chunk_hi_[u] <= unit_chunk_lo_[u]) return;
+  PETRA_CUDA(cudaEventRecord(eu_b_, st));
+  PETRA_CUDA(cudaStreamWaitEvent(wg_, eu_b_, 0));
+  if (eu_.fwd_pending) {
+    PETRA_CUDA(cudaStreamWaitEvent(wg_, fwd_done_, 0));
+    eu_.fwd_pending = false;
+  }
+  const int lo = unit_chunk_lo_[u], n = unit_chunk_hi_[u] - lo;
+  ProfScope ps("sgd_update", wg_, 0.0, 0.0);
+  sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), chunks_dev_->as<SgdChunk>() + lo, n, theta_->as<float>(),
+             v_->as<float>(), grad_->as<float>(), acc_ ? acc_->as<float>() : nullptr, desc_.accumulation_k, eu_.mode,
+             lr_dev_->as<float>(), desc_.momentum, desc_.weight_decay, desc_.nesterov, wg_, false,
+             nonfinite_->as<int>());
+  wg_active_ = true;
+  eu_.done[u] = 1;
+}
+
+// the tick's update of every unit not updated early (all of them when early updates are off)
+void Stage::enqueue_update_rest(int mode, cudaStream_t st) {
+  const bool any = eu_.active && std::any_of(eu_.done.begin(), eu_.done.end(), [](char c) { return c != 0; });
+  eu_.active = false;
+  if (!any) {
+    enqueue_update(mode, st);
+    return;
+  }
+  for (int u = 0; u < (int)eu_.done.size(); ++u) {
+    if (eu_.done[u] || unit_chunk_hi_[u] <= unit_chunk_lo_[u]) continue;
+    const int lo = unit_chunk_lo_[u], n = unit_chunk_hi_[u] - lo;
+    ProfScope ps("sgd_update", st, 0.0, 0.0);
+    sgd_update(segs_dev_->as<SgdSeg>(), (int)segs_.size(), chunks_dev_->as<SgdChunk>() + lo, n, theta_->as<float>(),
+               v_->as<float>(), grad_->as<float>(), acc_ ? acc_->as<float>() : nullptr, desc_.accumulation_k, mode,
+               lr_dev_->as<float>(), desc_.momentum, desc_.weight_decay, desc_.nesterov, st, false,
+               nonfinite_->as<int>());
+  }
 }
 
 // ------------------------------------------------------------------ layer kernels
@@ -1135,6 +1203,7 @@ void Stage::enqueue_backward_walk(int last_unit, bool recompute, const float *cx
       Bf16Out ob = (recompute && i > 0 && units_[i - 1].d.kind == PETRA_UNIT_REV && units_[i - 1].src() == d)
                        ? src_operand(units_[i - 1]) : Bf16Out{};
       unit_backward(u, recompute, nox, cx, tx, cd, td, st, ob, ready && recompute);
+      early_update(i, st);
       ready = ob.p != nullptr;
       cx[d] = tx[d];
       rox[d] = false;
@@ -1150,6 +1219,7 @@ void Stage::enqueue_backward_walk(int last_unit, bool recompute, const float *cx
         for (int h = 0; h < 2; ++h) td[h] = u.bd[h] ? u.bd[h]->as<float>() : od[h];
       bind_fifo_operands(u, slot);  // the forward converted this micro-batch's input into the slot
       unit_backward(u, recompute, xin, cx, nullptr, cd, td, st, Bf16Out{}, !u.fifo.bslot0.empty());
+      early_update(i, st);
       cx[0] = xin[0];
       cx[1] = xin[1];
       rox[0] = rox[1] = true;  // FIFO memory: copied out at the end, never written
@@ -1367,7 +1437,13 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
       if (a.od[h]) round_bf16_inplace(a.od[h], in_.numel(), s);
     }
   };
+  static const bool early_env = env_int("PETRA_EARLY_UPDATE", 1) != 0;
   auto enqueue = [&](cudaStream_t s) {
+    // early per-unit updates: on the wgrad stream, in a direct or captured (not profiled) tick
+    eu_.active = bwd && early_env && early_ok_ && wg_ && !Prof::enabled;
+    eu_.mode = mode;
+    eu_.fwd_pending = false;
+    eu_.done.assign(units_.size(), 0);
     if (is_last_) {
       ctx_ = 0;
       wait_on(s, a.wait_f);
@@ -1387,6 +1463,10 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
       enqueue_forward(a.x1, a.x2, a.o[0], a.o[1], push, false, nullptr, s);
       round_fwd(s);
       record(a.done_f, s);
+      if (eu_.active) {  // the early updates wait for this forward's reads of theta^t
+        PETRA_CUDA(cudaEventRecord(fwd_done_, s));
+        eu_.fwd_pending = true;
+      }
       ctx_ = 1;
       wait_on(side_, a.wait_b);
       enqueue_backward(a.xt[0], a.xt[1], a.d[0], a.d[1], a.oxt[0], a.oxt[1], a.od[0], a.od[1], pop, side_);
@@ -1412,7 +1492,7 @@ void Stage::tick(const TickArgs &a, float lr, cudaStream_t st, bool use_graph) {
       }
       ctx_ = 0;
     }
-    if (bwd) enqueue_update(mode, s);
+    if (bwd) enqueue_update_rest(mode, s);
   };
   if (!use_graph) {
     enqueue(st);

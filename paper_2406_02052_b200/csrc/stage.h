@@ -188,6 +188,21 @@ class Stage {
   int64_t max_seg_ = 0;
   DevPtr chunks_dev_;   // SgdChunk work items of the update (sgd_chunks)
   int n_chunks_ = 0;
+  // early per-unit updates (PETRA_EARLY_UPDATE): unit u's work items are chunks
+  // [unit_chunk_lo_[u], unit_chunk_hi_[u]); a unit's update runs on the wgrad stream as soon
+  // as its backward (dgrad, BN-backward sums) and wgrads are done and this tick's forward has
+  // read theta, instead of in the stage's one update launch at the end of the tick
+  std::vector<int> unit_chunk_lo_, unit_chunk_hi_;
+  bool early_ok_ = false;  // every unit's items contiguous
+  struct EarlyUpd {
+    bool active = false;
+    int mode = 0;
+    bool fwd_pending = false;  // the wgrad stream still has to wait for fwd_done_
+    std::vector<char> done;    // per unit: updated early this tick
+  } eu_;
+  cudaEvent_t eu_b_ = nullptr, fwd_done_ = nullptr;
+  void early_update(int unit, cudaStream_t st);
+  void enqueue_update_rest(int mode, cudaStream_t st);  // the units not updated early
   DevPtr part_[2], spart_[2], wgrad_ws_[2], counters_[2];  // per context (see Layer)
   int ctx_ = 0;                                 // workspace context being enqueued
   DevPtr &part() { return part_[ctx_]; }
