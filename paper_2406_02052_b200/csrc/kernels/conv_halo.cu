@@ -688,7 +688,7 @@ WHaloPlan whalo_plan(int B, int H, int W, int Ci, int Co) {
   const int64_t Mp = (int64_t)B * (H + 2) * (W + 2);
   p.KBtot = (int)cdiv(Mp, p.pb);
   const int items = (Ci / 64) * (Co / 64);
-  static const int ctas = env_int("PETRA_WGRAD_HALO_CTAS", 48);
+  static const int ctas = env_int("PETRA_WGRAD_HALO_CTAS", 32);
   const int want = std::max(1, std::min(p.KBtot, (int)cdiv(ctas, items)));
   p.kb_per_split = (int)cdiv(p.KBtot, want);
   p.splits = (int)cdiv(p.KBtot, p.kb_per_split);

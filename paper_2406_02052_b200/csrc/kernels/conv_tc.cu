@@ -1410,7 +1410,7 @@ WgradPlan wgrad_plan(const ConvGeom &g) {
   w.t = tiling(g.B, g.Ho, g.Wo, 64);
   w.KBtot = (int)(w.t.M() / 64);
   int tiles = w.n_mt * w.n_nt;
-  static const int ctas = env_int("PETRA_WGRAD_CTAS", 48);  // CTAs the split-K aims to fill
+  static const int ctas = env_int("PETRA_WGRAD_CTAS", 32);  // CTAs the split-K aims to fill
   int want = std::max(1, std::min(w.KBtot, (int)cdiv(ctas, tiles)));
   w.kb_per_split = (int)cdiv(w.KBtot, want);
   w.splits = (int)cdiv(w.KBtot, w.kb_per_split);

@@ -21,7 +21,7 @@ int env_int(const char *name, int dflt) {
 }
 
 int conv_grid(int work) {
-  static const int cap = std::max(1, std::min(kNumSMs, env_int("PETRA_CONV_CTAS", 96)));
+  static const int cap = std::max(1, std::min(kNumSMs, env_int("PETRA_CONV_CTAS", 40)));  // 40: DESIGN.md 7 "Grid sizing" (round-2 re-sweep)
   return std::max(1, std::min(work, cap));
 }
 
