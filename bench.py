@@ -373,6 +373,13 @@ def measure(model, stages, batch, precision, steps, warmup, world, rank, local, 
         "bound": bound, "kernel": name, "achieved": round(ach, 2), "peak": peak, "unit": unit,
         "frac": round(ach / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
         "frac_of_launch_rooflines": round(t_roof / t_meas, 4) if t_meas > 0 else None,
+        # the same flops over the SM-time the launches held (duration x min(1, CTAs / 148): the
+        # persistent conv CTAs take one SM each): the tensor-pipe fraction of the SMs the
+        # kernel occupied -- what the grid cap trades against latency
+        "frac_of_occupied_sms": (round(sum(r["flops"] for r in mine) / 1e9 / sum(
+            r["ms"] * min(1.0, max(1, r["ctas"]) / 148.0) for r in mine) / peak, 4)
+            if bound == "tensor" and mine else None),
+        "mean_ctas": round(sum(r["ctas"] for r in mine) / max(1, len(mine)), 1),
         "launch_rooflines": (f"sum over the category's {len(mine)} launches of max(algorithmic flops / "
                              f"{peaks['bf16_tflops']} TFLOP/s, algorithmic bytes / {peaks['hbm_gbs']} GB/s) = "
                              f"{t_roof:.4f} ms over {t_meas:.4f} ms measured; {n_hbm} launches HBM-bound"),

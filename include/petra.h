@@ -458,7 +458,8 @@ petra_status petra_profile(int32_t enable);
 petra_status petra_profile_read(petra_prof_entry *out, int32_t cap, int32_t *n);
 /* The same profile per logical kernel, in enqueue order: category index (the order of
  * petra_profile_read's categories before it drops empty ones is the order of first use;
- * `name` repeats it), event time, algorithmic flops and bytes of that one launch -- for a
+ * `name` repeats it), event time, algorithmic flops and bytes of that one launch and its
+ * largest grid -- for a
  * roofline per launch (each launch's own bound, max(flops / tensor peak, bytes / HBM peak)).
  * Writes min(cap, records) entries, *n = the number of records.  Errors: PETRA_E_ARG (NULL),
  * PETRA_E_CUDA. */
@@ -467,6 +468,7 @@ typedef struct {
   float ms;
   double flops;
   double bytes;
+  int32_t ctas;  /* largest grid (CTAs) the logical kernel launched */
 } petra_prof_record;
 petra_status petra_profile_records(petra_prof_record *out, int32_t cap, int32_t *n);
 

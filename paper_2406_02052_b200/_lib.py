@@ -150,7 +150,8 @@ def profile(enable: bool):
 
 
 class PetraProfRecord(C.Structure):
-    _fields_ = [("name", C.c_char * 32), ("ms", C.c_float), ("flops", C.c_double), ("bytes", C.c_double)]
+    _fields_ = [("name", C.c_char * 32), ("ms", C.c_float), ("flops", C.c_double), ("bytes", C.c_double),
+                ("ctas", C.c_int32)]
 
 
 def profile_records():
@@ -160,8 +161,8 @@ def profile_records():
     call("petra_profile_records", C.cast(one, C.c_void_p), 0, C.byref(n))
     arr = (PetraProfRecord * max(1, n.value))()
     call("petra_profile_records", C.cast(arr, C.c_void_p), n.value, C.byref(n))
-    return [dict(name=arr[i].name.decode(), ms=arr[i].ms, flops=arr[i].flops, bytes=arr[i].bytes)
-            for i in range(n.value)]
+    return [dict(name=arr[i].name.decode(), ms=arr[i].ms, flops=arr[i].flops, bytes=arr[i].bytes,
+                 ctas=arr[i].ctas) for i in range(n.value)]
 
 
 def profile_read():

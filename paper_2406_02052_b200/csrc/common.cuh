@@ -70,6 +70,7 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+  Prof::note_grid(grid);
   PETRA_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
@@ -95,6 +96,7 @@ inline void launch_k_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, si
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 3;
+  Prof::note_grid(grid);
   PETRA_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 

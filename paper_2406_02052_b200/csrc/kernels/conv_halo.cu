@@ -405,7 +405,9 @@ HaloPlan halo_plan(int B, int H, int W, int Cred, int N) {
 
 // a multiple of the N-tile count: every CTA's work items share one N tile
 int halo_grid(int work, int n_nt) {
-  const int g = conv_grid(work);
+  // PETRA_HALO_CTAS (default: the common conv cap)
+  static const int hcap = env_int("PETRA_HALO_CTAS", 0);
+  const int g = hcap > 0 ? std::max(1, std::min({work, hcap, kNumSMs})) : conv_grid(work);
   return std::max(n_nt, g / n_nt * n_nt);
 }
 

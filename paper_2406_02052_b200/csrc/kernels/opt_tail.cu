@@ -478,7 +478,9 @@ std::vector<SgdChunk> sgd_chunks(const std::vector<SgdSeg> &segs) {
 void sgd_update(const SgdSeg *segs_dev, int nseg, const SgdChunk *chunks_dev, int nchunks, float *theta, float *v,
                 const float *grad, float *acc, int k, int mode, const float *lr_dev, float mom, float wd, int nesterov,
                 cudaStream_t st, bool shadow_only, int *nonfinite) {
-  const unsigned grid = (unsigned)std::max(1, std::min(nchunks, 8 * kNumSMs));
+  // blocks stride over the items: PETRA_SGD_BLOCKS caps the grid (default 8 per SM)
+  static const int cap = std::max(1, env_int("PETRA_SGD_BLOCKS", 8 * kNumSMs));
+  const unsigned grid = (unsigned)std::max(1, std::min(nchunks, cap));
   launch_k(sgd_kernel, grid, 256, 0, st, segs_dev, chunks_dev, nchunks, theta, v, grad, acc, 1.f / (float)k, mode,
            lr_dev, mom, wd, nesterov, shadow_only ? 1 : 0, nonfinite);
   PETRA_LAUNCH_CHECK();

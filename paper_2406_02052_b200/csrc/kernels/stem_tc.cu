@@ -469,7 +469,8 @@ WPlan wplan(const ConvGeom &g) {
   WPlan w{};
   w.n_mt = (int)cdiv(padded_k(g), 128);
   w.KBtot = (int)cdiv(g.M(), 64);
-  const int want = std::max(1, std::min(w.KBtot, (int)cdiv(kNumSMs, w.n_mt)));
+  static const int wctas = std::max(1, std::min(kNumSMs, env_int("PETRA_STEM_WGRAD_CTAS", kNumSMs)));
+  const int want = std::max(1, std::min(w.KBtot, (int)cdiv(wctas, w.n_mt)));
   w.kb_per_split = (int)cdiv(w.KBtot, want);
   w.splits = (int)cdiv(w.KBtot, w.kb_per_split);
   return w;
@@ -524,7 +525,8 @@ StatsRows stem_fwd_tc(const ConvGeom &g, const __nv_bfloat16 *xq, const float *w
   P.w = w;
   P.out = z;
   P.stats = stats_part;
-  const int grid = (int)std::min<int64_t>(cdiv(P.M, 128), kNumSMs);
+  static const int fctas = std::max(1, std::min(kNumSMs, env_int("PETRA_STEM_CTAS", kNumSMs)));
+  const int grid = (int)std::min<int64_t>(cdiv(P.M, 128), fctas);
   const size_t smem = fwd_smem(P.N, P.KB);
   if (z_bf16) {
     if (P.N == 64) launch_k(stem_fwd_kernel<64, true>, grid, kThreads, smem, st, P);

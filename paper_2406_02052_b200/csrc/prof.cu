@@ -1,5 +1,8 @@
 // prof.cu -- launch counter and event-based per-category timing (product code).
 #include <cstdlib>
+#include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <cstring>
 
 #include "../../include/petra.h"
@@ -10,6 +13,7 @@
 namespace petra {
 std::atomic<int64_t> Prof::launches{0};
 bool Prof::enabled = false;
+int64_t Prof::scope_grid = 0;
 std::vector<Prof::Rec> Prof::recs;
 std::vector<std::string> Prof::names;
 std::vector<cudaEvent_t> Prof::pool;
@@ -102,6 +106,7 @@ petra_status petra_profile_records(petra_prof_record *out, int32_t cap, int32_t 
     cudaEventElapsedTime(&o.ms, r.a, r.b);
     o.flops = r.flops;
     o.bytes = r.bytes;
+    o.ctas = (int32_t)std::min<int64_t>(r.ctas, INT32_MAX);
   }
   *n = (int32_t)Prof::recs.size();
   return PETRA_OK;

@@ -6,6 +6,7 @@
 
 #include <nvtx3/nvToolsExt.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -38,7 +39,12 @@ struct Prof {
     int cat;
     cudaEvent_t a, b;
     double flops, bytes;
+    int64_t ctas;  // the largest grid launched inside the scope
   };
+  static int64_t scope_grid;  // largest grid since the innermost open ProfScope began
+  static void note_grid(const dim3 &g) {
+    if (enabled) scope_grid = std::max<int64_t>(scope_grid, (int64_t)g.x * g.y * g.z);
+  }
   static std::vector<Rec> recs;
   static std::vector<std::string> names;
   static std::vector<cudaEvent_t> pool;
@@ -52,8 +58,11 @@ struct ProfScope {
   cudaStream_t st;
   cudaEvent_t a{}, b{};
   double flops, bytes;
+  int64_t saved_grid = 0;
   ProfScope(const char *name, cudaStream_t s, double fl, double by) : st(s), flops(fl), bytes(by) {
     if (!Prof::enabled) return;
+    saved_grid = Prof::scope_grid;
+    Prof::scope_grid = 0;
     cat = Prof::category(name);
     a = Prof::ev();
     b = Prof::ev();
@@ -62,7 +71,8 @@ struct ProfScope {
   ~ProfScope() {
     if (cat < 0) return;
     record(b);
-    Prof::recs.push_back({cat, a, b, flops, bytes});
+    Prof::recs.push_back({cat, a, b, flops, bytes, Prof::scope_grid});
+    Prof::scope_grid = std::max(saved_grid, Prof::scope_grid);
   }
   // inside a stream capture (the profiled replay runs each stage tick as a one-off graph, so
   // the host's launch work is not between the two events) the record must be an event node
