@@ -1044,10 +1044,31 @@ ConvPlan conv_plan(int M, int N, int KB) {
   // widest N tile that still leaves `want_tiles` tiles (wider tiles reuse each A tile
   // over more columns: fewer operand bytes from L2 per MMA)
   static const int want_tiles = env_int("PETRA_CONV_TILES", 48);  // 48: R18 +1.4 %, serial conv -4.5 % (DESIGN 7)
-  for (int bn : {256, 128, 64}) {
-    if (N % bn) continue;
-    p.BN = bn;
-    if (mt * (N / bn) >= want_tiles) break;
+  static const int model = env_int("PETRA_CONV_PLAN", 1);
+  if (model) {
+    // PETRA_CONV_PLAN=1: the N tile with the fewest k-block rounds of the persistent grid --
+    // rounds = ceil(tiles / CTAs) x the measured cycles per k-block of that tile width (~460 /
+    // 610 / 710 for BN = 64 / 128 / 256) -- ties (within 5 %) to the fewer CTAs
+    double best_l = 0, best_s = 0;
+    bool first = true;
+    for (int bn : {256, 128, 64}) {
+      if (N % bn) continue;
+      const int t = mt * (N / bn), ctas = conv_grid(t);
+      const double c = bn == 256 ? 710.0 : (bn == 128 ? 610.0 : 460.0);
+      const double lat = (double)cdiv(t, ctas) * c, smt = lat * ctas;
+      if (first || lat < 0.95 * best_l || (lat <= 1.05 * best_l && smt < best_s)) {
+        best_l = lat;
+        best_s = smt;
+        p.BN = bn;
+        first = false;
+      }
+    }
+  } else {
+    for (int bn : {256, 128, 64}) {
+      if (N % bn) continue;
+      p.BN = bn;
+      if (mt * (N / bn) >= want_tiles) break;
+    }
   }
   const int tiles = mt * (N / p.BN);
   // split-K off by default: under the tick's stream concurrency the split's partial
