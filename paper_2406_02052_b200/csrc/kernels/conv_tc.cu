@@ -1577,7 +1577,7 @@ CUtensorMap plain_map_2d_strided(const void *base, CUtensorMapDataType dt, int e
 
 
 void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream_t st) {
-  static const bool v4 = env_int("PETRA_SPLITK_V4", 1) != 0;
+  static const bool v4 = env_int("PETRA_SPLITK_V4", 0) != 0;  // 0: R18 +1.4 % (grid-stride, <= 4 blocks per SM)
   if (v4 && n % 4 == 0 && (uintptr_t)part % 16 == 0 && (uintptr_t)out % 16 == 0) {
     const int64_t n4 = n / 4;
     launch_k(splitk_sum4_kernel, (unsigned)cdiv(n4, 32), 256, 0, st, reinterpret_cast<const float4 *>(part), splits, n4,
