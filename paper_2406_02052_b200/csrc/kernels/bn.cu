@@ -941,8 +941,15 @@ __global__ void bn_bwd_dz_kernel(int64_t M, int C, const TZ *__restrict__ z, con
 // a byte offset inside a TMA ring stage that can start a tensor-copy destination
 inline bool ring_aligned(size_t bytes) { return bytes % 128 == 0; }
 
+// grid-stride elementwise kernels: at most PETRA_EW_BLOCKS_PER_SM (default 8) 256-thread blocks per SM
 inline unsigned ew_grid(int64_t n) {
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs));
+  static const int per_sm = std::max(1, env_int("PETRA_EW_BLOCKS_PER_SM", 8));
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)per_sm * kNumSMs));
+}
+// row-stride kernels (one pixel row per block iteration): PETRA_ROW_BLOCKS_PER_SM (default 16)
+inline int64_t row_blocks() {
+  static const int per_sm = std::max(1, env_int("PETRA_ROW_BLOCKS_PER_SM", 16));
+  return (int64_t)per_sm * kNumSMs;
 }
 
 // grid of a per-channel elementwise pass over M x C (256 threads, 4 channels each):

@@ -1413,7 +1413,8 @@ void run_dgrad(const ConvGeom &g, const __nv_bfloat16 *dz, bool dz_pad, const __
       launch_any(ta, L, wt, g.Ci, wK, P, ws, false, st);
     }
   if (empty_mask) {
-    launch_k(phase_fill_kernel, (unsigned)std::min<int64_t>((int64_t)g.B * g.H, 16 * kNumSMs), 256, 0, st, 
+    static const int64_t rows_cap = (int64_t)std::max(1, env_int("PETRA_ROW_BLOCKS_PER_SM", 16)) * kNumSMs;
+    launch_k(phase_fill_kernel, (unsigned)std::min<int64_t>((int64_t)g.B * g.H, rows_cap), 256, 0, st, 
         g.B, g.H, g.W, g.Ci, empty_mask, addend, dx);
     PETRA_LAUNCH_CHECK();
   }

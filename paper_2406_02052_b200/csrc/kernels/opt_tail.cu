@@ -455,8 +455,15 @@ __global__ void f32_to_bf16_padded_kernel(const float4 *__restrict__ x, uint2 *_
   }
 }
 
+// grid-stride elementwise kernels: at most PETRA_EW_BLOCKS_PER_SM (default 8) 256-thread blocks per SM
 inline unsigned ew_grid(int64_t n) {
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8 * kNumSMs));
+  static const int per_sm = std::max(1, env_int("PETRA_EW_BLOCKS_PER_SM", 8));
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)per_sm * kNumSMs));
+}
+// row-stride kernels (one pixel row per block iteration): PETRA_ROW_BLOCKS_PER_SM (default 16)
+inline int64_t row_blocks() {
+  static const int per_sm = std::max(1, env_int("PETRA_ROW_BLOCKS_PER_SM", 16));
+  return (int64_t)per_sm * kNumSMs;
 }
 
 }  // namespace
@@ -584,7 +591,7 @@ void maxpool_fwd(const float *a, int B, int H, int W, int C, int Ho, int Wo, flo
                  cudaStream_t st) {
   if (C % 8 == 0 && (int64_t)B * H * W * C < ((int64_t)1 << 31)) {
     const int C4 = C / 4;
-    launch_k(maxpool_fwd_v4_kernel, (unsigned)std::min<int64_t>((int64_t)B * Ho, 16 * kNumSMs), 256, 0, st, 
+    launch_k(maxpool_fwd_v4_kernel, (unsigned)std::min<int64_t>((int64_t)B * Ho, row_blocks()), 256, 0, st, 
         reinterpret_cast<const float4 *>(a), B, H, W, C4, Ho, Wo, reinterpret_cast<float4 *>(o1),
         reinterpret_cast<float4 *>(o2), reinterpret_cast<uchar4 *>(arg));
   } else {
@@ -597,7 +604,7 @@ void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, in
                  float *da, cudaStream_t st) {
   if (C % 8 == 0 && (int64_t)B * H * W * C < ((int64_t)1 << 31)) {
     const int C4 = C / 4;
-    launch_k(maxpool_bwd_v4_kernel, (unsigned)std::min<int64_t>((int64_t)B * H, 16 * kNumSMs), 256, 0, st, 
+    launch_k(maxpool_bwd_v4_kernel, (unsigned)std::min<int64_t>((int64_t)B * H, row_blocks()), 256, 0, st, 
         reinterpret_cast<const float4 *>(d1), reinterpret_cast<const float4 *>(d2),
         reinterpret_cast<const uchar4 *>(arg), B, H, W, C4, Ho, Wo, reinterpret_cast<float4 *>(da));
   } else {
@@ -608,7 +615,7 @@ void maxpool_bwd(const float *d1, const float *d2, const uint8_t *arg, int B, in
 
 void f32_to_bf16_padded(const float *x, __nv_bfloat16 *y, int B, int H, int W, int C, cudaStream_t st) {
   const int C4 = C / 4;
-  launch_k(f32_to_bf16_padded_kernel, (unsigned)std::min<int64_t>((int64_t)B * H, 16 * kNumSMs), 256, 0, st, 
+  launch_k(f32_to_bf16_padded_kernel, (unsigned)std::min<int64_t>((int64_t)B * H, row_blocks()), 256, 0, st, 
       reinterpret_cast<const float4 *>(x), reinterpret_cast<uint2 *>(y), B, H, W, C4);
   PETRA_LAUNCH_CHECK();
 }
