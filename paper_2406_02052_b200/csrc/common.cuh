@@ -51,6 +51,12 @@ int env_int(const char *name, int dflt);
 // stage's two directions run concurrently, so a kernel that leaves SMs to its
 // neighbours raises the tick's throughput (measured); PETRA_CONV_CTAS.
 int conv_grid(int work);
+int conv_cap();
+// stages sharing this GPU (persistent-grid caps, prof.cu); set by petra_pipeline_create
+void set_stages_per_gpu(int n);
+int stages_per_gpu();
+int wgrad_ctas(const char *env_name);      // split-K target CTAs of the wgrads
+int wgrad_ctas_max(const char *env_name);  // ... the largest (workspace sizing)
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {

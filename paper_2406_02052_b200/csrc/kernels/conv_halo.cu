@@ -679,7 +679,7 @@ struct WHaloPlan {
   int pb, HR, box_rows, splits, kb_per_split, KBtot, cs;
   size_t smem;
 };
-WHaloPlan whalo_plan(int B, int H, int W, int Ci, int Co) {
+WHaloPlan whalo_plan(int B, int H, int W, int Ci, int Co, int ctas_override = 0) {
   WHaloPlan p{};
   static const int pb_env = env_int("PETRA_WGRAD_HALO_PB", 128);
   p.pb = pb_env == 128 ? 128 : 64;
@@ -690,7 +690,7 @@ WHaloPlan whalo_plan(int B, int H, int W, int Ci, int Co) {
   const int64_t Mp = (int64_t)B * (H + 2) * (W + 2);
   p.KBtot = (int)cdiv(Mp, p.pb);
   const int items = (Ci / 64) * (Co / 64);
-  static const int ctas = env_int("PETRA_WGRAD_HALO_CTAS", 32);
+  const int ctas = ctas_override > 0 ? ctas_override : wgrad_ctas("PETRA_WGRAD_HALO_CTAS");
   const int want = std::max(1, std::min(p.KBtot, (int)cdiv(ctas, items)));
   p.kb_per_split = (int)cdiv(p.KBtot, want);
   p.splits = (int)cdiv(p.KBtot, p.kb_per_split);
@@ -742,7 +742,7 @@ bool wgrad_halo_eligible(const ConvGeom &g) {
 
 size_t wgrad_halo_workspace(const ConvGeom &g) {
   if (!wgrad_halo_eligible(g)) return 0;
-  const WHaloPlan p = whalo_plan(g.B, g.H, g.W, g.Ci, g.Co);
+  const WHaloPlan p = whalo_plan(g.B, g.H, g.W, g.Ci, g.Co, wgrad_ctas_max("PETRA_WGRAD_HALO_CTAS"));
   const int parts = p.splits / p.cs;
   return parts > 1 ? (size_t)parts * g.Co * g.K() * sizeof(float) : 0;
 }

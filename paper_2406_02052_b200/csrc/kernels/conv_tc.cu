@@ -1424,7 +1424,7 @@ struct WgradPlan {
   int BN, splits, kb_per_split, n_mt, n_nt, KBtot;
   Tiling t;
 };
-WgradPlan wgrad_plan(const ConvGeom &g) {
+WgradPlan wgrad_plan(const ConvGeom &g, int ctas_override = 0) {
   WgradPlan w{};
   w.BN = g.Co % 256 == 0 ? 256 : (g.Co % 128 == 0 ? 128 : 64);
   w.n_nt = g.Co / w.BN;
@@ -1432,7 +1432,8 @@ WgradPlan wgrad_plan(const ConvGeom &g) {
   w.t = tiling(g.B, g.Ho, g.Wo, 64);
   w.KBtot = (int)(w.t.M() / 64);
   int tiles = w.n_mt * w.n_nt;
-  static const int ctas = env_int("PETRA_WGRAD_CTAS", 32);  // CTAs the split-K aims to fill
+  // CTAs the split-K aims to fill; workspaces are sized for the largest target
+  const int ctas = ctas_override > 0 ? ctas_override : wgrad_ctas("PETRA_WGRAD_CTAS");
   int want = std::max(1, std::min(w.KBtot, (int)cdiv(ctas, tiles)));
   w.kb_per_split = (int)cdiv(w.KBtot, want);
   w.splits = (int)cdiv(w.KBtot, w.kb_per_split);
@@ -1500,7 +1501,7 @@ bool conv_tc_supported(const ConvGeom &g, int mode) {
 size_t conv_tc_workspace(const ConvGeom &g, int mode) {
   if (!conv_tc_supported(g, mode)) return 0;
   if (mode == 2) {
-    WgradPlan w = wgrad_plan(g);
+    WgradPlan w = wgrad_plan(g, wgrad_ctas_max("PETRA_WGRAD_CTAS"));
     return std::max(w.splits > 1 ? (size_t)w.splits * g.Co * g.K() * sizeof(float) : (size_t)0,
                     wgrad_halo_workspace(g));
   }

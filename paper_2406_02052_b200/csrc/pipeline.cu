@@ -63,6 +63,12 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
   if (transport_ == PETRA_TRANSPORT_NCCL && !d.nccl_id) throw PetraError(PETRA_E_ARG, "NCCL transport needs nccl_id");
   if (transport_ == PETRA_TRANSPORT_LOCAL && group_ == 0) throw PetraError(PETRA_E_ARG, "LOCAL transport needs local_group");
   if (wire_ != PETRA_WIRE_FP32 && wire_ != PETRA_WIRE_BF16) throw PetraError(PETRA_E_ARG, "unknown wire format");
+  {  // persistent-grid caps for the stages sharing this GPU (prof.cu; PETRA_STAGES_PER_GPU pins it)
+    int n = 0;
+    for (int j = 1; j <= J_; ++j) n += sched_.local(j) ? 1 : 0;
+    const int pin = env_int("PETRA_STAGES_PER_GPU", 0);
+    set_stages_per_gpu(pin > 0 ? pin : n);
+  }
   stages_.resize(J_ + 2);
   fwd_.resize(J_ + 2);
   bwd_.resize(J_ + 2);

@@ -1,4 +1,6 @@
 // prof.cu -- launch counter and event-based per-category timing (product code).
+#include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <algorithm>
 #include <climits>
@@ -24,10 +26,32 @@ int env_int(const char *name, int dflt) {
   return (e && *e) ? atoi(e) : dflt;
 }
 
-int conv_grid(int work) {
-  static const int cap = std::max(1, std::min(kNumSMs, env_int("PETRA_CONV_CTAS", 40)));  // 40: DESIGN.md 7 "Grid sizing" (round-2 re-sweep)
-  return std::max(1, std::min(work, cap));
+// Persistent-grid caps by the number of stages that share the GPU (set by each pipeline
+// from its local stage count; 1 for the stage-level API): the fewer stages run
+// concurrently, the more of the GPU each kernel should take.  Measured (DESIGN.md 7 "Grid
+// sizing"): 1 stage (J = 1) 148 CTAs, 2 -> 96, 3 -> 64, >= 4 -> 40; wgrad splits 48 / 48 /
+// 32 / 32.  PETRA_CONV_CTAS / PETRA_WGRAD_CTAS / PETRA_WGRAD_HALO_CTAS override.
+static std::atomic<int> g_stages_per_gpu{1};
+void set_stages_per_gpu(int n) { g_stages_per_gpu.store(std::max(1, n)); }
+int stages_per_gpu() { return g_stages_per_gpu.load(); }
+int conv_cap() {
+  static const int env = env_int("PETRA_CONV_CTAS", 0);
+  if (env > 0) return std::min(kNumSMs, env);
+  const int n = stages_per_gpu();
+  return n <= 1 ? kNumSMs : (n == 2 ? 96 : (n == 3 ? 64 : 40));
 }
+int wgrad_ctas(const char *env_name) {
+  const int env = env_int(env_name, 0);
+  if (env > 0) return env;
+  return stages_per_gpu() <= 2 ? 48 : 32;
+}
+// the largest split target any stage count selects (workspace sizing: a stage's buffers must fit
+// the plans of every later launch, whatever the process's pipelines set meanwhile)
+int wgrad_ctas_max(const char *env_name) {
+  const int env = env_int(env_name, 0);
+  return env > 0 ? env : 48;
+}
+int conv_grid(int work) { return std::max(1, std::min(work, conv_cap())); }
 
 bool pdl_enabled() {
   static const bool on = [] {

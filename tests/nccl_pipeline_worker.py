@@ -41,6 +41,7 @@ def run(pipe, sr, rank, B, n_mb, J, lr=0.025):
 
 
 def main():
+    os.environ.setdefault("PETRA_STAGES_PER_GPU", "4")  # same kernel plans on every rank layout
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     dist.init_process_group("gloo")

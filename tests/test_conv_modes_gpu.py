@@ -19,7 +19,8 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 MODES = {
-    "cluster_split_k": {"PETRA_CONV_CS": "1"},
+    # at the J >= 4 grid cap (the plan's cost model compares against the capped grid)
+    "cluster_split_k": {"PETRA_CONV_CS": "1", "PETRA_CONV_CTAS": "40"},
     "cta_pair_kg2": {"PETRA_CONV_PAIR": "1"},
     "cta_pair_kg1": {"PETRA_CONV_PAIR": "1", "PETRA_CONV_PAIR_KG": "1"},
 }

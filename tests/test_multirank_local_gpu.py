@@ -11,6 +11,7 @@ and without joining the exchange into the caller's stream (join_comm = 0 lets th
 exchange of tick t run under tick t+1).  The integer reports of every rank must also
 be identical to world 1's (the schedule is replicated on every rank)."""
 import itertools
+import os
 
 import numpy as np
 import pytest
@@ -28,6 +29,10 @@ from paper_2406_02052_b200 import models as PM  # noqa: E402
 from paper_2406_02052_b200.dist import contiguous_stage_ranks  # noqa: E402
 
 _group = itertools.count(1)
+# the persistent-grid caps follow the stages per GPU (DESIGN.md 7 "Grid sizing"); pin them to
+# the world-1 value so that every rank layout runs the same kernel plans (the claim under test
+# is that the cross-rank plumbing changes nothing)
+os.environ["PETRA_STAGES_PER_GPU"] = "4"
 
 
 def _run(world, precision, join_comm, n_mb=6, B=8, counts=(5, 4, 4, 5), lr=0.025, wire="fp32"):
