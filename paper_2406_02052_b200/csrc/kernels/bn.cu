@@ -119,6 +119,9 @@ inline RedGeom red_geom(int64_t M, int C, int RT, int per_sm = 1) {
   // one wave: one block per SM (1024 / 512 threads, >= 64 KB of loads in flight), few
   // partials to merge
   int64_t want = std::max<int64_t>(1, (int64_t)per_sm * kNumSMs / g.ctiles);
+  // PETRA_BN_BLOCKS (experiment): at most that many blocks per pass (0: no cap)
+  static const int cap_blocks = env_int("PETRA_BN_BLOCKS", 0);
+  if (cap_blocks > 0) want = std::min<int64_t>(want, std::max(1, cap_blocks / g.ctiles));
   // at least `min_rows` rows per block (PETRA_BN_MIN_ROWS, default 128; at least 4 row groups): small
   // tensors otherwise spread over hundreds of blocks of a few rows each
   static const int min_rows = env_int("PETRA_BN_MIN_ROWS", 128);  // 128: R18 +2.9 % (DESIGN 7)
