@@ -105,10 +105,12 @@ Pipeline::Pipeline(const petra_pipeline_desc &d)
   // (2: one rank below the backward streams)
   const int tail_p = env_int("PETRA_TAIL_PRIO", 1);  // R18 +2.4 % (profiles/r02/tuning/tail_priority.txt)
   const int tail_rank = tail_p == 1 ? prio_hi : (tail_p == 2 ? std::min(prio_lo, prio_hi + 1) : (prio_lo + prio_hi) / 2);
+  // PETRA_FWD_PRIO (experiment): ranks above the middle for the other stages' streams
+  const int fwd_up = env_int("PETRA_FWD_PRIO", 0);
+  const int mid = std::max(prio_hi, (prio_lo + prio_hi) / 2 - fwd_up);
   for (int j = j0; j <= j1; ++j) {
     if (prio_on)
-      PETRA_CUDA(cudaStreamCreateWithPriority(&streams_[j], cudaStreamNonBlocking,
-                                              j == J_ ? tail_rank : (prio_lo + prio_hi) / 2));
+      PETRA_CUDA(cudaStreamCreateWithPriority(&streams_[j], cudaStreamNonBlocking, j == J_ ? tail_rank : mid));
     else PETRA_CUDA(cudaStreamCreateWithFlags(&streams_[j], cudaStreamNonBlocking));
     PETRA_CUDA(cudaEventCreateWithFlags(&done_[j], cudaEventDisableTiming));
   }
