@@ -369,7 +369,7 @@ HaloPlan halo_plan(int B, int H, int W, int Cred, int N) {
   // Weight-resident plan: one N tile (BN = N <= 128) whose 9 * Cred x N weights stay in
   // smem for the whole persistent CTA, so only the halos stream from L2 (~42 B/clk per
   // SM on B200: the weight stream, not the MMA, bounds the streamed plan for C = 64).
-  static const bool resident_ok = env_int("PETRA_HALO_RESIDENT", 1) != 0;
+  static const bool resident_ok = env_int("PETRA_HALO_RESIDENT", 0) != 0;  // 0 under the 40-CTA caps
   if (resident_ok && N <= 128) {
     const size_t wbytes = (size_t)9 * (Cred / 64) * N * 128;
     for (int T : {4, 2, 1}) {
