@@ -1587,7 +1587,9 @@ void splitk_sum(const float *part, int splits, int64_t n, float *out, cudaStream
     PETRA_LAUNCH_CHECK();
     return;
   }
-  launch_k(splitk_sum_kernel, (unsigned)std::min<int64_t>(cdiv(n, 256), 4 * kNumSMs), 256, 0, st, part, splits, n, out);
+  static const int per_sm = std::max(1, env_int("PETRA_SPLITK_BLOCKS_PER_SM", 1));
+  launch_k(splitk_sum_kernel, (unsigned)std::min<int64_t>(cdiv(n, 256), (int64_t)per_sm * kNumSMs), 256, 0, st, part,
+           splits, n, out);
   PETRA_LAUNCH_CHECK();
 }
 
